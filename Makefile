@@ -1,0 +1,36 @@
+# B200-native siting engine: one shared library with the sm_100a kernels and
+# the C-ABI (include/txsite_b200.h), the C++ host API + CLI on top of it, and
+# the CPU oracle (test infrastructure, oracle/Makefile).
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC -Xcompiler -Wall -Xptxas -warn-spills
+PKG := paper_2006_16783_b200
+BUILD := build
+CU_SRC := $(wildcard $(PKG)/csrc/*.cu)
+CPP_SRC := $(wildcard $(PKG)/csrc/*.cpp)
+HDRS := $(wildcard $(PKG)/csrc/*.hpp $(PKG)/csrc/*.cuh) include/txsite_b200.h
+OBJ := $(CU_SRC:$(PKG)/csrc/%.cu=$(BUILD)/%.o) $(CPP_SRC:$(PKG)/csrc/%.cpp=$(BUILD)/%.cpp.o)
+LIB := $(PKG)/libtxsite_b200.so
+
+all: $(LIB) oracle
+
+$(BUILD):
+	mkdir -p $(BUILD)
+
+$(BUILD)/%.o: $(PKG)/csrc/%.cu $(HDRS) | $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(BUILD)/%.cpp.o: $(PKG)/csrc/%.cpp $(HDRS) | $(BUILD)
+	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
+
+$(LIB): $(OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ)
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf $(BUILD) $(LIB)
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle clean

@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""Benchmark: end-to-end multiple-observer siting (VIX -> FINDMAX -> VIEWSHED
+-> SITE) on a BASELINE.json configuration, one JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl b200|reference]
+
+A "step" is one full siting run of the configuration on its synthetic seeded
+terrain.  `value` = device seconds per step with the terrain resident in HBM
+(CUDA events on the engine stream, L2 flushed between steps, max over ranks);
+`e2e` = the same run through the public API from pinned host memory: terrain
+H2D, the pipeline, the step list and the cumulative bitmap D2H inside the
+timed region.  `--impl reference` times the CPU oracle port (oracle/) on this
+host's cores on a bounded, extrapolated sample of the same workload.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "end-to-end siting sec; VIEWSHED LOS samples/s; SITE GB/s vs HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--site-mode", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--threads", type=int, default=0, help="CPU threads for the oracle legs (0 = all)")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle leg (cpu_baseline and --impl reference): bounded sample,
+# linearly extrapolated to the full configuration.
+# ---------------------------------------------------------------------------
+class CpuReference:
+    def __init__(self, cfg, threads):
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import numpy as np
+        import oracle_lib as O
+        self.O, self.np, self.cfg = O, np, cfg
+        self.threads = threads or (os.cpu_count() or 1)
+        c = cfg
+        self.z = O.generate_fractal(c.nrows, c.ncols, c.roughness, c.terrain_seed, c.zmin, c.zmax, self.threads)
+        if c.water_rows:
+            self.z[:c.water_rows] = 0
+        rng = np.random.default_rng(c.terrain_seed)
+        budget = 1.5e7 * self.threads        # LOS crossings per sampled component (~0.3-1 s)
+        if c.samples:
+            per_row = c.ncols * c.samples * 0.81 * c.roi
+            self.vix_rows = int(max(1, min(c.nrows, round(budget / per_row))))
+            self.scores = rng.integers(0, c.samples + 1, (c.nrows, c.ncols)).astype(np.uint8)
+            self.cr, self.cc, _ = O.find_candidates(self.scores, c.block, c.per_block)
+        else:
+            self.vix_rows = 0
+            self.cr, self.cc = O.random_observers(c.nrows, c.ncols, c.random_observers, c.observer_seed)
+        self.ncand = len(self.cr)
+        self.vs_n = int(max(8, min(self.ncand, round(budget / (7.0 * c.roi * c.roi)))))
+        # SITE: lazy greedy on the candidates of the top-left 1/16 sub-square
+        sub = (self.cr < c.nrows // 4) & (self.cc < c.ncols // 4)
+        self.sr, self.sc = self.cr[sub], self.cc[sub]
+        self.sw, self.sv = O.viewsheds(self.z, c.roi, c.height, c.height, self.sr, self.sc, self.threads)
+        self.sub_sel = max(1, c.max_selected // 16)
+        self.k = 0
+
+    def step(self):
+        O, np, c = self.O, self.np, self.cfg
+        parts = {}
+        if c.samples:
+            rb = (self.k * 977) % max(1, c.nrows - self.vix_rows)
+            t0 = time.perf_counter()
+            O.estimate_vix(self.z, c.roi, c.height, c.height, c.samples, c.vix_seed, self.threads,
+                           rows=(rb, rb + self.vix_rows))
+            parts["vix"] = (time.perf_counter() - t0) * c.nrows / self.vix_rows
+            t0 = time.perf_counter()
+            O.find_candidates(self.scores, c.block, c.per_block)
+            parts["findmax"] = time.perf_counter() - t0
+        idx = np.linspace(0, self.ncand - 1, self.vs_n).astype(np.int64)
+        idx = (idx + self.k) % self.ncand
+        t0 = time.perf_counter()
+        O.viewsheds(self.z, c.roi, c.height, c.height, self.cr[idx], self.cc[idx], self.threads)
+        parts["viewshed"] = (time.perf_counter() - t0) * self.ncand / self.vs_n
+        t0 = time.perf_counter()
+        O.site(self.sr, self.sc, self.sw, self.sv, c.nrows, c.ncols, c.target, self.sub_sel)
+        parts["site"] = (time.perf_counter() - t0) * 16
+        self.k += 1
+        return sum(parts.values()), parts
+
+    def sample_desc(self):
+        c = self.cfg
+        s = []
+        if c.samples:
+            s.append(f"VIX on {self.vix_rows}/{c.nrows} rows (x{c.nrows / self.vix_rows:.0f})")
+            s.append("FINDMAX full (synthetic VixMap)")
+        s.append(f"VIEWSHED on {self.vs_n}/{self.ncand} observers (x{self.ncand / self.vs_n:.1f})")
+        s.append(f"SITE lazy greedy on the {len(self.sr)} observers of the top-left 1/16 sub-square, "
+                 f"{self.sub_sel} picks (x16)")
+        return "; ".join(s) + "; extrapolated linearly to the full configuration"
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    ref = CpuReference(cfg, args.threads)
+    for _ in range(args.warmup):
+        ref.step()
+    vals = []
+    for _ in range(args.steps):
+        v, parts = ref.step()
+        vals.append(v)
+    value = statistics.mean(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(value * 1e3, 2), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32 (exact integer LOS arithmetic)", "data": "synthetic",
+        "config": {"workload": cfg.name, "nrows": cfg.nrows, "ncols": cfg.ncols, "roi": cfg.roi},
+        "cpu_baseline": {"value": round(value, 4), "unit": "s", "cores": ref.threads, "kind": "port",
+                         "sample": ref.sample_desc()},
+        "stages_s": {k: round(v, 4) for k, v in parts.items()},
+        "e2e": {"value": round(value, 4), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-i", str(self.idx), "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[5 + i] and "Not" not in r[5 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def load_traffic(kernel):
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+def run_b200(args, cfg):
+    import numpy as np
+    import torch
+    import paper_2006_16783_b200 as T
+    from paper_2006_16783_b200.configs import params_for, run, setup_terrain
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    eng = T.Engine(local)
+    params = params_for(cfg, args.site_mode)
+    setup_terrain(eng, cfg)
+    z_host = torch.empty((cfg.nrows, cfg.ncols), dtype=torch.int16, pin_memory=True).numpy()
+    z_host[:] = eng.terrain()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        run(eng, cfg, params)
+    eng.synchronize()
+
+    phys = os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local] if os.environ.get(
+        "CUDA_VISIBLE_DEVICES") else str(local)
+    clocks = Clocks(phys)
+    eng.reset_stats()
+    torch.cuda.synchronize()
+    barrier()
+    clocks.start()
+    step_ms = []
+    res = None
+    for _ in range(args.steps):
+        flush.zero_()                  # evict L2 (256 MB > 126 MB) outside the timed events
+        torch.cuda.synchronize()
+        eng.event_record(0)
+        res = run(eng, cfg, params)
+        eng.event_record(1)
+        step_ms.append(eng.event_elapsed(0, 1))
+    eng.synchronize()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    st = eng.stats()
+    barrier()
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / args.steps
+
+    # ---- e2e through the public API from pinned host memory ---------------
+    nw = (cfg.posts + 63) // 64
+    cum_host = torch.empty(nw * 8, dtype=torch.uint8, pin_memory=True).numpy().view(np.uint64)
+    e2e_ms = []
+    launches_e2e = 0
+    for _ in range(max(1, args.e2e_steps)):
+        flush.zero_()
+        torch.cuda.synchronize()
+        before = eng.stats()["kernel_launches"]
+        eng.event_record(2)
+        eng.set_terrain(z_host)
+        r2 = run(eng, cfg, params)
+        import ctypes
+        from paper_2006_16783_b200 import _native as N
+        eng._chk(N.lib.txs_get_cumulative(eng.handle, ctypes.c_void_p(cum_host.ctypes.data)))
+        eng.event_record(3)
+        e2e_ms.append(eng.event_elapsed(2, 3))
+        launches_e2e = eng.stats()["kernel_launches"] - before
+    e2e = statistics.mean(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e = float(t.item())
+    d2h = nw * 8 + len(r2["index"]) * 32
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    # ---- per-stage figures and the roofline of the dominant kernel -------
+    K = args.steps
+    peak, peak_kind = load_peaks()
+    stages = {}
+    if cfg.samples:
+        vix_ms = st["ms_vix"] / K
+        units = st["vix_crossings_full"] / K
+        stages["vix"] = {"ms": round(vix_ms, 3), "los_crossings": int(units),
+                         "los_samples_per_s": units / (vix_ms / 1e3) if vix_ms else None,
+                         "kernel": "k_vix", "bytes_per_launch": 4 * units}
+        fm_ms = st["ms_findmax"] / K
+        stages["findmax"] = {"ms": round(fm_ms, 3), "kernel": "k_findmax", "bytes_per_launch": 2 * cfg.posts}
+    vs_ms = st["ms_viewshed"] / K
+    vunits = st["viewshed_crossings"] / K
+    stages["viewshed"] = {"ms": round(vs_ms, 3), "los_crossings": int(vunits),
+                          "los_samples_per_s": vunits / (vs_ms / 1e3) if vs_ms else None,
+                          "kernel": "k_viewshed", "bytes_per_launch": 4 * vunits}
+    site_ms = st["ms_site"] / K
+    sbytes = st["site_bytes"] / K
+    stages["site"] = {"ms": round(site_ms, 3), "iterations": st["site_iterations"] // K,
+                      "site_gbs": sbytes / (site_ms / 1e3) / 1e9 if site_ms else None,
+                      "kernel": "k_update" if args.site_mode == 0 else "k_gain_full", "bytes_per_launch": sbytes,
+                      "mode": "incremental" if args.site_mode == 0 else "full-rescan"}
+    for s in stages.values():
+        s["achieved_gbs"] = round(s["bytes_per_launch"] / (s["ms"] / 1e3) / 1e9, 2) if s["ms"] else None
+    dom = max(stages, key=lambda k: stages[k]["ms"])
+    ach = stages[dom]["achieved_gbs"] or 0.0
+    roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+                "traffic": load_traffic(stages[dom]["kernel"]), "kernel": stages[dom]["kernel"], "stage": dom,
+                "peak_kind": peak_kind,
+                "bytes_model": "VIX/VIEWSHED: 4 B (two int16 posts) per grid-line crossing, no early exit; "
+                               "SITE: packed viewshed bytes streamed; FINDMAX: VixMap read twice"}
+    line = {
+        "metric": METRIC, "value": round(ms / 1e3, 5), "unit": "s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32 (exact integer LOS arithmetic)",
+        "data": "synthetic (seeded diamond-square terrain, BASELINE shapes)",
+        "config": {"workload": cfg.name, "nrows": cfg.nrows, "ncols": cfg.ncols, "roi": cfg.roi,
+                   "height": cfg.height, "vix_samples": cfg.samples, "block": cfg.block, "per_block": cfg.per_block,
+                   "max_selected": cfg.max_selected, "candidates": st["candidates"],
+                   "sited": int(len(res["index"])), "stop": res["stop"],
+                   "parallelism": f"replicas{world}" if world > 1 else "single-gpu",
+                   "l2": "flushed between steps (256 MB write outside the timed events)"},
+        "stages": stages,
+        "roofline": roofline,
+        "e2e": {"value": round(e2e / 1e3, 5), "unit": "s", "h2d_bytes_per_step": cfg.posts * 2,
+                "d2h_bytes_per_step": d2h, "kernel_launches_per_step": launches_e2e},
+        "gpu_launches": st["kernel_launches"],
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        ref = CpuReference(cfg, args.threads)
+        v, parts = ref.step()
+        line["cpu_baseline"] = {"value": round(v, 3), "unit": "s", "cores": ref.threads, "kind": "port",
+                                "sample": ref.sample_desc(), "stages_s": {k: round(x, 3) for k, x in parts.items()}}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    from paper_2006_16783_b200.configs import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_b200(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,175 @@
+/*
+ * txsite_b200.h — C-ABI drop-in boundary of the B200-native multiple-observer
+ * siting engine (arXiv 2006.16783; contract /root/reference/SPEC.md).
+ *
+ * The reference's boundary is the C++ stage API of namespace txsite
+ * (SPEC.md:176 estimate_vix, :228 partition, :238 find_candidates,
+ * :305 compute_all_viewsheds, :364 site, :433 run_pipeline) inside static lib
+ * txsite_core (proj/CMakeLists.txt:13-26).  The reference ships no binary ABI
+ * and no FFI (src/ is absent), so each entry point below names
+ * the SPEC operation it replaces; include/txsite/txsite.hpp re-exposes them as
+ * that C++ API and INTEGRATION.md shows the bindings (C++, ctypes).
+ *
+ * Conventions
+ *  - plain pointers and sizes only; host buffers are owned by the caller;
+ *  - every function returns txs_status; on failure txs_last_error(ctx) holds a
+ *    stage-tagged message ("stage-tagged message");
+ *  - stage outputs stay resident in HBM inside the context; the *_out host
+ *    pointers are optional copies (NULL = keep on device only);
+ *  - calls are synchronous at stage granularity; a context is not thread-safe;
+ *  - there is no CPU fallback: without a usable sm_100 device txs_create fails.
+ */
+#ifndef TXSITE_B200_H
+#define TXSITE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TXS_ABI_VERSION 1
+
+typedef enum txs_status {
+    TXS_OK = 0,
+    TXS_ERR_INVALID_ARGUMENT = 1, /* roi < 1, roi < 3 for partition (:232), zmin > zmax (:65) ... */
+    TXS_ERR_OFF_GRID = 2,         /* off-grid base point                                        */
+    TXS_ERR_STATE = 3,            /* a stage called before its input exists                                     */
+    TXS_ERR_CUDA = 4,             /* CUDA runtime / no sm_100 device                                            */
+    TXS_ERR_OUT_OF_MEMORY = 5,
+    TXS_ERR_RANGE = 6,            /* exceeds the exact-integer arithmetic envelope (DESIGN.md §2 D2)            */
+    TXS_ERR_SIZE_MISMATCH = 7,
+    TXS_ERR_NODATA = 8            /* NODATA sentinel -32768 rejected                              */
+} txs_status;
+
+/* SitingResult.stop_reason + max_selected. */
+typedef enum txs_stop {
+    TXS_STOP_TARGET_REACHED = 0,
+    TXS_STOP_ZERO_GAIN = 1,
+    TXS_STOP_EXHAUSTED = 2,
+    TXS_STOP_MAX_SELECTED = 3
+} txs_stop;
+
+/* SiteParams plus the knobs the BASELINE configs need. */
+typedef struct txs_params {
+    int32_t roi;               /* radius of interest in posts, >= 1                       */
+    int32_t tx_height;         /* h_t, integer elevation units, >= 0                       */
+    int32_t rx_height;         /* h_r                                                      */
+    int32_t samples_per_point; /* VIX samples per post (default 10), 1..255                */
+    int32_t per_block;         /* FINDMAX top-k per block (default 20)                     */
+    int32_t block_width;       /* 0 => ceil(roi/3); BASELINE fixes it        */
+    int32_t site_mode;         /* 0 = exact incremental gains, 1 = full rescan each round  */
+    int32_t _reserved;
+    double target_coverage;    /* (0,1]                                                    */
+    int64_t max_selected;      /* 0 => unlimited                             */
+    uint64_t seed;             /* VIX sampling seed                          */
+} txs_params;
+
+typedef struct txs_candidate { int32_t row, col, score, _pad; } txs_candidate;
+typedef struct txs_window { int32_t row0, col0, h, w; } txs_window;
+typedef struct txs_step {
+    int64_t index;    /* candidate index (block order) */
+    int32_t row, col; /* transmitter base                            */
+    int64_t gain;     /* marginal gain in cells                      */
+    double coverage;  /* cumulative coverage after this step         */
+} txs_step;
+
+/* Per-stage device timings (CUDA events on the context stream) and the
+ * algorithmic work counters the roofline figures are computed from. */
+typedef struct txs_stats {
+    double ms_terrain, ms_vix, ms_findmax, ms_viewshed, ms_site;
+    int64_t vix_los;                /* sampled LOS segments tested                          */
+    int64_t vix_crossings_full;     /* interior crossings of those segments, no early exit  */
+    int64_t viewshed_crossings;     /* R2 ray crossings evaluated (in-grid, no early exit)  */
+    int64_t viewshed_cells;         /* disk cells tested                                    */
+    int64_t site_iterations;
+    int64_t site_bytes;             /* packed viewshed bytes streamed by the gain kernels    */
+    int64_t site_launches;          /* kernels launched by the SITE loop                     */
+    int64_t candidates;
+    int64_t kernel_launches;        /* every kernel this context launched since reset        */
+} txs_stats;
+
+typedef struct txs_ctx txs_ctx;
+
+int txs_abi_version(void);
+/* 1 if a CUDA device with compute capability 10.x is visible. */
+int txs_device_ok(void);
+
+txs_status txs_create(int device, txs_ctx** out);
+void txs_destroy(txs_ctx* ctx);
+const char* txs_last_error(const txs_ctx* ctx);
+txs_status txs_get_stats(txs_ctx* ctx, txs_stats* out);
+txs_status txs_reset_stats(txs_ctx* ctx);
+txs_status txs_synchronize(txs_ctx* ctx);
+/* Device-side timing on the context stream: record event `slot` (0..15) now;
+ * elapsed milliseconds between two recorded slots (waits for slot b). */
+txs_status txs_event_record(txs_ctx* ctx, int slot);
+txs_status txs_event_elapsed(txs_ctx* ctx, int slot_a, int slot_b, double* ms);
+
+/* ---- terrain module ---------------------------------------- */
+/* load_binary's in-memory result: row-major int16, copied to HBM. */
+txs_status txs_set_terrain(txs_ctx* ctx, const int16_t* z, int64_t nrows, int64_t ncols);
+/* generate_fractal, decision D10; generated directly in HBM. */
+txs_status txs_generate_fractal(txs_ctx* ctx, int64_t nrows, int64_t ncols, double roughness,
+                                uint64_t seed, int32_t zmin, int32_t zmax);
+/* Config-3 water clamp: rows [row_begin,row_end) set to value. */
+txs_status txs_fill_rows(txs_ctx* ctx, int64_t row_begin, int64_t row_end, int16_t value);
+txs_status txs_get_terrain(txs_ctx* ctx, int16_t* z_out);
+txs_status txs_terrain_dims(const txs_ctx* ctx, int64_t* nrows, int64_t* ncols);
+
+/* ---- los module — batch form for parity tests --------------- */
+/* pairs: n x {tx_row, tx_col, rx_row, rx_col}; out: n bytes 0/1. */
+txs_status txs_is_visible_batch(txs_ctx* ctx, const int32_t* pairs, int64_t n, int32_t tx_height,
+                                int32_t rx_height, uint8_t* out);
+
+/* ---- vix module (SPEC.md:176 estimate_vix) ------------------------------------ */
+txs_status txs_estimate_vix(txs_ctx* ctx, const txs_params* p, uint8_t* scores_out);
+txs_status txs_set_vix(txs_ctx* ctx, const uint8_t* scores);  /* inject a VixMap */
+
+/* ---- candidates module (SPEC.md:228 partition, :238 find_candidates) ------- */
+txs_status txs_partition(int64_t nrows, int64_t ncols, int32_t roi, int32_t block_width,
+                         int64_t* bw_out, int64_t* blocks_x, int64_t* blocks_y);
+txs_status txs_find_candidates(txs_ctx* ctx, const txs_params* p, int64_t* n_out,
+                               txs_candidate* out, int64_t cap);
+txs_status txs_set_candidates(txs_ctx* ctx, const txs_candidate* c, int64_t n);
+/* Config 5: n uniformly random observers, row = next_below(nrows) then
+ * col = next_below(ncols) from SplitMix64(seed) (decision D11). */
+txs_status txs_random_observers(txs_ctx* ctx, int64_t n, uint64_t seed);
+txs_status txs_get_candidates(txs_ctx* ctx, txs_candidate* out, int64_t cap, int64_t* n_out);
+
+/* ---- viewshed module (SPEC.md:305 compute_all_viewsheds) ------------------- */
+txs_status txs_compute_viewsheds(txs_ctx* ctx, const txs_params* p);
+/* words_stride >= ceil((2roi+1)^2/64); popcounts optional. */
+txs_status txs_get_viewsheds(txs_ctx* ctx, int64_t first, int64_t count, txs_window* wins,
+                             uint64_t* words, int64_t words_stride, int64_t* popcounts);
+/* Inject packed viewsheds (for SITE parity on given input). */
+txs_status txs_set_viewsheds(txs_ctx* ctx, int32_t roi, int64_t n, const int32_t* rows,
+                             const int32_t* cols, const txs_window* wins, const uint64_t* words,
+                             int64_t words_stride);
+
+/* ---- siting module (SPEC.md:364 site, :374 marginal_gain, :384 coverage) --- */
+txs_status txs_site(txs_ctx* ctx, const txs_params* p, txs_step* steps, int64_t cap,
+                    int64_t* nsteps, int32_t* stop_reason);
+/* CumulativeShed words: dense row-major, (nrows*ncols+63)/64. */
+txs_status txs_get_cumulative(txs_ctx* ctx, uint64_t* words_out);
+/* marginal_gain of every resident viewshed against a caller cum (dense). */
+txs_status txs_marginal_gains(txs_ctx* ctx, const uint64_t* cum_dense, int64_t* gains_out);
+
+/* ---- cli module (SPEC.md:433 run_pipeline) ---------------------------------- */
+/* vix -> findmax -> viewshed -> site on the resident terrain, device-resident
+ * in between; stage_ms[4] = {vix, findmax, viewshed, site}. */
+txs_status txs_run_pipeline(txs_ctx* ctx, const txs_params* p, txs_step* steps, int64_t cap,
+                            int64_t* nsteps, int32_t* stop_reason, double* stage_ms);
+
+/* ---- host-only helpers (no GPU needed; used by the CPU test-suite) -------- */
+/* The frozen D5 ray template for roi: returns ray count; arrays filled when the
+ * caps suffice.  cell_begin has rays+1 entries. */
+int64_t txs_ray_template(int32_t roi, int32_t* p, int32_t* q, int64_t* cell_begin, int32_t* ca,
+                         int32_t* cb, int64_t cap_rays, int64_t cap_cells, int64_t* ncells);
+/* Self-test of host-side integer helpers (exact 64-bit division magic). 0 = ok. */
+int txs_selftest(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TXSITE_B200_H */

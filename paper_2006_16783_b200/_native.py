@@ -1,0 +1,101 @@
+"""ctypes binding of the C-ABI in include/txsite_b200.h (libtxsite_b200.so).
+
+This is the reference-side binding a Python caller adds; the
+engine itself is the sm_100a library.  There is no fallback: if the library is
+missing, importing this module raises.
+"""
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtxsite_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"libtxsite_b200.so not built ({LIB_PATH}); run `make` or __graft_entry__.build() — "
+        "the engine has no CPU fallback")
+
+lib = C.CDLL(LIB_PATH)
+
+i32, i64, u64, dbl, vp = C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_void_p
+
+STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "OFF_GRID", 3: "STATE", 4: "CUDA",
+          5: "OUT_OF_MEMORY", 6: "RANGE", 7: "SIZE_MISMATCH", 8: "NODATA"}
+STOP = {0: "target-reached", 1: "zero-gain", 2: "exhausted", 3: "max-selected"}
+
+
+class Params(C.Structure):
+    _fields_ = [("roi", i32), ("tx_height", i32), ("rx_height", i32), ("samples_per_point", i32),
+                ("per_block", i32), ("block_width", i32), ("site_mode", i32), ("_reserved", i32),
+                ("target_coverage", dbl), ("max_selected", i64), ("seed", u64)]
+
+
+class Candidate(C.Structure):
+    _fields_ = [("row", i32), ("col", i32), ("score", i32), ("_pad", i32)]
+
+
+class Window(C.Structure):
+    _fields_ = [("row0", i32), ("col0", i32), ("h", i32), ("w", i32)]
+
+
+class Step(C.Structure):
+    _fields_ = [("index", i64), ("row", i32), ("col", i32), ("gain", i64), ("coverage", dbl)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("ms_terrain", dbl), ("ms_vix", dbl), ("ms_findmax", dbl), ("ms_viewshed", dbl),
+                ("ms_site", dbl), ("vix_los", i64), ("vix_crossings_full", i64),
+                ("viewshed_crossings", i64), ("viewshed_cells", i64), ("site_iterations", i64),
+                ("site_bytes", i64), ("site_launches", i64), ("candidates", i64),
+                ("kernel_launches", i64)]
+
+
+def _sig(name, res, args):
+    f = getattr(lib, name)
+    f.restype = res
+    f.argtypes = args
+    return f
+
+
+_sig("txs_abi_version", C.c_int, [])
+_sig("txs_device_ok", C.c_int, [])
+_sig("txs_create", C.c_int, [C.c_int, C.POINTER(vp)])
+_sig("txs_destroy", None, [vp])
+_sig("txs_last_error", C.c_char_p, [vp])
+_sig("txs_get_stats", C.c_int, [vp, C.POINTER(Stats)])
+_sig("txs_reset_stats", C.c_int, [vp])
+_sig("txs_synchronize", C.c_int, [vp])
+_sig("txs_event_record", C.c_int, [vp, C.c_int])
+_sig("txs_event_elapsed", C.c_int, [vp, C.c_int, C.c_int, C.POINTER(dbl)])
+_sig("txs_set_terrain", C.c_int, [vp, vp, i64, i64])
+_sig("txs_generate_fractal", C.c_int, [vp, i64, i64, dbl, u64, i32, i32])
+_sig("txs_fill_rows", C.c_int, [vp, i64, i64, C.c_int16])
+_sig("txs_get_terrain", C.c_int, [vp, vp])
+_sig("txs_terrain_dims", C.c_int, [vp, C.POINTER(i64), C.POINTER(i64)])
+_sig("txs_is_visible_batch", C.c_int, [vp, vp, i64, i32, i32, vp])
+_sig("txs_estimate_vix", C.c_int, [vp, C.POINTER(Params), vp])
+_sig("txs_set_vix", C.c_int, [vp, vp])
+_sig("txs_partition", C.c_int, [i64, i64, i32, i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)])
+_sig("txs_find_candidates", C.c_int, [vp, C.POINTER(Params), C.POINTER(i64), vp, i64])
+_sig("txs_set_candidates", C.c_int, [vp, vp, i64])
+_sig("txs_random_observers", C.c_int, [vp, i64, u64])
+_sig("txs_get_candidates", C.c_int, [vp, vp, i64, C.POINTER(i64)])
+_sig("txs_compute_viewsheds", C.c_int, [vp, C.POINTER(Params)])
+_sig("txs_get_viewsheds", C.c_int, [vp, i64, i64, vp, vp, i64, vp])
+_sig("txs_set_viewsheds", C.c_int, [vp, i32, i64, vp, vp, vp, vp, i64])
+_sig("txs_site", C.c_int, [vp, C.POINTER(Params), vp, i64, C.POINTER(i64), C.POINTER(i32)])
+_sig("txs_get_cumulative", C.c_int, [vp, vp])
+_sig("txs_marginal_gains", C.c_int, [vp, vp, vp])
+_sig("txs_run_pipeline", C.c_int, [vp, C.POINTER(Params), vp, i64, C.POINTER(i64), C.POINTER(i32), vp])
+_sig("txs_ray_template", i64, [i32, vp, vp, vp, vp, vp, i64, i64, C.POINTER(i64)])
+_sig("txs_selftest", C.c_int, [])
+
+# every symbol the header declares (checked by the CPU test-suite)
+EXPORTS = [
+    "txs_abi_version", "txs_device_ok", "txs_create", "txs_destroy", "txs_last_error", "txs_get_stats",
+    "txs_reset_stats", "txs_synchronize", "txs_event_record", "txs_event_elapsed", "txs_set_terrain", "txs_generate_fractal", "txs_fill_rows",
+    "txs_get_terrain", "txs_terrain_dims", "txs_is_visible_batch", "txs_estimate_vix", "txs_set_vix",
+    "txs_partition", "txs_find_candidates", "txs_set_candidates", "txs_random_observers",
+    "txs_get_candidates", "txs_compute_viewsheds", "txs_get_viewsheds", "txs_set_viewsheds", "txs_site",
+    "txs_get_cumulative", "txs_marginal_gains", "txs_run_pipeline", "txs_ray_template", "txs_selftest",
+]

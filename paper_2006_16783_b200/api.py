@@ -1,0 +1,252 @@
+"""Python face of the engine, mirroring the reference's stage API
+(SPEC.md: terrain :22-104, los :117, vix :176, candidates :228/:238,
+viewshed :285/:305, siting :364/:374/:384, cli :433) over the C-ABI.
+
+Stage outputs stay resident in HBM inside an Engine; the methods copy to numpy
+only when asked (``copy=True``), like the ``*_out`` pointers of the C-ABI.
+"""
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+
+STOP = N.STOP
+
+
+class TxsError(RuntimeError):
+    def __init__(self, status, message):
+        super().__init__(f"{N.STATUS.get(status, status)}: {message}")
+        self.status = N.STATUS.get(status, status)
+
+
+def _p(a):
+    return C.c_void_p(a.ctypes.data) if a is not None else None
+
+
+def make_params(roi, tx_height=10, rx_height=10, samples=10, per_block=20, block_width=0,
+                target=0.95, max_selected=0, seed=0, site_mode=0):
+    """SiteParams plus block_width / seed / max_selected / site_mode."""
+    return N.Params(roi=roi, tx_height=tx_height, rx_height=rx_height, samples_per_point=samples,
+                    per_block=per_block, block_width=block_width, site_mode=site_mode, _reserved=0,
+                    target_coverage=target, max_selected=max_selected, seed=seed)
+
+
+def partition(nrows, ncols, roi, block_width=0):
+    """partition -> (block_width, blocks_x, blocks_y)."""
+    bw, bx, by = C.c_int64(), C.c_int64(), C.c_int64()
+    st = N.lib.txs_partition(nrows, ncols, roi, block_width, C.byref(bw), C.byref(bx), C.byref(by))
+    if st:
+        raise TxsError(st, "[findmax] partition: roi < 3 with the default block width, or bad dims")
+    return bw.value, bx.value, by.value
+
+
+def ray_template(roi):
+    """The frozen D5 ray template (host-side; no GPU needed)."""
+    nc = C.c_int64()
+    nr = N.lib.txs_ray_template(roi, None, None, None, None, None, 0, 0, C.byref(nc))
+    if nr < 0:
+        raise TxsError(1, "bad roi")
+    p, q = np.zeros(nr, np.int32), np.zeros(nr, np.int32)
+    cb = np.zeros(nr + 1, np.int64)
+    ca, cc = np.zeros(nc.value, np.int32), np.zeros(nc.value, np.int32)
+    N.lib.txs_ray_template(roi, _p(p), _p(q), _p(cb), _p(ca), _p(cc), nr, nc.value, None)
+    return p, q, cb, ca, cc
+
+
+def selftest():
+    return N.lib.txs_selftest() == 0
+
+
+def device_ok():
+    return bool(N.lib.txs_device_ok())
+
+
+def max_words(roi):
+    s = 2 * roi + 1
+    return (s * s + 63) // 64
+
+
+class Engine:
+    """One device context (txs_ctx).  Not thread-safe (the
+    orchestrator is single-threaded)."""
+
+    def __init__(self, device=0):
+        h = C.c_void_p()
+        st = N.lib.txs_create(device, C.byref(h))
+        if st:
+            raise TxsError(st, f"txs_create(device={device}) failed: no usable sm_100 device")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.lib.txs_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _chk(self, st):
+        if st:
+            raise TxsError(st, N.lib.txs_last_error(self._h).decode())
+
+    # ---- terrain ------------------------------------------------------------
+    def set_terrain(self, z):
+        z = np.ascontiguousarray(z, np.int16)
+        self._chk(N.lib.txs_set_terrain(self._h, _p(z), z.shape[0], z.shape[1]))
+
+    def generate_fractal(self, nrows, ncols, roughness, seed, zmin, zmax):
+        self._chk(N.lib.txs_generate_fractal(self._h, nrows, ncols, roughness, seed, zmin, zmax))
+
+    def fill_rows(self, row_begin, row_end, value):
+        self._chk(N.lib.txs_fill_rows(self._h, row_begin, row_end, value))
+
+    @property
+    def dims(self):
+        r, c = C.c_int64(), C.c_int64()
+        self._chk(N.lib.txs_terrain_dims(self._h, C.byref(r), C.byref(c)))
+        return r.value, c.value
+
+    def terrain(self):
+        nr, nc = self.dims
+        z = np.empty((nr, nc), np.int16)
+        self._chk(N.lib.txs_get_terrain(self._h, _p(z)))
+        return z
+
+    # ---- los ------------------------------------------------------------------
+    def is_visible_batch(self, pairs, tx_height, rx_height):
+        pairs = np.ascontiguousarray(pairs, np.int32).reshape(-1, 4)
+        out = np.zeros(len(pairs), np.uint8)
+        self._chk(N.lib.txs_is_visible_batch(self._h, _p(pairs), len(pairs), tx_height, rx_height, _p(out)))
+        return out
+
+    # ---- vix ------------------------------------------------------------------
+    def estimate_vix(self, params, copy=True):
+        out = np.empty(self.dims, np.uint8) if copy else None
+        self._chk(N.lib.txs_estimate_vix(self._h, C.byref(params), _p(out)))
+        return out
+
+    def set_vix(self, scores):
+        scores = np.ascontiguousarray(scores, np.uint8)
+        self._chk(N.lib.txs_set_vix(self._h, _p(scores)))
+
+    # ---- candidates -----------------------------------------------------------
+    def find_candidates(self, params, copy=True):
+        n = C.c_int64()
+        self._chk(N.lib.txs_find_candidates(self._h, C.byref(params), C.byref(n), None, 0))
+        return self.candidates() if copy else n.value
+
+    def candidates(self):
+        n = C.c_int64()
+        self._chk(N.lib.txs_get_candidates(self._h, None, 0, C.byref(n)))
+        buf = np.zeros((n.value, 4), np.int32)
+        self._chk(N.lib.txs_get_candidates(self._h, _p(buf), n.value, None))
+        return buf[:, 0].copy(), buf[:, 1].copy(), buf[:, 2].copy()
+
+    def set_candidates(self, rows, cols, scores=None):
+        n = len(rows)
+        buf = np.zeros((n, 4), np.int32)
+        buf[:, 0], buf[:, 1] = rows, cols
+        if scores is not None:
+            buf[:, 2] = scores
+        self._chk(N.lib.txs_set_candidates(self._h, _p(buf), n))
+
+    def random_observers(self, n, seed):
+        self._chk(N.lib.txs_random_observers(self._h, n, seed))
+
+    # ---- viewsheds --------------------------------------------------------------
+    def compute_all_viewsheds(self, params):
+        self._chk(N.lib.txs_compute_viewsheds(self._h, C.byref(params)))
+
+    def viewsheds(self, roi, first=0, count=None):
+        if count is None:
+            n = C.c_int64()
+            self._chk(N.lib.txs_get_candidates(self._h, None, 0, C.byref(n)))
+            count = n.value - first
+        stride = max_words(roi)
+        wins = np.zeros((count, 4), np.int32)
+        words = np.zeros((count, stride), np.uint64)
+        pops = np.zeros(count, np.int64)
+        self._chk(N.lib.txs_get_viewsheds(self._h, first, count, _p(wins), _p(words), stride, _p(pops)))
+        return wins, words, pops
+
+    def set_viewsheds(self, roi, rows, cols, wins, words):
+        rows = np.ascontiguousarray(rows, np.int32)
+        cols = np.ascontiguousarray(cols, np.int32)
+        wins = np.ascontiguousarray(wins, np.int32)
+        words = np.ascontiguousarray(words, np.uint64)
+        self._chk(N.lib.txs_set_viewsheds(self._h, roi, len(rows), _p(rows), _p(cols), _p(wins), _p(words),
+                                          words.shape[1]))
+
+    # ---- siting -----------------------------------------------------------------
+    def site(self, params, cap=None):
+        if cap is None:
+            n = C.c_int64()
+            self._chk(N.lib.txs_get_candidates(self._h, None, 0, C.byref(n)))
+            cap = n.value + 1
+        steps = (N.Step * max(cap, 1))()
+        ns, stop = C.c_int64(), C.c_int32()
+        self._chk(N.lib.txs_site(self._h, C.byref(params), steps, cap, C.byref(ns), C.byref(stop)))
+        return _steps_dict(steps, min(ns.value, cap), stop.value)
+
+    def cumulative(self):
+        nr, nc = self.dims
+        out = np.zeros((nr * nc + 63) // 64, np.uint64)
+        self._chk(N.lib.txs_get_cumulative(self._h, _p(out)))
+        return out
+
+    def marginal_gains(self, cum_dense):
+        cum = np.ascontiguousarray(cum_dense, np.uint64)
+        n = C.c_int64()
+        self._chk(N.lib.txs_get_candidates(self._h, None, 0, C.byref(n)))
+        out = np.zeros(max(n.value, 1), np.int64)
+        self._chk(N.lib.txs_marginal_gains(self._h, _p(cum), _p(out)))
+        return out[:n.value]
+
+    # ---- pipeline ---------------------------------------------------------------
+    def run_pipeline(self, params, cap=1 << 20):
+        steps = (N.Step * cap)()
+        ns, stop = C.c_int64(), C.c_int32()
+        ms = (C.c_double * 4)()
+        self._chk(N.lib.txs_run_pipeline(self._h, C.byref(params), steps, cap, C.byref(ns), C.byref(stop), ms))
+        d = _steps_dict(steps, min(ns.value, cap), stop.value)
+        d["stage_ms"] = dict(vix=ms[0], findmax=ms[1], viewshed=ms[2], site=ms[3])
+        return d
+
+    def stats(self):
+        s = N.Stats()
+        self._chk(N.lib.txs_get_stats(self._h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in N.Stats._fields_}
+
+    def reset_stats(self):
+        self._chk(N.lib.txs_reset_stats(self._h))
+
+    def synchronize(self):
+        self._chk(N.lib.txs_synchronize(self._h))
+
+    def event_record(self, slot):
+        self._chk(N.lib.txs_event_record(self._h, slot))
+
+    def event_elapsed(self, a, b):
+        ms = C.c_double()
+        self._chk(N.lib.txs_event_elapsed(self._h, a, b, C.byref(ms)))
+        return ms.value
+
+    @property
+    def handle(self):
+        return self._h
+
+
+_STEP_DT = np.dtype([("index", "<i8"), ("row", "<i4"), ("col", "<i4"), ("gain", "<i8"), ("coverage", "<f8")])
+
+
+def _steps_dict(steps, n, stop):
+    a = np.frombuffer(C.string_at(C.addressof(steps), n * C.sizeof(N.Step)), dtype=_STEP_DT)
+    return dict(index=a["index"].copy(), row=a["row"].copy(), col=a["col"].copy(),
+                gain=a["gain"].copy(), coverage=a["coverage"].copy(), stop=STOP[stop])

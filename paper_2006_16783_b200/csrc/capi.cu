@@ -1,0 +1,612 @@
+// C-ABI entry points (include/txsite_b200.h): context, terrain, argument
+// validation and the stage wrappers.  Kernels live in the per-stage .cu files.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "ctx.hpp"
+
+namespace txs {
+
+txs_status fail(txs_ctx* ctx, txs_status st, const char* stage, const std::string& msg) {
+    if (ctx) ctx->err = std::string("[") + stage + "] " + msg;
+    return st;
+}
+
+txs_status cuda_fail(txs_ctx* ctx, const char* stage, cudaError_t e) {
+    return fail(ctx, e == cudaErrorMemoryAllocation ? TXS_ERR_OUT_OF_MEMORY : TXS_ERR_CUDA, stage,
+                std::string("CUDA: ") + cudaGetErrorString(e));
+}
+
+txs_status ensure(txs_ctx* ctx, const char* stage, void** p, size_t* cap, size_t bytes) {
+    if (bytes <= *cap && *p) return TXS_OK;
+    if (*p) { cudaFree(*p); *p = nullptr; *cap = 0; }
+    if (bytes == 0) bytes = 16;
+    TXS_CUDA(ctx, stage, cudaMalloc(p, bytes));
+    *cap = bytes;
+    return TXS_OK;
+}
+
+txs_status check_params(txs_ctx* ctx, const char* stage, const txs_params* p, bool need_vix) {
+    if (!p) return fail(ctx, TXS_ERR_INVALID_ARGUMENT, stage, "params is NULL");
+    if (p->roi < 1) return fail(ctx, TXS_ERR_INVALID_ARGUMENT, stage, "roi < 1");
+    // exact-integer envelope (DESIGN.md §2 D2): int32 LOS sums need
+    // (2roi+1) * 4 * 65536 < 2^31; int16 template offsets need 2roi+1 < 2^15
+    if (p->roi > 4000) return fail(ctx, TXS_ERR_RANGE, stage, "roi > 4000 exceeds the exact-arithmetic envelope");
+    if (p->tx_height < 0 || p->rx_height < 0 || p->tx_height > 32767 || p->rx_height > 32767)
+        return fail(ctx, TXS_ERR_INVALID_ARGUMENT, stage, "heights must be in [0, 32767]");
+    if (need_vix && (p->samples_per_point < 1 || p->samples_per_point > 255))
+        return fail(ctx, TXS_ERR_INVALID_ARGUMENT, stage, "samples_per_point must be in [1, 255]");
+    if (!ctx->d_z) return fail(ctx, TXS_ERR_STATE, stage, "no terrain");
+    return TXS_OK;
+}
+
+}  // namespace txs
+
+using namespace txs;
+
+namespace {
+
+__global__ void k_nodata_check(const int16_t* __restrict__ z, int64_t n, int* flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (z[i] == -32768) { atomicExch(flag, 1); return; }
+}
+
+struct StageTimer {
+    txs_ctx* ctx;
+    double* slot;
+    StageTimer(txs_ctx* c, double* s) : ctx(c), slot(s) { cudaEventRecord(ctx->ev0, ctx->stream); }
+    txs_status stop(const char* stage) {
+        TXS_CUDA(ctx, stage, cudaEventRecord(ctx->ev1, ctx->stream));
+        TXS_CUDA(ctx, stage, cudaEventSynchronize(ctx->ev1));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        *slot += ms;
+        return TXS_OK;
+    }
+};
+
+int64_t default_bw(int32_t roi) { return (roi + 2) / 3; }
+
+}  // namespace
+
+extern "C" {
+
+int txs_abi_version(void) { return TXS_ABI_VERSION; }
+
+int txs_device_ok(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) { cudaGetLastError(); return 0; }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, 0) != cudaSuccess) return 0;
+    return prop.major == 10 ? 1 : 0;
+}
+
+txs_status txs_create(int device, txs_ctx** out) {
+    if (!out) return TXS_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0 || device < 0 || device >= n) { cudaGetLastError(); return TXS_ERR_CUDA; }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return TXS_ERR_CUDA;
+    if (prop.major != 10) return TXS_ERR_CUDA;   // sm_100a build only: no fallback
+    if (cudaSetDevice(device) != cudaSuccess) return TXS_ERR_CUDA;
+    txs_ctx* c = new txs_ctx();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
+        cudaMalloc(&c->d_counters, sizeof(unsigned long long) * kNumCounters) != cudaSuccess ||
+        cudaMalloc(&c->d_state, sizeof(SiteState)) != cudaSuccess ||
+        cudaMallocHost(&c->h_state, sizeof(SiteState)) != cudaSuccess) {
+        delete c;
+        return TXS_ERR_CUDA;
+    }
+    cudaMemset(c->d_counters, 0, sizeof(unsigned long long) * kNumCounters);
+    *out = c;
+    return TXS_OK;
+}
+
+void txs_destroy(txs_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    void* bufs[] = {c->d_z, c->d_vix, c->d_crow, c->d_ccol, c->d_cscore, c->d_words, c->d_win,
+                    c->d_pop, c->d_cum, c->d_delta[0], c->d_delta[1], c->d_gain, c->d_state,
+                    c->d_bucket_start, c->d_bucket_items, c->d_counters, c->d_scratch};
+    for (void* p : bufs) if (p) cudaFree(p);
+    for (auto& kv : c->templates) { cudaFree(kv.second.rays); cudaFree(kv.second.cells); }
+    if (c->h_state) cudaFreeHost(c->h_state);
+    for (cudaEvent_t e : c->user_ev) if (e) cudaEventDestroy(e);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char* txs_last_error(const txs_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+txs_status txs_synchronize(txs_ctx* c) {
+    if (!c) return TXS_ERR_INVALID_ARGUMENT;
+    TXS_CUDA(c, "sync", cudaStreamSynchronize(c->stream));
+    return TXS_OK;
+}
+
+txs_status txs_event_record(txs_ctx* c, int slot) {
+    if (!c || slot < 0 || slot >= 16) return TXS_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(c->device);
+    if (!c->user_ev[slot]) TXS_CUDA(c, "timing", cudaEventCreate(&c->user_ev[slot]));
+    TXS_CUDA(c, "timing", cudaEventRecord(c->user_ev[slot], c->stream));
+    return TXS_OK;
+}
+
+txs_status txs_event_elapsed(txs_ctx* c, int a, int b, double* ms) {
+    if (!c || !ms || a < 0 || a >= 16 || b < 0 || b >= 16 || !c->user_ev[a] || !c->user_ev[b])
+        return TXS_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(c->device);
+    TXS_CUDA(c, "timing", cudaEventSynchronize(c->user_ev[b]));
+    float f = 0.f;
+    TXS_CUDA(c, "timing", cudaEventElapsedTime(&f, c->user_ev[a], c->user_ev[b]));
+    *ms = f;
+    return TXS_OK;
+}
+
+txs_status txs_get_stats(txs_ctx* c, txs_stats* out) {
+    if (!c || !out) return TXS_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(c->device);
+    unsigned long long h[kNumCounters];
+    TXS_CUDA(c, "stats", cudaMemcpyAsync(h, c->d_counters, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    TXS_CUDA(c, "stats", cudaStreamSynchronize(c->stream));
+    *out = c->stats;
+    out->vix_los = (int64_t)h[kVixLos];
+    out->vix_crossings_full = (int64_t)h[kVixCrossFull];
+    out->viewshed_crossings = (int64_t)h[kVsCross];
+    out->viewshed_cells = (int64_t)h[kVsCells];
+    out->site_bytes = (int64_t)h[kSiteBytes];
+    out->candidates = c->ncand;
+    out->kernel_launches = c->launches;
+    return TXS_OK;
+}
+
+txs_status txs_reset_stats(txs_ctx* c) {
+    if (!c) return TXS_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(c->device);
+    c->stats = txs_stats{};
+    c->launches = 0;
+    TXS_CUDA(c, "stats", cudaMemsetAsync(c->d_counters, 0, sizeof(unsigned long long) * kNumCounters, c->stream));
+    return TXS_OK;
+}
+
+// ---- terrain ---------------------------------------------------------------
+static txs_status set_dims(txs_ctx* c, int64_t nrows, int64_t ncols) {
+    if (nrows < 2 || ncols < 2) return fail(c, TXS_ERR_INVALID_ARGUMENT, "read", "nrows and ncols must be >= 2");
+    if (nrows > 1000000 || ncols > 1000000) return fail(c, TXS_ERR_RANGE, "read", "grid dimension > 1e6");
+    TXS_CUDA(c, "read", cudaStreamSynchronize(c->stream));
+    if (ensure(c, "read", (void**)&c->d_z, &c->z_cap, sizeof(int16_t) * nrows * ncols) != TXS_OK)
+        return TXS_ERR_OUT_OF_MEMORY;
+    c->nrows = nrows;
+    c->ncols = ncols;
+    c->vix_valid = c->cand_valid = c->vs_valid = c->site_valid = false;
+    return TXS_OK;
+}
+
+txs_status txs_set_terrain(txs_ctx* c, const int16_t* z, int64_t nrows, int64_t ncols) {
+    if (!c || !z) return TXS_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(c->device);
+    txs_status st = set_dims(c, nrows, ncols);
+    if (st != TXS_OK) return st;
+    StageTimer t(c, &c->stats.ms_terrain);
+    const int64_t n = nrows * ncols;
+    TXS_CUDA(c, "read", cudaMemcpyAsync(c->d_z, z, sizeof(int16_t) * n, cudaMemcpyHostToDevice, c->stream));
+    int* flag = nullptr;
+    if (ensure(c, "read", &c->d_scratch, &c->scratch_cap, 64) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
+    flag = (int*)c->d_scratch;
+    TXS_CUDA(c, "read", cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
+    k_nodata_check<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_z, n, flag);
+    TXS_LAUNCHED(c, "read");
+    int h = 0;
+    TXS_CUDA(c, "read", cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    st = t.stop("read");
+    if (st != TXS_OK) return st;
+    if (h) { c->nrows = c->ncols = 0; return fail(c, TXS_ERR_NODATA, "read", "NODATA sentinel -32768 in terrain"); }
+    return TXS_OK;
+}
+
+txs_status txs_generate_fractal(txs_ctx* c, int64_t nrows, int64_t ncols, double roughness,
+                                uint64_t seed, int32_t zmin, int32_t zmax) {
+    if (!c) return TXS_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(c->device);
+    if (zmin > zmax) return fail(c, TXS_ERR_INVALID_ARGUMENT, "read", "zmin > zmax");
+    if (!(roughness > 0.0) || roughness > 1.0) return fail(c, TXS_ERR_INVALID_ARGUMENT, "read", "roughness must be in (0,1]");
+    if (zmin < -32767 || zmax > 32767) return fail(c, TXS_ERR_INVALID_ARGUMENT, "read", "elevations must fit int16 (no -32768)");
+    txs_status st = set_dims(c, nrows, ncols);
+    if (st != TXS_OK) return st;
+    StageTimer t(c, &c->stats.ms_terrain);
+    st = launch_generate(c, nrows, ncols, roughness, seed, zmin, zmax);
+    if (st != TXS_OK) return st;
+    return t.stop("read");
+}
+
+txs_status txs_fill_rows(txs_ctx* c, int64_t rb, int64_t re, int16_t v) {
+    if (!c) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->d_z) return fail(c, TXS_ERR_STATE, "read", "no terrain");
+    if (rb < 0 || re > c->nrows || rb > re || v == -32768)
+        return fail(c, TXS_ERR_INVALID_ARGUMENT, "read", "bad row range or value");
+    cudaSetDevice(c->device);
+    c->vix_valid = c->cand_valid = c->vs_valid = c->site_valid = false;
+    return launch_fill_rows(c, rb, re, v);
+}
+
+txs_status txs_get_terrain(txs_ctx* c, int16_t* z) {
+    if (!c || !z) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->d_z) return fail(c, TXS_ERR_STATE, "read", "no terrain");
+    cudaSetDevice(c->device);
+    TXS_CUDA(c, "read", cudaMemcpyAsync(z, c->d_z, sizeof(int16_t) * c->nrows * c->ncols, cudaMemcpyDeviceToHost, c->stream));
+    TXS_CUDA(c, "read", cudaStreamSynchronize(c->stream));
+    return TXS_OK;
+}
+
+txs_status txs_terrain_dims(const txs_ctx* c, int64_t* nrows, int64_t* ncols) {
+    if (!c || !nrows || !ncols) return TXS_ERR_INVALID_ARGUMENT;
+    *nrows = c->nrows;
+    *ncols = c->ncols;
+    return TXS_OK;
+}
+
+// ---- los -------------------------------------------------------------------
+txs_status txs_is_visible_batch(txs_ctx* c, const int32_t* pairs, int64_t n, int32_t ht,
+                                int32_t hr, uint8_t* out) {
+    if (!c || (n > 0 && (!pairs || !out)) || n < 0) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->d_z) return fail(c, TXS_ERR_STATE, "los", "no terrain");
+    if (ht < 0 || hr < 0 || ht > 32767 || hr > 32767) return fail(c, TXS_ERR_INVALID_ARGUMENT, "los", "bad heights");
+    if (n == 0) return TXS_OK;
+    cudaSetDevice(c->device);
+    for (int64_t i = 0; i < n; ++i) {
+        const int32_t* p = pairs + 4 * i;
+        if (p[0] < 0 || p[0] >= c->nrows || p[2] < 0 || p[2] >= c->nrows || p[1] < 0 ||
+            p[1] >= c->ncols || p[3] < 0 || p[3] >= c->ncols)
+            return fail(c, TXS_ERR_OFF_GRID, "los", "off-grid base point");
+        const int64_t dr = std::abs((int64_t)p[2] - p[0]), dc = std::abs((int64_t)p[3] - p[1]);
+        if (std::max(dr, dc) > 8000) return fail(c, TXS_ERR_RANGE, "los", "segment longer than 8000 posts");
+    }
+    int32_t* dp = nullptr;
+    uint8_t* dout = nullptr;
+    TXS_CUDA(c, "los", cudaMalloc(&dp, sizeof(int32_t) * 4 * n));
+    TXS_CUDA(c, "los", cudaMalloc(&dout, n));
+    TXS_CUDA(c, "los", cudaMemcpyAsync(dp, pairs, sizeof(int32_t) * 4 * n, cudaMemcpyHostToDevice, c->stream));
+    txs_status st = launch_los_batch(c, dp, n, ht, hr, dout);
+    if (st == TXS_OK) {
+        cudaMemcpyAsync(out, dout, n, cudaMemcpyDeviceToHost, c->stream);
+        cudaError_t e = cudaStreamSynchronize(c->stream);
+        if (e != cudaSuccess) st = cuda_fail(c, "los", e);
+    }
+    cudaFree(dp);
+    cudaFree(dout);
+    return st;
+}
+
+// ---- vix ---------------------------------------------------------------------
+txs_status txs_estimate_vix(txs_ctx* c, const txs_params* p, uint8_t* scores_out) {
+    if (!c) return TXS_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(c->device);
+    txs_status st = check_params(c, "vix", p, true);
+    if (st != TXS_OK) return st;
+    if (ensure(c, "vix", (void**)&c->d_vix, &c->vix_cap, (size_t)(c->nrows * c->ncols)) != TXS_OK)
+        return TXS_ERR_OUT_OF_MEMORY;
+    StageTimer t(c, &c->stats.ms_vix);
+    st = launch_vix(c, *p);
+    if (st != TXS_OK) return st;
+    st = t.stop("vix");
+    if (st != TXS_OK) return st;
+    c->vix_valid = true;
+    if (scores_out) {
+        TXS_CUDA(c, "vix", cudaMemcpyAsync(scores_out, c->d_vix, c->nrows * c->ncols, cudaMemcpyDeviceToHost, c->stream));
+        TXS_CUDA(c, "vix", cudaStreamSynchronize(c->stream));
+    }
+    return TXS_OK;
+}
+
+txs_status txs_set_vix(txs_ctx* c, const uint8_t* scores) {
+    if (!c || !scores) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->d_z) return fail(c, TXS_ERR_STATE, "vix", "no terrain");
+    cudaSetDevice(c->device);
+    if (ensure(c, "vix", (void**)&c->d_vix, &c->vix_cap, (size_t)(c->nrows * c->ncols)) != TXS_OK)
+        return TXS_ERR_OUT_OF_MEMORY;
+    TXS_CUDA(c, "vix", cudaMemcpyAsync(c->d_vix, scores, c->nrows * c->ncols, cudaMemcpyHostToDevice, c->stream));
+    TXS_CUDA(c, "vix", cudaStreamSynchronize(c->stream));
+    c->vix_valid = true;
+    return TXS_OK;
+}
+
+// ---- candidates ----------------------------------------------------------------
+txs_status txs_partition(int64_t nrows, int64_t ncols, int32_t roi, int32_t block_width,
+                         int64_t* bw, int64_t* bx, int64_t* by) {
+    if (!bw || !bx || !by || nrows < 1 || ncols < 1 || block_width < 0) return TXS_ERR_INVALID_ARGUMENT;
+    if (block_width == 0 && roi < 3) return TXS_ERR_INVALID_ARGUMENT;
+    *bw = block_width > 0 ? block_width : default_bw(roi);
+    *bx = (ncols + *bw - 1) / *bw;
+    *by = (nrows + *bw - 1) / *bw;
+    return TXS_OK;
+}
+
+txs_status txs_find_candidates(txs_ctx* c, const txs_params* p, int64_t* n_out, txs_candidate* out, int64_t cap) {
+    if (!c || !p) return TXS_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(c->device);
+    if (!c->vix_valid) return fail(c, TXS_ERR_STATE, "findmax", "no VixMap (run estimate_vix first)");
+    if (p->per_block < 1) return fail(c, TXS_ERR_INVALID_ARGUMENT, "findmax", "per_block < 1");
+    int64_t bw, bx, by;
+    if (txs_partition(c->nrows, c->ncols, p->roi, p->block_width, &bw, &bx, &by) != TXS_OK)
+        return fail(c, TXS_ERR_INVALID_ARGUMENT, "findmax", "roi < 3 with default block width");
+    StageTimer t(c, &c->stats.ms_findmax);
+    txs_status st = launch_findmax(c, *p, bw);
+    if (st != TXS_OK) return st;
+    st = t.stop("findmax");
+    if (st != TXS_OK) return st;
+    c->cand_valid = true;
+    c->vs_valid = c->site_valid = false;
+    if (n_out) *n_out = c->ncand;
+    if (out) return txs_get_candidates(c, out, cap, nullptr);
+    return TXS_OK;
+}
+
+txs_status txs_get_candidates(txs_ctx* c, txs_candidate* out, int64_t cap, int64_t* n_out) {
+    if (!c) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->cand_valid) return fail(c, TXS_ERR_STATE, "findmax", "no candidates");
+    if (n_out) *n_out = c->ncand;
+    if (!out) return TXS_OK;
+    cudaSetDevice(c->device);
+    const int64_t n = std::min(cap, c->ncand);
+    if (n <= 0) return TXS_OK;
+    std::vector<int32_t> r(n), cc(n), s(n);
+    TXS_CUDA(c, "findmax", cudaMemcpyAsync(r.data(), c->d_crow, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+    TXS_CUDA(c, "findmax", cudaMemcpyAsync(cc.data(), c->d_ccol, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+    TXS_CUDA(c, "findmax", cudaMemcpyAsync(s.data(), c->d_cscore, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+    TXS_CUDA(c, "findmax", cudaStreamSynchronize(c->stream));
+    for (int64_t i = 0; i < n; ++i) out[i] = txs_candidate{r[i], cc[i], s[i], 0};
+    return TXS_OK;
+}
+
+static txs_status alloc_cands(txs_ctx* c, int64_t n) {
+    const size_t need = sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1);
+    if (need <= c->cand_cap && c->d_crow) return TXS_OK;
+    for (int32_t** p : {&c->d_crow, &c->d_ccol, &c->d_cscore}) {
+        if (*p) cudaFree(*p);
+        *p = nullptr;
+    }
+    c->cand_cap = 0;
+    for (int32_t** p : {&c->d_crow, &c->d_ccol, &c->d_cscore})
+        TXS_CUDA(c, "findmax", cudaMalloc(p, need));
+    c->cand_cap = need;
+    return TXS_OK;
+}
+
+txs_status txs_set_candidates(txs_ctx* c, const txs_candidate* in, int64_t n) {
+    if (!c || n < 0 || (n > 0 && !in)) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->d_z) return fail(c, TXS_ERR_STATE, "findmax", "no terrain");
+    if (n >= 0x7fffffff) return fail(c, TXS_ERR_RANGE, "findmax", "too many candidates");
+    cudaSetDevice(c->device);
+    std::vector<int32_t> r(n), cc(n), s(n);
+    for (int64_t i = 0; i < n; ++i) {
+        if (in[i].row < 0 || in[i].row >= c->nrows || in[i].col < 0 || in[i].col >= c->ncols)
+            return fail(c, TXS_ERR_OFF_GRID, "viewshed", "candidate off grid");
+        r[i] = in[i].row; cc[i] = in[i].col; s[i] = in[i].score;
+    }
+    TXS_CUDA(c, "findmax", cudaStreamSynchronize(c->stream));
+    if (alloc_cands(c, n) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
+    if (n > 0) {
+        TXS_CUDA(c, "findmax", cudaMemcpyAsync(c->d_crow, r.data(), 4 * n, cudaMemcpyHostToDevice, c->stream));
+        TXS_CUDA(c, "findmax", cudaMemcpyAsync(c->d_ccol, cc.data(), 4 * n, cudaMemcpyHostToDevice, c->stream));
+        TXS_CUDA(c, "findmax", cudaMemcpyAsync(c->d_cscore, s.data(), 4 * n, cudaMemcpyHostToDevice, c->stream));
+        TXS_CUDA(c, "findmax", cudaStreamSynchronize(c->stream));
+    }
+    c->ncand = n;
+    c->cand_valid = true;
+    c->vs_valid = c->site_valid = false;
+    return TXS_OK;
+}
+
+txs_status txs_random_observers(txs_ctx* c, int64_t n, uint64_t seed) {
+    if (!c || n < 0) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->d_z) return fail(c, TXS_ERR_STATE, "findmax", "no terrain");
+    if (n >= 0x7fffffff) return fail(c, TXS_ERR_RANGE, "findmax", "too many observers");
+    cudaSetDevice(c->device);
+    TXS_CUDA(c, "findmax", cudaStreamSynchronize(c->stream));
+    if (alloc_cands(c, n) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
+    StageTimer t(c, &c->stats.ms_findmax);
+    txs_status st = launch_random_observers(c, n, seed);
+    if (st != TXS_OK) return st;
+    st = t.stop("findmax");
+    if (st != TXS_OK) return st;
+    c->ncand = n;
+    c->cand_valid = true;
+    c->vs_valid = c->site_valid = false;
+    return TXS_OK;
+}
+
+// ---- viewsheds -------------------------------------------------------------------
+txs_status txs_compute_viewsheds(txs_ctx* c, const txs_params* p) {
+    if (!c) return TXS_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(c->device);
+    txs_status st = check_params(c, "viewshed", p, false);
+    if (st != TXS_OK) return st;
+    if (!c->cand_valid) return fail(c, TXS_ERR_STATE, "viewshed", "no candidates");
+    StageTimer t(c, &c->stats.ms_viewshed);
+    st = launch_viewsheds(c, *p);
+    if (st != TXS_OK) return st;
+    st = t.stop("viewshed");
+    if (st != TXS_OK) return st;
+    c->vs_valid = true;
+    c->site_valid = false;
+    return TXS_OK;
+}
+
+txs_status txs_get_viewsheds(txs_ctx* c, int64_t first, int64_t count, txs_window* wins,
+                             uint64_t* words, int64_t stride, int64_t* pops) {
+    if (!c) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->vs_valid) return fail(c, TXS_ERR_STATE, "viewshed", "no viewsheds");
+    if (first < 0 || count < 0 || first + count > c->vs_n) return fail(c, TXS_ERR_INVALID_ARGUMENT, "viewshed", "range");
+    if (words && stride < c->vs_stride) return fail(c, TXS_ERR_INVALID_ARGUMENT, "viewshed", "words_stride too small");
+    if (count == 0) return TXS_OK;
+    cudaSetDevice(c->device);
+    std::vector<int4> w(count);
+    TXS_CUDA(c, "viewshed", cudaMemcpyAsync(w.data(), c->d_win + first, sizeof(int4) * count, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<int32_t> pc;
+    if (pops) {
+        pc.resize(count);
+        TXS_CUDA(c, "viewshed", cudaMemcpyAsync(pc.data(), c->d_pop + first, 4 * count, cudaMemcpyDeviceToHost, c->stream));
+    }
+    if (words)
+        TXS_CUDA(c, "viewshed", cudaMemcpy2DAsync(words, stride * 8, c->d_words + first * c->vs_stride,
+                                                  c->vs_stride * 8, c->vs_stride * 8, count,
+                                                  cudaMemcpyDeviceToHost, c->stream));
+    TXS_CUDA(c, "viewshed", cudaStreamSynchronize(c->stream));
+    for (int64_t i = 0; i < count; ++i) {
+        if (wins) wins[i] = txs_window{w[i].x, w[i].y, w[i].z, w[i].w};
+        if (pops) pops[i] = pc[i];
+        if (words) {   // zero the tail beyond the window's words (SPEC.md:298 padding)
+            const int64_t nw = ((int64_t)w[i].z * w[i].w + 63) / 64;
+            std::fill(words + i * stride + nw, words + (i + 1) * stride, 0ull);
+        }
+    }
+    return TXS_OK;
+}
+
+txs_status txs_set_viewsheds(txs_ctx* c, int32_t roi, int64_t n, const int32_t* rows, const int32_t* cols,
+                             const txs_window* wins, const uint64_t* words, int64_t stride) {
+    if (!c || n < 0 || roi < 1 || roi > 4000 || (n > 0 && (!rows || !cols || !wins || !words)))
+        return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->d_z) return fail(c, TXS_ERR_STATE, "site", "no terrain");
+    const int64_t mw = max_window_words(roi);
+    if (stride < mw) return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "words_stride too small");
+    std::vector<txs_candidate> cand(n);
+    std::vector<int4> w(n);
+    std::vector<int32_t> pop(n);
+    for (int64_t i = 0; i < n; ++i) {
+        const txs_window& x = wins[i];
+        if (x.row0 < 0 || x.col0 < 0 || x.h < 1 || x.w < 1 || x.row0 + x.h > c->nrows || x.col0 + x.w > c->ncols ||
+            x.h > 2 * roi + 1 || x.w > 2 * roi + 1)
+            return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "window out of bounds");
+        cand[i] = txs_candidate{rows[i], cols[i], 0, 0};
+        w[i] = make_int4(x.row0, x.col0, x.h, x.w);
+        const int64_t nw = ((int64_t)x.h * x.w + 63) / 64;
+        int64_t pc = 0;
+        for (int64_t k = 0; k < nw; ++k) pc += __builtin_popcountll(words[i * stride + k]);
+        pop[i] = (int32_t)pc;
+    }
+    txs_status st = txs_set_candidates(c, cand.data(), n);
+    if (st != TXS_OK) return st;
+    cudaSetDevice(c->device);
+    if (ensure(c, "site", (void**)&c->d_words, &c->words_cap, sizeof(uint64_t) * (n * mw + 8)) != TXS_OK ||
+        ensure(c, "site", (void**)&c->d_win, &c->win_cap, sizeof(int4) * std::max<int64_t>(1, n)) != TXS_OK)
+        return TXS_ERR_OUT_OF_MEMORY;
+    if (ensure(c, "site", (void**)&c->d_pop, &c->pop_cap, sizeof(int32_t) * std::max<int64_t>(1, n)) != TXS_OK)
+        return TXS_ERR_OUT_OF_MEMORY;
+    if (n > 0) {
+        TXS_CUDA(c, "site", cudaMemcpy2DAsync(c->d_words, mw * 8, words, stride * 8, mw * 8, n, cudaMemcpyHostToDevice, c->stream));
+        TXS_CUDA(c, "site", cudaMemcpyAsync(c->d_win, w.data(), sizeof(int4) * n, cudaMemcpyHostToDevice, c->stream));
+        TXS_CUDA(c, "site", cudaMemcpyAsync(c->d_pop, pop.data(), 4 * n, cudaMemcpyHostToDevice, c->stream));
+        TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+    }
+    c->vs_roi = roi;
+    c->vs_n = n;
+    c->vs_stride = mw;
+    c->vs_valid = true;
+    c->site_valid = false;
+    return TXS_OK;
+}
+
+// ---- siting ---------------------------------------------------------------------
+txs_status txs_site(txs_ctx* c, const txs_params* p, txs_step* steps, int64_t cap, int64_t* nsteps, int32_t* stop) {
+    if (!c || !p) return TXS_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(c->device);
+    if (!c->vs_valid) return fail(c, TXS_ERR_STATE, "site", "no viewsheds");
+    if (!(p->target_coverage > 0.0) || p->target_coverage > 1.0)
+        return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "target_coverage must be in (0,1]");
+    if (p->max_selected < 0) return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "max_selected < 0");
+    std::vector<txs_step> v;
+    int32_t sr = 0;
+    StageTimer t(c, &c->stats.ms_site);
+    txs_status st = run_site(c, *p, v, &sr);
+    if (st != TXS_OK) return st;
+    st = t.stop("site");
+    if (st != TXS_OK) return st;
+    c->site_valid = true;
+    if (nsteps) *nsteps = (int64_t)v.size();
+    if (stop) *stop = sr;
+    if (steps) std::copy(v.begin(), v.begin() + std::min<int64_t>(cap, (int64_t)v.size()), steps);
+    return TXS_OK;
+}
+
+txs_status txs_get_cumulative(txs_ctx* c, uint64_t* out) {
+    if (!c || !out) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->site_valid) return fail(c, TXS_ERR_STATE, "site", "no cumulative viewshed (run site first)");
+    cudaSetDevice(c->device);
+    return download_cum(c, out);
+}
+
+txs_status txs_marginal_gains(txs_ctx* c, const uint64_t* cum_dense, int64_t* gains_out) {
+    if (!c || !cum_dense || !gains_out) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->vs_valid) return fail(c, TXS_ERR_STATE, "site", "no viewsheds");
+    cudaSetDevice(c->device);
+    const int64_t nw = (c->nrows * c->ncols + 63) / 64;
+    uint64_t* dc = nullptr;
+    int64_t* dg = nullptr;
+    TXS_CUDA(c, "site", cudaMalloc(&dc, 8 * (nw + 1)));
+    TXS_CUDA(c, "site", cudaMalloc(&dg, 8 * std::max<int64_t>(1, c->vs_n)));
+    TXS_CUDA(c, "site", cudaMemcpyAsync(dc, cum_dense, 8 * nw, cudaMemcpyHostToDevice, c->stream));
+    TXS_CUDA(c, "site", cudaMemsetAsync(dc + nw, 0, 8, c->stream));
+    txs_status st = launch_marginal_gains(c, dc, dg);
+    if (st == TXS_OK && c->vs_n > 0) {
+        cudaMemcpyAsync(gains_out, dg, 8 * c->vs_n, cudaMemcpyDeviceToHost, c->stream);
+        cudaError_t e = cudaStreamSynchronize(c->stream);
+        if (e != cudaSuccess) st = cuda_fail(c, "site", e);
+    }
+    cudaFree(dc);
+    cudaFree(dg);
+    return st;
+}
+
+// ---- run_pipeline -----------------------------------------------
+txs_status txs_run_pipeline(txs_ctx* c, const txs_params* p, txs_step* steps, int64_t cap,
+                            int64_t* nsteps, int32_t* stop, double* stage_ms) {
+    if (!c || !p) return TXS_ERR_INVALID_ARGUMENT;
+    const txs_stats before = c->stats;
+    txs_status st = txs_estimate_vix(c, p, nullptr);
+    if (st != TXS_OK) return st;
+    st = txs_find_candidates(c, p, nullptr, nullptr, 0);
+    if (st != TXS_OK) return st;
+    st = txs_compute_viewsheds(c, p);
+    if (st != TXS_OK) return st;
+    st = txs_site(c, p, steps, cap, nsteps, stop);
+    if (st != TXS_OK) return st;
+    if (stage_ms) {
+        stage_ms[0] = c->stats.ms_vix - before.ms_vix;
+        stage_ms[1] = c->stats.ms_findmax - before.ms_findmax;
+        stage_ms[2] = c->stats.ms_viewshed - before.ms_viewshed;
+        stage_ms[3] = c->stats.ms_site - before.ms_site;
+    }
+    return TXS_OK;
+}
+
+int txs_selftest(void) {
+    // exact 64-bit modulo magic vs the hardware '%', divisors of the shapes
+    // the engine uses (2roi+1, 2A+1, grid dims) plus random ones
+    uint64_t ctr = 0;
+    auto rnd = [&]() { return sm_draw(0x1234567ull, ctr++); };
+    std::vector<uint64_t> ds = {3, 5, 7, 201, 401, 501, 1000, 4096, 16384, 46400, 2097153, 65537, 0xFFFFFFFFFFFFFFFFull};
+    for (int i = 0; i < 200; ++i) ds.push_back((rnd() >> (rnd() % 62)) | 2);
+    for (uint64_t d : ds) {
+        const FastMod64 f = make_fastmod(d);
+        for (int i = 0; i < 2000; ++i) {
+            uint64_t x = rnd();
+            if (i < 8) x = (i < 4) ? (uint64_t)i : ~(uint64_t)(i - 4);
+            if (i == 8) x = d * (x / d);
+            if (fm_div(f, x) != x / d || fm_mod(f, x) != x % d) return 1;
+        }
+    }
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,151 @@
+// Internal state of a txs_ctx: everything resident in HBM between stages.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/txsite_b200.h"
+#include "common.cuh"
+
+namespace txs {
+
+// D5 ray template in host form (built by raytemplate.cpp).
+struct RayTemplate {
+    int32_t roi = 0;
+    std::vector<int32_t> p, q;          // primitive directions, angle order
+    std::vector<int64_t> cell_begin;    // rays+1
+    std::vector<int32_t> ca, cb;        // owned cells sorted by projection
+};
+const RayTemplate& ray_template(int32_t roi);
+
+// Device copy: rays[r] = {p, q, cell_begin, cell_count}; cells packed (a & 0xffff) | (b << 16).
+struct RayTemplateDev {
+    int32_t roi = 0, nrays = 0;
+    int64_t ncells = 0;
+    int4* rays = nullptr;
+    uint32_t* cells = nullptr;
+};
+
+// Device-side SITE loop state (one struct, read/written by the loop kernels).
+constexpr int kMaxNb = 64;   // neighbour bucket ranges per winner
+struct SiteState {
+    unsigned long long best_key;   // (gain << 32) | (0xffffffff - idx), atomicMax target
+    long long nsel;
+    long long covered;
+    long long iter;
+    int done;
+    int stop;
+    int w_idx, w_gain;
+    int w_row0, w_col0, w_h, w_w;   // current winner window
+    int p_row0, p_col0, p_h, p_w;   // previous winner window (delta clearing)
+    int nb_count;
+    int nb_start[kMaxNb];
+    int nb_pref[kMaxNb + 1];
+};
+
+// device counter slots
+enum Counter : int {
+    kVixLos = 0, kVixCrossFull, kVsCross, kVsCells, kSiteBytes, kNumCounters
+};
+
+}  // namespace txs
+
+struct txs_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    int num_sms = 148;
+
+    // terrain: row-major int16 in HBM
+    int64_t nrows = 0, ncols = 0;
+    int16_t* d_z = nullptr;
+    size_t z_cap = 0;
+
+    // VixMap: one byte per post
+    uint8_t* d_vix = nullptr;
+    size_t vix_cap = 0;
+    bool vix_valid = false;
+
+    // candidates, in candidate-index order
+    int64_t ncand = 0;
+    int32_t *d_crow = nullptr, *d_ccol = nullptr, *d_cscore = nullptr;
+    size_t cand_cap = 0;
+    bool cand_valid = false;
+
+    // viewsheds: fixed stride of max window words per candidate
+    int32_t vs_roi = 0;
+    int64_t vs_n = 0, vs_stride = 0;
+    uint64_t* d_words = nullptr;
+    size_t words_cap = 0;
+    int4* d_win = nullptr;        // {row0, col0, h, w}
+    int32_t* d_pop = nullptr;     // popcount per viewshed
+    size_t win_cap = 0, pop_cap = 0;
+    bool vs_valid = false;
+    std::map<int32_t, txs::RayTemplateDev> templates;
+
+    // SITE: row-padded bitmaps (wpr words per terrain row)
+    int64_t wpr = 0;
+    uint64_t* d_cum = nullptr;
+    uint64_t* d_delta[2] = {nullptr, nullptr};
+    size_t bitmap_cap = 0;
+    int32_t* d_gain = nullptr;
+    size_t gain_cap = 0;
+    txs::SiteState* d_state = nullptr;
+    txs::SiteState* h_state = nullptr;   // pinned mirror
+    int32_t* d_bucket_start = nullptr;   // CSR over candidate buckets
+    int32_t* d_bucket_items = nullptr;
+    size_t bucket_cap = 0, bucket_items_cap = 0;
+    bool site_valid = false;
+
+    // stats
+    txs_stats stats{};
+    unsigned long long* d_counters = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t user_ev[16] = {};
+    int64_t launches = 0;
+
+    // scratch
+    void* d_scratch = nullptr;
+    size_t scratch_cap = 0;
+};
+
+namespace txs {
+
+txs_status fail(txs_ctx* ctx, txs_status st, const char* stage, const std::string& msg);
+txs_status cuda_fail(txs_ctx* ctx, const char* stage, cudaError_t e);
+// (re)allocate *p to at least bytes; contents not preserved
+txs_status ensure(txs_ctx* ctx, const char* stage, void** p, size_t* cap, size_t bytes);
+txs_status check_params(txs_ctx* ctx, const char* stage, const txs_params* p, bool need_vix);
+txs_status get_template(txs_ctx* ctx, int32_t roi, RayTemplateDev** out);
+inline int64_t max_window_words(int64_t roi) { return ((2 * roi + 1) * (2 * roi + 1) + 63) / 64; }
+
+// stage launchers (one .cu each)
+txs_status launch_generate(txs_ctx*, int64_t nrows, int64_t ncols, double roughness, uint64_t seed,
+                           int32_t zmin, int32_t zmax);
+txs_status launch_fill_rows(txs_ctx*, int64_t rb, int64_t re, int16_t v);
+txs_status launch_vix(txs_ctx*, const txs_params& p);
+txs_status launch_los_batch(txs_ctx*, const int32_t* d_pairs, int64_t n, int32_t ht, int32_t hr,
+                            uint8_t* d_out);
+txs_status launch_findmax(txs_ctx*, const txs_params& p, int64_t bw);
+txs_status launch_random_observers(txs_ctx*, int64_t n, uint64_t seed);
+txs_status launch_viewsheds(txs_ctx*, const txs_params& p);
+txs_status run_site(txs_ctx*, const txs_params& p, std::vector<txs_step>& steps, int32_t* stop);
+txs_status launch_marginal_gains(txs_ctx*, const uint64_t* d_cum_dense, int64_t* d_gains);
+txs_status download_cum(txs_ctx*, uint64_t* host_dense);
+
+}  // namespace txs
+
+#define TXS_CUDA(ctx, stage, call)                                   \
+    do {                                                             \
+        cudaError_t _e = (call);                                     \
+        if (_e != cudaSuccess) return txs::cuda_fail(ctx, stage, _e); \
+    } while (0)
+
+#define TXS_LAUNCHED(ctx, stage)                                                \
+    do {                                                                        \
+        ++(ctx)->launches;                                                      \
+        cudaError_t _e = cudaGetLastError();                                    \
+        if (_e != cudaSuccess) return txs::cuda_fail(ctx, stage, _e);           \
+    } while (0)

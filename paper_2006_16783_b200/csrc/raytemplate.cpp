@@ -1,0 +1,155 @@
+// Viewshed ray template (decision D5) — product code.
+//
+// SPEC.md:288,322 leave the R2 cell rule open; the frozen rule is:
+//   rays  = primitive directions of the midpoint-circle perimeter cells of
+//           radius roi ("midpoint-circle rasterization") plus the
+//           8 principal directions ("exact agreement on the 8
+//           axis/diagonal rays"), in angle order starting at (0,+1);
+//   owner = every lattice-disk cell (a,b) != (0,0) belongs to the forward ray
+//           with least perpendicular distance, ties to the lowest ray index.
+// Perpendicular distance |a q - b p| / |(p,q)| = |cell| * |sin(dtheta)| is
+// monotone in the angle gap for forward rays, so the owner is one of the two
+// rays bracketing the cell's angle: binary search + 2 exact int64 compares per
+// cell instead of the O(cells x rays) scan the oracle uses.
+#include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <numeric>
+#include <tuple>
+
+#include "ctx.hpp"
+
+namespace txs {
+
+namespace {
+
+struct Dir { int64_t p, q; };   // p = row offset, q = col offset
+
+inline int half_plane(const Dir& d) { return (d.p > 0 || (d.p == 0 && d.q > 0)) ? 0 : 1; }
+// strict angle order with x = q, y = p
+inline bool angle_less(const Dir& a, const Dir& b) {
+    const int ha = half_plane(a), hb = half_plane(b);
+    if (ha != hb) return ha < hb;
+    return a.q * b.p - a.p * b.q > 0;
+}
+
+std::vector<Dir> perimeter(int64_t R) {
+    std::vector<Dir> v;
+    int64_t x = R, y = 0, err = 1 - R;
+    while (x >= y) {
+        v.push_back({x, y});   v.push_back({y, x});
+        v.push_back({-y, x});  v.push_back({-x, y});
+        v.push_back({-x, -y}); v.push_back({-y, -x});
+        v.push_back({y, -x});  v.push_back({x, -y});
+        ++y;
+        if (err < 0) err += 2 * y + 1;
+        else { --x; err += 2 * (y - x) + 1; }
+    }
+    return v;
+}
+
+RayTemplate build(int32_t R) {
+    RayTemplate T;
+    T.roi = R;
+    std::vector<Dir> dirs;
+    for (const Dir& d : perimeter(R)) {
+        const int64_t g = std::gcd(std::llabs(d.p), std::llabs(d.q));
+        dirs.push_back({d.p / g, d.q / g});
+    }
+    for (int64_t p = -1; p <= 1; ++p)
+        for (int64_t q = -1; q <= 1; ++q)
+            if (p || q) dirs.push_back({p, q});
+    std::sort(dirs.begin(), dirs.end(), angle_less);
+    dirs.erase(std::unique(dirs.begin(), dirs.end(),
+                           [](const Dir& a, const Dir& b) { return a.p == b.p && a.q == b.q; }),
+               dirs.end());
+    const int64_t n = (int64_t)dirs.size();
+    for (const Dir& d : dirs) { T.p.push_back((int32_t)d.p); T.q.push_back((int32_t)d.q); }
+
+    std::vector<std::vector<std::tuple<int64_t, int32_t, int32_t>>> own((size_t)n);
+    for (int64_t a = -R; a <= R; ++a)
+        for (int64_t b = -R; b <= R; ++b) {
+            if ((a == 0 && b == 0) || a * a + b * b > (int64_t)R * R) continue;
+            const Dir c{a, b};
+            // first ray not less than the cell's direction
+            const int64_t hi = std::lower_bound(dirs.begin(), dirs.end(), c, angle_less) - dirs.begin();
+            const int64_t r1 = hi % n, r0 = (hi + n - 1) % n;
+            auto key = [&](int64_t r, int64_t* c2, int64_t* l2) {
+                const int64_t cr = a * dirs[r].q - b * dirs[r].p;
+                *c2 = cr * cr;
+                *l2 = dirs[r].p * dirs[r].p + dirs[r].q * dirs[r].q;
+            };
+            int64_t c0, l0, c1, l1;
+            key(r0, &c0, &l0);
+            key(r1, &c1, &l1);
+            int64_t best;
+            const __int128 lhs = (__int128)c1 * l0, rhs = (__int128)c0 * l1;   // c1/l1 vs c0/l0
+            if (lhs < rhs) best = r1;
+            else if (lhs > rhs) best = r0;
+            else best = std::min(r0, r1);
+            own[(size_t)best].emplace_back(a * dirs[best].p + b * dirs[best].q, (int32_t)a, (int32_t)b);
+        }
+    T.cell_begin.push_back(0);
+    for (int64_t r = 0; r < n; ++r) {
+        std::sort(own[(size_t)r].begin(), own[(size_t)r].end());
+        for (auto& [d, a, b] : own[(size_t)r]) { T.ca.push_back(a); T.cb.push_back(b); }
+        T.cell_begin.push_back((int64_t)T.ca.size());
+    }
+    return T;
+}
+
+}  // namespace
+
+const RayTemplate& ray_template(int32_t roi) {
+    static std::mutex mu;
+    static std::map<int32_t, RayTemplate> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(roi);
+    if (it == cache.end()) it = cache.emplace(roi, build(roi)).first;
+    return it->second;
+}
+
+txs_status get_template(txs_ctx* ctx, int32_t roi, RayTemplateDev** out) {
+    auto it = ctx->templates.find(roi);
+    if (it != ctx->templates.end()) { *out = &it->second; return TXS_OK; }
+    const RayTemplate& T = ray_template(roi);
+    RayTemplateDev D;
+    D.roi = roi;
+    D.nrays = (int32_t)T.p.size();
+    D.ncells = (int64_t)T.ca.size();
+    std::vector<int4> rays((size_t)D.nrays);
+    for (int32_t r = 0; r < D.nrays; ++r)
+        rays[(size_t)r] = make_int4(T.p[(size_t)r], T.q[(size_t)r], (int)T.cell_begin[(size_t)r],
+                                    (int)(T.cell_begin[(size_t)r + 1] - T.cell_begin[(size_t)r]));
+    std::vector<uint32_t> cells((size_t)D.ncells);
+    for (int64_t i = 0; i < D.ncells; ++i)
+        cells[(size_t)i] = ((uint32_t)(uint16_t)(int16_t)T.ca[(size_t)i]) |
+                           ((uint32_t)(uint16_t)(int16_t)T.cb[(size_t)i] << 16);
+    TXS_CUDA(ctx, "viewshed", cudaMalloc(&D.rays, sizeof(int4) * rays.size()));
+    TXS_CUDA(ctx, "viewshed", cudaMalloc(&D.cells, sizeof(uint32_t) * std::max<size_t>(1, cells.size())));
+    TXS_CUDA(ctx, "viewshed", cudaMemcpy(D.rays, rays.data(), sizeof(int4) * rays.size(), cudaMemcpyHostToDevice));
+    if (!cells.empty())
+        TXS_CUDA(ctx, "viewshed", cudaMemcpy(D.cells, cells.data(), sizeof(uint32_t) * cells.size(), cudaMemcpyHostToDevice));
+    *out = &(ctx->templates[roi] = D);
+    return TXS_OK;
+}
+
+}  // namespace txs
+
+extern "C" int64_t txs_ray_template(int32_t roi, int32_t* p, int32_t* q, int64_t* cell_begin,
+                                    int32_t* ca, int32_t* cb, int64_t cap_rays, int64_t cap_cells,
+                                    int64_t* ncells) {
+    if (roi < 1 || roi > 4000) return -1;
+    const txs::RayTemplate& T = txs::ray_template(roi);
+    const int64_t nr = (int64_t)T.p.size(), nc = (int64_t)T.ca.size();
+    if (ncells) *ncells = nc;
+    if (cap_rays >= nr && cap_cells >= nc && p && q && cell_begin && ca && cb) {
+        std::copy(T.p.begin(), T.p.end(), p);
+        std::copy(T.q.begin(), T.q.end(), q);
+        std::copy(T.cell_begin.begin(), T.cell_begin.end(), cell_begin);
+        std::copy(T.ca.begin(), T.ca.end(), ca);
+        std::copy(T.cb.begin(), T.cb.end(), cb);
+    }
+    return nr;
+}

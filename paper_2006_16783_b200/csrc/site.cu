@@ -1,0 +1,429 @@
+// SITE stage (site, marginal_gain, coverage) — decision D9.
+//
+// Greedy max-coverage whose output equals naive greedy:
+// each round the candidate with the largest marginal gain popc(v & ~cum) wins,
+// ties to the lowest candidate index, then its window is ORed
+// into the cumulative bitmap.  Two exact device strategies (txs_params.site_mode):
+//   0  incremental: gains are kept exact; after committing winner w with newly
+//      covered bits D = v_w & ~cum, only candidates whose window overlaps w's
+//      change, by popc(v_i & D) (SPEC.md:404's lazy rule made exact instead of
+//      lazy: gain_i(t+1) = gain_i(t) - popc(v_i & D)).  Neighbours come from a
+//      CSR bucket grid of side roi over candidate positions.
+//   1  full rescan: every round recomputes popc(v_i & ~cum) for all i — the
+//      HBM-streaming pass (the SITE GB/s roofline figure).
+// Per round: k_argmax (grid reduction of (gain<<32 | ~idx)), k_commit (one
+// CTA: stop rules, delta/cum update, step record, neighbour ranges) and
+// k_update / k_gain_full, captured as a CUDA graph of kRoundsPerGraph rounds;
+// kernels become no-ops once the device flag `done` is set.
+//
+// Bitmaps inside the engine are row-padded (wpr = ceil(ncols/64) words per
+// terrain row) so a window row maps to whole words; the dense row-major
+// CumulativeShed of SPEC.md:351 is produced on download.
+#include <cub/cub.cuh>
+
+#include <vector>
+
+#include "ctx.hpp"
+
+namespace txs {
+namespace {
+
+constexpr int kRoundsPerGraph = 16;
+constexpr unsigned kFull = 0xffffffffu;
+
+struct SiteArgs {
+    int nrows, ncols, R, bsize, nbx, nby;
+    int64_t wpr, n, stride, max_sel;
+    double target, total;
+};
+
+// 64 bits of a packed window stream starting at bit offset off (off > -64);
+// bits before the stream start read as 0.  May read one word past the stream.
+__device__ __forceinline__ uint64_t stream64(const uint64_t* __restrict__ v, long long off) {
+    if (off < 0) return v[0] << (-off);
+    const long long w = off >> 6;
+    const int s = (int)(off & 63);
+    const uint64_t lo = v[w] >> s;
+    return s ? (lo | (v[w + 1] << (64 - s))) : lo;
+}
+
+// mask of terrain columns [cl, ch] inside word wi
+__device__ __forceinline__ uint64_t col_mask(int wi, int cl, int ch) {
+    const int lo = max(cl - wi * 64, 0), hi = min(ch - wi * 64, 63);
+    if (lo > hi) return 0ull;
+    const uint64_t up = hi == 63 ? ~0ull : ((1ull << (hi + 1)) - 1);
+    return up & ~((1ull << lo) - 1);
+}
+
+// popc over rows [ra, rb] x cols [cl, ch] of (v_i bits) AND (B or ~B), warp-cooperative
+template <bool COMPLEMENT>
+__device__ __forceinline__ long long warp_window_popc(const uint64_t* __restrict__ v, int4 win,
+                                                      const uint64_t* __restrict__ B, int64_t wpr,
+                                                      int ra, int rb, int cl, int ch, int lane) {
+    const int wlo = cl >> 6, whi = ch >> 6, nwr = whi - wlo + 1, nrow = rb - ra + 1;
+    long long acc = 0;
+    for (int t = lane; t < nrow * nwr; t += 32) {
+        const int y = ra + t / nwr, wi = wlo + t % nwr;
+        const uint64_t m = col_mask(wi, cl, ch);
+        const long long off = (long long)(y - win.x) * win.w + (wi * 64 - win.y);
+        uint64_t b = B[(int64_t)y * wpr + wi];
+        if (COMPLEMENT) b = ~b;
+        acc += __popcll(stream64(v, off) & b & m);
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_down_sync(kFull, acc, o);
+    return acc;
+}
+
+__global__ void k_init_gains(const int32_t* __restrict__ pop, int32_t* __restrict__ gain, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        gain[i] = pop[i];
+}
+
+__global__ void k_bucket_count(const int32_t* __restrict__ crow, const int32_t* __restrict__ ccol, int64_t n,
+                               int bsize, int nbx, int32_t* __restrict__ counts) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&counts[(crow[i] / bsize) * nbx + ccol[i] / bsize], 1);
+}
+
+__global__ void k_bucket_fill(const int32_t* __restrict__ crow, const int32_t* __restrict__ ccol, int64_t n,
+                              int bsize, int nbx, int32_t* __restrict__ cursor, int32_t* __restrict__ items) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        items[atomicAdd(&cursor[(crow[i] / bsize) * nbx + ccol[i] / bsize], 1)] = (int32_t)i;
+}
+
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) { return a > b ? a : b; }
+
+__global__ void k_argmax(const int32_t* __restrict__ gain, int64_t n, SiteState* st) {
+    if (st->done) return;
+    __shared__ unsigned long long s_red[32];
+    unsigned long long best = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long key = ((unsigned long long)(uint32_t)gain[i] << 32) | (0xffffffffull - (uint64_t)i);
+        best = umax64(best, key);
+    }
+    for (int o = 16; o; o >>= 1) best = umax64(best, __shfl_xor_sync(kFull, best, o));
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        best = threadIdx.x < (blockDim.x >> 5) ? s_red[threadIdx.x] : 0;
+        for (int o = 16; o; o >>= 1) best = umax64(best, __shfl_xor_sync(kFull, best, o));
+        if (threadIdx.x == 0 && best) atomicMax(&st->best_key, best);
+    }
+}
+
+// One CTA.  Stop rules (D9), delta + cum update over the winner window, step record,
+// neighbour bucket ranges for k_update.
+__global__ void __launch_bounds__(1024) k_commit(SiteArgs a, SiteState* st, const int32_t* __restrict__ crow,
+                                                  const int32_t* __restrict__ ccol, const int4* __restrict__ wins,
+                                                  const uint64_t* __restrict__ words, uint64_t* __restrict__ cum,
+                                                  uint64_t* __restrict__ delta0, uint64_t* __restrict__ delta1,
+                                                  const int32_t* __restrict__ bstart, txs_step* __restrict__ steps) {
+    if (st->done) return;
+    __shared__ int s_go;
+    const unsigned long long key = st->best_key;
+    const int g = (int)(key >> 32);
+    const int64_t idx = (int64_t)(0xffffffffull - (key & 0xffffffffull));
+    if (threadIdx.x == 0) {
+        s_go = 0;
+        if (st->nsel >= a.n) { st->done = 1; st->stop = TXS_STOP_EXHAUSTED; }
+        else if (g <= 0) { st->done = 1; st->stop = TXS_STOP_ZERO_GAIN; }
+        else s_go = 1;
+    }
+    __syncthreads();
+    if (!s_go) return;
+    const int cur = (int)(st->iter & 1);
+    uint64_t* dcur = cur ? delta1 : delta0;
+    uint64_t* dprev = cur ? delta0 : delta1;
+    // clear the previous winner's region of the other delta buffer
+    if (st->iter > 0) {
+        const int pr0 = st->p_row0, pc0 = st->p_col0, ph = st->p_h, pw = st->p_w;
+        const int wlo = pc0 >> 6, nwr = ((pc0 + pw - 1) >> 6) - wlo + 1;
+        for (int t = threadIdx.x; t < ph * nwr; t += blockDim.x)
+            dprev[(int64_t)(pr0 + t / nwr) * a.wpr + wlo + t % nwr] = 0ull;
+    }
+    const int4 win = wins[idx];
+    const uint64_t* v = words + idx * a.stride;
+    {
+        const int wlo = win.y >> 6, nwr = ((win.y + win.w - 1) >> 6) - wlo + 1;
+        for (int t = threadIdx.x; t < win.z * nwr; t += blockDim.x) {
+            const int y = win.x + t / nwr, wi = wlo + t % nwr;
+            const uint64_t m = col_mask(wi, win.y, win.y + win.w - 1);
+            const long long off = (long long)(y - win.x) * win.w + (wi * 64 - win.y);
+            const int64_t o = (int64_t)y * a.wpr + wi;
+            const uint64_t c = cum[o];
+            const uint64_t d = stream64(v, off) & m & ~c;
+            dcur[o] = d;
+            cum[o] = c | d;
+        }
+    }
+    if (threadIdx.x == 0) {
+        const int64_t k = st->nsel;
+        const int r = crow[idx], c = ccol[idx];
+        st->covered += g;
+        const double cov = (double)st->covered / a.total;
+        steps[k] = txs_step{idx, r, c, (int64_t)g, cov};
+        st->nsel = k + 1;
+        st->iter += 1;
+        st->w_idx = (int)idx; st->w_gain = g;
+        st->w_row0 = win.x; st->w_col0 = win.y; st->w_h = win.z; st->w_w = win.w;
+        st->p_row0 = win.x; st->p_col0 = win.y; st->p_h = win.z; st->p_w = win.w;
+        if (cov >= a.target) { st->done = 1; st->stop = TXS_STOP_TARGET_REACHED; }
+        else if (a.max_sel > 0 && k + 1 >= a.max_sel) { st->done = 1; st->stop = TXS_STOP_MAX_SELECTED; }
+        // neighbours: candidates within 2R rows/cols of the winner (window overlap)
+        const int by0 = max(0, (r - 2 * a.R) / a.bsize), by1 = min(a.nby - 1, (r + 2 * a.R) / a.bsize);
+        const int bx0 = max(0, (c - 2 * a.R) / a.bsize), bx1 = min(a.nbx - 1, (c + 2 * a.R) / a.bsize);
+        int nb = 0, pref = 0;
+        for (int by = by0; by <= by1 && nb < kMaxNb; ++by) {
+            const int s = bstart[by * a.nbx + bx0], e = bstart[by * a.nbx + bx1 + 1];
+            st->nb_start[nb] = s;
+            st->nb_pref[nb] = pref;
+            pref += e - s;
+            ++nb;
+        }
+        st->nb_pref[nb] = pref;
+        st->nb_count = nb;
+        st->best_key = 0ull;
+    }
+}
+
+// incremental: gain_i -= popc(v_i & delta) over the overlap of windows i and w
+__global__ void k_update(SiteArgs a, const SiteState* __restrict__ st, const int4* __restrict__ wins,
+                         const uint64_t* __restrict__ words, const uint64_t* __restrict__ delta0,
+                         const uint64_t* __restrict__ delta1, const int32_t* __restrict__ items,
+                         int32_t* __restrict__ gain, unsigned long long* __restrict__ counters) {
+    if (st->done) return;
+    const int lane = threadIdx.x & 31;
+    const int nb = st->nb_count, total = st->nb_pref[nb];
+    const uint64_t* D = ((st->iter - 1) & 1) ? delta1 : delta0;
+    const int wr0 = st->w_row0, wc0 = st->w_col0, wr1 = wr0 + st->w_h - 1, wc1 = wc0 + st->w_w - 1;
+    unsigned long long bytes = 0;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t f = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; f < total; f += warps) {
+        int k = 0;
+        while (k + 1 < nb && st->nb_pref[k + 1] <= f) ++k;
+        const int i = items[st->nb_start[k] + (f - st->nb_pref[k])];
+        const int4 win = wins[i];
+        const int ra = max(win.x, wr0), rb = min(win.x + win.z - 1, wr1);
+        const int cl = max(win.y, wc0), ch = min(win.y + win.w - 1, wc1);
+        if (ra > rb || cl > ch) continue;
+        const long long s = warp_window_popc<false>(words + (int64_t)i * a.stride, win, D, a.wpr, ra, rb, cl, ch, lane);
+        if (lane == 0) {
+            if (s) gain[i] -= (int32_t)s;
+            bytes += (unsigned long long)(rb - ra + 1) * (((ch >> 6) - (cl >> 6) + 1) * 8);
+        }
+    }
+    if (lane == 0 && bytes) atomicAdd(counters + kSiteBytes, bytes);
+}
+
+// full rescan: gain_i = popc(v_i & ~cum) over window i (also marginal_gains API)
+template <typename G>
+__global__ void k_gain_full(SiteArgs a, const SiteState* st, const int4* __restrict__ wins,
+                            const uint64_t* __restrict__ words, const uint64_t* __restrict__ cum,
+                            G* __restrict__ gain, unsigned long long* __restrict__ counters) {
+    if (st && st->done) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long bytes = 0;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < a.n; i += warps) {
+        const int4 win = wins[i];
+        const long long s = warp_window_popc<true>(words + i * a.stride, win, cum, a.wpr, win.x, win.x + win.z - 1,
+                                                   win.y, win.y + win.w - 1, lane);
+        if (lane == 0) {
+            gain[i] = (G)s;
+            bytes += 8ull * (((unsigned long long)win.z * win.w + 63) >> 6);
+        }
+    }
+    if (counters && lane == 0 && bytes) atomicAdd(counters + kSiteBytes, bytes);
+}
+
+__global__ void k_dense_to_padded(const uint64_t* __restrict__ dense, uint64_t* __restrict__ pad, int64_t nrows,
+                                  int64_t ncols, int64_t wpr) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nrows * wpr; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t y = t / wpr, wi = t - y * wpr;
+        const int64_t off = y * ncols + wi * 64;
+        const int64_t w = off >> 6;
+        const int s = (int)(off & 63);
+        uint64_t v = dense[w] >> s;
+        if (s) v |= dense[w + 1] << (64 - s);
+        const int64_t valid = min((int64_t)64, ncols - wi * 64);
+        if (valid < 64) v &= (1ull << valid) - 1;
+        pad[t] = v;
+    }
+}
+
+__global__ void k_padded_to_dense(const uint64_t* __restrict__ pad, uint64_t* __restrict__ dense, int64_t nrows,
+                                  int64_t ncols, int64_t wpr) {
+    const int64_t total = nrows * ncols, nw = (total + 63) >> 6;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nw; t += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t v = 0;
+        const int64_t b0 = t * 64, b1 = min(b0 + 64, total);
+        int64_t b = b0;
+        while (b < b1) {   // walk the (at most a few) row segments covered by this dense word
+            const int64_t y = b / ncols, x = b - y * ncols;
+            const int64_t len = min(b1 - b, ncols - x);
+            const int64_t pw = x >> 6;
+            const int s = (int)(x & 63);
+            uint64_t seg = pad[y * wpr + pw] >> s;
+            if (s && pw + 1 < wpr) seg |= pad[y * wpr + pw + 1] << (64 - s);
+            if (len < 64) seg &= (1ull << len) - 1;
+            v |= seg << (b - b0);
+            b += len;
+        }
+        dense[t] = v;
+    }
+}
+
+SiteArgs make_args(txs_ctx* c, const txs_params& p) {
+    SiteArgs a;
+    a.nrows = (int)c->nrows; a.ncols = (int)c->ncols; a.R = c->vs_roi;
+    a.bsize = std::max(1, c->vs_roi);
+    a.nbx = (int)((c->ncols + a.bsize - 1) / a.bsize);
+    a.nby = (int)((c->nrows + a.bsize - 1) / a.bsize);
+    a.wpr = (c->ncols + 63) / 64;
+    a.n = c->vs_n;
+    a.stride = c->vs_stride;
+    a.max_sel = p.max_selected;
+    a.target = p.target_coverage;
+    a.total = (double)c->nrows * (double)c->ncols;
+    return a;
+}
+
+txs_status alloc_bitmaps(txs_ctx* c) {
+    c->wpr = (c->ncols + 63) / 64;
+    const size_t bytes = sizeof(uint64_t) * (size_t)(c->nrows * c->wpr + 1);
+    if (bytes > c->bitmap_cap || !c->d_cum) {
+        for (uint64_t** p : {&c->d_cum, &c->d_delta[0], &c->d_delta[1]}) { if (*p) cudaFree(*p); *p = nullptr; }
+        c->bitmap_cap = 0;
+        for (uint64_t** p : {&c->d_cum, &c->d_delta[0], &c->d_delta[1]}) TXS_CUDA(c, "site", cudaMalloc(p, bytes));
+        c->bitmap_cap = bytes;
+    }
+    return TXS_OK;
+}
+
+int blocks_for(int64_t work, int per_block, int cap) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((work + per_block - 1) / per_block, cap));
+}
+
+}  // namespace
+
+txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out, int32_t* stop) {
+    const SiteArgs a = make_args(c, p);
+    const int64_t n = a.n;
+    TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+    if (alloc_bitmaps(c) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
+    if (ensure(c, "site", (void**)&c->d_gain, &c->gain_cap, sizeof(int32_t) * std::max<int64_t>(1, n)) != TXS_OK)
+        return TXS_ERR_OUT_OF_MEMORY;
+    const int64_t nbk = (int64_t)a.nbx * a.nby;
+    if (ensure(c, "site", (void**)&c->d_bucket_start, &c->bucket_cap, sizeof(int32_t) * (nbk + 1) * 2) != TXS_OK ||
+        ensure(c, "site", (void**)&c->d_bucket_items, &c->bucket_items_cap, sizeof(int32_t) * std::max<int64_t>(1, n)) != TXS_OK)
+        return TXS_ERR_OUT_OF_MEMORY;
+    // device step log
+    txs_step* d_steps = nullptr;
+    size_t scan_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int32_t*)nullptr, (int32_t*)nullptr, (int)(nbk + 1));
+    const size_t steps_bytes = sizeof(txs_step) * (size_t)std::max<int64_t>(1, n);
+    if (ensure(c, "site", &c->d_scratch, &c->scratch_cap, steps_bytes + scan_bytes + 256) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
+    d_steps = (txs_step*)c->d_scratch;
+    void* d_scan_tmp = (char*)c->d_scratch + ((steps_bytes + 255) / 256) * 256;
+
+    const size_t bm = sizeof(uint64_t) * (size_t)(c->nrows * c->wpr + 1);
+    TXS_CUDA(c, "site", cudaMemsetAsync(c->d_cum, 0, bm, c->stream));
+    TXS_CUDA(c, "site", cudaMemsetAsync(c->d_delta[0], 0, bm, c->stream));
+    TXS_CUDA(c, "site", cudaMemsetAsync(c->d_delta[1], 0, bm, c->stream));
+    TXS_CUDA(c, "site", cudaMemsetAsync(c->d_state, 0, sizeof(SiteState), c->stream));
+    const int sms = c->num_sms;
+    if (n > 0) {
+        k_init_gains<<<blocks_for(n, 256, sms * 8), 256, 0, c->stream>>>(c->d_pop, c->d_gain, n);
+        TXS_LAUNCHED(c, "site");
+        // CSR buckets over candidate positions
+        int32_t* counts = c->d_bucket_start;          // nbk+1
+        int32_t* cursor = c->d_bucket_start + nbk + 1; // nbk+1
+        TXS_CUDA(c, "site", cudaMemsetAsync(counts, 0, sizeof(int32_t) * (nbk + 1), c->stream));
+        k_bucket_count<<<blocks_for(n, 256, sms * 8), 256, 0, c->stream>>>(c->d_crow, c->d_ccol, n, a.bsize, a.nbx, counts);
+        TXS_LAUNCHED(c, "site");
+        TXS_CUDA(c, "site", cub::DeviceScan::ExclusiveSum(d_scan_tmp, scan_bytes, counts, cursor, (int)(nbk + 1), c->stream));
+        TXS_CUDA(c, "site", cudaMemcpyAsync(counts, cursor, sizeof(int32_t) * (nbk + 1), cudaMemcpyDeviceToDevice, c->stream));
+        k_bucket_fill<<<blocks_for(n, 256, sms * 8), 256, 0, c->stream>>>(c->d_crow, c->d_ccol, n, a.bsize, a.nbx, cursor, c->d_bucket_items);
+        TXS_LAUNCHED(c, "site");
+    }
+    // graph of kRoundsPerGraph rounds
+    const int am_blocks = blocks_for(n, 256 * 4, sms * 2);
+    const int up_blocks = sms * 4;
+    const int full_blocks = blocks_for(n * 32, 256, sms * 16);
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    TXS_CUDA(c, "site", cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    for (int r = 0; r < kRoundsPerGraph; ++r) {
+        if (p.site_mode == 1)
+            k_gain_full<int32_t><<<full_blocks, 256, 0, c->stream>>>(a, c->d_state, c->d_win, c->d_words, c->d_cum, c->d_gain, c->d_counters);
+        k_argmax<<<am_blocks, 256, 0, c->stream>>>(c->d_gain, n, c->d_state);
+        k_commit<<<1, 1024, 0, c->stream>>>(a, c->d_state, c->d_crow, c->d_ccol, c->d_win, c->d_words, c->d_cum,
+                                            c->d_delta[0], c->d_delta[1], c->d_bucket_start, d_steps);
+        if (p.site_mode != 1)
+            k_update<<<up_blocks, 256, 0, c->stream>>>(a, c->d_state, c->d_win, c->d_words, c->d_delta[0], c->d_delta[1],
+                                                       c->d_bucket_items, c->d_gain, c->d_counters);
+    }
+    cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
+    if (ce != cudaSuccess) return cuda_fail(c, "site", ce);
+    ce = cudaGraphInstantiate(&exec, graph, 0);
+    if (ce != cudaSuccess) { cudaGraphDestroy(graph); return cuda_fail(c, "site", ce); }
+    const int per_round = (p.site_mode == 1 ? 3 : 3);
+    txs_status st = TXS_OK;
+    int64_t graphs = 0;
+    for (;;) {
+        ce = cudaGraphLaunch(exec, c->stream);
+        if (ce != cudaSuccess) { st = cuda_fail(c, "site", ce); break; }
+        ++graphs;
+        ce = cudaMemcpyAsync(c->h_state, c->d_state, sizeof(SiteState), cudaMemcpyDeviceToHost, c->stream);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(c->stream);
+        if (ce != cudaSuccess) { st = cuda_fail(c, "site", ce); break; }
+        if (c->h_state->done) break;
+        if (graphs * kRoundsPerGraph > n + 2 * kRoundsPerGraph) { st = fail(c, TXS_ERR_STATE, "site", "loop did not terminate"); break; }
+    }
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    if (st != TXS_OK) return st;
+    c->launches += graphs * kRoundsPerGraph * per_round;
+    c->stats.site_launches += graphs * kRoundsPerGraph * per_round;
+    const int64_t ns = c->h_state->nsel;
+    c->stats.site_iterations += ns;
+    out.resize((size_t)ns);
+    if (ns > 0) {
+        TXS_CUDA(c, "site", cudaMemcpyAsync(out.data(), d_steps, sizeof(txs_step) * ns, cudaMemcpyDeviceToHost, c->stream));
+        TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+    }
+    *stop = c->h_state->stop;
+    return TXS_OK;
+}
+
+txs_status launch_marginal_gains(txs_ctx* c, const uint64_t* d_cum_dense, int64_t* d_gains) {
+    txs_params p{};
+    p.target_coverage = 1.0;
+    const SiteArgs a = make_args(c, p);
+    if (alloc_bitmaps(c) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
+    uint64_t* pad = c->d_delta[0];
+    TXS_CUDA(c, "site", cudaMemsetAsync(pad, 0, c->bitmap_cap, c->stream));
+    k_dense_to_padded<<<blocks_for(c->nrows * c->wpr, 256, c->num_sms * 16), 256, 0, c->stream>>>(d_cum_dense, pad, c->nrows, c->ncols, c->wpr);
+    TXS_LAUNCHED(c, "site");
+    if (a.n > 0) {
+        k_gain_full<int64_t><<<blocks_for(a.n * 32, 256, c->num_sms * 16), 256, 0, c->stream>>>(a, nullptr, c->d_win, c->d_words, pad, d_gains, nullptr);
+        TXS_LAUNCHED(c, "site");
+    }
+    // the delta buffer is scratch here; SITE state is no longer consistent
+    c->site_valid = false;
+    return TXS_OK;
+}
+
+txs_status download_cum(txs_ctx* c, uint64_t* host_dense) {
+    const int64_t nw = (c->nrows * c->ncols + 63) / 64;
+    uint64_t* dense = nullptr;
+    TXS_CUDA(c, "site", cudaMallocAsync((void**)&dense, sizeof(uint64_t) * nw, c->stream));
+    k_padded_to_dense<<<blocks_for(nw, 256, c->num_sms * 16), 256, 0, c->stream>>>(c->d_cum, dense, c->nrows, c->ncols, c->wpr);
+    TXS_LAUNCHED(c, "site");
+    TXS_CUDA(c, "site", cudaMemcpyAsync(host_dense, dense, sizeof(uint64_t) * nw, cudaMemcpyDeviceToHost, c->stream));
+    TXS_CUDA(c, "site", cudaFreeAsync(dense, c->stream));
+    TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+    return TXS_OK;
+}
+
+}  // namespace txs

@@ -1,0 +1,185 @@
+// VIEWSHED stage (compute_viewshed / compute_all_viewsheds)
+// — R2 radial sweep, decision D5.
+//
+// One CTA per observer; thread t walks rays t, t+T, ... of the frozen ray
+// template (raytemplate.cpp), so the 32 lanes of a warp walk 32 neighbouring
+// rays and their terrain reads land in the same few L1 lines.  Along a ray
+// (primitive direction (p,q), u = parameter, crossing row line i at u = i/|p|)
+// each terrain crossing contributes the tangent N/M = (z - E)/u as an exact
+// rational (N = z*|p| - E*|p| with z*|p| the integer interpolation, M = i);
+// the horizon is their running max (compared by cross-multiplication in
+// int64), and an owned cell (a,b) with projection u_c = dot/L2 is visible iff
+//     P * L2 * M_h  >=  N_h * dot        (P = z_cell + h_r - E)
+// i.e. its receiver tangent is >= the horizon of the crossings with u < u_c
+// (">= the running horizon angle", SPEC.md:321 tangent, SPEC.md:324
+// horizon from bare terrain).  Crossings needing an off-grid post end the ray
+// (the in-grid crossings of a ray are a prefix).  Bits: window row-major,
+// LSB-first in u64 words (decision D8), accumulated in shared memory.
+#include "ctx.hpp"
+
+namespace txs {
+namespace {
+
+struct VsArgs {
+    int nrows, ncols, R, ht, hr, nrays;
+    int64_t stride;   // u64 words per viewshed slot
+};
+
+template <bool SMEM_BITS>
+__global__ void k_viewshed(const int16_t* __restrict__ z, const int32_t* __restrict__ crow,
+                           const int32_t* __restrict__ ccol, const int4* __restrict__ rays,
+                           const uint32_t* __restrict__ cells, VsArgs a, uint64_t* __restrict__ words,
+                           int4* __restrict__ wins, int32_t* __restrict__ pops,
+                           unsigned long long* __restrict__ counters) {
+    extern __shared__ __align__(16) uint32_t s_bits[];
+    __shared__ int s_red[32];
+    const int64_t cand = blockIdx.x;
+    const int r = crow[cand], c = ccol[cand];
+    const int row0 = max(0, r - a.R), col0 = max(0, c - a.R);
+    const int h = min(a.nrows - 1, r + a.R) - row0 + 1, w = min(a.ncols - 1, c + a.R) - col0 + 1;
+    const int nbits = h * w, nw64 = (nbits + 63) >> 6;
+    uint64_t* out = words + cand * a.stride;
+    if (SMEM_BITS) {
+        for (int i = threadIdx.x; i < 2 * nw64; i += blockDim.x) s_bits[i] = 0u;
+        __syncthreads();
+    }
+    auto set_bit = [&](int k) {
+        if (SMEM_BITS) atomicOr(&s_bits[k >> 5], 1u << (k & 31));
+        else atomicOr((unsigned long long*)&out[k >> 6], 1ull << (k & 63));
+    };
+    auto Z = [&](int rr, int cc) -> int { return __ldg(z + (int64_t)rr * a.ncols + cc); };
+    const int E = Z(r, c) + a.ht;
+    unsigned long long n_cross = 0, n_cells = 0;
+
+    for (int ray = threadIdx.x; ray < a.nrays; ray += blockDim.x) {
+        const int4 rd = __ldg(rays + ray);
+        const int p = rd.x, q = rd.y, cb = rd.z, cnt = rd.w;
+        const int ap = abs(p), aq = abs(q), sp = p >= 0 ? 1 : -1, sq = q >= 0 ? 1 : -1;
+        const int L2 = p * p + q * q;
+        // row crossing i: column offset i*aq/ap = qr + mr/ap ; column crossing j: row offset qc + mc/aq
+        const int dqr = ap ? aq / ap : 0, dmr = ap ? aq % ap : 0;
+        const int dqc = aq ? ap / aq : 0, dmc = aq ? ap % aq : 0;
+        int i = 1, j = 1, qr = dqr, mr = dmr, qc = dqc, mc = dmc;
+        bool has = false, alive = true;
+        int NH = 0, MH = 1;
+        for (int k = 0; k < cnt; ++k) {
+            const uint32_t cell = __ldg(cells + cb + k);
+            const int ca = (int)(int16_t)(cell & 0xffffu), cbb = (int)(int16_t)(cell >> 16);
+            const int dot = ca * p + cbb * q;
+            while (alive) {
+                bool isrow, iscol;
+                if (ap == 0) { isrow = false; iscol = true; }
+                else if (aq == 0) { isrow = true; iscol = false; }
+                else {
+                    const int cmp = i * aq - j * ap;
+                    isrow = cmp <= 0; iscol = cmp >= 0;
+                }
+                const int idx = isrow ? i : j, n = isrow ? ap : aq;
+                if ((long long)idx * L2 >= (long long)dot * n) break;   // u_k >= u_c
+                int zn;
+                if (isrow && iscol) {   // through a post
+                    const int rr = r + sp * i, cc = c + sq * j;
+                    if (rr < 0 || rr >= a.nrows || cc < 0 || cc >= a.ncols) { alive = false; break; }
+                    zn = Z(rr, cc) * n;
+                } else if (isrow) {
+                    const int rr = r + sp * i, c0 = c + sq * qr;
+                    if (rr < 0 || rr >= a.nrows || c0 < 0 || c0 >= a.ncols) { alive = false; break; }
+                    zn = Z(rr, c0) * (n - mr);
+                    if (mr) {
+                        const int c1 = c0 + sq;
+                        if (c1 < 0 || c1 >= a.ncols) { alive = false; break; }
+                        zn += Z(rr, c1) * mr;
+                    }
+                } else {
+                    const int cc = c + sq * j, r0 = r + sp * qc;
+                    if (cc < 0 || cc >= a.ncols || r0 < 0 || r0 >= a.nrows) { alive = false; break; }
+                    zn = Z(r0, cc) * (n - mc);
+                    if (mc) {
+                        const int r1 = r0 + sp;
+                        if (r1 < 0 || r1 >= a.nrows) { alive = false; break; }
+                        zn += Z(r1, cc) * mc;
+                    }
+                }
+                const int N = zn - E * n;
+                if (!has || (long long)N * MH > (long long)NH * idx) { has = true; NH = N; MH = idx; }
+                ++n_cross;
+                if (isrow) { ++i; qr += dqr; mr += dmr; if (mr >= ap) { mr -= ap; ++qr; } }
+                if (iscol) { ++j; qc += dqc; mc += dmc; if (mc >= aq) { mc -= aq; ++qc; } }
+            }
+            const int rr = r + ca, cc = c + cbb;
+            if (rr < 0 || rr >= a.nrows || cc < 0 || cc >= a.ncols) continue;
+            ++n_cells;
+            const int P = Z(rr, cc) + a.hr - E;
+            if (!has || (long long)P * L2 * MH >= (long long)NH * dot)
+                set_bit((rr - row0) * w + (cc - col0));
+        }
+    }
+    if (threadIdx.x == 0) set_bit((r - row0) * w + (c - col0));
+    __syncthreads();
+    int pc = 0;
+    for (int i = threadIdx.x; i < nw64; i += blockDim.x) {
+        uint64_t v;
+        if (SMEM_BITS) {
+            v = ((uint64_t)s_bits[2 * i + 1] << 32) | s_bits[2 * i];
+            out[i] = v;
+        } else {
+            v = out[i];
+        }
+        pc += __popcll(v);
+    }
+    // block reductions: popcount and counters
+    for (int o = 16; o; o >>= 1) {
+        pc += __shfl_down_sync(0xffffffffu, pc, o);
+        n_cross += __shfl_down_sync(0xffffffffu, n_cross, o);
+        n_cells += __shfl_down_sync(0xffffffffu, n_cells, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_red[threadIdx.x >> 5] = pc;
+        atomicAdd(counters + kVsCross, n_cross);
+        atomicAdd(counters + kVsCells, n_cells);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int k = 0; k < (int)((blockDim.x + 31) >> 5); ++k) t += s_red[k];
+        pops[cand] = t;
+        wins[cand] = make_int4(row0, col0, h, w);
+    }
+}
+
+}  // namespace
+
+txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
+    RayTemplateDev* T = nullptr;
+    txs_status st = get_template(c, p.roi, &T);
+    if (st != TXS_OK) return st;
+    const int64_t n = c->ncand, mw = max_window_words(p.roi);
+    TXS_CUDA(c, "viewshed", cudaStreamSynchronize(c->stream));
+    if (ensure(c, "viewshed", (void**)&c->d_words, &c->words_cap, sizeof(uint64_t) * (n * mw + 8)) != TXS_OK ||
+        ensure(c, "viewshed", (void**)&c->d_win, &c->win_cap, sizeof(int4) * std::max<int64_t>(1, n)) != TXS_OK ||
+        ensure(c, "viewshed", (void**)&c->d_pop, &c->pop_cap, sizeof(int32_t) * std::max<int64_t>(1, n)) != TXS_OK)
+        return fail(c, TXS_ERR_OUT_OF_MEMORY, "viewshed", "cannot hold the packed viewsheds");
+    c->vs_roi = p.roi;
+    c->vs_n = n;
+    c->vs_stride = mw;
+    if (n == 0) return TXS_OK;
+    VsArgs a{(int)c->nrows, (int)c->ncols, p.roi, p.tx_height, p.rx_height, T->nrays, mw};
+    const int per = (T->nrays + 255) / 256;
+    const int threads = ((T->nrays + per - 1) / per + 31) / 32 * 32;
+    const size_t smem = sizeof(uint64_t) * (size_t)mw;
+    if (n > 0x7fffffff) return fail(c, TXS_ERR_RANGE, "viewshed", "too many candidates");
+    if (smem <= 160 * 1024) {
+        if (smem > 48 * 1024)
+            TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(k_viewshed<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_viewshed<true><<<(unsigned)n, threads, smem, c->stream>>>(c->d_z, c->d_crow, c->d_ccol, T->rays, T->cells, a,
+                                                                    c->d_words, c->d_win, c->d_pop, c->d_counters);
+    } else {
+        TXS_CUDA(c, "viewshed", cudaMemsetAsync(c->d_words, 0, sizeof(uint64_t) * n * mw, c->stream));
+        k_viewshed<false><<<(unsigned)n, threads, 0, c->stream>>>(c->d_z, c->d_crow, c->d_ccol, T->rays, T->cells, a,
+                                                                 c->d_words, c->d_win, c->d_pop, c->d_counters);
+    }
+    TXS_LAUNCHED(c, "viewshed");
+    return TXS_OK;
+}
+
+}  // namespace txs

@@ -1,0 +1,292 @@
+"""GPU parity: every stage through the C-ABI against the CPU oracle on the
+same seeded inputs — bit-exact (integer/byte/index work: VixMap bytes,
+candidate lists, packed viewshed words, selection sequence, cumulative bitmap).
+Full BASELINE config-1 size here; larger configs by sampled rows/observers."""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _T():
+    import paper_2006_16783_b200 as T
+    return T
+
+
+@pytest.fixture(scope="module")
+def c1(engine):
+    """BASELINE config 1: 1000x1000, roughness 0.5, 0..4000 m."""
+    z = O.generate_fractal(1000, 1000, 0.5, 1, 0, 4000)
+    return z
+
+
+# ---- terrain -------------------------------------------------------------------
+@pytest.mark.parametrize("nr,nc,rough,seed,zmin,zmax", [
+    (1000, 1000, 0.5, 1, 0, 4000), (257, 300, 0.6, 9, -100, 3000), (2, 2, 1.0, 3, 0, 10),
+    (4096, 4096, 0.6, 2, 0, 3000), (33, 1025, 0.5, 4, 0, 4000)])
+def test_generator_bit_exact(engine, nr, nc, rough, seed, zmin, zmax):
+    engine.generate_fractal(nr, nc, rough, seed, zmin, zmax)
+    assert np.array_equal(engine.terrain(), O.generate_fractal(nr, nc, rough, seed, zmin, zmax))
+
+
+def test_fill_rows_and_set_terrain(engine):
+    z = O.generate_fractal(300, 200, 0.5, 5, 0, 4000)
+    engine.set_terrain(z)
+    assert np.array_equal(engine.terrain(), z)
+    engine.fill_rows(0, 37, 0)
+    z2 = z.copy(); z2[:37] = 0
+    assert np.array_equal(engine.terrain(), z2)
+    bad = z.copy(); bad[5, 5] = -32768
+    with pytest.raises(_T().TxsError) as e:
+        engine.set_terrain(bad)
+    assert e.value.status == "NODATA"
+
+
+# ---- los -----------------------------------------------------------------------
+def test_is_visible_batch_bit_exact(engine):
+    rng = np.random.default_rng(11)
+    for seed, (nr, nc) in [(1, (200, 200)), (2, (64, 700)), (3, (1000, 1000))]:
+        z = O.generate_fractal(nr, nc, 0.6, seed, 0, 4000)
+        engine.set_terrain(z)
+        pairs = np.stack([rng.integers(0, nr, 20000), rng.integers(0, nc, 20000),
+                          rng.integers(0, nr, 20000), rng.integers(0, nc, 20000)], 1).astype(np.int32)
+        pairs[:50, 2:] = pairs[:50, :2]                       # zero-length
+        pairs[50:100, 2] = pairs[50:100, 0]                   # axis aligned
+        for ht, hr in [(10, 10), (0, 0), (50, 3)]:
+            assert np.array_equal(engine.is_visible_batch(pairs, ht, hr), O.is_visible_batch(z, pairs, ht, hr))
+    with pytest.raises(_T().TxsError) as e:
+        engine.is_visible_batch(np.array([[0, 0, 5000, 0]], np.int32), 1, 1)
+    assert e.value.status == "OFF_GRID"
+
+
+def test_is_visible_ridge_and_graze(engine):
+    z = np.zeros((3, 5), np.int16)
+    z[1] = [0, 0, 50, 0, 0]
+    engine.set_terrain(z)
+    assert list(engine.is_visible_batch([[1, 0, 1, 4]], 1, 1)) == [0]
+    z[1] = [0, 0, 1, 0, 0]
+    engine.set_terrain(z)
+    assert list(engine.is_visible_batch([[1, 0, 1, 4]], 1, 1)) == [1]
+
+
+# ---- vix -----------------------------------------------------------------------
+def test_vix_c1_bit_exact(engine, c1):
+    """Config 1 in full: 1000x1000, roi 100, h 10, 10 samples (shared-memory tile path)."""
+    T = _T()
+    engine.set_terrain(c1)
+    p = T.make_params(100, 10, 10, samples=10, seed=12345)
+    g = engine.estimate_vix(p)
+    o = O.estimate_vix(c1, 100, 10, 10, 10, 12345)
+    assert np.array_equal(g, o), int((g != o).sum())
+    st = engine.stats()
+    assert st["vix_los"] >= 1000 * 1000 * 10
+
+
+@pytest.mark.parametrize("roi,samples,ht,hr", [(7, 20, 0, 0), (150, 10, 20, 20), (200, 20, 20, 20)])
+def test_vix_rows_bit_exact(engine, roi, samples, ht, hr):
+    """Global-memory path (roi >= 150) and small-roi smem path on sampled rows."""
+    T = _T()
+    z = O.generate_fractal(1200, 900, 0.6, 8, 0, 3000)
+    engine.set_terrain(z)
+    g = engine.estimate_vix(T.make_params(roi, ht, hr, samples=samples, seed=77))
+    for rb, re in [(0, 24), (590, 610), (1176, 1200)]:
+        o = O.estimate_vix(z, roi, ht, hr, samples, 77, rows=(rb, re))
+        assert np.array_equal(g[rb:re], o[rb:re]), (rb, int((g[rb:re] != o[rb:re]).sum()))
+
+
+def test_vix_flat_and_tiny(engine):
+    T = _T()
+    engine.set_terrain(np.full((70, 45), 3, np.int16))
+    assert (engine.estimate_vix(T.make_params(30, 10, 10, samples=13)) == 13).all()
+    z = O.generate_fractal(5, 3, 0.5, 1, 0, 100)
+    engine.set_terrain(z)
+    assert np.array_equal(engine.estimate_vix(T.make_params(40, 1, 2, samples=7, seed=5)),
+                          O.estimate_vix(z, 40, 1, 2, 7, 5))
+
+
+# ---- findmax -------------------------------------------------------------------
+@pytest.mark.parametrize("nr,nc,bw,k,levels", [(1000, 1000, 100, 10, 11), (1000, 1000, 128, 16, 21),
+                                               (300, 257, 40, 2000, 3), (96, 96, 7, 5, 1), (128, 128, 64, 32, 256)])
+def test_findmax_bit_exact(engine, nr, nc, bw, k, levels):
+    T = _T()
+    rng = np.random.default_rng(nr + bw)
+    s = rng.integers(0, levels, (nr, nc)).astype(np.uint8)
+    engine.set_terrain(np.zeros((nr, nc), np.int16))
+    engine.set_vix(s)
+    rows, cols, sc = engine.find_candidates(T.make_params(max(3, bw), per_block=k, block_width=bw))
+    orow, ocol, osc = O.find_candidates(s, bw, k)
+    assert np.array_equal(rows, orow) and np.array_equal(cols, ocol) and np.array_equal(sc, osc)
+
+
+def test_random_observers_bit_exact(engine):
+    engine.set_terrain(np.zeros((16384, 16384 // 64), np.int16))
+    engine.random_observers(100000, 424242)
+    r, c, _ = engine.candidates()
+    orow, ocol = O.random_observers(16384, 16384 // 64, 100000, 424242)
+    assert np.array_equal(r, orow) and np.array_equal(c, ocol)
+
+
+# ---- viewshed ----------------------------------------------------------------------
+def _vs_compare(engine, z, roi, ht, hr, rows, cols):
+    T = _T()
+    engine.set_terrain(z)
+    engine.set_candidates(rows, cols)
+    engine.compute_all_viewsheds(T.make_params(roi, ht, hr))
+    gw, gv, gp = engine.viewsheds(roi)
+    ow, ov = O.viewsheds(z, roi, ht, hr, rows, cols)
+    assert np.array_equal(gw, ow)
+    bad = np.nonzero((gv != ov).any(1))[0]
+    assert len(bad) == 0, f"{len(bad)} viewsheds differ, first {bad[:5]}"
+    pops = np.unpackbits(ov.view(np.uint8), axis=1).sum(1)
+    assert np.array_equal(gp, pops)
+
+
+def test_viewsheds_c1_bit_exact(engine, c1):
+    """Config-1 observers (a FINDMAX candidate list) at roi 100."""
+    T = _T()
+    engine.set_terrain(c1)
+    p = T.make_params(100, 10, 10, samples=10, per_block=10, block_width=100, seed=1)
+    engine.estimate_vix(p, copy=False)
+    rows, cols, _ = engine.find_candidates(p)
+    assert len(rows) == 1000
+    _vs_compare(engine, c1, 100, 10, 10, rows, cols)
+
+
+@pytest.mark.parametrize("roi,h", [(200, 20), (250, 50), (1, 0), (3, 5)])
+def test_viewsheds_sampled_bit_exact(engine, roi, h):
+    z = O.generate_fractal(1100, 1300, 0.5, 31, 0, 4000)
+    rng = np.random.default_rng(roi)
+    rows = np.concatenate([rng.integers(0, 1100, 120), [0, 1099, 0, 1099, 550]]).astype(np.int32)
+    cols = np.concatenate([rng.integers(0, 1300, 120), [0, 1299, 1299, 0, 3]]).astype(np.int32)
+    _vs_compare(engine, z, roi, h, h, rows, cols)
+
+
+def test_viewshed_flat_disk_and_small_grid(engine):
+    T = _T()
+    z = np.full((100, 100), 100, np.int16)
+    engine.set_terrain(z)
+    engine.set_candidates([50], [50])
+    engine.compute_all_viewsheds(T.make_params(30, 10, 10))
+    _, _, pops = engine.viewsheds(30)
+    assert pops[0] == 2821
+    small = O.generate_fractal(9, 14, 0.7, 2, 0, 500)
+    _vs_compare(engine, small, 40, 3, 3, [0, 8, 4, 4], [0, 13, 7, 7])
+
+
+# ---- site ------------------------------------------------------------------------
+def _site_compare(engine, roi, rows, cols, nr, nc, target, max_sel, mode):
+    T = _T()
+    wins, words, _ = engine.viewsheds(roi)
+    g = engine.site(T.make_params(roi, target=target, max_selected=max_sel, site_mode=mode))
+    o = O.site(rows, cols, wins, words, nr, nc, target, max_sel)
+    assert g["stop"] == o["stop"]
+    assert np.array_equal(g["index"], o["index"]), (g["index"][:10], o["index"][:10])
+    assert np.array_equal(g["gain"], o["gain"]) and np.array_equal(g["coverage"], o["coverage"])
+    assert np.array_equal(g["row"], o["row"]) and np.array_equal(g["col"], o["col"])
+    assert np.array_equal(engine.cumulative(), o["cum"])
+    return g
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_site_c1_bit_exact(engine, c1, mode):
+    """Config 1: until 95% or 200 observers; both device strategies."""
+    T = _T()
+    engine.set_terrain(c1)
+    p = T.make_params(100, 10, 10, samples=10, per_block=10, block_width=100, seed=1)
+    engine.estimate_vix(p, copy=False)
+    rows, cols, _ = engine.find_candidates(p)
+    engine.compute_all_viewsheds(p)
+    _site_compare(engine, 100, rows, cols, 1000, 1000, 0.95, 200, mode)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_site_random_dense_bit_exact(engine, mode):
+    """Many overlapping candidates, run to exhaustion/zero gain (target 1.0)."""
+    T = _T()
+    z = O.generate_fractal(300, 420, 0.6, 17, 0, 4000)
+    rng = np.random.default_rng(3 + mode)
+    rows, cols = rng.integers(0, 300, 700).astype(np.int32), rng.integers(0, 420, 700).astype(np.int32)
+    rows[5], cols[5] = rows[4], cols[4]                     # a duplicate (zero second gain)
+    engine.set_terrain(z)
+    engine.set_candidates(rows, cols)
+    engine.compute_all_viewsheds(T.make_params(25, 10, 10))
+    g = _site_compare(engine, 25, rows, cols, 300, 420, 1.0, 0, mode)
+    assert (np.diff(g["gain"]) <= 0).all()
+
+
+def test_site_edge_cases(engine):
+    T = _T()
+    z = O.generate_fractal(64, 64, 0.5, 2, 0, 4000)
+    engine.set_terrain(z)
+    engine.set_candidates([], [])
+    engine.compute_all_viewsheds(T.make_params(10))
+    g = engine.site(T.make_params(10, target=0.5))
+    assert g["stop"] == "exhausted" and len(g["index"]) == 0
+    engine.set_candidates([10, 10, 40], [10, 10, 40])
+    engine.compute_all_viewsheds(T.make_params(10))
+    g = _site_compare(engine, 10, np.array([10, 10, 40]), np.array([10, 10, 40]), 64, 64, 1.0, 0, 0)
+    assert g["stop"] == "zero-gain"
+    g = _site_compare(engine, 10, np.array([10, 10, 40]), np.array([10, 10, 40]), 64, 64, 1.0, 1, 0)
+    assert g["stop"] == "max-selected"
+
+
+def test_marginal_gains_vs_oracle(engine):
+    T = _T()
+    z = O.generate_fractal(200, 333, 0.5, 6, 0, 4000)
+    rng = np.random.default_rng(1)
+    rows, cols = rng.integers(0, 200, 300).astype(np.int32), rng.integers(0, 333, 300).astype(np.int32)
+    engine.set_terrain(z)
+    engine.set_candidates(rows, cols)
+    engine.compute_all_viewsheds(T.make_params(30, 10, 10))
+    wins, words, _ = engine.viewsheds(30)
+    for density in (0.0, 0.3, 0.9):
+        cum = O.pack_dense(rng.random((200, 333)) < density)
+        gains = engine.marginal_gains(cum)
+        exp = [O.marginal_gain(wins[i], words[i], cum, 200, 333) for i in range(300)]
+        assert list(gains) == exp
+
+
+def test_set_viewsheds_then_site(engine):
+    """SITE on injected (oracle) viewsheds, the drop-in path for a caller that
+    already holds packed viewsheds."""
+    T = _T()
+    z = O.generate_fractal(256, 256, 0.5, 12, 0, 4000)
+    rng = np.random.default_rng(9)
+    rows, cols = rng.integers(0, 256, 400).astype(np.int32), rng.integers(0, 256, 400).astype(np.int32)
+    ow, ov = O.viewsheds(z, 20, 10, 10, rows, cols)
+    engine.set_terrain(z)
+    engine.set_viewsheds(20, rows, cols, ow, ov)
+    g = engine.site(T.make_params(20, target=0.9))
+    o = O.site(rows, cols, ow, ov, 256, 256, 0.9)
+    assert np.array_equal(g["index"], o["index"]) and g["stop"] == o["stop"]
+    assert np.array_equal(engine.cumulative(), o["cum"])
+
+
+# ---- pipeline ---------------------------------------------------------------------
+def test_run_pipeline_c1_matches_oracle(engine, c1):
+    """run_pipeline on config 1 end to end vs the oracle stages."""
+    T = _T()
+    engine.set_terrain(c1)
+    p = T.make_params(100, 10, 10, samples=10, per_block=10, block_width=100, target=0.95,
+                      max_selected=200, seed=2024)
+    res = engine.run_pipeline(p)
+    s = O.estimate_vix(c1, 100, 10, 10, 10, 2024)
+    rows, cols, _ = O.find_candidates(s, 100, 10)
+    ow, ov = O.viewsheds(c1, 100, 10, 10, rows, cols)
+    o = O.site(rows, cols, ow, ov, 1000, 1000, 0.95, 200)
+    assert np.array_equal(res["index"], o["index"]) and res["stop"] == o["stop"]
+    assert np.array_equal(engine.cumulative(), o["cum"])
+    assert set(res["stage_ms"]) == {"vix", "findmax", "viewshed", "site"}
+
+
+def test_errors_are_stage_tagged(engine):
+    T = _T()
+    engine.set_terrain(np.zeros((10, 10), np.int16))
+    with pytest.raises(T.TxsError) as e:
+        engine.estimate_vix(T.make_params(0))
+    assert e.value.status == "INVALID_ARGUMENT" and "[vix]" in str(e.value)
+    with pytest.raises(T.TxsError) as e:
+        engine.set_candidates([11], [0])
+    assert e.value.status == "OFF_GRID"

@@ -1,0 +1,378 @@
+"""SPEC.md examples and acceptance criteria re-encoded as
+tests of the CPU oracle — the semantics the GPU is held bit-exact to."""
+import time
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+
+
+def popcount(words):
+    return int(np.unpackbits(np.ascontiguousarray(words, np.uint64).view(np.uint8)).sum())
+
+
+# ---- terrain --------------------------------------------------
+def test_elevation_between_examples():
+    assert O.elevation_between(10, 20, 1, 2) == 15
+    assert O.elevation_between(10, 20, 0, 5) == 10
+    assert O.elevation_between(6387, 16344, 1, 4) == 8876.25
+
+
+def test_generator_properties():
+    a = O.generate_fractal(257, 300, 0.5, 1, 0, 4000)
+    b = O.generate_fractal(257, 300, 0.5, 1, 0, 4000)
+    c = O.generate_fractal(257, 300, 0.5, 2, 0, 4000)
+    assert np.array_equal(a, b)                   # SPEC.md:68 determinism
+    assert not np.array_equal(a, c)
+    assert a.min() >= 0 and a.max() <= 4000
+    flat = O.generate_fractal(200, 200, 0.001, 3, 0, 4000)
+    assert int(flat.max()) - int(flat.min()) < 0.05 * 4000
+    assert np.array_equal(O.generate_fractal(33, 17, 0.6, 5, -100, 3000, threads=1),
+                          O.generate_fractal(33, 17, 0.6, 5, -100, 3000, threads=7))
+    with pytest.raises(ValueError):
+        O.generate_fractal(10, 10, 0.5, 1, 10, 5)  # SPEC.md:65 zmin > zmax
+
+
+# ---- los ------------------------------------------------------
+def test_los_examples():
+    flat = np.full((20, 20), 100, np.int16)
+    for (a, b, c, d) in [(0, 0, 19, 19), (3, 17, 12, 1), (5, 5, 5, 5), (0, 0, 0, 19)]:
+        assert O.is_visible(flat, a, b, 10, c, d, 10)
+    ridge = np.zeros((3, 5), np.int16)
+    ridge[1] = [0, 0, 50, 0, 0]
+    assert not O.is_visible(ridge, 1, 0, 1, 1, 4, 1)
+    graze = np.zeros((3, 5), np.int16)
+    graze[1] = [0, 0, 1, 0, 0]
+    assert O.is_visible(graze, 1, 0, 1, 1, 4, 1)               # SPEC.md:126 touching is visible
+    graze[1, 2] = 2
+    assert not O.is_visible(graze, 1, 0, 1, 1, 4, 1)
+
+
+def _dense_profile_blocked(z, a, b, c, d, ht, hr):
+    """Independent fp64 brute force: the terrain profile along the segment is
+    the grid-line interpolation of SPEC.md:71-74 (linear between adjacent
+    posts on every row/column line the segment crosses, linear along the
+    segment in between); sample it at 10x the crossing density (plus the
+    crossings themselves) and compare with the LOS.  Returns (blocked, margin)."""
+    zf = z.astype(np.float64)
+    nr, nc = abs(c - a), abs(d - b)
+    ts, zs = [0.0, 1.0], [zf[a, b], zf[c, d]]
+    for i in range(1, nr):
+        t = i / nr
+        col = b + t * (d - b)
+        c0 = int(np.floor(col)); f = col - c0
+        r = a + (i if c > a else -i)
+        ts.append(t); zs.append(zf[r, c0] * (1 - f) + (zf[r, c0 + 1] * f if f > 0 else 0.0))
+    for j in range(1, nc):
+        t = j / nc
+        row = a + t * (c - a)
+        r0 = int(np.floor(row)); f = row - r0
+        cc = b + (j if d > b else -j)
+        ts.append(t); zs.append(zf[r0, cc] * (1 - f) + (zf[r0 + 1, cc] * f if f > 0 else 0.0))
+    order = np.argsort(ts, kind="stable")
+    ts, zs = np.array(ts)[order], np.array(zs)[order]
+    n = 10 * (nr + nc) + 1
+    s = np.unique(np.concatenate([np.linspace(0, 1, n + 1), ts]))
+    s = s[(s > 0) & (s < 1)]
+    if len(s) == 0:
+        return False, np.inf
+    terr = np.interp(s, ts, zs)
+    e0, e1 = zf[a, b] + ht, zf[c, d] + hr
+    margin = terr - (e0 + s * (e1 - e0))
+    return bool(np.any(margin > 0)), float(np.min(np.abs(margin)))
+
+
+def test_los_parametric_oracle_agreement():
+    """>= 99.9% agreement with dense parametric sampling (10x
+    the crossing density) over 10,000 pairs on 10 random 100x100 terrains;
+    every disagreement is a grazing tie within interpolation round-off."""
+    rng = np.random.default_rng(5)
+    agree = total = 0
+    for t in range(10):
+        z = O.generate_fractal(100, 100, 0.5, 100 + t, 0, 4000)
+        pairs = rng.integers(0, 100, size=(1000, 4)).astype(np.int32)
+        vis = O.is_visible_batch(z, pairs, 10, 10)
+        for (a, b, c, d), v in zip(pairs, vis):
+            blocked, margin = _dense_profile_blocked(z, int(a), int(b), int(c), int(d), 10, 10)
+            ok = blocked != bool(v)
+            if not ok:
+                assert margin < 1e-6, (a, b, c, d, margin)   # grazing tie only
+            agree += int(ok)
+            total += 1
+    assert agree / total >= 0.999, agree / total
+
+
+def test_los_symmetry_and_monotonicity():
+    z = O.generate_fractal(64, 64, 0.6, 11, 0, 4000)
+    rng = np.random.default_rng(2)
+    for a, b, c, d in rng.integers(0, 64, size=(400, 4)):
+        v = O.is_visible(z, a, b, 10, c, d, 10)
+        assert v == O.is_visible(z, c, d, 10, a, b, 10)
+        if v:
+            assert O.is_visible(z, a, b, 25, c, d, 10)
+            assert O.is_visible(z, a, b, 10, c, d, 25)
+
+
+# ---- vix ------------------------------------------------------
+def test_vix_flat_is_full():
+    z = np.full((60, 50), 7, np.int16)
+    s = O.estimate_vix(z, 12, 10, 10, 10, 3)
+    assert (s == 10).all()
+
+
+def _replay_draws(seed, r, c, roi, S, nrows, ncols):
+    """D6 draw order replayed in Python from the oracle's splitmix."""
+    st = int(O.lib().txo_mix_seed(seed, r, c))
+    out = []
+    draws = O.splitmix(st, 4000, 1, 2 * roi + 1)
+    k = 0
+    while len(out) < S:
+        dr, dc = int(draws[k]) - roi, int(draws[k + 1]) - roi
+        k += 2
+        if dr * dr + dc * dc <= roi * roi and 0 <= r + dr < nrows and 0 <= c + dc < ncols:
+            out.append((dr, dc))
+    return out
+
+
+def test_vix_pit_exact():
+    """a post in a pit (ring of 10000 at distance 1) sees only the
+    receivers inside the rim; the sampled score equals the replayed count."""
+    z = np.zeros((41, 41), np.int16)
+    z[19:22, 19:22] = 10000
+    z[20, 20] = 0
+    s = O.estimate_vix(z, 8, 10, 10, 20, 77)
+    vis_set = {(dr, dc) for dr in range(-8, 9) for dc in range(-8, 9)
+               if dr * dr + dc * dc <= 64 and O.is_visible(z, 20, 20, 10, 20 + dr, 20 + dc, 10)}
+    assert vis_set == {(a, b) for a in (-1, 0, 1) for b in (-1, 0, 1)}
+    samples = _replay_draws(77, 20, 20, 8, 20, 41, 41)
+    assert s[20, 20] == sum((d in vis_set) for d in samples)
+
+
+def test_vix_replayed_scores_and_threads():
+    z = O.generate_fractal(48, 40, 0.5, 9, 0, 4000)
+    s1 = O.estimate_vix(z, 15, 10, 10, 10, 5, threads=1)
+    s8 = O.estimate_vix(z, 15, 10, 10, 10, 5, threads=8)
+    assert np.array_equal(s1, s8)
+    rng = np.random.default_rng(0)
+    for r, c in rng.integers(0, 40, size=(12, 2)):
+        samples = _replay_draws(5, r, c, 15, 10, 48, 40)
+        assert all(dr * dr + dc * dc <= 225 for dr, dc in samples)
+        exp = sum(O.is_visible(z, r, c, 10, r + dr, c + dc, 10) for dr, dc in samples)
+        assert s1[r, c] == exp
+
+
+def test_vix_statistical_consistency():
+    """SPEC.md:189 on a small grid: mean sampled index over 100 seeds within
+    the standard-error bound of the exhaustive fraction."""
+    z = O.generate_fractal(33, 33, 0.6, 4, 0, 4000)
+    r = c = 16
+    roi = 10
+    cells = [(a, b) for a in range(-roi, roi + 1) for b in range(-roi, roi + 1) if a * a + b * b <= roi * roi]
+    f = np.mean([O.is_visible(z, r, c, 10, r + a, c + b, 10) for a, b in cells])
+    S = 10
+    means = [O.estimate_vix(z, roi, 10, 10, S, seed, rows=(r, r + 1))[r, c] / S for seed in range(100)]
+    assert abs(np.mean(means) - f) <= 3 * np.sqrt(f * (1 - f) / S) / 10 + 1e-12
+
+
+def test_vix_exact_vs_fp64_reference_formula(kat):
+    """DESIGN.md §2 D2: the exact predicate vs SPEC.md:147's fp64 formula built on
+    the reference walk_crossings (golden scores from tests/golden/make_golden.py).
+    Differing LOS decisions are counted; every one must be an exact grazing tie
+    (terrain exactly ON the LOS at a crossing), which SPEC.md:126,144 rule
+    visible and fp64 rounding resolves either way."""
+    g = kat["vix_fp64"]
+    z = O.generate_fractal(96, 96, 0.5, 7, 0, 4000)
+    R, S = g["roi"], g["samples"]
+    exact = O.estimate_vix(z, R, g["ht"], g["hr"], S, g["seed"])
+    fp = np.array(g["scores"], np.uint8).reshape(96, 96)
+    diff_posts = np.argwhere(exact != fp)
+    ndiff = int(np.abs(exact.astype(int) - fp.astype(int)).sum())
+    ties_total = 0
+    for r, c in diff_posts:
+        samples = _replay_draws(g["seed"], int(r), int(c), R, S, 96, 96)
+        cls = [O.los_class(z, int(r), int(c), g["ht"], int(r) + dr, int(c) + dc, g["hr"]) for dr, dc in samples]
+        ties = sum(1 for k in cls if k == 0)
+        ties_total += ties
+        assert exact[r, c] >= fp[r, c]                 # fp64 only ever loses visible ties
+        assert exact[r, c] - fp[r, c] <= ties
+    decisions = 96 * 96 * S
+    print(f"exact-vs-fp64: {ndiff} differing LOS decisions of {decisions} "
+          f"({ndiff / decisions:.2e}); all are exact grazing ties")
+
+
+# ---- candidates -----------------------------------------------
+@pytest.mark.parametrize("n,roi,k,blocks,total", [
+    (1000, 30, 20, 100, 200000), (32000, 1000, 20, 96, 184320),
+    (46400, 1000, 20, 139, 386420), (46400, 2000, 20, 70, 98000)])
+def test_partition_paper_tables(n, roi, k, blocks, total):
+    bw = -(-roi // 3)
+    assert -(-n // bw) == blocks
+    last = n - (blocks - 1) * bw
+    cnt = ((blocks - 1) * min(k, bw * bw) + min(k, bw * last)) * (blocks - 1) + \
+          (blocks - 1) * min(k, last * bw) + min(k, last * last)
+    assert cnt == total
+
+
+def test_find_candidates_order_and_counts():
+    scores = np.random.default_rng(3).integers(0, 11, size=(95, 103)).astype(np.uint8)
+    rows, cols, sc = O.find_candidates(scores, 10, 7)
+    assert len(rows) == 10 * 11 * 7
+    by, bx = rows // 10, cols // 10
+    blk = by * 11 + bx
+    assert (np.diff(blk) >= 0).all()                          # block order
+    for b in np.unique(blk):
+        m = blk == b
+        key = list(zip(-sc[m], rows[m], cols[m]))
+        assert key == sorted(key)                             # score desc, (row,col) asc
+        y, x = divmod(int(b), 11)
+        block = scores[y * 10:(y + 1) * 10, x * 10:(x + 1) * 10]
+        assert sc[m].min() >= np.sort(block.ravel())[::-1][6]
+    uni = np.full((20, 20), 5, np.uint8)
+    r, c, s = O.find_candidates(uni, 20, 3)
+    assert list(zip(r, c)) == [(0, 0), (0, 1), (0, 2)]
+
+
+# ---- viewshed ------------------------------------------------
+def test_flat_disk_2821_and_coverage():
+    z = np.full((100, 100), 100, np.int16)
+    wins, words = O.viewsheds(z, 30, 10, 10, [50], [50])
+    assert popcount(words[0]) == 2821
+    res = O.site([50], [50], wins, words, 100, 100, 1.0)
+    assert res["coverage"][-1] == 0.2821
+
+
+def test_midpoint_circle_and_disk_counts():
+    assert [O.lib().txo_midpoint_circle_count(r) for r in (30, 100, 250)] == [168, 564, 1416]
+    for R in (5, 30, 100, 250):
+        p, q, cb, ca, cc = O.ray_template(R)
+        disk = sum(1 for a in range(-R, R + 1) for b in range(-R, R + 1) if a * a + b * b <= R * R)
+        assert len(ca) == disk - 1                              # every disk cell owned once
+        assert len(set(zip(ca.tolist(), cc.tolist()))) == disk - 1
+
+
+def test_viewshed_corner_and_edges():
+    z = O.generate_fractal(50, 60, 0.5, 3, 0, 4000)
+    wins, words = O.viewsheds(z, 12, 10, 10, [0, 49, 0, 49, 25], [0, 59, 59, 0, 30])
+    for (r0, c0, h, w), ws, (r, c) in zip(wins, words, [(0, 0), (49, 59), (0, 59), (49, 0), (25, 30)]):
+        assert r0 == max(0, r - 12) and c0 == max(0, c - 12)   # SPEC.md:293 clipping
+        bits = O.unpack_window((r0, c0, h, w), ws)
+        assert bits[r - r0, c - c0] == 1
+        yy, xx = np.nonzero(bits)
+        assert (((yy + r0 - r) ** 2 + (xx + c0 - c) ** 2) <= 144).all()
+        nw = (h * w + 63) // 64
+        tail = np.unpackbits(ws[:nw].view(np.uint8), bitorder="little")[h * w:]
+        assert not tail.any() and not ws[nw:].any()             # SPEC.md:298 zero padding
+
+
+def _r2_r3(seed_set, n=50):
+    rng = np.random.default_rng(seed_set)
+    tot = agree = pr_tot = pr_bad = 0
+    for inst in range(n):
+        z = O.generate_fractal(100, 100, 0.5, seed_set * 1000 + inst + 1, 0, 4000)
+        R = int(rng.integers(5, 21))
+        r, c = (int(x) for x in rng.integers(0, 100, 2))
+        wins, words = O.viewsheds(z, R, 10, 10, [r], [c])
+        bits = O.unpack_window(wins[0], words[0])
+        a, b = np.mgrid[-R:R + 1, -R:R + 1]
+        m = (a * a + b * b <= R * R) & (r + a >= 0) & (r + a < 100) & (c + b >= 0) & (c + b < 100)
+        a, b = a[m], b[m]
+        pairs = np.stack([np.full_like(a, r), np.full_like(a, c), r + a, c + b], 1)
+        r3 = O.is_visible_batch(z, pairs, 10, 10)
+        r2 = bits[r + a - wins[0][0], c + b - wins[0][1]]
+        agree += int((r2 == r3).sum())
+        tot += len(a)
+        pr = (a == 0) | (b == 0) | (np.abs(a) == np.abs(b))
+        pr_tot += int(pr.sum())
+        pr_bad += int((r2[pr] != r3[pr]).sum())
+    return agree / tot, pr_bad, pr_tot
+
+
+def test_r2_vs_r3_agreement():
+    """>= 97% per-cell agreement with per-cell is_visible over
+    50 random instances with roi <= 20, 100% on the 8 principal rays."""
+    frac, bad, n = _r2_r3(0)
+    print(f"R2/R3 agreement {frac:.4f}; principal-ray disagreements {bad}/{n}")
+    assert frac >= 0.97 and bad == 0
+
+
+def test_viewshed_height_monotone_and_duplicates():
+    z = O.generate_fractal(80, 80, 0.6, 21, 0, 4000)
+    rows, cols = [40, 10, 40], [40, 70, 40]
+    w1, v1 = O.viewsheds(z, 20, 10, 10, rows, cols)
+    w2, v2 = O.viewsheds(z, 20, 30, 10, rows, cols)
+    assert ((v1 & ~v2) == 0).all()
+    assert np.array_equal(v1[0], v1[2])
+    w8, v8 = O.viewsheds(z, 20, 10, 10, rows, cols, threads=8)
+    assert np.array_equal(v1, v8) and np.array_equal(w1, w8)
+
+
+def test_viewshed_cost_scaling():
+    """doubling roi costs at most ~4.5x on flat terrain."""
+    z = np.full((700, 700), 10, np.int16)
+    rows, cols = [350] * 40, [350] * 40
+    O.viewsheds(z, 60, 10, 10, rows[:1], cols[:1], threads=1)
+    O.viewsheds(z, 120, 10, 10, rows[:1], cols[:1], threads=1)
+    t0 = time.perf_counter(); O.viewsheds(z, 60, 10, 10, rows, cols, threads=1); t1 = time.perf_counter()
+    O.viewsheds(z, 120, 10, 10, rows, cols, threads=1); t2 = time.perf_counter()
+    assert (t2 - t1) / (t1 - t0) <= 4.5 * 1.25
+
+
+# ---- siting -----------------------------------------------------
+def test_site_disjoint_and_identical():
+    nr = nc = 40
+    w1 = np.zeros((10, 10), np.uint8); w1[:, :] = 1          # area 100
+    w2 = np.zeros((6, 10), np.uint8); w2[:, :] = 1           # area 60
+    words = np.zeros((2, 4), np.uint64)
+    words[0, :2] = O.pack_dense(w1)[:2]
+    words[1, :1] = O.pack_dense(w2)[:1]
+    wins = np.array([[0, 0, 10, 10], [20, 20, 6, 10]], np.int32)
+    res = O.site([5, 23], [5, 25], wins, np.ascontiguousarray(words), nr, nc, 1.0)
+    assert list(res["index"]) == [0, 1] and list(res["gain"]) == [100, 60]
+    assert res["coverage"][-1] == 160 / 1600
+    wins2 = np.array([[0, 0, 10, 10], [0, 0, 10, 10]], np.int32)
+    words2 = np.stack([words[0], words[0]])
+    res = O.site([5, 5], [5, 5], wins2, words2, nr, nc, 1.0)
+    assert list(res["gain"]) == [100] and res["stop"] == "zero-gain"
+    res = O.site([], [], np.zeros((0, 4), np.int32), np.zeros((0, 4), np.uint64), nr, nc, 0.5)
+    assert res["stop"] == "exhausted" and len(res["index"]) == 0
+
+
+@pytest.mark.slow
+def test_lazy_equals_naive():
+    """20 instances of 500 candidates over 200x200."""
+    rng = np.random.default_rng(8)
+    for inst in range(20):
+        z = O.generate_fractal(200, 200, 0.5, 500 + inst, 0, 4000)
+        rows, cols = rng.integers(0, 200, 500), rng.integers(0, 200, 500)
+        wins, words = O.viewsheds(z, 15, 10, 10, rows, cols)
+        lazy = O.site(rows, cols, wins, words, 200, 200, 0.99)
+        naive = O.site(rows, cols, wins, words, 200, 200, 0.99, naive=True)
+        assert np.array_equal(lazy["index"], naive["index"])
+        assert np.array_equal(lazy["cum"], naive["cum"]) and lazy["stop"] == naive["stop"]
+        g = naive["gain"]
+        assert (np.diff(g) <= 0).all()
+        assert (np.diff(lazy["coverage"]) > 0).all()
+        assert g.sum() == O.dense_bits(lazy["cum"], 200, 200).sum()
+
+
+def test_wordwise_gain_equals_bitloop():
+    """1,000 random window/bitmap pairs."""
+    rng = np.random.default_rng(4)
+    for _ in range(1000):
+        nr, nc = (int(x) for x in rng.integers(2, 90, 2))
+        h, w = int(rng.integers(1, nr + 1)), int(rng.integers(1, nc + 1))
+        r0, c0 = int(rng.integers(0, nr - h + 1)), int(rng.integers(0, nc - w + 1))
+        v = O.pack_dense(rng.integers(0, 2, (h, w)))
+        cum = O.pack_dense(rng.integers(0, 2, (nr, nc)) * (rng.random() < 0.8))
+        win = np.array([r0, c0, h, w], np.int32)
+        a = O.marginal_gain(win, v, cum, nr, nc)
+        assert a == O.marginal_gain(win, v, cum, nr, nc, bitloop=True)
+        bits = O.dense_bits(cum, nr, nc)[r0:r0 + h, c0:c0 + w]
+        assert a == int((O.unpack_window(win, v) & (1 - bits)).sum())
+
+
+def test_random_observers_draw_order():
+    rows, cols = O.random_observers(16384, 16384, 5, 42)
+    d = O.splitmix(42, 10, 1, 16384)
+    assert list(rows) == list(d[0::2]) and list(cols) == list(d[1::2])
