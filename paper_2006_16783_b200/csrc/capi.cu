@@ -113,11 +113,15 @@ void txs_destroy(txs_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    void* bufs[] = {c->d_z, c->d_vix, c->d_crow, c->d_ccol, c->d_cscore, c->d_words, c->d_win,
-                    c->d_pop, c->d_cum, c->d_delta[0], c->d_delta[1], c->d_gain, c->d_state,
+    void* bufs[] = {c->d_z, c->d_zt, c->d_vix, c->d_crow, c->d_ccol, c->d_cscore, c->d_words, c->d_win,
+                    c->d_pop, c->d_cum, c->d_dlist, c->d_gain, c->d_state,
                     c->d_bucket_start, c->d_bucket_items, c->d_counters, c->d_scratch};
     for (void* p : bufs) if (p) cudaFree(p);
-    for (auto& kv : c->templates) { cudaFree(kv.second.rays); cudaFree(kv.second.cells); }
+    for (auto& kv : c->templates) {
+        cudaFree(kv.second.rays); cudaFree(kv.second.cells);
+        if (kv.second.groups) cudaFree(kv.second.groups);
+        if (kv.second.events) cudaFree(kv.second.events);
+    }
     if (c->h_state) cudaFreeHost(c->h_state);
     for (cudaEvent_t e : c->user_ev) if (e) cudaEventDestroy(e);
     if (c->ev0) cudaEventDestroy(c->ev0);
@@ -189,6 +193,7 @@ static txs_status set_dims(txs_ctx* c, int64_t nrows, int64_t ncols) {
     c->nrows = nrows;
     c->ncols = ncols;
     c->vix_valid = c->cand_valid = c->vs_valid = c->site_valid = false;
+    c->zt_valid = false;
     return TXS_OK;
 }
 
@@ -236,6 +241,7 @@ txs_status txs_fill_rows(txs_ctx* c, int64_t rb, int64_t re, int16_t v) {
         return fail(c, TXS_ERR_INVALID_ARGUMENT, "read", "bad row range or value");
     cudaSetDevice(c->device);
     c->vix_valid = c->cand_valid = c->vs_valid = c->site_valid = false;
+    c->zt_valid = false;
     return launch_fill_rows(c, rb, re, v);
 }
 

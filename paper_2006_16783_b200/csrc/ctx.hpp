@@ -21,25 +21,41 @@ struct RayTemplate {
 const RayTemplate& ray_template(int32_t roi);
 
 // Device copy: rays[r] = {p, q, cell_begin, cell_count}; cells packed (a & 0xffff) | (b << 16).
+// For roi <= kEvMaxRoi also the merged per-ray event stream (see raytemplate.cpp):
+// 32-lane groups of neighbouring rays, events interleaved [step][lane].
+constexpr int kEvMaxRoi = 250;
+enum EvType : uint32_t { kEvRow = 0, kEvCol = 1, kEvPost = 2, kEvCell = 3, kEvNop = 4 };
 struct RayTemplateDev {
     int32_t roi = 0, nrays = 0;
     int64_t ncells = 0;
     int4* rays = nullptr;
     uint32_t* cells = nullptr;
+    int32_t ngroups = 0;
+    int2* groups = nullptr;      // {first event row (x32 lanes), steps}
+    uint32_t* events = nullptr;
+    int64_t nevents = 0;
 };
+// host-side event stream (exposed for tests through txs_event_template)
+struct EventTemplate {
+    std::vector<int2> groups;
+    std::vector<uint32_t> events;
+};
+const EventTemplate& event_template(int32_t roi);
 
 // Device-side SITE loop state (one struct, read/written by the loop kernels).
 constexpr int kMaxNb = 64;   // neighbour bucket ranges per winner
+struct DeltaWord { int y, wi; unsigned long long d; };   // newly covered bits of one cum word
 struct SiteState {
     unsigned long long best_key;   // (gain << 32) | (0xffffffff - idx), atomicMax target
+    unsigned int blocks_done;      // last-block detection in k_argmax
+    int dcount;                    // entries in the delta list this round
     long long nsel;
     long long covered;
-    long long iter;
-    int done;
+    int done;                      // no more commits
+    int finish;                    // commit this round, then done
     int stop;
     int w_idx, w_gain;
     int w_row0, w_col0, w_h, w_w;   // current winner window
-    int p_row0, p_col0, p_h, p_w;   // previous winner window (delta clearing)
     int nb_count;
     int nb_start[kMaxNb];
     int nb_pref[kMaxNb + 1];
@@ -62,6 +78,9 @@ struct txs_ctx {
     int64_t nrows = 0, ncols = 0;
     int16_t* d_z = nullptr;
     size_t z_cap = 0;
+    int16_t* d_zt = nullptr;      // column-major copy (VIX global path)
+    size_t zt_cap = 0;
+    bool zt_valid = false;
 
     // VixMap: one byte per post
     uint8_t* d_vix = nullptr;
@@ -88,7 +107,8 @@ struct txs_ctx {
     // SITE: row-padded bitmaps (wpr words per terrain row)
     int64_t wpr = 0;
     uint64_t* d_cum = nullptr;
-    uint64_t* d_delta[2] = {nullptr, nullptr};
+    txs::DeltaWord* d_dlist = nullptr;
+    size_t dlist_cap = 0;
     size_t bitmap_cap = 0;
     int32_t* d_gain = nullptr;
     size_t gain_cap = 0;

@@ -99,7 +99,73 @@ RayTemplate build(int32_t R) {
     return T;
 }
 
+// Merged per-ray event stream (decision D5 evaluated in u order): for each ray
+// the crossings of its primitive direction interleaved with its owned cells,
+// a cell emitted before every crossing with u_k >= u_c, nothing after the
+// last cell.  Event word: bits 0-2 type, 3-11 row offset, 12-20 col offset
+// (9-bit two's complement), 21-28 interpolation weight m.  Crossing offsets
+// name the first interpolation post; the second lies one step along +sign(q)
+// columns (row line) or +sign(p) rows (column line).
+inline uint32_t pack_ev(uint32_t type, int dr, int dc, int m) {
+    return type | ((uint32_t)(dr & 0x1ff) << 3) | ((uint32_t)(dc & 0x1ff) << 12) | ((uint32_t)m << 21);
+}
+
+EventTemplate build_events(const RayTemplate& T) {
+    EventTemplate E;
+    const int64_t nrays = (int64_t)T.p.size();
+    std::vector<std::vector<uint32_t>> per((size_t)nrays);
+    for (int64_t r = 0; r < nrays; ++r) {
+        const int64_t p = T.p[(size_t)r], q = T.q[(size_t)r];
+        const int64_t ap = std::llabs(p), aq = std::llabs(q), sp = p >= 0 ? 1 : -1, sq = q >= 0 ? 1 : -1;
+        const int64_t L2 = p * p + q * q;
+        const int64_t dqr = ap ? aq / ap : 0, dmr = ap ? aq % ap : 0, dqc = aq ? ap / aq : 0, dmc = aq ? ap % aq : 0;
+        int64_t i = 1, j = 1, qr = dqr, mr = dmr, qc = dqc, mc = dmc;
+        auto& ev = per[(size_t)r];
+        for (int64_t k = T.cell_begin[(size_t)r]; k < T.cell_begin[(size_t)r + 1]; ++k) {
+            const int64_t a = T.ca[(size_t)k], b = T.cb[(size_t)k], dot = a * p + b * q;
+            for (;;) {
+                bool isrow, iscol;
+                if (ap == 0) { isrow = false; iscol = true; }
+                else if (aq == 0) { isrow = true; iscol = false; }
+                else { const int64_t cmp = i * aq - j * ap; isrow = cmp <= 0; iscol = cmp >= 0; }
+                const int64_t idx = isrow ? i : j, n = isrow ? ap : aq;
+                if (idx * L2 >= dot * n) break;
+                if (isrow && iscol) ev.push_back(pack_ev(kEvPost, (int)(sp * i), (int)(sq * j), 0));
+                else if (isrow) ev.push_back(pack_ev(aq == 0 ? kEvPost : kEvRow, (int)(sp * i), (int)(sq * qr), (int)mr));
+                else ev.push_back(pack_ev(ap == 0 ? kEvPost : kEvCol, (int)(sp * qc), (int)(sq * j), (int)mc));
+                if (isrow) { ++i; qr += dqr; mr += dmr; if (mr >= ap) { mr -= ap; ++qr; } }
+                if (iscol) { ++j; qc += dqc; mc += dmc; if (mc >= aq) { mc -= aq; ++qc; } }
+            }
+            ev.push_back(pack_ev(kEvCell, (int)a, (int)b, 0));
+        }
+    }
+    const int64_t ngroups = (nrays + 31) / 32;
+    int64_t row = 0;
+    for (int64_t g = 0; g < ngroups; ++g) {
+        size_t steps = 0;
+        for (int64_t l = 0; l < 32 && g * 32 + l < nrays; ++l) steps = std::max(steps, per[(size_t)(g * 32 + l)].size());
+        E.groups.push_back(make_int2((int)row, (int)steps));
+        for (size_t s = 0; s < steps; ++s)
+            for (int64_t l = 0; l < 32; ++l) {
+                const int64_t r = g * 32 + l;
+                E.events.push_back(r < nrays && s < per[(size_t)r].size() ? per[(size_t)r][s] : (uint32_t)kEvNop);
+            }
+        row += (int64_t)steps;
+    }
+    return E;
+}
+
 }  // namespace
+
+const EventTemplate& event_template(int32_t roi) {
+    static std::mutex mu;
+    static std::map<int32_t, EventTemplate> cache;
+    const RayTemplate& T = ray_template(roi);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(roi);
+    if (it == cache.end()) it = cache.emplace(roi, build_events(T)).first;
+    return it->second;
+}
 
 const RayTemplate& ray_template(int32_t roi) {
     static std::mutex mu;
@@ -126,6 +192,16 @@ txs_status get_template(txs_ctx* ctx, int32_t roi, RayTemplateDev** out) {
     for (int64_t i = 0; i < D.ncells; ++i)
         cells[(size_t)i] = ((uint32_t)(uint16_t)(int16_t)T.ca[(size_t)i]) |
                            ((uint32_t)(uint16_t)(int16_t)T.cb[(size_t)i] << 16);
+    if (roi <= kEvMaxRoi) {
+        const EventTemplate& E = event_template(roi);
+        D.ngroups = (int32_t)E.groups.size();
+        D.nevents = (int64_t)E.events.size();
+        TXS_CUDA(ctx, "viewshed", cudaMalloc(&D.groups, sizeof(int2) * E.groups.size()));
+        TXS_CUDA(ctx, "viewshed", cudaMalloc(&D.events, sizeof(uint32_t) * std::max<size_t>(1, E.events.size())));
+        TXS_CUDA(ctx, "viewshed", cudaMemcpy(D.groups, E.groups.data(), sizeof(int2) * E.groups.size(), cudaMemcpyHostToDevice));
+        if (!E.events.empty())
+            TXS_CUDA(ctx, "viewshed", cudaMemcpy(D.events, E.events.data(), sizeof(uint32_t) * E.events.size(), cudaMemcpyHostToDevice));
+    }
     TXS_CUDA(ctx, "viewshed", cudaMalloc(&D.rays, sizeof(int4) * rays.size()));
     TXS_CUDA(ctx, "viewshed", cudaMalloc(&D.cells, sizeof(uint32_t) * std::max<size_t>(1, cells.size())));
     TXS_CUDA(ctx, "viewshed", cudaMemcpy(D.rays, rays.data(), sizeof(int4) * rays.size(), cudaMemcpyHostToDevice));

@@ -93,126 +93,155 @@ __global__ void k_bucket_fill(const int32_t* __restrict__ crow, const int32_t* _
 
 __device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) { return a > b ? a : b; }
 
-__global__ void k_argmax(const int32_t* __restrict__ gain, int64_t n, SiteState* st) {
+struct LoopPtrs {
+    const int32_t* crow;
+    const int32_t* ccol;
+    const int4* wins;
+    const int32_t* bstart;
+    txs_step* steps;
+};
+
+// Grid argmax of (gain << 32 | ~idx); the last CTA to finish takes the
+// round's decision (SPEC.md:367 stop rules in decision-D9 order), records the
+// step and the winner window, and computes the neighbour bucket ranges.
+__global__ void k_argmax(const int32_t* __restrict__ gain, SiteArgs a, SiteState* st, LoopPtrs lp) {
     if (st->done) return;
+    if (st->finish) {   // previous round committed the final pick
+        if (blockIdx.x == 0 && threadIdx.x == 0) st->done = 1;
+        return;
+    }
     __shared__ unsigned long long s_red[32];
+    __shared__ bool s_last;
     unsigned long long best = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long key = ((unsigned long long)(uint32_t)gain[i] << 32) | (0xffffffffull - (uint64_t)i);
         best = umax64(best, key);
     }
     for (int o = 16; o; o >>= 1) best = umax64(best, __shfl_xor_sync(kFull, best, o));
     if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = best;
     __syncthreads();
-    if (threadIdx.x < 32) {
-        best = threadIdx.x < (blockDim.x >> 5) ? s_red[threadIdx.x] : 0;
-        for (int o = 16; o; o >>= 1) best = umax64(best, __shfl_xor_sync(kFull, best, o));
-        if (threadIdx.x == 0 && best) atomicMax(&st->best_key, best);
-    }
-}
-
-// One CTA.  Stop rules (D9), delta + cum update over the winner window, step record,
-// neighbour bucket ranges for k_update.
-__global__ void __launch_bounds__(1024) k_commit(SiteArgs a, SiteState* st, const int32_t* __restrict__ crow,
-                                                  const int32_t* __restrict__ ccol, const int4* __restrict__ wins,
-                                                  const uint64_t* __restrict__ words, uint64_t* __restrict__ cum,
-                                                  uint64_t* __restrict__ delta0, uint64_t* __restrict__ delta1,
-                                                  const int32_t* __restrict__ bstart, txs_step* __restrict__ steps) {
-    if (st->done) return;
-    __shared__ int s_go;
-    const unsigned long long key = st->best_key;
-    const int g = (int)(key >> 32);
-    const int64_t idx = (int64_t)(0xffffffffull - (key & 0xffffffffull));
     if (threadIdx.x == 0) {
-        s_go = 0;
-        if (st->nsel >= a.n) { st->done = 1; st->stop = TXS_STOP_EXHAUSTED; }
-        else if (g <= 0) { st->done = 1; st->stop = TXS_STOP_ZERO_GAIN; }
-        else s_go = 1;
+        best = 0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) best = umax64(best, s_red[k]);
+        if (best) atomicMax(&st->best_key, best);
+        __threadfence();
+        s_last = atomicAdd(&st->blocks_done, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (!s_go) return;
-    const int cur = (int)(st->iter & 1);
-    uint64_t* dcur = cur ? delta1 : delta0;
-    uint64_t* dprev = cur ? delta0 : delta1;
-    // clear the previous winner's region of the other delta buffer
-    if (st->iter > 0) {
-        const int pr0 = st->p_row0, pc0 = st->p_col0, ph = st->p_h, pw = st->p_w;
-        const int wlo = pc0 >> 6, nwr = ((pc0 + pw - 1) >> 6) - wlo + 1;
-        for (int t = threadIdx.x; t < ph * nwr; t += blockDim.x)
-            dprev[(int64_t)(pr0 + t / nwr) * a.wpr + wlo + t % nwr] = 0ull;
-    }
-    const int4 win = wins[idx];
-    const uint64_t* v = words + idx * a.stride;
-    {
-        const int wlo = win.y >> 6, nwr = ((win.y + win.w - 1) >> 6) - wlo + 1;
-        for (int t = threadIdx.x; t < win.z * nwr; t += blockDim.x) {
-            const int y = win.x + t / nwr, wi = wlo + t % nwr;
-            const uint64_t m = col_mask(wi, win.y, win.y + win.w - 1);
-            const long long off = (long long)(y - win.x) * win.w + (wi * 64 - win.y);
-            const int64_t o = (int64_t)y * a.wpr + wi;
-            const uint64_t c = cum[o];
-            const uint64_t d = stream64(v, off) & m & ~c;
-            dcur[o] = d;
-            cum[o] = c | d;
-        }
-    }
-    if (threadIdx.x == 0) {
-        const int64_t k = st->nsel;
-        const int r = crow[idx], c = ccol[idx];
-        st->covered += g;
-        const double cov = (double)st->covered / a.total;
-        steps[k] = txs_step{idx, r, c, (int64_t)g, cov};
-        st->nsel = k + 1;
-        st->iter += 1;
-        st->w_idx = (int)idx; st->w_gain = g;
-        st->w_row0 = win.x; st->w_col0 = win.y; st->w_h = win.z; st->w_w = win.w;
-        st->p_row0 = win.x; st->p_col0 = win.y; st->p_h = win.z; st->p_w = win.w;
-        if (cov >= a.target) { st->done = 1; st->stop = TXS_STOP_TARGET_REACHED; }
-        else if (a.max_sel > 0 && k + 1 >= a.max_sel) { st->done = 1; st->stop = TXS_STOP_MAX_SELECTED; }
-        // neighbours: candidates within 2R rows/cols of the winner (window overlap)
-        const int by0 = max(0, (r - 2 * a.R) / a.bsize), by1 = min(a.nby - 1, (r + 2 * a.R) / a.bsize);
-        const int bx0 = max(0, (c - 2 * a.R) / a.bsize), bx1 = min(a.nbx - 1, (c + 2 * a.R) / a.bsize);
-        int nb = 0, pref = 0;
-        for (int by = by0; by <= by1 && nb < kMaxNb; ++by) {
-            const int s = bstart[by * a.nbx + bx0], e = bstart[by * a.nbx + bx1 + 1];
-            st->nb_start[nb] = s;
-            st->nb_pref[nb] = pref;
-            pref += e - s;
-            ++nb;
-        }
+    if (!s_last || threadIdx.x != 0) return;
+    __threadfence();
+    const unsigned long long key = atomicAdd(&st->best_key, 0ull);
+    st->best_key = 0ull;
+    st->blocks_done = 0u;
+    const int g = (int)(key >> 32);
+    const int64_t idx = (int64_t)(0xffffffffull - (key & 0xffffffffull));
+    if (st->nsel >= a.n) { st->done = 1; st->stop = TXS_STOP_EXHAUSTED; return; }
+    if (g <= 0) { st->done = 1; st->stop = TXS_STOP_ZERO_GAIN; return; }
+    const int4 win = lp.wins[idx];
+    const int r = lp.crow[idx], c = lp.ccol[idx];
+    const long long k = st->nsel;
+    st->covered += g;
+    const double cov = (double)st->covered / a.total;
+    lp.steps[k] = txs_step{idx, r, c, (int64_t)g, cov};
+    st->nsel = k + 1;
+    st->w_idx = (int)idx; st->w_gain = g;
+    st->w_row0 = win.x; st->w_col0 = win.y; st->w_h = win.z; st->w_w = win.w;
+    st->dcount = 0;
+    if (cov >= a.target) { st->finish = 1; st->stop = TXS_STOP_TARGET_REACHED; }
+    else if (a.max_sel > 0 && k + 1 >= a.max_sel) { st->finish = 1; st->stop = TXS_STOP_MAX_SELECTED; }
+    // neighbours: candidates within 2R rows/cols of the winner (window overlap);
+    // consecutive buckets of one bucket row are one CSR range
+    const int by0 = max(0, (r - 2 * a.R) / a.bsize), by1 = min(a.nby - 1, (r + 2 * a.R) / a.bsize);
+    const int bx0 = max(0, (c - 2 * a.R) / a.bsize), bx1 = min(a.nbx - 1, (c + 2 * a.R) / a.bsize);
+    int nb = 0, pref = 0;
+    for (int by = by0; by <= by1 && nb < kMaxNb; ++by) {
+        const int s0 = lp.bstart[by * a.nbx + bx0], e0 = lp.bstart[by * a.nbx + bx1 + 1];
+        st->nb_start[nb] = s0;
         st->nb_pref[nb] = pref;
-        st->nb_count = nb;
-        st->best_key = 0ull;
+        pref += e0 - s0;
+        ++nb;
+    }
+    st->nb_pref[nb] = pref;
+    st->nb_count = nb;
+}
+
+// Newly covered bits of the winner: d = v_w & ~cum per cum word of its window;
+// cum |= d; non-zero d words appended to the delta list for k_update.
+__global__ void k_commit(SiteArgs a, SiteState* st, const uint64_t* __restrict__ words, uint64_t* __restrict__ cum,
+                         DeltaWord* __restrict__ dlist) {
+    if (st->done) return;
+    const int idx = st->w_idx;
+    const int r0 = st->w_row0, c0 = st->w_col0, h = st->w_h, w = st->w_w;
+    const uint64_t* v = words + (int64_t)idx * a.stride;
+    const int wlo = c0 >> 6, nwr = ((c0 + w - 1) >> 6) - wlo + 1;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < h * nwr; t += gridDim.x * blockDim.x) {
+        const int y = r0 + t / nwr, wi = wlo + t % nwr;
+        const uint64_t m = col_mask(wi, c0, c0 + w - 1);
+        const long long off = (long long)(y - r0) * w + (wi * 64 - c0);
+        const int64_t o = (int64_t)y * a.wpr + wi;
+        const uint64_t cw = cum[o];
+        const uint64_t d = stream64(v, off) & m & ~cw;
+        if (d) {
+            cum[o] = cw | d;
+            dlist[atomicAdd(&st->dcount, 1)] = DeltaWord{y, wi, d};
+        }
     }
 }
 
-// incremental: gain_i -= popc(v_i & delta) over the overlap of windows i and w
-__global__ void k_update(SiteArgs a, const SiteState* __restrict__ st, const int4* __restrict__ wins,
-                         const uint64_t* __restrict__ words, const uint64_t* __restrict__ delta0,
-                         const uint64_t* __restrict__ delta1, const int32_t* __restrict__ items,
-                         int32_t* __restrict__ gain, unsigned long long* __restrict__ counters) {
-    if (st->done) return;
-    const int lane = threadIdx.x & 31;
-    const int nb = st->nb_count, total = st->nb_pref[nb];
-    const uint64_t* D = ((st->iter - 1) & 1) ? delta1 : delta0;
+// incremental: gain_i -= popc(v_i & delta) for the neighbours i whose window
+// overlaps the winner's; one CTA per neighbour scans the (short, L2-resident)
+// delta list and touches v_i only at delta words inside its window.
+constexpr int kUpdThreads = 128;
+
+__global__ void __launch_bounds__(kUpdThreads) k_update(SiteArgs a, const SiteState* __restrict__ st,
+                                                         const int4* __restrict__ wins,
+                                                         const uint64_t* __restrict__ words,
+                                                         const DeltaWord* __restrict__ dlist,
+                                                         const int32_t* __restrict__ items,
+                                                         int32_t* __restrict__ gain,
+                                                         unsigned long long* __restrict__ counters) {
+    if (st->done || st->finish) return;
+    __shared__ int s_red[kUpdThreads / 32];
+    __shared__ int s_cnt[kUpdThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nb = st->nb_count, total = st->nb_pref[nb], nd = st->dcount;
     const int wr0 = st->w_row0, wc0 = st->w_col0, wr1 = wr0 + st->w_h - 1, wc1 = wc0 + st->w_w - 1;
-    unsigned long long bytes = 0;
-    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t f = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; f < total; f += warps) {
+    unsigned long long bytes_all = 0;
+    for (int f = blockIdx.x; f < total; f += gridDim.x) {
         int k = 0;
         while (k + 1 < nb && st->nb_pref[k + 1] <= f) ++k;
         const int i = items[st->nb_start[k] + (f - st->nb_pref[k])];
         const int4 win = wins[i];
         const int ra = max(win.x, wr0), rb = min(win.x + win.z - 1, wr1);
         const int cl = max(win.y, wc0), ch = min(win.y + win.w - 1, wc1);
-        if (ra > rb || cl > ch) continue;
-        const long long s = warp_window_popc<false>(words + (int64_t)i * a.stride, win, D, a.wpr, ra, rb, cl, ch, lane);
-        if (lane == 0) {
-            if (s) gain[i] -= (int32_t)s;
-            bytes += (unsigned long long)(rb - ra + 1) * (((ch >> 6) - (cl >> 6) + 1) * 8);
+        if (ra > rb || cl > ch) continue;   // uniform across the CTA
+        const uint64_t* v = words + (int64_t)i * a.stride;
+        const int wlo = cl >> 6, whi = ch >> 6;
+        int acc = 0, touched = 0;
+        for (int t = threadIdx.x; t < nd; t += kUpdThreads) {
+            const DeltaWord e = dlist[t];
+            if (e.y < ra || e.y > rb || e.wi < wlo || e.wi > whi) continue;
+            const uint64_t dm = e.d & col_mask(e.wi, cl, ch);
+            if (!dm) continue;
+            const long long off = (long long)(e.y - win.x) * win.w + (e.wi * 64 - win.y);
+            acc += __popcll(stream64(v, off) & dm);
+            ++touched;
         }
+        for (int o = 16; o; o >>= 1) {
+            acc += __shfl_down_sync(kFull, acc, o);
+            touched += __shfl_down_sync(kFull, touched, o);
+        }
+        if (lane == 0) { s_red[warp] = acc; s_cnt[warp] = touched; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int t = 0, tb = 0;
+            for (int q = 0; q < kUpdThreads / 32; ++q) { t += s_red[q]; tb += s_cnt[q]; }
+            if (t) gain[i] -= t;
+            bytes_all += 16ull * (unsigned long long)tb;
+        }
+        __syncthreads();
     }
-    if (lane == 0 && bytes) atomicAdd(counters + kSiteBytes, bytes);
+    if (threadIdx.x == 0 && bytes_all) atomicAdd(counters + kSiteBytes, bytes_all);
 }
 
 // full rescan: gain_i = popc(v_i & ~cum) over window i (also marginal_gains API)
@@ -291,12 +320,11 @@ SiteArgs make_args(txs_ctx* c, const txs_params& p) {
 txs_status alloc_bitmaps(txs_ctx* c) {
     c->wpr = (c->ncols + 63) / 64;
     const size_t bytes = sizeof(uint64_t) * (size_t)(c->nrows * c->wpr + 1);
-    if (bytes > c->bitmap_cap || !c->d_cum) {
-        for (uint64_t** p : {&c->d_cum, &c->d_delta[0], &c->d_delta[1]}) { if (*p) cudaFree(*p); *p = nullptr; }
-        c->bitmap_cap = 0;
-        for (uint64_t** p : {&c->d_cum, &c->d_delta[0], &c->d_delta[1]}) TXS_CUDA(c, "site", cudaMalloc(p, bytes));
-        c->bitmap_cap = bytes;
-    }
+    if (ensure(c, "site", (void**)&c->d_cum, &c->bitmap_cap, bytes) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
+    // delta list: at most one entry per cum word of a full window
+    const int64_t side = 2 * (int64_t)std::max(1, c->vs_roi) + 1;
+    const size_t dl = sizeof(DeltaWord) * (size_t)(side * ((side + 63) / 64 + 1));
+    if (ensure(c, "site", (void**)&c->d_dlist, &c->dlist_cap, dl) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
     return TXS_OK;
 }
 
@@ -328,8 +356,6 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
 
     const size_t bm = sizeof(uint64_t) * (size_t)(c->nrows * c->wpr + 1);
     TXS_CUDA(c, "site", cudaMemsetAsync(c->d_cum, 0, bm, c->stream));
-    TXS_CUDA(c, "site", cudaMemsetAsync(c->d_delta[0], 0, bm, c->stream));
-    TXS_CUDA(c, "site", cudaMemsetAsync(c->d_delta[1], 0, bm, c->stream));
     TXS_CUDA(c, "site", cudaMemsetAsync(c->d_state, 0, sizeof(SiteState), c->stream));
     const int sms = c->num_sms;
     if (n > 0) {
@@ -348,20 +374,21 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
     }
     // graph of kRoundsPerGraph rounds
     const int am_blocks = blocks_for(n, 256 * 4, sms * 2);
-    const int up_blocks = sms * 4;
+    const int cm_blocks = 16;
+    const int up_blocks = sms * 8;
     const int full_blocks = blocks_for(n * 32, 256, sms * 16);
+    const LoopPtrs lp{c->d_crow, c->d_ccol, c->d_win, c->d_bucket_start, d_steps};
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     TXS_CUDA(c, "site", cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     for (int r = 0; r < kRoundsPerGraph; ++r) {
         if (p.site_mode == 1)
             k_gain_full<int32_t><<<full_blocks, 256, 0, c->stream>>>(a, c->d_state, c->d_win, c->d_words, c->d_cum, c->d_gain, c->d_counters);
-        k_argmax<<<am_blocks, 256, 0, c->stream>>>(c->d_gain, n, c->d_state);
-        k_commit<<<1, 1024, 0, c->stream>>>(a, c->d_state, c->d_crow, c->d_ccol, c->d_win, c->d_words, c->d_cum,
-                                            c->d_delta[0], c->d_delta[1], c->d_bucket_start, d_steps);
+        k_argmax<<<am_blocks, 256, 0, c->stream>>>(c->d_gain, a, c->d_state, lp);
+        k_commit<<<cm_blocks, 256, 0, c->stream>>>(a, c->d_state, c->d_words, c->d_cum, c->d_dlist);
         if (p.site_mode != 1)
-            k_update<<<up_blocks, 256, 0, c->stream>>>(a, c->d_state, c->d_win, c->d_words, c->d_delta[0], c->d_delta[1],
-                                                       c->d_bucket_items, c->d_gain, c->d_counters);
+            k_update<<<up_blocks, kUpdThreads, 0, c->stream>>>(a, c->d_state, c->d_win, c->d_words, c->d_dlist,
+                                                               c->d_bucket_items, c->d_gain, c->d_counters);
     }
     cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
     if (ce != cudaSuccess) return cuda_fail(c, "site", ce);
@@ -401,16 +428,15 @@ txs_status launch_marginal_gains(txs_ctx* c, const uint64_t* d_cum_dense, int64_
     p.target_coverage = 1.0;
     const SiteArgs a = make_args(c, p);
     if (alloc_bitmaps(c) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
-    uint64_t* pad = c->d_delta[0];
-    TXS_CUDA(c, "site", cudaMemsetAsync(pad, 0, c->bitmap_cap, c->stream));
+    uint64_t* pad = nullptr;
+    TXS_CUDA(c, "site", cudaMallocAsync((void**)&pad, sizeof(uint64_t) * (size_t)(c->nrows * c->wpr + 1), c->stream));
     k_dense_to_padded<<<blocks_for(c->nrows * c->wpr, 256, c->num_sms * 16), 256, 0, c->stream>>>(d_cum_dense, pad, c->nrows, c->ncols, c->wpr);
     TXS_LAUNCHED(c, "site");
     if (a.n > 0) {
         k_gain_full<int64_t><<<blocks_for(a.n * 32, 256, c->num_sms * 16), 256, 0, c->stream>>>(a, nullptr, c->d_win, c->d_words, pad, d_gains, nullptr);
         TXS_LAUNCHED(c, "site");
     }
-    // the delta buffer is scratch here; SITE state is no longer consistent
-    c->site_valid = false;
+    TXS_CUDA(c, "site", cudaFreeAsync(pad, c->stream));
     return TXS_OK;
 }
 

@@ -147,6 +147,137 @@ __global__ void k_viewshed(const int16_t* __restrict__ z, const int32_t* __restr
     }
 }
 
+// Event-stream variant (roi <= kEvMaxRoi): the merged per-ray events of the
+// template are read [step][lane] (one coalesced 128-byte line per warp step)
+// and every event — row/column/post crossing or owned cell — goes through the
+// same branch-free arithmetic: value v = z0*w0 + z1*w1, then
+//   crossing:  X = v - E*n,           Y = line index   (horizon candidate X/Y)
+//   cell:      X = (v + h_r - E)*L2,  Y = dot          (receiver tangent X/Y)
+// compared with the horizon NH/MH by X*MH vs NH*Y (int64).  Lanes of a warp
+// are 32 neighbouring rays; the CTA's warps stride over the ray groups.
+template <bool INTERIOR>
+__device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, int c, int E, int row0, int col0, int w,
+                                          const VsArgs& a, const int4* __restrict__ rays,
+                                          const int2* __restrict__ groups, const uint32_t* __restrict__ events,
+                                          int ngroups, uint32_t* s_bits, uint64_t* gout, bool smem_bits,
+                                          unsigned long long& n_cross, unsigned long long& n_cells) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int16_t* __restrict__ P = z + (int64_t)r * a.ncols + c;
+    for (int g = warp; g < ngroups; g += nwarps) {
+        const int2 grp = __ldg(groups + g);
+        const int ray = g * 32 + lane;
+        int p = 0, q = 0;
+        if (ray < a.nrays) { const int4 rd = __ldg(rays + ray); p = rd.x; q = rd.y; }
+        const int ap = abs(p), aq = abs(q);
+        const int sp = p >= 0 ? 1 : -1, sq = q >= 0 ? 1 : -1;
+        const int L2 = p * p + q * q;
+        int i = 0, j = 0;
+        bool has = false, alive = true;
+        int NH = 0, MH = 1;
+        const uint32_t* ev = events + (int64_t)grp.x * 32 + lane;
+        for (int st = 0; st < grp.y; ++st) {
+            const uint32_t e = __ldg(ev + (int64_t)st * 32);
+            const uint32_t type = e & 7u;
+            const int dr = ((int)(e << 20)) >> 23, dc = ((int)(e << 11)) >> 23;
+            const int m = (int)((e >> 21) & 0xffu);
+            const bool isrow = type == kEvRow, iscol = type == kEvCol, ispost = type == kEvPost;
+            const bool iscell = type == kEvCell, iscross = type <= kEvPost;
+            i += (isrow || ispost);
+            j += (iscol || ispost);
+            const int rr = r + dr, cc = c + dc;
+            const int dr1 = iscol ? sp : 0, dc1 = isrow ? sq : 0;
+            bool inb = true;
+            if (!INTERIOR) {
+                inb = rr >= 0 && rr < a.nrows && cc >= 0 && cc < a.ncols &&
+                      rr + dr1 >= 0 && rr + dr1 < a.nrows && cc + dc1 >= 0 && cc + dc1 < a.ncols;
+            }
+            const bool use = inb && type != kEvNop;
+            const int off0 = use ? dr * a.ncols + dc : 0;
+            const int off1 = use ? off0 + dr1 * a.ncols + dc1 : 0;
+            const int z0 = __ldg(P + off0), z1 = __ldg(P + off1);
+            const bool byrow = isrow || (ispost && ap > 0);
+            const int n = iscell ? 1 : (byrow ? ap : aq);
+            const int w1 = (isrow || iscol) ? m : 0;
+            const int v = z0 * (n - w1) + z1 * w1;
+            long long X;
+            int Y;
+            if (iscell) { X = (long long)(v + a.hr - E) * L2; Y = dr * p + dc * q; }
+            else { X = (long long)(v - E * n); Y = byrow ? i : j; }
+            const long long lhs = X * MH, rhs = (long long)NH * Y;
+            if (iscross) {
+                if (!inb) alive = false;
+                else if (alive && (!has || lhs > rhs)) { has = true; NH = (int)X; MH = Y; ++n_cross; }
+                else if (alive) ++n_cross;
+            } else if (iscell && inb) {
+                ++n_cells;
+                if (!has || lhs >= rhs) {
+                    const int k = (rr - row0) * w + (cc - col0);
+                    if (smem_bits) atomicOr(&s_bits[k >> 5], 1u << (k & 31));
+                    else atomicOr((unsigned long long*)&gout[k >> 6], 1ull << (k & 63));
+                }
+            }
+        }
+    }
+}
+
+template <bool SMEM_BITS>
+__global__ void k_viewshed_ev(const int16_t* __restrict__ z, const int32_t* __restrict__ crow,
+                              const int32_t* __restrict__ ccol, const int4* __restrict__ rays,
+                              const int2* __restrict__ groups, const uint32_t* __restrict__ events, int ngroups,
+                              VsArgs a, uint64_t* __restrict__ words, int4* __restrict__ wins,
+                              int32_t* __restrict__ pops, unsigned long long* __restrict__ counters) {
+    extern __shared__ __align__(16) uint32_t s_bits[];
+    __shared__ int s_red[32];
+    const int64_t cand = blockIdx.x;
+    const int r = crow[cand], c = ccol[cand];
+    const int row0 = max(0, r - a.R), col0 = max(0, c - a.R);
+    const int h = min(a.nrows - 1, r + a.R) - row0 + 1, w = min(a.ncols - 1, c + a.R) - col0 + 1;
+    const int nw64 = (h * w + 63) >> 6;
+    uint64_t* out = words + cand * a.stride;
+    if (SMEM_BITS) {
+        for (int i = threadIdx.x; i < 2 * nw64; i += blockDim.x) s_bits[i] = 0u;
+        __syncthreads();
+    }
+    const int E = __ldg(z + (int64_t)r * a.ncols + c) + a.ht;
+    unsigned long long n_cross = 0, n_cells = 0;
+    // every crossing/cell post lies within roi+1 of the observer
+    const bool interior = r - a.R - 1 >= 0 && r + a.R + 1 < a.nrows && c - a.R - 1 >= 0 && c + a.R + 1 < a.ncols;
+    if (interior)
+        vs_events<true>(z, r, c, E, row0, col0, w, a, rays, groups, events, ngroups, s_bits, out, SMEM_BITS, n_cross, n_cells);
+    else
+        vs_events<false>(z, r, c, E, row0, col0, w, a, rays, groups, events, ngroups, s_bits, out, SMEM_BITS, n_cross, n_cells);
+    if (threadIdx.x == 0) {
+        const int k = (r - row0) * w + (c - col0);
+        if (SMEM_BITS) atomicOr(&s_bits[k >> 5], 1u << (k & 31));
+        else atomicOr((unsigned long long*)&out[k >> 6], 1ull << (k & 63));
+    }
+    __syncthreads();
+    int pc = 0;
+    for (int i = threadIdx.x; i < nw64; i += blockDim.x) {
+        uint64_t v;
+        if (SMEM_BITS) { v = ((uint64_t)s_bits[2 * i + 1] << 32) | s_bits[2 * i]; out[i] = v; }
+        else v = out[i];
+        pc += __popcll(v);
+    }
+    for (int o = 16; o; o >>= 1) {
+        pc += __shfl_down_sync(0xffffffffu, pc, o);
+        n_cross += __shfl_down_sync(0xffffffffu, n_cross, o);
+        n_cells += __shfl_down_sync(0xffffffffu, n_cells, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_red[threadIdx.x >> 5] = pc;
+        atomicAdd(counters + kVsCross, n_cross);
+        atomicAdd(counters + kVsCells, n_cells);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += s_red[k];
+        pops[cand] = t;
+        wins[cand] = make_int4(row0, col0, h, w);
+    }
+}
+
 }  // namespace
 
 txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
@@ -164,19 +295,40 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
     c->vs_stride = mw;
     if (n == 0) return TXS_OK;
     VsArgs a{(int)c->nrows, (int)c->ncols, p.roi, p.tx_height, p.rx_height, T->nrays, mw};
-    const int per = (T->nrays + 255) / 256;
-    const int threads = ((T->nrays + per - 1) / per + 31) / 32 * 32;
     const size_t smem = sizeof(uint64_t) * (size_t)mw;
     if (n > 0x7fffffff) return fail(c, TXS_ERR_RANGE, "viewshed", "too many candidates");
-    if (smem <= 160 * 1024) {
-        if (smem > 48 * 1024)
-            TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(k_viewshed<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_viewshed<true><<<(unsigned)n, threads, smem, c->stream>>>(c->d_z, c->d_crow, c->d_ccol, T->rays, T->cells, a,
-                                                                    c->d_words, c->d_win, c->d_pop, c->d_counters);
+    const bool smem_bits = smem <= 160 * 1024;
+    if (!smem_bits) TXS_CUDA(c, "viewshed", cudaMemsetAsync(c->d_words, 0, sizeof(uint64_t) * n * mw, c->stream));
+    if (T->events) {
+        // warps per CTA: the divisor of the group count closest to 12 (balanced strides)
+        int best = 1;
+        for (int wv = 1; wv <= 32; ++wv)
+            if (T->ngroups % wv == 0 && std::abs(wv - 12) < std::abs(best - 12)) best = wv;
+        if (best < 4) best = std::min(T->ngroups, 8);
+        const int threads = 32 * best;
+        if (smem_bits) {
+            if (smem > 48 * 1024)
+                TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(k_viewshed_ev<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_viewshed_ev<true><<<(unsigned)n, threads, smem, c->stream>>>(c->d_z, c->d_crow, c->d_ccol, T->rays, T->groups,
+                                                                          T->events, T->ngroups, a, c->d_words, c->d_win,
+                                                                          c->d_pop, c->d_counters);
+        } else {
+            k_viewshed_ev<false><<<(unsigned)n, threads, 0, c->stream>>>(c->d_z, c->d_crow, c->d_ccol, T->rays, T->groups,
+                                                                        T->events, T->ngroups, a, c->d_words, c->d_win,
+                                                                        c->d_pop, c->d_counters);
+        }
     } else {
-        TXS_CUDA(c, "viewshed", cudaMemsetAsync(c->d_words, 0, sizeof(uint64_t) * n * mw, c->stream));
-        k_viewshed<false><<<(unsigned)n, threads, 0, c->stream>>>(c->d_z, c->d_crow, c->d_ccol, T->rays, T->cells, a,
-                                                                 c->d_words, c->d_win, c->d_pop, c->d_counters);
+        const int per = (T->nrays + 255) / 256;
+        const int threads = ((T->nrays + per - 1) / per + 31) / 32 * 32;
+        if (smem_bits) {
+            if (smem > 48 * 1024)
+                TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(k_viewshed<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_viewshed<true><<<(unsigned)n, threads, smem, c->stream>>>(c->d_z, c->d_crow, c->d_ccol, T->rays, T->cells, a,
+                                                                        c->d_words, c->d_win, c->d_pop, c->d_counters);
+        } else {
+            k_viewshed<false><<<(unsigned)n, threads, 0, c->stream>>>(c->d_z, c->d_crow, c->d_ccol, T->rays, T->cells, a,
+                                                                     c->d_words, c->d_win, c->d_pop, c->d_counters);
+        }
     }
     TXS_LAUNCHED(c, "viewshed");
     return TXS_OK;

@@ -15,6 +15,8 @@
 // r,c)); draws 2j,2j+1 give (dr,dc) = next_below(2R+1)-R, rejected outside the
 // lattice disk or the grid.  Lane l evaluates draw k+l directly (the splitmix
 // state is a counter), a ballot keeps the first S accepted pairs in order.
+#include <cstdlib>
+
 #include "ctx.hpp"
 
 namespace txs {
@@ -36,40 +38,70 @@ struct TerrainView {
     }
 };
 
-// exact floor(num / n) and remainder for 0 <= num < 2^24, n >= 1, via fp32 reciprocal + one fix-up
-__device__ __forceinline__ void divmod_small(int num, int n, float rinv, int& q, int& m) {
-    q = __float2int_rz(__int2float_rn(num) * rinv);
-    m = num - q * n;
-    if (m >= n) { ++q; m -= n; }
-    if (m < 0) { --q; m += n; }
+// Warp-cooperative exact LOS: returns true (uniform) iff the segment is blocked.
+// Major-axis form: with M = the longer of |dr|,|dc| (major lines i = 1..M-1)
+// and m_ = the shorter, step i covers the major-line crossing at
+// x_i = i*m_/M = q + r/M (posts A = (i,q), B = (i,q+1)) and — iff 0 < r < m_ —
+// the single minor-line crossing j = q between major lines i-1 and i (posts
+// C = (i-1,q), A; weight on A = j*M - (i-1)*m_).  Exact int32 tests:
+//   zA*(M-r) + zB*r            > E*M  + i*(Zt-E)
+//   zC*(m_-w) + zA*w           > E*m_ + j*(Zt-E)
+// Lanes take kIlp steps each per round (32*kIlp steps), all loads issued
+// before the compares; C = (i-1,q) is needed only when q moved from step i-1
+// to i (0 < r < m_), where it equals B of step i-1, held by the neighbouring
+// lane: a warp shuffle replaces that third load (one edge lane loads it).
+// FAR walks the steps from the receiver end (blocking terrain tends to sit
+// near the elevated endpoints' far side), which shortens early exits.
+template <bool SMEM>
+__device__ __forceinline__ int load_z(const int16_t* base, int off) {
+    if (SMEM) return base[off];
+    return __ldg(base + off);
 }
 
-// Warp-cooperative exact LOS: returns true (uniform) iff the segment is blocked.
-__device__ __forceinline__ bool warp_blocked(const TerrainView& T, int r, int c, int dr, int dc, int E, int Zt, int lane) {
+template <bool SMEM, int ILP, bool FAR>
+__device__ __forceinline__ bool warp_blocked(const int16_t* P, int stride, int dr, int dc, int E, int Zt, int lane) {
     const int nr = abs(dr), nc = abs(dc);
-    const int sr = dr >= 0 ? 1 : -1, sc = dc >= 0 ? 1 : -1;
-    const int nrow = nr > 1 ? nr - 1 : 0, ncol = nc > 1 ? nc - 1 : 0, total = nrow + ncol;
-    const int D = Zt - E;
-    const float rr_inv = nr ? __frcp_rn((float)nr) : 0.f, rc_inv = nc ? __frcp_rn((float)nc) : 0.f;
-    for (int g0 = 0; g0 < total; g0 += 32) {
-        const int g = g0 + lane;
+    const bool rows_major = nr >= nc;
+    const int nM = rows_major ? nr : nc, nm = rows_major ? nc : nr;
+    const int stepM = rows_major ? (dr >= 0 ? stride : -stride) : (dc >= 0 ? 1 : -1);
+    const int stepm = rows_major ? (dc >= 0 ? 1 : -1) : (dr >= 0 ? stride : -stride);
+    const int steps = nM - 1;
+    const int D = Zt - E, EM = E * nM, Em = E * nm;
+    const float rcp = nM ? __frcp_rn((float)nM) : 0.f;
+    const int q32 = nM ? (32 * nm) / nM : 0, r32 = nM ? (32 * nm) % nM : 0;
+    // the lane holding step i-1 in the same slot, and the edge lane without one
+    const int edge = FAR ? 31 : 0;
+    for (int k0 = 0; k0 < steps; k0 += 32 * ILP) {
+        int i = FAR ? steps - k0 - lane : k0 + 1 + lane;
+        const int num = max(i, 0) * nm;
+        int q = __float2int_rz(__int2float_rn(num) * rcp);
+        int r = num - q * nM;
+        if (r >= nM) { ++q; r -= nM; }
+        if (r < 0) { --q; r += nM; }
+        int zA[ILP], zB[ILP], zC[ILP], ii[ILP], qq[ILP], rr[ILP];
+#pragma unroll
+        for (int u = 0; u < ILP; ++u) {
+            const bool valid = i >= 1 && i <= steps;
+            const int offA = valid ? i * stepM + q * stepm : 0;
+            zA[u] = load_z<SMEM>(P, offA);
+            zB[u] = load_z<SMEM>(P, valid && r ? offA + stepm : offA);
+            zC[u] = lane == edge ? load_z<SMEM>(P, valid ? offA - stepM : 0) : 0;
+            ii[u] = valid ? i : -1;
+            qq[u] = q;
+            rr[u] = r;
+            if (FAR) { i -= 32; q -= q32; r -= r32; if (r < 0) { r += nM; --q; } }
+            else { i += 32; q += q32; r += r32; if (r >= nM) { r -= nM; ++q; } }
+        }
         bool b = false;
-        if (g < nrow) {
-            const int i = g + 1;
-            int q, m;
-            divmod_small(i * nc, nr, rr_inv, q, m);
-            const int rr = r + sr * i, c0 = c + sc * q;
-            int zn = T.at(rr, c0) * (nr - m);
-            if (m) zn += T.at(rr, c0 + sc) * m;
-            b = zn > E * nr + i * D;
-        } else if (g < total) {
-            const int j = g - nrow + 1;
-            int q, m;
-            divmod_small(j * nr, nc, rc_inv, q, m);
-            const int cc = c + sc * j, r0 = r + sr * q;
-            int zn = T.at(r0, cc) * (nc - m);
-            if (m) zn += T.at(r0 + sr, cc) * m;
-            b = zn > E * nc + j * D;
+#pragma unroll
+        for (int u = 0; u < ILP; ++u) {
+            const int nb = FAR ? __shfl_down_sync(kFull, zB[u], 1) : __shfl_up_sync(kFull, zB[u], 1);
+            const int zc = lane == edge ? zC[u] : nb;
+            const int iu = ii[u], qu = qq[u], ru = rr[u];
+            const bool v = iu > 0;
+            b |= v && zA[u] * (nM - ru) + zB[u] * ru > EM + iu * D;
+            const int w = qu * nM - (iu - 1) * nm;
+            b |= v && ru > 0 && ru < nm && zc * (nm - w) + zA[u] * w > Em + qu * D;
         }
         if (__any_sync(kFull, b)) return true;
     }
@@ -78,9 +110,19 @@ __device__ __forceinline__ bool warp_blocked(const TerrainView& T, int r, int c,
 
 __device__ __forceinline__ int warp_of_thread() { return threadIdx.x >> 5; }
 
-__device__ __forceinline__ int gcd_i(int a, int b) {
-    while (b) { const int t = a % b; a = b; b = t; }
-    return a;
+// distinct interior crossings of a (dr,dc) segment: |dr|+|dc|-gcd-1 (binary gcd)
+__device__ __forceinline__ int crossings_of(int dr, int dc) {
+    unsigned a = abs(dr), b = abs(dc);
+    if (a == 0 || b == 0) return (int)(a + b) > 0 ? (int)(a + b) - 1 : 0;
+    const int n = (int)(a + b);
+    const int sh = __ffs(a | b) - 1;
+    a >>= __ffs(a) - 1;
+    while (b) {
+        b >>= __ffs(b) - 1;
+        if (a > b) { const unsigned t = a; a = b; b = t; }
+        b -= a;
+    }
+    return n - (int)(a << sh) - 1;
 }
 
 struct VixArgs {
@@ -90,8 +132,8 @@ struct VixArgs {
     int tiles_x;
 };
 
-template <bool SMEM>
-__global__ void __launch_bounds__(kVixThreads) k_vix(const int16_t* __restrict__ z, int nrows, int ncols,
+template <bool SMEM, int ILP, bool FAR>
+__global__ void __launch_bounds__(kVixThreads, 2) k_vix(const int16_t* __restrict__ z, const int16_t* __restrict__ zt, int nrows, int ncols,
                                                       uint8_t* __restrict__ out, VixArgs a,
                                                       unsigned long long* __restrict__ counters) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
@@ -135,27 +177,55 @@ __global__ void __launch_bounds__(kVixThreads) k_vix(const int16_t* __restrict__
             nacc += __popc(mask);
         }
         __syncwarp();
-        // ---- test them ----
+        // ---- test them: lane s holds sample s (groups of 32) with its receiver elevation ----
         int vis = 0;
-        for (int sidx = 0; sidx < a.S; ++sidx) {
-            const int pk = s_samp[sidx];
-            const int dr = (int)(int16_t)(pk & 0xffff), dc = pk >> 16;
-            const int Zt = T.at(r + dr, c + dc) + a.hr;
-            vis += warp_blocked(T, r, c, dr, dc, E, Zt, lane) ? 0 : 1;
-            if (lane == 0) {
-                const int nr = abs(dr), nc = abs(dc);
-                n_cross += (nr && nc) ? (nr + nc - gcd_i(nr, nc) - 1) : (nr + nc > 0 ? nr + nc - 1 : 0);
+        for (int s0 = 0; s0 < a.S; s0 += 32) {
+            const int ns = min(32, a.S - s0);
+            int my_dr = 0, my_dc = 0, my_zt = 0;
+            if (lane < ns) {
+                const int pk = s_samp[s0 + lane];
+                my_dr = (int)(int16_t)(pk & 0xffff);
+                my_dc = pk >> 16;
+                my_zt = T.at(r + my_dr, c + my_dc) + a.hr;
+                n_cross += crossings_of(my_dr, my_dc);
+            }
+            const int16_t* P = SMEM ? T.s + (r - T.sr0) * T.sw + (c - T.sc0) : T.g + (int64_t)r * ncols + c;
+            const int stride = SMEM ? T.sw : ncols;
+            // global path: walk row-major segments on the column-major copy so the
+            // lanes' consecutive major steps are contiguous in memory
+            const int16_t* PT = SMEM ? P : zt + (int64_t)c * nrows + r;
+            for (int sidx = 0; sidx < ns; ++sidx) {
+                const int dr = __shfl_sync(kFull, my_dr, sidx), dc = __shfl_sync(kFull, my_dc, sidx);
+                const int Zt = __shfl_sync(kFull, my_zt, sidx);
+                const bool tr = !SMEM && abs(dr) > abs(dc);
+                const bool blk = tr ? warp_blocked<SMEM, ILP, FAR>(PT, nrows, dc, dr, E, Zt, lane)
+                                    : warp_blocked<SMEM, ILP, FAR>(P, stride, dr, dc, E, Zt, lane);
+                vis += blk ? 0 : 1;
             }
         }
         __syncwarp();
-        if (lane == 0) {
-            out[(int64_t)r * ncols + c] = (uint8_t)vis;
-            n_los += a.S;
-        }
+        if (lane == 0) out[(int64_t)r * ncols + c] = (uint8_t)vis;
+        n_los += a.S;
     }
+    for (int o = 16; o; o >>= 1) n_cross += __shfl_down_sync(kFull, n_cross, o);
     if (lane == 0 && n_los) {
         atomicAdd(counters + kVixLos, n_los);
         atomicAdd(counters + kVixCrossFull, n_cross);
+    }
+}
+
+// column-major copy of the terrain: zt[c*nrows + r] = z[r*ncols + c]
+__global__ void k_transpose(const int16_t* __restrict__ z, int16_t* __restrict__ zt, int nrows, int ncols) {
+    __shared__ int16_t t[32][33];
+    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    for (int y = threadIdx.y; y < 32; y += 8) {
+        const int r = r0 + y, c = c0 + threadIdx.x;
+        if (r < nrows && c < ncols) t[y][threadIdx.x] = z[(int64_t)r * ncols + c];
+    }
+    __syncthreads();
+    for (int x = threadIdx.y; x < 32; x += 8) {
+        const int c = c0 + x, r = r0 + threadIdx.x;
+        if (r < nrows && c < ncols) zt[(int64_t)c * nrows + r] = t[threadIdx.x][x];
     }
 }
 
@@ -166,9 +236,9 @@ __global__ void k_los_batch(const int16_t* __restrict__ z, int nrows, int ncols,
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     if (w >= n) return;
     const int4 p = pairs[w];
-    TerrainView T{z, nullptr, ncols, 0, 0, 0};
-    const int E = T.at(p.x, p.y) + ht, Zt = T.at(p.z, p.w) + hr;
-    const bool blocked = warp_blocked(T, p.x, p.y, p.z - p.x, p.w - p.y, E, Zt, lane);
+    const int16_t* P = z + (int64_t)p.x * ncols + p.y;
+    const int E = __ldg(P) + ht, Zt = __ldg(z + (int64_t)p.z * ncols + p.w) + hr;
+    const bool blocked = warp_blocked<false, 4, false>(P, ncols, p.z - p.x, p.w - p.y, E, Zt, lane);
     if (lane == 0) out[w] = blocked ? 0 : 1;
 }
 
@@ -185,12 +255,34 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     const int64_t side = kTile + 2 * (int64_t)p.roi;
     const size_t samp = sizeof(int) * (kVixWarps * (size_t)a.S + 4);
     const size_t smem = samp + sizeof(int16_t) * side * side;
+    // experiment knob: TXS_VIX_VARIANT = <ilp><order> e.g. "4n", "2f"
+    const char* var = getenv("TXS_VIX_VARIANT");
+    const int ilp = var && var[0] == '4' ? 4 : (var && var[0] == '2' ? 2 : 1);   // default: 1 (measured best)
+    const bool far = var && var[0] && var[1] == 'f';
+    auto go = [&](auto kern, size_t sm) -> txs_status {
+        if (sm > 48 * 1024) TXS_CUDA(c, "vix", cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        kern<<<(unsigned)tiles, kVixThreads, sm, c->stream>>>(c->d_z, c->d_zt, (int)c->nrows, (int)c->ncols, c->d_vix, a, c->d_counters);
+        return TXS_OK;
+    };
+    txs_status st;
     if (smem <= 110 * 1024) {   // two CTAs per SM
-        TXS_CUDA(c, "vix", cudaFuncSetAttribute(k_vix<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_vix<true><<<(unsigned)tiles, kVixThreads, smem, c->stream>>>(c->d_z, (int)c->nrows, (int)c->ncols, c->d_vix, a, c->d_counters);
+        if (ilp == 1) st = far ? go(k_vix<true, 1, true>, smem) : go(k_vix<true, 1, false>, smem);
+        else if (ilp == 2) st = far ? go(k_vix<true, 2, true>, smem) : go(k_vix<true, 2, false>, smem);
+        else st = far ? go(k_vix<true, 4, true>, smem) : go(k_vix<true, 4, false>, smem);
     } else {
-        k_vix<false><<<(unsigned)tiles, kVixThreads, samp, c->stream>>>(c->d_z, (int)c->nrows, (int)c->ncols, c->d_vix, a, c->d_counters);
+        if (!c->zt_valid) {
+            if (ensure(c, "vix", (void**)&c->d_zt, &c->zt_cap, sizeof(int16_t) * c->nrows * c->ncols) != TXS_OK)
+                return TXS_ERR_OUT_OF_MEMORY;
+            dim3 tb(32, 8), tg((unsigned)((c->ncols + 31) / 32), (unsigned)((c->nrows + 31) / 32));
+            k_transpose<<<tg, tb, 0, c->stream>>>(c->d_z, c->d_zt, (int)c->nrows, (int)c->ncols);
+            TXS_LAUNCHED(c, "vix");
+            c->zt_valid = true;
+        }
+        if (ilp == 1) st = far ? go(k_vix<false, 1, true>, samp) : go(k_vix<false, 1, false>, samp);
+        else if (ilp == 2) st = far ? go(k_vix<false, 2, true>, samp) : go(k_vix<false, 2, false>, samp);
+        else st = far ? go(k_vix<false, 4, true>, samp) : go(k_vix<false, 4, false>, samp);
     }
+    if (st != TXS_OK) return st;
     TXS_LAUNCHED(c, "vix");
     return TXS_OK;
 }

@@ -154,7 +154,7 @@ def test_viewsheds_c1_bit_exact(engine, c1):
     _vs_compare(engine, c1, 100, 10, 10, rows, cols)
 
 
-@pytest.mark.parametrize("roi,h", [(200, 20), (250, 50), (1, 0), (3, 5)])
+@pytest.mark.parametrize("roi,h", [(200, 20), (250, 50), (1, 0), (3, 5), (300, 10), (100, 10)])
 def test_viewsheds_sampled_bit_exact(engine, roi, h):
     z = O.generate_fractal(1100, 1300, 0.5, 31, 0, 4000)
     rng = np.random.default_rng(roi)
