@@ -12,7 +12,10 @@ HDRS := $(wildcard $(PKG)/csrc/*.hpp $(PKG)/csrc/*.cuh) include/txsite_b200.h
 OBJ := $(CU_SRC:$(PKG)/csrc/%.cu=$(BUILD)/%.o) $(CPP_SRC:$(PKG)/csrc/%.cpp=$(BUILD)/%.cpp.o)
 LIB := $(PKG)/libtxsite_b200.so
 
-all: $(LIB) oracle
+HOSTLIB := $(PKG)/libtxsite_host.so
+CLI := $(PKG)/bin/txsite
+
+all: $(LIB) $(HOSTLIB) $(CLI) oracle
 
 $(BUILD):
 	mkdir -p $(BUILD)
@@ -26,11 +29,18 @@ $(BUILD)/%.cpp.o: $(PKG)/csrc/%.cpp $(HDRS) | $(BUILD)
 $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ)
 
+$(HOSTLIB): $(PKG)/host/txsite.cpp include/txsite/txsite.hpp include/txsite_b200.h $(LIB)
+	g++ -std=c++17 -O2 -fPIC -shared -Wall -Wextra -Iinclude -o $@ $(PKG)/host/txsite.cpp -L$(PKG) -ltxsite_b200 -Wl,-rpath,'$$ORIGIN'
+
+$(CLI): $(PKG)/host/txsite_main.cpp $(HOSTLIB)
+	mkdir -p $(PKG)/bin
+	g++ -std=c++17 -O2 -Wall -Wextra -Iinclude -o $@ $(PKG)/host/txsite_main.cpp -L$(PKG) -ltxsite_host -ltxsite_b200 -Wl,-rpath,'$$ORIGIN/..'
+
 oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -rf $(BUILD) $(LIB)
+	rm -rf $(BUILD) $(LIB) $(HOSTLIB) $(CLI)
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean

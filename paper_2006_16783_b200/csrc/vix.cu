@@ -15,8 +15,6 @@
 // r,c)); draws 2j,2j+1 give (dr,dc) = next_below(2R+1)-R, rejected outside the
 // lattice disk or the grid.  Lane l evaluates draw k+l directly (the splitmix
 // state is a counter), a ballot keeps the first S accepted pairs in order.
-#include <cstdlib>
-
 #include "ctx.hpp"
 
 namespace txs {
@@ -50,58 +48,61 @@ struct TerrainView {
 // before the compares; C = (i-1,q) is needed only when q moved from step i-1
 // to i (0 < r < m_), where it equals B of step i-1, held by the neighbouring
 // lane: a warp shuffle replaces that third load (one edge lane loads it).
-// FAR walks the steps from the receiver end (blocking terrain tends to sit
-// near the elevated endpoints' far side), which shortens early exits.
 template <bool SMEM>
 __device__ __forceinline__ int load_z(const int16_t* base, int off) {
     if (SMEM) return base[off];
     return __ldg(base + off);
 }
 
-template <bool SMEM, int ILP, bool FAR>
+template <bool SMEM, int ILP>
 __device__ __forceinline__ bool warp_blocked(const int16_t* P, int stride, int dr, int dc, int E, int Zt, int lane) {
     const int nr = abs(dr), nc = abs(dc);
     const bool rows_major = nr >= nc;
     const int nM = rows_major ? nr : nc, nm = rows_major ? nc : nr;
+    const int steps = nM - 1;
+    if (steps <= 0) return false;
     const int stepM = rows_major ? (dr >= 0 ? stride : -stride) : (dc >= 0 ? 1 : -1);
     const int stepm = rows_major ? (dc >= 0 ? 1 : -1) : (dr >= 0 ? stride : -stride);
-    const int steps = nM - 1;
-    const int D = Zt - E, EM = E * nM, Em = E * nm;
-    const float rcp = nM ? __frcp_rn((float)nM) : 0.f;
-    const int q32 = nM ? (32 * nm) / nM : 0, r32 = nM ? (32 * nm) % nM : 0;
-    // the lane holding step i-1 in the same slot, and the edge lane without one
-    const int edge = FAR ? 31 : 0;
-    for (int k0 = 0; k0 < steps; k0 += 32 * ILP) {
-        int i = FAR ? steps - k0 - lane : k0 + 1 + lane;
-        const int num = max(i, 0) * nm;
-        int q = __float2int_rz(__int2float_rn(num) * rcp);
-        int r = num - q * nM;
+    const int D = Zt - E;
+    // per-lane DDA state at step i: q = floor(i*nm/nM), r = i*nm mod nM (one
+    // fp32-reciprocal division per sample, then exact increments of 32 steps)
+    const float rcp = __fdividef(1.0f, (float)nM);
+    auto divmod = [&](int num, int& q, int& r) {
+        q = __float2int_rz(__int2float_rn(num) * rcp);
+        r = num - q * nM;
         if (r >= nM) { ++q; r -= nM; }
         if (r < 0) { --q; r += nM; }
-        int zA[ILP], zB[ILP], zC[ILP], ii[ILP], qq[ILP], rr[ILP];
-#pragma unroll
-        for (int u = 0; u < ILP; ++u) {
-            const bool valid = i >= 1 && i <= steps;
-            const int offA = valid ? i * stepM + q * stepm : 0;
-            zA[u] = load_z<SMEM>(P, offA);
-            zB[u] = load_z<SMEM>(P, valid && r ? offA + stepm : offA);
-            zC[u] = lane == edge ? load_z<SMEM>(P, valid ? offA - stepM : 0) : 0;
-            ii[u] = valid ? i : -1;
-            qq[u] = q;
-            rr[u] = r;
-            if (FAR) { i -= 32; q -= q32; r -= r32; if (r < 0) { r += nM; --q; } }
-            else { i += 32; q += q32; r += r32; if (r >= nM) { r -= nM; ++q; } }
-        }
+    };
+    int q32, r32;
+    divmod(32 * nm, q32, r32);
+    int i = 1 + lane;
+    int q, r;
+    divmod(max(i, 0) * nm, q, r);
+    int off = i * stepM + q * stepm;                 // post A = (i, q)
+    int rhsM = E * nM + i * D;                       // major-line LOS numerator
+    int rhsm = E * nm + q * D;                       // minor-line LOS numerator
+    const int dOffM = 32 * stepM, dRhsM = 32 * D;
+    for (int k0 = 0; k0 < steps; k0 += 32 * ILP) {
         bool b = false;
 #pragma unroll
         for (int u = 0; u < ILP; ++u) {
-            const int nb = FAR ? __shfl_down_sync(kFull, zB[u], 1) : __shfl_up_sync(kFull, zB[u], 1);
-            const int zc = lane == edge ? zC[u] : nb;
-            const int iu = ii[u], qu = qq[u], ru = rr[u];
-            const bool v = iu > 0;
-            b |= v && zA[u] * (nM - ru) + zB[u] * ru > EM + iu * D;
-            const int w = qu * nM - (iu - 1) * nm;
-            b |= v && ru > 0 && ru < nm && zc * (nm - w) + zA[u] * w > Em + qu * D;
+            const bool valid = i >= 1 && i <= steps;
+            const int oA = valid ? off : 0;
+            const int zA = load_z<SMEM>(P, oA);
+            const int zB = (valid && r) ? load_z<SMEM>(P, oA + stepm) : 0;
+            // C = (i-1, q): B of the neighbouring step when q moved (needed only then)
+            const int zCl = (lane == 0 && valid) ? load_z<SMEM>(P, oA - stepM) : 0;
+            const int nb = __shfl_up_sync(kFull, zB, 1);
+            const int zC = lane == 0 ? zCl : nb;
+            b |= valid && zA * (nM - r) + zB * r > rhsM;
+            // minor line j = q between major lines i-1 and i: weight on A = nm - r
+            b |= valid && r > 0 && r < nm && zC * r + zA * (nm - r) > rhsm;
+            // advance 32 steps
+            i += 32;
+            off += dOffM;
+            rhsM += dRhsM;
+            r += r32; q += q32; off += q32 * stepm; rhsm += q32 * D;
+            if (r >= nM) { r -= nM; ++q; off += stepm; rhsm += D; }
         }
         if (__any_sync(kFull, b)) return true;
     }
@@ -132,7 +133,7 @@ struct VixArgs {
     int tiles_x;
 };
 
-template <bool SMEM, int ILP, bool FAR>
+template <bool SMEM, int ILP>
 __global__ void __launch_bounds__(kVixThreads, 2) k_vix(const int16_t* __restrict__ z, const int16_t* __restrict__ zt, int nrows, int ncols,
                                                       uint8_t* __restrict__ out, VixArgs a,
                                                       unsigned long long* __restrict__ counters) {
@@ -198,8 +199,8 @@ __global__ void __launch_bounds__(kVixThreads, 2) k_vix(const int16_t* __restric
                 const int dr = __shfl_sync(kFull, my_dr, sidx), dc = __shfl_sync(kFull, my_dc, sidx);
                 const int Zt = __shfl_sync(kFull, my_zt, sidx);
                 const bool tr = !SMEM && abs(dr) > abs(dc);
-                const bool blk = tr ? warp_blocked<SMEM, ILP, FAR>(PT, nrows, dc, dr, E, Zt, lane)
-                                    : warp_blocked<SMEM, ILP, FAR>(P, stride, dr, dc, E, Zt, lane);
+                const bool blk = tr ? warp_blocked<SMEM, ILP>(PT, nrows, dc, dr, E, Zt, lane)
+                                    : warp_blocked<SMEM, ILP>(P, stride, dr, dc, E, Zt, lane);
                 vis += blk ? 0 : 1;
             }
         }
@@ -238,7 +239,7 @@ __global__ void k_los_batch(const int16_t* __restrict__ z, int nrows, int ncols,
     const int4 p = pairs[w];
     const int16_t* P = z + (int64_t)p.x * ncols + p.y;
     const int E = __ldg(P) + ht, Zt = __ldg(z + (int64_t)p.z * ncols + p.w) + hr;
-    const bool blocked = warp_blocked<false, 4, false>(P, ncols, p.z - p.x, p.w - p.y, E, Zt, lane);
+    const bool blocked = warp_blocked<false, 1>(P, ncols, p.z - p.x, p.w - p.y, E, Zt, lane);
     if (lane == 0) out[w] = blocked ? 0 : 1;
 }
 
@@ -255,10 +256,8 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     const int64_t side = kTile + 2 * (int64_t)p.roi;
     const size_t samp = sizeof(int) * (kVixWarps * (size_t)a.S + 4);
     const size_t smem = samp + sizeof(int16_t) * side * side;
-    // experiment knob: TXS_VIX_VARIANT = <ilp><order> e.g. "4n", "2f"
-    const char* var = getenv("TXS_VIX_VARIANT");
-    const int ilp = var && var[0] == '4' ? 4 : (var && var[0] == '2' ? 2 : 1);   // default: 1 (measured best)
-    const bool far = var && var[0] && var[1] == 'f';
+    // measured on B200 (profiles/): one step per lane between warp votes (ILP 1,
+    // steps walked from the transmitter) beat 2 and 4 and receiver-first walks
     auto go = [&](auto kern, size_t sm) -> txs_status {
         if (sm > 48 * 1024) TXS_CUDA(c, "vix", cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         kern<<<(unsigned)tiles, kVixThreads, sm, c->stream>>>(c->d_z, c->d_zt, (int)c->nrows, (int)c->ncols, c->d_vix, a, c->d_counters);
@@ -266,9 +265,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     };
     txs_status st;
     if (smem <= 110 * 1024) {   // two CTAs per SM
-        if (ilp == 1) st = far ? go(k_vix<true, 1, true>, smem) : go(k_vix<true, 1, false>, smem);
-        else if (ilp == 2) st = far ? go(k_vix<true, 2, true>, smem) : go(k_vix<true, 2, false>, smem);
-        else st = far ? go(k_vix<true, 4, true>, smem) : go(k_vix<true, 4, false>, smem);
+        st = go(k_vix<true, 1>, smem);
     } else {
         if (!c->zt_valid) {
             if (ensure(c, "vix", (void**)&c->d_zt, &c->zt_cap, sizeof(int16_t) * c->nrows * c->ncols) != TXS_OK)
@@ -278,9 +275,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
             TXS_LAUNCHED(c, "vix");
             c->zt_valid = true;
         }
-        if (ilp == 1) st = far ? go(k_vix<false, 1, true>, samp) : go(k_vix<false, 1, false>, samp);
-        else if (ilp == 2) st = far ? go(k_vix<false, 2, true>, samp) : go(k_vix<false, 2, false>, samp);
-        else st = far ? go(k_vix<false, 4, true>, samp) : go(k_vix<false, 4, false>, samp);
+        st = go(k_vix<false, 1>, samp);
     }
     if (st != TXS_OK) return st;
     TXS_LAUNCHED(c, "vix");

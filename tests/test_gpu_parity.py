@@ -290,3 +290,40 @@ def test_errors_are_stage_tagged(engine):
     with pytest.raises(T.TxsError) as e:
         engine.set_candidates([11], [0])
     assert e.value.status == "OFF_GRID"
+
+
+# ---- C++ host API + CLI (the reference's tools/txsite_main.cpp flags) ----------
+def test_cli_matches_oracle_and_is_deterministic(tmp_path):
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "paper_2006_16783_b200", "bin", "txsite")
+    args = [exe, "--synth", "--nrows", "300", "--ncols", "260", "--seed", "5", "--roughness", "0.5",
+            "--roi", "20", "--tx-height", "10", "--rx-height", "10", "--samples", "10", "--per-block", "4",
+            "--block-width", "30", "--coverage", "0.9", "--vix-seed", "7", "--snapshots", "1,2,4"]
+    outs = []
+    for k in range(2):
+        d = tmp_path / f"run{k}"
+        d.mkdir()
+        r = subprocess.run(args + ["--out-dir", str(d)], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        outs.append({f: (d / f).read_bytes() for f in ("result.csv", "cumshed.pgm", "cumshed_1.pgm",
+                                                         "cumshed_2.pgm", "cumshed_4.pgm")})
+    assert outs[0] == outs[1]
+    z = O.generate_fractal(300, 260, 0.5, 5, 0, 4000)
+    s = O.estimate_vix(z, 20, 10, 10, 10, 7)
+    rows, cols, _ = O.find_candidates(s, 30, 4)
+    ow, ov = O.viewsheds(z, 20, 10, 10, rows, cols)
+    o = O.site(rows, cols, ow, ov, 300, 260, 0.9)
+    lines = outs[0]["result.csv"].decode().strip().splitlines()
+    assert lines[0] == "rank,row,col,marginal_gain,cumulative_coverage"
+    got = [tuple(int(x) for x in l.split(",")[1:4]) for l in lines[1:]]
+    exp = list(zip(o["row"].tolist(), o["col"].tolist(), o["gain"].tolist()))
+    assert got == exp
+    pgm = outs[0]["cumshed.pgm"]
+    assert pgm.startswith(b"P5\n260 300\n255\n")
+    img = np.frombuffer(pgm[len(b"P5\n260 300\n255\n"):], np.uint8).reshape(300, 260)
+    assert np.array_equal(img == 255, O.dense_bits(o["cum"], 300, 260) == 1)
+    a1 = np.frombuffer(outs[0]["cumshed_1.pgm"][15:], np.uint8)
+    a2 = np.frombuffer(outs[0]["cumshed_2.pgm"][15:], np.uint8)
+    assert ((a1 <= a2)).all()
