@@ -161,6 +161,33 @@ txs_status txs_marginal_gains(txs_ctx* ctx, const uint64_t* cum_dense, int64_t* 
 txs_status txs_run_pipeline(txs_ctx* ctx, const txs_params* p, txs_step* steps, int64_t cap,
                             int64_t* nsteps, int32_t* stop_reason, double* stage_ms);
 
+/* ---- multi-GPU row-band shards ---------------------------------
+ * A sharded context owns rows [row_begin,row_end) of a global nrows x ncols grid
+ * and holds terrain rows [max(0,row_begin-halo), min(nrows,row_end+halo)).
+ * Terrain input is those rows (txs_set_terrain) or the global generator
+ * (txs_generate_fractal with the global dims, cropped on the device).  VIX and
+ * FINDMAX cover the band only (bands align to FINDMAX block rows); candidate
+ * global ids are base + local index (txs_set_candidate_base), or the global
+ * draw index for txs_random_observers.  SITE runs as rounds driven by the
+ * caller: every rank reports its local best key, the caller reduces the max
+ * across ranks (the one collective), the owner exports the winner's window,
+ * every rank applies it.  No collective runs inside the engine. */
+txs_status txs_set_shard(txs_ctx* ctx, int64_t nrows, int64_t ncols, int64_t row_begin, int64_t row_end,
+                         int32_t halo);
+txs_status txs_shard_info(const txs_ctx* ctx, int64_t* held_row0, int64_t* held_rows, int64_t* band_begin,
+                          int64_t* band_end);
+txs_status txs_set_candidate_base(txs_ctx* ctx, int64_t gid0);
+txs_status txs_site_shard_begin(txs_ctx* ctx, const txs_params* p);
+/* key = (gain << 32) | (0xffffffff - global id) of the best local candidate, 0 if none */
+txs_status txs_site_shard_best(txs_ctx* ctx, uint64_t* key);
+/* If this rank owns global id gid: *owned = 1 and its observer position,
+ * window and packed words (words_stride u64) are written. */
+txs_status txs_site_shard_export(txs_ctx* ctx, int64_t gid, int32_t* owned, int32_t* row, int32_t* col,
+                                 txs_window* win, uint64_t* words, int64_t words_stride);
+/* OR the winner window into the held cum rows and update the local gains. */
+txs_status txs_site_shard_apply(txs_ctx* ctx, int32_t row, int32_t col, const txs_window* win,
+                                const uint64_t* words);
+
 /* ---- host-only helpers (no GPU needed; used by the CPU test-suite) -------- */
 /* The frozen D5 ray template for roi: returns ray count; arrays filled when the
  * caps suffice.  cell_begin has rays+1 entries. */

@@ -87,6 +87,13 @@ _sig("txs_site", C.c_int, [vp, C.POINTER(Params), vp, i64, C.POINTER(i64), C.POI
 _sig("txs_get_cumulative", C.c_int, [vp, vp])
 _sig("txs_marginal_gains", C.c_int, [vp, vp, vp])
 _sig("txs_run_pipeline", C.c_int, [vp, C.POINTER(Params), vp, i64, C.POINTER(i64), C.POINTER(i32), vp])
+_sig("txs_set_shard", C.c_int, [vp, i64, i64, i64, i64, i32])
+_sig("txs_shard_info", C.c_int, [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)])
+_sig("txs_set_candidate_base", C.c_int, [vp, i64])
+_sig("txs_site_shard_begin", C.c_int, [vp, C.POINTER(Params)])
+_sig("txs_site_shard_best", C.c_int, [vp, C.POINTER(u64)])
+_sig("txs_site_shard_export", C.c_int, [vp, i64, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32), vp, vp, i64])
+_sig("txs_site_shard_apply", C.c_int, [vp, i32, i32, vp, vp])
 _sig("txs_ray_template", i64, [i32, vp, vp, vp, vp, vp, i64, i64, C.POINTER(i64)])
 _sig("txs_selftest", C.c_int, [])
 
@@ -98,4 +105,6 @@ EXPORTS = [
     "txs_partition", "txs_find_candidates", "txs_set_candidates", "txs_random_observers",
     "txs_get_candidates", "txs_compute_viewsheds", "txs_get_viewsheds", "txs_set_viewsheds", "txs_site",
     "txs_get_cumulative", "txs_marginal_gains", "txs_run_pipeline", "txs_ray_template", "txs_selftest",
+    "txs_set_shard", "txs_shard_info", "txs_set_candidate_base", "txs_site_shard_begin", "txs_site_shard_best",
+    "txs_site_shard_export", "txs_site_shard_apply",
 ]

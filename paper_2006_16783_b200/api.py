@@ -219,6 +219,41 @@ class Engine:
         d["stage_ms"] = dict(vix=ms[0], findmax=ms[1], viewshed=ms[2], site=ms[3])
         return d
 
+    # ---- row-band shards --------------------------------------------
+    def set_shard(self, nrows, ncols, row_begin, row_end, halo):
+        self._chk(N.lib.txs_set_shard(self._h, nrows, ncols, row_begin, row_end, halo))
+
+    def shard_info(self):
+        a, b, c, d = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        self._chk(N.lib.txs_shard_info(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
+        return a.value, b.value, c.value, d.value
+
+    def set_candidate_base(self, gid0):
+        self._chk(N.lib.txs_set_candidate_base(self._h, gid0))
+
+    def site_shard_begin(self, params):
+        self._chk(N.lib.txs_site_shard_begin(self._h, C.byref(params)))
+
+    def site_shard_best(self):
+        k = C.c_uint64()
+        self._chk(N.lib.txs_site_shard_best(self._h, C.byref(k)))
+        return k.value
+
+    def site_shard_export(self, gid, roi):
+        owned, r, c = C.c_int32(), C.c_int32(), C.c_int32()
+        win = np.zeros(4, np.int32)
+        words = np.zeros(max_words(roi), np.uint64)
+        self._chk(N.lib.txs_site_shard_export(self._h, gid, C.byref(owned), C.byref(r), C.byref(c), _p(win),
+                                              _p(words), len(words)))
+        if not owned.value:
+            return None
+        return r.value, c.value, win, words
+
+    def site_shard_apply(self, row, col, win, words):
+        win = np.ascontiguousarray(win, np.int32)
+        words = np.ascontiguousarray(words, np.uint64)
+        self._chk(N.lib.txs_site_shard_apply(self._h, row, col, _p(win), _p(words)))
+
     def stats(self):
         s = N.Stats()
         self._chk(N.lib.txs_get_stats(self._h, C.byref(s)))

@@ -60,8 +60,9 @@ def setup_terrain(engine, cfg):
 
 def run(engine, cfg, params):
     """One end-to-end siting on the resident terrain; returns the result dict."""
+    cap = cfg.max_selected + 1 if cfg.max_selected > 0 else 1 << 20
     if cfg.random_observers:
         engine.random_observers(cfg.random_observers, cfg.observer_seed)
         engine.compute_all_viewsheds(params)
-        return engine.site(params, cap=cfg.max_selected + 1)
-    return engine.run_pipeline(params, cap=cfg.max_selected + 1)
+        return engine.site(params, cap=min(cap, cfg.random_observers + 1))
+    return engine.run_pipeline(params, cap=cap)

@@ -192,16 +192,30 @@ static txs_status set_dims(txs_ctx* c, int64_t nrows, int64_t ncols) {
         return TXS_ERR_OUT_OF_MEMORY;
     c->nrows = nrows;
     c->ncols = ncols;
+    c->sharded = false;
+    c->z_off = 0; c->z_rows = nrows; c->band_r0 = 0; c->band_r1 = nrows;
     c->vix_valid = c->cand_valid = c->vs_valid = c->site_valid = false;
     c->zt_valid = false;
     return TXS_OK;
 }
 
+static void invalidate(txs_ctx* c) {
+    c->vix_valid = c->cand_valid = c->vs_valid = c->site_valid = false;
+    c->zt_valid = false;
+}
+
 txs_status txs_set_terrain(txs_ctx* c, const int16_t* z, int64_t nrows, int64_t ncols) {
     if (!c || !z) return TXS_ERR_INVALID_ARGUMENT;
     cudaSetDevice(c->device);
-    txs_status st = set_dims(c, nrows, ncols);
-    if (st != TXS_OK) return st;
+    txs_status st = TXS_OK;
+    if (c->sharded) {
+        if (nrows != c->z_rows || ncols != c->ncols)
+            return fail(c, TXS_ERR_SIZE_MISMATCH, "read", "sharded context: terrain must be the band + halo rows");
+        invalidate(c);
+    } else {
+        st = set_dims(c, nrows, ncols);
+        if (st != TXS_OK) return st;
+    }
     StageTimer t(c, &c->stats.ms_terrain);
     const int64_t n = nrows * ncols;
     TXS_CUDA(c, "read", cudaMemcpyAsync(c->d_z, z, sizeof(int16_t) * n, cudaMemcpyHostToDevice, c->stream));
@@ -215,7 +229,10 @@ txs_status txs_set_terrain(txs_ctx* c, const int16_t* z, int64_t nrows, int64_t 
     TXS_CUDA(c, "read", cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     st = t.stop("read");
     if (st != TXS_OK) return st;
-    if (h) { c->nrows = c->ncols = 0; return fail(c, TXS_ERR_NODATA, "read", "NODATA sentinel -32768 in terrain"); }
+    if (h) {
+        if (!c->sharded) c->nrows = c->ncols = 0;
+        return fail(c, TXS_ERR_NODATA, "read", "NODATA sentinel -32768 in terrain");
+    }
     return TXS_OK;
 }
 
@@ -226,8 +243,15 @@ txs_status txs_generate_fractal(txs_ctx* c, int64_t nrows, int64_t ncols, double
     if (zmin > zmax) return fail(c, TXS_ERR_INVALID_ARGUMENT, "read", "zmin > zmax");
     if (!(roughness > 0.0) || roughness > 1.0) return fail(c, TXS_ERR_INVALID_ARGUMENT, "read", "roughness must be in (0,1]");
     if (zmin < -32767 || zmax > 32767) return fail(c, TXS_ERR_INVALID_ARGUMENT, "read", "elevations must fit int16 (no -32768)");
-    txs_status st = set_dims(c, nrows, ncols);
-    if (st != TXS_OK) return st;
+    txs_status st = TXS_OK;
+    if (c->sharded) {
+        if (nrows != c->nrows || ncols != c->ncols)
+            return fail(c, TXS_ERR_SIZE_MISMATCH, "read", "sharded context: generate the global grid dimensions");
+        invalidate(c);
+    } else {
+        st = set_dims(c, nrows, ncols);
+        if (st != TXS_OK) return st;
+    }
     StageTimer t(c, &c->stats.ms_terrain);
     st = launch_generate(c, nrows, ncols, roughness, seed, zmin, zmax);
     if (st != TXS_OK) return st;
@@ -240,16 +264,16 @@ txs_status txs_fill_rows(txs_ctx* c, int64_t rb, int64_t re, int16_t v) {
     if (rb < 0 || re > c->nrows || rb > re || v == -32768)
         return fail(c, TXS_ERR_INVALID_ARGUMENT, "read", "bad row range or value");
     cudaSetDevice(c->device);
-    c->vix_valid = c->cand_valid = c->vs_valid = c->site_valid = false;
-    c->zt_valid = false;
-    return launch_fill_rows(c, rb, re, v);
+    invalidate(c);
+    const int64_t lb = std::max(rb, c->z_off) - c->z_off, le = std::min(re, c->z_off + c->z_rows) - c->z_off;
+    return launch_fill_rows(c, lb, std::max(lb, le), v);
 }
 
 txs_status txs_get_terrain(txs_ctx* c, int16_t* z) {
     if (!c || !z) return TXS_ERR_INVALID_ARGUMENT;
     if (!c->d_z) return fail(c, TXS_ERR_STATE, "read", "no terrain");
     cudaSetDevice(c->device);
-    TXS_CUDA(c, "read", cudaMemcpyAsync(z, c->d_z, sizeof(int16_t) * c->nrows * c->ncols, cudaMemcpyDeviceToHost, c->stream));
+    TXS_CUDA(c, "read", cudaMemcpyAsync(z, c->d_z, sizeof(int16_t) * c->z_rows * c->ncols, cudaMemcpyDeviceToHost, c->stream));
     TXS_CUDA(c, "read", cudaStreamSynchronize(c->stream));
     return TXS_OK;
 }
@@ -271,7 +295,8 @@ txs_status txs_is_visible_batch(txs_ctx* c, const int32_t* pairs, int64_t n, int
     cudaSetDevice(c->device);
     for (int64_t i = 0; i < n; ++i) {
         const int32_t* p = pairs + 4 * i;
-        if (p[0] < 0 || p[0] >= c->nrows || p[2] < 0 || p[2] >= c->nrows || p[1] < 0 ||
+        const int64_t lo = c->z_off, hi = c->z_off + c->z_rows;
+        if (p[0] < lo || p[0] >= hi || p[2] < lo || p[2] >= hi || p[1] < 0 ||
             p[1] >= c->ncols || p[3] < 0 || p[3] >= c->ncols)
             return fail(c, TXS_ERR_OFF_GRID, "los", "off-grid base point");
         const int64_t dr = std::abs((int64_t)p[2] - p[0]), dc = std::abs((int64_t)p[3] - p[1]);
@@ -299,7 +324,11 @@ txs_status txs_estimate_vix(txs_ctx* c, const txs_params* p, uint8_t* scores_out
     cudaSetDevice(c->device);
     txs_status st = check_params(c, "vix", p, true);
     if (st != TXS_OK) return st;
-    if (ensure(c, "vix", (void**)&c->d_vix, &c->vix_cap, (size_t)(c->nrows * c->ncols)) != TXS_OK)
+    if (c->sharded && ((c->band_r0 - c->z_off < p->roi && c->z_off > 0) ||
+                       (c->z_off + c->z_rows - c->band_r1 < p->roi && c->z_off + c->z_rows < c->nrows)))
+        return fail(c, TXS_ERR_RANGE, "vix", "shard halo smaller than roi");
+    const int64_t band = c->band_r1 - c->band_r0;
+    if (ensure(c, "vix", (void**)&c->d_vix, &c->vix_cap, (size_t)std::max<int64_t>(1, band * c->ncols)) != TXS_OK)
         return TXS_ERR_OUT_OF_MEMORY;
     StageTimer t(c, &c->stats.ms_vix);
     st = launch_vix(c, *p);
@@ -308,7 +337,7 @@ txs_status txs_estimate_vix(txs_ctx* c, const txs_params* p, uint8_t* scores_out
     if (st != TXS_OK) return st;
     c->vix_valid = true;
     if (scores_out) {
-        TXS_CUDA(c, "vix", cudaMemcpyAsync(scores_out, c->d_vix, c->nrows * c->ncols, cudaMemcpyDeviceToHost, c->stream));
+        TXS_CUDA(c, "vix", cudaMemcpyAsync(scores_out, c->d_vix, band * c->ncols, cudaMemcpyDeviceToHost, c->stream));
         TXS_CUDA(c, "vix", cudaStreamSynchronize(c->stream));
     }
     return TXS_OK;
@@ -318,9 +347,10 @@ txs_status txs_set_vix(txs_ctx* c, const uint8_t* scores) {
     if (!c || !scores) return TXS_ERR_INVALID_ARGUMENT;
     if (!c->d_z) return fail(c, TXS_ERR_STATE, "vix", "no terrain");
     cudaSetDevice(c->device);
-    if (ensure(c, "vix", (void**)&c->d_vix, &c->vix_cap, (size_t)(c->nrows * c->ncols)) != TXS_OK)
+    const int64_t band = c->band_r1 - c->band_r0;
+    if (ensure(c, "vix", (void**)&c->d_vix, &c->vix_cap, (size_t)std::max<int64_t>(1, band * c->ncols)) != TXS_OK)
         return TXS_ERR_OUT_OF_MEMORY;
-    TXS_CUDA(c, "vix", cudaMemcpyAsync(c->d_vix, scores, c->nrows * c->ncols, cudaMemcpyHostToDevice, c->stream));
+    TXS_CUDA(c, "vix", cudaMemcpyAsync(c->d_vix, scores, band * c->ncols, cudaMemcpyHostToDevice, c->stream));
     TXS_CUDA(c, "vix", cudaStreamSynchronize(c->stream));
     c->vix_valid = true;
     return TXS_OK;
@@ -345,6 +375,8 @@ txs_status txs_find_candidates(txs_ctx* c, const txs_params* p, int64_t* n_out, 
     int64_t bw, bx, by;
     if (txs_partition(c->nrows, c->ncols, p->roi, p->block_width, &bw, &bx, &by) != TXS_OK)
         return fail(c, TXS_ERR_INVALID_ARGUMENT, "findmax", "roi < 3 with default block width");
+    if (c->sharded && (c->band_r0 % bw != 0 || (c->band_r1 % bw != 0 && c->band_r1 != c->nrows)))
+        return fail(c, TXS_ERR_INVALID_ARGUMENT, "findmax", "shard band not aligned to block rows");
     StageTimer t(c, &c->stats.ms_findmax);
     txs_status st = launch_findmax(c, *p, bw);
     if (st != TXS_OK) return st;
@@ -352,6 +384,7 @@ txs_status txs_find_candidates(txs_ctx* c, const txs_params* p, int64_t* n_out, 
     if (st != TXS_OK) return st;
     c->cand_valid = true;
     c->vs_valid = c->site_valid = false;
+    c->h_cgid.clear();
     if (n_out) *n_out = c->ncand;
     if (out) return txs_get_candidates(c, out, cap, nullptr);
     return TXS_OK;
@@ -395,8 +428,8 @@ txs_status txs_set_candidates(txs_ctx* c, const txs_candidate* in, int64_t n) {
     cudaSetDevice(c->device);
     std::vector<int32_t> r(n), cc(n), s(n);
     for (int64_t i = 0; i < n; ++i) {
-        if (in[i].row < 0 || in[i].row >= c->nrows || in[i].col < 0 || in[i].col >= c->ncols)
-            return fail(c, TXS_ERR_OFF_GRID, "viewshed", "candidate off grid");
+        if (in[i].row < c->band_r0 || in[i].row >= c->band_r1 || in[i].col < 0 || in[i].col >= c->ncols)
+            return fail(c, TXS_ERR_OFF_GRID, "viewshed", c->sharded ? "candidate outside the shard band" : "candidate off grid");
         r[i] = in[i].row; cc[i] = in[i].col; s[i] = in[i].score;
     }
     TXS_CUDA(c, "findmax", cudaStreamSynchronize(c->stream));
@@ -410,6 +443,7 @@ txs_status txs_set_candidates(txs_ctx* c, const txs_candidate* in, int64_t n) {
     c->ncand = n;
     c->cand_valid = true;
     c->vs_valid = c->site_valid = false;
+    c->h_cgid.clear();
     return TXS_OK;
 }
 
@@ -426,6 +460,22 @@ txs_status txs_random_observers(txs_ctx* c, int64_t n, uint64_t seed) {
     st = t.stop("findmax");
     if (st != TXS_OK) return st;
     c->ncand = n;
+    c->h_cgid.clear();
+    if (c->sharded && n > 0) {   // keep the band's observers, with their global draw index as id
+        std::vector<int32_t> r(n), cc(n);
+        TXS_CUDA(c, "findmax", cudaMemcpy(r.data(), c->d_crow, 4 * n, cudaMemcpyDeviceToHost));
+        TXS_CUDA(c, "findmax", cudaMemcpy(cc.data(), c->d_ccol, 4 * n, cudaMemcpyDeviceToHost));
+        std::vector<int32_t> kr, kc;
+        for (int64_t i = 0; i < n; ++i)
+            if (r[i] >= c->band_r0 && r[i] < c->band_r1) { kr.push_back(r[i]); kc.push_back(cc[i]); c->h_cgid.push_back((int32_t)i); }
+        const int64_t m = (int64_t)kr.size();
+        if (m > 0) {
+            TXS_CUDA(c, "findmax", cudaMemcpy(c->d_crow, kr.data(), 4 * m, cudaMemcpyHostToDevice));
+            TXS_CUDA(c, "findmax", cudaMemcpy(c->d_ccol, kc.data(), 4 * m, cudaMemcpyHostToDevice));
+        }
+        c->ncand = m;
+        if (m == 0) c->h_cgid.clear();
+    }
     c->cand_valid = true;
     c->vs_valid = c->site_valid = false;
     return TXS_OK;
@@ -438,6 +488,9 @@ txs_status txs_compute_viewsheds(txs_ctx* c, const txs_params* p) {
     txs_status st = check_params(c, "viewshed", p, false);
     if (st != TXS_OK) return st;
     if (!c->cand_valid) return fail(c, TXS_ERR_STATE, "viewshed", "no candidates");
+    if (c->sharded && ((c->band_r0 - c->z_off < p->roi + 1 && c->z_off > 0) ||
+                       (c->z_off + c->z_rows - c->band_r1 < p->roi + 1 && c->z_off + c->z_rows < c->nrows)))
+        return fail(c, TXS_ERR_RANGE, "viewshed", "shard halo smaller than roi + 1");
     StageTimer t(c, &c->stats.ms_viewshed);
     st = launch_viewsheds(c, *p);
     if (st != TXS_OK) return st;
@@ -528,6 +581,7 @@ txs_status txs_site(txs_ctx* c, const txs_params* p, txs_step* steps, int64_t ca
     if (!c || !p) return TXS_ERR_INVALID_ARGUMENT;
     cudaSetDevice(c->device);
     if (!c->vs_valid) return fail(c, TXS_ERR_STATE, "site", "no viewsheds");
+    if (c->sharded) return fail(c, TXS_ERR_STATE, "site", "sharded context: drive SITE with txs_site_shard_*");
     if (!(p->target_coverage > 0.0) || p->target_coverage > 1.0)
         return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "target_coverage must be in (0,1]");
     if (p->max_selected < 0) return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "max_selected < 0");
@@ -594,6 +648,85 @@ txs_status txs_run_pipeline(txs_ctx* c, const txs_params* p, txs_step* steps, in
         stage_ms[3] = c->stats.ms_site - before.ms_site;
     }
     return TXS_OK;
+}
+
+// ---- shards ------------------------------------------------------------------
+txs_status txs_set_shard(txs_ctx* c, int64_t nrows, int64_t ncols, int64_t rb, int64_t re, int32_t halo) {
+    if (!c) return TXS_ERR_INVALID_ARGUMENT;
+    if (nrows < 2 || ncols < 2 || rb < 0 || re > nrows || rb >= re || halo < 0)
+        return fail(c, TXS_ERR_INVALID_ARGUMENT, "read", "bad shard geometry");
+    cudaSetDevice(c->device);
+    TXS_CUDA(c, "read", cudaStreamSynchronize(c->stream));
+    const int64_t z0 = std::max<int64_t>(0, rb - halo), z1 = std::min<int64_t>(nrows, re + halo);
+    if (ensure(c, "read", (void**)&c->d_z, &c->z_cap, sizeof(int16_t) * (z1 - z0) * ncols) != TXS_OK)
+        return TXS_ERR_OUT_OF_MEMORY;
+    c->nrows = nrows; c->ncols = ncols;
+    c->z_off = z0; c->z_rows = z1 - z0; c->band_r0 = rb; c->band_r1 = re;
+    c->sharded = true;
+    c->cand_gid0 = 0;
+    c->h_cgid.clear();
+    invalidate(c);
+    return TXS_OK;
+}
+
+txs_status txs_shard_info(const txs_ctx* c, int64_t* h0, int64_t* hr, int64_t* b0, int64_t* b1) {
+    if (!c || !h0 || !hr || !b0 || !b1) return TXS_ERR_INVALID_ARGUMENT;
+    *h0 = c->z_off; *hr = c->z_rows; *b0 = c->band_r0; *b1 = c->band_r1;
+    return TXS_OK;
+}
+
+txs_status txs_set_candidate_base(txs_ctx* c, int64_t gid0) {
+    if (!c || gid0 < 0) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->h_cgid.empty()) return fail(c, TXS_ERR_STATE, "findmax", "candidates carry explicit global ids");
+    c->cand_gid0 = gid0;
+    c->site_valid = false;
+    return TXS_OK;
+}
+
+txs_status txs_site_shard_begin(txs_ctx* c, const txs_params* p) {
+    if (!c || !p) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->vs_valid) return fail(c, TXS_ERR_STATE, "site", "no viewsheds");
+    cudaSetDevice(c->device);
+    return shard_site_begin(c, *p);
+}
+
+txs_status txs_site_shard_best(txs_ctx* c, uint64_t* key) {
+    if (!c || !key) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->site_valid) return fail(c, TXS_ERR_STATE, "site", "call txs_site_shard_begin first");
+    cudaSetDevice(c->device);
+    return shard_site_best(c, key);
+}
+
+txs_status txs_site_shard_export(txs_ctx* c, int64_t gid, int32_t* owned, int32_t* row, int32_t* col,
+                                 txs_window* win, uint64_t* words, int64_t stride) {
+    if (!c || !owned || !row || !col || !win) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->vs_valid) return fail(c, TXS_ERR_STATE, "site", "no viewsheds");
+    int64_t li = -1;
+    if (c->h_cgid.empty()) {
+        if (gid >= c->cand_gid0 && gid < c->cand_gid0 + c->ncand) li = gid - c->cand_gid0;
+    } else {
+        auto it = std::lower_bound(c->h_cgid.begin(), c->h_cgid.end(), (int32_t)gid);
+        if (it != c->h_cgid.end() && *it == gid) li = it - c->h_cgid.begin();
+    }
+    *owned = li >= 0 ? 1 : 0;
+    if (li < 0) return TXS_OK;
+    txs_candidate cand;
+    cudaSetDevice(c->device);
+    TXS_CUDA(c, "site", cudaMemcpyAsync(&cand.row, c->d_crow + li, 4, cudaMemcpyDeviceToHost, c->stream));
+    TXS_CUDA(c, "site", cudaMemcpyAsync(&cand.col, c->d_ccol + li, 4, cudaMemcpyDeviceToHost, c->stream));
+    TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+    *row = cand.row; *col = cand.col;
+    return txs_get_viewsheds(c, li, 1, win, words, stride, nullptr);
+}
+
+txs_status txs_site_shard_apply(txs_ctx* c, int32_t row, int32_t col, const txs_window* win, const uint64_t* words) {
+    if (!c || !win || !words) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->site_valid) return fail(c, TXS_ERR_STATE, "site", "call txs_site_shard_begin first");
+    if (win->row0 < 0 || win->col0 < 0 || win->h < 1 || win->w < 1 || win->row0 + win->h > c->nrows ||
+        win->col0 + win->w > c->ncols)
+        return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "window out of bounds");
+    cudaSetDevice(c->device);
+    return shard_site_apply(c, row, col, *win, words);
 }
 
 int txs_selftest(void) {

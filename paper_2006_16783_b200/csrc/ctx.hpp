@@ -59,6 +59,7 @@ struct SiteState {
     int nb_count;
     int nb_start[kMaxNb];
     int nb_pref[kMaxNb + 1];
+    unsigned long long shard_key;  // sharded SITE: local best key
 };
 
 // device counter slots
@@ -74,10 +75,15 @@ struct txs_ctx {
     std::string err;
     int num_sms = 148;
 
-    // terrain: row-major int16 in HBM
+    // terrain: row-major int16 in HBM.  nrows/ncols are the
+    // GLOBAL grid; the context holds rows [z_off, z_off + z_rows) of it (all of
+    // it unless sharded) and owns the band [band_r0, band_r1).
     int64_t nrows = 0, ncols = 0;
     int16_t* d_z = nullptr;
     size_t z_cap = 0;
+    int64_t z_off = 0, z_rows = 0, band_r0 = 0, band_r1 = 0;
+    bool sharded = false;
+    const int16_t* zv() const { return d_z - z_off * ncols; }   // indexed by global row
     int16_t* d_zt = nullptr;      // column-major copy (VIX global path)
     size_t zt_cap = 0;
     bool zt_valid = false;
@@ -87,8 +93,13 @@ struct txs_ctx {
     size_t vix_cap = 0;
     bool vix_valid = false;
 
-    // candidates, in candidate-index order
+    // candidates, in candidate-index order; global id of local
+    // candidate i = cand_gid0 + i, or h_cgid[i] when set (sharded random observers)
     int64_t ncand = 0;
+    int64_t cand_gid0 = 0;
+    std::vector<int32_t> h_cgid;
+    int32_t* d_cgid = nullptr;
+    size_t cgid_cap = 0;
     int32_t *d_crow = nullptr, *d_ccol = nullptr, *d_cscore = nullptr;
     size_t cand_cap = 0;
     bool cand_valid = false;
@@ -104,8 +115,12 @@ struct txs_ctx {
     bool vs_valid = false;
     std::map<int32_t, txs::RayTemplateDev> templates;
 
-    // SITE: row-padded bitmaps (wpr words per terrain row)
+    // SITE: row-padded bitmaps (wpr words per terrain row) over
+    // the cum region rows [cum_r0, cum_r1) (whole grid unless sharded)
     int64_t wpr = 0;
+    int64_t cum_r0 = 0, cum_r1 = 0;
+    uint64_t* d_xfer = nullptr;          // sharded SITE: the broadcast winner window
+    size_t xfer_cap = 0;
     uint64_t* d_cum = nullptr;
     txs::DeltaWord* d_dlist = nullptr;
     size_t dlist_cap = 0;
@@ -143,7 +158,7 @@ inline int64_t max_window_words(int64_t roi) { return ((2 * roi + 1) * (2 * roi 
 
 // stage launchers (one .cu each)
 txs_status launch_generate(txs_ctx*, int64_t nrows, int64_t ncols, double roughness, uint64_t seed,
-                           int32_t zmin, int32_t zmax);
+                           int32_t zmin, int32_t zmax);   // writes held rows [z_off, z_off+z_rows)
 txs_status launch_fill_rows(txs_ctx*, int64_t rb, int64_t re, int16_t v);
 txs_status launch_vix(txs_ctx*, const txs_params& p);
 txs_status launch_los_batch(txs_ctx*, const int32_t* d_pairs, int64_t n, int32_t ht, int32_t hr,
@@ -154,6 +169,9 @@ txs_status launch_viewsheds(txs_ctx*, const txs_params& p);
 txs_status run_site(txs_ctx*, const txs_params& p, std::vector<txs_step>& steps, int32_t* stop);
 txs_status launch_marginal_gains(txs_ctx*, const uint64_t* d_cum_dense, int64_t* d_gains);
 txs_status download_cum(txs_ctx*, uint64_t* host_dense);
+txs_status shard_site_begin(txs_ctx*, const txs_params& p);
+txs_status shard_site_best(txs_ctx*, uint64_t* key);
+txs_status shard_site_apply(txs_ctx*, int32_t row, int32_t col, const txs_window& win, const uint64_t* words);
 
 }  // namespace txs
 

@@ -17,7 +17,7 @@ constexpr int kFmWarps = kFmThreads / 32;
 constexpr int kMaxPerBlock = 8192;
 
 struct FmArgs {
-    int nrows, ncols, bw, bx_count, k;
+    int nrows, ncols, bw, bx_count, k, by0;   // by0: first block row of the band
     int64_t row_total_full;   // candidates of one full-height block row
 };
 
@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(kFmThreads) k_findmax(const uint8_t* __restric
     extern __shared__ int2 s_list[];   // (score, linear index) of posts above theta
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int by = blockIdx.x / a.bx_count, bxi = blockIdx.x % a.bx_count;
-    const int r0 = by * a.bw, c0 = bxi * a.bw;
+    const int r0 = (a.by0 + by) * a.bw, c0 = bxi * a.bw;
     const int h = min(a.bw, a.nrows - r0), w = min(a.bw, a.ncols - c0), n = h * w;
     const int kk = min(a.k, n);
     const int64_t out0 = (int64_t)by * a.row_total_full + (int64_t)bxi * min(a.k, h * a.bw);
@@ -113,13 +113,14 @@ txs_status launch_findmax(txs_ctx* c, const txs_params& p, int64_t bw) {
     FmArgs a;
     a.nrows = (int)c->nrows; a.ncols = (int)c->ncols; a.bw = (int)bw; a.k = p.per_block;
     a.bx_count = (int)((c->ncols + bw - 1) / bw);
-    const int64_t by_count = (c->nrows + bw - 1) / bw;
+    a.by0 = (int)(c->band_r0 / bw);
+    const int64_t by_count = (c->band_r1 - c->band_r0 + bw - 1) / bw;
     const int64_t wlast = c->ncols - (int64_t)(a.bx_count - 1) * bw;
     auto row_total = [&](int64_t h) {
         return (int64_t)(a.bx_count - 1) * std::min<int64_t>(a.k, h * bw) + std::min<int64_t>(a.k, h * wlast);
     };
     a.row_total_full = row_total(bw);
-    const int64_t hlast = c->nrows - (by_count - 1) * bw;
+    const int64_t hlast = std::min<int64_t>(bw, c->nrows - (a.by0 + by_count - 1) * bw);
     const int64_t n = (by_count - 1) * a.row_total_full + row_total(hlast);
     const int64_t nblocks = by_count * a.bx_count;
     if (nblocks > 0x7fffffff || n >= 0x7fffffff) return fail(c, TXS_ERR_RANGE, "findmax", "too many blocks");
@@ -134,7 +135,8 @@ txs_status launch_findmax(txs_ctx* c, const txs_params& p, int64_t bw) {
     const size_t smem = sizeof(int2) * (size_t)std::max(1, std::min<int>(a.k, a.bw * a.bw));
     if (smem > 48 * 1024)
         TXS_CUDA(c, "findmax", cudaFuncSetAttribute(k_findmax, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_findmax<<<(unsigned)nblocks, kFmThreads, smem, c->stream>>>(c->d_vix, a, c->d_crow, c->d_ccol, c->d_cscore);
+    k_findmax<<<(unsigned)nblocks, kFmThreads, smem, c->stream>>>(c->d_vix - c->band_r0 * c->ncols, a, c->d_crow,
+                                                                  c->d_ccol, c->d_cscore);
     TXS_LAUNCHED(c, "findmax");
     c->ncand = n;
     return TXS_OK;

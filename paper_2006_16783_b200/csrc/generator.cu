@@ -55,11 +55,12 @@ __global__ void k_square(int32_t* __restrict__ cv, int64_t N, int64_t s, uint64_
     }
 }
 
-__global__ void k_crop(const int32_t* __restrict__ cv, int64_t N, int16_t* __restrict__ z, int64_t nrows,
+// crop held rows [row0, row0 + rows) of the canvas into z (rows x ncols)
+__global__ void k_crop(const int32_t* __restrict__ cv, int64_t N, int16_t* __restrict__ z, int64_t row0, int64_t rows,
                        int64_t ncols, int64_t zmin, int64_t zmax) {
-    const int64_t range = zmax - zmin, mid = zmin + range / 2, total = nrows * ncols;
+    const int64_t range = zmax - zmin, mid = zmin + range / 2, total = rows * ncols;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t y = t / ncols, x = t - y * ncols;
+        const int64_t y = row0 + t / ncols, x = t % ncols;
         int64_t v = mid + floordiv64((int64_t)cv[y * N + x] * range, (int64_t)1 << 21);
         v = v < zmin ? zmin : (v > zmax ? zmax : v);
         z[t] = (int16_t)v;
@@ -99,7 +100,7 @@ txs_status launch_generate(txs_ctx* c, int64_t nrows, int64_t ncols, double roug
         k_square<<<grid_for(work, c->num_sms), 256, 0, c->stream>>>(cv, N, s, seed, A, mod_for(A));
         TXS_LAUNCHED(c, "read");
     }
-    k_crop<<<grid_for(nrows * ncols, c->num_sms), 256, 0, c->stream>>>(cv, N, c->d_z, nrows, ncols, zmin, zmax);
+    k_crop<<<grid_for(c->z_rows * ncols, c->num_sms), 256, 0, c->stream>>>(cv, N, c->d_z, c->z_off, c->z_rows, ncols, zmin, zmax);
     TXS_LAUNCHED(c, "read");
     TXS_CUDA(c, "read", cudaFreeAsync(cv, c->stream));
     return TXS_OK;

@@ -33,6 +33,7 @@ constexpr unsigned kFull = 0xffffffffu;
 
 struct SiteArgs {
     int nrows, ncols, R, bsize, nbx, nby;
+    int cr0, cr1;                     // cum region rows held [cr0, cr1)
     int64_t wpr, n, stride, max_sel;
     double target, total;
 };
@@ -167,15 +168,17 @@ __global__ void k_argmax(const int32_t* __restrict__ gain, SiteArgs a, SiteState
 
 // Newly covered bits of the winner: d = v_w & ~cum per cum word of its window;
 // cum |= d; non-zero d words appended to the delta list for k_update.
+// (sharded: the window comes from `xfer` and only the held cum rows are touched)
 __global__ void k_commit(SiteArgs a, SiteState* st, const uint64_t* __restrict__ words, uint64_t* __restrict__ cum,
-                         DeltaWord* __restrict__ dlist) {
+                         DeltaWord* __restrict__ dlist, const uint64_t* __restrict__ xfer) {
     if (st->done) return;
     const int idx = st->w_idx;
     const int r0 = st->w_row0, c0 = st->w_col0, h = st->w_h, w = st->w_w;
-    const uint64_t* v = words + (int64_t)idx * a.stride;
+    const uint64_t* v = xfer ? xfer : words + (int64_t)idx * a.stride;
     const int wlo = c0 >> 6, nwr = ((c0 + w - 1) >> 6) - wlo + 1;
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < h * nwr; t += gridDim.x * blockDim.x) {
-        const int y = r0 + t / nwr, wi = wlo + t % nwr;
+    const int ya = max(r0, a.cr0), yb = min(r0 + h, a.cr1);   // held rows of the window
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < (yb - ya) * nwr; t += gridDim.x * blockDim.x) {
+        const int y = ya + t / nwr, wi = wlo + t % nwr;
         const uint64_t m = col_mask(wi, c0, c0 + w - 1);
         const long long off = (long long)(y - r0) * w + (wi * 64 - c0);
         const int64_t o = (int64_t)y * a.wpr + wi;
@@ -280,8 +283,9 @@ __global__ void k_dense_to_padded(const uint64_t* __restrict__ dense, uint64_t* 
     }
 }
 
+// pad is indexed by global row; rows outside [cr0, cr1) read as zero
 __global__ void k_padded_to_dense(const uint64_t* __restrict__ pad, uint64_t* __restrict__ dense, int64_t nrows,
-                                  int64_t ncols, int64_t wpr) {
+                                  int64_t ncols, int64_t wpr, int64_t cr0, int64_t cr1) {
     const int64_t total = nrows * ncols, nw = (total + 63) >> 6;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nw; t += (int64_t)gridDim.x * blockDim.x) {
         uint64_t v = 0;
@@ -292,8 +296,11 @@ __global__ void k_padded_to_dense(const uint64_t* __restrict__ pad, uint64_t* __
             const int64_t len = min(b1 - b, ncols - x);
             const int64_t pw = x >> 6;
             const int s = (int)(x & 63);
-            uint64_t seg = pad[y * wpr + pw] >> s;
-            if (s && pw + 1 < wpr) seg |= pad[y * wpr + pw + 1] << (64 - s);
+            uint64_t seg = 0;
+            if (y >= cr0 && y < cr1) {
+                seg = pad[y * wpr + pw] >> s;
+                if (s && pw + 1 < wpr) seg |= pad[y * wpr + pw + 1] << (64 - s);
+            }
             if (len < 64) seg &= (1ull << len) - 1;
             v |= seg << (b - b0);
             b += len;
@@ -314,12 +321,16 @@ SiteArgs make_args(txs_ctx* c, const txs_params& p) {
     a.max_sel = p.max_selected;
     a.target = p.target_coverage;
     a.total = (double)c->nrows * (double)c->ncols;
+    a.cr0 = (int)c->cum_r0; a.cr1 = (int)c->cum_r1;
     return a;
 }
 
-txs_status alloc_bitmaps(txs_ctx* c) {
+// cum over the held region rows [r0, r1) (whole grid unless sharded) + delta list
+txs_status alloc_bitmaps(txs_ctx* c, int64_t r0, int64_t r1) {
     c->wpr = (c->ncols + 63) / 64;
-    const size_t bytes = sizeof(uint64_t) * (size_t)(c->nrows * c->wpr + 1);
+    c->cum_r0 = r0;
+    c->cum_r1 = r1;
+    const size_t bytes = sizeof(uint64_t) * (size_t)((r1 - r0) * c->wpr + 1);
     if (ensure(c, "site", (void**)&c->d_cum, &c->bitmap_cap, bytes) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
     // delta list: at most one entry per cum word of a full window
     const int64_t side = 2 * (int64_t)std::max(1, c->vs_roi) + 1;
@@ -332,13 +343,33 @@ int blocks_for(int64_t work, int per_block, int cap) {
     return (int)std::max<int64_t>(1, std::min<int64_t>((work + per_block - 1) / per_block, cap));
 }
 
+// gains <- popcounts; CSR buckets (side roi) over the candidates' positions
+txs_status init_gains_buckets(txs_ctx* c, const SiteArgs& a, void* d_scan_tmp, size_t scan_bytes) {
+    const int64_t n = a.n, nbk = (int64_t)a.nbx * a.nby;
+    const int sms = c->num_sms;
+    if (n == 0) return TXS_OK;
+    k_init_gains<<<blocks_for(n, 256, sms * 8), 256, 0, c->stream>>>(c->d_pop, c->d_gain, n);
+    TXS_LAUNCHED(c, "site");
+    int32_t* counts = c->d_bucket_start;            // nbk+1
+    int32_t* cursor = c->d_bucket_start + nbk + 1;  // nbk+1
+    TXS_CUDA(c, "site", cudaMemsetAsync(counts, 0, sizeof(int32_t) * (nbk + 1), c->stream));
+    k_bucket_count<<<blocks_for(n, 256, sms * 8), 256, 0, c->stream>>>(c->d_crow, c->d_ccol, n, a.bsize, a.nbx, counts);
+    TXS_LAUNCHED(c, "site");
+    TXS_CUDA(c, "site", cub::DeviceScan::ExclusiveSum(d_scan_tmp, scan_bytes, counts, cursor, (int)(nbk + 1), c->stream));
+    TXS_CUDA(c, "site", cudaMemcpyAsync(counts, cursor, sizeof(int32_t) * (nbk + 1), cudaMemcpyDeviceToDevice, c->stream));
+    k_bucket_fill<<<blocks_for(n, 256, sms * 8), 256, 0, c->stream>>>(c->d_crow, c->d_ccol, n, a.bsize, a.nbx, cursor, c->d_bucket_items);
+    TXS_LAUNCHED(c, "site");
+    return TXS_OK;
+}
+
 }  // namespace
 
 txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out, int32_t* stop) {
+    TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+    if (alloc_bitmaps(c, 0, c->nrows) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
     const SiteArgs a = make_args(c, p);
     const int64_t n = a.n;
-    TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
-    if (alloc_bitmaps(c) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
+    uint64_t* cumv = c->d_cum;   // region starts at row 0
     if (ensure(c, "site", (void**)&c->d_gain, &c->gain_cap, sizeof(int32_t) * std::max<int64_t>(1, n)) != TXS_OK)
         return TXS_ERR_OUT_OF_MEMORY;
     const int64_t nbk = (int64_t)a.nbx * a.nby;
@@ -354,24 +385,11 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
     d_steps = (txs_step*)c->d_scratch;
     void* d_scan_tmp = (char*)c->d_scratch + ((steps_bytes + 255) / 256) * 256;
 
-    const size_t bm = sizeof(uint64_t) * (size_t)(c->nrows * c->wpr + 1);
+    const size_t bm = sizeof(uint64_t) * (size_t)((c->cum_r1 - c->cum_r0) * c->wpr + 1);
     TXS_CUDA(c, "site", cudaMemsetAsync(c->d_cum, 0, bm, c->stream));
     TXS_CUDA(c, "site", cudaMemsetAsync(c->d_state, 0, sizeof(SiteState), c->stream));
     const int sms = c->num_sms;
-    if (n > 0) {
-        k_init_gains<<<blocks_for(n, 256, sms * 8), 256, 0, c->stream>>>(c->d_pop, c->d_gain, n);
-        TXS_LAUNCHED(c, "site");
-        // CSR buckets over candidate positions
-        int32_t* counts = c->d_bucket_start;          // nbk+1
-        int32_t* cursor = c->d_bucket_start + nbk + 1; // nbk+1
-        TXS_CUDA(c, "site", cudaMemsetAsync(counts, 0, sizeof(int32_t) * (nbk + 1), c->stream));
-        k_bucket_count<<<blocks_for(n, 256, sms * 8), 256, 0, c->stream>>>(c->d_crow, c->d_ccol, n, a.bsize, a.nbx, counts);
-        TXS_LAUNCHED(c, "site");
-        TXS_CUDA(c, "site", cub::DeviceScan::ExclusiveSum(d_scan_tmp, scan_bytes, counts, cursor, (int)(nbk + 1), c->stream));
-        TXS_CUDA(c, "site", cudaMemcpyAsync(counts, cursor, sizeof(int32_t) * (nbk + 1), cudaMemcpyDeviceToDevice, c->stream));
-        k_bucket_fill<<<blocks_for(n, 256, sms * 8), 256, 0, c->stream>>>(c->d_crow, c->d_ccol, n, a.bsize, a.nbx, cursor, c->d_bucket_items);
-        TXS_LAUNCHED(c, "site");
-    }
+    if (init_gains_buckets(c, a, d_scan_tmp, scan_bytes) != TXS_OK) return TXS_ERR_CUDA;
     // graph of kRoundsPerGraph rounds
     const int am_blocks = blocks_for(n, 256 * 4, sms * 2);
     const int cm_blocks = 16;
@@ -383,9 +401,9 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
     TXS_CUDA(c, "site", cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     for (int r = 0; r < kRoundsPerGraph; ++r) {
         if (p.site_mode == 1)
-            k_gain_full<int32_t><<<full_blocks, 256, 0, c->stream>>>(a, c->d_state, c->d_win, c->d_words, c->d_cum, c->d_gain, c->d_counters);
+            k_gain_full<int32_t><<<full_blocks, 256, 0, c->stream>>>(a, c->d_state, c->d_win, c->d_words, cumv, c->d_gain, c->d_counters);
         k_argmax<<<am_blocks, 256, 0, c->stream>>>(c->d_gain, a, c->d_state, lp);
-        k_commit<<<cm_blocks, 256, 0, c->stream>>>(a, c->d_state, c->d_words, c->d_cum, c->d_dlist);
+        k_commit<<<cm_blocks, 256, 0, c->stream>>>(a, c->d_state, c->d_words, cumv, c->d_dlist, nullptr);
         if (p.site_mode != 1)
             k_update<<<up_blocks, kUpdThreads, 0, c->stream>>>(a, c->d_state, c->d_win, c->d_words, c->d_dlist,
                                                                c->d_bucket_items, c->d_gain, c->d_counters);
@@ -426,8 +444,9 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
 txs_status launch_marginal_gains(txs_ctx* c, const uint64_t* d_cum_dense, int64_t* d_gains) {
     txs_params p{};
     p.target_coverage = 1.0;
-    const SiteArgs a = make_args(c, p);
-    if (alloc_bitmaps(c) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
+    SiteArgs a = make_args(c, p);
+    a.cr0 = 0; a.cr1 = (int)c->nrows;
+    c->wpr = (c->ncols + 63) / 64;
     uint64_t* pad = nullptr;
     TXS_CUDA(c, "site", cudaMallocAsync((void**)&pad, sizeof(uint64_t) * (size_t)(c->nrows * c->wpr + 1), c->stream));
     k_dense_to_padded<<<blocks_for(c->nrows * c->wpr, 256, c->num_sms * 16), 256, 0, c->stream>>>(d_cum_dense, pad, c->nrows, c->ncols, c->wpr);
@@ -444,11 +463,119 @@ txs_status download_cum(txs_ctx* c, uint64_t* host_dense) {
     const int64_t nw = (c->nrows * c->ncols + 63) / 64;
     uint64_t* dense = nullptr;
     TXS_CUDA(c, "site", cudaMallocAsync((void**)&dense, sizeof(uint64_t) * nw, c->stream));
-    k_padded_to_dense<<<blocks_for(nw, 256, c->num_sms * 16), 256, 0, c->stream>>>(c->d_cum, dense, c->nrows, c->ncols, c->wpr);
+    k_padded_to_dense<<<blocks_for(nw, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+        c->d_cum - c->cum_r0 * c->wpr, dense, c->nrows, c->ncols, c->wpr, c->cum_r0, c->cum_r1);
     TXS_LAUNCHED(c, "site");
     TXS_CUDA(c, "site", cudaMemcpyAsync(host_dense, dense, sizeof(uint64_t) * nw, cudaMemcpyDeviceToHost, c->stream));
     TXS_CUDA(c, "site", cudaFreeAsync(dense, c->stream));
     TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+    return TXS_OK;
+}
+
+// ---- sharded SITE rounds -------------------------------------------
+namespace {
+
+__global__ void k_shard_best(const int32_t* __restrict__ gain, const int32_t* __restrict__ cgid, int64_t gid0,
+                             int64_t n, SiteState* st) {
+    __shared__ unsigned long long s_red[32];
+    unsigned long long best = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t gid = cgid ? (uint64_t)cgid[i] : (uint64_t)(gid0 + i);
+        best = umax64(best, ((unsigned long long)(uint32_t)gain[i] << 32) | (0xffffffffull - gid));
+    }
+    for (int o = 16; o; o >>= 1) best = umax64(best, __shfl_xor_sync(kFull, best, o));
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < (int)(blockDim.x >> 5); ++k) best = umax64(best, s_red[k]);
+        best = umax64(best, s_red[0]);
+        if (best) atomicMax(&st->shard_key, best);
+    }
+}
+
+__global__ void k_shard_prep(SiteArgs a, SiteState* st, int r, int c, int4 win, const int32_t* __restrict__ bstart) {
+    st->done = 0; st->finish = 0; st->dcount = 0; st->w_idx = -1;
+    st->w_row0 = win.x; st->w_col0 = win.y; st->w_h = win.z; st->w_w = win.w;
+    const int by0 = max(0, (r - 2 * a.R) / a.bsize), by1 = min(a.nby - 1, (r + 2 * a.R) / a.bsize);
+    const int bx0 = max(0, (c - 2 * a.R) / a.bsize), bx1 = min(a.nbx - 1, (c + 2 * a.R) / a.bsize);
+    int nb = 0, pref = 0;
+    for (int by = by0; by <= by1 && nb < kMaxNb; ++by) {
+        const int s0 = bstart[by * a.nbx + bx0], e0 = bstart[by * a.nbx + bx1 + 1];
+        st->nb_start[nb] = s0;
+        st->nb_pref[nb] = pref;
+        pref += e0 - s0;
+        ++nb;
+    }
+    st->nb_pref[nb] = pref;
+    st->nb_count = nb;
+}
+
+}  // namespace
+
+txs_status shard_site_begin(txs_ctx* c, const txs_params& p) {
+    TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+    const int64_t R = c->vs_roi;
+    if (alloc_bitmaps(c, std::max<int64_t>(0, c->band_r0 - R), std::min<int64_t>(c->nrows, c->band_r1 + R)) != TXS_OK)
+        return TXS_ERR_OUT_OF_MEMORY;
+    const SiteArgs a = make_args(c, p);
+    const int64_t n = a.n, nbk = (int64_t)a.nbx * a.nby;
+    if (ensure(c, "site", (void**)&c->d_gain, &c->gain_cap, sizeof(int32_t) * std::max<int64_t>(1, n)) != TXS_OK ||
+        ensure(c, "site", (void**)&c->d_bucket_start, &c->bucket_cap, sizeof(int32_t) * (nbk + 1) * 2) != TXS_OK ||
+        ensure(c, "site", (void**)&c->d_bucket_items, &c->bucket_items_cap, sizeof(int32_t) * std::max<int64_t>(1, n)) != TXS_OK)
+        return TXS_ERR_OUT_OF_MEMORY;
+    size_t scan_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int32_t*)nullptr, (int32_t*)nullptr, (int)(nbk + 1));
+    if (ensure(c, "site", &c->d_scratch, &c->scratch_cap, scan_bytes + 256) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
+    TXS_CUDA(c, "site", cudaMemsetAsync(c->d_cum, 0, sizeof(uint64_t) * ((c->cum_r1 - c->cum_r0) * c->wpr + 1), c->stream));
+    TXS_CUDA(c, "site", cudaMemsetAsync(c->d_state, 0, sizeof(SiteState), c->stream));
+    if (init_gains_buckets(c, a, c->d_scratch, scan_bytes) != TXS_OK) return TXS_ERR_CUDA;
+    if (!c->h_cgid.empty()) {
+        if (ensure(c, "site", (void**)&c->d_cgid, &c->cgid_cap, sizeof(int32_t) * c->h_cgid.size()) != TXS_OK)
+            return TXS_ERR_OUT_OF_MEMORY;
+        TXS_CUDA(c, "site", cudaMemcpyAsync(c->d_cgid, c->h_cgid.data(), sizeof(int32_t) * c->h_cgid.size(),
+                                            cudaMemcpyHostToDevice, c->stream));
+    }
+    const int64_t mw = max_window_words(R) + 2;
+    if (ensure(c, "site", (void**)&c->d_xfer, &c->xfer_cap, sizeof(uint64_t) * mw) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
+    TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+    c->site_valid = true;
+    return TXS_OK;
+}
+
+txs_status shard_site_best(txs_ctx* c, uint64_t* key) {
+    const int64_t n = c->vs_n;
+    TXS_CUDA(c, "site", cudaMemsetAsync(&c->d_state->shard_key, 0, sizeof(unsigned long long), c->stream));
+    if (n > 0) {
+        k_shard_best<<<blocks_for(n, 1024, c->num_sms * 2), 256, 0, c->stream>>>(
+            c->d_gain, c->h_cgid.empty() ? nullptr : c->d_cgid, c->cand_gid0, n, c->d_state);
+        TXS_LAUNCHED(c, "site");
+    }
+    unsigned long long k = 0;
+    TXS_CUDA(c, "site", cudaMemcpyAsync(&k, &c->d_state->shard_key, sizeof(k), cudaMemcpyDeviceToHost, c->stream));
+    TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+    *key = k;
+    return TXS_OK;
+}
+
+txs_status shard_site_apply(txs_ctx* c, int32_t row, int32_t col, const txs_window& win, const uint64_t* words) {
+    txs_params p{};
+    p.target_coverage = 1.0;
+    const SiteArgs a = make_args(c, p);
+    const int64_t nw = ((int64_t)win.h * win.w + 63) / 64;
+    if (nw + 2 > (int64_t)(c->xfer_cap / sizeof(uint64_t)))
+        return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "window larger than the engine's roi");
+    TXS_CUDA(c, "site", cudaMemcpyAsync(c->d_xfer, words, sizeof(uint64_t) * nw, cudaMemcpyHostToDevice, c->stream));
+    TXS_CUDA(c, "site", cudaMemsetAsync(c->d_xfer + nw, 0, sizeof(uint64_t) * 2, c->stream));
+    k_shard_prep<<<1, 1, 0, c->stream>>>(a, c->d_state, row, col, make_int4(win.row0, win.col0, win.h, win.w),
+                                        c->d_bucket_start);
+    TXS_LAUNCHED(c, "site");
+    uint64_t* cumv = c->d_cum - c->cum_r0 * c->wpr;
+    k_commit<<<16, 256, 0, c->stream>>>(a, c->d_state, c->d_words, cumv, c->d_dlist, c->d_xfer);
+    TXS_LAUNCHED(c, "site");
+    k_update<<<c->num_sms * 8, kUpdThreads, 0, c->stream>>>(a, c->d_state, c->d_win, c->d_words, c->d_dlist,
+                                                           c->d_bucket_items, c->d_gain, c->d_counters);
+    TXS_LAUNCHED(c, "site");
+    c->stats.site_iterations += 1;
     return TXS_OK;
 }
 

@@ -309,11 +309,11 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
         if (smem_bits) {
             if (smem > 48 * 1024)
                 TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(k_viewshed_ev<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            k_viewshed_ev<true><<<(unsigned)n, threads, smem, c->stream>>>(c->d_z, c->d_crow, c->d_ccol, T->rays, T->groups,
+            k_viewshed_ev<true><<<(unsigned)n, threads, smem, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups,
                                                                           T->events, T->ngroups, a, c->d_words, c->d_win,
                                                                           c->d_pop, c->d_counters);
         } else {
-            k_viewshed_ev<false><<<(unsigned)n, threads, 0, c->stream>>>(c->d_z, c->d_crow, c->d_ccol, T->rays, T->groups,
+            k_viewshed_ev<false><<<(unsigned)n, threads, 0, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups,
                                                                         T->events, T->ngroups, a, c->d_words, c->d_win,
                                                                         c->d_pop, c->d_counters);
         }
@@ -323,10 +323,10 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
         if (smem_bits) {
             if (smem > 48 * 1024)
                 TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(k_viewshed<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            k_viewshed<true><<<(unsigned)n, threads, smem, c->stream>>>(c->d_z, c->d_crow, c->d_ccol, T->rays, T->cells, a,
+            k_viewshed<true><<<(unsigned)n, threads, smem, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->cells, a,
                                                                         c->d_words, c->d_win, c->d_pop, c->d_counters);
         } else {
-            k_viewshed<false><<<(unsigned)n, threads, 0, c->stream>>>(c->d_z, c->d_crow, c->d_ccol, T->rays, T->cells, a,
+            k_viewshed<false><<<(unsigned)n, threads, 0, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->cells, a,
                                                                      c->d_words, c->d_win, c->d_pop, c->d_counters);
         }
     }

@@ -131,6 +131,8 @@ struct VixArgs {
     uint64_t seed;
     FastMod64 span;   // 2R+1
     int tiles_x;
+    int row0, row_end;   // band rows [row0, row_end)
+    int zr0, zr1;        // held terrain rows [zr0, zr1)
 };
 
 template <bool SMEM, int ILP>
@@ -142,10 +144,10 @@ __global__ void __launch_bounds__(kVixThreads, 2) k_vix(const int16_t* __restric
     int* s_samp = (int*)s_dyn + warp_of_thread() * a.S;
     int16_t* s_tile = (int16_t*)((int*)s_dyn + kVixWarps * a.S + 4);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int ty0 = (blockIdx.x / a.tiles_x) * kTile, tx0 = (blockIdx.x % a.tiles_x) * kTile;
+    const int ty0 = a.row0 + (blockIdx.x / a.tiles_x) * kTile, tx0 = (blockIdx.x % a.tiles_x) * kTile;
     TerrainView T{z, nullptr, ncols, 0, 0, 0};
     if (SMEM) {
-        const int r0 = max(0, ty0 - a.R), r1 = min(nrows - 1, ty0 + kTile - 1 + a.R);
+        const int r0 = max(a.zr0, ty0 - a.R), r1 = min(a.zr1 - 1, ty0 + kTile - 1 + a.R);
         const int c0 = max(0, tx0 - a.R), c1 = min(ncols - 1, tx0 + kTile - 1 + a.R);
         const int sh = r1 - r0 + 1, sw = c1 - c0 + 1;
         for (int i = threadIdx.x; i < sh * sw; i += kVixThreads) {
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(kVixThreads, 2) k_vix(const int16_t* __restric
     unsigned long long n_los = 0, n_cross = 0;
     for (int pi = warp; pi < kTile * kTile; pi += kVixWarps) {
         const int r = ty0 + pi / kTile, c = tx0 + pi % kTile;
-        if (r >= nrows || c >= ncols) continue;
+        if (r >= a.row_end || c >= ncols) continue;
         const uint64_t base = mix_seed(a.seed, (uint64_t)r, (uint64_t)c);
         const int E = T.at(r, c) + a.ht;
         // ---- draw S receivers (D6) ----
@@ -194,12 +196,12 @@ __global__ void __launch_bounds__(kVixThreads, 2) k_vix(const int16_t* __restric
             const int stride = SMEM ? T.sw : ncols;
             // global path: walk row-major segments on the column-major copy so the
             // lanes' consecutive major steps are contiguous in memory
-            const int16_t* PT = SMEM ? P : zt + (int64_t)c * nrows + r;
+            const int16_t* PT = SMEM ? P : zt + (int64_t)c * (a.zr1 - a.zr0) + (r - a.zr0);
             for (int sidx = 0; sidx < ns; ++sidx) {
                 const int dr = __shfl_sync(kFull, my_dr, sidx), dc = __shfl_sync(kFull, my_dc, sidx);
                 const int Zt = __shfl_sync(kFull, my_zt, sidx);
                 const bool tr = !SMEM && abs(dr) > abs(dc);
-                const bool blk = tr ? warp_blocked<SMEM, ILP>(PT, nrows, dc, dr, E, Zt, lane)
+                const bool blk = tr ? warp_blocked<SMEM, ILP>(PT, a.zr1 - a.zr0, dc, dr, E, Zt, lane)
                                     : warp_blocked<SMEM, ILP>(P, stride, dr, dc, E, Zt, lane);
                 vis += blk ? 0 : 1;
             }
@@ -251,7 +253,9 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     a.seed = p.seed;
     a.span = make_fastmod((uint64_t)(2 * p.roi + 1));
     a.tiles_x = (int)((c->ncols + kTile - 1) / kTile);
-    const int64_t tiles = a.tiles_x * ((c->nrows + kTile - 1) / kTile);
+    a.row0 = (int)c->band_r0; a.row_end = (int)c->band_r1;
+    a.zr0 = (int)c->z_off; a.zr1 = (int)(c->z_off + c->z_rows);
+    const int64_t tiles = a.tiles_x * ((c->band_r1 - c->band_r0 + kTile - 1) / kTile);
     if (tiles > 0x7fffffff) return fail(c, TXS_ERR_RANGE, "vix", "grid too large");
     const int64_t side = kTile + 2 * (int64_t)p.roi;
     const size_t samp = sizeof(int) * (kVixWarps * (size_t)a.S + 4);
@@ -260,7 +264,8 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     // steps walked from the transmitter) beat 2 and 4 and receiver-first walks
     auto go = [&](auto kern, size_t sm) -> txs_status {
         if (sm > 48 * 1024) TXS_CUDA(c, "vix", cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        kern<<<(unsigned)tiles, kVixThreads, sm, c->stream>>>(c->d_z, c->d_zt, (int)c->nrows, (int)c->ncols, c->d_vix, a, c->d_counters);
+        kern<<<(unsigned)tiles, kVixThreads, sm, c->stream>>>(c->zv(), c->d_zt, (int)c->nrows, (int)c->ncols,
+                                                              c->d_vix - c->band_r0 * c->ncols, a, c->d_counters);
         return TXS_OK;
     };
     txs_status st;
@@ -268,10 +273,10 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         st = go(k_vix<true, 1>, smem);
     } else {
         if (!c->zt_valid) {
-            if (ensure(c, "vix", (void**)&c->d_zt, &c->zt_cap, sizeof(int16_t) * c->nrows * c->ncols) != TXS_OK)
+            if (ensure(c, "vix", (void**)&c->d_zt, &c->zt_cap, sizeof(int16_t) * c->z_rows * c->ncols) != TXS_OK)
                 return TXS_ERR_OUT_OF_MEMORY;
-            dim3 tb(32, 8), tg((unsigned)((c->ncols + 31) / 32), (unsigned)((c->nrows + 31) / 32));
-            k_transpose<<<tg, tb, 0, c->stream>>>(c->d_z, c->d_zt, (int)c->nrows, (int)c->ncols);
+            dim3 tb(32, 8), tg((unsigned)((c->ncols + 31) / 32), (unsigned)((c->z_rows + 31) / 32));
+            k_transpose<<<tg, tb, 0, c->stream>>>(c->d_z, c->d_zt, (int)c->z_rows, (int)c->ncols);
             TXS_LAUNCHED(c, "vix");
             c->zt_valid = true;
         }
@@ -285,7 +290,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
 txs_status launch_los_batch(txs_ctx* c, const int32_t* d_pairs, int64_t n, int32_t ht, int32_t hr, uint8_t* d_out) {
     const int64_t threads = n * 32;
     const unsigned blocks = (unsigned)((threads + 255) / 256);
-    k_los_batch<<<blocks, 256, 0, c->stream>>>(c->d_z, (int)c->nrows, (int)c->ncols, (const int4*)d_pairs, n, ht, hr, d_out);
+    k_los_batch<<<blocks, 256, 0, c->stream>>>(c->zv(), (int)c->nrows, (int)c->ncols, (const int4*)d_pairs, n, ht, hr, d_out);
     TXS_LAUNCHED(c, "los");
     return TXS_OK;
 }

@@ -1,0 +1,200 @@
+"""Row-band multi-GPU orchestration of the siting pipeline.
+
+Rank k owns a contiguous band of FINDMAX block rows and holds terrain for the
+band +- (roi+1) rows.  VIX, FINDMAX and VIEWSHED run independently per rank
+(no data-path collective).  Global candidate ids are the exclusive prefix of
+the per-band counts plus the local index, which reproduces single-GPU block
+order.  SITE is the one exchange: every round each rank
+reports its best (gain << 32 | ~gid) key, the max is reduced across ranks
+(allreduce MAX), the owner of the winner contributes its window and packed
+words to an allreduce SUM that every other rank feeds zeros into (a broadcast
+whose root is data-dependent), and every rank ORs the window into its held
+cumulative rows and updates its local gains.  Stop rules (decision D9) are
+evaluated identically on every rank from the reduced key.
+
+`ranks` is the list of (engine, band index) pairs this process drives: one per
+process with TorchComm over NCCL (one GPU each), or several on one device with
+LocalComm (the single-GPU emulation the tests use).  An "engine" is anything
+with the shard methods of paper_2006_16783_b200.Engine.
+"""
+import numpy as np
+
+STOP_TARGET, STOP_ZERO, STOP_EXHAUSTED, STOP_MAX = "target-reached", "zero-gain", "exhausted", "max-selected"
+
+
+def plan_bands(nrows, block, world):
+    """Split the ceil(nrows/block) FINDMAX block rows over `world` ranks as
+    evenly as possible; returns [(row_begin, row_end)] (empty when world exceeds
+    the block rows)."""
+    nb = -(-nrows // block)
+    base, extra = divmod(nb, world)
+    out, b = [], 0
+    for k in range(world):
+        cnt = base + (1 if k < extra else 0)
+        out.append((min(nrows, b * block), min(nrows, (b + cnt) * block)))
+        b += cnt
+    return out
+
+
+class LocalComm:
+    """Collectives over a single process (all ranks local)."""
+    world = 1
+
+    def max_i64(self, x):
+        return int(x)
+
+    def sum_i64(self, arr):
+        return arr
+
+    def allgather_i64(self, arr):
+        return np.asarray(arr, np.int64)
+
+
+class TorchComm:
+    """Collectives through torch.distributed (NCCL on GPUs, gloo on CPU).  Keys
+    are < 2^63 (gain < 2^31), so signed int64 MAX is exact; the winner payload
+    is reinterpreted as int64 for a SUM with zeros (bit-exact)."""
+
+    def __init__(self, device="cpu"):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.device = torch, dist, device
+        self.world = dist.get_world_size()
+
+    def max_i64(self, x):
+        t = self.torch.tensor([int(x)], dtype=self.torch.int64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return int(t.item())
+
+    def sum_i64(self, arr):
+        t = self.torch.from_numpy(np.ascontiguousarray(arr).view(np.int64).copy()).to(self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return t.cpu().numpy().view(np.uint64)
+
+    def allgather_i64(self, arr):
+        a = np.ascontiguousarray(arr, np.int64)
+        t = self.torch.from_numpy(a.copy()).to(self.device)
+        outs = [self.torch.zeros_like(t) for _ in range(self.world)]
+        self.dist.all_gather(outs, t)
+        return np.concatenate([o.cpu().numpy() for o in outs])
+
+
+def _mw(roi):
+    s = 2 * roi + 1
+    return (s * s + 63) // 64
+
+
+def setup_sharded(ranks, cfg, nbands, host_terrain=None):
+    """Give every local rank its band + (roi+1)-row halo of the configuration's
+    terrain: generated on the device (cropped), or copied from `host_terrain`
+    (the full grid, e.g. pinned host memory).  Returns the active ranks."""
+    nr, nc, roi = cfg.nrows, cfg.ncols, cfg.roi
+    bands = plan_bands(nr, cfg.block if cfg.block else max(1, roi), nbands)
+    halo = roi + 1
+    active = []
+    for eng, k in ranks:
+        r0, r1 = bands[k]
+        if r1 <= r0:
+            continue
+        eng.set_shard(nr, nc, r0, r1, halo)
+        if host_terrain is None:
+            eng.generate_fractal(nr, nc, cfg.roughness, cfg.terrain_seed, cfg.zmin, cfg.zmax)
+            if cfg.water_rows:
+                eng.fill_rows(0, cfg.water_rows, 0)
+        else:
+            h0, hr, _, _ = eng.shard_info()
+            eng.set_terrain(host_terrain[h0:h0 + hr])
+        active.append((eng, k))
+    return active
+
+
+def run_sharded(ranks, comm, cfg, params, nbands, setup=True, with_cum=True):
+    """Run one configuration (paper_2006_16783_b200.configs.Config) over row
+    bands.  Returns dict(index,row,col,gain,coverage,stop,cum) with the global
+    dense cumulative bitmap.  With setup=False the ranks already
+    hold their terrain (setup_sharded)."""
+    nr, nc, roi = cfg.nrows, cfg.ncols, cfg.roi
+    bands = plan_bands(nr, cfg.block if cfg.block else max(1, roi), nbands)
+    if setup:
+        active = setup_sharded(ranks, cfg, nbands)
+    else:
+        active = [(e, k) for e, k in ranks if bands[k][1] > bands[k][0]]
+    # ---- VIX + FINDMAX per band, global ids by prefix over band order --------
+    counts = np.zeros(nbands, np.int64)
+    for eng, k in active:
+        if cfg.random_observers:
+            eng.random_observers(cfg.random_observers, cfg.observer_seed)   # ids = global draw index
+            counts[k] = 0
+        else:
+            eng.estimate_vix(params, copy=False)
+            counts[k] = eng.find_candidates(params, copy=False)
+    counts = comm.allgather_i64(counts).reshape(-1, nbands).sum(0)
+    if cfg.random_observers:
+        total_cand = cfg.random_observers
+    else:
+        prefix = np.concatenate([[0], np.cumsum(counts)[:-1]])
+        for eng, k in active:
+            eng.set_candidate_base(int(prefix[k]))
+        total_cand = int(counts.sum())
+    # ---- VIEWSHED per band --------------------------------------------------------
+    for eng, _ in active:
+        eng.compute_all_viewsheds(params)
+        eng.site_shard_begin(params)
+    # ---- SITE rounds ----------------------------------------------------------------
+    total = float(nr) * float(nc)
+    mw = _mw(roi)
+    idx, rows, cols, gains, covs = [], [], [], [], []
+    covered, stop = 0, STOP_EXHAUSTED
+    target, max_sel = params.target_coverage, params.max_selected
+    while True:
+        if len(idx) >= total_cand:
+            stop = STOP_EXHAUSTED
+            break
+        key = max([eng.site_shard_best() for eng, _ in active] + [0])
+        key = comm.max_i64(key)
+        g = key >> 32
+        if g <= 0:
+            stop = STOP_ZERO
+            break
+        gid = 0xFFFFFFFF - (key & 0xFFFFFFFF)
+        payload = np.zeros(6 + mw, np.uint64)
+        for eng, _ in active:
+            ex = eng.site_shard_export(gid, roi)
+            if ex is not None:
+                r, c, win, words = ex
+                payload[0], payload[1] = r, c
+                payload[2:6] = win.astype(np.uint64)
+                payload[6:] = words
+        payload = comm.sum_i64(payload)
+        r, c = int(payload[0]), int(payload[1])
+        win = payload[2:6].astype(np.int32)
+        words = np.ascontiguousarray(payload[6:])
+        for eng, _ in active:
+            eng.site_shard_apply(r, c, win, words)
+        covered += g
+        cov = covered / total
+        idx.append(gid); rows.append(r); cols.append(c); gains.append(g); covs.append(cov)
+        if cov >= target:
+            stop = STOP_TARGET
+            break
+        if max_sel > 0 and len(idx) >= max_sel:
+            stop = STOP_MAX
+            break
+    out = dict(index=np.array(idx, np.int64), row=np.array(rows, np.int32), col=np.array(cols, np.int32),
+               gain=np.array(gains, np.int64), coverage=np.array(covs), stop=stop)
+    if not with_cum:
+        return out
+    # ---- global cumulative bitmap: each band's rows, summed (disjoint bits) ----
+    nw = (nr * nc + 63) // 64
+    cum = np.zeros(nw, np.uint64)
+    for eng, k in active:
+        r0, r1 = bands[k]
+        part = eng.cumulative()
+        bits = np.unpackbits(part.view(np.uint8), bitorder="little")[: nr * nc]
+        mask = np.zeros(nr * nc, np.uint8)
+        mask[r0 * nc: r1 * nc] = 1
+        packed = np.packbits(np.concatenate([bits & mask, np.zeros(nw * 64 - nr * nc, np.uint8)]),
+                             bitorder="little").view(np.uint64)
+        cum |= packed
+    out["cum"] = comm.sum_i64(cum)
+    return out

@@ -327,3 +327,30 @@ def test_cli_matches_oracle_and_is_deterministic(tmp_path):
     a1 = np.frombuffer(outs[0]["cumshed_1.pgm"][15:], np.uint8)
     a2 = np.frombuffer(outs[0]["cumshed_2.pgm"][15:], np.uint8)
     assert ((a1 <= a2)).all()
+
+
+# ---- row-band shards on one device (virtual ranks) ---------------
+@pytest.mark.parametrize("kind,nb", [("findmax", 1), ("findmax", 2), ("findmax", 3), ("observers", 2),
+                                     ("observers", 4)])
+def test_sharded_engine_matches_single(kind, nb):
+    T = _T()
+    from paper_2006_16783_b200.configs import Config, params_for, run, setup_terrain
+    from paper_2006_16783_b200.shard import LocalComm, run_sharded
+    if kind == "findmax":
+        cfg = Config("s1", 600, 500, 0.5, 0, 4000, 20, 10, 10, 50, 4, 0.9, 0, 5, 6, water_rows=37)
+    else:
+        cfg = Config("s2", 512, 480, 0.6, 0, 3000, 30, 20, 0, 0, 0, 1.0, 40, 8, 9,
+                     random_observers=2000, observer_seed=77)
+    params = params_for(cfg)
+    engines = [T.Engine(0) for _ in range(nb)]
+    res = run_sharded([(e, k) for k, e in enumerate(engines)], LocalComm(), cfg, params, nb)
+    with T.Engine(0) as e:
+        setup_terrain(e, cfg)
+        single = run(e, cfg, params)
+        cum = e.cumulative()
+    for x in engines:
+        x.close()
+    assert res["stop"] == single["stop"]
+    assert np.array_equal(res["index"], single["index"])
+    assert np.array_equal(res["gain"], single["gain"]) and np.array_equal(res["coverage"], single["coverage"])
+    assert np.array_equal(res["cum"], cum)
