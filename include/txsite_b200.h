@@ -193,6 +193,9 @@ txs_status txs_site_shard_apply(txs_ctx* ctx, int32_t row, int32_t col, const tx
  * caps suffice.  cell_begin has rays+1 entries. */
 int64_t txs_ray_template(int32_t roi, int32_t* p, int32_t* q, int64_t* cell_begin, int32_t* ca,
                          int32_t* cb, int64_t cap_rays, int64_t cap_cells, int64_t* ncells);
+/* Size of the VIEWSHED event stream for roi (<= 250): events, events incl.
+ * warp padding, 32-ray groups.  0 = ok. */
+int txs_event_template_info(int32_t roi, int64_t* real_events, int64_t* padded_events, int32_t* groups);
 /* Self-test of host-side integer helpers (exact 64-bit division magic). 0 = ok. */
 int txs_selftest(void);
 

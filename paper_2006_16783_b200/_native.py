@@ -96,6 +96,7 @@ _sig("txs_site_shard_export", C.c_int, [vp, i64, C.POINTER(i32), C.POINTER(i32),
 _sig("txs_site_shard_apply", C.c_int, [vp, i32, i32, vp, vp])
 _sig("txs_ray_template", i64, [i32, vp, vp, vp, vp, vp, i64, i64, C.POINTER(i64)])
 _sig("txs_selftest", C.c_int, [])
+_sig("txs_event_template_info", C.c_int, [i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(i32)])
 
 # every symbol the header declares (checked by the CPU test-suite)
 EXPORTS = [
@@ -106,5 +107,5 @@ EXPORTS = [
     "txs_get_candidates", "txs_compute_viewsheds", "txs_get_viewsheds", "txs_set_viewsheds", "txs_site",
     "txs_get_cumulative", "txs_marginal_gains", "txs_run_pipeline", "txs_ray_template", "txs_selftest",
     "txs_set_shard", "txs_shard_info", "txs_set_candidate_base", "txs_site_shard_begin", "txs_site_shard_best",
-    "txs_site_shard_export", "txs_site_shard_apply",
+    "txs_site_shard_export", "txs_site_shard_apply", "txs_event_template_info",
 ]

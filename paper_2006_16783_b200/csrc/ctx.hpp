@@ -22,7 +22,8 @@ const RayTemplate& ray_template(int32_t roi);
 
 // Device copy: rays[r] = {p, q, cell_begin, cell_count}; cells packed (a & 0xffff) | (b << 16).
 // For roi <= kEvMaxRoi also the merged per-ray event stream (see raytemplate.cpp):
-// 32-lane groups of neighbouring rays, events interleaved [step][lane].
+// 32-lane groups of neighbouring rays, events interleaved [step][lane], each
+// event = {word (type, offsets, weight, byrow bit), y (line index or cell dot)}.
 constexpr int kEvMaxRoi = 250;
 enum EvType : uint32_t { kEvRow = 0, kEvCol = 1, kEvPost = 2, kEvCell = 3, kEvNop = 4 };
 struct RayTemplateDev {
@@ -32,13 +33,13 @@ struct RayTemplateDev {
     uint32_t* cells = nullptr;
     int32_t ngroups = 0;
     int2* groups = nullptr;      // {first event row (x32 lanes), steps}
-    uint32_t* events = nullptr;
+    uint2* events = nullptr;
     int64_t nevents = 0;
 };
 // host-side event stream (exposed for tests through txs_event_template)
 struct EventTemplate {
     std::vector<int2> groups;
-    std::vector<uint32_t> events;
+    std::vector<uint2> events;
 };
 const EventTemplate& event_template(int32_t roi);
 

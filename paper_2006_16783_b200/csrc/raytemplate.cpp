@@ -103,17 +103,22 @@ RayTemplate build(int32_t R) {
 // the crossings of its primitive direction interleaved with its owned cells,
 // a cell emitted before every crossing with u_k >= u_c, nothing after the
 // last cell.  Event word: bits 0-2 type, 3-11 row offset, 12-20 col offset
-// (9-bit two's complement), 21-28 interpolation weight m.  Crossing offsets
-// name the first interpolation post; the second lies one step along +sign(q)
-// columns (row line) or +sign(p) rows (column line).
-inline uint32_t pack_ev(uint32_t type, int dr, int dc, int m) {
-    return type | ((uint32_t)(dr & 0x1ff) << 3) | ((uint32_t)(dc & 0x1ff) << 12) | ((uint32_t)m << 21);
+// (9-bit two's complement), 21-28 interpolation weight m, bit 29 "byrow"
+// (the crossing's denominator is |p| and its index the row-line index).
+// Crossing offsets name the first interpolation post; the second lies one
+// step along +sign(q) columns (row line) or +sign(p) rows (column line).
+// The event's y is the crossing's line index (its slope's M) or, for a cell,
+// its projection numerator dot = a*p + b*q.
+inline uint2 pack_ev(uint32_t type, int dr, int dc, int m, bool byrow, int64_t y) {
+    return make_uint2(type | ((uint32_t)(dr & 0x1ff) << 3) | ((uint32_t)(dc & 0x1ff) << 12) | ((uint32_t)m << 21) |
+                          ((uint32_t)byrow << 29),
+                      (uint32_t)y);
 }
 
 EventTemplate build_events(const RayTemplate& T) {
     EventTemplate E;
     const int64_t nrays = (int64_t)T.p.size();
-    std::vector<std::vector<uint32_t>> per((size_t)nrays);
+    std::vector<std::vector<uint2>> per((size_t)nrays);
     for (int64_t r = 0; r < nrays; ++r) {
         const int64_t p = T.p[(size_t)r], q = T.q[(size_t)r];
         const int64_t ap = std::llabs(p), aq = std::llabs(q), sp = p >= 0 ? 1 : -1, sq = q >= 0 ? 1 : -1;
@@ -130,13 +135,13 @@ EventTemplate build_events(const RayTemplate& T) {
                 else { const int64_t cmp = i * aq - j * ap; isrow = cmp <= 0; iscol = cmp >= 0; }
                 const int64_t idx = isrow ? i : j, n = isrow ? ap : aq;
                 if (idx * L2 >= dot * n) break;
-                if (isrow && iscol) ev.push_back(pack_ev(kEvPost, (int)(sp * i), (int)(sq * j), 0));
-                else if (isrow) ev.push_back(pack_ev(aq == 0 ? kEvPost : kEvRow, (int)(sp * i), (int)(sq * qr), (int)mr));
-                else ev.push_back(pack_ev(ap == 0 ? kEvPost : kEvCol, (int)(sp * qc), (int)(sq * j), (int)mc));
+                if (isrow && iscol) ev.push_back(pack_ev(kEvPost, (int)(sp * i), (int)(sq * j), 0, true, i));
+                else if (isrow) ev.push_back(pack_ev(aq == 0 ? kEvPost : kEvRow, (int)(sp * i), (int)(sq * qr), (int)mr, true, i));
+                else ev.push_back(pack_ev(ap == 0 ? kEvPost : kEvCol, (int)(sp * qc), (int)(sq * j), (int)mc, false, j));
                 if (isrow) { ++i; qr += dqr; mr += dmr; if (mr >= ap) { mr -= ap; ++qr; } }
                 if (iscol) { ++j; qc += dqc; mc += dmc; if (mc >= aq) { mc -= aq; ++qc; } }
             }
-            ev.push_back(pack_ev(kEvCell, (int)a, (int)b, 0));
+            ev.push_back(pack_ev(kEvCell, (int)a, (int)b, 0, false, dot));
         }
     }
     const int64_t ngroups = (nrays + 31) / 32;
@@ -148,7 +153,8 @@ EventTemplate build_events(const RayTemplate& T) {
         for (size_t s = 0; s < steps; ++s)
             for (int64_t l = 0; l < 32; ++l) {
                 const int64_t r = g * 32 + l;
-                E.events.push_back(r < nrays && s < per[(size_t)r].size() ? per[(size_t)r][s] : (uint32_t)kEvNop);
+                E.events.push_back(r < nrays && s < per[(size_t)r].size() ? per[(size_t)r][s]
+                                                                         : make_uint2((uint32_t)kEvNop, 0u));
             }
         row += (int64_t)steps;
     }
@@ -197,10 +203,10 @@ txs_status get_template(txs_ctx* ctx, int32_t roi, RayTemplateDev** out) {
         D.ngroups = (int32_t)E.groups.size();
         D.nevents = (int64_t)E.events.size();
         TXS_CUDA(ctx, "viewshed", cudaMalloc(&D.groups, sizeof(int2) * E.groups.size()));
-        TXS_CUDA(ctx, "viewshed", cudaMalloc(&D.events, sizeof(uint32_t) * std::max<size_t>(1, E.events.size())));
+        TXS_CUDA(ctx, "viewshed", cudaMalloc(&D.events, sizeof(uint2) * std::max<size_t>(1, E.events.size())));
         TXS_CUDA(ctx, "viewshed", cudaMemcpy(D.groups, E.groups.data(), sizeof(int2) * E.groups.size(), cudaMemcpyHostToDevice));
         if (!E.events.empty())
-            TXS_CUDA(ctx, "viewshed", cudaMemcpy(D.events, E.events.data(), sizeof(uint32_t) * E.events.size(), cudaMemcpyHostToDevice));
+            TXS_CUDA(ctx, "viewshed", cudaMemcpy(D.events, E.events.data(), sizeof(uint2) * E.events.size(), cudaMemcpyHostToDevice));
     }
     TXS_CUDA(ctx, "viewshed", cudaMalloc(&D.rays, sizeof(int4) * rays.size()));
     TXS_CUDA(ctx, "viewshed", cudaMalloc(&D.cells, sizeof(uint32_t) * std::max<size_t>(1, cells.size())));
@@ -228,4 +234,15 @@ extern "C" int64_t txs_ray_template(int32_t roi, int32_t* p, int32_t* q, int64_t
         std::copy(T.cb.begin(), T.cb.end(), cb);
     }
     return nr;
+}
+
+extern "C" int txs_event_template_info(int32_t roi, int64_t* real_events, int64_t* padded_events, int32_t* groups) {
+    if (roi < 1 || roi > txs::kEvMaxRoi || !real_events || !padded_events || !groups) return 1;
+    const txs::EventTemplate& E = txs::event_template(roi);
+    int64_t real = 0;
+    for (const uint2& e : E.events) real += (e.x & 7u) != txs::kEvNop;
+    *real_events = real;
+    *padded_events = (int64_t)E.events.size();
+    *groups = (int32_t)E.groups.size();
+    return 0;
 }

@@ -15,6 +15,8 @@
 // horizon from bare terrain).  Crossings needing an off-grid post end the ray
 // (the in-grid crossings of a ray are a prefix).  Bits: window row-major,
 // LSB-first in u64 words (decision D8), accumulated in shared memory.
+#include <cub/cub.cuh>
+
 #include "ctx.hpp"
 
 namespace txs {
@@ -22,7 +24,8 @@ namespace {
 
 struct VsArgs {
     int nrows, ncols, R, ht, hr, nrays;
-    int64_t stride;   // u64 words per viewshed slot
+    int64_t stride;       // u64 words per viewshed slot
+    const int32_t* perm;  // processing order (spatially sorted), or null
 };
 
 template <bool SMEM_BITS>
@@ -33,7 +36,7 @@ __global__ void k_viewshed(const int16_t* __restrict__ z, const int32_t* __restr
                            unsigned long long* __restrict__ counters) {
     extern __shared__ __align__(16) uint32_t s_bits[];
     __shared__ int s_red[32];
-    const int64_t cand = blockIdx.x;
+    const int64_t cand = a.perm ? a.perm[blockIdx.x] : blockIdx.x;
     const int r = crow[cand], c = ccol[cand];
     const int row0 = max(0, r - a.R), col0 = max(0, c - a.R);
     const int h = min(a.nrows - 1, r + a.R) - row0 + 1, w = min(a.ncols - 1, c + a.R) - col0 + 1;
@@ -148,72 +151,93 @@ __global__ void k_viewshed(const int16_t* __restrict__ z, const int32_t* __restr
 }
 
 // Event-stream variant (roi <= kEvMaxRoi): the merged per-ray events of the
-// template are read [step][lane] (one coalesced 128-byte line per warp step)
-// and every event — row/column/post crossing or owned cell — goes through the
-// same branch-free arithmetic: value v = z0*w0 + z1*w1, then
-//   crossing:  X = v - E*n,           Y = line index   (horizon candidate X/Y)
-//   cell:      X = (v + h_r - E)*L2,  Y = dot          (receiver tangent X/Y)
-// compared with the horizon NH/MH by X*MH vs NH*Y (int64).  Lanes of a warp
+// template are read [step][lane] (one coalesced 8-byte-per-lane load per warp
+// step) and every event — row/column/post crossing or owned cell — goes
+// through the same branch-free arithmetic with one value v = z0*(n-m) + z1*m:
+//   crossing:  X = v - E*n,        M = y (line index)     horizon candidate X/M
+//   cell:      X = z + h_r - E,    M = L2*MH, y = dot      receiver tangent test
+// and one pair of 32x32->64-bit products X*M vs NH*y against the horizon
+// NH/MH (cells: P*L2*MH >= NH*dot, crossings: N*MH > NH*M).  Lanes of a warp
 // are 32 neighbouring rays; the CTA's warps stride over the ray groups.
+constexpr int kVsUnroll = 4;
+
 template <bool INTERIOR>
 __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, int c, int E, int row0, int col0, int w,
                                           const VsArgs& a, const int4* __restrict__ rays,
-                                          const int2* __restrict__ groups, const uint32_t* __restrict__ events,
+                                          const int2* __restrict__ groups, const uint2* __restrict__ events,
                                           int ngroups, uint32_t* s_bits, uint64_t* gout, bool smem_bits,
                                           unsigned long long& n_cross, unsigned long long& n_cells) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int16_t* __restrict__ P = z + (int64_t)r * a.ncols + c;
+    const int Ehr = E - a.hr;
+    // interior observers: unclipped window, bit = (dr+R)*(2R+1) + (dc+R)
+    const int W2 = 2 * a.R + 1, K0 = a.R * W2 + a.R;
     for (int g = warp; g < ngroups; g += nwarps) {
         const int2 grp = __ldg(groups + g);
         const int ray = g * 32 + lane;
         int p = 0, q = 0;
         if (ray < a.nrays) { const int4 rd = __ldg(rays + ray); p = rd.x; q = rd.y; }
         const int ap = abs(p), aq = abs(q);
+        const int stepr = p >= 0 ? a.ncols : -a.ncols, stepc = q >= 0 ? 1 : -1;
         const int sp = p >= 0 ? 1 : -1, sq = q >= 0 ? 1 : -1;
         const int L2 = p * p + q * q;
-        int i = 0, j = 0;
+        const int Eap = E * ap, Eaq = E * aq;
         bool has = false, alive = true;
-        int NH = 0, MH = 1;
-        const uint32_t* ev = events + (int64_t)grp.x * 32 + lane;
-        for (int st = 0; st < grp.y; ++st) {
-            const uint32_t e = __ldg(ev + (int64_t)st * 32);
-            const uint32_t type = e & 7u;
-            const int dr = ((int)(e << 20)) >> 23, dc = ((int)(e << 11)) >> 23;
-            const int m = (int)((e >> 21) & 0xffu);
-            const bool isrow = type == kEvRow, iscol = type == kEvCol, ispost = type == kEvPost;
-            const bool iscell = type == kEvCell, iscross = type <= kEvPost;
-            i += (isrow || ispost);
-            j += (iscol || ispost);
-            const int rr = r + dr, cc = c + dc;
-            const int dr1 = iscol ? sp : 0, dc1 = isrow ? sq : 0;
-            bool inb = true;
-            if (!INTERIOR) {
-                inb = rr >= 0 && rr < a.nrows && cc >= 0 && cc < a.ncols &&
-                      rr + dr1 >= 0 && rr + dr1 < a.nrows && cc + dc1 >= 0 && cc + dc1 < a.ncols;
+        int NH = 0, MH = 1, L2MH = L2;
+        const uint2* ev = events + (int64_t)grp.x * 32 + lane;
+        for (int st0 = 0; st0 < grp.y; st0 += kVsUnroll) {
+            uint2 ee[kVsUnroll];
+            int z0[kVsUnroll], z1[kVsUnroll], kb[kVsUnroll];
+            bool ok[kVsUnroll];
+#pragma unroll
+            for (int u = 0; u < kVsUnroll; ++u)
+                ee[u] = st0 + u < grp.y ? __ldg(ev + (int64_t)(st0 + u) * 32) : make_uint2((uint32_t)kEvNop, 0u);
+#pragma unroll
+            for (int u = 0; u < kVsUnroll; ++u) {
+                const uint32_t e = ee[u].x, type = e & 7u;
+                const int dr = ((int)(e << 20)) >> 23, dc = ((int)(e << 11)) >> 23;
+                const bool isrow = type == kEvRow, iscol = type == kEvCol;
+                bool inb = type != kEvNop;
+                if (!INTERIOR) {
+                    const int rr = r + dr, cc = c + dc;
+                    const int r1 = rr + (iscol ? sp : 0), c1 = cc + (isrow ? sq : 0);
+                    inb = inb && rr >= 0 && rr < a.nrows && cc >= 0 && cc < a.ncols && r1 >= 0 && r1 < a.nrows &&
+                          c1 >= 0 && c1 < a.ncols;
+                    kb[u] = (rr - row0) * w + (cc - col0);
+                } else {
+                    kb[u] = dr * W2 + dc + K0;
+                }
+                const int off0 = inb ? dr * a.ncols + dc : 0;
+                const int off1 = inb ? off0 + (iscol ? stepr : (isrow ? stepc : 0)) : 0;
+                z0[u] = __ldg(P + off0);
+                z1[u] = __ldg(P + off1);
+                ok[u] = inb;
             }
-            const bool use = inb && type != kEvNop;
-            const int off0 = use ? dr * a.ncols + dc : 0;
-            const int off1 = use ? off0 + dr1 * a.ncols + dc1 : 0;
-            const int z0 = __ldg(P + off0), z1 = __ldg(P + off1);
-            const bool byrow = isrow || (ispost && ap > 0);
-            const int n = iscell ? 1 : (byrow ? ap : aq);
-            const int w1 = (isrow || iscol) ? m : 0;
-            const int v = z0 * (n - w1) + z1 * w1;
-            long long X;
-            int Y;
-            if (iscell) { X = (long long)(v + a.hr - E) * L2; Y = dr * p + dc * q; }
-            else { X = (long long)(v - E * n); Y = byrow ? i : j; }
-            const long long lhs = X * MH, rhs = (long long)NH * Y;
-            if (iscross) {
-                if (!inb) alive = false;
-                else if (alive && (!has || lhs > rhs)) { has = true; NH = (int)X; MH = Y; ++n_cross; }
-                else if (alive) ++n_cross;
-            } else if (iscell && inb) {
-                ++n_cells;
-                if (!has || lhs >= rhs) {
-                    const int k = (rr - row0) * w + (cc - col0);
-                    if (smem_bits) atomicOr(&s_bits[k >> 5], 1u << (k & 31));
-                    else atomicOr((unsigned long long*)&gout[k >> 6], 1ull << (k & 63));
+#pragma unroll
+            for (int u = 0; u < kVsUnroll; ++u) {
+                const uint32_t e = ee[u].x, type = e & 7u;
+                const int y = (int)ee[u].y;
+                const int m = (int)((e >> 21) & 0xffu);
+                const bool byrow = (e >> 29) & 1u;
+                const bool iscell = type == kEvCell, iscross = type <= kEvPost;
+                const int n = iscell ? 1 : (byrow ? ap : aq);
+                const int v = z0[u] * (n - m) + z1[u] * m;
+                const int X = v - (iscell ? Ehr : (byrow ? Eap : Eaq));
+                const long long lhs = (long long)X * (iscell ? L2MH : MH);
+                const long long rhs = (long long)NH * y;
+                if (iscross) {
+                    if (!ok[u]) alive = false;
+                    else if (alive) {
+                        ++n_cross;
+                        if (!has || lhs > rhs) { has = true; NH = X; MH = y; L2MH = L2 * y; }
+                    }
+                } else if (iscell && ok[u]) {
+                    ++n_cells;
+                    if (!has || lhs >= rhs) {
+                        const int k = kb[u];
+                        if (smem_bits) atomicOr(&s_bits[k >> 5], 1u << (k & 31));
+                        else atomicOr((unsigned long long*)&gout[k >> 6], 1ull << (k & 63));
+                    }
                 }
             }
         }
@@ -223,12 +247,12 @@ __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, 
 template <bool SMEM_BITS>
 __global__ void k_viewshed_ev(const int16_t* __restrict__ z, const int32_t* __restrict__ crow,
                               const int32_t* __restrict__ ccol, const int4* __restrict__ rays,
-                              const int2* __restrict__ groups, const uint32_t* __restrict__ events, int ngroups,
+                              const int2* __restrict__ groups, const uint2* __restrict__ events, int ngroups,
                               VsArgs a, uint64_t* __restrict__ words, int4* __restrict__ wins,
                               int32_t* __restrict__ pops, unsigned long long* __restrict__ counters) {
     extern __shared__ __align__(16) uint32_t s_bits[];
     __shared__ int s_red[32];
-    const int64_t cand = blockIdx.x;
+    const int64_t cand = a.perm ? a.perm[blockIdx.x] : blockIdx.x;
     const int r = crow[cand], c = ccol[cand];
     const int row0 = max(0, r - a.R), col0 = max(0, c - a.R);
     const int h = min(a.nrows - 1, r + a.R) - row0 + 1, w = min(a.ncols - 1, c + a.R) - col0 + 1;
@@ -278,6 +302,14 @@ __global__ void k_viewshed_ev(const int16_t* __restrict__ z, const int32_t* __re
     }
 }
 
+__global__ void k_tile_keys(const int32_t* __restrict__ crow, const int32_t* __restrict__ ccol, int64_t n, int tiles_x,
+                            uint32_t* __restrict__ keys, int32_t* __restrict__ idx) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    keys[i] = (uint32_t)((crow[i] >> 6) * tiles_x + (ccol[i] >> 6));
+    idx[i] = (int32_t)i;
+}
+
 }  // namespace
 
 txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
@@ -294,7 +326,28 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
     c->vs_n = n;
     c->vs_stride = mw;
     if (n == 0) return TXS_OK;
-    VsArgs a{(int)c->nrows, (int)c->ncols, p.roi, p.tx_height, p.rx_height, T->nrays, mw};
+    VsArgs a{(int)c->nrows, (int)c->ncols, p.roi, p.tx_height, p.rx_height, T->nrays, mw, nullptr};
+    // Process observers in 64x64-tile order so the CTAs resident at any moment
+    // read overlapping terrain windows (L2 reuse; config 5's observers are
+    // random over a 537 MB terrain).  Output slots keep candidate order.
+    if (n >= 4096) {
+        const int tiles_x = (int)((c->ncols + 63) / 64);
+        size_t tmp_bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr, (int32_t*)nullptr,
+                                        (int32_t*)nullptr, (int)n);
+        const size_t need = 16 * (size_t)n + tmp_bytes + 256;
+        if (ensure(c, "viewshed", &c->d_scratch, &c->scratch_cap, need) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
+        uint32_t* keys = (uint32_t*)c->d_scratch;
+        uint32_t* keys2 = keys + n;
+        int32_t* idx = (int32_t*)(keys2 + n);
+        int32_t* perm = idx + n;
+        void* tmp = perm + n;
+        k_tile_keys<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->d_crow, c->d_ccol, n, tiles_x, keys, idx);
+        TXS_LAUNCHED(c, "viewshed");
+        TXS_CUDA(c, "viewshed", cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, idx, perm, (int)n, 0, 32,
+                                                                c->stream));
+        a.perm = perm;
+    }
     const size_t smem = sizeof(uint64_t) * (size_t)mw;
     if (n > 0x7fffffff) return fail(c, TXS_ERR_RANGE, "viewshed", "too many candidates");
     const bool smem_bits = smem <= 160 * 1024;
