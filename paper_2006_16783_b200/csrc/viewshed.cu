@@ -17,6 +17,8 @@
 // LSB-first in u64 words (decision D8), accumulated in shared memory.
 #include <cub/cub.cuh>
 
+#include <cstdlib>
+
 #include "ctx.hpp"
 
 namespace txs {
@@ -26,6 +28,8 @@ struct VsArgs {
     int nrows, ncols, R, ht, hr, nrays;
     int64_t stride;       // u64 words per viewshed slot
     const int32_t* perm;  // processing order (spatially sorted), or null
+    int64_t n;            // observers
+    long long tmpl_cross, tmpl_cells;   // template crossings / cells (interior observers)
 };
 
 template <bool SMEM_BITS>
@@ -244,6 +248,81 @@ __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, 
     }
 }
 
+// Interior fast path for K observers per CTA: each warp walks its ray group
+// once, the event load/decode/offsets are shared and every observer keeps its
+// own horizon (NH, MH) and bitmap — K independent dependency chains per lane.
+// Interior observers have every post in the grid and an unclipped window, so
+// no bounds tests and no counting (the template's totals are added instead).
+template <int K>
+__device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const int* rk, const int* ck, const int* Ek,
+                                            const VsArgs& a, const int4* __restrict__ rays,
+                                            const int2* __restrict__ groups, const uint2* __restrict__ events,
+                                            int ngroups, uint32_t* s_bits, int bits_stride) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int W2 = 2 * a.R + 1, K0 = a.R * W2 + a.R;
+    const int16_t* __restrict__ P[K];
+    int Ehr[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        P[k] = z + (int64_t)rk[k] * a.ncols + ck[k];
+        Ehr[k] = Ek[k] - a.hr;
+    }
+    for (int g = warp; g < ngroups; g += nwarps) {
+        const int2 grp = __ldg(groups + g);
+        const int ray = g * 32 + lane;
+        int p = 0, q = 0;
+        if (ray < a.nrays) { const int4 rd = __ldg(rays + ray); p = rd.x; q = rd.y; }
+        const int ap = abs(p), aq = abs(q);
+        const int stepr = p >= 0 ? a.ncols : -a.ncols, stepc = q >= 0 ? 1 : -1;
+        const int L2 = p * p + q * q;
+        bool has[K];
+        int NH[K], MH[K], L2MH[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) { has[k] = false; NH[k] = 0; MH[k] = 1; L2MH[k] = L2; }
+        const uint2* ev = events + (int64_t)grp.x * 32 + lane;
+        for (int st0 = 0; st0 < grp.y; st0 += 2) {
+            uint2 ee[2];
+            int z0[2][K], z1[2][K], kb[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                ee[u] = st0 + u < grp.y ? __ldg(ev + (int64_t)(st0 + u) * 32) : make_uint2((uint32_t)kEvNop, 0u);
+                const uint32_t e = ee[u].x, type = e & 7u;
+                const int dr = ((int)(e << 20)) >> 23, dc = ((int)(e << 11)) >> 23;
+                const bool isrow = type == kEvRow, iscol = type == kEvCol;
+                kb[u] = dr * W2 + dc + K0;
+                const int off0 = type != kEvNop ? dr * a.ncols + dc : 0;
+                const int off1 = off0 + (iscol ? stepr : (isrow ? stepc : 0));
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    z0[u][k] = __ldg(P[k] + off0);
+                    z1[u][k] = __ldg(P[k] + off1);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const uint32_t e = ee[u].x, type = e & 7u;
+                const int y = (int)ee[u].y;
+                const int m = (int)((e >> 21) & 0xffu);
+                const bool byrow = (e >> 29) & 1u;
+                const bool iscell = type == kEvCell, iscross = type <= kEvPost;
+                const int n = iscell ? 1 : (byrow ? ap : aq);
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const int v = z0[u][k] * (n - m) + z1[u][k] * m;
+                    const int X = v - (iscell ? Ehr[k] : n * Ek[k]);
+                    const long long lhs = (long long)X * (iscell ? L2MH[k] : MH[k]);
+                    const long long rhs = (long long)NH[k] * y;
+                    if (iscross && (!has[k] || lhs > rhs)) { has[k] = true; NH[k] = X; MH[k] = y; L2MH[k] = L2 * y; }
+                    if (iscell && (!has[k] || lhs >= rhs)) {
+                        const int kk = kb[u];
+                        atomicOr(&s_bits[k * bits_stride + (kk >> 5)], 1u << (kk & 31));
+                    }
+                }
+            }
+        }
+    }
+}
+
 template <bool SMEM_BITS>
 __global__ void k_viewshed_ev(const int16_t* __restrict__ z, const int32_t* __restrict__ crow,
                               const int32_t* __restrict__ ccol, const int4* __restrict__ rays,
@@ -302,6 +381,93 @@ __global__ void k_viewshed_ev(const int16_t* __restrict__ z, const int32_t* __re
     }
 }
 
+// K observers per CTA (shared event stream, smem bitmaps); CTAs where some
+// observer is not interior fall back to one observer at a time.
+template <int K>
+__global__ void k_viewshed_evk(const int16_t* __restrict__ z, const int32_t* __restrict__ crow,
+                               const int32_t* __restrict__ ccol, const int4* __restrict__ rays,
+                               const int2* __restrict__ groups, const uint2* __restrict__ events, int ngroups,
+                               VsArgs a, uint64_t* __restrict__ words, int4* __restrict__ wins,
+                               int32_t* __restrict__ pops, unsigned long long* __restrict__ counters) {
+    extern __shared__ __align__(16) uint32_t s_bits[];
+    __shared__ int s_red[32];
+    const int bits_stride = (int)(2 * a.stride);
+    int64_t cand[K];
+    int rk[K], ck[K], Ek[K], row0[K], col0[K], hh[K], ww[K];
+    bool all_int = true;
+    int nk = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int64_t slot = (int64_t)blockIdx.x * K + k;
+        cand[k] = slot < a.n ? (a.perm ? a.perm[slot] : slot) : -1;
+        if (cand[k] < 0) { all_int = false; rk[k] = ck[k] = Ek[k] = row0[k] = col0[k] = hh[k] = ww[k] = 0; continue; }
+        ++nk;
+        const int r = crow[cand[k]], c = ccol[cand[k]];
+        rk[k] = r; ck[k] = c;
+        row0[k] = max(0, r - a.R); col0[k] = max(0, c - a.R);
+        hh[k] = min(a.nrows - 1, r + a.R) - row0[k] + 1;
+        ww[k] = min(a.ncols - 1, c + a.R) - col0[k] + 1;
+        Ek[k] = __ldg(z + (int64_t)r * a.ncols + c) + a.ht;
+        all_int = all_int && r - a.R - 1 >= 0 && r + a.R + 1 < a.nrows && c - a.R - 1 >= 0 && c + a.R + 1 < a.ncols;
+    }
+    for (int i = threadIdx.x; i < K * bits_stride; i += blockDim.x) s_bits[i] = 0u;
+    __syncthreads();
+    unsigned long long n_cross = 0, n_cells = 0;
+    if (all_int) {
+        vs_events_k<K>(z, rk, ck, Ek, a, rays, groups, events, ngroups, s_bits, bits_stride);
+        if (threadIdx.x == 0) { n_cross = (unsigned long long)(K * a.tmpl_cross); n_cells = (unsigned long long)(K * a.tmpl_cells); }
+    } else {
+        for (int k = 0; k < K; ++k) {
+            if (cand[k] < 0) continue;
+            const bool in = rk[k] - a.R - 1 >= 0 && rk[k] + a.R + 1 < a.nrows && ck[k] - a.R - 1 >= 0 &&
+                            ck[k] + a.R + 1 < a.ncols;
+            if (in)
+                vs_events<true>(z, rk[k], ck[k], Ek[k], row0[k], col0[k], ww[k], a, rays, groups, events, ngroups,
+                                s_bits + k * bits_stride, nullptr, true, n_cross, n_cells);
+            else
+                vs_events<false>(z, rk[k], ck[k], Ek[k], row0[k], col0[k], ww[k], a, rays, groups, events, ngroups,
+                                 s_bits + k * bits_stride, nullptr, true, n_cross, n_cells);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+        if (threadIdx.x == k && cand[k] >= 0) {
+            const int b = (rk[k] - row0[k]) * ww[k] + (ck[k] - col0[k]);
+            atomicOr(&s_bits[k * bits_stride + (b >> 5)], 1u << (b & 31));
+        }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        if (cand[k] < 0) continue;
+        const int nw64 = (hh[k] * ww[k] + 63) >> 6;
+        uint64_t* out = words + cand[k] * a.stride;
+        int pc = 0;
+        for (int i = threadIdx.x; i < nw64; i += blockDim.x) {
+            const uint64_t v = ((uint64_t)s_bits[k * bits_stride + 2 * i + 1] << 32) | s_bits[k * bits_stride + 2 * i];
+            out[i] = v;
+            pc += __popcll(v);
+        }
+        for (int o = 16; o; o >>= 1) pc += __shfl_down_sync(0xffffffffu, pc, o);
+        if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = pc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int t = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_red[w];
+            pops[cand[k]] = t;
+            wins[cand[k]] = make_int4(row0[k], col0[k], hh[k], ww[k]);
+        }
+        __syncthreads();
+    }
+    for (int o = 16; o; o >>= 1) {
+        n_cross += __shfl_down_sync(0xffffffffu, n_cross, o);
+        n_cells += __shfl_down_sync(0xffffffffu, n_cells, o);
+    }
+    if ((threadIdx.x & 31) == 0 && (n_cross || n_cells)) {
+        atomicAdd(counters + kVsCross, n_cross);
+        atomicAdd(counters + kVsCells, n_cells);
+    }
+}
+
 __global__ void k_tile_keys(const int32_t* __restrict__ crow, const int32_t* __restrict__ ccol, int64_t n, int tiles_x,
                             uint32_t* __restrict__ keys, int32_t* __restrict__ idx) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -326,7 +492,7 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
     c->vs_n = n;
     c->vs_stride = mw;
     if (n == 0) return TXS_OK;
-    VsArgs a{(int)c->nrows, (int)c->ncols, p.roi, p.tx_height, p.rx_height, T->nrays, mw, nullptr};
+    VsArgs a{(int)c->nrows, (int)c->ncols, p.roi, p.tx_height, p.rx_height, T->nrays, mw, nullptr, n, 0, 0};
     // Process observers in 64x64-tile order so the CTAs resident at any moment
     // read overlapping terrain windows (L2 reuse; config 5's observers are
     // random over a 537 MB terrain).  Output slots keep candidate order.
@@ -352,7 +518,39 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
     if (n > 0x7fffffff) return fail(c, TXS_ERR_RANGE, "viewshed", "too many candidates");
     const bool smem_bits = smem <= 160 * 1024;
     if (!smem_bits) TXS_CUDA(c, "viewshed", cudaMemsetAsync(c->d_words, 0, sizeof(uint64_t) * n * mw, c->stream));
-    if (T->events) {
+    a.n = n;
+    {
+        const EventTemplate& Et = event_template(p.roi <= kEvMaxRoi ? p.roi : 1);
+        long long cr = 0, ce = 0;
+        for (const uint2& e : Et.events) { const uint32_t t = e.x & 7u; cr += t <= kEvPost; ce += t == kEvCell; }
+        a.tmpl_cross = cr; a.tmpl_cells = ce;
+    }
+    // observers per CTA (measured on B200, profiles/): 4 while the K bitmaps stay
+    // <= 100 KB (R <= 200), 2 at R = 250, 1 when the grid would not fill the SMs
+    int kobs = 1;
+    for (int k : {4, 2})
+        if ((size_t)k * smem <= 100 * 1024 && n >= (int64_t)k * c->num_sms * 4) { kobs = k; break; }
+    if (const char* kenv = getenv("TXS_VS_K")) kobs = atoi(kenv);
+    if (T->events && smem_bits && (kobs == 2 || kobs == 4) && (size_t)kobs * smem <= 200 * 1024) {
+        int best = 1;
+        for (int wv = 1; wv <= 32; ++wv)
+            if (T->ngroups % wv == 0 && std::abs(wv - 12) < std::abs(best - 12)) best = wv;
+        if (best < 4) best = std::min(T->ngroups, 8);
+        const int threads = 32 * best;
+        const size_t sm = (size_t)kobs * smem;
+        const unsigned grid = (unsigned)((n + kobs - 1) / kobs);
+        if (kobs == 2) {
+            if (sm > 48 * 1024)
+                TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(k_viewshed_evk<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            k_viewshed_evk<2><<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
+                                                                 T->ngroups, a, c->d_words, c->d_win, c->d_pop, c->d_counters);
+        } else {
+            if (sm > 48 * 1024)
+                TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(k_viewshed_evk<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            k_viewshed_evk<4><<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
+                                                                 T->ngroups, a, c->d_words, c->d_win, c->d_pop, c->d_counters);
+        }
+    } else if (T->events) {
         // warps per CTA: the divisor of the group count closest to 12 (balanced strides)
         int best = 1;
         for (int wv = 1; wv <= 32; ++wv)
