@@ -45,11 +45,9 @@ const EventTemplate& event_template(int32_t roi);
 
 // Device-side SITE loop state (one struct, read/written by the loop kernels).
 constexpr int kMaxNb = 64;   // neighbour bucket ranges per winner
-struct DeltaWord { int y, wi; unsigned long long d; };   // newly covered bits of one cum word
 struct SiteState {
     unsigned long long best_key;   // (gain << 32) | (0xffffffff - idx), atomicMax target
     unsigned int blocks_done;      // last-block detection in k_argmax
-    int dcount;                    // entries in the delta list this round
     long long nsel;
     long long covered;
     int done;                      // no more commits
@@ -123,8 +121,12 @@ struct txs_ctx {
     uint64_t* d_xfer = nullptr;          // sharded SITE: the broadcast winner window
     size_t xfer_cap = 0;
     uint64_t* d_cum = nullptr;
-    txs::DeltaWord* d_dlist = nullptr;
-    size_t dlist_cap = 0;
+    // per-round delta: newly covered words over the winner window (row pitch
+    // dpitch words) and per-row [lo, hi] spans of non-zero words
+    uint64_t* d_dwin = nullptr;
+    int2* d_dspan = nullptr;
+    size_t dwin_cap = 0, dspan_cap = 0;
+    int64_t dpitch = 0;
     size_t bitmap_cap = 0;
     int32_t* d_gain = nullptr;
     size_t gain_cap = 0;

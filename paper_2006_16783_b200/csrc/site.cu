@@ -34,6 +34,7 @@ constexpr unsigned kFull = 0xffffffffu;
 struct SiteArgs {
     int nrows, ncols, R, bsize, nbx, nby;
     int cr0, cr1;                     // cum region rows held [cr0, cr1)
+    int dpitch;                       // delta window row pitch (words)
     int64_t wpr, n, stride, max_sel;
     double target, total;
 };
@@ -105,7 +106,8 @@ struct LoopPtrs {
 // Grid argmax of (gain << 32 | ~idx); the last CTA to finish takes the
 // round's decision (SPEC.md:367 stop rules in decision-D9 order), records the
 // step and the winner window, and computes the neighbour bucket ranges.
-__global__ void k_argmax(const int32_t* __restrict__ gain, SiteArgs a, SiteState* st, LoopPtrs lp) {
+__global__ void k_argmax(const int32_t* __restrict__ gain, SiteArgs a, SiteState* st, LoopPtrs lp,
+                         int2* __restrict__ dspan) {
     if (st->done) return;
     if (st->finish) {   // previous round committed the final pick
         if (blockIdx.x == 0 && threadIdx.x == 0) st->done = 1;
@@ -129,7 +131,9 @@ __global__ void k_argmax(const int32_t* __restrict__ gain, SiteArgs a, SiteState
         s_last = atomicAdd(&st->blocks_done, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (!s_last || threadIdx.x != 0) return;
+    if (!s_last) return;
+    for (int y = threadIdx.x; y < 2 * a.R + 1; y += blockDim.x) dspan[y] = make_int2(0x7fffffff, -1);
+    if (threadIdx.x != 0) return;
     __threadfence();
     const unsigned long long key = atomicAdd(&st->best_key, 0ull);
     st->best_key = 0ull;
@@ -147,7 +151,6 @@ __global__ void k_argmax(const int32_t* __restrict__ gain, SiteArgs a, SiteState
     st->nsel = k + 1;
     st->w_idx = (int)idx; st->w_gain = g;
     st->w_row0 = win.x; st->w_col0 = win.y; st->w_h = win.z; st->w_w = win.w;
-    st->dcount = 0;
     if (cov >= a.target) { st->finish = 1; st->stop = TXS_STOP_TARGET_REACHED; }
     else if (a.max_sel > 0 && k + 1 >= a.max_sel) { st->finish = 1; st->stop = TXS_STOP_MAX_SELECTED; }
     // neighbours: candidates within 2R rows/cols of the winner (window overlap);
@@ -167,10 +170,11 @@ __global__ void k_argmax(const int32_t* __restrict__ gain, SiteArgs a, SiteState
 }
 
 // Newly covered bits of the winner: d = v_w & ~cum per cum word of its window;
-// cum |= d; non-zero d words appended to the delta list for k_update.
+// cum |= d; d is stored in the window-shaped delta buffer and every row keeps
+// the span [lo, hi] of its non-zero words for k_update.
 // (sharded: the window comes from `xfer` and only the held cum rows are touched)
 __global__ void k_commit(SiteArgs a, SiteState* st, const uint64_t* __restrict__ words, uint64_t* __restrict__ cum,
-                         DeltaWord* __restrict__ dlist, const uint64_t* __restrict__ xfer) {
+                         uint64_t* __restrict__ dwin, int2* __restrict__ dspan, const uint64_t* __restrict__ xfer) {
     if (st->done) return;
     const int idx = st->w_idx;
     const int r0 = st->w_row0, c0 = st->w_col0, h = st->w_h, w = st->w_w;
@@ -178,28 +182,31 @@ __global__ void k_commit(SiteArgs a, SiteState* st, const uint64_t* __restrict__
     const int wlo = c0 >> 6, nwr = ((c0 + w - 1) >> 6) - wlo + 1;
     const int ya = max(r0, a.cr0), yb = min(r0 + h, a.cr1);   // held rows of the window
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < (yb - ya) * nwr; t += gridDim.x * blockDim.x) {
-        const int y = ya + t / nwr, wi = wlo + t % nwr;
+        const int y = ya + t / nwr, b = t % nwr, wi = wlo + b;
         const uint64_t m = col_mask(wi, c0, c0 + w - 1);
         const long long off = (long long)(y - r0) * w + (wi * 64 - c0);
         const int64_t o = (int64_t)y * a.wpr + wi;
         const uint64_t cw = cum[o];
         const uint64_t d = stream64(v, off) & m & ~cw;
+        dwin[(int64_t)(y - r0) * a.dpitch + b] = d;
         if (d) {
             cum[o] = cw | d;
-            dlist[atomicAdd(&st->dcount, 1)] = DeltaWord{y, wi, d};
+            atomicMin(&dspan[y - r0].x, b);
+            atomicMax(&dspan[y - r0].y, b);
         }
     }
 }
 
 // incremental: gain_i -= popc(v_i & delta) for the neighbours i whose window
-// overlaps the winner's; one CTA per neighbour scans the (short, L2-resident)
-// delta list and touches v_i only at delta words inside its window.
+// overlaps the winner's; one CTA per neighbour, its threads over the overlap
+// rows, each row visiting only the delta span of non-zero words.
 constexpr int kUpdThreads = 128;
 
 __global__ void __launch_bounds__(kUpdThreads) k_update(SiteArgs a, const SiteState* __restrict__ st,
                                                          const int4* __restrict__ wins,
                                                          const uint64_t* __restrict__ words,
-                                                         const DeltaWord* __restrict__ dlist,
+                                                         const uint64_t* __restrict__ dwin,
+                                                         const int2* __restrict__ dspan,
                                                          const int32_t* __restrict__ items,
                                                          int32_t* __restrict__ gain,
                                                          unsigned long long* __restrict__ counters) {
@@ -207,8 +214,9 @@ __global__ void __launch_bounds__(kUpdThreads) k_update(SiteArgs a, const SiteSt
     __shared__ int s_red[kUpdThreads / 32];
     __shared__ int s_cnt[kUpdThreads / 32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nb = st->nb_count, total = st->nb_pref[nb], nd = st->dcount;
+    const int nb = st->nb_count, total = st->nb_pref[nb];
     const int wr0 = st->w_row0, wc0 = st->w_col0, wr1 = wr0 + st->w_h - 1, wc1 = wc0 + st->w_w - 1;
+    const int wlo_w = wc0 >> 6;
     unsigned long long bytes_all = 0;
     for (int f = blockIdx.x; f < total; f += gridDim.x) {
         int k = 0;
@@ -219,16 +227,19 @@ __global__ void __launch_bounds__(kUpdThreads) k_update(SiteArgs a, const SiteSt
         const int cl = max(win.y, wc0), ch = min(win.y + win.w - 1, wc1);
         if (ra > rb || cl > ch) continue;   // uniform across the CTA
         const uint64_t* v = words + (int64_t)i * a.stride;
-        const int wlo = cl >> 6, whi = ch >> 6;
+        const int blo = (cl >> 6) - wlo_w, bhi = (ch >> 6) - wlo_w;   // overlap words, winner-relative
         int acc = 0, touched = 0;
-        for (int t = threadIdx.x; t < nd; t += kUpdThreads) {
-            const DeltaWord e = dlist[t];
-            if (e.y < ra || e.y > rb || e.wi < wlo || e.wi > whi) continue;
-            const uint64_t dm = e.d & col_mask(e.wi, cl, ch);
-            if (!dm) continue;
-            const long long off = (long long)(e.y - win.x) * win.w + (e.wi * 64 - win.y);
-            acc += __popcll(stream64(v, off) & dm);
-            ++touched;
+        for (int y = ra + threadIdx.x; y <= rb; y += kUpdThreads) {
+            const int2 sp = dspan[y - wr0];
+            const int lo = max(sp.x, blo), hi = min(sp.y, bhi);
+            for (int b = lo; b <= hi; ++b) {
+                const int wi = wlo_w + b;
+                const uint64_t dm = dwin[(int64_t)(y - wr0) * a.dpitch + b] & col_mask(wi, cl, ch);
+                if (!dm) continue;
+                const long long off = (long long)(y - win.x) * win.w + (wi * 64 - win.y);
+                acc += __popcll(stream64(v, off) & dm);
+                ++touched;
+            }
         }
         for (int o = 16; o; o >>= 1) {
             acc += __shfl_down_sync(kFull, acc, o);
@@ -322,6 +333,7 @@ SiteArgs make_args(txs_ctx* c, const txs_params& p) {
     a.target = p.target_coverage;
     a.total = (double)c->nrows * (double)c->ncols;
     a.cr0 = (int)c->cum_r0; a.cr1 = (int)c->cum_r1;
+    a.dpitch = (int)c->dpitch;
     return a;
 }
 
@@ -332,10 +344,12 @@ txs_status alloc_bitmaps(txs_ctx* c, int64_t r0, int64_t r1) {
     c->cum_r1 = r1;
     const size_t bytes = sizeof(uint64_t) * (size_t)((r1 - r0) * c->wpr + 1);
     if (ensure(c, "site", (void**)&c->d_cum, &c->bitmap_cap, bytes) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
-    // delta list: at most one entry per cum word of a full window
+    // delta window: (2R+1) rows x dpitch words, plus per-row spans
     const int64_t side = 2 * (int64_t)std::max(1, c->vs_roi) + 1;
-    const size_t dl = sizeof(DeltaWord) * (size_t)(side * ((side + 63) / 64 + 1));
-    if (ensure(c, "site", (void**)&c->d_dlist, &c->dlist_cap, dl) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
+    c->dpitch = (side + 63) / 64 + 1;
+    if (ensure(c, "site", (void**)&c->d_dwin, &c->dwin_cap, sizeof(uint64_t) * (size_t)(side * c->dpitch)) != TXS_OK ||
+        ensure(c, "site", (void**)&c->d_dspan, &c->dspan_cap, sizeof(int2) * (size_t)side) != TXS_OK)
+        return TXS_ERR_OUT_OF_MEMORY;
     return TXS_OK;
 }
 
@@ -402,11 +416,11 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
     for (int r = 0; r < kRoundsPerGraph; ++r) {
         if (p.site_mode == 1)
             k_gain_full<int32_t><<<full_blocks, 256, 0, c->stream>>>(a, c->d_state, c->d_win, c->d_words, cumv, c->d_gain, c->d_counters);
-        k_argmax<<<am_blocks, 256, 0, c->stream>>>(c->d_gain, a, c->d_state, lp);
-        k_commit<<<cm_blocks, 256, 0, c->stream>>>(a, c->d_state, c->d_words, cumv, c->d_dlist, nullptr);
+        k_argmax<<<am_blocks, 256, 0, c->stream>>>(c->d_gain, a, c->d_state, lp, c->d_dspan);
+        k_commit<<<cm_blocks, 256, 0, c->stream>>>(a, c->d_state, c->d_words, cumv, c->d_dwin, c->d_dspan, nullptr);
         if (p.site_mode != 1)
-            k_update<<<up_blocks, kUpdThreads, 0, c->stream>>>(a, c->d_state, c->d_win, c->d_words, c->d_dlist,
-                                                               c->d_bucket_items, c->d_gain, c->d_counters);
+            k_update<<<up_blocks, kUpdThreads, 0, c->stream>>>(a, c->d_state, c->d_win, c->d_words, c->d_dwin,
+                                                               c->d_dspan, c->d_bucket_items, c->d_gain, c->d_counters);
     }
     cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
     if (ce != cudaSuccess) return cuda_fail(c, "site", ce);
@@ -493,8 +507,11 @@ __global__ void k_shard_best(const int32_t* __restrict__ gain, const int32_t* __
     }
 }
 
-__global__ void k_shard_prep(SiteArgs a, SiteState* st, int r, int c, int4 win, const int32_t* __restrict__ bstart) {
-    st->done = 0; st->finish = 0; st->dcount = 0; st->w_idx = -1;
+__global__ void k_shard_prep(SiteArgs a, SiteState* st, int r, int c, int4 win, const int32_t* __restrict__ bstart,
+                             int2* __restrict__ dspan) {
+    for (int y = threadIdx.x; y < 2 * a.R + 1; y += blockDim.x) dspan[y] = make_int2(0x7fffffff, -1);
+    if (threadIdx.x != 0) return;
+    st->done = 0; st->finish = 0; st->w_idx = -1;
     st->w_row0 = win.x; st->w_col0 = win.y; st->w_h = win.z; st->w_w = win.w;
     const int by0 = max(0, (r - 2 * a.R) / a.bsize), by1 = min(a.nby - 1, (r + 2 * a.R) / a.bsize);
     const int bx0 = max(0, (c - 2 * a.R) / a.bsize), bx1 = min(a.nbx - 1, (c + 2 * a.R) / a.bsize);
@@ -566,13 +583,13 @@ txs_status shard_site_apply(txs_ctx* c, int32_t row, int32_t col, const txs_wind
         return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "window larger than the engine's roi");
     TXS_CUDA(c, "site", cudaMemcpyAsync(c->d_xfer, words, sizeof(uint64_t) * nw, cudaMemcpyHostToDevice, c->stream));
     TXS_CUDA(c, "site", cudaMemsetAsync(c->d_xfer + nw, 0, sizeof(uint64_t) * 2, c->stream));
-    k_shard_prep<<<1, 1, 0, c->stream>>>(a, c->d_state, row, col, make_int4(win.row0, win.col0, win.h, win.w),
-                                        c->d_bucket_start);
+    k_shard_prep<<<1, 256, 0, c->stream>>>(a, c->d_state, row, col, make_int4(win.row0, win.col0, win.h, win.w),
+                                          c->d_bucket_start, c->d_dspan);
     TXS_LAUNCHED(c, "site");
     uint64_t* cumv = c->d_cum - c->cum_r0 * c->wpr;
-    k_commit<<<16, 256, 0, c->stream>>>(a, c->d_state, c->d_words, cumv, c->d_dlist, c->d_xfer);
+    k_commit<<<16, 256, 0, c->stream>>>(a, c->d_state, c->d_words, cumv, c->d_dwin, c->d_dspan, c->d_xfer);
     TXS_LAUNCHED(c, "site");
-    k_update<<<c->num_sms * 8, kUpdThreads, 0, c->stream>>>(a, c->d_state, c->d_win, c->d_words, c->d_dlist,
+    k_update<<<c->num_sms * 8, kUpdThreads, 0, c->stream>>>(a, c->d_state, c->d_win, c->d_words, c->d_dwin, c->d_dspan,
                                                            c->d_bucket_items, c->d_gain, c->d_counters);
     TXS_LAUNCHED(c, "site");
     c->stats.site_iterations += 1;
