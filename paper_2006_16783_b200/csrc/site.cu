@@ -259,21 +259,60 @@ __global__ void __launch_bounds__(kUpdThreads) k_update(SiteArgs a, const SiteSt
 }
 
 // full rescan: gain_i = popc(v_i & ~cum) over window i (also marginal_gains API)
+// Streaming form: lane j of the candidate's warp reads packed word j (one
+// coalesced, L1-bypassing load per word; the viewshed words are the only HBM
+// stream), locates its 64 window bits (row y, column x; a word spans
+// <= 1 + ceil(64/w) window rows) and ANDs each row segment with the
+// complement of the cum bits extracted from the row-padded, L2-resident cum.
 template <typename G>
 __global__ void k_gain_full(SiteArgs a, const SiteState* st, const int4* __restrict__ wins,
                             const uint64_t* __restrict__ words, const uint64_t* __restrict__ cum,
                             G* __restrict__ gain, unsigned long long* __restrict__ counters) {
-    if (st && st->done) return;
+    if (st && (st->done || st->finish)) return;
     const int lane = threadIdx.x & 31;
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long bytes = 0;
     for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < a.n; i += warps) {
         const int4 win = wins[i];
-        const long long s = warp_window_popc<true>(words + i * a.stride, win, cum, a.wpr, win.x, win.x + win.z - 1,
-                                                   win.y, win.y + win.w - 1, lane);
+        const int w = win.w, nbits = win.z * w, nwords = (nbits + 63) >> 6;
+        const uint64_t* v = words + i * a.stride;
+        const float rcp = __fdividef(1.0f, (float)w);
+        int bit0 = 64 * lane;   // lane's first word; then +2048 bits per step
+        int y = __float2int_rz(__int2float_rn(bit0) * rcp);
+        int x = bit0 - y * w;
+        if (x >= w) { ++y; x -= w; }
+        if (x < 0) { --y; x += w; }
+        int dy = __float2int_rz(2048.0f * rcp), dx = 2048 - dy * w;
+        if (dx >= w) { ++dy; dx -= w; }
+        if (dx < 0) { --dy; dx += w; }
+        int acc = 0;
+        constexpr int U = 4;   // words in flight per lane
+        for (int j0 = lane; j0 < nwords; j0 += 32 * U) {
+            uint64_t vw[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) vw[u] = j0 + 32 * u < nwords ? __ldcs(v + j0 + 32 * u) : 0ull;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                int rem = min(64, nbits - bit0), pos = 0, yy = y, xx = x;
+                while (rem > 0) {
+                    const int len = min(rem, w - xx);
+                    const uint64_t m = len == 64 ? ~0ull : ((1ull << len) - 1);
+                    const int64_t cbit = (int64_t)(win.x + yy) * a.wpr * 64 + win.y + xx;
+                    const int64_t cw = cbit >> 6;
+                    const int sh = (int)(cbit & 63);
+                    uint64_t cb = __ldg(cum + cw) >> sh;
+                    if (sh) cb |= __ldg(cum + cw + 1) << (64 - sh);
+                    acc += __popcll((vw[u] >> pos) & ~cb & m);
+                    pos += len; rem -= len; ++yy; xx = 0;
+                }
+                bit0 += 2048; y += dy; x += dx;
+                if (x >= w) { x -= w; ++y; }
+            }
+        }
+        for (int o = 16; o; o >>= 1) acc += __shfl_down_sync(kFull, acc, o);
         if (lane == 0) {
-            gain[i] = (G)s;
-            bytes += 8ull * (((unsigned long long)win.z * win.w + 63) >> 6);
+            gain[i] = (G)acc;
+            bytes += 8ull * (unsigned long long)nwords;
         }
     }
     if (counters && lane == 0 && bytes) atomicAdd(counters + kSiteBytes, bytes);
