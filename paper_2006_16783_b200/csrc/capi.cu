@@ -506,7 +506,8 @@ txs_status txs_get_viewsheds(txs_ctx* c, int64_t first, int64_t count, txs_windo
     if (!c) return TXS_ERR_INVALID_ARGUMENT;
     if (!c->vs_valid) return fail(c, TXS_ERR_STATE, "viewshed", "no viewsheds");
     if (first < 0 || count < 0 || first + count > c->vs_n) return fail(c, TXS_ERR_INVALID_ARGUMENT, "viewshed", "range");
-    if (words && stride < c->vs_stride) return fail(c, TXS_ERR_INVALID_ARGUMENT, "viewshed", "words_stride too small");
+    const int64_t dstr = max_window_words(c->vs_roi);   // SPEC layout
+    if (words && stride < dstr) return fail(c, TXS_ERR_INVALID_ARGUMENT, "viewshed", "words_stride too small");
     if (count == 0) return TXS_OK;
     cudaSetDevice(c->device);
     std::vector<int4> w(count);
@@ -516,18 +517,23 @@ txs_status txs_get_viewsheds(txs_ctx* c, int64_t first, int64_t count, txs_windo
         pc.resize(count);
         TXS_CUDA(c, "viewshed", cudaMemcpyAsync(pc.data(), c->d_pop + first, 4 * count, cudaMemcpyDeviceToHost, c->stream));
     }
-    if (words)
-        TXS_CUDA(c, "viewshed", cudaMemcpy2DAsync(words, stride * 8, c->d_words + first * c->vs_stride,
-                                                  c->vs_stride * 8, c->vs_stride * 8, count,
-                                                  cudaMemcpyDeviceToHost, c->stream));
+    if (words) {   // convert the resident cum-aligned rows to the SPEC dense layout, in chunks
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(count, (int64_t)(256 << 20) / (8 * dstr)));
+        uint64_t* tmp = nullptr;
+        TXS_CUDA(c, "viewshed", cudaMallocAsync((void**)&tmp, sizeof(uint64_t) * chunk * dstr, c->stream));
+        for (int64_t b = 0; b < count; b += chunk) {
+            const int64_t m = std::min(chunk, count - b);
+            if (viewsheds_to_dense(c, first + b, m, tmp, dstr) != TXS_OK) { cudaFreeAsync(tmp, c->stream); return TXS_ERR_CUDA; }
+            TXS_CUDA(c, "viewshed", cudaMemcpy2DAsync(words + b * stride, stride * 8, tmp, dstr * 8, dstr * 8, m,
+                                                      cudaMemcpyDeviceToHost, c->stream));
+        }
+        TXS_CUDA(c, "viewshed", cudaFreeAsync(tmp, c->stream));
+    }
     TXS_CUDA(c, "viewshed", cudaStreamSynchronize(c->stream));
     for (int64_t i = 0; i < count; ++i) {
         if (wins) wins[i] = txs_window{w[i].x, w[i].y, w[i].z, w[i].w};
         if (pops) pops[i] = pc[i];
-        if (words) {   // zero the tail beyond the window's words (SPEC.md:298 padding)
-            const int64_t nw = ((int64_t)w[i].z * w[i].w + 63) / 64;
-            std::fill(words + i * stride + nw, words + (i + 1) * stride, 0ull);
-        }
+        if (words) std::fill(words + i * stride + dstr, words + (i + 1) * stride, 0ull);
     }
     return TXS_OK;
 }
@@ -537,8 +543,8 @@ txs_status txs_set_viewsheds(txs_ctx* c, int32_t roi, int64_t n, const int32_t* 
     if (!c || n < 0 || roi < 1 || roi > 4000 || (n > 0 && (!rows || !cols || !wins || !words)))
         return TXS_ERR_INVALID_ARGUMENT;
     if (!c->d_z) return fail(c, TXS_ERR_STATE, "site", "no terrain");
-    const int64_t mw = max_window_words(roi);
-    if (stride < mw) return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "words_stride too small");
+    const int64_t dstr = max_window_words(roi), astr = aligned_stride(roi);
+    if (stride < dstr) return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "words_stride too small");
     std::vector<txs_candidate> cand(n);
     std::vector<int4> w(n);
     std::vector<int32_t> pop(n);
@@ -557,20 +563,25 @@ txs_status txs_set_viewsheds(txs_ctx* c, int32_t roi, int64_t n, const int32_t* 
     txs_status st = txs_set_candidates(c, cand.data(), n);
     if (st != TXS_OK) return st;
     cudaSetDevice(c->device);
-    if (ensure(c, "site", (void**)&c->d_words, &c->words_cap, sizeof(uint64_t) * (n * mw + 8)) != TXS_OK ||
-        ensure(c, "site", (void**)&c->d_win, &c->win_cap, sizeof(int4) * std::max<int64_t>(1, n)) != TXS_OK)
-        return TXS_ERR_OUT_OF_MEMORY;
-    if (ensure(c, "site", (void**)&c->d_pop, &c->pop_cap, sizeof(int32_t) * std::max<int64_t>(1, n)) != TXS_OK)
+    if (ensure(c, "site", (void**)&c->d_words, &c->words_cap, sizeof(uint64_t) * (n * astr + 8)) != TXS_OK ||
+        ensure(c, "site", (void**)&c->d_win, &c->win_cap, sizeof(int4) * std::max<int64_t>(1, n)) != TXS_OK ||
+        ensure(c, "site", (void**)&c->d_pop, &c->pop_cap, sizeof(int32_t) * std::max<int64_t>(1, n)) != TXS_OK)
         return TXS_ERR_OUT_OF_MEMORY;
     if (n > 0) {
-        TXS_CUDA(c, "site", cudaMemcpy2DAsync(c->d_words, mw * 8, words, stride * 8, mw * 8, n, cudaMemcpyHostToDevice, c->stream));
+        uint64_t* tmp = nullptr;
+        TXS_CUDA(c, "site", cudaMallocAsync((void**)&tmp, sizeof(uint64_t) * (n * dstr + 2), c->stream));
+        TXS_CUDA(c, "site", cudaMemcpy2DAsync(tmp, dstr * 8, words, stride * 8, dstr * 8, n, cudaMemcpyHostToDevice, c->stream));
+        TXS_CUDA(c, "site", cudaMemsetAsync(tmp + n * dstr, 0, 16, c->stream));
         TXS_CUDA(c, "site", cudaMemcpyAsync(c->d_win, w.data(), sizeof(int4) * n, cudaMemcpyHostToDevice, c->stream));
         TXS_CUDA(c, "site", cudaMemcpyAsync(c->d_pop, pop.data(), 4 * n, cudaMemcpyHostToDevice, c->stream));
+        st = viewsheds_from_dense(c, tmp, dstr, c->d_win, c->d_words, astr, n);
+        cudaFreeAsync(tmp, c->stream);
+        if (st != TXS_OK) return st;
         TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
     }
     c->vs_roi = roi;
     c->vs_n = n;
-    c->vs_stride = mw;
+    c->vs_stride = astr;
     c->vs_valid = true;
     c->site_valid = false;
     return TXS_OK;

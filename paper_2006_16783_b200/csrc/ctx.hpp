@@ -157,7 +157,16 @@ txs_status cuda_fail(txs_ctx* ctx, const char* stage, cudaError_t e);
 txs_status ensure(txs_ctx* ctx, const char* stage, void** p, size_t* cap, size_t bytes);
 txs_status check_params(txs_ctx* ctx, const char* stage, const txs_params* p, bool need_vix);
 txs_status get_template(txs_ctx* ctx, int32_t roi, RayTemplateDev** out);
+// SPEC layout (decision D8): window rows packed densely, LSB-first.
 inline int64_t max_window_words(int64_t roi) { return ((2 * roi + 1) * (2 * roi + 1) + 63) / 64; }
+// Engine-internal layout ("cum-aligned rows"): window row y occupies the
+// terrain's own 64-bit column words (col0>>6) .. ((col0+w-1)>>6), so cell
+// (y, x) is bit (col0+x)&63 of word y*nwr + ((col0+x)>>6) - (col0>>6); bits
+// outside the window are zero.  Every SITE kernel then ANDs whole words with
+// the row-padded cumulative bitmap.  Converted to/from the SPEC layout at the
+// C-ABI (txs_get_viewsheds / txs_set_viewsheds).
+__host__ __device__ inline int win_nwr(int col0, int w) { return ((col0 + w - 1) >> 6) - (col0 >> 6) + 1; }
+inline int64_t aligned_stride(int64_t roi) { return (2 * roi + 1) * ((2 * roi + 63) / 64 + 1); }
 
 // stage launchers (one .cu each)
 txs_status launch_generate(txs_ctx*, int64_t nrows, int64_t ncols, double roughness, uint64_t seed,
@@ -173,6 +182,10 @@ txs_status run_site(txs_ctx*, const txs_params& p, std::vector<txs_step>& steps,
 txs_status launch_marginal_gains(txs_ctx*, const uint64_t* d_cum_dense, int64_t* d_gains);
 txs_status download_cum(txs_ctx*, uint64_t* host_dense);
 txs_status shard_site_begin(txs_ctx*, const txs_params& p);
+// layout conversion for candidates [first, first+count): aligned (resident) <-> dense (SPEC)
+txs_status viewsheds_to_dense(txs_ctx*, int64_t first, int64_t count, uint64_t* d_dense, int64_t dstride);
+txs_status viewsheds_from_dense(txs_ctx*, const uint64_t* d_dense, int64_t dstride, const int4* d_wins,
+                                uint64_t* d_aligned, int64_t astride, int64_t count);
 txs_status shard_site_best(txs_ctx*, uint64_t* key);
 txs_status shard_site_apply(txs_ctx*, int32_t row, int32_t col, const txs_window& win, const uint64_t* words);
 

@@ -39,43 +39,6 @@ struct SiteArgs {
     double target, total;
 };
 
-// 64 bits of a packed window stream starting at bit offset off (off > -64);
-// bits before the stream start read as 0.  May read one word past the stream.
-__device__ __forceinline__ uint64_t stream64(const uint64_t* __restrict__ v, long long off) {
-    if (off < 0) return v[0] << (-off);
-    const long long w = off >> 6;
-    const int s = (int)(off & 63);
-    const uint64_t lo = v[w] >> s;
-    return s ? (lo | (v[w + 1] << (64 - s))) : lo;
-}
-
-// mask of terrain columns [cl, ch] inside word wi
-__device__ __forceinline__ uint64_t col_mask(int wi, int cl, int ch) {
-    const int lo = max(cl - wi * 64, 0), hi = min(ch - wi * 64, 63);
-    if (lo > hi) return 0ull;
-    const uint64_t up = hi == 63 ? ~0ull : ((1ull << (hi + 1)) - 1);
-    return up & ~((1ull << lo) - 1);
-}
-
-// popc over rows [ra, rb] x cols [cl, ch] of (v_i bits) AND (B or ~B), warp-cooperative
-template <bool COMPLEMENT>
-__device__ __forceinline__ long long warp_window_popc(const uint64_t* __restrict__ v, int4 win,
-                                                      const uint64_t* __restrict__ B, int64_t wpr,
-                                                      int ra, int rb, int cl, int ch, int lane) {
-    const int wlo = cl >> 6, whi = ch >> 6, nwr = whi - wlo + 1, nrow = rb - ra + 1;
-    long long acc = 0;
-    for (int t = lane; t < nrow * nwr; t += 32) {
-        const int y = ra + t / nwr, wi = wlo + t % nwr;
-        const uint64_t m = col_mask(wi, cl, ch);
-        const long long off = (long long)(y - win.x) * win.w + (wi * 64 - win.y);
-        uint64_t b = B[(int64_t)y * wpr + wi];
-        if (COMPLEMENT) b = ~b;
-        acc += __popcll(stream64(v, off) & b & m);
-    }
-    for (int o = 16; o; o >>= 1) acc += __shfl_down_sync(kFull, acc, o);
-    return acc;
-}
-
 __global__ void k_init_gains(const int32_t* __restrict__ pop, int32_t* __restrict__ gain, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         gain[i] = pop[i];
@@ -169,9 +132,10 @@ __global__ void k_argmax(const int32_t* __restrict__ gain, SiteArgs a, SiteState
     st->nb_count = nb;
 }
 
-// Newly covered bits of the winner: d = v_w & ~cum per cum word of its window;
-// cum |= d; d is stored in the window-shaped delta buffer and every row keeps
-// the span [lo, hi] of its non-zero words for k_update.
+// Newly covered bits of the winner: d = v_w & ~cum per cum word of its window
+// (the viewshed rows are cum-aligned, so word b of window row y IS cum word
+// (row0+y, (col0>>6)+b)); cum |= d; d is stored in the window-shaped delta
+// buffer and every row keeps the span [lo, hi] of its non-zero words.
 // (sharded: the window comes from `xfer` and only the held cum rows are touched)
 __global__ void k_commit(SiteArgs a, SiteState* st, const uint64_t* __restrict__ words, uint64_t* __restrict__ cum,
                          uint64_t* __restrict__ dwin, int2* __restrict__ dspan, const uint64_t* __restrict__ xfer) {
@@ -179,15 +143,13 @@ __global__ void k_commit(SiteArgs a, SiteState* st, const uint64_t* __restrict__
     const int idx = st->w_idx;
     const int r0 = st->w_row0, c0 = st->w_col0, h = st->w_h, w = st->w_w;
     const uint64_t* v = xfer ? xfer : words + (int64_t)idx * a.stride;
-    const int wlo = c0 >> 6, nwr = ((c0 + w - 1) >> 6) - wlo + 1;
+    const int wlo = c0 >> 6, nwr = win_nwr(c0, w);
     const int ya = max(r0, a.cr0), yb = min(r0 + h, a.cr1);   // held rows of the window
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < (yb - ya) * nwr; t += gridDim.x * blockDim.x) {
-        const int y = ya + t / nwr, b = t % nwr, wi = wlo + b;
-        const uint64_t m = col_mask(wi, c0, c0 + w - 1);
-        const long long off = (long long)(y - r0) * w + (wi * 64 - c0);
-        const int64_t o = (int64_t)y * a.wpr + wi;
+        const int y = ya + t / nwr, b = t % nwr;
+        const int64_t o = (int64_t)y * a.wpr + wlo + b;
         const uint64_t cw = cum[o];
-        const uint64_t d = stream64(v, off) & m & ~cw;
+        const uint64_t d = v[(y - r0) * nwr + b] & ~cw;
         dwin[(int64_t)(y - r0) * a.dpitch + b] = d;
         if (d) {
             cum[o] = cw | d;
@@ -228,16 +190,16 @@ __global__ void __launch_bounds__(kUpdThreads) k_update(SiteArgs a, const SiteSt
         if (ra > rb || cl > ch) continue;   // uniform across the CTA
         const uint64_t* v = words + (int64_t)i * a.stride;
         const int blo = (cl >> 6) - wlo_w, bhi = (ch >> 6) - wlo_w;   // overlap words, winner-relative
+        const int nwr_i = win_nwr(win.y, win.w), shift_i = wlo_w - (win.y >> 6);   // winner word b = i word b+shift
         int acc = 0, touched = 0;
         for (int y = ra + threadIdx.x; y <= rb; y += kUpdThreads) {
             const int2 sp = dspan[y - wr0];
             const int lo = max(sp.x, blo), hi = min(sp.y, bhi);
+            const uint64_t* vr = v + (int64_t)(y - win.x) * nwr_i + shift_i;
             for (int b = lo; b <= hi; ++b) {
-                const int wi = wlo_w + b;
-                const uint64_t dm = dwin[(int64_t)(y - wr0) * a.dpitch + b] & col_mask(wi, cl, ch);
-                if (!dm) continue;
-                const long long off = (long long)(y - win.x) * win.w + (wi * 64 - win.y);
-                acc += __popcll(stream64(v, off) & dm);
+                const uint64_t d = dwin[(int64_t)(y - wr0) * a.dpitch + b];
+                if (!d) continue;
+                acc += __popcll(vr[b] & d);   // both zero outside their windows: the AND is the overlap
                 ++touched;
             }
         }
@@ -259,11 +221,10 @@ __global__ void __launch_bounds__(kUpdThreads) k_update(SiteArgs a, const SiteSt
 }
 
 // full rescan: gain_i = popc(v_i & ~cum) over window i (also marginal_gains API)
-// Streaming form: lane j of the candidate's warp reads packed word j (one
-// coalesced, L1-bypassing load per word; the viewshed words are the only HBM
-// stream), locates its 64 window bits (row y, column x; a word spans
-// <= 1 + ceil(64/w) window rows) and ANDs each row segment with the
-// complement of the cum bits extracted from the row-padded, L2-resident cum.
+// Streaming form over the cum-aligned layout: lane t of the candidate's warp
+// reads word t (one coalesced, L1-bypassing load; the viewshed words are the
+// only HBM stream) = word b of window row y, whose cum counterpart is the
+// L2-resident cum word (row0+y, (col0>>6)+b): gain = sum popc(v & ~cum).
 template <typename G>
 __global__ void k_gain_full(SiteArgs a, const SiteState* st, const int4* __restrict__ wins,
                             const uint64_t* __restrict__ words, const uint64_t* __restrict__ cum,
@@ -274,48 +235,93 @@ __global__ void k_gain_full(SiteArgs a, const SiteState* st, const int4* __restr
     unsigned long long bytes = 0;
     for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < a.n; i += warps) {
         const int4 win = wins[i];
-        const int w = win.w, nbits = win.z * w, nwords = (nbits + 63) >> 6;
+        const int nwr = win_nwr(win.y, win.w), total = win.z * nwr;
         const uint64_t* v = words + i * a.stride;
-        const float rcp = __fdividef(1.0f, (float)w);
-        int bit0 = 64 * lane;   // lane's first word; then +2048 bits per step
-        int y = __float2int_rz(__int2float_rn(bit0) * rcp);
-        int x = bit0 - y * w;
-        if (x >= w) { ++y; x -= w; }
-        if (x < 0) { --y; x += w; }
-        int dy = __float2int_rz(2048.0f * rcp), dx = 2048 - dy * w;
-        if (dx >= w) { ++dy; dx -= w; }
-        if (dx < 0) { --dy; dx += w; }
+        const uint64_t* crow = cum + (int64_t)win.x * a.wpr + (win.y >> 6);
+        // word t -> (y, b): y = t / nwr via incremental steps of 32 words
+        int y = lane / nwr, b = lane - y * nwr;
+        const int dy = 32 / nwr, db = 32 - dy * nwr;
         int acc = 0;
-        constexpr int U = 4;   // words in flight per lane
-        for (int j0 = lane; j0 < nwords; j0 += 32 * U) {
-            uint64_t vw[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) vw[u] = j0 + 32 * u < nwords ? __ldcs(v + j0 + 32 * u) : 0ull;
+        constexpr int U = 4;
+        for (int t0 = lane; t0 < total; t0 += 32 * U) {
+            uint64_t vw[U], cw[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                int rem = min(64, nbits - bit0), pos = 0, yy = y, xx = x;
-                while (rem > 0) {
-                    const int len = min(rem, w - xx);
-                    const uint64_t m = len == 64 ? ~0ull : ((1ull << len) - 1);
-                    const int64_t cbit = (int64_t)(win.x + yy) * a.wpr * 64 + win.y + xx;
-                    const int64_t cw = cbit >> 6;
-                    const int sh = (int)(cbit & 63);
-                    uint64_t cb = __ldg(cum + cw) >> sh;
-                    if (sh) cb |= __ldg(cum + cw + 1) << (64 - sh);
-                    acc += __popcll((vw[u] >> pos) & ~cb & m);
-                    pos += len; rem -= len; ++yy; xx = 0;
-                }
-                bit0 += 2048; y += dy; x += dx;
-                if (x >= w) { x -= w; ++y; }
+                const bool ok = t0 + 32 * u < total;
+                vw[u] = ok ? __ldcs(v + t0 + 32 * u) : 0ull;
+                cw[u] = ok ? __ldg(crow + (int64_t)y * a.wpr + b) : 0ull;
+                y += dy; b += db;
+                if (b >= nwr) { b -= nwr; ++y; }
             }
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc += __popcll(vw[u] & ~cw[u]);
         }
         for (int o = 16; o; o >>= 1) acc += __shfl_down_sync(kFull, acc, o);
         if (lane == 0) {
             gain[i] = (G)acc;
-            bytes += 8ull * (unsigned long long)nwords;
+            bytes += 8ull * (((unsigned long long)win.z * win.w + 63) >> 6);   // SPEC-layout (algorithmic) bytes
         }
     }
     if (counters && lane == 0 && bytes) atomicAdd(counters + kSiteBytes, bytes);
+}
+
+// ---- layout conversion: SPEC dense rows <-> cum-aligned rows ------------------------
+__global__ void k_aligned_to_dense(const uint64_t* __restrict__ al, int64_t astride, const int4* __restrict__ wins,
+                                   int64_t count, uint64_t* __restrict__ dense, int64_t dstride) {
+    const int64_t total = count * dstride;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / dstride;
+        const int j = (int)(t - i * dstride);
+        const int4 win = wins[i];
+        const int w = win.w, nbits = win.z * w, nwr = win_nwr(win.y, w);
+        uint64_t out = 0;
+        if (64 * j < nbits) {
+            const uint64_t* v = al + i * astride;
+            int bit0 = 64 * j, rem = min(64, nbits - bit0), pos = 0;
+            int y = bit0 / w, x = bit0 - y * w;
+            while (rem > 0) {
+                const int len = min(rem, w - x);
+                const int col = (win.y & 63) + x;            // bit position inside the aligned row
+                const int wo = col >> 6, sh = col & 63;
+                const uint64_t* row = v + (int64_t)y * nwr;
+                uint64_t seg = row[wo] >> sh;
+                if (sh && wo + 1 < nwr) seg |= row[wo + 1] << (64 - sh);
+                if (len < 64) seg &= (1ull << len) - 1;
+                out |= seg << pos;
+                pos += len; rem -= len; ++y; x = 0;
+            }
+        }
+        dense[i * dstride + j] = out;
+    }
+}
+
+__global__ void k_dense_to_aligned(const uint64_t* __restrict__ dense, int64_t dstride, const int4* __restrict__ wins,
+                                   int64_t count, uint64_t* __restrict__ al, int64_t astride) {
+    const int64_t total = count * astride;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / astride;
+        const int k = (int)(t - i * astride);
+        const int4 win = wins[i];
+        const int w = win.w, nwr = win_nwr(win.y, w);
+        uint64_t out = 0;
+        if (k < win.z * nwr) {
+            const int y = k / nwr, b = k - y * nwr;
+            const int base = win.y & ~63;                  // column of bit 0 of word 0
+            const int cl = max(win.y, base + 64 * b), ch = min(win.y + w - 1, base + 64 * b + 63);
+            if (cl <= ch) {
+                const uint64_t* dv = dense + i * dstride;
+                const int len = ch - cl + 1;
+                const long long off = (long long)y * w + (cl - win.y);
+                const int64_t wd = off >> 6;
+                const int sh = (int)(off & 63);
+                uint64_t seg = dv[wd] >> sh;
+                if (sh && 64 - sh < len) seg |= dv[wd + 1] << (64 - sh);
+                if (len < 64) seg &= (1ull << len) - 1;
+                out = seg << (cl - base - 64 * b);
+            }
+        }
+        al[i * astride + k] = out;
+    }
 }
 
 __global__ void k_dense_to_padded(const uint64_t* __restrict__ dense, uint64_t* __restrict__ pad, int64_t nrows,
@@ -568,6 +574,23 @@ __global__ void k_shard_prep(SiteArgs a, SiteState* st, int r, int c, int4 win, 
 
 }  // namespace
 
+txs_status viewsheds_to_dense(txs_ctx* c, int64_t first, int64_t count, uint64_t* d_dense, int64_t dstride) {
+    if (count <= 0) return TXS_OK;
+    k_aligned_to_dense<<<blocks_for(count * dstride, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+        c->d_words + first * c->vs_stride, c->vs_stride, c->d_win + first, count, d_dense, dstride);
+    TXS_LAUNCHED(c, "viewshed");
+    return TXS_OK;
+}
+
+txs_status viewsheds_from_dense(txs_ctx* c, const uint64_t* d_dense, int64_t dstride, const int4* d_wins,
+                                uint64_t* d_aligned, int64_t astride, int64_t count) {
+    if (count <= 0) return TXS_OK;
+    k_dense_to_aligned<<<blocks_for(count * astride, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+        d_dense, dstride, d_wins, count, d_aligned, astride);
+    TXS_LAUNCHED(c, "site");
+    return TXS_OK;
+}
+
 txs_status shard_site_begin(txs_ctx* c, const txs_params& p) {
     TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
     const int64_t R = c->vs_roi;
@@ -591,7 +614,7 @@ txs_status shard_site_begin(txs_ctx* c, const txs_params& p) {
         TXS_CUDA(c, "site", cudaMemcpyAsync(c->d_cgid, c->h_cgid.data(), sizeof(int32_t) * c->h_cgid.size(),
                                             cudaMemcpyHostToDevice, c->stream));
     }
-    const int64_t mw = max_window_words(R) + 2;
+    const int64_t mw = max_window_words(R) + 2 + aligned_stride(R) + 2;
     if (ensure(c, "site", (void**)&c->d_xfer, &c->xfer_cap, sizeof(uint64_t) * mw) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
     TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
     c->site_valid = true;
@@ -617,16 +640,24 @@ txs_status shard_site_apply(txs_ctx* c, int32_t row, int32_t col, const txs_wind
     txs_params p{};
     p.target_coverage = 1.0;
     const SiteArgs a = make_args(c, p);
-    const int64_t nw = ((int64_t)win.h * win.w + 63) / 64;
-    if (nw + 2 > (int64_t)(c->xfer_cap / sizeof(uint64_t)))
+    const int64_t nw = ((int64_t)win.h * win.w + 63) / 64, dstr = max_window_words(c->vs_roi);
+    const int64_t astr = aligned_stride(c->vs_roi);
+    if (nw > dstr || win.h > 2 * c->vs_roi + 1 || win.w > 2 * c->vs_roi + 1)
         return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "window larger than the engine's roi");
-    TXS_CUDA(c, "site", cudaMemcpyAsync(c->d_xfer, words, sizeof(uint64_t) * nw, cudaMemcpyHostToDevice, c->stream));
-    TXS_CUDA(c, "site", cudaMemsetAsync(c->d_xfer + nw, 0, sizeof(uint64_t) * 2, c->stream));
+    // xfer = [dense words (dstr+2)] [aligned words (astr)] [window int4]
+    uint64_t* xd = c->d_xfer;
+    uint64_t* xa = c->d_xfer + dstr + 2;
+    int4* xw = (int4*)(xa + astr);
+    const int4 w4 = make_int4(win.row0, win.col0, win.h, win.w);
+    TXS_CUDA(c, "site", cudaMemcpyAsync(xd, words, sizeof(uint64_t) * nw, cudaMemcpyHostToDevice, c->stream));
+    TXS_CUDA(c, "site", cudaMemsetAsync(xd + nw, 0, sizeof(uint64_t) * (dstr + 2 - nw), c->stream));
+    TXS_CUDA(c, "site", cudaMemcpyAsync(xw, &w4, sizeof(int4), cudaMemcpyHostToDevice, c->stream));
+    if (viewsheds_from_dense(c, xd, dstr, xw, xa, astr, 1) != TXS_OK) return TXS_ERR_CUDA;
     k_shard_prep<<<1, 256, 0, c->stream>>>(a, c->d_state, row, col, make_int4(win.row0, win.col0, win.h, win.w),
                                           c->d_bucket_start, c->d_dspan);
     TXS_LAUNCHED(c, "site");
     uint64_t* cumv = c->d_cum - c->cum_r0 * c->wpr;
-    k_commit<<<16, 256, 0, c->stream>>>(a, c->d_state, c->d_words, cumv, c->d_dwin, c->d_dspan, c->d_xfer);
+    k_commit<<<16, 256, 0, c->stream>>>(a, c->d_state, c->d_words, cumv, c->d_dwin, c->d_dspan, xa);
     TXS_LAUNCHED(c, "site");
     k_update<<<c->num_sms * 8, kUpdThreads, 0, c->stream>>>(a, c->d_state, c->d_win, c->d_words, c->d_dwin, c->d_dspan,
                                                            c->d_bucket_items, c->d_gain, c->d_counters);

@@ -29,8 +29,25 @@ struct VsArgs {
     int64_t stride;       // u64 words per viewshed slot
     const int32_t* perm;  // processing order (spatially sorted), or null
     int64_t n;            // observers
+    int sbits;            // smem bitmap u32 words per observer: (2R+1) rows x (2*Wmax+1) (odd pitch)
     long long tmpl_cross, tmpl_cells;   // template crossings / cells (interior observers)
 };
+
+// Aligned output word b of window row y, gathered from the window-dense smem
+// bitmap (row-major h x w bits): the smem copy stays compact (3 CTAs/SM at
+// R=250) and the cum-aligned layout is produced on the way out.
+__device__ __forceinline__ uint64_t aligned_word_from_dense(const uint32_t* sb, int y, int b, int col0, int w) {
+    const int base = col0 & ~63;
+    const int cl = max(col0, base + 64 * b), ch = min(col0 + w - 1, base + 64 * b + 63);
+    if (cl > ch) return 0ull;
+    const int off = y * w + (cl - col0), len = ch - cl + 1;
+    const int w0 = off >> 5, sh = off & 31;
+    const uint64_t lo = (uint64_t)sb[w0] | ((uint64_t)sb[w0 + 1] << 32);
+    uint64_t seg = lo >> sh;
+    if (sh) seg |= (uint64_t)sb[w0 + 2] << (64 - sh);
+    if (len < 64) seg &= (1ull << len) - 1;
+    return seg << (cl - base - 64 * b);
+}
 
 template <bool SMEM_BITS>
 __global__ void k_viewshed(const int16_t* __restrict__ z, const int32_t* __restrict__ crow,
@@ -44,10 +61,14 @@ __global__ void k_viewshed(const int16_t* __restrict__ z, const int32_t* __restr
     const int r = crow[cand], c = ccol[cand];
     const int row0 = max(0, r - a.R), col0 = max(0, c - a.R);
     const int h = min(a.nrows - 1, r + a.R) - row0 + 1, w = min(a.ncols - 1, c + a.R) - col0 + 1;
-    const int nbits = h * w, nw64 = (nbits + 63) >> 6;
+    // smem: window-dense bits (RS = w); global: cum-aligned rows (RS = nwr*64)
+    const int nwr = win_nwr(col0, w);
+    const int abase = SMEM_BITS ? col0 : (col0 & ~63);
+    const int RS = SMEM_BITS ? w : nwr << 6;
+    const int nw64 = h * nwr;
     uint64_t* out = words + cand * a.stride;
     if (SMEM_BITS) {
-        for (int i = threadIdx.x; i < 2 * nw64; i += blockDim.x) s_bits[i] = 0u;
+        for (int i = threadIdx.x; i < (h * w + 31) / 32 + 3; i += blockDim.x) s_bits[i] = 0u;
         __syncthreads();
     }
     auto set_bit = [&](int k) {
@@ -118,16 +139,17 @@ __global__ void k_viewshed(const int16_t* __restrict__ z, const int32_t* __restr
             ++n_cells;
             const int P = Z(rr, cc) + a.hr - E;
             if (!has || (long long)P * L2 * MH >= (long long)NH * dot)
-                set_bit((rr - row0) * w + (cc - col0));
+                set_bit((rr - row0) * RS + (cc - abase));
         }
     }
-    if (threadIdx.x == 0) set_bit((r - row0) * w + (c - col0));
+    if (threadIdx.x == 0) set_bit((r - row0) * RS + (c - abase));
     __syncthreads();
     int pc = 0;
     for (int i = threadIdx.x; i < nw64; i += blockDim.x) {
         uint64_t v;
         if (SMEM_BITS) {
-            v = ((uint64_t)s_bits[2 * i + 1] << 32) | s_bits[2 * i];
+            const int y = i / nwr;
+            v = aligned_word_from_dense(s_bits, y, i - y * nwr, col0, w);
             out[i] = v;
         } else {
             v = out[i];
@@ -166,7 +188,7 @@ __global__ void k_viewshed(const int16_t* __restrict__ z, const int32_t* __restr
 constexpr int kVsUnroll = 4;
 
 template <bool INTERIOR>
-__device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, int c, int E, int row0, int col0, int w,
+__device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, int c, int E, int row0, int abase, int RS,
                                           const VsArgs& a, const int4* __restrict__ rays,
                                           const int2* __restrict__ groups, const uint2* __restrict__ events,
                                           int ngroups, uint32_t* s_bits, uint64_t* gout, bool smem_bits,
@@ -174,8 +196,8 @@ __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int16_t* __restrict__ P = z + (int64_t)r * a.ncols + c;
     const int Ehr = E - a.hr;
-    // interior observers: unclipped window, bit = (dr+R)*(2R+1) + (dc+R)
-    const int W2 = 2 * a.R + 1, K0 = a.R * W2 + a.R;
+    // cell (r+dr, c+dc) -> aligned bit (r+dr-row0)*RS + (c+dc-abase) = dr*RS + dc + K0
+    const int K0 = (r - row0) * RS + (c - abase);
     for (int g = warp; g < ngroups; g += nwarps) {
         const int2 grp = __ldg(groups + g);
         const int ray = g * 32 + lane;
@@ -207,10 +229,8 @@ __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, 
                     const int r1 = rr + (iscol ? sp : 0), c1 = cc + (isrow ? sq : 0);
                     inb = inb && rr >= 0 && rr < a.nrows && cc >= 0 && cc < a.ncols && r1 >= 0 && r1 < a.nrows &&
                           c1 >= 0 && c1 < a.ncols;
-                    kb[u] = (rr - row0) * w + (cc - col0);
-                } else {
-                    kb[u] = dr * W2 + dc + K0;
                 }
+                kb[u] = dr * RS + dc + K0;
                 const int off0 = inb ? dr * a.ncols + dc : 0;
                 const int off1 = inb ? off0 + (iscol ? stepr : (isrow ? stepc : 0)) : 0;
                 z0[u] = __ldg(P + off0);
@@ -255,11 +275,11 @@ __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, 
 // no bounds tests and no counting (the template's totals are added instead).
 template <int K>
 __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const int* rk, const int* ck, const int* Ek,
+                                            const int* RSk, const int* K0k,
                                             const VsArgs& a, const int4* __restrict__ rays,
                                             const int2* __restrict__ groups, const uint2* __restrict__ events,
                                             int ngroups, uint32_t* s_bits, int bits_stride) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const int W2 = 2 * a.R + 1, K0 = a.R * W2 + a.R;
     const int16_t* __restrict__ P[K];
     int Ehr[K];
 #pragma unroll
@@ -282,14 +302,14 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
         const uint2* ev = events + (int64_t)grp.x * 32 + lane;
         for (int st0 = 0; st0 < grp.y; st0 += 2) {
             uint2 ee[2];
-            int z0[2][K], z1[2][K], kb[2];
+            int z0[2][K], z1[2][K], dru[2], dcu[2];
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 ee[u] = st0 + u < grp.y ? __ldg(ev + (int64_t)(st0 + u) * 32) : make_uint2((uint32_t)kEvNop, 0u);
                 const uint32_t e = ee[u].x, type = e & 7u;
                 const int dr = ((int)(e << 20)) >> 23, dc = ((int)(e << 11)) >> 23;
                 const bool isrow = type == kEvRow, iscol = type == kEvCol;
-                kb[u] = dr * W2 + dc + K0;
+                dru[u] = dr; dcu[u] = dc;
                 const int off0 = type != kEvNop ? dr * a.ncols + dc : 0;
                 const int off1 = off0 + (iscol ? stepr : (isrow ? stepc : 0));
 #pragma unroll
@@ -314,7 +334,7 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
                     const long long rhs = (long long)NH[k] * y;
                     if (iscross && (!has[k] || lhs > rhs)) { has[k] = true; NH[k] = X; MH[k] = y; L2MH[k] = L2 * y; }
                     if (iscell && (!has[k] || lhs >= rhs)) {
-                        const int kk = kb[u];
+                        const int kk = dru[u] * RSk[k] + dcu[u] + K0k[k];
                         atomicOr(&s_bits[k * bits_stride + (kk >> 5)], 1u << (kk & 31));
                     }
                 }
@@ -335,10 +355,14 @@ __global__ void k_viewshed_ev(const int16_t* __restrict__ z, const int32_t* __re
     const int r = crow[cand], c = ccol[cand];
     const int row0 = max(0, r - a.R), col0 = max(0, c - a.R);
     const int h = min(a.nrows - 1, r + a.R) - row0 + 1, w = min(a.ncols - 1, c + a.R) - col0 + 1;
-    const int nw64 = (h * w + 63) >> 6;
+    // smem: window-dense bits (RS = w); global: cum-aligned rows (RS = nwr*64)
+    const int nwr = win_nwr(col0, w);
+    const int abase = SMEM_BITS ? col0 : (col0 & ~63);
+    const int RS = SMEM_BITS ? w : nwr << 6;
+    const int nw64 = h * nwr;
     uint64_t* out = words + cand * a.stride;
     if (SMEM_BITS) {
-        for (int i = threadIdx.x; i < 2 * nw64; i += blockDim.x) s_bits[i] = 0u;
+        for (int i = threadIdx.x; i < (h * w + 31) / 32 + 3; i += blockDim.x) s_bits[i] = 0u;
         __syncthreads();
     }
     const int E = __ldg(z + (int64_t)r * a.ncols + c) + a.ht;
@@ -346,11 +370,11 @@ __global__ void k_viewshed_ev(const int16_t* __restrict__ z, const int32_t* __re
     // every crossing/cell post lies within roi+1 of the observer
     const bool interior = r - a.R - 1 >= 0 && r + a.R + 1 < a.nrows && c - a.R - 1 >= 0 && c + a.R + 1 < a.ncols;
     if (interior)
-        vs_events<true>(z, r, c, E, row0, col0, w, a, rays, groups, events, ngroups, s_bits, out, SMEM_BITS, n_cross, n_cells);
+        vs_events<true>(z, r, c, E, row0, abase, RS, a, rays, groups, events, ngroups, s_bits, out, SMEM_BITS, n_cross, n_cells);
     else
-        vs_events<false>(z, r, c, E, row0, col0, w, a, rays, groups, events, ngroups, s_bits, out, SMEM_BITS, n_cross, n_cells);
+        vs_events<false>(z, r, c, E, row0, abase, RS, a, rays, groups, events, ngroups, s_bits, out, SMEM_BITS, n_cross, n_cells);
     if (threadIdx.x == 0) {
-        const int k = (r - row0) * w + (c - col0);
+        const int k = (r - row0) * RS + (c - abase);
         if (SMEM_BITS) atomicOr(&s_bits[k >> 5], 1u << (k & 31));
         else atomicOr((unsigned long long*)&out[k >> 6], 1ull << (k & 63));
     }
@@ -358,7 +382,11 @@ __global__ void k_viewshed_ev(const int16_t* __restrict__ z, const int32_t* __re
     int pc = 0;
     for (int i = threadIdx.x; i < nw64; i += blockDim.x) {
         uint64_t v;
-        if (SMEM_BITS) { v = ((uint64_t)s_bits[2 * i + 1] << 32) | s_bits[2 * i]; out[i] = v; }
+        if (SMEM_BITS) {
+            const int y = i / nwr;
+            v = aligned_word_from_dense(s_bits, y, i - y * nwr, col0, w);
+            out[i] = v;
+        }
         else v = out[i];
         pc += __popcll(v);
     }
@@ -391,22 +419,29 @@ __global__ void k_viewshed_evk(const int16_t* __restrict__ z, const int32_t* __r
                                int32_t* __restrict__ pops, unsigned long long* __restrict__ counters) {
     extern __shared__ __align__(16) uint32_t s_bits[];
     __shared__ int s_red[32];
-    const int bits_stride = (int)(2 * a.stride);
+    const int bits_stride = a.sbits;
     int64_t cand[K];
-    int rk[K], ck[K], Ek[K], row0[K], col0[K], hh[K], ww[K];
+    int rk[K], ck[K], Ek[K], row0[K], col0[K], hh[K], ww[K], RSk[K], K0k[K], abk[K];
     bool all_int = true;
     int nk = 0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const int64_t slot = (int64_t)blockIdx.x * K + k;
         cand[k] = slot < a.n ? (a.perm ? a.perm[slot] : slot) : -1;
-        if (cand[k] < 0) { all_int = false; rk[k] = ck[k] = Ek[k] = row0[k] = col0[k] = hh[k] = ww[k] = 0; continue; }
+        if (cand[k] < 0) {
+            all_int = false;
+            rk[k] = ck[k] = Ek[k] = row0[k] = col0[k] = hh[k] = ww[k] = RSk[k] = K0k[k] = abk[k] = 0;
+            continue;
+        }
         ++nk;
         const int r = crow[cand[k]], c = ccol[cand[k]];
         rk[k] = r; ck[k] = c;
         row0[k] = max(0, r - a.R); col0[k] = max(0, c - a.R);
         hh[k] = min(a.nrows - 1, r + a.R) - row0[k] + 1;
         ww[k] = min(a.ncols - 1, c + a.R) - col0[k] + 1;
+        RSk[k] = ww[k];          // smem bitmap: window-dense rows
+        abk[k] = col0[k];
+        K0k[k] = (r - row0[k]) * RSk[k] + (c - abk[k]);
         Ek[k] = __ldg(z + (int64_t)r * a.ncols + c) + a.ht;
         all_int = all_int && r - a.R - 1 >= 0 && r + a.R + 1 < a.nrows && c - a.R - 1 >= 0 && c + a.R + 1 < a.ncols;
     }
@@ -414,7 +449,7 @@ __global__ void k_viewshed_evk(const int16_t* __restrict__ z, const int32_t* __r
     __syncthreads();
     unsigned long long n_cross = 0, n_cells = 0;
     if (all_int) {
-        vs_events_k<K>(z, rk, ck, Ek, a, rays, groups, events, ngroups, s_bits, bits_stride);
+        vs_events_k<K>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride);
         if (threadIdx.x == 0) { n_cross = (unsigned long long)(K * a.tmpl_cross); n_cells = (unsigned long long)(K * a.tmpl_cells); }
     } else {
         for (int k = 0; k < K; ++k) {
@@ -422,28 +457,30 @@ __global__ void k_viewshed_evk(const int16_t* __restrict__ z, const int32_t* __r
             const bool in = rk[k] - a.R - 1 >= 0 && rk[k] + a.R + 1 < a.nrows && ck[k] - a.R - 1 >= 0 &&
                             ck[k] + a.R + 1 < a.ncols;
             if (in)
-                vs_events<true>(z, rk[k], ck[k], Ek[k], row0[k], col0[k], ww[k], a, rays, groups, events, ngroups,
+                vs_events<true>(z, rk[k], ck[k], Ek[k], row0[k], abk[k], RSk[k], a, rays, groups, events, ngroups,
                                 s_bits + k * bits_stride, nullptr, true, n_cross, n_cells);
             else
-                vs_events<false>(z, rk[k], ck[k], Ek[k], row0[k], col0[k], ww[k], a, rays, groups, events, ngroups,
+                vs_events<false>(z, rk[k], ck[k], Ek[k], row0[k], abk[k], RSk[k], a, rays, groups, events, ngroups,
                                  s_bits + k * bits_stride, nullptr, true, n_cross, n_cells);
         }
     }
 #pragma unroll
     for (int k = 0; k < K; ++k)
         if (threadIdx.x == k && cand[k] >= 0) {
-            const int b = (rk[k] - row0[k]) * ww[k] + (ck[k] - col0[k]);
+            const int b = K0k[k];   // the observer's own cell
             atomicOr(&s_bits[k * bits_stride + (b >> 5)], 1u << (b & 31));
         }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         if (cand[k] < 0) continue;
-        const int nw64 = (hh[k] * ww[k] + 63) >> 6;
+        const int nwr = win_nwr(col0[k], ww[k]);
+        const int nw64 = hh[k] * nwr;
         uint64_t* out = words + cand[k] * a.stride;
         int pc = 0;
         for (int i = threadIdx.x; i < nw64; i += blockDim.x) {
-            const uint64_t v = ((uint64_t)s_bits[k * bits_stride + 2 * i + 1] << 32) | s_bits[k * bits_stride + 2 * i];
+            const int y = i / nwr;
+            const uint64_t v = aligned_word_from_dense(s_bits + k * bits_stride, y, i - y * nwr, col0[k], ww[k]);
             out[i] = v;
             pc += __popcll(v);
         }
@@ -482,7 +519,7 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
     RayTemplateDev* T = nullptr;
     txs_status st = get_template(c, p.roi, &T);
     if (st != TXS_OK) return st;
-    const int64_t n = c->ncand, mw = max_window_words(p.roi);
+    const int64_t n = c->ncand, mw = aligned_stride(p.roi);   // engine-internal cum-aligned layout
     TXS_CUDA(c, "viewshed", cudaStreamSynchronize(c->stream));
     if (ensure(c, "viewshed", (void**)&c->d_words, &c->words_cap, sizeof(uint64_t) * (n * mw + 8)) != TXS_OK ||
         ensure(c, "viewshed", (void**)&c->d_win, &c->win_cap, sizeof(int4) * std::max<int64_t>(1, n)) != TXS_OK ||
@@ -492,7 +529,7 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
     c->vs_n = n;
     c->vs_stride = mw;
     if (n == 0) return TXS_OK;
-    VsArgs a{(int)c->nrows, (int)c->ncols, p.roi, p.tx_height, p.rx_height, T->nrays, mw, nullptr, n, 0, 0};
+    VsArgs a{(int)c->nrows, (int)c->ncols, p.roi, p.tx_height, p.rx_height, T->nrays, mw, nullptr, n, 0, 0, 0};
     // Process observers in 64x64-tile order so the CTAs resident at any moment
     // read overlapping terrain windows (L2 reuse; config 5's observers are
     // random over a 537 MB terrain).  Output slots keep candidate order.
@@ -514,7 +551,8 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
                                                                 c->stream));
         a.perm = perm;
     }
-    const size_t smem = sizeof(uint64_t) * (size_t)mw;
+    a.sbits = (int)(((2 * p.roi + 1) * (2 * p.roi + 1) + 31) / 32 + 4);   // window-dense smem bitmap (+pad)
+    const size_t smem = sizeof(uint32_t) * (size_t)a.sbits;
     if (n > 0x7fffffff) return fail(c, TXS_ERR_RANGE, "viewshed", "too many candidates");
     const bool smem_bits = smem <= 160 * 1024;
     if (!smem_bits) TXS_CUDA(c, "viewshed", cudaMemsetAsync(c->d_words, 0, sizeof(uint64_t) * n * mw, c->stream));
@@ -525,11 +563,11 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
         for (const uint2& e : Et.events) { const uint32_t t = e.x & 7u; cr += t <= kEvPost; ce += t == kEvCell; }
         a.tmpl_cross = cr; a.tmpl_cells = ce;
     }
-    // observers per CTA (measured on B200, profiles/): 4 while the K bitmaps stay
-    // <= 100 KB (R <= 200), 2 at R = 250, 1 when the grid would not fill the SMs
+    // observers per CTA (measured on B200 with the cum-aligned output, profiles/):
+    // 2 (C2 20.1 ms vs 21.8 / 25.3 for K=1 / 4; C5 1.85 s vs 1.96 / 2.91 s),
+    // 1 when the grid would not fill the SMs
     int kobs = 1;
-    for (int k : {4, 2})
-        if ((size_t)k * smem <= 100 * 1024 && n >= (int64_t)k * c->num_sms * 4) { kobs = k; break; }
+    if (2 * smem <= 100 * 1024 && n >= (int64_t)2 * c->num_sms * 4) kobs = 2;
     if (const char* kenv = getenv("TXS_VS_K")) kobs = atoi(kenv);
     if (T->events && smem_bits && (kobs == 2 || kobs == 4) && (size_t)kobs * smem <= 200 * 1024) {
         int best = 1;
