@@ -127,6 +127,8 @@ struct txs_ctx {
     int2* d_dspan = nullptr;
     size_t dwin_cap = 0, dspan_cap = 0;
     int64_t dpitch = 0;
+    unsigned long long* d_partials = nullptr;   // persistent SITE loop: per-CTA argmax
+    size_t partials_cap = 0;
     size_t bitmap_cap = 0;
     int32_t* d_gain = nullptr;
     size_t gain_cap = 0;

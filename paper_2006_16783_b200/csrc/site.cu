@@ -19,14 +19,18 @@
 // Bitmaps inside the engine are row-padded (wpr = ceil(ncols/64) words per
 // terrain row) so a window row maps to whole words; the dense row-major
 // CumulativeShed of SPEC.md:351 is produced on download.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
+#include <cstdlib>
 #include <vector>
 
 #include "ctx.hpp"
 
 namespace txs {
 namespace {
+
+namespace cg = cooperative_groups;
 
 constexpr int kRoundsPerGraph = 16;
 constexpr unsigned kFull = 0xffffffffu;
@@ -137,15 +141,12 @@ __global__ void k_argmax(const int32_t* __restrict__ gain, SiteArgs a, SiteState
 // (row0+y, (col0>>6)+b)); cum |= d; d is stored in the window-shaped delta
 // buffer and every row keeps the span [lo, hi] of its non-zero words.
 // (sharded: the window comes from `xfer` and only the held cum rows are touched)
-__global__ void k_commit(SiteArgs a, SiteState* st, const uint64_t* __restrict__ words, uint64_t* __restrict__ cum,
-                         uint64_t* __restrict__ dwin, int2* __restrict__ dspan, const uint64_t* __restrict__ xfer) {
-    if (st->done) return;
-    const int idx = st->w_idx;
-    const int r0 = st->w_row0, c0 = st->w_col0, h = st->w_h, w = st->w_w;
-    const uint64_t* v = xfer ? xfer : words + (int64_t)idx * a.stride;
+__device__ __forceinline__ void commit_body(const SiteArgs& a, int r0, int c0, int h, int w, const uint64_t* __restrict__ v,
+                                            uint64_t* __restrict__ cum, uint64_t* __restrict__ dwin,
+                                            int2* __restrict__ dspan, int tid, int nthreads) {
     const int wlo = c0 >> 6, nwr = win_nwr(c0, w);
     const int ya = max(r0, a.cr0), yb = min(r0 + h, a.cr1);   // held rows of the window
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < (yb - ya) * nwr; t += gridDim.x * blockDim.x) {
+    for (int t = tid; t < (yb - ya) * nwr; t += nthreads) {
         const int y = ya + t / nwr, b = t % nwr;
         const int64_t o = (int64_t)y * a.wpr + wlo + b;
         const uint64_t cw = cum[o];
@@ -159,31 +160,38 @@ __global__ void k_commit(SiteArgs a, SiteState* st, const uint64_t* __restrict__
     }
 }
 
+__global__ void k_commit(SiteArgs a, SiteState* st, const uint64_t* __restrict__ words, uint64_t* __restrict__ cum,
+                         uint64_t* __restrict__ dwin, int2* __restrict__ dspan, const uint64_t* __restrict__ xfer) {
+    if (st->done) return;
+    const uint64_t* v = xfer ? xfer : words + (int64_t)st->w_idx * a.stride;
+    commit_body(a, st->w_row0, st->w_col0, st->w_h, st->w_w, v, cum, dwin, dspan, blockIdx.x * blockDim.x + threadIdx.x,
+                gridDim.x * blockDim.x);
+}
+
 // incremental: gain_i -= popc(v_i & delta) for the neighbours i whose window
 // overlaps the winner's; one CTA per neighbour, its threads over the overlap
 // rows, each row visiting only the delta span of non-zero words.
 constexpr int kUpdThreads = 128;
 
-__global__ void __launch_bounds__(kUpdThreads) k_update(SiteArgs a, const SiteState* __restrict__ st,
-                                                         const int4* __restrict__ wins,
-                                                         const uint64_t* __restrict__ words,
-                                                         const uint64_t* __restrict__ dwin,
-                                                         const int2* __restrict__ dspan,
-                                                         const int32_t* __restrict__ items,
-                                                         int32_t* __restrict__ gain,
-                                                         unsigned long long* __restrict__ counters) {
-    if (st->done || st->finish) return;
-    __shared__ int s_red[kUpdThreads / 32];
-    __shared__ int s_cnt[kUpdThreads / 32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nb = st->nb_count, total = st->nb_pref[nb];
-    const int wr0 = st->w_row0, wc0 = st->w_col0, wr1 = wr0 + st->w_h - 1, wc1 = wc0 + st->w_w - 1;
-    const int wlo_w = wc0 >> 6;
+// One CTA per neighbour f in [first, total) step `stride`: the CTA's threads
+// take the overlap rows (short per-thread dependency chains — this loop is
+// latency-bound), each row visiting only the delta span of non-zero words.
+// nb_* describe the neighbour list (CSR bucket ranges).  Returns the SITE
+// bytes touched (counted by thread 0).
+__device__ __forceinline__ unsigned long long update_body(const SiteArgs& a, int wr0, int wc0, int wh, int ww, int nb,
+                                                          const int* nb_start, const int* nb_pref,
+                                                          const int4* __restrict__ wins, const uint64_t* __restrict__ words,
+                                                          const uint64_t* __restrict__ dwin, const int2* __restrict__ dspan,
+                                                          const int32_t* __restrict__ items, int32_t* __restrict__ gain,
+                                                          int first, int stride, int* s_red, int* s_cnt) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int total = nb_pref[nb];
+    const int wr1 = wr0 + wh - 1, wc1 = wc0 + ww - 1, wlo_w = wc0 >> 6;
     unsigned long long bytes_all = 0;
-    for (int f = blockIdx.x; f < total; f += gridDim.x) {
+    for (int f = first; f < total; f += stride) {
         int k = 0;
-        while (k + 1 < nb && st->nb_pref[k + 1] <= f) ++k;
-        const int i = items[st->nb_start[k] + (f - st->nb_pref[k])];
+        while (k + 1 < nb && nb_pref[k + 1] <= f) ++k;
+        const int i = items[nb_start[k] + (f - nb_pref[k])];
         const int4 win = wins[i];
         const int ra = max(win.x, wr0), rb = min(win.x + win.z - 1, wr1);
         const int cl = max(win.y, wc0), ch = min(win.y + win.w - 1, wc1);
@@ -192,7 +200,7 @@ __global__ void __launch_bounds__(kUpdThreads) k_update(SiteArgs a, const SiteSt
         const int blo = (cl >> 6) - wlo_w, bhi = (ch >> 6) - wlo_w;   // overlap words, winner-relative
         const int nwr_i = win_nwr(win.y, win.w), shift_i = wlo_w - (win.y >> 6);   // winner word b = i word b+shift
         int acc = 0, touched = 0;
-        for (int y = ra + threadIdx.x; y <= rb; y += kUpdThreads) {
+        for (int y = ra + threadIdx.x; y <= rb; y += blockDim.x) {
             const int2 sp = dspan[y - wr0];
             const int lo = max(sp.x, blo), hi = min(sp.y, bhi);
             const uint64_t* vr = v + (int64_t)(y - win.x) * nwr_i + shift_i;
@@ -211,16 +219,130 @@ __global__ void __launch_bounds__(kUpdThreads) k_update(SiteArgs a, const SiteSt
         __syncthreads();
         if (threadIdx.x == 0) {
             int t = 0, tb = 0;
-            for (int q = 0; q < kUpdThreads / 32; ++q) { t += s_red[q]; tb += s_cnt[q]; }
+            for (int q = 0; q < nw; ++q) { t += s_red[q]; tb += s_cnt[q]; }
             if (t) gain[i] -= t;
             bytes_all += 16ull * (unsigned long long)tb;
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0 && bytes_all) atomicAdd(counters + kSiteBytes, bytes_all);
+    return bytes_all;
 }
 
-// full rescan: gain_i = popc(v_i & ~cum) over window i (also marginal_gains API)
+__global__ void __launch_bounds__(kUpdThreads) k_update(SiteArgs a, const SiteState* __restrict__ st,
+                                                         const int4* __restrict__ wins,
+                                                         const uint64_t* __restrict__ words,
+                                                         const uint64_t* __restrict__ dwin,
+                                                         const int2* __restrict__ dspan,
+                                                         const int32_t* __restrict__ items,
+                                                         int32_t* __restrict__ gain,
+                                                         unsigned long long* __restrict__ counters) {
+    if (st->done || st->finish) return;
+    __shared__ int s_red[32], s_cnt[32];
+    const unsigned long long bytes = update_body(a, st->w_row0, st->w_col0, st->w_h, st->w_w, st->nb_count, st->nb_start,
+                                                 st->nb_pref, wins, words, dwin, dspan, items, gain, blockIdx.x,
+                                                 gridDim.x, s_red, s_cnt);
+    if (threadIdx.x == 0 && bytes) atomicAdd(counters + kSiteBytes, bytes);
+}
+
+// ---- persistent SITE loop (one cooperative launch for the whole greedy) ----------
+// Phase A: per-CTA partial argmax of (gain << 32 | ~idx)            -> grid sync
+// Phase B: every CTA reduces the partials (identical winner and stop
+//          decisions everywhere); CTA 0 records the step; all CTAs commit
+//          the winner window into cum and the delta                 -> grid sync
+// Phase C: neighbour gains -= popc(v_i & delta)                      -> grid sync
+// Delta spans are double-buffered so the next round's buffer is reset during
+// the current commit.
+constexpr int kLoopThreads = 256;
+
+__global__ void __launch_bounds__(kLoopThreads) k_site_loop(SiteArgs a, SiteState* st, LoopPtrs lp,
+                                                             int32_t* __restrict__ gain, const int32_t* __restrict__ items,
+                                                             const uint64_t* __restrict__ words, uint64_t* __restrict__ cum,
+                                                             uint64_t* __restrict__ dwin, int2* __restrict__ dspan0,
+                                                             int2* __restrict__ dspan1,
+                                                             unsigned long long* __restrict__ partials,
+                                                             unsigned long long* __restrict__ counters) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ unsigned long long s_key[kLoopThreads / 32];
+    __shared__ int s_red[32], s_cnt[32];
+    __shared__ int s_nb, s_nbstart[kMaxNb], s_nbpref[kMaxNb + 1];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gtid = blockIdx.x * blockDim.x + tid, gthreads = gridDim.x * blockDim.x;
+    const int side = 2 * a.R + 1;
+    if (blockIdx.x == 0)
+        for (int y = tid; y < side; y += blockDim.x) dspan0[y] = make_int2(0x7fffffff, -1);
+    grid.sync();
+    long long nsel = 0, covered = 0;
+    int stop = TXS_STOP_EXHAUSTED;
+    unsigned long long bytes_all = 0;
+    for (int it = 0;; ++it) {
+        int2* sp = (it & 1) ? dspan1 : dspan0;
+        int2* spn = (it & 1) ? dspan0 : dspan1;
+        // ---- A: partial argmax
+        unsigned long long best = 0;
+        for (int64_t i = gtid; i < a.n; i += gthreads)
+            best = umax64(best, ((unsigned long long)(uint32_t)gain[i] << 32) | (0xffffffffull - (uint64_t)i));
+        for (int o = 16; o; o >>= 1) best = umax64(best, __shfl_xor_sync(kFull, best, o));
+        if (lane == 0) s_key[warp] = best;
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long b = 0;
+            for (int k = 0; k < kLoopThreads / 32; ++k) b = umax64(b, s_key[k]);
+            partials[blockIdx.x] = b;
+        }
+        grid.sync();
+        // ---- B: global winner (redundantly in every CTA), step record, commit
+        best = 0;
+        for (int k = tid; k < (int)gridDim.x; k += blockDim.x) best = umax64(best, partials[k]);
+        for (int o = 16; o; o >>= 1) best = umax64(best, __shfl_xor_sync(kFull, best, o));
+        __syncthreads();   // s_key reuse
+        if (lane == 0) s_key[warp] = best;
+        __syncthreads();
+        unsigned long long key = 0;
+        for (int k = 0; k < kLoopThreads / 32; ++k) key = umax64(key, s_key[k]);
+        const int g = (int)(key >> 32);
+        const int64_t idx = (int64_t)(0xffffffffull - (key & 0xffffffffull));
+        if (nsel >= a.n) { stop = TXS_STOP_EXHAUSTED; break; }
+        if (g <= 0) { stop = TXS_STOP_ZERO_GAIN; break; }
+        const int4 win = lp.wins[idx];
+        const int r = lp.crow[idx], c = lp.ccol[idx];
+        covered += g;
+        const double cov = (double)covered / a.total;
+        if (gtid == 0) lp.steps[nsel] = txs_step{idx, r, c, (int64_t)g, cov};
+        ++nsel;
+        commit_body(a, win.x, win.y, win.z, win.w, words + idx * a.stride, cum, dwin, sp, gtid, gthreads);
+        if (blockIdx.x == 0)
+            for (int y = tid; y < side; y += blockDim.x) spn[y] = make_int2(0x7fffffff, -1);
+        if (cov >= a.target) { stop = TXS_STOP_TARGET_REACHED; break; }
+        if (a.max_sel > 0 && nsel >= a.max_sel) { stop = TXS_STOP_MAX_SELECTED; break; }
+        if (tid == 0) {
+            const int by0 = max(0, (r - 2 * a.R) / a.bsize), by1 = min(a.nby - 1, (r + 2 * a.R) / a.bsize);
+            const int bx0 = max(0, (c - 2 * a.R) / a.bsize), bx1 = min(a.nbx - 1, (c + 2 * a.R) / a.bsize);
+            int nb = 0, pref = 0;
+            for (int by = by0; by <= by1 && nb < kMaxNb; ++by) {
+                const int s0 = lp.bstart[by * a.nbx + bx0], e0 = lp.bstart[by * a.nbx + bx1 + 1];
+                s_nbstart[nb] = s0;
+                s_nbpref[nb] = pref;
+                pref += e0 - s0;
+                ++nb;
+            }
+            s_nbpref[nb] = pref;
+            s_nb = nb;
+        }
+        grid.sync();
+        // ---- C: neighbour updates
+        bytes_all += update_body(a, win.x, win.y, win.z, win.w, s_nb, s_nbstart, s_nbpref, lp.wins, words, dwin, sp,
+                                 items, gain, blockIdx.x, gridDim.x, s_red, s_cnt);
+        grid.sync();
+    }
+    if (tid == 0 && bytes_all) atomicAdd(counters + kSiteBytes, bytes_all);
+    if (gtid == 0) {
+        st->nsel = nsel;
+        st->covered = covered;
+        st->stop = stop;
+        st->done = 1;
+    }
+}
+
 // Streaming form over the cum-aligned layout: lane t of the candidate's warp
 // reads word t (one coalesced, L1-bypassing load; the viewshed words are the
 // only HBM stream) = word b of window row y, whose cum counterpart is the
@@ -393,7 +515,7 @@ txs_status alloc_bitmaps(txs_ctx* c, int64_t r0, int64_t r1) {
     const int64_t side = 2 * (int64_t)std::max(1, c->vs_roi) + 1;
     c->dpitch = (side + 63) / 64 + 1;
     if (ensure(c, "site", (void**)&c->d_dwin, &c->dwin_cap, sizeof(uint64_t) * (size_t)(side * c->dpitch)) != TXS_OK ||
-        ensure(c, "site", (void**)&c->d_dspan, &c->dspan_cap, sizeof(int2) * (size_t)side) != TXS_OK)
+        ensure(c, "site", (void**)&c->d_dspan, &c->dspan_cap, sizeof(int2) * (size_t)(2 * side)) != TXS_OK)
         return TXS_ERR_OUT_OF_MEMORY;
     return TXS_OK;
 }
@@ -449,6 +571,44 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
     TXS_CUDA(c, "site", cudaMemsetAsync(c->d_state, 0, sizeof(SiteState), c->stream));
     const int sms = c->num_sms;
     if (init_gains_buckets(c, a, d_scan_tmp, scan_bytes) != TXS_OK) return TXS_ERR_CUDA;
+    const LoopPtrs lp0{c->d_crow, c->d_ccol, c->d_win, c->d_bucket_start, d_steps};
+    // Persistent loop vs graph of per-round kernels (measured, profiles/): the
+    // persistent kernel wins while a round touches few neighbours (C1 0.72 vs
+    // 1.28 ms, C3 47 vs 62 ms); with thousands of neighbours per round (C5) the
+    // per-round kernels' wider update grid wins (109 vs 197 ms).
+    const double span = 4.0 * a.R + 1.0;
+    const double expected_nb = (double)n * span * span / ((double)c->nrows * (double)c->ncols);
+    const bool persistent = p.site_mode == 0 && (expected_nb <= 1000.0 || getenv("TXS_SITE_PERSISTENT")) &&
+                            !getenv("TXS_SITE_GRAPH");
+    if (persistent) {
+        // persistent cooperative loop: as many co-resident CTAs as fit, <= 2 per SM
+        int per_sm = 0;
+        TXS_CUDA(c, "site", cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_site_loop, kLoopThreads, 0));
+        const int grid = std::max(1, std::min(per_sm, 2)) * sms;
+        if (ensure(c, "site", (void**)&c->d_partials, &c->partials_cap, sizeof(unsigned long long) * grid) != TXS_OK)
+            return TXS_ERR_OUT_OF_MEMORY;
+        int2* sp1 = c->d_dspan + (2 * a.R + 1);
+        SiteArgs aa = a;
+        LoopPtrs lpp = lp0;
+        int32_t* g_ = c->d_gain; const int32_t* it_ = c->d_bucket_items; const uint64_t* w_ = c->d_words;
+        uint64_t* cu_ = cumv; uint64_t* dw_ = c->d_dwin; int2* s0_ = c->d_dspan; unsigned long long* pa_ = c->d_partials;
+        unsigned long long* co_ = c->d_counters; SiteState* st_ = c->d_state;
+        void* args[] = {&aa, &st_, &lpp, &g_, &it_, &w_, &cu_, &dw_, &s0_, &sp1, &pa_, &co_};
+        TXS_CUDA(c, "site", cudaLaunchCooperativeKernel((void*)k_site_loop, grid, kLoopThreads, args, 0, c->stream));
+        TXS_LAUNCHED(c, "site");
+        c->stats.site_launches += 1;
+        TXS_CUDA(c, "site", cudaMemcpyAsync(c->h_state, c->d_state, sizeof(SiteState), cudaMemcpyDeviceToHost, c->stream));
+        TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+        const int64_t ns = c->h_state->nsel;
+        c->stats.site_iterations += ns;
+        out.resize((size_t)ns);
+        if (ns > 0) {
+            TXS_CUDA(c, "site", cudaMemcpyAsync(out.data(), d_steps, sizeof(txs_step) * ns, cudaMemcpyDeviceToHost, c->stream));
+            TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+        }
+        *stop = c->h_state->stop;
+        return TXS_OK;
+    }
     // graph of kRoundsPerGraph rounds
     const int am_blocks = blocks_for(n, 256 * 4, sms * 2);
     const int cm_blocks = 16;
