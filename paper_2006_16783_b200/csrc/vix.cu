@@ -109,6 +109,80 @@ __device__ __forceinline__ bool warp_blocked(const int16_t* P, int stride, int d
     return false;
 }
 
+// Per-sample walk geometry, computed by the lane that owns the sample and
+// broadcast with shuffles (one setup per 32 samples instead of per sample).
+struct SegGeom {
+    int nM, nm, stepM, stepm, D, q32, r32;
+    float rcp;
+};
+
+__device__ __forceinline__ SegGeom seg_geom(int dr, int dc, int stride, int D) {
+    SegGeom g;
+    const int nr = abs(dr), nc = abs(dc);
+    const bool rows_major = nr >= nc;
+    g.nM = rows_major ? nr : nc;
+    g.nm = rows_major ? nc : nr;
+    g.stepM = rows_major ? (dr >= 0 ? stride : -stride) : (dc >= 0 ? 1 : -1);
+    g.stepm = rows_major ? (dc >= 0 ? 1 : -1) : (dr >= 0 ? stride : -stride);
+    g.D = D;
+    g.rcp = g.nM ? __fdividef(1.0f, (float)g.nM) : 0.f;
+    const int num = 32 * g.nm;
+    int q = __float2int_rz(__int2float_rn(num) * g.rcp), r = num - q * g.nM;
+    if (r >= g.nM) { ++q; r -= g.nM; }
+    if (r < 0) { --q; r += g.nM; }
+    g.q32 = q; g.r32 = r;
+    return g;
+}
+
+__device__ __forceinline__ SegGeom shfl_geom(const SegGeom& g, int src) {
+    SegGeom o;
+    o.nM = __shfl_sync(kFull, g.nM, src);
+    o.nm = __shfl_sync(kFull, g.nm, src);
+    o.stepM = __shfl_sync(kFull, g.stepM, src);
+    o.stepm = __shfl_sync(kFull, g.stepm, src);
+    o.D = __shfl_sync(kFull, g.D, src);
+    o.q32 = __shfl_sync(kFull, g.q32, src);
+    o.r32 = __shfl_sync(kFull, g.r32, src);
+    o.rcp = __shfl_sync(kFull, g.rcp, src);
+    return o;
+}
+
+// The walk of warp_blocked on precomputed geometry (one step per lane per vote).
+template <bool SMEM>
+__device__ __forceinline__ bool warp_walk(const int16_t* P, const SegGeom& g, int E, int lane) {
+    const int nM = g.nM, nm = g.nm, steps = nM - 1;
+    if (steps <= 0) return false;
+    const int stepM = g.stepM, stepm = g.stepm, D = g.D;
+    int i = 1 + lane;
+    const int num = i * nm;
+    int q = __float2int_rz(__int2float_rn(num) * g.rcp), r = num - q * nM;
+    if (r >= nM) { ++q; r -= nM; }
+    if (r < 0) { --q; r += nM; }
+    int off = i * stepM + q * stepm;                 // post A = (i, q)
+    int rhsM = E * nM + i * D;                       // major-line LOS numerator
+    int rhsm = E * nm + q * D;                       // minor-line LOS numerator
+    const int dOffM = 32 * stepM + g.q32 * stepm, dRhsM = 32 * D, dRhsm = g.q32 * D;
+    for (int k0 = 0; k0 < steps; k0 += 32) {
+        const bool valid = i <= steps;
+        const int oA = valid ? off : 0;
+        const int zA = load_z<SMEM>(P, oA);
+        const int zB = (valid && r) ? load_z<SMEM>(P, oA + stepm) : 0;
+        const int zCl = (lane == 0 && valid) ? load_z<SMEM>(P, oA - stepM) : 0;
+        const int nb = __shfl_up_sync(kFull, zB, 1);
+        const int zC = lane == 0 ? zCl : nb;
+        bool b = valid && zA * (nM - r) + zB * r > rhsM;
+        b |= valid && r > 0 && r < nm && zC * r + zA * (nm - r) > rhsm;
+        if (__any_sync(kFull, b)) return true;
+        i += 32;
+        off += dOffM;
+        rhsM += dRhsM;
+        rhsm += dRhsm;
+        r += g.r32;
+        if (r >= nM) { r -= nM; off += stepm; rhsm += D; }
+    }
+    return false;
+}
+
 __device__ __forceinline__ int warp_of_thread() { return threadIdx.x >> 5; }
 
 // distinct interior crossings of a (dr,dc) segment: |dr|+|dc|-gcd-1 (binary gcd)
@@ -184,25 +258,25 @@ __global__ void __launch_bounds__(kVixThreads, 2) k_vix(const int16_t* __restric
         int vis = 0;
         for (int s0 = 0; s0 < a.S; s0 += 32) {
             const int ns = min(32, a.S - s0);
-            int my_dr = 0, my_dc = 0, my_zt = 0;
-            if (lane < ns) {
-                const int pk = s_samp[s0 + lane];
-                my_dr = (int)(int16_t)(pk & 0xffff);
-                my_dc = pk >> 16;
-                my_zt = T.at(r + my_dr, c + my_dc) + a.hr;
-                n_cross += crossings_of(my_dr, my_dc);
-            }
             const int16_t* P = SMEM ? T.s + (r - T.sr0) * T.sw + (c - T.sc0) : T.g + (int64_t)r * ncols + c;
             const int stride = SMEM ? T.sw : ncols;
             // global path: walk row-major segments on the column-major copy so the
             // lanes' consecutive major steps are contiguous in memory
             const int16_t* PT = SMEM ? P : zt + (int64_t)c * (a.zr1 - a.zr0) + (r - a.zr0);
+            SegGeom my{};
+            bool my_tr = false;
+            if (lane < ns) {
+                const int pk = s_samp[s0 + lane];
+                const int dr = (int)(int16_t)(pk & 0xffff), dc = pk >> 16;
+                const int zt_ = T.at(r + dr, c + dc) + a.hr;
+                n_cross += crossings_of(dr, dc);
+                my_tr = !SMEM && abs(dr) > abs(dc);
+                my = my_tr ? seg_geom(dc, dr, a.zr1 - a.zr0, zt_ - E) : seg_geom(dr, dc, stride, zt_ - E);
+            }
+            const unsigned trmask = __ballot_sync(kFull, my_tr);
             for (int sidx = 0; sidx < ns; ++sidx) {
-                const int dr = __shfl_sync(kFull, my_dr, sidx), dc = __shfl_sync(kFull, my_dc, sidx);
-                const int Zt = __shfl_sync(kFull, my_zt, sidx);
-                const bool tr = !SMEM && abs(dr) > abs(dc);
-                const bool blk = tr ? warp_blocked<SMEM, ILP>(PT, a.zr1 - a.zr0, dc, dr, E, Zt, lane)
-                                    : warp_blocked<SMEM, ILP>(P, stride, dr, dc, E, Zt, lane);
+                const SegGeom g = shfl_geom(my, sidx);
+                const bool blk = warp_walk<SMEM>(((trmask >> sidx) & 1u) ? PT : P, g, E, lane);
                 vis += blk ? 0 : 1;
             }
         }
