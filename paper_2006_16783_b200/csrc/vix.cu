@@ -124,6 +124,7 @@ __device__ __forceinline__ SegGeom seg_geom(int dr, int dc, int stride, int D) {
     g.nm = rows_major ? nc : nr;
     g.stepM = rows_major ? (dr >= 0 ? stride : -stride) : (dc >= 0 ? 1 : -1);
     g.stepm = rows_major ? (dc >= 0 ? 1 : -1) : (dr >= 0 ? stride : -stride);
+    if (g.nm == 0) g.stepm = 0;   // axis-aligned: B (weight 0) must not leave the segment's line
     g.D = D;
     g.rcp = g.nM ? __fdividef(1.0f, (float)g.nM) : 0.f;
     const int num = 32 * g.nm;
@@ -147,7 +148,25 @@ __device__ __forceinline__ SegGeom shfl_geom(const SegGeom& g, int src) {
     return o;
 }
 
-// The walk of warp_blocked on precomputed geometry (one step per lane per vote).
+// The walk of warp_blocked on precomputed geometry (one step per lane per
+// vote).  Rounds where all 32 lanes hold a real step run without validity
+// predicates; B is always loaded (for a valid step q+1 <= m_, so it is a post
+// of the segment's bounding box) and weighted by r.
+template <bool SMEM, bool CHECK>
+__device__ __forceinline__ bool walk_round(const int16_t* P, int nM, int nm, int stepM, int stepm, int steps, int lane,
+                                           int i, int r, int off, int rhsM, int rhsm) {
+    const bool valid = !CHECK || i <= steps;
+    const int oA = valid ? off : 0;
+    const int zA = load_z<SMEM>(P, oA);
+    const int zB = load_z<SMEM>(P, valid ? oA + stepm : 0);
+    const int zCl = lane == 0 ? load_z<SMEM>(P, valid ? oA - stepM : 0) : 0;
+    const int nb = __shfl_up_sync(kFull, zB, 1);
+    const int zC = lane == 0 ? zCl : nb;
+    bool b = zA * (nM - r) + zB * r > rhsM;
+    b |= r > 0 && r < nm && zC * r + zA * (nm - r) > rhsm;
+    return valid && b;
+}
+
 template <bool SMEM>
 __device__ __forceinline__ bool warp_walk(const int16_t* P, const SegGeom& g, int E, int lane) {
     const int nM = g.nM, nm = g.nm, steps = nM - 1;
@@ -162,17 +181,10 @@ __device__ __forceinline__ bool warp_walk(const int16_t* P, const SegGeom& g, in
     int rhsM = E * nM + i * D;                       // major-line LOS numerator
     int rhsm = E * nm + q * D;                       // minor-line LOS numerator
     const int dOffM = 32 * stepM + g.q32 * stepm, dRhsM = 32 * D, dRhsm = g.q32 * D;
-    for (int k0 = 0; k0 < steps; k0 += 32) {
-        const bool valid = i <= steps;
-        const int oA = valid ? off : 0;
-        const int zA = load_z<SMEM>(P, oA);
-        const int zB = (valid && r) ? load_z<SMEM>(P, oA + stepm) : 0;
-        const int zCl = (lane == 0 && valid) ? load_z<SMEM>(P, oA - stepM) : 0;
-        const int nb = __shfl_up_sync(kFull, zB, 1);
-        const int zC = lane == 0 ? zCl : nb;
-        bool b = valid && zA * (nM - r) + zB * r > rhsM;
-        b |= valid && r > 0 && r < nm && zC * r + zA * (nm - r) > rhsm;
-        if (__any_sync(kFull, b)) return true;
+    const int full = steps >> 5;                     // rounds with every lane valid
+    for (int k = 0; k < full; ++k) {
+        if (__any_sync(kFull, walk_round<SMEM, false>(P, nM, nm, stepM, stepm, steps, lane, i, r, off, rhsM, rhsm)))
+            return true;
         i += 32;
         off += dOffM;
         rhsM += dRhsM;
@@ -180,6 +192,8 @@ __device__ __forceinline__ bool warp_walk(const int16_t* P, const SegGeom& g, in
         r += g.r32;
         if (r >= nM) { r -= nM; off += stepm; rhsm += D; }
     }
+    if (steps & 31)
+        return __any_sync(kFull, walk_round<SMEM, true>(P, nM, nm, stepM, stepm, steps, lane, i, r, off, rhsM, rhsm));
     return false;
 }
 
