@@ -11,11 +11,13 @@ CPP_SRC := $(wildcard $(PKG)/csrc/*.cpp)
 HDRS := $(wildcard $(PKG)/csrc/*.hpp $(PKG)/csrc/*.cuh) include/txsite_b200.h
 OBJ := $(CU_SRC:$(PKG)/csrc/%.cu=$(BUILD)/%.o) $(CPP_SRC:$(PKG)/csrc/%.cpp=$(BUILD)/%.cpp.o)
 LIB := $(PKG)/libtxsite_b200.so
+CHECKED := $(PKG)/libtxsite_b200_checked.so
+CHK_OBJ := $(CU_SRC:$(PKG)/csrc/%.cu=$(BUILD)/chk_%.o) $(CPP_SRC:$(PKG)/csrc/%.cpp=$(BUILD)/chk_%.cpp.o)
 
 HOSTLIB := $(PKG)/libtxsite_host.so
 CLI := $(PKG)/bin/txsite
 
-all: $(LIB) $(HOSTLIB) $(CLI) oracle
+all: $(LIB) $(CHECKED) $(HOSTLIB) $(CLI) oracle
 
 $(BUILD):
 	mkdir -p $(BUILD)
@@ -29,6 +31,14 @@ $(BUILD)/%.cpp.o: $(PKG)/csrc/%.cpp $(HDRS) | $(BUILD)
 $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ)
 
+# bounds-checked variant for the tests (terrain loads trap when out of range)
+$(BUILD)/chk_%.o: $(PKG)/csrc/%.cu $(HDRS) | $(BUILD)
+	$(NVCC) $(NVFLAGS) -DTXS_BOUNDS_CHECK -c $< -o $@
+$(BUILD)/chk_%.cpp.o: $(PKG)/csrc/%.cpp $(HDRS) | $(BUILD)
+	$(NVCC) $(NVFLAGS) -DTXS_BOUNDS_CHECK -x cu -c $< -o $@
+$(CHECKED): $(CHK_OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(CHK_OBJ)
+
 $(HOSTLIB): $(PKG)/host/txsite.cpp include/txsite/txsite.hpp include/txsite_b200.h $(LIB)
 	g++ -std=c++17 -O2 -fPIC -shared -Wall -Wextra -Iinclude -o $@ $(PKG)/host/txsite.cpp -L$(PKG) -ltxsite_b200 -Wl,-rpath,'$$ORIGIN'
 
@@ -40,7 +50,7 @@ oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -rf $(BUILD) $(LIB) $(HOSTLIB) $(CLI)
+	rm -rf $(BUILD) $(LIB) $(CHECKED) $(HOSTLIB) $(CLI)
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean

@@ -8,7 +8,10 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtxsite_b200.so")
+# TXS_CHECKED=1 loads the bounds-checked build (tests only; traps on an
+# out-of-range terrain load instead of reading it)
+LIB_PATH = os.path.join(_HERE, "libtxsite_b200_checked.so" if os.environ.get("TXS_CHECKED") == "1"
+                        else "libtxsite_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -76,4 +76,28 @@ __host__ __device__ __forceinline__ int64_t floordiv64(int64_t a, int64_t b) {
     return q;
 }
 
+// ---- bounds-checked build (make checked -> libtxsite_b200_checked.so) ---------
+// Every global terrain load goes through zld(); with TXS_BOUNDS_CHECK it traps
+// on an address outside the held terrain rows (compute-sanitizer is not
+// available on the B200 pool, so the tests run edge-heavy workloads on this
+// build instead).  Release builds compile zld() to a plain __ldg.
+// Two ranges: the held terrain rows and (VIX global path) their column-major copy.
+struct ZBounds { const int16_t* lo; const int16_t* hi; const int16_t* lo2; const int16_t* hi2; };
+#ifdef TXS_BOUNDS_CHECK
+static __device__ ZBounds g_zb;
+__device__ __forceinline__ int zld(const int16_t* p) {
+    if ((p < g_zb.lo || p >= g_zb.hi) && (p < g_zb.lo2 || p >= g_zb.hi2)) __trap();
+    return __ldg(p);
+}
+inline void set_zbounds(const int16_t* lo, const int16_t* hi, cudaStream_t s, const int16_t* lo2 = nullptr,
+                        const int16_t* hi2 = nullptr) {
+    const ZBounds b{lo, hi, lo2, hi2};
+    cudaMemcpyToSymbolAsync(g_zb, &b, sizeof(b), 0, cudaMemcpyHostToDevice, s);
+}
+#else
+__device__ __forceinline__ int zld(const int16_t* p) { return __ldg(p); }
+inline void set_zbounds(const int16_t*, const int16_t*, cudaStream_t, const int16_t* = nullptr,
+                        const int16_t* = nullptr) {}
+#endif
+
 }  // namespace txs

@@ -75,7 +75,7 @@ __global__ void k_viewshed(const int16_t* __restrict__ z, const int32_t* __restr
         if (SMEM_BITS) atomicOr(&s_bits[k >> 5], 1u << (k & 31));
         else atomicOr((unsigned long long*)&out[k >> 6], 1ull << (k & 63));
     };
-    auto Z = [&](int rr, int cc) -> int { return __ldg(z + (int64_t)rr * a.ncols + cc); };
+    auto Z = [&](int rr, int cc) -> int { return zld(z + (int64_t)rr * a.ncols + cc); };
     const int E = Z(r, c) + a.ht;
     unsigned long long n_cross = 0, n_cells = 0;
 
@@ -233,8 +233,8 @@ __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, 
                 kb[u] = dr * RS + dc + K0;
                 const int off0 = inb ? dr * a.ncols + dc : 0;
                 const int off1 = inb ? off0 + (iscol ? stepr : (isrow ? stepc : 0)) : 0;
-                z0[u] = __ldg(P + off0);
-                z1[u] = __ldg(P + off1);
+                z0[u] = zld(P + off0);
+                z1[u] = zld(P + off1);
                 ok[u] = inb;
             }
 #pragma unroll
@@ -314,8 +314,8 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
                 const int off1 = off0 + (iscol ? stepr : (isrow ? stepc : 0));
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
-                    z0[u][k] = __ldg(P[k] + off0);
-                    z1[u][k] = __ldg(P[k] + off1);
+                    z0[u][k] = zld(P[k] + off0);
+                    z1[u][k] = zld(P[k] + off1);
                 }
             }
 #pragma unroll
@@ -365,7 +365,7 @@ __global__ void k_viewshed_ev(const int16_t* __restrict__ z, const int32_t* __re
         for (int i = threadIdx.x; i < (h * w + 31) / 32 + 3; i += blockDim.x) s_bits[i] = 0u;
         __syncthreads();
     }
-    const int E = __ldg(z + (int64_t)r * a.ncols + c) + a.ht;
+    const int E = zld(z + (int64_t)r * a.ncols + c) + a.ht;
     unsigned long long n_cross = 0, n_cells = 0;
     // every crossing/cell post lies within roi+1 of the observer
     const bool interior = r - a.R - 1 >= 0 && r + a.R + 1 < a.nrows && c - a.R - 1 >= 0 && c + a.R + 1 < a.ncols;
@@ -442,7 +442,7 @@ __global__ void k_viewshed_evk(const int16_t* __restrict__ z, const int32_t* __r
         RSk[k] = ww[k];          // smem bitmap: window-dense rows
         abk[k] = col0[k];
         K0k[k] = (r - row0[k]) * RSk[k] + (c - abk[k]);
-        Ek[k] = __ldg(z + (int64_t)r * a.ncols + c) + a.ht;
+        Ek[k] = zld(z + (int64_t)r * a.ncols + c) + a.ht;
         all_int = all_int && r - a.R - 1 >= 0 && r + a.R + 1 < a.nrows && c - a.R - 1 >= 0 && c + a.R + 1 < a.ncols;
     }
     for (int i = threadIdx.x; i < K * bits_stride; i += blockDim.x) s_bits[i] = 0u;
@@ -520,6 +520,7 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
     txs_status st = get_template(c, p.roi, &T);
     if (st != TXS_OK) return st;
     const int64_t n = c->ncand, mw = aligned_stride(p.roi);   // engine-internal cum-aligned layout
+    set_zbounds(c->d_z, c->d_z + c->z_rows * c->ncols, c->stream);
     TXS_CUDA(c, "viewshed", cudaStreamSynchronize(c->stream));
     if (ensure(c, "viewshed", (void**)&c->d_words, &c->words_cap, sizeof(uint64_t) * (n * mw + 8)) != TXS_OK ||
         ensure(c, "viewshed", (void**)&c->d_win, &c->win_cap, sizeof(int4) * std::max<int64_t>(1, n)) != TXS_OK ||

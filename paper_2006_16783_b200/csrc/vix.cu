@@ -51,7 +51,7 @@ struct TerrainView {
 template <bool SMEM>
 __device__ __forceinline__ int load_z(const int16_t* base, int off) {
     if (SMEM) return base[off];
-    return __ldg(base + off);
+    return zld(base + off);
 }
 
 template <bool SMEM, int ILP>
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kVixThreads, 2) k_vix(const int16_t* __restric
         const int sh = r1 - r0 + 1, sw = c1 - c0 + 1;
         for (int i = threadIdx.x; i < sh * sw; i += kVixThreads) {
             const int y = i / sw, x = i - y * sw;
-            s_tile[i] = __ldg(z + (int64_t)(r0 + y) * ncols + c0 + x);
+            s_tile[i] = zld(z + (int64_t)(r0 + y) * ncols + c0 + x);
         }
         T.s = s_tile; T.sr0 = r0; T.sc0 = c0; T.sw = sw;
         __syncthreads();
@@ -328,7 +328,7 @@ __global__ void k_los_batch(const int16_t* __restrict__ z, int nrows, int ncols,
     if (w >= n) return;
     const int4 p = pairs[w];
     const int16_t* P = z + (int64_t)p.x * ncols + p.y;
-    const int E = __ldg(P) + ht, Zt = __ldg(z + (int64_t)p.z * ncols + p.w) + hr;
+    const int E = zld(P) + ht, Zt = zld(z + (int64_t)p.z * ncols + p.w) + hr;
     const bool blocked = warp_blocked<false, 1>(P, ncols, p.z - p.x, p.w - p.y, E, Zt, lane);
     if (lane == 0) out[w] = blocked ? 0 : 1;
 }
@@ -357,6 +357,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         return TXS_OK;
     };
     txs_status st;
+    set_zbounds(c->d_z, c->d_z + c->z_rows * c->ncols, c->stream);
     if (smem <= 110 * 1024) {   // two CTAs per SM
         st = go(k_vix<true, 1>, smem);
     } else {
@@ -368,6 +369,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
             TXS_LAUNCHED(c, "vix");
             c->zt_valid = true;
         }
+        set_zbounds(c->d_z, c->d_z + c->z_rows * c->ncols, c->stream, c->d_zt, c->d_zt + c->z_rows * c->ncols);
         st = go(k_vix<false, 1>, samp);
     }
     if (st != TXS_OK) return st;
@@ -378,6 +380,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
 txs_status launch_los_batch(txs_ctx* c, const int32_t* d_pairs, int64_t n, int32_t ht, int32_t hr, uint8_t* d_out) {
     const int64_t threads = n * 32;
     const unsigned blocks = (unsigned)((threads + 255) / 256);
+    set_zbounds(c->d_z, c->d_z + c->z_rows * c->ncols, c->stream);
     k_los_batch<<<blocks, 256, 0, c->stream>>>(c->zv(), (int)c->nrows, (int)c->ncols, (const int4*)d_pairs, n, ht, hr, d_out);
     TXS_LAUNCHED(c, "los");
     return TXS_OK;

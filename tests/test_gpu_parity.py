@@ -354,3 +354,19 @@ def test_sharded_engine_matches_single(kind, nb):
     assert np.array_equal(res["index"], single["index"])
     assert np.array_equal(res["gain"], single["gain"]) and np.array_equal(res["coverage"], single["coverage"])
     assert np.array_equal(res["cum"], cum)
+
+
+def test_bounds_checked_build_edge_workloads():
+    """compute-sanitizer is closed on the B200 pool: run edge-heavy workloads
+    (global-path VIX at roi 150 on a 1024^2 grid whose terrain ends on an
+    allocation boundary, corner observers at roi 250, both SITE modes, shards)
+    on the bounds-checked build, where any out-of-range terrain load traps."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TXS_CHECKED="1")
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "memcheck_run.py")], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "sharded" in r.stdout
