@@ -12,6 +12,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # out-of-range terrain load instead of reading it)
 LIB_PATH = os.path.join(_HERE, "libtxsite_b200_checked.so" if os.environ.get("TXS_CHECKED") == "1"
                         else "libtxsite_b200.so")
+# TXS_LIB=<path> loads an alternative build of the same C-ABI (kernel A/B runs)
+LIB_PATH = os.environ.get("TXS_LIB", LIB_PATH)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

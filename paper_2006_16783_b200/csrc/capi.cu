@@ -113,7 +113,7 @@ void txs_destroy(txs_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    void* bufs[] = {c->d_z, c->d_zt, c->d_vix, c->d_crow, c->d_ccol, c->d_cscore, c->d_words, c->d_win,
+    void* bufs[] = {c->d_z, c->d_zt, c->d_pairs, c->d_vix, c->d_crow, c->d_ccol, c->d_cscore, c->d_words, c->d_win,
                     c->d_pop, c->d_cum, c->d_dwin, c->d_dspan, c->d_partials, c->d_gain, c->d_state,
                     c->d_bucket_start, c->d_bucket_items, c->d_counters, c->d_scratch};
     for (void* p : bufs) if (p) cudaFree(p);
@@ -195,13 +195,11 @@ static txs_status set_dims(txs_ctx* c, int64_t nrows, int64_t ncols) {
     c->sharded = false;
     c->z_off = 0; c->z_rows = nrows; c->band_r0 = 0; c->band_r1 = nrows;
     c->vix_valid = c->cand_valid = c->vs_valid = c->site_valid = false;
-    c->zt_valid = false;
     return TXS_OK;
 }
 
 static void invalidate(txs_ctx* c) {
     c->vix_valid = c->cand_valid = c->vs_valid = c->site_valid = false;
-    c->zt_valid = false;
 }
 
 txs_status txs_set_terrain(txs_ctx* c, const int16_t* z, int64_t nrows, int64_t ncols) {

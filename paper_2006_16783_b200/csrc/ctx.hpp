@@ -85,7 +85,8 @@ struct txs_ctx {
     const int16_t* zv() const { return d_z - z_off * ncols; }   // indexed by global row
     int16_t* d_zt = nullptr;      // column-major copy (VIX global path)
     size_t zt_cap = 0;
-    bool zt_valid = false;
+    void* d_pairs = nullptr;      // quad planes QV+, QV-, QT+, QT- (VIX global path)
+    size_t pairs_cap = 0;
 
     // VixMap: one byte per post
     uint8_t* d_vix = nullptr;

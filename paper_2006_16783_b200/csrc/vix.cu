@@ -305,6 +305,207 @@ __global__ void __launch_bounds__(kVixThreads, 2) k_vix(const int16_t* __restric
     }
 }
 
+// ---- quad-plane global path (roi <= 255) ----------------------------------------
+// Every segment is walked with its major step +1 in memory: a segment whose
+// major component is negative is walked from the receiver instead (same
+// crossings, same exact predicates — the LOS line is symmetric:
+// Zt*M + (M-i)*(E-Zt) = E*M + i*(Zt-E)).  Four planes of uint2 hold, per
+// post A, the two post pairs a step needs:
+//   .x = (A, B)  B = A one minor step on   -> zA*(M-r) + zB*r   (dp2a.lo)
+//   .y = (C, A)  C = A one major step back -> zC*r + zA*(m-r)   (dp2a.hi)
+// so one coalesced 64-bit load and two dp2a (16-bit x 8-bit dot products,
+// exact) evaluate both crossings of a step, with no shuffles:
+//   plane 0 QV+ [y*ncols + c] = {(z(y,c), z(y+1,c)), (z(y,c-1), z(y,c))}   |dc| >= |dr|, minor +row
+//   plane 1 QV- [y*ncols + c] = {(z(y,c), z(y-1,c)), (z(y,c-1), z(y,c))}   minor -row
+//   plane 2 QT+ [c*H + y]     = {(z(y,c), z(y,c+1)), (z(y-1,c), z(y,c))}   |dr| > |dc|, minor +col
+//   plane 3 QT- [c*H + y]     = {(z(y,c), z(y,c-1)), (z(y-1,c), z(y,c))}   minor -col
+// (y = held row, H = held rows; neighbours outside the held terrain are 0
+// and only ever carry weight 0).  Weights: both byte pairs come from one
+// word W = (M + 255r) | (256m - 255r) << 16, linear in r.
+__device__ __forceinline__ uint32_t pk16(int lo, int hi) { return (uint16_t)lo | ((uint32_t)(uint16_t)hi << 16); }
+
+__global__ void k_quads(const int16_t* __restrict__ z, uint2* __restrict__ q, int H, int ncols) {
+    __shared__ int16_t t[34][36];   // held rows y0-1 .. y0+32, cols c0-1 .. c0+32
+    const int c0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    for (int i = tid; i < 34 * 34; i += 256) {
+        const int yy = i / 34, xx = i - yy * 34, y = y0 + yy - 1, c = c0 + xx - 1;
+        t[yy][xx] = (y >= 0 && y < H && c >= 0 && c < ncols) ? z[(int64_t)y * ncols + c] : (int16_t)0;
+    }
+    __syncthreads();
+    const int64_t n = (int64_t)H * ncols;
+    for (int yy = threadIdx.y; yy < 32; yy += 8) {
+        const int y = y0 + yy, c = c0 + threadIdx.x, ty = yy + 1, tx = threadIdx.x + 1;
+        if (y < H && c < ncols) {
+            const int a = t[ty][tx];
+            const uint32_t ca = pk16(t[ty][tx - 1], a);
+            const int64_t w = (int64_t)y * ncols + c;
+            q[w] = make_uint2(pk16(a, t[ty + 1][tx]), ca);
+            q[n + w] = make_uint2(pk16(a, t[ty - 1][tx]), ca);
+        }
+    }
+    for (int xx = threadIdx.y; xx < 32; xx += 8) {
+        const int c = c0 + xx, y = y0 + threadIdx.x, ty = threadIdx.x + 1, tx = xx + 1;
+        if (y < H && c < ncols) {
+            const int a = t[ty][tx];
+            const uint32_t ca = pk16(t[ty - 1][tx], a);
+            const int64_t w = (int64_t)c * H + y;
+            q[2 * n + w] = make_uint2(pk16(a, t[ty][tx + 1]), ca);
+            q[3 * n + w] = make_uint2(pk16(a, t[ty][tx - 1]), ca);
+        }
+    }
+}
+
+__device__ __forceinline__ uint2 qld(const uint2* p) {
+#ifdef TXS_BOUNDS_CHECK
+    const int16_t* s = (const int16_t*)p;
+    if (s < g_zb.lo2 || s + 3 >= g_zb.hi2) __trap();
+#endif
+    return __ldg(p);
+}
+
+// sum of signed 16-bit halves of `pair` times unsigned weight bytes 0,1 (lo) or 2,3 (hi) of w
+__device__ __forceinline__ int dp2lo(uint32_t pair, uint32_t w) {
+    int d;
+    asm("dp2a.lo.s32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(pair), "r"(w), "r"(0));
+    return d;
+}
+__device__ __forceinline__ int dp2hi(uint32_t pair, uint32_t w) {
+    int d;
+    asm("dp2a.hi.s32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(pair), "r"(w), "r"(0));
+    return d;
+}
+
+// Per-sample walk geometry, computed by the lane that owns the sample and kept
+// in shared memory (two 16-byte broadcast loads per sample; the registers of
+// the walk stay free for occupancy).
+struct __align__(16) QuadGeom {
+    const uint2* Q;   // start post's entry in its plane
+    int Es;           // LOS height at the start post (E, or Zt when reversed)
+    int D;            // LOS rise start -> end
+    int nMm;          // M | m << 16 (0: nothing to walk)
+    int sm;           // minor step in plane words
+    int qr32;         // q32 | r32 << 16: advance of (q, r) over 32 major steps
+    float rcp;        // 1/M
+};
+
+#ifndef VIX_MINB
+#define VIX_MINB 4    // CTAs per SM: 64 warps hide the L2 latency of the plane loads
+#endif
+
+__device__ __forceinline__ bool quad_test(uint2 v, int r, int nm, uint32_t wb, int rhsM, int rhsm) {
+    const uint32_t W = wb + (uint32_t)r * 0xFF0100FFu;   // (+255 lo, -255 hi) per unit r
+    return (dp2lo(v.x, W) > rhsM) | (((unsigned)(r - 1) < (unsigned)(nm - 1)) & (dp2hi(v.y, W) > rhsm));
+}
+
+// One segment per warp, lane l taking major steps l+1, l+33, ...; a vote after
+// every 32 steps.  Returns true (uniform) iff the segment is blocked.
+__device__ __forceinline__ bool quad_walk(const QuadGeom& g, int lane) {
+    const int nM = g.nMm & 0xffff, nm = g.nMm >> 16, steps = nM - 1;
+    if (steps <= 0) return false;
+    const uint2* Q = g.Q;
+    const int sm = g.sm, D = g.D;
+    const int q32 = g.qr32 & 0xffff, r32 = g.qr32 >> 16;
+    const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
+    int i = 1 + lane;
+    const int num = i * nm;
+    int q = __float2int_rz(__int2float_rn(num) * g.rcp), r = num - q * nM;
+    if (r >= nM) { ++q; r -= nM; }
+    if (r < 0) { --q; r += nM; }
+    int off = i + q * sm;
+    int rhsM = g.Es * nM + i * D, rhsm = g.Es * nm + q * D;
+    const int dOff = 32 + q32 * sm, dRhsM = 32 * D, dRhsm = q32 * D;
+    for (int k = steps >> 5; k; --k) {
+        if (__any_sync(kFull, quad_test(qld(Q + off), r, nm, wb, rhsM, rhsm))) return true;
+        off += dOff; rhsM += dRhsM; rhsm += dRhsm; r += r32;
+        if (r >= nM) { r -= nM; off += sm; rhsm += D; }
+    }
+    if (steps & 31) {
+        const bool valid = (steps & ~31) + 1 + lane <= steps;
+        return __any_sync(kFull, valid && quad_test(qld(Q + (valid ? off : 0)), r, nm, wb, rhsM, rhsm));
+    }
+    return false;
+}
+
+__global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16_t* __restrict__ z,
+                                                                   const uint2* __restrict__ qp, int nrows, int ncols,
+                                                                   uint8_t* __restrict__ out, VixArgs a,
+                                                                   unsigned long long* __restrict__ counters) {
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    // dynamic smem: [geometry: kVixWarps x 32][samples: kVixWarps x S ints]
+    QuadGeom* s_geo = (QuadGeom*)s_dyn + warp_of_thread() * 32;
+    int* s_samp = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + warp_of_thread() * a.S;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ty0 = a.row0 + (blockIdx.x / a.tiles_x) * kTile, tx0 = (blockIdx.x % a.tiles_x) * kTile;
+    const int R2 = a.R * a.R;
+    unsigned long long n_cross = 0;
+    int n_posts = 0;
+    for (int pi = warp; pi < kTile * kTile; pi += kVixWarps) {
+        const int r = ty0 + pi / kTile, c = tx0 + pi % kTile;
+        if (r >= a.row_end || c >= ncols) continue;
+        const uint64_t base = mix_seed(a.seed, (uint64_t)r, (uint64_t)c);
+        const int E = zld(z + (int64_t)r * ncols + c) + a.ht;
+        // ---- draw S receivers (D6) ----
+        int nacc = 0;
+        for (uint64_t k = 0; nacc < a.S; k += 32) {
+            const int v = (int)fm_mod(a.span, sm_draw(base, k + lane)) - a.R;
+            const int dc = __shfl_down_sync(kFull, v, 1);
+            const int dr = v;
+            const bool ok = !(lane & 1) && dr * dr + dc * dc <= R2 && r + dr >= 0 && r + dr < nrows &&
+                            c + dc >= 0 && c + dc < ncols;
+            const unsigned mask = __ballot_sync(kFull, ok);
+            if (ok) {
+                const int slot = nacc + __popc(mask & ((1u << lane) - 1));
+                if (slot < a.S) s_samp[slot] = (dr & 0xffff) | (dc << 16);
+            }
+            nacc += __popc(mask);
+        }
+        __syncwarp();
+        int vis = 0;
+        for (int s0 = 0; s0 < a.S; s0 += 32) {
+            const int ns = min(32, a.S - s0);
+            if (lane < ns) {
+                const int H = a.zr1 - a.zr0;
+                const int pk = s_samp[s0 + lane];
+                int dr = (int)(int16_t)(pk & 0xffff), dc = pk >> 16;
+                const int Zt = zld(z + (int64_t)(r + dr) * ncols + (c + dc)) + a.hr;
+                n_cross += crossings_of(dr, dc);
+                const bool tr = abs(dr) > abs(dc);
+                const bool rev = tr ? dr < 0 : dc < 0;      // walk from the receiver
+                const int y = r - a.zr0 + (rev ? dr : 0), x = c + (rev ? dc : 0);   // start post
+                if (rev) { dr = -dr; dc = -dc; }
+                const int nM = tr ? dr : dc, nm = tr ? abs(dc) : abs(dr);
+                const bool mneg = (tr ? dc : dr) < 0;
+                const int64_t n = (int64_t)H * ncols;
+                QuadGeom g;
+                g.Q = qp + (tr ? 2 * n + (int64_t)x * H + y : (int64_t)y * ncols + x) + (mneg ? n : 0);
+                g.Es = rev ? Zt : E;
+                g.D = rev ? E - Zt : Zt - E;
+                g.nMm = nM | (nm << 16);
+                const int stride = tr ? H : ncols;
+                g.sm = mneg ? -stride : stride;
+                g.rcp = nM ? __fdividef(1.0f, (float)nM) : 0.f;
+                const int num = 32 * nm;
+                int q = __float2int_rz(__int2float_rn(num) * g.rcp), rr = num - q * nM;
+                if (rr >= nM) { ++q; rr -= nM; }
+                if (rr < 0) { --q; rr += nM; }
+                g.qr32 = q | (rr << 16);
+                s_geo[lane] = g;
+            }
+            __syncwarp();
+            for (int sidx = 0; sidx < ns; ++sidx) vis += quad_walk(s_geo[sidx], lane) ? 0 : 1;
+            __syncwarp();
+        }
+        if (lane == 0) out[(int64_t)r * ncols + c] = (uint8_t)vis;
+        ++n_posts;
+    }
+    for (int o = 16; o; o >>= 1) n_cross += __shfl_down_sync(kFull, n_cross, o);
+    if (lane == 0 && n_posts) {
+        atomicAdd(counters + kVixLos, (unsigned long long)n_posts * a.S);
+        atomicAdd(counters + kVixCrossFull, n_cross);
+    }
+}
+
 // column-major copy of the terrain: zt[c*nrows + r] = z[r*ncols + c]
 __global__ void k_transpose(const int16_t* __restrict__ z, int16_t* __restrict__ zt, int nrows, int ncols) {
     __shared__ int16_t t[32][33];
@@ -348,8 +549,6 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     const int64_t side = kTile + 2 * (int64_t)p.roi;
     const size_t samp = sizeof(int) * (kVixWarps * (size_t)a.S + 4);
     const size_t smem = samp + sizeof(int16_t) * side * side;
-    // measured on B200 (profiles/): one step per lane between warp votes (ILP 1,
-    // steps walked from the transmitter) beat 2 and 4 and receiver-first walks
     auto go = [&](auto kern, size_t sm) -> txs_status {
         if (sm > 48 * 1024) TXS_CUDA(c, "vix", cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         kern<<<(unsigned)tiles, kVixThreads, sm, c->stream>>>(c->zv(), c->d_zt, (int)c->nrows, (int)c->ncols,
@@ -357,17 +556,49 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         return TXS_OK;
     };
     txs_status st;
+    // path (measured on B200, profiles/README.md): the quad planes whenever
+    // roi <= 255 (dp2a weight bytes) and their 32 B/post fit in half the free
+    // HBM -- they beat the shared-memory tile at roi 100 and the column-major
+    // copy at roi 200; else the shared-memory tile when two CTAs fit; else the
+    // column-major copy.  TXS_VIX_PATH=smem|pairs|zt overrides (measurement).
+    size_t freeb = 0, totalb = 0;
+    cudaMemGetInfo(&freeb, &totalb);
+    const size_t qbytes = sizeof(uint2) * 4 * (size_t)(c->z_rows * c->ncols);
+    const bool quads_ok = p.roi <= 255 && (qbytes <= c->pairs_cap || qbytes <= freeb / 2);
+    int path = quads_ok ? 1 : (smem <= 110 * 1024 ? 0 : 2);
+    if (const char* e = getenv("TXS_VIX_PATH")) {
+        if (!strcmp(e, "smem") && smem <= 200 * 1024) path = 0;
+        if (!strcmp(e, "pairs") && p.roi <= 255) path = 1;
+        if (!strcmp(e, "zt")) path = 2;
+    }
     set_zbounds(c->d_z, c->d_z + c->z_rows * c->ncols, c->stream);
-    if (smem <= 110 * 1024) {   // two CTAs per SM
+    if (path == 0) {
         st = go(k_vix<true, 1>, smem);
+    } else if (path == 1) {
+        const int64_t n = c->z_rows * c->ncols;
+        // rebuilt on every call (part of the timed stage; ~1 HBM pass of 34 B/post)
+        if (ensure(c, "vix", (void**)&c->d_pairs, &c->pairs_cap, sizeof(uint2) * 4 * n) != TXS_OK)
+            return TXS_ERR_OUT_OF_MEMORY;
+        {
+            dim3 tb(32, 8), tg((unsigned)((c->ncols + 31) / 32), (unsigned)((c->z_rows + 31) / 32));
+            k_quads<<<tg, tb, 0, c->stream>>>(c->d_z, (uint2*)c->d_pairs, (int)c->z_rows, (int)c->ncols);
+            TXS_LAUNCHED(c, "vix");
+        }
+        const uint2* qp = (const uint2*)c->d_pairs;
+        set_zbounds(c->d_z, c->d_z + n, c->stream, (const int16_t*)qp, (const int16_t*)(qp + 4 * n));
+        const size_t qsm = samp + sizeof(QuadGeom) * kVixWarps * 32;
+        if (qsm > 48 * 1024)
+            TXS_CUDA(c, "vix", cudaFuncSetAttribute(k_vix_quads, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm));
+        k_vix_quads<<<(unsigned)tiles, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols,
+                                                                       c->d_vix - c->band_r0 * c->ncols, a, c->d_counters);
+        st = TXS_OK;
     } else {
-        if (!c->zt_valid) {
-            if (ensure(c, "vix", (void**)&c->d_zt, &c->zt_cap, sizeof(int16_t) * c->z_rows * c->ncols) != TXS_OK)
-                return TXS_ERR_OUT_OF_MEMORY;
+        if (ensure(c, "vix", (void**)&c->d_zt, &c->zt_cap, sizeof(int16_t) * c->z_rows * c->ncols) != TXS_OK)
+            return TXS_ERR_OUT_OF_MEMORY;
+        {
             dim3 tb(32, 8), tg((unsigned)((c->ncols + 31) / 32), (unsigned)((c->z_rows + 31) / 32));
             k_transpose<<<tg, tb, 0, c->stream>>>(c->d_z, c->d_zt, (int)c->z_rows, (int)c->ncols);
             TXS_LAUNCHED(c, "vix");
-            c->zt_valid = true;
         }
         set_zbounds(c->d_z, c->d_z + c->z_rows * c->ncols, c->stream, c->d_zt, c->d_zt + c->z_rows * c->ncols);
         st = go(k_vix<false, 1>, samp);

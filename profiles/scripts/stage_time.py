@@ -1,0 +1,35 @@
+"""Time single stages on a BASELINE configuration (device-side stage timers of
+the C-ABI): python profiles/scripts/stage_time.py c2 vix [reps].  Used for
+kernel A/B measurements (TXS_VIX_PATH / TXS_VS_K env overrides)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+from paper_2006_16783_b200 import Engine  # noqa: E402
+from paper_2006_16783_b200.configs import CONFIGS, params_for, setup_terrain  # noqa: E402
+
+cfg = CONFIGS[sys.argv[1]]
+stages = sys.argv[2].split(",")
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+e = Engine()
+setup_terrain(e, cfg)
+p = params_for(cfg)
+out = {}
+for st in stages:
+    ts = []
+    for _ in range(reps + 1):
+        e.reset_stats()
+        if st == "vix":
+            e.estimate_vix(p, copy=False)
+        elif st == "viewshed":
+            if cfg.random_observers:
+                e.random_observers(cfg.random_observers, cfg.observer_seed)
+            else:
+                e.estimate_vix(p, copy=False)
+                e.find_candidates(p, copy=False)
+            e.reset_stats()
+            e.compute_all_viewsheds(p)
+        e.synchronize()
+        ts.append(e.stats()["ms_" + st])
+    out[st] = min(ts[1:])
+print(sys.argv[1], os.environ.get("TXS_VIX_PATH", ""), os.environ.get("TXS_VS_K", ""), out, flush=True)

@@ -96,6 +96,22 @@ def test_vix_rows_bit_exact(engine, roi, samples, ht, hr):
         assert np.array_equal(g[rb:re], o[rb:re]), (rb, int((g[rb:re] != o[rb:re]).sum()))
 
 
+@pytest.mark.parametrize("path", ["smem", "pairs", "zt"])
+@pytest.mark.parametrize("roi,samples,ht,hr", [(60, 24, 15, 5), (141, 33, 0, 30), (255, 9, 20, 20)])
+def test_vix_paths_bit_exact(engine, monkeypatch, path, roi, samples, ht, hr):
+    """Every VIX kernel path (shared-memory tile, quad planes, column-major copy),
+    forced with TXS_VIX_PATH, against the oracle -- including roi 255, where the
+    quad path's dp2a weights reach 255; rows at both grid edges."""
+    T = _T()
+    z = O.generate_fractal(700, 610, 0.7, 21, -500, 3000)
+    engine.set_terrain(z)
+    monkeypatch.setenv("TXS_VIX_PATH", path)
+    g = engine.estimate_vix(T.make_params(roi, ht, hr, samples=samples, seed=31))
+    for rb, re in [(0, 6), (300, 306), (694, 700)]:
+        o = O.estimate_vix(z, roi, ht, hr, samples, 31, rows=(rb, re))
+        assert np.array_equal(g[rb:re], o[rb:re]), (path, rb, int((g[rb:re] != o[rb:re]).sum()))
+
+
 def test_vix_flat_and_tiny(engine):
     T = _T()
     engine.set_terrain(np.full((70, 45), 3, np.int16))
