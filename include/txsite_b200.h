@@ -87,6 +87,7 @@ typedef struct txs_stats {
     int64_t site_launches;          /* kernels launched by the SITE loop                     */
     int64_t candidates;
     int64_t kernel_launches;        /* every kernel this context launched since reset        */
+    double ms_site_rounds;          /* device time of the SITE round loop alone (no setup)   */
 } txs_stats;
 
 typedef struct txs_ctx txs_ctx;

@@ -52,7 +52,7 @@ class Stats(C.Structure):
                 ("ms_site", dbl), ("vix_los", i64), ("vix_crossings_full", i64),
                 ("viewshed_crossings", i64), ("viewshed_cells", i64), ("site_iterations", i64),
                 ("site_bytes", i64), ("site_launches", i64), ("candidates", i64),
-                ("kernel_launches", i64)]
+                ("kernel_launches", i64), ("ms_site_rounds", dbl)]
 
 
 def _sig(name, res, args):

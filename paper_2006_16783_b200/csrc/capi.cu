@@ -98,6 +98,7 @@ txs_status txs_create(int device, txs_ctx** out) {
     c->num_sms = prop.multiProcessorCount;
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
+        cudaEventCreate(&c->ev_r0) != cudaSuccess || cudaEventCreate(&c->ev_r1) != cudaSuccess ||
         cudaMalloc(&c->d_counters, sizeof(unsigned long long) * kNumCounters) != cudaSuccess ||
         cudaMalloc(&c->d_state, sizeof(SiteState)) != cudaSuccess ||
         cudaMallocHost(&c->h_state, sizeof(SiteState)) != cudaSuccess) {
@@ -126,6 +127,8 @@ void txs_destroy(txs_ctx* c) {
     for (cudaEvent_t e : c->user_ev) if (e) cudaEventDestroy(e);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->ev_r0) cudaEventDestroy(c->ev_r0);
+    if (c->ev_r1) cudaEventDestroy(c->ev_r1);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }

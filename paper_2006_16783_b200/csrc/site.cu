@@ -347,6 +347,8 @@ __global__ void __launch_bounds__(kLoopThreads) k_site_loop(SiteArgs a, SiteStat
 // reads word t (one coalesced, L1-bypassing load; the viewshed words are the
 // only HBM stream) = word b of window row y, whose cum counterpart is the
 // L2-resident cum word (row0+y, (col0>>6)+b): gain = sum popc(v & ~cum).
+// (measured: 4 loads in flight per lane at 46 registers beat 8 or 16 in flight
+// and tighter register bounds, profiles/README.md)
 template <typename G>
 __global__ void k_gain_full(SiteArgs a, const SiteState* st, const int4* __restrict__ wins,
                             const uint64_t* __restrict__ words, const uint64_t* __restrict__ cum,
@@ -383,6 +385,89 @@ __global__ void k_gain_full(SiteArgs a, const SiteState* st, const int4* __restr
             gain[i] = (G)acc;
             bytes += 8ull * (((unsigned long long)win.z * win.w + 63) >> 6);   // SPEC-layout (algorithmic) bytes
         }
+    }
+    if (counters && lane == 0 && bytes) atomicAdd(counters + kSiteBytes, bytes);
+}
+
+// Bucket-tiled form of k_gain_full (mode-1 rounds): one CTA per candidate
+// bucket (side bsize = roi, the CSR grid of mode 0) first copies the cum
+// region every window of the bucket lies in -- rows [by*bs - R, (by+1)*bs + R),
+// words [(bx*bs - R) >> 6, ((bx+1)*bs - 1 + R) >> 6] -- into shared memory,
+// then its warps stream the bucket's candidates' packed words from HBM (8
+// coalesced 256-byte loads in flight per warp) against that copy.  The cum is
+// read from L2 once per bucket instead of once per candidate, so the L2 carries
+// little more than the HBM stream itself.
+constexpr int kTiledThreads = 512;
+
+struct TileBox {
+    int ry0, ry1, wx0, wx1;
+};
+__device__ __forceinline__ TileBox tile_box(const SiteArgs& a, int bkt) {
+    const int by = bkt / a.nbx, bx = bkt - by * a.nbx;
+    TileBox t;
+    t.ry0 = max(max(0, a.cr0), by * a.bsize - a.R);
+    t.ry1 = min(min(a.nrows, a.cr1), (by + 1) * a.bsize + a.R);
+    t.wx0 = max(0, bx * a.bsize - a.R) >> 6;
+    t.wx1 = (min(a.ncols - 1, (bx + 1) * a.bsize - 1 + a.R) >> 6) + 1;
+    return t;
+}
+
+template <typename G>
+__global__ void __launch_bounds__(kTiledThreads, 2) k_gain_tiled(SiteArgs a, const SiteState* st,
+                                                               const int4* __restrict__ wins,
+                                                               const uint64_t* __restrict__ words,
+                                                               const uint64_t* __restrict__ cum,
+                                                               const int32_t* __restrict__ bstart,
+                                                               const int32_t* __restrict__ items,
+                                                               G* __restrict__ gain,
+                                                               unsigned long long* __restrict__ counters) {
+    if (st && (st->done || st->finish)) return;
+    extern __shared__ __align__(16) uint64_t s_cum[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int W = kTiledThreads / 32;
+    const int nbk = a.nbx * a.nby;
+    unsigned long long bytes = 0;
+    for (int bkt = blockIdx.x; bkt < nbk; bkt += gridDim.x) {
+        const int k0 = bstart[bkt], k1 = bstart[bkt + 1];
+        if (k0 == k1) continue;
+        const TileBox tb = tile_box(a, bkt);
+        const int pw = tb.wx1 - tb.wx0;
+        for (int t = tid; t < (tb.ry1 - tb.ry0) * pw; t += kTiledThreads) {
+            const int y = t / pw, x = t - y * pw;
+            s_cum[t] = cum[(int64_t)(tb.ry0 + y) * a.wpr + tb.wx0 + x];
+        }
+        __syncthreads();
+        for (int k = k0 + warp; k < k1; k += W) {
+            const int64_t i = items[k];
+            const int4 win = wins[i];
+            const int nwr = win_nwr(win.y, win.w), total = win.z * nwr;
+            const uint64_t* v = words + i * a.stride;
+            const uint64_t* crow = s_cum + (win.x - tb.ry0) * pw + ((win.y >> 6) - tb.wx0);
+            int y = lane / nwr, b = lane - y * nwr;
+            const int dy = 32 / nwr, db = 32 - dy * nwr;
+            int acc = 0;
+            constexpr int U = 8;
+            for (int t0 = lane; t0 < total; t0 += 32 * U) {
+                uint64_t vw[U];
+                int co[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    vw[u] = t0 + 32 * u < total ? __ldcs(v + t0 + 32 * u) : 0ull;
+                    co[u] = y * pw + b;
+                    y += dy; b += db;
+                    if (b >= nwr) { b -= nwr; ++y; }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (t0 + 32 * u < total) acc += __popcll(vw[u] & ~crow[co[u]]);
+            }
+            for (int o = 16; o; o >>= 1) acc += __shfl_down_sync(kFull, acc, o);
+            if (lane == 0) {
+                gain[i] = (G)acc;
+                bytes += 8ull * (((unsigned long long)win.z * win.w + 63) >> 6);   // SPEC-layout (algorithmic) bytes
+            }
+        }
+        __syncthreads();
     }
     if (counters && lane == 0 && bytes) atomicAdd(counters + kSiteBytes, bytes);
 }
@@ -504,6 +589,41 @@ SiteArgs make_args(txs_ctx* c, const txs_params& p) {
     return a;
 }
 
+// accumulate the device time between ev_r0 and ev_r1 (stream already synced)
+static void add_round_time(txs_ctx* c) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->ev_r0, c->ev_r1) == cudaSuccess) c->stats.ms_site_rounds += ms;
+}
+
+int blocks_for(int64_t work, int per_block, int cap) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((work + per_block - 1) / per_block, cap));
+}
+
+// Full gain pass (popc(v_i & ~cum) for every candidate): bucket-tiled when the
+// buckets exist (SITE rounds), hold >= 64 candidates on average and the
+// bucket's cum region fits two CTAs per SM (roi <= ~280) -- measured: C5 (244
+// per bucket) 4.26 -> 4.97 TB/s; C2 (39) and C3 (5) stream faster with
+// k_gain_full, which reads each candidate's cum words from L2.
+template <typename G>
+static void launch_gain_pass(txs_ctx* c, const SiteArgs& a, const SiteState* st, const uint64_t* cum, G* gain,
+                             unsigned long long* counters, bool buckets) {
+    const int64_t rows = (int64_t)a.bsize + 2 * a.R;
+    const int64_t pw = (a.bsize + 2 * (int64_t)a.R + 63) / 64 + 1;
+    const size_t smem = sizeof(uint64_t) * (size_t)(rows * pw);
+    const bool dense = a.n >= 64 * (int64_t)a.nbx * a.nby;
+    if (buckets && dense && smem <= 110 * 1024 && !getenv("TXS_GAIN_REG")) {
+        auto kern = k_gain_tiled<G>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int64_t nbk = (int64_t)a.nbx * a.nby;
+        const int grid = (int)std::min<int64_t>(nbk, (int64_t)c->num_sms * 2 * 8);
+        kern<<<grid, kTiledThreads, smem, c->stream>>>(a, st, c->d_win, c->d_words, cum, c->d_bucket_start,
+                                                       c->d_bucket_items, gain, counters);
+    } else {
+        k_gain_full<G><<<blocks_for(a.n * 32, 256, c->num_sms * 16), 256, 0, c->stream>>>(a, st, c->d_win, c->d_words,
+                                                                                          cum, gain, counters);
+    }
+}
+
 // cum over the held region rows [r0, r1) (whole grid unless sharded) + delta list
 txs_status alloc_bitmaps(txs_ctx* c, int64_t r0, int64_t r1) {
     c->wpr = (c->ncols + 63) / 64;
@@ -520,9 +640,6 @@ txs_status alloc_bitmaps(txs_ctx* c, int64_t r0, int64_t r1) {
     return TXS_OK;
 }
 
-int blocks_for(int64_t work, int per_block, int cap) {
-    return (int)std::max<int64_t>(1, std::min<int64_t>((work + per_block - 1) / per_block, cap));
-}
 
 // gains <- popcounts; CSR buckets (side roi) over the candidates' positions
 txs_status init_gains_buckets(txs_ctx* c, const SiteArgs& a, void* d_scan_tmp, size_t scan_bytes) {
@@ -594,11 +711,14 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
         uint64_t* cu_ = cumv; uint64_t* dw_ = c->d_dwin; int2* s0_ = c->d_dspan; unsigned long long* pa_ = c->d_partials;
         unsigned long long* co_ = c->d_counters; SiteState* st_ = c->d_state;
         void* args[] = {&aa, &st_, &lpp, &g_, &it_, &w_, &cu_, &dw_, &s0_, &sp1, &pa_, &co_};
+        cudaEventRecord(c->ev_r0, c->stream);
         TXS_CUDA(c, "site", cudaLaunchCooperativeKernel((void*)k_site_loop, grid, kLoopThreads, args, 0, c->stream));
         TXS_LAUNCHED(c, "site");
+        cudaEventRecord(c->ev_r1, c->stream);
         c->stats.site_launches += 1;
         TXS_CUDA(c, "site", cudaMemcpyAsync(c->h_state, c->d_state, sizeof(SiteState), cudaMemcpyDeviceToHost, c->stream));
         TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+        add_round_time(c);
         const int64_t ns = c->h_state->nsel;
         c->stats.site_iterations += ns;
         out.resize((size_t)ns);
@@ -613,14 +733,12 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
     const int am_blocks = blocks_for(n, 256 * 4, sms * 2);
     const int cm_blocks = 16;
     const int up_blocks = sms * 8;
-    const int full_blocks = blocks_for(n * 32, 256, sms * 16);
     const LoopPtrs lp{c->d_crow, c->d_ccol, c->d_win, c->d_bucket_start, d_steps};
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     TXS_CUDA(c, "site", cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     for (int r = 0; r < kRoundsPerGraph; ++r) {
-        if (p.site_mode == 1)
-            k_gain_full<int32_t><<<full_blocks, 256, 0, c->stream>>>(a, c->d_state, c->d_win, c->d_words, cumv, c->d_gain, c->d_counters);
+        if (p.site_mode == 1) launch_gain_pass<int32_t>(c, a, c->d_state, cumv, c->d_gain, c->d_counters, true);
         k_argmax<<<am_blocks, 256, 0, c->stream>>>(c->d_gain, a, c->d_state, lp, c->d_dspan);
         k_commit<<<cm_blocks, 256, 0, c->stream>>>(a, c->d_state, c->d_words, cumv, c->d_dwin, c->d_dspan, nullptr);
         if (p.site_mode != 1)
@@ -635,11 +753,14 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
     txs_status st = TXS_OK;
     int64_t graphs = 0;
     for (;;) {
+        cudaEventRecord(c->ev_r0, c->stream);
         ce = cudaGraphLaunch(exec, c->stream);
         if (ce != cudaSuccess) { st = cuda_fail(c, "site", ce); break; }
+        cudaEventRecord(c->ev_r1, c->stream);
         ++graphs;
         ce = cudaMemcpyAsync(c->h_state, c->d_state, sizeof(SiteState), cudaMemcpyDeviceToHost, c->stream);
         if (ce == cudaSuccess) ce = cudaStreamSynchronize(c->stream);
+        if (ce == cudaSuccess) add_round_time(c);
         if (ce != cudaSuccess) { st = cuda_fail(c, "site", ce); break; }
         if (c->h_state->done) break;
         if (graphs * kRoundsPerGraph > n + 2 * kRoundsPerGraph) { st = fail(c, TXS_ERR_STATE, "site", "loop did not terminate"); break; }
@@ -671,7 +792,7 @@ txs_status launch_marginal_gains(txs_ctx* c, const uint64_t* d_cum_dense, int64_
     k_dense_to_padded<<<blocks_for(c->nrows * c->wpr, 256, c->num_sms * 16), 256, 0, c->stream>>>(d_cum_dense, pad, c->nrows, c->ncols, c->wpr);
     TXS_LAUNCHED(c, "site");
     if (a.n > 0) {
-        k_gain_full<int64_t><<<blocks_for(a.n * 32, 256, c->num_sms * 16), 256, 0, c->stream>>>(a, nullptr, c->d_win, c->d_words, pad, d_gains, nullptr);
+        launch_gain_pass<int64_t>(c, a, nullptr, pad, d_gains, nullptr, false);
         TXS_LAUNCHED(c, "site");
     }
     TXS_CUDA(c, "site", cudaFreeAsync(pad, c->stream));

@@ -29,7 +29,24 @@ for st in stages:
                 e.find_candidates(p, copy=False)
             e.reset_stats()
             e.compute_all_viewsheds(p)
+        elif st == "site1":   # full-rescan SITE, 64 rounds (the streaming figure)
+            if _ == 0:
+                if cfg.random_observers:
+                    e.random_observers(cfg.random_observers, cfg.observer_seed)
+                else:
+                    e.estimate_vix(p, copy=False)
+                    e.find_candidates(p, copy=False)
+                e.compute_all_viewsheds(p)
+            e.reset_stats()
+            p1 = params_for(cfg, site_mode=1)
+            p1.max_selected = 64
+            e.site(p1, cap=65)
         e.synchronize()
-        ts.append(e.stats()["ms_" + st])
+        s = e.stats()
+        ts.append(s["ms_" + st.rstrip("1")])
+        if st == "site1":
+            out["site1_gbs"] = round(s["site_bytes"] / (s["ms_site"] / 1e3) / 1e9, 1)
+            out["site1_rounds_ms"] = round(s["ms_site_rounds"], 3)
+            out["site1_rounds_gbs"] = round(s["site_bytes"] / (s["ms_site_rounds"] / 1e3) / 1e9, 1)
     out[st] = min(ts[1:])
 print(sys.argv[1], os.environ.get("TXS_VIX_PATH", ""), os.environ.get("TXS_VS_K", ""), out, flush=True)

@@ -232,6 +232,22 @@ def test_site_random_dense_bit_exact(engine, mode):
     assert (np.diff(g["gain"]) <= 0).all()
 
 
+@pytest.mark.parametrize("mode", [0, 1])
+def test_site_bucket_tiled_bit_exact(engine, mode):
+    """>= 64 candidates per roi-sized bucket: mode 1 takes the bucket-tiled gain
+    kernel (cum region staged in shared memory); grid edges included."""
+    T = _T()
+    z = O.generate_fractal(200, 256, 0.5, 5, 0, 2000)
+    rng = np.random.default_rng(11)
+    n = 9500
+    rows, cols = rng.integers(0, 200, n).astype(np.int32), rng.integers(0, 256, n).astype(np.int32)
+    rows[:4], cols[:4] = [0, 199, 0, 199], [0, 255, 255, 0]
+    engine.set_terrain(z)
+    engine.set_candidates(rows, cols)
+    engine.compute_all_viewsheds(T.make_params(20, 5, 5))
+    _site_compare(engine, 20, rows, cols, 200, 256, 1.0, 0, mode)
+
+
 def test_site_edge_cases(engine):
     T = _T()
     z = O.generate_fractal(64, 64, 0.5, 2, 0, 4000)
