@@ -214,11 +214,28 @@ __device__ __forceinline__ int crossings_of(int dr, int dc) {
     return n - (int)(a << sh) - 1;
 }
 
+// gcd table for |dr|,|dc| <= 255 (the quad path's crossing statistic: one L2
+// load per sample instead of a binary-gcd loop)
+__global__ void k_gcd_table(uint8_t* __restrict__ t) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= 256 * 256) return;
+    unsigned a = idx >> 8, b = idx & 255;
+    while (b) { const unsigned r = a % b; a = b; b = r; }
+    t[idx] = (uint8_t)a;
+}
+__device__ __forceinline__ int crossings_tab(int dr, int dc, const uint8_t* __restrict__ gt) {
+    const int a = abs(dr), b = abs(dc);
+    if (a == 0 || b == 0) return a + b > 0 ? a + b - 1 : 0;
+    return a + b - (int)__ldg(gt + (a << 8) + b) - 1;
+}
+
 struct VixArgs {
     int R, ht, hr, S;
     uint64_t seed;
     FastMod64 span;   // 2R+1
-    int tiles_x;
+    int tiles_x, tiles_y;
+    int hp, wp;          // quad T-plane column pitch, V-plane row pitch
+    int strip;           // tile columns per traversal strip (quad path)
     int row0, row_end;   // band rows [row0, row_end)
     int zr0, zr1;        // held terrain rows [zr0, zr1)
 };
@@ -315,16 +332,19 @@ __global__ void __launch_bounds__(kVixThreads, 2) k_vix(const int16_t* __restric
 //   .y = (C, A)  C = A one major step back -> zC*r + zA*(m-r)   (dp2a.hi)
 // so one coalesced 64-bit load and two dp2a (16-bit x 8-bit dot products,
 // exact) evaluate both crossings of a step, with no shuffles:
-//   plane 0 QV+ [y*ncols + c] = {(z(y,c), z(y+1,c)), (z(y,c-1), z(y,c))}   |dc| >= |dr|, minor +row
-//   plane 1 QV- [y*ncols + c] = {(z(y,c), z(y-1,c)), (z(y,c-1), z(y,c))}   minor -row
-//   plane 2 QT+ [c*H + y]     = {(z(y,c), z(y,c+1)), (z(y-1,c), z(y,c))}   |dr| > |dc|, minor +col
-//   plane 3 QT- [c*H + y]     = {(z(y,c), z(y,c-1)), (z(y-1,c), z(y,c))}   minor -col
-// (y = held row, H = held rows; neighbours outside the held terrain are 0
+//   plane 0 QV+ [y*Wp + c]    = {(z(y,c), z(y+1,c)), (z(y,c-1), z(y,c))}   |dc| >= |dr|, minor +row
+//   plane 1 QV- [y*Wp + c]    = {(z(y,c), z(y-1,c)), (z(y,c-1), z(y,c))}   minor -row
+//   plane 2 QT+ [c*Hp + y]    = {(z(y,c), z(y,c+1)), (z(y-1,c), z(y,c))}   |dr| > |dc|, minor +col
+//   plane 3 QT- [c*Hp + y]    = {(z(y,c), z(y,c-1)), (z(y-1,c), z(y,c))}   minor -col
+// (y = held row, H = held rows; Wp and Hp = the V planes' row pitch and the
+// T planes' column pitch: ncols resp. H rounded to 32 plus 16 -- with a
+// power-of-two pitch the rows of a tile's window alias onto few L2 slices;
+// neighbours outside the held terrain are 0
 // and only ever carry weight 0).  Weights: both byte pairs come from one
 // word W = (M + 255r) | (256m - 255r) << 16, linear in r.
 __device__ __forceinline__ uint32_t pk16(int lo, int hi) { return (uint16_t)lo | ((uint32_t)(uint16_t)hi << 16); }
 
-__global__ void k_quads(const int16_t* __restrict__ z, uint2* __restrict__ q, int H, int ncols) {
+__global__ void k_quads(const int16_t* __restrict__ z, uint2* __restrict__ q, int H, int Hp, int Wp, int ncols) {
     __shared__ int16_t t[34][36];   // held rows y0-1 .. y0+32, cols c0-1 .. c0+32
     const int c0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
     const int tid = threadIdx.y * 32 + threadIdx.x;
@@ -333,13 +353,13 @@ __global__ void k_quads(const int16_t* __restrict__ z, uint2* __restrict__ q, in
         t[yy][xx] = (y >= 0 && y < H && c >= 0 && c < ncols) ? z[(int64_t)y * ncols + c] : (int16_t)0;
     }
     __syncthreads();
-    const int64_t n = (int64_t)H * ncols;
+    const int64_t n = (int64_t)H * Wp;
     for (int yy = threadIdx.y; yy < 32; yy += 8) {
         const int y = y0 + yy, c = c0 + threadIdx.x, ty = yy + 1, tx = threadIdx.x + 1;
         if (y < H && c < ncols) {
             const int a = t[ty][tx];
             const uint32_t ca = pk16(t[ty][tx - 1], a);
-            const int64_t w = (int64_t)y * ncols + c;
+            const int64_t w = (int64_t)y * Wp + c;
             q[w] = make_uint2(pk16(a, t[ty + 1][tx]), ca);
             q[n + w] = make_uint2(pk16(a, t[ty - 1][tx]), ca);
         }
@@ -349,9 +369,9 @@ __global__ void k_quads(const int16_t* __restrict__ z, uint2* __restrict__ q, in
         if (y < H && c < ncols) {
             const int a = t[ty][tx];
             const uint32_t ca = pk16(t[ty - 1][tx], a);
-            const int64_t w = (int64_t)c * H + y;
-            q[2 * n + w] = make_uint2(pk16(a, t[ty][tx + 1]), ca);
-            q[3 * n + w] = make_uint2(pk16(a, t[ty][tx - 1]), ca);
+            const int64_t w = 2 * n + (int64_t)c * Hp + y, nT = (int64_t)ncols * Hp;
+            q[w] = make_uint2(pk16(a, t[ty][tx + 1]), ca);
+            q[nT + w] = make_uint2(pk16(a, t[ty][tx - 1]), ca);
         }
     }
 }
@@ -430,13 +450,23 @@ __device__ __forceinline__ bool quad_walk(const QuadGeom& g, int lane) {
 __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16_t* __restrict__ z,
                                                                    const uint2* __restrict__ qp, int nrows, int ncols,
                                                                    uint8_t* __restrict__ out, VixArgs a,
+                                                                   const uint8_t* __restrict__ gcdt,
                                                                    unsigned long long* __restrict__ counters) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
     // dynamic smem: [geometry: kVixWarps x 32][samples: kVixWarps x S ints]
     QuadGeom* s_geo = (QuadGeom*)s_dyn + warp_of_thread() * 32;
     int* s_samp = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + warp_of_thread() * a.S;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int ty0 = a.row0 + (blockIdx.x / a.tiles_x) * kTile, tx0 = (blockIdx.x % a.tiles_x) * kTile;
+    // tiles in vertical strips of a.strip tile columns, row-major inside a strip
+    int ty, tx;
+    {
+        const int strip_tiles = a.strip * a.tiles_y;
+        const int sidx = blockIdx.x / strip_tiles, rem = blockIdx.x - sidx * strip_tiles;
+        const int sw = min(a.strip, a.tiles_x - sidx * a.strip);
+        ty = rem / sw;
+        tx = sidx * a.strip + (rem - ty * sw);
+    }
+    const int ty0 = a.row0 + ty * kTile, tx0 = tx * kTile;
     const int R2 = a.R * a.R;
     unsigned long long n_cross = 0;
     int n_posts = 0;
@@ -469,20 +499,20 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
                 const int pk = s_samp[s0 + lane];
                 int dr = (int)(int16_t)(pk & 0xffff), dc = pk >> 16;
                 const int Zt = zld(z + (int64_t)(r + dr) * ncols + (c + dc)) + a.hr;
-                n_cross += crossings_of(dr, dc);
+                n_cross += crossings_tab(dr, dc, gcdt);
                 const bool tr = abs(dr) > abs(dc);
                 const bool rev = tr ? dr < 0 : dc < 0;      // walk from the receiver
                 const int y = r - a.zr0 + (rev ? dr : 0), x = c + (rev ? dc : 0);   // start post
                 if (rev) { dr = -dr; dc = -dc; }
                 const int nM = tr ? dr : dc, nm = tr ? abs(dc) : abs(dr);
                 const bool mneg = (tr ? dc : dr) < 0;
-                const int64_t n = (int64_t)H * ncols;
+                const int64_t n = (int64_t)H * a.wp, nT = (int64_t)ncols * a.hp;
                 QuadGeom g;
-                g.Q = qp + (tr ? 2 * n + (int64_t)x * H + y : (int64_t)y * ncols + x) + (mneg ? n : 0);
+                g.Q = qp + (tr ? 2 * n + (int64_t)x * a.hp + y + (mneg ? nT : 0) : (int64_t)y * a.wp + x + (mneg ? n : 0));
                 g.Es = rev ? Zt : E;
                 g.D = rev ? E - Zt : Zt - E;
                 g.nMm = nM | (nm << 16);
-                const int stride = tr ? H : ncols;
+                const int stride = tr ? a.hp : a.wp;
                 g.sm = mneg ? -stride : stride;
                 g.rcp = nM ? __fdividef(1.0f, (float)nM) : 0.f;
                 const int num = 32 * nm;
@@ -542,6 +572,14 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     a.seed = p.seed;
     a.span = make_fastmod((uint64_t)(2 * p.roi + 1));
     a.tiles_x = (int)((c->ncols + kTile - 1) / kTile);
+    a.tiles_y = (int)((c->band_r1 - c->band_r0 + kTile - 1) / kTile);
+    a.hp = (int)(((c->z_rows + 31) & ~(int64_t)31) + 16);
+    a.wp = (int)(((c->ncols + 31) & ~(int64_t)31) + 16);
+    // traversal order (measured, profiles/README.md): strips of 16 tile columns
+    // at roi 200 (C2 60.2 -> 57.6 ms); row-major at roi 100 (C3: strips raise
+    // the L2 hit rate 81 -> 99 % yet run 457 -> 550 ms)
+    a.strip = p.roi >= 150 ? 16 : a.tiles_x;
+    if (const char* e = getenv("TXS_VIX_STRIP")) a.strip = std::max(1, std::min(a.tiles_x, atoi(e)));
     a.row0 = (int)c->band_r0; a.row_end = (int)c->band_r1;
     a.zr0 = (int)c->z_off; a.zr1 = (int)(c->z_off + c->z_rows);
     const int64_t tiles = a.tiles_x * ((c->band_r1 - c->band_r0 + kTile - 1) / kTile);
@@ -563,7 +601,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     // column-major copy.  TXS_VIX_PATH=smem|pairs|zt overrides (measurement).
     size_t freeb = 0, totalb = 0;
     cudaMemGetInfo(&freeb, &totalb);
-    const size_t qbytes = sizeof(uint2) * 4 * (size_t)(c->z_rows * c->ncols);
+    const size_t qbytes = sizeof(uint2) * (size_t)(2 * c->z_rows * (int64_t)a.wp + 2 * c->ncols * (int64_t)a.hp);
     const bool quads_ok = p.roi <= 255 && (qbytes <= c->pairs_cap || qbytes <= freeb / 2);
     int path = quads_ok ? 1 : (smem <= 110 * 1024 ? 0 : 2);
     if (const char* e = getenv("TXS_VIX_PATH")) {
@@ -575,22 +613,28 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     if (path == 0) {
         st = go(k_vix<true, 1>, smem);
     } else if (path == 1) {
-        const int64_t n = c->z_rows * c->ncols;
+        const int64_t n = c->z_rows * c->ncols, nq = 2 * c->z_rows * (int64_t)a.wp + 2 * c->ncols * (int64_t)a.hp;
         // rebuilt on every call (part of the timed stage; ~1 HBM pass of 34 B/post)
-        if (ensure(c, "vix", (void**)&c->d_pairs, &c->pairs_cap, sizeof(uint2) * 4 * n) != TXS_OK)
+        if (ensure(c, "vix", (void**)&c->d_pairs, &c->pairs_cap, sizeof(uint2) * nq) != TXS_OK)
             return TXS_ERR_OUT_OF_MEMORY;
         {
             dim3 tb(32, 8), tg((unsigned)((c->ncols + 31) / 32), (unsigned)((c->z_rows + 31) / 32));
-            k_quads<<<tg, tb, 0, c->stream>>>(c->d_z, (uint2*)c->d_pairs, (int)c->z_rows, (int)c->ncols);
+            k_quads<<<tg, tb, 0, c->stream>>>(c->d_z, (uint2*)c->d_pairs, (int)c->z_rows, a.hp, a.wp, (int)c->ncols);
             TXS_LAUNCHED(c, "vix");
         }
         const uint2* qp = (const uint2*)c->d_pairs;
-        set_zbounds(c->d_z, c->d_z + n, c->stream, (const int16_t*)qp, (const int16_t*)(qp + 4 * n));
+        set_zbounds(c->d_z, c->d_z + n, c->stream, (const int16_t*)qp, (const int16_t*)(qp + nq));
         const size_t qsm = samp + sizeof(QuadGeom) * kVixWarps * 32;
         if (qsm > 48 * 1024)
             TXS_CUDA(c, "vix", cudaFuncSetAttribute(k_vix_quads, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm));
+        if (!c->d_gcd) {
+            TXS_CUDA(c, "vix", cudaMalloc((void**)&c->d_gcd, 256 * 256));
+            k_gcd_table<<<256, 256, 0, c->stream>>>(c->d_gcd);
+            TXS_LAUNCHED(c, "vix");
+        }
         k_vix_quads<<<(unsigned)tiles, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols,
-                                                                       c->d_vix - c->band_r0 * c->ncols, a, c->d_counters);
+                                                                       c->d_vix - c->band_r0 * c->ncols, a, c->d_gcd,
+                                                                       c->d_counters);
         st = TXS_OK;
     } else {
         if (ensure(c, "vix", (void**)&c->d_zt, &c->zt_cap, sizeof(int16_t) * c->z_rows * c->ncols) != TXS_OK)
