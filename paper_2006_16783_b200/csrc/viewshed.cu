@@ -31,7 +31,48 @@ struct VsArgs {
     int64_t n;            // observers
     int sbits;            // smem bitmap u32 words per observer: (2R+1) rows x (2*Wmax+1) (odd pitch)
     long long tmpl_cross, tmpl_cells;   // template crossings / cells (interior observers)
+    const uint32_t* pairs;  // pair planes of the held rows (interior K-observer path), or null
+    int p2, pw;             // pair-plane row pitch (words) and V-plane offset inside a row
+    int zoff;               // first held terrain row
 };
+
+// Pair planes for the interior K-observer sweep: held row y occupies p2 = 2*pw
+// words, [H pairs | V pairs], H[x] = z(y,x) | z(y,x+1) << 16 and
+// V[x] = z(y,x) | z(y+1,x) << 16 (0 past the last column / held row).  A grid
+// crossing interpolates between exactly such a pair, so one 32-bit load and one
+// dp2a (signed 16-bit halves x unsigned weight bytes, exact) replace two
+// 16-bit loads and two multiplies; for a ray stepping to -col (-row) the pair
+// one post back is read and the weight bytes are swapped.
+__global__ void k_vs_pairs(const int16_t* __restrict__ z, uint32_t* __restrict__ out, int H, int ncols, int pw) {
+    const int64_t total = (int64_t)H * pw;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int y = (int)(t / pw), x = (int)(t - (int64_t)y * pw);
+        uint32_t hv = 0, vv = 0;
+        if (x < ncols) {
+            const int16_t* zr = z + (int64_t)y * ncols;
+            const uint32_t a = (uint16_t)zr[x];
+            hv = a | ((x + 1 < ncols ? (uint32_t)(uint16_t)zr[x + 1] : 0u) << 16);
+            vv = a | ((y + 1 < H ? (uint32_t)(uint16_t)zr[x + ncols] : 0u) << 16);
+        }
+        uint32_t* row = out + (int64_t)y * 2 * pw;
+        row[x] = hv;
+        row[pw + x] = vv;
+    }
+}
+
+__device__ __forceinline__ uint32_t vs_pld(const uint32_t* p) {
+#ifdef TXS_BOUNDS_CHECK
+    const int16_t* q = (const int16_t*)p;
+    if (q < g_zb.lo2 || q + 1 >= g_zb.hi2) __trap();
+#endif
+    return __ldg(p);
+}
+
+__device__ __forceinline__ int vs_dp2(uint32_t pair, uint32_t w) {
+    int d;
+    asm("dp2a.lo.s32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(pair), "r"(w), "r"(0));
+    return d;
+}
 
 // Aligned output word b of window row y, gathered from the window-dense smem
 // bitmap (row-major h x w bits): the smem copy stays compact (3 CTAs/SM at
@@ -273,18 +314,20 @@ __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, 
 // own horizon (NH, MH) and bitmap — K independent dependency chains per lane.
 // Interior observers have every post in the grid and an unclipped window, so
 // no bounds tests and no counting (the template's totals are added instead).
-template <int K>
+template <int K, bool PAIRS>
 __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const int* rk, const int* ck, const int* Ek,
                                             const int* RSk, const int* K0k,
                                             const VsArgs& a, const int4* __restrict__ rays,
                                             const int2* __restrict__ groups, const uint2* __restrict__ events,
                                             int ngroups, uint32_t* s_bits, int bits_stride) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const int16_t* __restrict__ P[K];
+    const uint32_t* __restrict__ B[K];   // PAIRS: the observer's word in the pair planes
+    const int16_t* __restrict__ P[K];    // else: the observer's post
     int Ehr[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        P[k] = z + (int64_t)rk[k] * a.ncols + ck[k];
+        if (PAIRS) B[k] = a.pairs + (int64_t)(rk[k] - a.zoff) * a.p2 + ck[k];
+        else P[k] = z + (int64_t)rk[k] * a.ncols + ck[k];
         Ehr[k] = Ek[k] - a.hr;
     }
     for (int g = warp; g < ngroups; g += nwarps) {
@@ -293,6 +336,10 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
         int p = 0, q = 0;
         if (ray < a.nrays) { const int4 rd = __ldg(rays + ray); p = rd.x; q = rd.y; }
         const int ap = abs(p), aq = abs(q);
+        // PAIRS: row crossing reads the H pair (c, c+1) or, stepping to -col,
+        // (c-1, c) with swapped weights; column crossing the V pair likewise
+        const int hadj = q < 0 ? -1 : 0, vadj = a.pw + (p < 0 ? -a.p2 : 0);
+        const bool hswap = q < 0, vswap = p < 0;
         const int stepr = p >= 0 ? a.ncols : -a.ncols, stepc = q >= 0 ? 1 : -1;
         const int L2 = p * p + q * q;
         bool has[K];
@@ -302,7 +349,9 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
         const uint2* ev = events + (int64_t)grp.x * 32 + lane;
         for (int st0 = 0; st0 < grp.y; st0 += 2) {
             uint2 ee[2];
-            int z0[2][K], z1[2][K], dru[2], dcu[2];
+            uint32_t pr[2][K];
+            int z0[2][K], z1[2][K];
+            int dru[2], dcu[2];
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 ee[u] = st0 + u < grp.y ? __ldg(ev + (int64_t)(st0 + u) * 32) : make_uint2((uint32_t)kEvNop, 0u);
@@ -310,12 +359,18 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
                 const int dr = ((int)(e << 20)) >> 23, dc = ((int)(e << 11)) >> 23;
                 const bool isrow = type == kEvRow, iscol = type == kEvCol;
                 dru[u] = dr; dcu[u] = dc;
-                const int off0 = type != kEvNop ? dr * a.ncols + dc : 0;
-                const int off1 = off0 + (iscol ? stepr : (isrow ? stepc : 0));
+                if (PAIRS) {
+                    const int off = type != kEvNop ? dr * a.p2 + dc + (isrow ? hadj : (iscol ? vadj : 0)) : 0;
 #pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    z0[u][k] = zld(P[k] + off0);
-                    z1[u][k] = zld(P[k] + off1);
+                    for (int k = 0; k < K; ++k) pr[u][k] = vs_pld(B[k] + off);
+                } else {
+                    const int off0 = type != kEvNop ? dr * a.ncols + dc : 0;
+                    const int off1 = off0 + (iscol ? stepr : (isrow ? stepc : 0));
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        z0[u][k] = zld(P[k] + off0);
+                        z1[u][k] = zld(P[k] + off1);
+                    }
                 }
             }
 #pragma unroll
@@ -326,9 +381,11 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
                 const bool byrow = (e >> 29) & 1u;
                 const bool iscell = type == kEvCell, iscross = type <= kEvPost;
                 const int n = iscell ? 1 : (byrow ? ap : aq);
+                const bool swap = (type == kEvRow && hswap) || (type == kEvCol && vswap);
+                const uint32_t W = swap ? (uint32_t)(m | ((n - m) << 8)) : (uint32_t)((n - m) | (m << 8));
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
-                    const int v = z0[u][k] * (n - m) + z1[u][k] * m;
+                    const int v = PAIRS ? vs_dp2(pr[u][k], W) : z0[u][k] * (n - m) + z1[u][k] * m;
                     const int X = v - (iscell ? Ehr[k] : n * Ek[k]);
                     const long long lhs = (long long)X * (iscell ? L2MH[k] : MH[k]);
                     const long long rhs = (long long)NH[k] * y;
@@ -449,7 +506,8 @@ __global__ void k_viewshed_evk(const int16_t* __restrict__ z, const int32_t* __r
     __syncthreads();
     unsigned long long n_cross = 0, n_cells = 0;
     if (all_int) {
-        vs_events_k<K>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride);
+        if (a.pairs) vs_events_k<K, true>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride);
+        else vs_events_k<K, false>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride);
         if (threadIdx.x == 0) { n_cross = (unsigned long long)(K * a.tmpl_cross); n_cells = (unsigned long long)(K * a.tmpl_cells); }
     } else {
         for (int k = 0; k < K; ++k) {
@@ -530,7 +588,8 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
     c->vs_n = n;
     c->vs_stride = mw;
     if (n == 0) return TXS_OK;
-    VsArgs a{(int)c->nrows, (int)c->ncols, p.roi, p.tx_height, p.rx_height, T->nrays, mw, nullptr, n, 0, 0, 0};
+    VsArgs a{(int)c->nrows, (int)c->ncols, p.roi, p.tx_height, p.rx_height, T->nrays, mw, nullptr, n, 0, 0, 0,
+             nullptr, 0, 0, 0};
     // Process observers in 64x64-tile order so the CTAs resident at any moment
     // read overlapping terrain windows (L2 reuse; config 5's observers are
     // random over a 537 MB terrain).  Output slots keep candidate order.
@@ -578,6 +637,26 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
         const int threads = 32 * best;
         const size_t sm = (size_t)kobs * smem;
         const unsigned grid = (unsigned)((n + kobs - 1) / kobs);
+        // pair planes of the held rows (rebuilt per call, part of the timed stage;
+        // shares the VIX quad-plane scratch buffer) -- measured (profiles/README.md):
+        // C5 (roi 250) 1852 -> 1786 ms, C2 (200) +0.9 %, C3 (100) +3.9 %, so only
+        // for roi >= 225; TXS_VS_PAIRS=0/1 overrides
+        bool use_pairs = p.roi >= 225;
+        if (const char* e = getenv("TXS_VS_PAIRS")) use_pairs = atoi(e) != 0;
+        if (use_pairs) {
+        a.pw = (int)(((c->ncols + 31) & ~(int64_t)31) + 16);
+        a.p2 = 2 * a.pw;
+        a.zoff = (int)c->z_off;
+        const int64_t pwords = c->z_rows * (int64_t)a.p2;
+        if (ensure(c, "viewshed", (void**)&c->d_pairs, &c->pairs_cap, sizeof(uint32_t) * pwords) != TXS_OK)
+            return TXS_ERR_OUT_OF_MEMORY;
+        k_vs_pairs<<<(unsigned)std::min<int64_t>((c->z_rows * a.pw + 255) / 256, (int64_t)c->num_sms * 32), 256, 0,
+                     c->stream>>>(c->d_z, (uint32_t*)c->d_pairs, (int)c->z_rows, (int)c->ncols, a.pw);
+        TXS_LAUNCHED(c, "viewshed");
+        a.pairs = (const uint32_t*)c->d_pairs;
+        set_zbounds(c->d_z, c->d_z + c->z_rows * c->ncols, c->stream, (const int16_t*)a.pairs,
+                    (const int16_t*)(a.pairs + pwords));
+        }
         if (kobs == 2) {
             if (sm > 48 * 1024)
                 TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(k_viewshed_evk<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
