@@ -315,14 +315,15 @@ def run_b200(args, cfg):
         units = st["vix_crossings_full"] / K
         stages["vix"] = {"ms": round(vix_ms, 3), "los_crossings": int(units),
                          "los_samples_per_s": units / (vix_ms / 1e3) if vix_ms else None,
-                         "kernel": "k_vix", "bytes_per_launch": 4 * units}
+                         "kernel": "k_vix_quads" if cfg.roi <= 255 else "k_vix", "bytes_per_launch": 4 * units}
         fm_ms = st["ms_findmax"] / K
         stages["findmax"] = {"ms": round(fm_ms, 3), "kernel": "k_findmax", "bytes_per_launch": 2 * cfg.posts}
     vs_ms = st["ms_viewshed"] / K
     vunits = st["viewshed_crossings"] / K
     stages["viewshed"] = {"ms": round(vs_ms, 3), "los_crossings": int(vunits),
                           "los_samples_per_s": vunits / (vs_ms / 1e3) if vs_ms else None,
-                          "kernel": "k_viewshed", "bytes_per_launch": 4 * vunits}
+                          "kernel": "k_viewshed_evk" if cfg.roi <= 250 else "k_viewshed",
+                          "bytes_per_launch": 4 * vunits}
     site_ms = st["ms_site"] / K
     sbytes = st["site_bytes"] / K
     stages["site"] = {"ms": round(site_ms, 3), "iterations": st["site_iterations"] // K,
