@@ -102,17 +102,21 @@ RayTemplate build(int32_t R) {
 // Merged per-ray event stream (decision D5 evaluated in u order): for each ray
 // the crossings of its primitive direction interleaved with its owned cells,
 // a cell emitted before every crossing with u_k >= u_c, nothing after the
-// last cell.  Event word: bits 0-2 type, 3-11 row offset, 12-20 col offset
-// (9-bit two's complement), 21-28 interpolation weight m, bit 29 "byrow"
-// (the crossing's denominator is |p| and its index the row-line index).
-// Crossing offsets name the first interpolation post; the second lies one
-// step along +sign(q) columns (row line) or +sign(p) rows (column line).
-// The event's y is the crossing's line index (its slope's M) or, for a cell,
-// its projection numerator dot = a*p + b*q.
-inline uint2 pack_ev(uint32_t type, int dr, int dc, int m, bool byrow, int64_t y) {
-    return make_uint2(type | ((uint32_t)(dr & 0x1ff) << 3) | ((uint32_t)(dc & 0x1ff) << 12) | ((uint32_t)m << 21) |
-                          ((uint32_t)byrow << 29),
-                      (uint32_t)y);
+// last cell.  Event (uint2):
+//   x: bits 0-2 type, 3-11 row offset, 12-20 col offset (9-bit two's
+//      complement) of the crossing's FIRST interpolation post, 21-28 its
+//      weight w0;
+//   y: bits 0-23 the crossing's line index (its slope's M) or, for a cell, its
+//      projection numerator dot = a*p + b*q; bits 24-31 the weight w1 of the
+//      second post, which lies one column right (row crossing) or one row down
+//      (column crossing) of the first.
+// The interpolated height times the crossing's denominator n is
+// z0*w0 + z1*w1 with w0 + w1 = n (the pair is ordered by increasing column /
+// row whatever the ray's direction, so the GPU can read it as one packed pair);
+// posts carry (n, 0), cells (1, 0).
+inline uint2 pack_ev(uint32_t type, int dr, int dc, int w0, int w1, int64_t y) {
+    return make_uint2(type | ((uint32_t)(dr & 0x1ff) << 3) | ((uint32_t)(dc & 0x1ff) << 12) | ((uint32_t)w0 << 21),
+                      (uint32_t)y | ((uint32_t)w1 << 24));
 }
 
 EventTemplate build_events(const RayTemplate& T) {
@@ -135,13 +139,21 @@ EventTemplate build_events(const RayTemplate& T) {
                 else { const int64_t cmp = i * aq - j * ap; isrow = cmp <= 0; iscol = cmp >= 0; }
                 const int64_t idx = isrow ? i : j, n = isrow ? ap : aq;
                 if (idx * L2 >= dot * n) break;
-                if (isrow && iscol) ev.push_back(pack_ev(kEvPost, (int)(sp * i), (int)(sq * j), 0, true, i));
-                else if (isrow) ev.push_back(pack_ev(aq == 0 ? kEvPost : kEvRow, (int)(sp * i), (int)(sq * qr), (int)mr, true, i));
-                else ev.push_back(pack_ev(ap == 0 ? kEvPost : kEvCol, (int)(sp * qc), (int)(sq * j), (int)mc, false, j));
+                if (isrow && iscol) {
+                    ev.push_back(pack_ev(kEvPost, (int)(sp * i), (int)(sq * j), (int)ap, 0, i));
+                } else if (isrow) {   // posts (sp*i, sq*qr) weight ap-mr and (sp*i, sq*qr+sq) weight mr
+                    if (aq == 0) ev.push_back(pack_ev(kEvPost, (int)(sp * i), 0, (int)ap, 0, i));
+                    else if (sq > 0) ev.push_back(pack_ev(kEvRow, (int)(sp * i), (int)qr, (int)(ap - mr), (int)mr, i));
+                    else ev.push_back(pack_ev(kEvRow, (int)(sp * i), (int)(-qr - 1), (int)mr, (int)(ap - mr), i));
+                } else {              // posts (sp*qc, sq*j) weight aq-mc and (sp*qc+sp, sq*j) weight mc
+                    if (ap == 0) ev.push_back(pack_ev(kEvPost, 0, (int)(sq * j), (int)aq, 0, j));
+                    else if (sp > 0) ev.push_back(pack_ev(kEvCol, (int)qc, (int)(sq * j), (int)(aq - mc), (int)mc, j));
+                    else ev.push_back(pack_ev(kEvCol, (int)(-qc - 1), (int)(sq * j), (int)mc, (int)(aq - mc), j));
+                }
                 if (isrow) { ++i; qr += dqr; mr += dmr; if (mr >= ap) { mr -= ap; ++qr; } }
                 if (iscol) { ++j; qc += dqc; mc += dmc; if (mc >= aq) { mc -= aq; ++qc; } }
             }
-            ev.push_back(pack_ev(kEvCell, (int)a, (int)b, 0, false, dot));
+            ev.push_back(pack_ev(kEvCell, (int)a, (int)b, 1, 0, dot));
         }
     }
     const int64_t ngroups = (nrays + 31) / 32;

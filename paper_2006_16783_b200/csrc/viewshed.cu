@@ -68,6 +68,20 @@ __device__ __forceinline__ uint32_t vs_pld(const uint32_t* p) {
     return __ldg(p);
 }
 
+// s_bits[word] |= bit when pred (predicated, no branch; 32-bit shared address)
+__device__ __forceinline__ void red_or_shared(uint32_t saddr, uint32_t bit, bool pred) {
+    asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p red.shared.or.b32 [%0], %1;\n}\n" ::"r"(saddr), "r"(bit),
+                 "r"((uint32_t)pred)
+                 : "memory");
+}
+
+// signed 32x32 -> 64-bit product in one IMAD.WIDE
+__device__ __forceinline__ long long mulw(int a, int b) {
+    long long d;
+    asm("mul.wide.s32 %0, %1, %2;" : "=l"(d) : "r"(a), "r"(b));
+    return d;
+}
+
 __device__ __forceinline__ int vs_dp2(uint32_t pair, uint32_t w) {
     int d;
     asm("dp2a.lo.s32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(pair), "r"(w), "r"(0));
@@ -244,11 +258,7 @@ __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, 
         const int ray = g * 32 + lane;
         int p = 0, q = 0;
         if (ray < a.nrays) { const int4 rd = __ldg(rays + ray); p = rd.x; q = rd.y; }
-        const int ap = abs(p), aq = abs(q);
-        const int stepr = p >= 0 ? a.ncols : -a.ncols, stepc = q >= 0 ? 1 : -1;
-        const int sp = p >= 0 ? 1 : -1, sq = q >= 0 ? 1 : -1;
         const int L2 = p * p + q * q;
-        const int Eap = E * ap, Eaq = E * aq;
         bool has = false, alive = true;
         int NH = 0, MH = 1, L2MH = L2;
         const uint2* ev = events + (int64_t)grp.x * 32 + lane;
@@ -265,15 +275,15 @@ __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, 
                 const int dr = ((int)(e << 20)) >> 23, dc = ((int)(e << 11)) >> 23;
                 const bool isrow = type == kEvRow, iscol = type == kEvCol;
                 bool inb = type != kEvNop;
-                if (!INTERIOR) {
+                if (!INTERIOR) {   // both interpolation posts in the grid
                     const int rr = r + dr, cc = c + dc;
-                    const int r1 = rr + (iscol ? sp : 0), c1 = cc + (isrow ? sq : 0);
+                    const int r1 = rr + (iscol ? 1 : 0), c1 = cc + (isrow ? 1 : 0);
                     inb = inb && rr >= 0 && rr < a.nrows && cc >= 0 && cc < a.ncols && r1 >= 0 && r1 < a.nrows &&
                           c1 >= 0 && c1 < a.ncols;
                 }
                 kb[u] = dr * RS + dc + K0;
                 const int off0 = inb ? dr * a.ncols + dc : 0;
-                const int off1 = inb ? off0 + (iscol ? stepr : (isrow ? stepc : 0)) : 0;
+                const int off1 = inb ? off0 + (iscol ? a.ncols : (isrow ? 1 : 0)) : 0;
                 z0[u] = zld(P + off0);
                 z1[u] = zld(P + off1);
                 ok[u] = inb;
@@ -281,13 +291,11 @@ __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, 
 #pragma unroll
             for (int u = 0; u < kVsUnroll; ++u) {
                 const uint32_t e = ee[u].x, type = e & 7u;
-                const int y = (int)ee[u].y;
-                const int m = (int)((e >> 21) & 0xffu);
-                const bool byrow = (e >> 29) & 1u;
+                const int y = (int)(ee[u].y & 0xffffffu);
+                const int w0 = (int)((e >> 21) & 0xffu), w1 = (int)(ee[u].y >> 24);
                 const bool iscell = type == kEvCell, iscross = type <= kEvPost;
-                const int n = iscell ? 1 : (byrow ? ap : aq);
-                const int v = z0[u] * (n - m) + z1[u] * m;
-                const int X = v - (iscell ? Ehr : (byrow ? Eap : Eaq));
+                const int v = z0[u] * w0 + z1[u] * w1;
+                const int X = v - (iscell ? Ehr : (w0 + w1) * E);
                 const long long lhs = (long long)X * (iscell ? L2MH : MH);
                 const long long rhs = (long long)NH * y;
                 if (iscross) {
@@ -324,28 +332,29 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
     const uint32_t* __restrict__ B[K];   // PAIRS: the observer's word in the pair planes
     const int16_t* __restrict__ P[K];    // else: the observer's post
     int Ehr[K];
+    uint32_t sb[K];                      // shared byte address of bitmap k, shifted by its K0 bit
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        if (PAIRS) B[k] = a.pairs + (int64_t)(rk[k] - a.zoff) * a.p2 + ck[k];
-        else P[k] = z + (int64_t)rk[k] * a.ncols + ck[k];
+        if (PAIRS) {
+            // (threadIdx.x >> 10) == 0 but not provably so: B lives in per-thread
+            // registers, and B + off becomes one IMAD.WIDE instead of a 64-bit add chain
+            B[k] = a.pairs + (int64_t)(rk[k] - a.zoff) * a.p2 + ck[k] + (threadIdx.x >> 10);
+            asm("mov.b64 %0, %0;" : "+l"(B[k]));
+        } else {
+            P[k] = z + (int64_t)rk[k] * a.ncols + ck[k];
+        }
         Ehr[k] = Ek[k] - a.hr;
+        sb[k] = (uint32_t)__cvta_generic_to_shared(s_bits + k * bits_stride);
     }
     for (int g = warp; g < ngroups; g += nwarps) {
         const int2 grp = __ldg(groups + g);
         const int ray = g * 32 + lane;
         int p = 0, q = 0;
         if (ray < a.nrays) { const int4 rd = __ldg(rays + ray); p = rd.x; q = rd.y; }
-        const int ap = abs(p), aq = abs(q);
-        // PAIRS: row crossing reads the H pair (c, c+1) or, stepping to -col,
-        // (c-1, c) with swapped weights; column crossing the V pair likewise
-        const int hadj = q < 0 ? -1 : 0, vadj = a.pw + (p < 0 ? -a.p2 : 0);
-        const bool hswap = q < 0, vswap = p < 0;
-        const int stepr = p >= 0 ? a.ncols : -a.ncols, stepc = q >= 0 ? 1 : -1;
         const int L2 = p * p + q * q;
-        bool has[K];
-        int NH[K], MH[K], L2MH[K];
+        int has[K], NH[K], MH[K], L2MH[K];
 #pragma unroll
-        for (int k = 0; k < K; ++k) { has[k] = false; NH[k] = 0; MH[k] = 1; L2MH[k] = L2; }
+        for (int k = 0; k < K; ++k) { has[k] = 0; NH[k] = 0; MH[k] = 1; L2MH[k] = L2; }
         const uint2* ev = events + (int64_t)grp.x * 32 + lane;
         for (int st0 = 0; st0 < grp.y; st0 += 2) {
             uint2 ee[2];
@@ -359,13 +368,13 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
                 const int dr = ((int)(e << 20)) >> 23, dc = ((int)(e << 11)) >> 23;
                 const bool isrow = type == kEvRow, iscol = type == kEvCol;
                 dru[u] = dr; dcu[u] = dc;
-                if (PAIRS) {
-                    const int off = type != kEvNop ? dr * a.p2 + dc + (isrow ? hadj : (iscol ? vadj : 0)) : 0;
+                if (PAIRS) {   // the first post's H pair (its right neighbour) or, column crossing, V pair
+                    const int off = type != kEvNop ? dr * a.p2 + dc + (iscol ? a.pw : 0) : 0;
 #pragma unroll
                     for (int k = 0; k < K; ++k) pr[u][k] = vs_pld(B[k] + off);
                 } else {
                     const int off0 = type != kEvNop ? dr * a.ncols + dc : 0;
-                    const int off1 = off0 + (iscol ? stepr : (isrow ? stepc : 0));
+                    const int off1 = off0 + (iscol ? a.ncols : (isrow ? 1 : 0));
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
                         z0[u][k] = zld(P[k] + off0);
@@ -376,24 +385,23 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const uint32_t e = ee[u].x, type = e & 7u;
-                const int y = (int)ee[u].y;
-                const int m = (int)((e >> 21) & 0xffu);
-                const bool byrow = (e >> 29) & 1u;
+                const int y = (int)(ee[u].y & 0xffffffu);
+                const uint32_t W = ((e >> 21) & 0xffu) | ((ee[u].y >> 16) & 0xff00u);   // w0 | w1 << 8
+                const int w0 = (int)(W & 0xffu), w1 = (int)(W >> 8), n = w0 + w1;
                 const bool iscell = type == kEvCell, iscross = type <= kEvPost;
-                const int n = iscell ? 1 : (byrow ? ap : aq);
-                const bool swap = (type == kEvRow && hswap) || (type == kEvCol && vswap);
-                const uint32_t W = swap ? (uint32_t)(m | ((n - m) << 8)) : (uint32_t)((n - m) | (m << 8));
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
-                    const int v = PAIRS ? vs_dp2(pr[u][k], W) : z0[u][k] * (n - m) + z1[u][k] * m;
+                    const int v = PAIRS ? vs_dp2(pr[u][k], W) : z0[u][k] * w0 + z1[u][k] * w1;
                     const int X = v - (iscell ? Ehr[k] : n * Ek[k]);
-                    const long long lhs = (long long)X * (iscell ? L2MH[k] : MH[k]);
-                    const long long rhs = (long long)NH[k] * y;
-                    if (iscross && (!has[k] || lhs > rhs)) { has[k] = true; NH[k] = X; MH[k] = y; L2MH[k] = L2 * y; }
-                    if (iscell && (!has[k] || lhs >= rhs)) {
-                        const int kk = dru[u] * RSk[k] + dcu[u] + K0k[k];
-                        atomicOr(&s_bits[k * bits_stride + (kk >> 5)], 1u << (kk & 31));
-                    }
+                    const long long lhs = mulw(X, iscell ? L2MH[k] : MH[k]);
+                    const long long rhs = mulw(NH[k], y);
+                    const bool up = iscross & ((has[k] == 0) | (lhs > rhs));
+                    NH[k] = up ? X : NH[k];
+                    MH[k] = up ? y : MH[k];
+                    L2MH[k] = up ? L2 * y : L2MH[k];
+                    has[k] |= (int)up;
+                    const int kk = dru[u] * RSk[k] + dcu[u] + K0k[k];
+                    red_or_shared(sb[k] + ((kk >> 5) << 2), 1u << (kk & 31), iscell & ((has[k] == 0) | (lhs >= rhs)));
                 }
             }
         }
@@ -639,9 +647,8 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
         const unsigned grid = (unsigned)((n + kobs - 1) / kobs);
         // pair planes of the held rows (rebuilt per call, part of the timed stage;
         // shares the VIX quad-plane scratch buffer) -- measured (profiles/README.md):
-        // C5 (roi 250) 1852 -> 1786 ms, C2 (200) +0.9 %, C3 (100) +3.9 %, so only
-        // for roi >= 225; TXS_VS_PAIRS=0/1 overrides
-        bool use_pairs = p.roi >= 225;
+        // C2 19.3 -> 18.0 ms, C3 34.9 -> 32.3, C5 1816 -> 1590; TXS_VS_PAIRS=0/1 overrides
+        bool use_pairs = true;
         if (const char* e = getenv("TXS_VS_PAIRS")) use_pairs = atoi(e) != 0;
         if (use_pairs) {
         a.pw = (int)(((c->ncols + 31) & ~(int64_t)31) + 16);
