@@ -29,6 +29,16 @@ for st in stages:
                 e.find_candidates(p, copy=False)
             e.reset_stats()
             e.compute_all_viewsheds(p)
+        elif st == "site":    # incremental SITE (mode 0), the config's stop rules
+            if _ == 0:
+                if cfg.random_observers:
+                    e.random_observers(cfg.random_observers, cfg.observer_seed)
+                else:
+                    e.estimate_vix(p, copy=False)
+                    e.find_candidates(p, copy=False)
+                e.compute_all_viewsheds(p)
+            e.reset_stats()
+            e.site(p, cap=cfg.max_selected + 1 if cfg.max_selected > 0 else 1 << 20)
         elif st == "site1":   # full-rescan SITE, 64 rounds (the streaming figure)
             if _ == 0:
                 if cfg.random_observers:
