@@ -205,6 +205,43 @@ def load_traffic(kernel):
         return None
 
 
+def stage_figures(st, K, cfg, site_mode):
+    """Per-stage device times and algorithmic throughputs from the engine's
+    stats over K steps, and the roofline of the dominant stage's kernel."""
+    peak, peak_kind = load_peaks()
+    stages = {}
+    if cfg.samples:
+        vix_ms = st["ms_vix"] / K
+        units = st["vix_crossings_full"] / K
+        stages["vix"] = {"ms": round(vix_ms, 3), "los_crossings": int(units),
+                         "los_samples_per_s": units / (vix_ms / 1e3) if vix_ms else None,
+                         "kernel": "k_vix_quads" if cfg.roi <= 255 else "k_vix", "bytes_per_launch": 4 * units}
+        fm_ms = st["ms_findmax"] / K
+        stages["findmax"] = {"ms": round(fm_ms, 3), "kernel": "k_findmax", "bytes_per_launch": 2 * cfg.posts}
+    vs_ms = st["ms_viewshed"] / K
+    vunits = st["viewshed_crossings"] / K
+    stages["viewshed"] = {"ms": round(vs_ms, 3), "los_crossings": int(vunits),
+                          "los_samples_per_s": vunits / (vs_ms / 1e3) if vs_ms else None,
+                          "kernel": "k_viewshed_evk" if cfg.roi <= 250 else "k_viewshed",
+                          "bytes_per_launch": 4 * vunits}
+    site_ms = st["ms_site"] / K
+    sbytes = st["site_bytes"] / K
+    stages["site"] = {"ms": round(site_ms, 3), "iterations": int(st["site_iterations"] // K),
+                      "site_gbs": sbytes / (site_ms / 1e3) / 1e9 if site_ms else None,
+                      "kernel": "k_site_loop/k_update" if site_mode == 0 else "k_gain_full",
+                      "bytes_per_launch": sbytes, "mode": "incremental" if site_mode == 0 else "full-rescan"}
+    for s_ in stages.values():
+        s_["achieved_gbs"] = round(s_["bytes_per_launch"] / (s_["ms"] / 1e3) / 1e9, 2) if s_["ms"] else None
+    dom = max(stages, key=lambda k: stages[k]["ms"])
+    ach = stages[dom]["achieved_gbs"] or 0.0
+    roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+                "traffic": load_traffic(stages[dom]["kernel"]), "kernel": stages[dom]["kernel"], "stage": dom,
+                "peak_kind": peak_kind,
+                "bytes_model": "VIX/VIEWSHED: 4 B (two int16 posts) per grid-line crossing, no early exit; "
+                               "SITE: packed viewshed bytes streamed; FINDMAX: VixMap read twice"}
+    return stages, roofline, peak
+
+
 def run_b200(args, cfg):
     import numpy as np
     import torch
@@ -308,39 +345,9 @@ def run_b200(args, cfg):
 
     # ---- per-stage figures and the roofline of the dominant kernel -------
     K = args.steps
-    peak, peak_kind = load_peaks()
-    stages = {}
-    if cfg.samples:
-        vix_ms = st["ms_vix"] / K
-        units = st["vix_crossings_full"] / K
-        stages["vix"] = {"ms": round(vix_ms, 3), "los_crossings": int(units),
-                         "los_samples_per_s": units / (vix_ms / 1e3) if vix_ms else None,
-                         "kernel": "k_vix_quads" if cfg.roi <= 255 else "k_vix", "bytes_per_launch": 4 * units}
-        fm_ms = st["ms_findmax"] / K
-        stages["findmax"] = {"ms": round(fm_ms, 3), "kernel": "k_findmax", "bytes_per_launch": 2 * cfg.posts}
-    vs_ms = st["ms_viewshed"] / K
-    vunits = st["viewshed_crossings"] / K
-    stages["viewshed"] = {"ms": round(vs_ms, 3), "los_crossings": int(vunits),
-                          "los_samples_per_s": vunits / (vs_ms / 1e3) if vs_ms else None,
-                          "kernel": "k_viewshed_evk" if cfg.roi <= 250 else "k_viewshed",
-                          "bytes_per_launch": 4 * vunits}
-    site_ms = st["ms_site"] / K
-    sbytes = st["site_bytes"] / K
-    stages["site"] = {"ms": round(site_ms, 3), "iterations": st["site_iterations"] // K,
-                      "site_gbs": sbytes / (site_ms / 1e3) / 1e9 if site_ms else None,
-                      "kernel": "k_update" if args.site_mode == 0 else "k_gain_full", "bytes_per_launch": sbytes,
-                      "mode": "incremental" if args.site_mode == 0 else "full-rescan"}
-    for s in stages.values():
-        s["achieved_gbs"] = round(s["bytes_per_launch"] / (s["ms"] / 1e3) / 1e9, 2) if s["ms"] else None
+    stages, roofline, peak = stage_figures(st, K, cfg, args.site_mode)
     site_stream["frac_of_hbm"] = round(site_stream["gbs"] / peak, 4) if site_stream["gbs"] else None
     stages["site_stream"] = site_stream
-    dom = max((k for k in stages if k != "site_stream"), key=lambda k: stages[k]["ms"])
-    ach = stages[dom]["achieved_gbs"] or 0.0
-    roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
-                "traffic": load_traffic(stages[dom]["kernel"]), "kernel": stages[dom]["kernel"], "stage": dom,
-                "peak_kind": peak_kind,
-                "bytes_model": "VIX/VIEWSHED: 4 B (two int16 posts) per grid-line crossing, no early exit; "
-                               "SITE: packed viewshed bytes streamed; FINDMAX: VixMap read twice"}
     line = {
         "metric": METRIC, "value": round(ms / 1e3, 5), "unit": "s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "weak",
@@ -387,7 +394,20 @@ def run_b200_sharded(args, cfg):
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]), RANK="0", WORLD_SIZE="1")
         sk.close()
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", init_method="env://", device_id=torch.device(f"cuda:{local}"))
+    # NCCL may print its version line on stdout at communicator init (depending
+    # on NCCL_DEBUG): keep stdout for the one JSON line by pointing fd 1 at
+    # stderr while the communicator comes up
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device(f"cuda:{local}"))
+        dist.barrier()
+        torch.cuda.synchronize()
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
     dev = f"cuda:{local}"
     comm = TorchComm(dev)
     eng = T.Engine(local)
@@ -399,20 +419,37 @@ def run_b200_sharded(args, cfg):
     z_host[:] = eng.terrain()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for _ in range(args.warmup):
-        run_sharded(ranks, comm, cfg, params, world, setup=False, with_cum=False)
+        run_sharded(ranks, comm, cfg, params, world, setup=False, with_cum=False, device_rounds=True)
     eng.reset_stats()
     torch.cuda.synchronize()
     dist.barrier()
-    step_ms, res = [], None
+    phys = os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local] if os.environ.get(
+        "CUDA_VISIBLE_DEVICES") else str(local)
+    clocks = Clocks(phys)
+    clocks.start()
+    step_ms, res, site_ms = [], None, 0.0
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
         dist.barrier()
         eng.event_record(0)
-        res = run_sharded(ranks, comm, cfg, params, world, setup=False, with_cum=False)
+        res = run_sharded(ranks, comm, cfg, params, world, setup=False, with_cum=False, device_rounds=True)
         eng.event_record(1)
         step_ms.append(eng.event_elapsed(0, 1))
+        site_ms += res.get("site_ms", 0.0)
+    clk = clocks.stop()
     st = eng.stats()
+    # stage times: max over ranks; work units: summed over the bands
+    tm = torch.tensor([st["ms_vix"], st["ms_findmax"], st["ms_viewshed"], st["ms_site"] + site_ms,
+                       st["site_iterations"] + args.steps * len(res["index"])], device=dev, dtype=torch.float64)
+    dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    tc = torch.tensor([st["vix_crossings_full"], st["viewshed_crossings"], st["site_bytes"]], device=dev,
+                      dtype=torch.float64)
+    dist.all_reduce(tc, op=dist.ReduceOp.SUM)
+    agg = dict(st)
+    agg.update(ms_vix=tm[0].item(), ms_findmax=tm[1].item(), ms_viewshed=tm[2].item(), ms_site=tm[3].item(),
+               site_iterations=int(tm[4].item()), vix_crossings_full=tc[0].item(), viewshed_crossings=tc[1].item(),
+               site_bytes=tc[2].item())
     t = torch.tensor([sum(step_ms) / args.steps], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
@@ -424,7 +461,7 @@ def run_b200_sharded(args, cfg):
         eng.event_record(2)
         eng.set_shard(cfg.nrows, cfg.ncols, b0, b1, cfg.roi + 1)
         eng.set_terrain(z_host)
-        r2 = run_sharded(ranks, comm, cfg, params, world, setup=False, with_cum=True)
+        r2 = run_sharded(ranks, comm, cfg, params, world, setup=False, with_cum=True, device_rounds=True)
         eng.event_record(3)
         e2e_ms.append(eng.event_elapsed(2, 3))
     t = torch.tensor([statistics.mean(e2e_ms)], device=dev, dtype=torch.float64)
@@ -433,6 +470,7 @@ def run_b200_sharded(args, cfg):
     launches = torch.tensor([st["kernel_launches"]], device=dev, dtype=torch.int64)
     dist.all_reduce(launches, op=dist.ReduceOp.SUM)
     if rank == 0:
+        stages, roofline, _ = stage_figures(agg, args.steps, cfg, args.site_mode)
         line = {
             "metric": METRIC, "value": round(ms / 1e3, 5), "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
@@ -440,11 +478,15 @@ def run_b200_sharded(args, cfg):
             "data": "synthetic (seeded diamond-square terrain, BASELINE shapes)",
             "config": {"workload": cfg.name, "nrows": cfg.nrows, "ncols": cfg.ncols, "roi": cfg.roi,
                        "sited": int(len(res["index"])), "stop": res["stop"],
-                       "parallelism": f"rowband{world} (halo roi+1, NCCL allreduce per SITE round)",
+                       "parallelism": f"rowband{world} (halo roi+1; SITE rounds device-resident, two "
+                                      f"stream-ordered NCCL allreduces per round, {res.get('rounds_mode')})",
                        "l2": "flushed between steps (256 MB write outside the timed events)"},
             "e2e": {"value": round(e2e / 1e3, 5), "unit": "s", "h2d_bytes_per_step": cfg.posts * 2,
                     "d2h_bytes_per_step": ((cfg.posts + 63) // 64) * 8 + len(r2["index"]) * 32},
             "gpu_launches": int(launches.item()),
+            "stages": stages,
+            "roofline": roofline,
+            "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

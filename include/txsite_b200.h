@@ -189,6 +189,29 @@ txs_status txs_site_shard_export(txs_ctx* ctx, int64_t gid, int32_t* owned, int3
 txs_status txs_site_shard_apply(txs_ctx* ctx, int32_t row, int32_t col, const txs_window* win,
                                 const uint64_t* words);
 
+/* Device-resident form of the same round (no host round trip; for
+ * collectives issued on the context stream, e.g. NCCL through
+ * torch.distributed on txs_stream()):
+ *   txs_site_shard_best_dev    d_key[0] = this rank's best key (0 once stopped)
+ *   -- caller: allreduce(MAX) of d_key over the ranks --
+ *   txs_site_shard_export_dev  d_payload = the winner's {row, col, row0, col0, h, w,
+ *                              cum-aligned words} if this rank owns it, else zeros
+ *                              (txs_site_shard_payload_words() u64)
+ *   -- caller: allreduce(SUM) of d_payload (a broadcast from the data-dependent owner) --
+ *   txs_site_shard_apply_dev   stop rules (decision D9, total_candidates = global
+ *                              count), step record, cum OR + local gain updates;
+ *                              rounds after the stop are no-ops
+ * txs_site_shard_result copies the recorded steps and the stop reason (-1 while
+ * running).  All three calls are stream-ordered and return without waiting. */
+txs_status txs_site_shard_best_dev(txs_ctx* ctx, uint64_t* d_key);
+txs_status txs_site_shard_export_dev(txs_ctx* ctx, const uint64_t* d_key, uint64_t* d_payload);
+txs_status txs_site_shard_apply_dev(txs_ctx* ctx, const uint64_t* d_key, const uint64_t* d_payload,
+                                    int64_t total_candidates);
+int64_t txs_site_shard_payload_words(const txs_ctx* ctx);
+txs_status txs_site_shard_result(txs_ctx* ctx, txs_step* steps, int64_t cap, int64_t* nsteps, int32_t* stop_reason);
+/* The context's CUDA stream (a cudaStream_t), for ordering external work with it. */
+void* txs_stream(txs_ctx* ctx);
+
 /* ---- host-only helpers (no GPU needed; used by the CPU test-suite) -------- */
 /* The frozen D5 ray template for roi: returns ray count; arrays filled when the
  * caps suffice.  cell_begin has rays+1 entries. */

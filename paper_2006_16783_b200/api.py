@@ -254,6 +254,30 @@ class Engine:
         words = np.ascontiguousarray(words, np.uint64)
         self._chk(N.lib.txs_site_shard_apply(self._h, row, col, _p(win), _p(words)))
 
+    # ---- device-resident shard rounds (pointers are device addresses, e.g. torch tensors' data_ptr())
+    def site_shard_best_dev(self, d_key):
+        self._chk(N.lib.txs_site_shard_best_dev(self._h, C.c_void_p(d_key)))
+
+    def site_shard_export_dev(self, d_key, d_payload):
+        self._chk(N.lib.txs_site_shard_export_dev(self._h, C.c_void_p(d_key), C.c_void_p(d_payload)))
+
+    def site_shard_apply_dev(self, d_key, d_payload, total_candidates):
+        self._chk(N.lib.txs_site_shard_apply_dev(self._h, C.c_void_p(d_key), C.c_void_p(d_payload), total_candidates))
+
+    def site_shard_payload_words(self):
+        return int(N.lib.txs_site_shard_payload_words(self._h))
+
+    def site_shard_result(self, cap):
+        steps = (N.Step * max(1, cap))()
+        ns, stop = C.c_int64(), C.c_int32()
+        self._chk(N.lib.txs_site_shard_result(self._h, steps, cap, C.byref(ns), C.byref(stop)))
+        d = _steps_dict(steps, min(ns.value, cap), 0)
+        d["stop"] = STOP[stop.value] if stop.value >= 0 else None
+        return d
+
+    def stream(self):
+        return N.lib.txs_stream(self._h)
+
     def stats(self):
         s = N.Stats()
         self._chk(N.lib.txs_get_stats(self._h, C.byref(s)))

@@ -114,7 +114,7 @@ void txs_destroy(txs_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    void* bufs[] = {c->d_z, c->d_zt, c->d_pairs, c->d_gcd, c->d_vix, c->d_crow, c->d_ccol, c->d_cscore, c->d_words, c->d_win,
+    void* bufs[] = {c->d_shard_steps, c->d_z, c->d_zt, c->d_pairs, c->d_gcd, c->d_vix, c->d_crow, c->d_ccol, c->d_cscore, c->d_words, c->d_win,
                     c->d_pop, c->d_cum, c->d_dwin, c->d_dspan, c->d_partials, c->d_gain, c->d_state,
                     c->d_bucket_start, c->d_bucket_items, c->d_counters, c->d_scratch};
     for (void* p : bufs) if (p) cudaFree(p);
@@ -740,6 +740,48 @@ txs_status txs_site_shard_apply(txs_ctx* c, int32_t row, int32_t col, const txs_
     cudaSetDevice(c->device);
     return shard_site_apply(c, row, col, *win, words);
 }
+
+txs_status txs_site_shard_best_dev(txs_ctx* c, uint64_t* d_key) {
+    if (!c || !d_key) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->site_valid) return fail(c, TXS_ERR_STATE, "site", "call txs_site_shard_begin first");
+    cudaSetDevice(c->device);
+    return shard_site_best_dev(c, d_key);
+}
+
+txs_status txs_site_shard_export_dev(txs_ctx* c, const uint64_t* d_key, uint64_t* d_payload) {
+    if (!c || !d_key || !d_payload) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->site_valid) return fail(c, TXS_ERR_STATE, "site", "call txs_site_shard_begin first");
+    cudaSetDevice(c->device);
+    return shard_site_export_dev(c, d_key, d_payload);
+}
+
+txs_status txs_site_shard_apply_dev(txs_ctx* c, const uint64_t* d_key, const uint64_t* d_payload, int64_t total) {
+    if (!c || !d_key || !d_payload || total < 0) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->site_valid) return fail(c, TXS_ERR_STATE, "site", "call txs_site_shard_begin first");
+    cudaSetDevice(c->device);
+    return shard_site_apply_dev(c, d_key, d_payload, total);
+}
+
+int64_t txs_site_shard_payload_words(const txs_ctx* c) { return c ? shard_payload_words(c) : 0; }
+
+txs_status txs_site_shard_result(txs_ctx* c, txs_step* steps, int64_t cap, int64_t* nsteps, int32_t* stop) {
+    if (!c || !nsteps || !stop || (cap > 0 && !steps)) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->site_valid) return fail(c, TXS_ERR_STATE, "site", "call txs_site_shard_begin first");
+    cudaSetDevice(c->device);
+    TXS_CUDA(c, "site", cudaMemcpyAsync(c->h_state, c->d_state, sizeof(SiteState), cudaMemcpyDeviceToHost, c->stream));
+    TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+    const int64_t ns = c->h_state->nsel;
+    *nsteps = ns;
+    *stop = (c->h_state->done || c->h_state->finish) ? c->h_state->stop : -1;
+    const int64_t m = std::min<int64_t>({ns, cap, (int64_t)(c->shard_steps_cap / sizeof(txs_step))});
+    if (m > 0) {
+        TXS_CUDA(c, "site", cudaMemcpyAsync(steps, c->d_shard_steps, sizeof(txs_step) * m, cudaMemcpyDeviceToHost, c->stream));
+        TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+    }
+    return TXS_OK;
+}
+
+void* txs_stream(txs_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
 int txs_selftest(void) {
     // exact 64-bit modulo magic vs the hardware '%', divisors of the shapes

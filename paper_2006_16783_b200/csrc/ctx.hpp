@@ -122,6 +122,10 @@ struct txs_ctx {
     int64_t cum_r0 = 0, cum_r1 = 0;
     uint64_t* d_xfer = nullptr;          // sharded SITE: the broadcast winner window
     size_t xfer_cap = 0;
+    txs_step* d_shard_steps = nullptr;   // sharded SITE (device rounds): step log
+    size_t shard_steps_cap = 0;
+    double shard_target = 1.0;           // sharded SITE: stop rules of txs_site_shard_begin
+    int64_t shard_max_sel = 0;
     uint64_t* d_cum = nullptr;
     // per-round delta: newly covered words over the winner window (row pitch
     // dpitch words) and per-row [lo, hi] spans of non-zero words
@@ -193,6 +197,10 @@ txs_status viewsheds_from_dense(txs_ctx*, const uint64_t* d_dense, int64_t dstri
                                 uint64_t* d_aligned, int64_t astride, int64_t count);
 txs_status shard_site_best(txs_ctx*, uint64_t* key);
 txs_status shard_site_apply(txs_ctx*, int32_t row, int32_t col, const txs_window& win, const uint64_t* words);
+txs_status shard_site_best_dev(txs_ctx*, uint64_t* d_key);
+txs_status shard_site_export_dev(txs_ctx*, const uint64_t* d_key, uint64_t* d_payload);
+txs_status shard_site_apply_dev(txs_ctx*, const uint64_t* d_key, const uint64_t* d_payload, int64_t total);
+int64_t shard_payload_words(const txs_ctx*);
 
 }  // namespace txs
 

@@ -853,6 +853,115 @@ __global__ void k_shard_prep(SiteArgs a, SiteState* st, int r, int c, int4 win, 
     st->nb_count = nb;
 }
 
+// ---- device-resident shard rounds ----
+// Best local key, or 0 once this context's SITE stopped (done / final pick made).
+__global__ void k_shard_best_dev(const int32_t* __restrict__ gain, const int32_t* __restrict__ cgid, int64_t gid0,
+                                 int64_t n, const SiteState* st, unsigned long long* __restrict__ d_key) {
+    if (st->done || st->finish) return;
+    __shared__ unsigned long long s_red[32];
+    unsigned long long best = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t gid = cgid ? (uint64_t)cgid[i] : (uint64_t)(gid0 + i);
+        best = umax64(best, ((unsigned long long)(uint32_t)gain[i] << 32) | (0xffffffffull - gid));
+    }
+    for (int o = 16; o; o >>= 1) best = umax64(best, __shfl_xor_sync(kFull, best, o));
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < (int)(blockDim.x >> 5); ++k) best = umax64(best, s_red[k]);
+        best = umax64(best, s_red[0]);
+        if (best) atomicMax(d_key, best);
+    }
+}
+
+// One CTA: zero the payload; the rank holding the reduced key's candidate
+// writes {row, col, row0, col0, h, w, cum-aligned words} (the same layout on
+// every rank: aligned words are anchored to global terrain columns).
+__global__ void k_shard_export_dev(const SiteState* st, const unsigned long long* __restrict__ d_key,
+                                   const int32_t* __restrict__ cgid, int64_t gid0, int64_t n,
+                                   const int32_t* __restrict__ crow, const int32_t* __restrict__ ccol,
+                                   const int4* __restrict__ wins, const uint64_t* __restrict__ words, int64_t stride,
+                                   uint64_t* __restrict__ payload, int64_t pwords) {
+    __shared__ int64_t s_li;
+    for (int64_t t = threadIdx.x; t < pwords; t += blockDim.x) payload[t] = 0ull;
+    if (threadIdx.x == 0) {
+        s_li = -1;
+        const unsigned long long key = *d_key;
+        if (!st->done && !st->finish && (key >> 32) > 0) {
+            const int64_t gid = (int64_t)(0xffffffffull - (key & 0xffffffffull));
+            if (!cgid) {
+                if (gid >= gid0 && gid < gid0 + n) s_li = gid - gid0;
+            } else {   // sorted global draw indices
+                int64_t lo = 0, hi = n;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    if ((int64_t)cgid[mid] < gid) lo = mid + 1; else hi = mid;
+                }
+                if (lo < n && (int64_t)cgid[lo] == gid) s_li = lo;
+            }
+        }
+    }
+    __syncthreads();
+    const int64_t li = s_li;
+    if (li < 0) return;
+    const int4 win = wins[li];
+    const int total = win.z * win_nwr(win.y, win.w);
+    if (threadIdx.x == 0) {
+        payload[0] = (uint64_t)(uint32_t)crow[li];
+        payload[1] = (uint64_t)(uint32_t)ccol[li];
+        payload[2] = (uint64_t)(uint32_t)win.x;
+        payload[3] = (uint64_t)(uint32_t)win.y;
+        payload[4] = (uint64_t)(uint32_t)win.z;
+        payload[5] = (uint64_t)(uint32_t)win.w;
+    }
+    const uint64_t* v = words + li * stride;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) payload[6 + t] = v[t];
+}
+
+// One CTA: the round's decision from the reduced key and payload (identical on
+// every rank), step record, winner window and neighbour ranges; k_commit and
+// k_update follow and no-op once done.
+__global__ void k_shard_decide_dev(SiteArgs a, SiteState* st, const unsigned long long* __restrict__ d_key,
+                                   const uint64_t* __restrict__ payload, int64_t total_cand,
+                                   const int32_t* __restrict__ bstart, int2* __restrict__ dspan,
+                                   txs_step* __restrict__ steps, int64_t steps_cap) {
+    if (st->done) return;
+    if (st->finish) {   // the previous round committed the final pick
+        if (threadIdx.x == 0) st->done = 1;
+        return;
+    }
+    for (int y = threadIdx.x; y < 2 * a.R + 1; y += blockDim.x) dspan[y] = make_int2(0x7fffffff, -1);
+    if (threadIdx.x != 0) return;
+    if (st->nsel >= total_cand) { st->done = 1; st->stop = TXS_STOP_EXHAUSTED; return; }
+    const unsigned long long key = *d_key;
+    const long long g = (long long)(key >> 32);
+    if (g <= 0) { st->done = 1; st->stop = TXS_STOP_ZERO_GAIN; return; }
+    const int64_t gid = (int64_t)(0xffffffffull - (key & 0xffffffffull));
+    const int r = (int)(uint32_t)payload[0], c = (int)(uint32_t)payload[1];
+    st->w_row0 = (int)(uint32_t)payload[2]; st->w_col0 = (int)(uint32_t)payload[3];
+    st->w_h = (int)(uint32_t)payload[4]; st->w_w = (int)(uint32_t)payload[5];
+    st->w_idx = -1;
+    st->covered += g;
+    const double cov = (double)st->covered / a.total;
+    const long long k = st->nsel;
+    if (k < steps_cap) steps[k] = txs_step{gid, r, c, (int64_t)g, cov};
+    st->nsel = k + 1;
+    if (cov >= a.target) { st->finish = 1; st->stop = TXS_STOP_TARGET_REACHED; }
+    else if (a.max_sel > 0 && k + 1 >= a.max_sel) { st->finish = 1; st->stop = TXS_STOP_MAX_SELECTED; }
+    const int by0 = max(0, (r - 2 * a.R) / a.bsize), by1 = min(a.nby - 1, (r + 2 * a.R) / a.bsize);
+    const int bx0 = max(0, (c - 2 * a.R) / a.bsize), bx1 = min(a.nbx - 1, (c + 2 * a.R) / a.bsize);
+    int nb = 0, pref = 0;
+    for (int by = by0; by <= by1 && nb < kMaxNb; ++by) {
+        const int s0 = bstart[by * a.nbx + bx0], e0 = bstart[by * a.nbx + bx1 + 1];
+        st->nb_start[nb] = s0;
+        st->nb_pref[nb] = pref;
+        pref += e0 - s0;
+        ++nb;
+    }
+    st->nb_pref[nb] = pref;
+    st->nb_count = nb;
+}
+
 }  // namespace
 
 txs_status viewsheds_to_dense(txs_ctx* c, int64_t first, int64_t count, uint64_t* d_dense, int64_t dstride) {
@@ -898,6 +1007,8 @@ txs_status shard_site_begin(txs_ctx* c, const txs_params& p) {
     const int64_t mw = max_window_words(R) + 2 + aligned_stride(R) + 2;
     if (ensure(c, "site", (void**)&c->d_xfer, &c->xfer_cap, sizeof(uint64_t) * mw) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
     TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+    c->shard_target = p.target_coverage;
+    c->shard_max_sel = p.max_selected;
     c->site_valid = true;
     return TXS_OK;
 }
@@ -944,6 +1055,49 @@ txs_status shard_site_apply(txs_ctx* c, int32_t row, int32_t col, const txs_wind
                                                            c->d_bucket_items, c->d_gain, c->d_counters);
     TXS_LAUNCHED(c, "site");
     c->stats.site_iterations += 1;
+    return TXS_OK;
+}
+
+int64_t shard_payload_words(const txs_ctx* c) { return 6 + aligned_stride(c->vs_roi); }
+
+txs_status shard_site_best_dev(txs_ctx* c, uint64_t* d_key) {
+    const int64_t n = c->vs_n;
+    TXS_CUDA(c, "site", cudaMemsetAsync(d_key, 0, sizeof(uint64_t), c->stream));
+    if (n > 0) {
+        k_shard_best_dev<<<blocks_for(n, 1024, c->num_sms * 2), 256, 0, c->stream>>>(
+            c->d_gain, c->h_cgid.empty() ? nullptr : c->d_cgid, c->cand_gid0, n, c->d_state,
+            (unsigned long long*)d_key);
+        TXS_LAUNCHED(c, "site");
+    }
+    return TXS_OK;
+}
+
+txs_status shard_site_export_dev(txs_ctx* c, const uint64_t* d_key, uint64_t* d_payload) {
+    k_shard_export_dev<<<1, 256, 0, c->stream>>>(c->d_state, (const unsigned long long*)d_key,
+                                                 c->h_cgid.empty() ? nullptr : c->d_cgid, c->cand_gid0, c->vs_n,
+                                                 c->d_crow, c->d_ccol, c->d_win, c->d_words, c->vs_stride, d_payload,
+                                                 shard_payload_words(c));
+    TXS_LAUNCHED(c, "site");
+    return TXS_OK;
+}
+
+txs_status shard_site_apply_dev(txs_ctx* c, const uint64_t* d_key, const uint64_t* d_payload, int64_t total) {
+    txs_params p{};
+    p.target_coverage = c->shard_target;
+    p.max_selected = c->shard_max_sel;
+    const SiteArgs a = make_args(c, p);
+    const int64_t cap = std::max<int64_t>(1, total);
+    if (ensure(c, "site", (void**)&c->d_shard_steps, &c->shard_steps_cap, sizeof(txs_step) * cap) != TXS_OK)
+        return TXS_ERR_OUT_OF_MEMORY;
+    k_shard_decide_dev<<<1, 256, 0, c->stream>>>(a, c->d_state, (const unsigned long long*)d_key, d_payload, total,
+                                                 c->d_bucket_start, c->d_dspan, c->d_shard_steps, cap);
+    TXS_LAUNCHED(c, "site");
+    uint64_t* cumv = c->d_cum - c->cum_r0 * c->wpr;
+    k_commit<<<16, 256, 0, c->stream>>>(a, c->d_state, c->d_words, cumv, c->d_dwin, c->d_dspan, d_payload + 6);
+    TXS_LAUNCHED(c, "site");
+    k_update<<<c->num_sms * 8, kUpdThreads, 0, c->stream>>>(a, c->d_state, c->d_win, c->d_words, c->d_dwin, c->d_dspan,
+                                                           c->d_bucket_items, c->d_gain, c->d_counters);
+    TXS_LAUNCHED(c, "site");
     return TXS_OK;
 }
 

@@ -49,17 +49,38 @@ class LocalComm:
     def allgather_i64(self, arr):
         return np.asarray(arr, np.int64)
 
+    # device-round collectives over the local ranks' device buffers (tests:
+    # every engine's stream is drained, the reduction runs on torch's stream)
+    def max_dev(self, tensors, engines):
+        return self._reduce_dev(tensors, engines, "max")
+
+    def sum_dev(self, tensors, engines):
+        return self._reduce_dev(tensors, engines, "sum")
+
+    @staticmethod
+    def _reduce_dev(tensors, engines, op):
+        import torch
+        for e in engines:
+            e.synchronize()
+        if len(tensors) > 1:
+            st = torch.stack(tensors)
+            red = st.max(0).values if op == "max" else st.sum(0)
+            for t in tensors:
+                t.copy_(red)
+            torch.cuda.synchronize()
+
 
 class TorchComm:
     """Collectives through torch.distributed (NCCL on GPUs, gloo on CPU).  Keys
     are < 2^63 (gain < 2^31), so signed int64 MAX is exact; the winner payload
     is reinterpreted as int64 for a SUM with zeros (bit-exact)."""
 
-    def __init__(self, device="cpu"):
+    def __init__(self, device="cpu", graphs=True):
         import torch
         import torch.distributed as dist
         self.torch, self.dist, self.device = torch, dist, device
         self.world = dist.get_world_size()
+        self.graphs = graphs and str(device).startswith("cuda")   # capture device rounds as CUDA graphs
 
     def max_i64(self, x):
         t = self.torch.tensor([int(x)], dtype=self.torch.int64, device=self.device)
@@ -77,6 +98,19 @@ class TorchComm:
         outs = [self.torch.zeros_like(t) for _ in range(self.world)]
         self.dist.all_gather(outs, t)
         return np.concatenate([o.cpu().numpy() for o in outs])
+
+    # device-round collectives: issued on the engine's stream, so they order
+    # with its kernels without any host wait (one engine per process)
+    def max_dev(self, tensors, engines):
+        self._on_stream(tensors[0], engines[0], self.dist.ReduceOp.MAX)
+
+    def sum_dev(self, tensors, engines):
+        self._on_stream(tensors[0], engines[0], self.dist.ReduceOp.SUM)
+
+    def _on_stream(self, t, eng, op):
+        s = self.torch.cuda.ExternalStream(eng.stream(), device=t.device)
+        with self.torch.cuda.stream(s):
+            self.dist.all_reduce(t, op=op)
 
 
 def _mw(roi):
@@ -108,11 +142,14 @@ def setup_sharded(ranks, cfg, nbands, host_terrain=None):
     return active
 
 
-def run_sharded(ranks, comm, cfg, params, nbands, setup=True, with_cum=True):
+def run_sharded(ranks, comm, cfg, params, nbands, setup=True, with_cum=True, device_rounds=False):
     """Run one configuration (paper_2006_16783_b200.configs.Config) over row
     bands.  Returns dict(index,row,col,gain,coverage,stop,cum) with the global
     dense cumulative bitmap.  With setup=False the ranks already
-    hold their terrain (setup_sharded)."""
+    hold their terrain (setup_sharded).  device_rounds=True runs the SITE
+    rounds on the device (txs_site_shard_*_dev): keys and winner payloads stay
+    in device buffers and the two collectives per round are stream-ordered,
+    so the host only polls for the stop every few rounds."""
     nr, nc, roi = cfg.nrows, cfg.ncols, cfg.roi
     bands = plan_bands(nr, cfg.block if cfg.block else max(1, roi), nbands)
     if setup:
@@ -141,6 +178,11 @@ def run_sharded(ranks, comm, cfg, params, nbands, setup=True, with_cum=True):
         eng.compute_all_viewsheds(params)
         eng.site_shard_begin(params)
     # ---- SITE rounds ----------------------------------------------------------------
+    if device_rounds:
+        out = _device_rounds(active, comm, total_cand)
+        if not with_cum:
+            return out
+        return _with_cum(out, active, comm, bands, nr, nc)
     total = float(nr) * float(nc)
     mw = _mw(roi)
     idx, rows, cols, gains, covs = [], [], [], [], []
@@ -184,7 +226,11 @@ def run_sharded(ranks, comm, cfg, params, nbands, setup=True, with_cum=True):
                gain=np.array(gains, np.int64), coverage=np.array(covs), stop=stop)
     if not with_cum:
         return out
-    # ---- global cumulative bitmap: each band's rows, summed (disjoint bits) ----
+    return _with_cum(out, active, comm, bands, nr, nc)
+
+
+def _with_cum(out, active, comm, bands, nr, nc):
+    """Global cumulative bitmap: each band's rows, summed (disjoint bits)."""
     nw = (nr * nc + 63) // 64
     cum = np.zeros(nw, np.uint64)
     for eng, k in active:
@@ -198,3 +244,61 @@ def run_sharded(ranks, comm, cfg, params, nbands, setup=True, with_cum=True):
         cum |= packed
     out["cum"] = comm.sum_i64(cum)
     return out
+
+
+def _device_rounds(active, comm, total_cand, poll_every=16):
+    """SITE rounds with the keys and payloads in device buffers (see run_sharded).
+    With one engine per process (TorchComm) a block of `poll_every` rounds --
+    engine kernels and NCCL collectives, all on the engine's stream -- is
+    captured once as a CUDA graph and replayed until the device reports the stop."""
+    import torch
+    engines = [e for e, _ in active]
+    pw = engines[0].site_shard_payload_words()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    keys = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in engines]
+    pays = [torch.zeros(pw, dtype=torch.int64, device=dev) for _ in engines]
+    torch.cuda.synchronize()
+
+    def one_round():
+        for e, k in zip(engines, keys):
+            e.site_shard_best_dev(k.data_ptr())
+        comm.max_dev(keys, engines)
+        for e, k, p in zip(engines, keys, pays):
+            e.site_shard_export_dev(k.data_ptr(), p.data_ptr())
+        comm.sum_dev(pays, engines)
+        for e, k, p in zip(engines, keys, pays):
+            e.site_shard_apply_dev(k.data_ptr(), p.data_ptr(), total_cand)
+
+    engines[0].event_record(14)
+    one_round()                                   # eager: sizes the device step log
+    done = 1
+    graph = None
+    if len(engines) == 1 and getattr(comm, "graphs", False):
+        try:
+            s = torch.cuda.ExternalStream(engines[0].stream(), device=dev)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=s):
+                for _ in range(poll_every):
+                    one_round()
+        except Exception as ex:                   # capture unsupported here: eager rounds
+            import sys
+            print(f"shard: CUDA-graph capture of the SITE rounds failed ({ex!r}); eager rounds", file=sys.stderr)
+            graph = None
+            torch.cuda.synchronize()
+    res = engines[0].site_shard_result(max(1, total_cand))
+    while res["stop"] is None and done <= total_cand + 1:
+        if graph is not None:
+            graph.replay()
+            done += poll_every
+        else:
+            for _ in range(poll_every):
+                one_round()
+            done += poll_every
+        res = engines[0].site_shard_result(max(1, total_cand))
+    engines[0].event_record(15)
+    res = engines[0].site_shard_result(max(1, total_cand))
+    if res["stop"] is None:
+        raise RuntimeError("sharded SITE did not stop")
+    res["site_ms"] = engines[0].event_elapsed(14, 15)   # device time of the rounds (rank-local)
+    res["rounds_mode"] = "graph" if graph is not None else "eager"
+    return res

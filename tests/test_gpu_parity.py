@@ -362,9 +362,12 @@ def test_cli_matches_oracle_and_is_deterministic(tmp_path):
 
 
 # ---- row-band shards on one device (virtual ranks) ---------------
+@pytest.mark.parametrize("device_rounds", [False, True])
 @pytest.mark.parametrize("kind,nb", [("findmax", 1), ("findmax", 2), ("findmax", 3), ("observers", 2),
                                      ("observers", 4)])
-def test_sharded_engine_matches_single(kind, nb):
+def test_sharded_engine_matches_single(kind, nb, device_rounds):
+    """Row bands on virtual ranks (one device) == the single-context run, with
+    the SITE rounds host-driven or device-resident (txs_site_shard_*_dev)."""
     T = _T()
     from paper_2006_16783_b200.configs import Config, params_for, run, setup_terrain
     from paper_2006_16783_b200.shard import LocalComm, run_sharded
@@ -375,7 +378,8 @@ def test_sharded_engine_matches_single(kind, nb):
                      random_observers=2000, observer_seed=77)
     params = params_for(cfg)
     engines = [T.Engine(0) for _ in range(nb)]
-    res = run_sharded([(e, k) for k, e in enumerate(engines)], LocalComm(), cfg, params, nb)
+    res = run_sharded([(e, k) for k, e in enumerate(engines)], LocalComm(), cfg, params, nb,
+                      device_rounds=device_rounds)
     with T.Engine(0) as e:
         setup_terrain(e, cfg)
         single = run(e, cfg, params)
@@ -402,3 +406,33 @@ def test_bounds_checked_build_edge_workloads():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "sharded" in r.stdout
+
+
+def test_sharded_bench_torchrun_world1():
+    """bench.py's row-band path under torchrun (NCCL, world 1): device-resident
+    SITE rounds captured as a CUDA graph with the NCCL collectives, one JSON
+    line on stdout, and the same picks as the single-context bench line."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "bench.py"), "--gpus", "1",
+           "--sharded", "--config", "c1", "--steps", "1", "--warmup", "1", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert "graph" in d["config"]["parallelism"] and d["roofline"] and d["stages"]["site"]["ms"] > 0
+    r1 = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "c1", "--steps", "1",
+                         "--warmup", "1", "--no-cpu-baseline"], cwd=root, capture_output=True, text=True, timeout=600)
+    assert r1.returncode == 0, r1.stderr[-3000:]
+    d1 = json.loads(r1.stdout.strip().splitlines()[-1])
+    assert d["config"]["sited"] == d1["config"]["sited"] and d["config"]["stop"] == d1["config"]["stop"]
