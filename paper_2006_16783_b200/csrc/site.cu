@@ -701,7 +701,11 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
         // persistent cooperative loop: as many co-resident CTAs as fit, <= 2 per SM
         int per_sm = 0;
         TXS_CUDA(c, "site", cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_site_loop, kLoopThreads, 0));
-        const int grid = std::max(1, std::min(per_sm, 2)) * sms;
+        // CTAs per SM (measured, profiles/README.md): 4 when a round updates
+        // hundreds of neighbours (C2: 10.2 -> 9.1 ms), else 2 (C3: grid syncs dominate)
+        int want = expected_nb >= 400.0 ? 4 : 2;
+        if (const char* e = getenv("TXS_SITE_LOOP_CTAS")) want = std::max(1, atoi(e));
+        const int grid = std::max(1, std::min(per_sm, want)) * sms;
         if (ensure(c, "site", (void**)&c->d_partials, &c->partials_cap, sizeof(unsigned long long) * grid) != TXS_OK)
             return TXS_ERR_OUT_OF_MEMORY;
         int2* sp1 = c->d_dspan + (2 * a.R + 1);
