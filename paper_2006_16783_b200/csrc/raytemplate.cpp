@@ -104,8 +104,8 @@ RayTemplate build(int32_t R) {
 // a cell emitted before every crossing with u_k >= u_c, nothing after the
 // last cell.  Event (uint2):
 //   x: bits 0-2 type, 3-11 row offset, 12-20 col offset (9-bit two's
-//      complement) of the crossing's FIRST interpolation post, 21-28 its
-//      weight w0;
+//      complement) of the crossing's FIRST interpolation post, 24-31 its
+//      weight w0 (so that one byte permute yields the dp2a weight word);
 //   y: bits 0-23 the crossing's line index (its slope's M) or, for a cell, its
 //      projection numerator dot = a*p + b*q; bits 24-31 the weight w1 of the
 //      second post, which lies one column right (row crossing) or one row down
@@ -115,7 +115,7 @@ RayTemplate build(int32_t R) {
 // row whatever the ray's direction, so the GPU can read it as one packed pair);
 // posts carry (n, 0), cells (1, 0).
 inline uint2 pack_ev(uint32_t type, int dr, int dc, int w0, int w1, int64_t y) {
-    return make_uint2(type | ((uint32_t)(dr & 0x1ff) << 3) | ((uint32_t)(dc & 0x1ff) << 12) | ((uint32_t)w0 << 21),
+    return make_uint2(type | ((uint32_t)(dr & 0x1ff) << 3) | ((uint32_t)(dc & 0x1ff) << 12) | ((uint32_t)w0 << 24),
                       (uint32_t)y | ((uint32_t)w1 << 24));
 }
 

@@ -292,7 +292,7 @@ __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, 
             for (int u = 0; u < kVsUnroll; ++u) {
                 const uint32_t e = ee[u].x, type = e & 7u;
                 const int y = (int)(ee[u].y & 0xffffffu);
-                const int w0 = (int)((e >> 21) & 0xffu), w1 = (int)(ee[u].y >> 24);
+                const int w0 = (int)(e >> 24), w1 = (int)(ee[u].y >> 24);
                 const bool iscell = type == kEvCell, iscross = type <= kEvPost;
                 const int v = z0[u] * w0 + z1[u] * w1;
                 const int X = v - (iscell ? Ehr : (w0 + w1) * E);
@@ -332,7 +332,8 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
     const uint32_t* __restrict__ B[K];   // PAIRS: the observer's word in the pair planes
     const int16_t* __restrict__ P[K];    // else: the observer's post
     int Ehr[K];
-    uint32_t sb[K];                      // shared byte address of bitmap k, shifted by its K0 bit
+    uint32_t sb[K];                      // shared byte address of bitmap k
+    const int RS0 = RSk[0], K00 = K0k[0];   // identical for every interior observer
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         if (PAIRS) {
@@ -386,9 +387,13 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
             for (int u = 0; u < 2; ++u) {
                 const uint32_t e = ee[u].x, type = e & 7u;
                 const int y = (int)(ee[u].y & 0xffffffu);
-                const uint32_t W = ((e >> 21) & 0xffu) | ((ee[u].y >> 16) & 0xff00u);   // w0 | w1 << 8
-                const int w0 = (int)(W & 0xffu), w1 = (int)(W >> 8), n = w0 + w1;
+                const uint32_t W = __byte_perm(e, ee[u].y, 0x73u);   // w0 | w1 << 8
+                const int w0 = (int)(W & 0xffu), w1 = (int)((W >> 8) & 0xffu), n = w0 + w1;
                 const bool iscell = type == kEvCell, iscross = type <= kEvPost;
+                // interior observers share the window geometry (pitch 2R+1, origin
+                // bit R*(2R+1)+R): the cell's word and bit are observer-independent
+                const int kk = dru[u] * RS0 + dcu[u] + K00;
+                const uint32_t cw4 = (uint32_t)(kk >> 5) << 2, cbit = 1u << (kk & 31);
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     const int v = PAIRS ? vs_dp2(pr[u][k], W) : z0[u][k] * w0 + z1[u][k] * w1;
@@ -400,8 +405,7 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
                     MH[k] = up ? y : MH[k];
                     L2MH[k] = up ? L2 * y : L2MH[k];
                     has[k] |= (int)up;
-                    const int kk = dru[u] * RSk[k] + dcu[u] + K0k[k];
-                    red_or_shared(sb[k] + ((kk >> 5) << 2), 1u << (kk & 31), iscell & ((has[k] == 0) | (lhs >= rhs)));
+                    red_or_shared(sb[k] + cw4, cbit, iscell & ((has[k] == 0) | (lhs >= rhs)));
                 }
             }
         }

@@ -170,6 +170,21 @@ def test_viewsheds_c1_bit_exact(engine, c1):
     _vs_compare(engine, c1, 100, 10, 10, rows, cols)
 
 
+@pytest.mark.parametrize("k,pairs", [(1, 0), (2, 0), (2, 1), (4, 1)])
+def test_viewsheds_k_paths_bit_exact(engine, monkeypatch, k, pairs):
+    """Every VIEWSHED sweep: K observers per CTA (1/2/4, TXS_VS_K), int16 posts
+    or H/V pair planes (TXS_VS_PAIRS), tile-sorted order (n >= 4096), CTAs
+    mixing interior and edge observers -- all against the oracle."""
+    rng = np.random.default_rng(100 + k)
+    z = O.generate_fractal(700, 650, 0.6, 33, -200, 2500)
+    n = 5000
+    rows, cols = rng.integers(0, 700, n).astype(np.int32), rng.integers(0, 650, n).astype(np.int32)
+    rows[:6], cols[:6] = [0, 699, 0, 699, 41, 658], [0, 649, 649, 0, 41, 608]
+    monkeypatch.setenv("TXS_VS_K", str(k))
+    monkeypatch.setenv("TXS_VS_PAIRS", str(pairs))
+    _vs_compare(engine, z, 40, 15, 5, rows, cols)
+
+
 @pytest.mark.parametrize("roi,h", [(200, 20), (250, 50), (1, 0), (3, 5), (300, 10), (100, 10)])
 def test_viewsheds_sampled_bit_exact(engine, roi, h):
     z = O.generate_fractal(1100, 1300, 0.5, 31, 0, 4000)
