@@ -263,6 +263,23 @@ def test_site_bucket_tiled_bit_exact(engine, mode):
     _site_compare(engine, 20, rows, cols, 200, 256, 1.0, 0, mode)
 
 
+@pytest.mark.parametrize("ctas", ["", "1", "3"])
+def test_site_persistent_loop_widths(engine, monkeypatch, ctas):
+    """Persistent SITE loop with 400-1000 expected neighbours per round (4 CTAs
+    per SM by default) and forced widths, against the oracle."""
+    T = _T()
+    z = O.generate_fractal(300, 300, 0.6, 9, 0, 2500)
+    rng = np.random.default_rng(21)
+    n = 6000
+    rows, cols = rng.integers(0, 300, n).astype(np.int32), rng.integers(0, 300, n).astype(np.int32)
+    engine.set_terrain(z)
+    engine.set_candidates(rows, cols)
+    engine.compute_all_viewsheds(T.make_params(20, 8, 4))
+    if ctas:
+        monkeypatch.setenv("TXS_SITE_LOOP_CTAS", ctas)
+    _site_compare(engine, 20, rows, cols, 300, 300, 0.97, 0, 0)
+
+
 def test_site_edge_cases(engine):
     T = _T()
     z = O.generate_fractal(64, 64, 0.5, 2, 0, 4000)
