@@ -353,9 +353,15 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
         int p = 0, q = 0;
         if (ray < a.nrays) { const int4 rd = __ldg(rays + ray); p = rd.x; q = rd.y; }
         const int L2 = p * p + q * q;
-        int has[K], NH[K], MH[K], L2MH[K];
+        // horizon NH/MH, starting at a sentinel below every real tangent: any
+        // crossing replaces it and every cell before the first crossing is
+        // visible.  Exact for int16 terrain, heights <= 32767 (txs_params
+        // check) and roi <= 250: a crossing's |X| <= 98302*255 < 2^30 <= 2^30*M,
+        // a cell's |X|*L2 <= 98302*L2 < 2^30*dot (an owned cell lies ahead of
+        // its ray: dot >= 0.7*|(p,q)|, and |(p,q)| <= 354)
+        int NH[K], MH[K], L2MH[K];
 #pragma unroll
-        for (int k = 0; k < K; ++k) { has[k] = 0; NH[k] = 0; MH[k] = 1; L2MH[k] = L2; }
+        for (int k = 0; k < K; ++k) { NH[k] = -(1 << 30); MH[k] = 1; L2MH[k] = L2; }
         const uint2* ev = events + (int64_t)grp.x * 32 + lane;
         for (int st0 = 0; st0 < grp.y; st0 += 2) {
             uint2 ee[2];
@@ -400,12 +406,11 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
                     const int X = v - (iscell ? Ehr[k] : n * Ek[k]);
                     const long long lhs = mulw(X, iscell ? L2MH[k] : MH[k]);
                     const long long rhs = mulw(NH[k], y);
-                    const bool up = iscross & ((has[k] == 0) | (lhs > rhs));
+                    const bool up = iscross & (lhs > rhs);
                     NH[k] = up ? X : NH[k];
                     MH[k] = up ? y : MH[k];
                     L2MH[k] = up ? L2 * y : L2MH[k];
-                    has[k] |= (int)up;
-                    red_or_shared(sb[k] + cw4, cbit, iscell & ((has[k] == 0) | (lhs >= rhs)));
+                    red_or_shared(sb[k] + cw4, cbit, iscell & (lhs >= rhs));
                 }
             }
         }
