@@ -362,7 +362,8 @@ def run_b200(args, cfg):
         "stages": stages,
         "roofline": roofline,
         "e2e": {"value": round(e2e / 1e3, 5), "unit": "s", "h2d_bytes_per_step": cfg.posts * 2,
-                "d2h_bytes_per_step": d2h, "kernel_launches_per_step": launches_e2e},
+                "d2h_bytes_per_step": d2h, "kernel_launches_per_step": launches_e2e,
+                "steps_ms": [round(x, 3) for x in e2e_ms]},
         "gpu_launches": st["kernel_launches"],
         "clocks": clk,
     }
