@@ -35,7 +35,7 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--site-mode", type=int, default=0)
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--threads", type=int, default=0, help="CPU threads for the oracle legs (0 = all)")
     ap.add_argument("--sharded", action="store_true", help="row-band path even at N=1 (NCCL world of 1)")
@@ -331,7 +331,10 @@ def run_b200(args, cfg):
         eng.event_record(3)
         e2e_ms.append(eng.event_elapsed(2, 3))
         launches_e2e = eng.stats()["kernel_launches"] - before
-    e2e = statistics.mean(e2e_ms)
+    # median over the e2e steps: a host-side stall (seen as an occasional
+    # 200-400 ms gap between the step's device events) does not set the figure;
+    # every step's time is reported beside it
+    e2e = statistics.median(e2e_ms)
     if world > 1:
         t = torch.tensor([e2e], device=f"cuda:{local}", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -363,7 +366,7 @@ def run_b200(args, cfg):
         "roofline": roofline,
         "e2e": {"value": round(e2e / 1e3, 5), "unit": "s", "h2d_bytes_per_step": cfg.posts * 2,
                 "d2h_bytes_per_step": d2h, "kernel_launches_per_step": launches_e2e,
-                "steps_ms": [round(x, 3) for x in e2e_ms]},
+                "steps_ms": [round(x, 3) for x in e2e_ms], "statistic": "median"},
         "gpu_launches": st["kernel_launches"],
         "clocks": clk,
     }
@@ -465,7 +468,7 @@ def run_b200_sharded(args, cfg):
         r2 = run_sharded(ranks, comm, cfg, params, world, setup=False, with_cum=True, device_rounds=True)
         eng.event_record(3)
         e2e_ms.append(eng.event_elapsed(2, 3))
-    t = torch.tensor([statistics.mean(e2e_ms)], device=dev, dtype=torch.float64)
+    t = torch.tensor([statistics.median(e2e_ms)], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e = float(t.item())
     launches = torch.tensor([st["kernel_launches"]], device=dev, dtype=torch.int64)
