@@ -26,7 +26,8 @@ namespace {
 #ifndef VIX_THREADS
 #define VIX_THREADS 512
 #endif
-constexpr int kTile = VIX_TILE;    // posts per tile side
+constexpr int kTile = 32;          // posts per tile side (shared-memory tile / column-major paths)
+constexpr int kTileQ = VIX_TILE;   // posts per tile side (quad-plane path)
 constexpr int kVixThreads = VIX_THREADS;   // 16 warps
 constexpr int kVixWarps = kVixThreads / 32;
 constexpr unsigned kFull = 0xffffffffu;
@@ -472,12 +473,12 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
         ty = rem / sw;
         tx = sidx * a.strip + (rem - ty * sw);
     }
-    const int ty0 = a.row0 + ty * kTile, tx0 = tx * kTile;
+    const int ty0 = a.row0 + ty * kTileQ, tx0 = tx * kTileQ;
     const int R2 = a.R * a.R;
     unsigned long long n_cross = 0;
     int n_posts = 0;
-    for (int pi = warp; pi < kTile * kTile; pi += kVixWarps) {
-        const int r = ty0 + pi / kTile, c = tx0 + pi % kTile;
+    for (int pi = warp; pi < kTileQ * kTileQ; pi += kVixWarps) {
+        const int r = ty0 + pi / kTileQ, c = tx0 + pi % kTileQ;
         if (r >= a.row_end || c >= ncols) continue;
         const uint64_t base = mix_seed(a.seed, (uint64_t)r, (uint64_t)c);
         const int E = zld(z + (int64_t)r * ncols + c) + a.ht;
@@ -579,6 +580,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     a.span = make_fastmod((uint64_t)(2 * p.roi + 1));
     a.tiles_x = (int)((c->ncols + kTile - 1) / kTile);
     a.tiles_y = (int)((c->band_r1 - c->band_r0 + kTile - 1) / kTile);
+    const int tq = kTileQ;   // the quad path's tiles (see path 1 below)
     a.hp = (int)(((c->z_rows + 31) & ~(int64_t)31) + 16);
     a.wp = (int)(((c->ncols + 31) & ~(int64_t)31) + 16);
     // traversal order (measured, profiles/README.md): strips of 16 tile columns
@@ -638,9 +640,16 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
             k_gcd_table<<<256, 256, 0, c->stream>>>(c->d_gcd);
             TXS_LAUNCHED(c, "vix");
         }
-        k_vix_quads<<<(unsigned)tiles, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols,
-                                                                       c->d_vix - c->band_r0 * c->ncols, a, c->d_gcd,
-                                                                       c->d_counters);
+        VixArgs aq = a;   // the quad path's own (smaller) tiles
+        aq.tiles_x = (int)((c->ncols + tq - 1) / tq);
+        aq.tiles_y = (int)((c->band_r1 - c->band_r0 + tq - 1) / tq);
+        aq.strip = p.roi >= 150 ? 16 : aq.tiles_x;
+        if (const char* e = getenv("TXS_VIX_STRIP")) aq.strip = std::max(1, std::min(aq.tiles_x, atoi(e)));
+        const int64_t tiles_q = (int64_t)aq.tiles_x * aq.tiles_y;
+        if (tiles_q > 0x7fffffff) return fail(c, TXS_ERR_RANGE, "vix", "grid too large");
+        k_vix_quads<<<(unsigned)tiles_q, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols,
+                                                                         c->d_vix - c->band_r0 * c->ncols, aq,
+                                                                         c->d_gcd, c->d_counters);
         st = TXS_OK;
     } else {
         if (ensure(c, "vix", (void**)&c->d_zt, &c->zt_cap, sizeof(int16_t) * c->z_rows * c->ncols) != TXS_OK)
