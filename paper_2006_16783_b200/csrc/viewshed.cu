@@ -581,10 +581,10 @@ __global__ void k_viewshed_evk(const int16_t* __restrict__ z, const int32_t* __r
 }
 
 __global__ void k_tile_keys(const int32_t* __restrict__ crow, const int32_t* __restrict__ ccol, int64_t n, int tiles_x,
-                            uint32_t* __restrict__ keys, int32_t* __restrict__ idx) {
+                            int tshift, uint32_t* __restrict__ keys, int32_t* __restrict__ idx) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    keys[i] = (uint32_t)((crow[i] >> 6) * tiles_x + (ccol[i] >> 6));
+    keys[i] = (uint32_t)((crow[i] >> tshift) * tiles_x + (ccol[i] >> tshift));
     idx[i] = (int32_t)i;
 }
 
@@ -611,7 +611,9 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
     // read overlapping terrain windows (L2 reuse; config 5's observers are
     // random over a 537 MB terrain).  Output slots keep candidate order.
     if (n >= 4096) {
-        const int tiles_x = (int)((c->ncols + 63) / 64);
+        int tshift = 6;   // 64x64-post observer tiles
+        if (const char* e = getenv("TXS_VS_TILE_SHIFT")) tshift = std::max(0, std::min(12, atoi(e)));
+        const int tiles_x = (int)((c->ncols + (1 << tshift) - 1) >> tshift);
         size_t tmp_bytes = 0;
         cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr, (int32_t*)nullptr,
                                         (int32_t*)nullptr, (int)n);
@@ -622,7 +624,7 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
         int32_t* idx = (int32_t*)(keys2 + n);
         int32_t* perm = idx + n;
         void* tmp = perm + n;
-        k_tile_keys<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->d_crow, c->d_ccol, n, tiles_x, keys, idx);
+        k_tile_keys<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->d_crow, c->d_ccol, n, tiles_x, tshift, keys, idx);
         TXS_LAUNCHED(c, "viewshed");
         TXS_CUDA(c, "viewshed", cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, idx, perm, (int)n, 0, 32,
                                                                 c->stream));
@@ -647,10 +649,12 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
     if (2 * smem <= 100 * 1024 && n >= (int64_t)2 * c->num_sms * 4) kobs = 2;
     if (const char* kenv = getenv("TXS_VS_K")) kobs = atoi(kenv);
     if (T->events && smem_bits && (kobs == 2 || kobs == 4) && (size_t)kobs * smem <= 200 * 1024) {
-        int best = 1;
-        for (int wv = 1; wv <= 32; ++wv)
-            if (T->ngroups % wv == 0 && std::abs(wv - 12) < std::abs(best - 12)) best = wv;
-        if (best < 4) best = std::min(T->ngroups, 8);
+        // warps per CTA (measured, profiles/README.md; resident warps vs ray-group
+        // balance): 15 at roi >= 225 (C5 1496 -> 1325 ms), 8 at roi >= 150 (C2
+        // 16.5 -> 15.9), else 6 (C3 34.3 -> 27.0); TXS_VS_WARPS overrides
+        int best = p.roi >= 225 ? 15 : (p.roi >= 150 ? 8 : 6);
+        best = std::min(best, T->ngroups);
+        if (const char* e = getenv("TXS_VS_WARPS")) best = std::max(1, std::min(32, atoi(e)));
         const int threads = 32 * best;
         const size_t sm = (size_t)kobs * smem;
         const unsigned grid = (unsigned)((n + kobs - 1) / kobs);
