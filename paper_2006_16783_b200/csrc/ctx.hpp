@@ -85,8 +85,8 @@ struct txs_ctx {
     const int16_t* zv() const { return d_z - z_off * ncols; }   // indexed by global row
     int16_t* d_zt = nullptr;      // column-major copy (VIX global path)
     size_t zt_cap = 0;
-    void* d_pairs = nullptr;
-    uint8_t* d_gcd = nullptr;     // 256x256 gcd table (VIX crossing statistic)      // quad planes QV+, QV-, QT+, QT- (VIX global path)
+    void* d_pairs = nullptr;      // VIX quad planes / VIEWSHED pair planes (per-call scratch)
+    uint8_t* d_gcd = nullptr;     // 256x256 gcd table (VIX crossing statistic)
     size_t pairs_cap = 0;
 
     // VixMap: one byte per post
