@@ -176,6 +176,10 @@ __global__ void k_commit(SiteArgs a, SiteState* st, const uint64_t* __restrict__
 #endif
 constexpr int kUpdThreads = SITE_UPD_THREADS;
 constexpr int kUpdPerSm = 32;   // k_update CTAs per SM
+#ifndef SITE_UPD_U
+#define SITE_UPD_U 4
+#endif
+constexpr int kUpdU = SITE_UPD_U;   // delta words in flight per row in the neighbour updates
 
 // One CTA per neighbour f in [first, total) step `stride`: the CTA's threads
 // take the overlap rows (short per-thread dependency chains — this loop is
@@ -208,11 +212,19 @@ __device__ __forceinline__ unsigned long long update_body(const SiteArgs& a, int
             const int2 sp = dspan[y - wr0];
             const int lo = max(sp.x, blo), hi = min(sp.y, bhi);
             const uint64_t* vr = v + (int64_t)(y - win.x) * nwr_i + shift_i;
-            for (int b = lo; b <= hi; ++b) {
-                const uint64_t d = dwin[(int64_t)(y - wr0) * a.dpitch + b];
-                if (!d) continue;
-                acc += __popcll(vr[b] & d);   // both zero outside their windows: the AND is the overlap
-                ++touched;
+            const uint64_t* dr = dwin + (int64_t)(y - wr0) * a.dpitch;
+            // kUpdU delta words in flight, then the viewshed words under the non-zero
+            // ones (two dependent latencies per kUpdU words instead of per word)
+            for (int b0 = lo; b0 <= hi; b0 += kUpdU) {
+                uint64_t d[kUpdU];
+#pragma unroll
+                for (int u = 0; u < kUpdU; ++u) d[u] = b0 + u <= hi ? dr[b0 + u] : 0ull;
+#pragma unroll
+                for (int u = 0; u < kUpdU; ++u)
+                    if (d[u]) {
+                        acc += __popcll(vr[b0 + u] & d[u]);   // both zero outside their windows: the AND is the overlap
+                        ++touched;
+                    }
             }
         }
         for (int o = 16; o; o >>= 1) {
