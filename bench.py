@@ -308,12 +308,17 @@ def run_b200(args, cfg):
     assert np.array_equal(r1["index"], res["index"][:len(r1["index"])]), "full-rescan SITE diverged from incremental"
     # rounds-only device time (the gain pass + argmax + commit of each round;
     # bucket/gain initialisation excluded -- it is in stages.site's ms)
+    # kernel-level: the gain pass alone (CUDA events around back-to-back passes
+    # against the final cum), the SURVEY §8(d) SITE roofline figure
+    gp_ms, gp_bytes = eng.time_gain_pass(8)
     rms = st1["ms_site_rounds"]
     site_stream = {"ms": round(rms, 3), "ms_with_setup": round(st1["ms_site"], 3),
                    "iterations": int(st1["site_iterations"]), "bytes": int(st1["site_bytes"]),
                    "gbs": round(st1["site_bytes"] / (rms / 1e3) / 1e9, 1) if rms else None,
                    "kernel": "k_gain_tiled" if cfg.random_observers else "k_gain_full",
-                   "mode": "full-rescan (same picks as incremental)"}
+                   "mode": "full-rescan (same picks as incremental)",
+                   "kernel_ms_per_pass": round(gp_ms, 4), "kernel_bytes_per_pass": int(gp_bytes),
+                   "kernel_gbs": round(gp_bytes / (gp_ms / 1e3) / 1e9, 1) if gp_ms else None}
 
     # ---- e2e through the public API from pinned host memory ---------------
     nw = (cfg.posts + 63) // 64
@@ -350,6 +355,7 @@ def run_b200(args, cfg):
     K = args.steps
     stages, roofline, peak = stage_figures(st, K, cfg, args.site_mode)
     site_stream["frac_of_hbm"] = round(site_stream["gbs"] / peak, 4) if site_stream["gbs"] else None
+    site_stream["kernel_frac_of_hbm"] = round(site_stream["kernel_gbs"] / peak, 4) if site_stream["kernel_gbs"] else None
     stages["site_stream"] = site_stream
     line = {
         "metric": METRIC, "value": round(ms / 1e3, 5), "unit": "s", "n_gpus": world, "steps": K,

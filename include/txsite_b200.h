@@ -155,6 +155,12 @@ txs_status txs_site(txs_ctx* ctx, const txs_params* p, txs_step* steps, int64_t 
 txs_status txs_get_cumulative(txs_ctx* ctx, uint64_t* words_out);
 /* marginal_gain of every resident viewshed against a caller cum (dense). */
 txs_status txs_marginal_gains(txs_ctx* ctx, const uint64_t* cum_dense, int64_t* gains_out);
+/* Measurement: `reps` full gain passes (popc(v_i & ~cum) for every candidate, the
+ * full-rescan SITE kernel) against the context's current cumulative bitmap (after
+ * txs_site), timed with CUDA events on the context stream; the incremental gains
+ * are overwritten.  ms_per_pass = mean device time of one pass, bytes_per_pass =
+ * packed viewshed bytes streamed (SPEC layout, algorithmic). */
+txs_status txs_time_gain_pass(txs_ctx* ctx, int32_t reps, double* ms_per_pass, int64_t* bytes_per_pass);
 
 /* ---- cli module (SPEC.md:433 run_pipeline) ---------------------------------- */
 /* vix -> findmax -> viewshed -> site on the resident terrain, device-resident

@@ -278,6 +278,12 @@ class Engine:
     def stream(self):
         return N.lib.txs_stream(self._h)
 
+    def time_gain_pass(self, reps=5):
+        """(ms per full gain pass, packed bytes per pass) against the current cum (after site())."""
+        ms, b = C.c_double(), C.c_int64()
+        self._chk(N.lib.txs_time_gain_pass(self._h, reps, C.byref(ms), C.byref(b)))
+        return ms.value, b.value
+
     def stats(self):
         s = N.Stats()
         self._chk(N.lib.txs_get_stats(self._h, C.byref(s)))

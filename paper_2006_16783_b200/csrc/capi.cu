@@ -618,6 +618,13 @@ txs_status txs_get_cumulative(txs_ctx* c, uint64_t* out) {
     return download_cum(c, out);
 }
 
+txs_status txs_time_gain_pass(txs_ctx* c, int32_t reps, double* ms, int64_t* bytes) {
+    if (!c || !ms || !bytes || reps < 1) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->site_valid || !c->vs_valid) return fail(c, TXS_ERR_STATE, "site", "run txs_site first");
+    cudaSetDevice(c->device);
+    return time_gain_pass(c, reps, ms, bytes);
+}
+
 txs_status txs_marginal_gains(txs_ctx* c, const uint64_t* cum_dense, int64_t* gains_out) {
     if (!c || !cum_dense || !gains_out) return TXS_ERR_INVALID_ARGUMENT;
     if (!c->vs_valid) return fail(c, TXS_ERR_STATE, "site", "no viewsheds");

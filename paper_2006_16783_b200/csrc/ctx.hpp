@@ -189,6 +189,7 @@ txs_status launch_random_observers(txs_ctx*, int64_t n, uint64_t seed);
 txs_status launch_viewsheds(txs_ctx*, const txs_params& p);
 txs_status run_site(txs_ctx*, const txs_params& p, std::vector<txs_step>& steps, int32_t* stop);
 txs_status launch_marginal_gains(txs_ctx*, const uint64_t* d_cum_dense, int64_t* d_gains);
+txs_status time_gain_pass(txs_ctx*, int32_t reps, double* ms, int64_t* bytes);
 txs_status download_cum(txs_ctx*, uint64_t* host_dense);
 txs_status shard_site_begin(txs_ctx*, const txs_params& p);
 // layout conversion for candidates [first, first+count): aligned (resident) <-> dense (SPEC)

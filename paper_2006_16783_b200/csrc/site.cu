@@ -824,6 +824,30 @@ txs_status launch_marginal_gains(txs_ctx* c, const uint64_t* d_cum_dense, int64_
     return TXS_OK;
 }
 
+txs_status time_gain_pass(txs_ctx* c, int32_t reps, double* ms, int64_t* bytes) {
+    txs_params p{};
+    p.target_coverage = 1.0;
+    const SiteArgs a = make_args(c, p);
+    uint64_t* cumv = c->d_cum - c->cum_r0 * c->wpr;
+    TXS_CUDA(c, "site", cudaMemsetAsync(c->d_counters + kSiteBytes, 0, sizeof(unsigned long long), c->stream));
+    launch_gain_pass<int32_t>(c, a, nullptr, cumv, c->d_gain, c->d_counters, true);   // warm-up (+ byte count)
+    TXS_LAUNCHED(c, "site");
+    unsigned long long b = 0;
+    TXS_CUDA(c, "site", cudaMemcpyAsync(&b, c->d_counters + kSiteBytes, sizeof(b), cudaMemcpyDeviceToHost, c->stream));
+    cudaEventRecord(c->ev_r0, c->stream);
+    for (int k = 0; k < reps; ++k) {
+        launch_gain_pass<int32_t>(c, a, nullptr, cumv, c->d_gain, nullptr, true);
+        TXS_LAUNCHED(c, "site");
+    }
+    cudaEventRecord(c->ev_r1, c->stream);
+    TXS_CUDA(c, "site", cudaEventSynchronize(c->ev_r1));
+    float t = 0.f;
+    cudaEventElapsedTime(&t, c->ev_r0, c->ev_r1);
+    *ms = reps > 0 ? (double)t / reps : 0.0;
+    *bytes = (int64_t)b;
+    return TXS_OK;
+}
+
 txs_status download_cum(txs_ctx* c, uint64_t* host_dense) {
     const int64_t nw = (c->nrows * c->ncols + 63) / 64;
     uint64_t* dense = nullptr;

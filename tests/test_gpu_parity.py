@@ -468,3 +468,23 @@ def test_sharded_bench_torchrun_world1():
     assert r1.returncode == 0, r1.stderr[-3000:]
     d1 = json.loads(r1.stdout.strip().splitlines()[-1])
     assert d["config"]["sited"] == d1["config"]["sited"] and d["config"]["stop"] == d1["config"]["stop"]
+
+
+def test_time_gain_pass_counts_packed_bytes(engine):
+    """txs_time_gain_pass: the timed full gain pass streams exactly the packed
+    (SPEC-layout) bytes of every candidate window, and leaves exact gains."""
+    T = _T()
+    z = O.generate_fractal(300, 300, 0.6, 19, 0, 2000)
+    rng = np.random.default_rng(4)
+    rows, cols = rng.integers(0, 300, 500).astype(np.int32), rng.integers(0, 300, 500).astype(np.int32)
+    engine.set_terrain(z)
+    engine.set_candidates(rows, cols)
+    engine.compute_all_viewsheds(T.make_params(30, 10, 10))
+    wins, words, _ = engine.viewsheds(30)
+    engine.site(T.make_params(30, target=0.5, max_selected=5))
+    ms, nbytes = engine.time_gain_pass(3)
+    assert ms > 0
+    assert nbytes == int(sum(8 * ((int(h) * int(w) + 63) // 64) for _, _, h, w in wins))
+    cum = engine.cumulative()
+    exp = [O.marginal_gain(wins[i], words[i], cum, 300, 300) for i in range(len(rows))]
+    assert np.array_equal(engine.marginal_gains(cum), np.array(exp))
