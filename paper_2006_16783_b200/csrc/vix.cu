@@ -245,6 +245,7 @@ struct VixArgs {
     int strip;           // tile columns per traversal strip (quad path)
     int row0, row_end;   // band rows [row0, row_end)
     int zr0, zr1;        // held terrain rows [zr0, zr1)
+    int pv, pt, st_off;  // skip map: SV row pitch, ST column pitch, ST offset (int16 entries)
 };
 
 template <bool SMEM, int ILP>
@@ -404,17 +405,23 @@ __device__ __forceinline__ int dp2hi(uint32_t pair, uint32_t w) {
 }
 
 // Per-sample walk geometry, computed by the lane that owns the sample and kept
-// in shared memory (two 16-byte broadcast loads per sample; the registers of
-// the walk stay free for occupancy).
-struct __align__(16) QuadGeom {
+// in shared memory as two 16-byte records: the skip test reads only the first,
+// the exact walk both (the registers of the walk stay free for occupancy).
+// Divisions by M are exact fixed-point multiplies: with mag = ceil(2^16 m / M),
+// floor(x m / M) = (x mag) >> 16 for every 0 <= x <= 255 (the error x(mag -
+// 2^16 m/M)/2^16 < 255/2^16 < 1/M cannot carry past the next integer).
+struct __align__(16) QuadGeomC {   // skip test
+    int soff;         // skip-map entry of the start post's block (padded block indices)
+    int LE;           // Es * M
+    int D;            // LOS rise start -> end
+    int w;            // M | tr << 8 | mneg << 9 | ys3 << 10 | mag << 12   (M = 0: nothing to walk)
+};
+struct __align__(16) QuadGeomF {   // exact walk
     const uint2* Q;   // start post's entry in its plane
     int Es;           // LOS height at the start post (E, or Zt when reversed)
-    int D;            // LOS rise start -> end
-    int nMm;          // M | m << 16 (0: nothing to walk)
-    int sm;           // minor step in plane words
-    int qr32;         // q32 | r32 << 16: advance of (q, r) over 32 major steps
-    float rcp;        // 1/M
+    int msm;          // m | sm << 8 (sm = minor step in plane words, 0 for axis-aligned segments)
 };
+struct QuadGeom { QuadGeomC c; QuadGeomF f; };
 
 #ifndef VIX_MINB
 #define VIX_MINB 4    // CTAs per SM: 64 warps hide the L2 latency of the plane loads
@@ -425,44 +432,111 @@ __device__ __forceinline__ bool quad_test(uint2 v, int r, int nm, uint32_t wb, i
     return (dp2lo(v.x, W) > rhsM) | (((unsigned)(r - 1) < (unsigned)(nm - 1)) & (dp2hi(v.y, W) > rhsm));
 }
 
-// One segment per warp, lane l taking major steps l+1, l+33, ...; a vote after
-// every 32 steps.  Returns true (uniform) iff the segment is blocked.
-__device__ __forceinline__ bool quad_walk(const QuadGeom& g, int lane) {
-    const int nM = g.nMm & 0xffff, nm = g.nMm >> 16, steps = nM - 1;
+// Plane geometry shared by every walk of a launch.
+struct QuadPitch {
+    int pv, pt;       // skip map: SV row pitch, ST column pitch (int16)
+};
+
+// Full walk: one segment per warp, lane l taking major steps l+1, l+33, ...;
+// a vote after every 32 steps.  Returns true (uniform) iff the segment is
+// blocked.  (TXS_VIX_SKIP=0: every step of every segment is evaluated.)
+__device__ __forceinline__ bool quad_walk(const QuadGeom* gp, int lane) {
+    const QuadGeomC c = gp->c;
+    const int nM = c.w & 0xff, steps = nM - 1;
     if (steps <= 0) return false;
-    const uint2* Q = g.Q;
-    const int sm = g.sm, D = g.D;
-    const int q32 = g.qr32 & 0xffff, r32 = g.qr32 >> 16;
+    const QuadGeomF f = gp->f;
+    const int nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 12, D = c.D;
     const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
+    const int q32 = (32 * mag) >> 16, r32 = 32 * nm - q32 * nM;
     int i = 1 + lane;
-    const int num = i * nm;
-    int q = __float2int_rz(__int2float_rn(num) * g.rcp), r = num - q * nM;
-    if (r >= nM) { ++q; r -= nM; }
-    if (r < 0) { --q; r += nM; }
+    int q = (i * mag) >> 16, r = i * nm - q * nM;
     int off = i + q * sm;
-    int rhsM = g.Es * nM + i * D, rhsm = g.Es * nm + q * D;
+    int rhsM = c.LE + i * D, rhsm = f.Es * nm + q * D;
     const int dOff = 32 + q32 * sm, dRhsM = 32 * D, dRhsm = q32 * D;
     for (int k = steps >> 5; k; --k) {
-        if (__any_sync(kFull, quad_test(qld(Q + off), r, nm, wb, rhsM, rhsm))) return true;
+        if (__any_sync(kFull, quad_test(qld(f.Q + off), r, nm, wb, rhsM, rhsm))) return true;
         off += dOff; rhsM += dRhsM; rhsm += dRhsm; r += r32;
         if (r >= nM) { r -= nM; off += sm; rhsm += D; }
     }
     if (steps & 31) {
         const bool valid = (steps & ~31) + 1 + lane <= steps;
-        return __any_sync(kFull, valid && quad_test(qld(Q + (valid ? off : 0)), r, nm, wb, rhsM, rhsm));
+        return __any_sync(kFull, valid && quad_test(qld(f.Q + (valid ? off : 0)), r, nm, wb, rhsM, rhsm));
     }
     return false;
 }
 
+// Hierarchical walk with a conservative skip test (exact: it only ever skips
+// steps that cannot block).  Steps are taken in groups of 4: group g holds
+// major steps 4g+1..4g+4, whose crossings lie at t in (4g/M, (4g+4)/M] and use
+// posts with major offsets 4g..4g+4 and minor offsets q(4g+1)..q(4g+1)+4 -- a
+// 5x5 window, so inside the 8x8 posts of two-by-two 4x4 blocks at the window's
+// corner block.  The skip map holds, per block corner, the maximum elevation of
+// those 8x8 posts (k_skipmap).  The interpolated terrain at any crossing of the
+// group is at most that maximum, and the LOS over the group is at least its
+// value at one end, so
+//     smax * M  <=  Es*M + min(4g*D, min(4g+4, M-1)*D)
+// proves that no crossing of the group is blocked.  Lane l tests group 32k+l
+// from the (L1-resident) skip map; only groups that fail the test are walked
+// exactly, 8 groups x 4 steps per warp pass, with the predicates of quad_test.
+__device__ __forceinline__ bool quad_walk_skip(const QuadGeom* gp, const QuadPitch& P, const int16_t* __restrict__ smap,
+                                               int* s_fail, int lane) {
+    const QuadGeomC c = gp->c;
+    const int nM = c.w & 0xff, steps = nM - 1;
+    if (steps <= 0) return false;
+    const int mag = (unsigned)c.w >> 12, D = c.D;
+    // minor block of group g's window corner: (c0 + sgn*q(4g+1)) >> 2
+    const bool mneg = c.w & 0x200;
+    const int ys3 = (c.w >> 10) & 3;
+    const int c0 = mneg ? ys3 - 4 : ys3, sgn = mneg ? -1 : 1;
+    const int sp = (c.w & 0x100) ? P.pt : P.pv;
+    const int ngroups = (steps + 3) >> 2;
+    const int16_t* S = smap + c.soff;
+    for (int g0 = 0; g0 < ngroups; g0 += 32) {
+        const int gi = g0 + lane;
+        bool fail = false;
+        if (gi < ngroups) {
+            const int q1 = ((4 * gi + 1) * mag) >> 16;
+            const int smax = __ldg(S + gi + ((c0 + sgn * q1) >> 2) * sp);
+            fail = smax * nM > c.LE + min(4 * gi * D, min(4 * gi + 4, steps) * D);
+        }
+        const unsigned F = __ballot_sync(kFull, fail);
+        if (!F) continue;
+        if (fail) s_fail[__popc(F & ((1u << lane) - 1))] = gi;
+        __syncwarp();
+        const QuadGeomF f = gp->f;
+        const int nm = f.msm & 0xff, sm = f.msm >> 8;
+        const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
+        const int cnt = __popc(F);
+        for (int j = 0; j < cnt; j += 8) {
+            const int sub = j + (lane >> 2);
+            bool b = false;
+            if (sub < cnt) {
+                const int i = 4 * s_fail[sub] + 1 + (lane & 3);
+                if (i <= steps) {
+                    const int q = (i * mag) >> 16, r = i * nm - q * nM;
+                    b = quad_test(qld(f.Q + i + q * sm), r, nm, wb, c.LE + i * D, f.Es * nm + q * D);
+                }
+            }
+            if (__any_sync(kFull, b)) return true;
+        }
+        __syncwarp();
+    }
+    return false;
+}
+
+template <bool SKIP>
 __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16_t* __restrict__ z,
                                                                    const uint2* __restrict__ qp, int nrows, int ncols,
                                                                    uint8_t* __restrict__ out, VixArgs a,
                                                                    const uint8_t* __restrict__ gcdt,
+                                                                   const int16_t* __restrict__ smap,
                                                                    unsigned long long* __restrict__ counters) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
-    // dynamic smem: [geometry: kVixWarps x 32][samples: kVixWarps x S ints]
+    // dynamic smem: [geometry: kVixWarps x 32][failed groups: kVixWarps x 32][samples: kVixWarps x S ints]
     QuadGeom* s_geo = (QuadGeom*)s_dyn + warp_of_thread() * 32;
-    int* s_samp = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + warp_of_thread() * a.S;
+    int* s_fail = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + warp_of_thread() * 32;
+    int* s_samp = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + kVixWarps * 32 + warp_of_thread() * a.S;
+    const QuadPitch PQ{a.pv, a.pt};
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // tiles in vertical strips of a.strip tile columns, row-major inside a strip
     int ty, tx;
@@ -515,22 +589,25 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
                 const bool mneg = (tr ? dc : dr) < 0;
                 const int64_t n = (int64_t)H * a.wp, nT = (int64_t)ncols * a.hp;
                 QuadGeom g;
-                g.Q = qp + (tr ? 2 * n + (int64_t)x * a.hp + y + (mneg ? nT : 0) : (int64_t)y * a.wp + x + (mneg ? n : 0));
-                g.Es = rev ? Zt : E;
-                g.D = rev ? E - Zt : Zt - E;
-                g.nMm = nM | (nm << 16);
                 const int stride = tr ? a.hp : a.wp;
-                g.sm = mneg ? -stride : stride;
-                g.rcp = nM ? __fdividef(1.0f, (float)nM) : 0.f;
-                const int num = 32 * nm;
-                int q = __float2int_rz(__int2float_rn(num) * g.rcp), rr = num - q * nM;
-                if (rr >= nM) { ++q; rr -= nM; }
-                if (rr < 0) { --q; rr += nM; }
-                g.qr32 = q | (rr << 16);
+                const int Es = rev ? Zt : E;
+                g.f.Q = qp + (tr ? 2 * n + (int64_t)x * a.hp + y + (mneg ? nT : 0) : (int64_t)y * a.wp + x + (mneg ? n : 0));
+                g.f.Es = Es;
+                g.f.msm = nm | ((nm == 0 ? 0 : (mneg ? -stride : stride)) * 256);
+                // skip map (k_skipmap): padded 4x4-block indices of the start post,
+                // SV row-major for column-major walks, ST column-major for row-major ones
+                const int maj = tr ? y : x, mnr = tr ? x : y;
+                const int mag = nM ? (nm * 65536 + nM - 1) / nM : 0;
+                g.c.soff = tr ? a.st_off + ((maj >> 2) + 1) + ((mnr >> 2) + 1) * a.pt
+                              : ((maj >> 2) + 1) + ((mnr >> 2) + 1) * a.pv;
+                g.c.LE = Es * nM;
+                g.c.D = rev ? E - Zt : Zt - E;
+                g.c.w = nM | ((int)tr << 8) | ((int)mneg << 9) | ((mnr & 3) << 10) | (mag << 12);
                 s_geo[lane] = g;
             }
             __syncwarp();
-            for (int sidx = 0; sidx < ns; ++sidx) vis += quad_walk(s_geo[sidx], lane) ? 0 : 1;
+            for (int sidx = 0; sidx < ns; ++sidx)
+                vis += (SKIP ? quad_walk_skip(s_geo + sidx, PQ, smap, s_fail, lane) : quad_walk(s_geo + sidx, lane)) ? 0 : 1;
             __syncwarp();
         }
         if (lane == 0) out[(int64_t)r * ncols + c] = (uint8_t)vis;
@@ -541,6 +618,36 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
         atomicAdd(counters + kVixLos, (unsigned long long)n_posts * a.S);
         atomicAdd(counters + kVixCrossFull, n_cross);
     }
+}
+
+// Skip map of quad_walk_skip.  Pass 1: per 4x4 block the maximum elevation,
+// stored with one block of padding on every side (padded index = block + 1;
+// padding blocks hold no posts: -32768).  Pass 2: per padded block corner
+// (pr, pc) the maximum of blocks pr..pr+1 x pc..pc+1 -- the 8x8 posts from
+// post (4(pr-1), 4(pc-1)) -- written row-major (SV) and column-major (ST) so
+// that lanes stepping along a walk's major axis read consecutive entries.
+__global__ void k_blockmax(const int16_t* __restrict__ z, int H, int W, int16_t* __restrict__ bp, int Hb, int Wb) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)(Hb + 2) * (Wb + 2)) return;
+    const int pr = (int)(idx / (Wb + 2)), pc = (int)(idx - (int64_t)pr * (Wb + 2));
+    const int br = pr - 1, bc = pc - 1;
+    int m = -32768;
+    if (br >= 0 && br < Hb && bc >= 0 && bc < Wb) {
+        for (int y = 4 * br; y < min(4 * br + 4, H); ++y)
+            for (int x = 4 * bc; x < min(4 * bc + 4, W); ++x) m = max(m, (int)z[(int64_t)y * W + x]);
+    }
+    bp[idx] = (int16_t)m;
+}
+
+__global__ void k_skipmap(const int16_t* __restrict__ bp, int Hb, int Wb, int16_t* __restrict__ sv, int pv,
+                          int16_t* __restrict__ st, int pt) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)(Hb + 1) * (Wb + 1)) return;
+    const int pr = (int)(idx / (Wb + 1)), pc = (int)(idx - (int64_t)pr * (Wb + 1));
+    const int16_t* b = bp + (int64_t)pr * (Wb + 2) + pc;
+    const int16_t m = max(max(b[0], b[1]), max(b[Wb + 2], b[Wb + 3]));
+    sv[(int64_t)pr * pv + pc] = m;
+    st[(int64_t)pc * pt + pr] = m;
 }
 
 // column-major copy of the terrain: zt[c*nrows + r] = z[r*ncols + c]
@@ -622,19 +729,40 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         st = go(k_vix<true, 1>, smem);
     } else if (path == 1) {
         const int64_t n = c->z_rows * c->ncols, nq = 2 * c->z_rows * (int64_t)a.wp + 2 * c->ncols * (int64_t)a.hp;
+        // skip map (k_skipmap) behind the quad planes: SV, ST, then the block maxima
+        const int Hb = (int)((c->z_rows + 3) / 4), Wb = (int)((c->ncols + 3) / 4);
+        a.pv = ((Wb + 1) + 7) & ~7;
+        a.pt = ((Hb + 1) + 7) & ~7;
+        const int64_t nsv = (int64_t)(Hb + 1) * a.pv, nst = (int64_t)(Wb + 1) * a.pt;
+        const int64_t nbp = (int64_t)(Hb + 2) * (Wb + 2);
+        if (nsv + nst > 0x7fffffff) return fail(c, TXS_ERR_RANGE, "vix", "grid too large");
+        a.st_off = (int)nsv;
+        bool skip = true;
+        if (const char* e = getenv("TXS_VIX_SKIP")) skip = atoi(e) != 0;
+        const size_t map_bytes = skip ? sizeof(int16_t) * (size_t)(nsv + nst + nbp) : 0;
         // rebuilt on every call (part of the timed stage; ~1 HBM pass of 34 B/post)
-        if (ensure(c, "vix", (void**)&c->d_pairs, &c->pairs_cap, sizeof(uint2) * nq) != TXS_OK)
+        if (ensure(c, "vix", (void**)&c->d_pairs, &c->pairs_cap, sizeof(uint2) * nq + map_bytes) != TXS_OK)
             return TXS_ERR_OUT_OF_MEMORY;
         {
             dim3 tb(32, 8), tg((unsigned)((c->ncols + 31) / 32), (unsigned)((c->z_rows + 31) / 32));
             k_quads<<<tg, tb, 0, c->stream>>>(c->d_z, (uint2*)c->d_pairs, (int)c->z_rows, a.hp, a.wp, (int)c->ncols);
             TXS_LAUNCHED(c, "vix");
         }
+        int16_t* smap = skip ? (int16_t*)((uint2*)c->d_pairs + nq) : nullptr;
+        if (skip) {
+            int16_t* bp = smap + nsv + nst;
+            k_blockmax<<<(unsigned)((nbp + 255) / 256), 256, 0, c->stream>>>(c->d_z, (int)c->z_rows, (int)c->ncols, bp, Hb, Wb);
+            TXS_LAUNCHED(c, "vix");
+            const int64_t ns = (int64_t)(Hb + 1) * (Wb + 1);
+            k_skipmap<<<(unsigned)((ns + 255) / 256), 256, 0, c->stream>>>(bp, Hb, Wb, smap, a.pv, smap + nsv, a.pt);
+            TXS_LAUNCHED(c, "vix");
+        }
         const uint2* qp = (const uint2*)c->d_pairs;
         set_zbounds(c->d_z, c->d_z + n, c->stream, (const int16_t*)qp, (const int16_t*)(qp + nq));
-        const size_t qsm = samp + sizeof(QuadGeom) * kVixWarps * 32;
+        const size_t qsm = samp + (sizeof(QuadGeom) + sizeof(int)) * kVixWarps * 32;
+        auto kq = skip ? k_vix_quads<true> : k_vix_quads<false>;
         if (qsm > 48 * 1024)
-            TXS_CUDA(c, "vix", cudaFuncSetAttribute(k_vix_quads, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm));
+            TXS_CUDA(c, "vix", cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm));
         if (!c->d_gcd) {
             TXS_CUDA(c, "vix", cudaMalloc((void**)&c->d_gcd, 256 * 256));
             k_gcd_table<<<256, 256, 0, c->stream>>>(c->d_gcd);
@@ -647,9 +775,9 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         if (const char* e = getenv("TXS_VIX_STRIP")) aq.strip = std::max(1, std::min(aq.tiles_x, atoi(e)));
         const int64_t tiles_q = (int64_t)aq.tiles_x * aq.tiles_y;
         if (tiles_q > 0x7fffffff) return fail(c, TXS_ERR_RANGE, "vix", "grid too large");
-        k_vix_quads<<<(unsigned)tiles_q, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols,
-                                                                         c->d_vix - c->band_r0 * c->ncols, aq,
-                                                                         c->d_gcd, c->d_counters);
+        kq<<<(unsigned)tiles_q, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols,
+                                                                c->d_vix - c->band_r0 * c->ncols, aq, c->d_gcd, smap,
+                                                                c->d_counters);
         st = TXS_OK;
     } else {
         if (ensure(c, "vix", (void**)&c->d_zt, &c->zt_cap, sizeof(int16_t) * c->z_rows * c->ncols) != TXS_OK)

@@ -112,6 +112,32 @@ def test_vix_paths_bit_exact(engine, monkeypatch, path, roi, samples, ht, hr):
         assert np.array_equal(g[rb:re], o[rb:re]), (path, rb, int((g[rb:re] != o[rb:re]).sum()))
 
 
+@pytest.mark.parametrize("nr,nc,rough,zmin,zmax,roi,samples,ht,hr", [
+    (700, 610, 0.7, -500, 3000, 60, 24, 15, 5),      # rough, negative elevations
+    (513, 777, 0.5, 0, 4000, 100, 10, 10, 10),       # smooth (most groups skipped)
+    (400, 401, 0.9, -32000, 32000, 255, 9, 0, 0),    # near-full int16 range, roi 255
+    (300, 300, 0.3, 0, 50, 200, 20, 1, 1),           # low relief, grazing LOS
+    (37, 1000, 0.6, 0, 3000, 150, 16, 20, 20),       # thin grid: windows off both edges
+])
+def test_vix_skip_map_matches_full_walk(engine, monkeypatch, nr, nc, rough, zmin, zmax, roi, samples, ht, hr):
+    """The quad path's conservative skip test (TXS_VIX_SKIP, default on) gives
+    the full walk's VixMap bit for bit over the whole grid, and the oracle's on
+    edge rows."""
+    T = _T()
+    z = O.generate_fractal(nr, nc, rough, 5, zmin, zmax)
+    engine.set_terrain(z)
+    p = T.make_params(roi, ht, hr, samples=samples, seed=9)
+    monkeypatch.setenv("TXS_VIX_PATH", "pairs")
+    monkeypatch.setenv("TXS_VIX_SKIP", "0")
+    full = engine.estimate_vix(p)
+    monkeypatch.setenv("TXS_VIX_SKIP", "1")
+    skip = engine.estimate_vix(p)
+    assert np.array_equal(full, skip), int((full != skip).sum())
+    for rb, re in [(0, 3), (nr - 3, nr)]:
+        o = O.estimate_vix(z, roi, ht, hr, samples, 9, rows=(rb, re))
+        assert np.array_equal(skip[rb:re], o[rb:re]), rb
+
+
 def test_vix_flat_and_tiny(engine):
     T = _T()
     engine.set_terrain(np.full((70, 45), 3, np.int16))
