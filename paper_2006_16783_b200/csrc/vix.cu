@@ -475,9 +475,10 @@ __device__ __forceinline__ bool quad_walk(const QuadGeom* gp, int lane) {
 // group is at most that maximum, and the LOS over the group is at least its
 // value at one end, so
 //     smax * M  <=  Es*M + min(4g*D, min(4g+4, M-1)*D)
-// proves that no crossing of the group is blocked.  Lane l tests group 32k+l
-// from the (L1-resident) skip map; only groups that fail the test are walked
-// exactly, 8 groups x 4 steps per warp pass, with the predicates of quad_test.
+// proves that no crossing of the group is blocked.
+//
+// Sequential form (TXS_VIX_SKIP=2): one segment per warp pass, lane l testing
+// group 32k+l, failing groups walked in order with an exit at the first block.
 __device__ __forceinline__ bool quad_walk_skip(const QuadGeom* gp, const QuadPitch& P, const int16_t* __restrict__ smap,
                                                int* s_fail, int lane) {
     const QuadGeomC c = gp->c;
@@ -524,7 +525,83 @@ __device__ __forceinline__ bool quad_walk_skip(const QuadGeom* gp, const QuadPit
     return false;
 }
 
-template <bool SKIP>
+//
+// A batch of up to 32 segments (lane l built segment l's geometry g) is tested
+// as one flattened list of (segment, group) pairs, 32 per warp pass, so lanes
+// do not idle on short segments; the pairs that fail are walked exactly, 8
+// groups x 4 steps per pass, with the predicates of quad_test, skipping
+// segments already found blocked.  Returns the number of visible segments.
+__device__ __forceinline__ int batch_skip(const QuadGeom& g, int ns, int lane, QuadGeom* s_geo, int* s_pre,
+                                          int* s_fail, const int16_t* __restrict__ smap, const QuadPitch& P) {
+    const int nMl = g.c.w & 0xff;
+    const int ng = (lane < ns && nMl >= 2) ? (nMl + 2) >> 2 : 0;   // ceil((M-1)/4) groups
+    const unsigned nz = __ballot_sync(kFull, ng > 0);
+    int inc = ng;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += t;
+    }
+    const int T = __shfl_sync(kFull, inc, 31);
+    if (ng > 0) {   // compacted: segments with groups, in lane order; prefixes strictly increase
+        const int slot = __popc(nz & ((1u << lane) - 1));
+        s_geo[slot] = g;
+        s_pre[slot] = inc - ng;
+    }
+    __syncwarp();
+    const int myp = lane < __popc(nz) ? s_pre[lane] : 0x7fffffff;
+    unsigned blk = 0;   // blocked slots
+    for (int base = 0; base < T; base += 32) {
+        // slot of pair base+lane: (slots starting at or before base) - 1 + (starts in (base, base+lane])
+        const unsigned B = __reduce_or_sync(kFull, (myp > base && myp < base + 32) ? 1u << (myp - base) : 0u);
+        const int cb = __popc(__ballot_sync(kFull, myp <= base));
+        const int p = base + lane;
+        bool fail = false;
+        int ent = 0;
+        const int sl = cb - 1 + __popc(B & ((2u << lane) - 1));
+        if (p < T && !((blk >> sl) & 1u)) {   // pairs of segments already blocked are dropped
+            const int gi = p - s_pre[sl];
+            const QuadGeomC c = s_geo[sl].c;
+            const int nM = c.w & 0xff, steps = nM - 1, mag = (unsigned)c.w >> 12;
+            const bool mneg = c.w & 0x200;
+            const int ys3 = (c.w >> 10) & 3;
+            const int q1 = ((4 * gi + 1) * mag) >> 16;
+            const int mb = (mneg ? ys3 - 4 - q1 : ys3 + q1) >> 2;
+            const int smax = __ldg(smap + c.soff + gi + mb * ((c.w & 0x100) ? P.pt : P.pv));
+            fail = smax * nM > c.LE + min(4 * gi * c.D, min(4 * gi + 4, steps) * c.D);
+            ent = sl | (gi << 8);
+        }
+        const unsigned F = __ballot_sync(kFull, fail);
+        if (!F) continue;
+        if (fail) s_fail[__popc(F & ((1u << lane) - 1))] = ent;
+        __syncwarp();
+        const int cnt = __popc(F);
+        for (int j = 0; j < cnt; j += 8) {
+            const int sub = j + (lane >> 2);
+            bool b = false;
+            int sl = 0;
+            if (sub < cnt) {
+                const int e = s_fail[sub];
+                sl = e & 0xff;
+                const int i = 4 * (e >> 8) + 1 + (lane & 3);
+                const QuadGeomC c = s_geo[sl].c;
+                const int nM = c.w & 0xff;
+                if (i < nM && !((blk >> sl) & 1u)) {
+                    const QuadGeomF f = s_geo[sl].f;
+                    const int nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 12;
+                    const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
+                    const int q = (i * mag) >> 16, r = i * nm - q * nM;
+                    b = quad_test(qld(f.Q + i + q * sm), r, nm, wb, c.LE + i * c.D, f.Es * nm + q * c.D);
+                }
+            }
+            blk |= __reduce_or_sync(kFull, b ? 1u << sl : 0u);
+        }
+        __syncwarp();
+    }
+    return ns - __popc(blk);
+}
+
+template <int SKIP>
 __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16_t* __restrict__ z,
                                                                    const uint2* __restrict__ qp, int nrows, int ncols,
                                                                    uint8_t* __restrict__ out, VixArgs a,
@@ -532,10 +609,11 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
                                                                    const int16_t* __restrict__ smap,
                                                                    unsigned long long* __restrict__ counters) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
-    // dynamic smem: [geometry: kVixWarps x 32][failed groups: kVixWarps x 32][samples: kVixWarps x S ints]
+    // dynamic smem: [geometry: kVixWarps x 32][failed groups, group prefixes: 2 x kVixWarps x 32][samples: kVixWarps x S ints]
     QuadGeom* s_geo = (QuadGeom*)s_dyn + warp_of_thread() * 32;
     int* s_fail = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + warp_of_thread() * 32;
-    int* s_samp = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + kVixWarps * 32 + warp_of_thread() * a.S;
+    int* s_pre = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + kVixWarps * 32 + warp_of_thread() * 32;
+    int* s_samp = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + 2 * kVixWarps * 32 + warp_of_thread() * a.S;
     const QuadPitch PQ{a.pv, a.pt};
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // tiles in vertical strips of a.strip tile columns, row-major inside a strip
@@ -575,6 +653,7 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
         int vis = 0;
         for (int s0 = 0; s0 < a.S; s0 += 32) {
             const int ns = min(32, a.S - s0);
+            QuadGeom g{};
             if (lane < ns) {
                 const int H = a.zr1 - a.zr0;
                 const int pk = s_samp[s0 + lane];
@@ -588,7 +667,6 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
                 const int nM = tr ? dr : dc, nm = tr ? abs(dc) : abs(dr);
                 const bool mneg = (tr ? dc : dr) < 0;
                 const int64_t n = (int64_t)H * a.wp, nT = (int64_t)ncols * a.hp;
-                QuadGeom g;
                 const int stride = tr ? a.hp : a.wp;
                 const int Es = rev ? Zt : E;
                 g.f.Q = qp + (tr ? 2 * n + (int64_t)x * a.hp + y + (mneg ? nT : 0) : (int64_t)y * a.wp + x + (mneg ? n : 0));
@@ -603,11 +681,15 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
                 g.c.LE = Es * nM;
                 g.c.D = rev ? E - Zt : Zt - E;
                 g.c.w = nM | ((int)tr << 8) | ((int)mneg << 9) | ((mnr & 3) << 10) | (mag << 12);
-                s_geo[lane] = g;
             }
-            __syncwarp();
-            for (int sidx = 0; sidx < ns; ++sidx)
-                vis += (SKIP ? quad_walk_skip(s_geo + sidx, PQ, smap, s_fail, lane) : quad_walk(s_geo + sidx, lane)) ? 0 : 1;
+            if (SKIP == 1) {
+                vis += batch_skip(g, ns, lane, s_geo, s_pre, s_fail, smap, PQ);
+            } else {
+                s_geo[lane] = g;
+                __syncwarp();
+                for (int sidx = 0; sidx < ns; ++sidx)
+                    vis += (SKIP == 2 ? quad_walk_skip(s_geo + sidx, PQ, smap, s_fail, lane) : quad_walk(s_geo + sidx, lane)) ? 0 : 1;
+            }
             __syncwarp();
         }
         if (lane == 0) out[(int64_t)r * ncols + c] = (uint8_t)vis;
@@ -737,8 +819,12 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         const int64_t nbp = (int64_t)(Hb + 2) * (Wb + 2);
         if (nsv + nst > 0x7fffffff) return fail(c, TXS_ERR_RANGE, "vix", "grid too large");
         a.st_off = (int)nsv;
-        bool skip = true;
-        if (const char* e = getenv("TXS_VIX_SKIP")) skip = atoi(e) != 0;
+        // 1: flattened (segment, group) skip test, 2: per-segment skip test, 0: full walk.
+        // Measured (profiles/README.md): flattened at roi 100 (C3 425 -> 250 ms, C4
+        // 4280 -> 2018 vs 326 / 2614 per segment); per segment at roi 200, where
+        // blocked segments gain from the in-order early exit (C2 55.0 -> 50.1 vs 57.1)
+        int skip = p.roi >= 150 ? 2 : 1;
+        if (const char* e = getenv("TXS_VIX_SKIP")) skip = std::max(0, std::min(2, atoi(e)));
         const size_t map_bytes = skip ? sizeof(int16_t) * (size_t)(nsv + nst + nbp) : 0;
         // rebuilt on every call (part of the timed stage; ~1 HBM pass of 34 B/post)
         if (ensure(c, "vix", (void**)&c->d_pairs, &c->pairs_cap, sizeof(uint2) * nq + map_bytes) != TXS_OK)
@@ -759,8 +845,8 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         }
         const uint2* qp = (const uint2*)c->d_pairs;
         set_zbounds(c->d_z, c->d_z + n, c->stream, (const int16_t*)qp, (const int16_t*)(qp + nq));
-        const size_t qsm = samp + (sizeof(QuadGeom) + sizeof(int)) * kVixWarps * 32;
-        auto kq = skip ? k_vix_quads<true> : k_vix_quads<false>;
+        const size_t qsm = samp + (sizeof(QuadGeom) + 2 * sizeof(int)) * kVixWarps * 32;
+        auto kq = skip == 1 ? k_vix_quads<1> : skip == 2 ? k_vix_quads<2> : k_vix_quads<0>;
         if (qsm > 48 * 1024)
             TXS_CUDA(c, "vix", cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm));
         if (!c->d_gcd) {

@@ -1,4 +1,4 @@
-"""A/B of the VIX skip map (TXS_VIX_SKIP=0/1): device time of the VIX stage
+"""A/B of the VIX skip map (TXS_VIX_SKIP=0 full walk / 1 flattened / 2 per-segment): device time of the VIX stage
 (min of reps) and a bit-exact comparison of the two VixMaps, per config.
 python profiles/scripts/vix_skip.py c1,c2,c3 [reps]"""
 import os
@@ -17,7 +17,8 @@ for name in sys.argv[1].split(","):
     setup_terrain(e, cfg)
     p = params_for(cfg)
     res, maps = {}, {}
-    for skip in ("0", "1"):
+    modes = ("0", "1", "2")
+    for skip in modes:
         os.environ["TXS_VIX_SKIP"] = skip
         ts = []
         for k in range(reps + 1):
@@ -28,8 +29,8 @@ for name in sys.argv[1].split(","):
             e.synchronize()
             ts.append(e.stats()["ms_vix"])
         res[skip] = min(ts[1:])
-    same = bool(np.array_equal(maps["0"], maps["1"]))
-    print(f"{name}: full {res['0']:.2f} ms  skip {res['1']:.2f} ms  x{res['0'] / res['1']:.2f}  identical={same}",
-          flush=True)
+    same = all(np.array_equal(maps["0"], maps[m]) for m in modes)
+    print(f"{name}: full {res['0']:.2f} ms  flattened skip {res['1']:.2f} ms  per-segment skip {res['2']:.2f} ms  "
+          f"identical={same}", flush=True)
     assert same
     e.close()

@@ -130,9 +130,10 @@ def test_vix_skip_map_matches_full_walk(engine, monkeypatch, nr, nc, rough, zmin
     monkeypatch.setenv("TXS_VIX_PATH", "pairs")
     monkeypatch.setenv("TXS_VIX_SKIP", "0")
     full = engine.estimate_vix(p)
-    monkeypatch.setenv("TXS_VIX_SKIP", "1")
-    skip = engine.estimate_vix(p)
-    assert np.array_equal(full, skip), int((full != skip).sum())
+    for mode in ("2", "1"):   # per-segment, flattened (default)
+        monkeypatch.setenv("TXS_VIX_SKIP", mode)
+        skip = engine.estimate_vix(p)
+        assert np.array_equal(full, skip), (mode, int((full != skip).sum()))
     for rb, re in [(0, 3), (nr - 3, nr)]:
         o = O.estimate_vix(z, roi, ht, hr, samples, 9, rows=(rb, re))
         assert np.array_equal(skip[rb:re], o[rb:re]), rb
