@@ -412,9 +412,9 @@ __device__ __forceinline__ int dp2hi(uint32_t pair, uint32_t w) {
 // 2^16 m/M)/2^16 < 255/2^16 < 1/M cannot carry past the next integer).
 struct __align__(16) QuadGeomC {   // skip test
     int soff;         // skip-map entry of the start post's block (padded block indices)
-    int LE;           // Es * M
-    int D;            // LOS rise start -> end
-    int w;            // M | tr << 8 | mneg << 9 | ys3 << 10 | mag << 12   (M = 0: nothing to walk)
+    int LE2;          // Es*M + min(0, 4D)  (Es = LOS height at the start post, D = LOS rise)
+    int D4;           // 4D
+    int w;            // M | c0 << 8 | tr << 11 | mneg << 12 | mag << 13   (M = 0: nothing to walk)
 };
 struct __align__(16) QuadGeomF {   // exact walk
     const uint2* Q;   // start post's entry in its plane
@@ -445,13 +445,13 @@ __device__ __forceinline__ bool quad_walk(const QuadGeom* gp, int lane) {
     const int nM = c.w & 0xff, steps = nM - 1;
     if (steps <= 0) return false;
     const QuadGeomF f = gp->f;
-    const int nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 12, D = c.D;
+    const int nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 13, D = c.D4 >> 2;
     const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
     const int q32 = (32 * mag) >> 16, r32 = 32 * nm - q32 * nM;
     int i = 1 + lane;
     int q = (i * mag) >> 16, r = i * nm - q * nM;
     int off = i + q * sm;
-    int rhsM = c.LE + i * D, rhsm = f.Es * nm + q * D;
+    int rhsM = c.LE2 - min(0, c.D4) + i * D, rhsm = f.Es * nm + q * D;
     const int dOff = 32 + q32 * sm, dRhsM = 32 * D, dRhsm = q32 * D;
     for (int k = steps >> 5; k; --k) {
         if (__any_sync(kFull, quad_test(qld(f.Q + off), r, nm, wb, rhsM, rhsm))) return true;
@@ -474,8 +474,12 @@ __device__ __forceinline__ bool quad_walk(const QuadGeom* gp, int lane) {
 // those 8x8 posts (k_skipmap).  The interpolated terrain at any crossing of the
 // group is at most that maximum, and the LOS over the group is at least its
 // value at one end, so
-//     smax * M  <=  Es*M + min(4g*D, min(4g+4, M-1)*D)
-// proves that no crossing of the group is blocked.
+//     smax * M  <=  Es*M + 4g*D + min(0, 4D)  =  LE2 + g*D4
+// proves that no crossing of the group is blocked.  The window's minor corner
+// block, relative to the start post's, is mb = (c0 + q(4g+1)) >> 2 for a
+// positive minor direction (c0 = the start post's minor offset in its block),
+// and -((c0 + q(4g+1)) >> 2) for a negative one (c0 = 7 - that offset), so the
+// map index is soff + g + ((c0 + q(4g+1)) >> 2) * ssp with a signed pitch ssp.
 //
 // Sequential form (TXS_VIX_SKIP=2): one segment per warp pass, lane l testing
 // group 32k+l, failing groups walked in order with an exit at the first block.
@@ -484,28 +488,24 @@ __device__ __forceinline__ bool quad_walk_skip(const QuadGeom* gp, const QuadPit
     const QuadGeomC c = gp->c;
     const int nM = c.w & 0xff, steps = nM - 1;
     if (steps <= 0) return false;
-    const int mag = (unsigned)c.w >> 12, D = c.D;
-    // minor block of group g's window corner: (c0 + sgn*q(4g+1)) >> 2
-    const bool mneg = c.w & 0x200;
-    const int ys3 = (c.w >> 10) & 3;
-    const int c0 = mneg ? ys3 - 4 : ys3, sgn = mneg ? -1 : 1;
-    const int sp = (c.w & 0x100) ? P.pt : P.pv;
+    const int mag = (unsigned)c.w >> 13, mag4 = mag << 2, c0 = (c.w >> 8) & 7;
+    const int sp = (c.w & 0x800) ? P.pt : P.pv, ssp = (c.w & 0x1000) ? -sp : sp;
     const int ngroups = (steps + 3) >> 2;
     const int16_t* S = smap + c.soff;
     for (int g0 = 0; g0 < ngroups; g0 += 32) {
         const int gi = g0 + lane;
         bool fail = false;
         if (gi < ngroups) {
-            const int q1 = ((4 * gi + 1) * mag) >> 16;
-            const int smax = __ldg(S + gi + ((c0 + sgn * q1) >> 2) * sp);
-            fail = smax * nM > c.LE + min(4 * gi * D, min(4 * gi + 4, steps) * D);
+            const int q1 = (gi * mag4 + mag) >> 16;
+            const int smax = __ldg(S + gi + ((c0 + q1) >> 2) * ssp);
+            fail = smax * nM > c.LE2 + gi * c.D4;
         }
         const unsigned F = __ballot_sync(kFull, fail);
         if (!F) continue;
         if (fail) s_fail[__popc(F & ((1u << lane) - 1))] = gi;
         __syncwarp();
         const QuadGeomF f = gp->f;
-        const int nm = f.msm & 0xff, sm = f.msm >> 8;
+        const int nm = f.msm & 0xff, sm = f.msm >> 8, D = c.D4 >> 2, LE = c.LE2 - min(0, c.D4);
         const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
         const int cnt = __popc(F);
         for (int j = 0; j < cnt; j += 8) {
@@ -515,7 +515,7 @@ __device__ __forceinline__ bool quad_walk_skip(const QuadGeom* gp, const QuadPit
                 const int i = 4 * s_fail[sub] + 1 + (lane & 3);
                 if (i <= steps) {
                     const int q = (i * mag) >> 16, r = i * nm - q * nM;
-                    b = quad_test(qld(f.Q + i + q * sm), r, nm, wb, c.LE + i * D, f.Es * nm + q * D);
+                    b = quad_test(qld(f.Q + i + q * sm), r, nm, wb, LE + i * D, f.Es * nm + q * D);
                 }
             }
             if (__any_sync(kFull, b)) return true;
@@ -527,16 +527,20 @@ __device__ __forceinline__ bool quad_walk_skip(const QuadGeom* gp, const QuadPit
 
 //
 // A batch of up to 32 segments (lane l built segment l's geometry g) is tested
-// as one flattened list of (segment, group) pairs, 32 per warp pass, so lanes
-// do not idle on short segments; the pairs that fail are walked exactly, 8
-// groups x 4 steps per pass, with the predicates of quad_test, skipping
-// segments already found blocked.  Returns the number of visible segments.
+// as one flattened list of (segment, unit) pairs, 32 per warp pass, so lanes
+// do not idle on short segments; a unit is kVixUnit consecutive groups, tested
+// by one lane (the per-pair bookkeeping is paid once per unit).  The groups
+// that fail are walked exactly, 8 groups x 4 steps per pass, with the
+// predicates of quad_test, skipping segments already found blocked.  Returns
+// the number of visible segments.
+constexpr int kVixUnit = 4;
 __device__ __forceinline__ int batch_skip(const QuadGeom& g, int ns, int lane, QuadGeom* s_geo, int* s_pre,
                                           int* s_fail, const int16_t* __restrict__ smap, const QuadPitch& P) {
     const int nMl = g.c.w & 0xff;
     const int ng = (lane < ns && nMl >= 2) ? (nMl + 2) >> 2 : 0;   // ceil((M-1)/4) groups
+    const int nu = (ng + kVixUnit - 1) / kVixUnit;
     const unsigned nz = __ballot_sync(kFull, ng > 0);
-    int inc = ng;
+    int inc = nu;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const int t = __shfl_up_sync(kFull, inc, o);
@@ -546,55 +550,71 @@ __device__ __forceinline__ int batch_skip(const QuadGeom& g, int ns, int lane, Q
     if (ng > 0) {   // compacted: segments with groups, in lane order; prefixes strictly increase
         const int slot = __popc(nz & ((1u << lane) - 1));
         s_geo[slot] = g;
-        s_pre[slot] = inc - ng;
+        const int sp = (g.c.w & 0x800) ? P.pt : P.pv;
+        s_pre[slot] = (inc - nu) | (((g.c.w & 0x1000) ? -sp : sp) << 16);   // unit prefix | signed map pitch
     }
     __syncwarp();
-    const int myp = lane < __popc(nz) ? s_pre[lane] : 0x7fffffff;
+    const int myp = lane < __popc(nz) ? s_pre[lane] & 0xffff : 0x7fffffff;
     unsigned blk = 0;   // blocked slots
     for (int base = 0; base < T; base += 32) {
         // slot of pair base+lane: (slots starting at or before base) - 1 + (starts in (base, base+lane])
         const unsigned B = __reduce_or_sync(kFull, (myp > base && myp < base + 32) ? 1u << (myp - base) : 0u);
         const int cb = __popc(__ballot_sync(kFull, myp <= base));
         const int p = base + lane;
-        bool fail = false;
-        int ent = 0;
         const int sl = cb - 1 + __popc(B & ((2u << lane) - 1));
+        unsigned fm = 0;   // failing groups of this lane's unit
+        int g0 = 0;
         if (p < T && !((blk >> sl) & 1u)) {   // pairs of segments already blocked are dropped
-            const int gi = p - s_pre[sl];
+            const int ps = s_pre[sl];
             const QuadGeomC c = s_geo[sl].c;
-            const int nM = c.w & 0xff, steps = nM - 1, mag = (unsigned)c.w >> 12;
-            const bool mneg = c.w & 0x200;
-            const int ys3 = (c.w >> 10) & 3;
-            const int q1 = ((4 * gi + 1) * mag) >> 16;
-            const int mb = (mneg ? ys3 - 4 - q1 : ys3 + q1) >> 2;
-            const int smax = __ldg(smap + c.soff + gi + mb * ((c.w & 0x100) ? P.pt : P.pv));
-            fail = smax * nM > c.LE + min(4 * gi * c.D, min(4 * gi + 4, steps) * c.D);
-            ent = sl | (gi << 8);
+            const int nM = c.w & 0xff, mag = (unsigned)c.w >> 13, c0 = (c.w >> 8) & 7, ssp = ps >> 16;
+            const int ngs = (nM + 2) >> 2;
+            g0 = (p - (ps & 0xffff)) * kVixUnit;
+            const int16_t* S = smap + c.soff;
+            int q1 = (g0 * (mag << 2) + mag) >> 16;
+#pragma unroll
+            for (int k = 0; k < kVixUnit; ++k) {
+                const int gi = g0 + k;
+                if (k == 0 || gi < ngs) {
+                    const int smax = __ldg(S + gi + ((c0 + q1) >> 2) * ssp);
+                    if (smax * nM > c.LE2 + gi * c.D4) fm |= 1u << k;
+                }
+                q1 = ((gi + 1) * (mag << 2) + mag) >> 16;
+            }
         }
-        const unsigned F = __ballot_sync(kFull, fail);
+        const unsigned F = __ballot_sync(kFull, fm != 0);
         if (!F) continue;
-        if (fail) s_fail[__popc(F & ((1u << lane) - 1))] = ent;
+        // failing groups -> s_fail (slot | group << 8), in (slot, group) order
+        const int nf = __popc(fm);
+        int off = nf;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(kFull, off, o);
+            if (lane >= o) off += t;
+        }
+        const int cnt = __shfl_sync(kFull, off, 31);
+        off -= nf;
+        for (unsigned m = fm; m; m &= m - 1) s_fail[off++] = sl | ((g0 + __ffs(m) - 1) << 8);
         __syncwarp();
-        const int cnt = __popc(F);
         for (int j = 0; j < cnt; j += 8) {
             const int sub = j + (lane >> 2);
             bool b = false;
-            int sl = 0;
+            int sf = 0;
             if (sub < cnt) {
                 const int e = s_fail[sub];
-                sl = e & 0xff;
+                sf = e & 0xff;
                 const int i = 4 * (e >> 8) + 1 + (lane & 3);
-                const QuadGeomC c = s_geo[sl].c;
+                const QuadGeomC c = s_geo[sf].c;
                 const int nM = c.w & 0xff;
-                if (i < nM && !((blk >> sl) & 1u)) {
-                    const QuadGeomF f = s_geo[sl].f;
-                    const int nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 12;
+                if (i < nM && !((blk >> sf) & 1u)) {
+                    const QuadGeomF f = s_geo[sf].f;
+                    const int nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 13, D = c.D4 >> 2;
                     const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
                     const int q = (i * mag) >> 16, r = i * nm - q * nM;
-                    b = quad_test(qld(f.Q + i + q * sm), r, nm, wb, c.LE + i * c.D, f.Es * nm + q * c.D);
+                    b = quad_test(qld(f.Q + i + q * sm), r, nm, wb, c.LE2 - min(0, c.D4) + i * D, f.Es * nm + q * D);
                 }
             }
-            blk |= __reduce_or_sync(kFull, b ? 1u << sl : 0u);
+            blk |= __reduce_or_sync(kFull, b ? 1u << sf : 0u);
         }
         __syncwarp();
     }
@@ -609,11 +629,12 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
                                                                    const int16_t* __restrict__ smap,
                                                                    unsigned long long* __restrict__ counters) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
-    // dynamic smem: [geometry: kVixWarps x 32][failed groups, group prefixes: 2 x kVixWarps x 32][samples: kVixWarps x S ints]
+    // dynamic smem: [geometry: kVixWarps x 32][failed groups: kVixWarps x 32 x kVixUnit][unit prefixes: kVixWarps x 32]
+    //               [samples: kVixWarps x S ints]
     QuadGeom* s_geo = (QuadGeom*)s_dyn + warp_of_thread() * 32;
-    int* s_fail = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + warp_of_thread() * 32;
-    int* s_pre = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + kVixWarps * 32 + warp_of_thread() * 32;
-    int* s_samp = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + 2 * kVixWarps * 32 + warp_of_thread() * a.S;
+    int* s_fail = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + warp_of_thread() * 32 * kVixUnit;
+    int* s_pre = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + kVixWarps * 32 * kVixUnit + warp_of_thread() * 32;
+    int* s_samp = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + kVixWarps * 32 * (kVixUnit + 1) + warp_of_thread() * a.S;
     const QuadPitch PQ{a.pv, a.pt};
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // tiles in vertical strips of a.strip tile columns, row-major inside a strip
@@ -678,9 +699,10 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
                 const int mag = nM ? (nm * 65536 + nM - 1) / nM : 0;
                 g.c.soff = tr ? a.st_off + ((maj >> 2) + 1) + ((mnr >> 2) + 1) * a.pt
                               : ((maj >> 2) + 1) + ((mnr >> 2) + 1) * a.pv;
-                g.c.LE = Es * nM;
-                g.c.D = rev ? E - Zt : Zt - E;
-                g.c.w = nM | ((int)tr << 8) | ((int)mneg << 9) | ((mnr & 3) << 10) | (mag << 12);
+                const int D = rev ? E - Zt : Zt - E;
+                g.c.LE2 = Es * nM + min(0, 4 * D);
+                g.c.D4 = 4 * D;
+                g.c.w = nM | ((mneg ? 7 - (mnr & 3) : (mnr & 3)) << 8) | ((int)tr << 11) | ((int)mneg << 12) | (mag << 13);
             }
             if (SKIP == 1) {
                 vis += batch_skip(g, ns, lane, s_geo, s_pre, s_fail, smap, PQ);
@@ -819,11 +841,11 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         const int64_t nbp = (int64_t)(Hb + 2) * (Wb + 2);
         if (nsv + nst > 0x7fffffff) return fail(c, TXS_ERR_RANGE, "vix", "grid too large");
         a.st_off = (int)nsv;
-        // 1: flattened (segment, group) skip test, 2: per-segment skip test, 0: full walk.
-        // Measured (profiles/README.md): flattened at roi 100 (C3 425 -> 250 ms, C4
-        // 4280 -> 2018 vs 326 / 2614 per segment); per segment at roi 200, where
-        // blocked segments gain from the in-order early exit (C2 55.0 -> 50.1 vs 57.1)
-        int skip = p.roi >= 150 ? 2 : 1;
+        // 1: flattened (segment, unit) skip test, 2: per-segment skip test, 0: full walk.
+        // Measured (profiles/README.md), ms: C2 55.4 / 45.8 / 48.9, C3 429 / 212 / 313,
+        // C4 4273 / 1688 / 2508 (full / flattened / per segment)
+        int skip = 1;
+        if (a.pv >= 32768 || a.pt >= 32768) skip = 0;   // signed 16-bit map pitches (batch_skip)
         if (const char* e = getenv("TXS_VIX_SKIP")) skip = std::max(0, std::min(2, atoi(e)));
         const size_t map_bytes = skip ? sizeof(int16_t) * (size_t)(nsv + nst + nbp) : 0;
         // rebuilt on every call (part of the timed stage; ~1 HBM pass of 34 B/post)
@@ -845,7 +867,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         }
         const uint2* qp = (const uint2*)c->d_pairs;
         set_zbounds(c->d_z, c->d_z + n, c->stream, (const int16_t*)qp, (const int16_t*)(qp + nq));
-        const size_t qsm = samp + (sizeof(QuadGeom) + 2 * sizeof(int)) * kVixWarps * 32;
+        const size_t qsm = samp + (sizeof(QuadGeom) + (kVixUnit + 1) * sizeof(int)) * kVixWarps * 32;
         auto kq = skip == 1 ? k_vix_quads<1> : skip == 2 ? k_vix_quads<2> : k_vix_quads<0>;
         if (qsm > 48 * 1024)
             TXS_CUDA(c, "vix", cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm));
