@@ -533,8 +533,11 @@ __device__ __forceinline__ bool quad_walk_skip(const QuadGeom* gp, const QuadPit
 // that fail are walked exactly, 8 groups x 4 steps per pass, with the
 // predicates of quad_test, skipping segments already found blocked.  Returns
 // the number of visible segments.
-constexpr int kVixUnit = 4;
-__device__ __forceinline__ int batch_skip(const QuadGeom& g, int ns, int lane, QuadGeom* s_geo, int* s_pre,
+#ifndef VIX_UNIT
+#define VIX_UNIT 8   // measured: 2 / 4 / 8 -> c2 51.8 / 45.7 / 44.3 ms, c3 218.9 / 211.5 / 210.6
+#endif
+constexpr int kVixUnit = VIX_UNIT;
+__device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int lane, QuadGeom* s_geo, int* s_pre,
                                           int* s_fail, const int16_t* __restrict__ smap, const QuadPitch& P) {
     const int nMl = g.c.w & 0xff;
     const int ng = (lane < ns && nMl >= 2) ? (nMl + 2) >> 2 : 0;   // ceil((M-1)/4) groups
@@ -618,7 +621,9 @@ __device__ __forceinline__ int batch_skip(const QuadGeom& g, int ns, int lane, Q
         }
         __syncwarp();
     }
-    return ns - __popc(blk);
+    // visible lanes (lane order): segments without groups, and slots not blocked
+    const int slot = __popc(nz & ((1u << lane) - 1));
+    return __ballot_sync(kFull, lane < ns && (ng == 0 || !((blk >> slot) & 1u)));
 }
 
 template <int SKIP>
@@ -630,11 +635,11 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
                                                                    unsigned long long* __restrict__ counters) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
     // dynamic smem: [geometry: kVixWarps x 32][failed groups: kVixWarps x 32 x kVixUnit][unit prefixes: kVixWarps x 32]
-    //               [samples: kVixWarps x S ints]
+    //               [sample queue: kVixWarps x 64 ints]
     QuadGeom* s_geo = (QuadGeom*)s_dyn + warp_of_thread() * 32;
     int* s_fail = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + warp_of_thread() * 32 * kVixUnit;
     int* s_pre = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + kVixWarps * 32 * kVixUnit + warp_of_thread() * 32;
-    int* s_samp = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + kVixWarps * 32 * (kVixUnit + 1) + warp_of_thread() * a.S;
+    int* s_q = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + kVixWarps * 32 * (kVixUnit + 1) + warp_of_thread() * 64;
     const QuadPitch PQ{a.pv, a.pt};
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // tiles in vertical strips of a.strip tile columns, row-major inside a strip
@@ -650,12 +655,83 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
     const int R2 = a.R * a.R;
     unsigned long long n_cross = 0;
     int n_posts = 0;
-    for (int pi = warp; pi < kTileQ * kTileQ; pi += kVixWarps) {
-        const int r = ty0 + pi / kTileQ, c = tx0 + pi % kTileQ;
+    // The warp's posts are pi = warp + 16 j (j < kPPW).  Their receivers (D6)
+    // are drawn post by post into a per-warp queue of (dr, dc, j) and tested 32
+    // at a time, so a batch is full whatever S is; lane j keeps post j's
+    // observer elevation and visible count.
+    constexpr int kPPW = kTileQ * kTileQ / kVixWarps;
+    int myE = 0, mycnt = 0, qn = 0;
+    auto post_rc = [&](int j, int& r, int& c) {
+        const int pi = warp + kVixWarps * j;
+        r = ty0 + pi / kTileQ;
+        c = tx0 + pi % kTileQ;
+    };
+    auto run_batch = [&](int ns) {
+        QuadGeom g{};
+        int pj = 0;
+        if (lane < ns) {
+            const int H = a.zr1 - a.zr0;
+            const int pk = s_q[lane];
+            int dr = (pk & 0x1ff) - 256, dc = ((pk >> 9) & 0x1ff) - 256;
+            pj = pk >> 18;
+            int r, c;
+            post_rc(pj, r, c);
+            const int E = __shfl_sync(__activemask(), myE, pj);
+            const int Zt = zld(z + (int64_t)(r + dr) * ncols + (c + dc)) + a.hr;
+            n_cross += crossings_tab(dr, dc, gcdt);
+            const bool tr = abs(dr) > abs(dc);
+            const bool rev = tr ? dr < 0 : dc < 0;      // walk from the receiver
+            const int y = r - a.zr0 + (rev ? dr : 0), x = c + (rev ? dc : 0);   // start post
+            if (rev) { dr = -dr; dc = -dc; }
+            const int nM = tr ? dr : dc, nm = tr ? abs(dc) : abs(dr);
+            const bool mneg = (tr ? dc : dr) < 0;
+            const int64_t n = (int64_t)H * a.wp, nT = (int64_t)ncols * a.hp;
+            const int stride = tr ? a.hp : a.wp;
+            const int Es = rev ? Zt : E;
+            g.f.Q = qp + (tr ? 2 * n + (int64_t)x * a.hp + y + (mneg ? nT : 0) : (int64_t)y * a.wp + x + (mneg ? n : 0));
+            g.f.Es = Es;
+            g.f.msm = nm | ((nm == 0 ? 0 : (mneg ? -stride : stride)) * 256);
+            // skip map (k_skipmap): padded 4x4-block indices of the start post,
+            // SV row-major for column-major walks, ST column-major for row-major ones
+            const int maj = tr ? y : x, mnr = tr ? x : y;
+            const int mag = nM ? (nm * 65536 + nM - 1) / nM : 0;
+            g.c.soff = tr ? a.st_off + ((maj >> 2) + 1) + ((mnr >> 2) + 1) * a.pt
+                          : ((maj >> 2) + 1) + ((mnr >> 2) + 1) * a.pv;
+            const int D = rev ? E - Zt : Zt - E;
+            g.c.LE2 = Es * nM + min(0, 4 * D);
+            g.c.D4 = 4 * D;
+            g.c.w = nM | ((mneg ? 7 - (mnr & 3) : (mnr & 3)) << 8) | ((int)tr << 11) | ((int)mneg << 12) | (mag << 13);
+        }
+        __syncwarp();
+        unsigned vism;
+        if (SKIP == 1) {
+            vism = batch_skip(g, ns, lane, s_geo, s_pre, s_fail, smap, PQ);
+        } else {
+            s_geo[lane] = g;
+            __syncwarp();
+            bool vis = false;
+            for (int sidx = 0; sidx < ns; ++sidx) {
+                const bool blk = SKIP == 2 ? quad_walk_skip(s_geo + sidx, PQ, smap, s_fail, lane) : quad_walk(s_geo + sidx, lane);
+                if (lane == sidx) vis = !blk;
+            }
+            vism = __ballot_sync(kFull, vis);
+        }
+#pragma unroll
+        for (int j = 0; j < kPPW; ++j) {
+            const int cj = __popc(vism & __ballot_sync(kFull, lane < ns && pj == j));
+            if (lane == j) mycnt += cj;
+        }
+        __syncwarp();
+    };
+    for (int j = 0; j < kPPW; ++j) {
+        int r, c;
+        post_rc(j, r, c);
         if (r >= a.row_end || c >= ncols) continue;
+        ++n_posts;
         const uint64_t base = mix_seed(a.seed, (uint64_t)r, (uint64_t)c);
         const int E = zld(z + (int64_t)r * ncols + c) + a.ht;
-        // ---- draw S receivers (D6) ----
+        if (lane == j) myE = E;
+        // ---- draw S receivers (D6) into the queue ----
         int nacc = 0;
         for (uint64_t k = 0; nacc < a.S; k += 32) {
             const int v = (int)fm_mod(a.span, sm_draw(base, k + lane)) - a.R;
@@ -664,58 +740,30 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
             const bool ok = !(lane & 1) && dr * dr + dc * dc <= R2 && r + dr >= 0 && r + dr < nrows &&
                             c + dc >= 0 && c + dc < ncols;
             const unsigned mask = __ballot_sync(kFull, ok);
+            const int take = min(__popc(mask), a.S - nacc);
             if (ok) {
-                const int slot = nacc + __popc(mask & ((1u << lane) - 1));
-                if (slot < a.S) s_samp[slot] = (dr & 0xffff) | (dc << 16);
+                const int rank = __popc(mask & ((1u << lane) - 1));
+                if (rank < take) s_q[qn + rank] = (dr + 256) | ((dc + 256) << 9) | (j << 18);
             }
-            nacc += __popc(mask);
-        }
-        __syncwarp();
-        int vis = 0;
-        for (int s0 = 0; s0 < a.S; s0 += 32) {
-            const int ns = min(32, a.S - s0);
-            QuadGeom g{};
-            if (lane < ns) {
-                const int H = a.zr1 - a.zr0;
-                const int pk = s_samp[s0 + lane];
-                int dr = (int)(int16_t)(pk & 0xffff), dc = pk >> 16;
-                const int Zt = zld(z + (int64_t)(r + dr) * ncols + (c + dc)) + a.hr;
-                n_cross += crossings_tab(dr, dc, gcdt);
-                const bool tr = abs(dr) > abs(dc);
-                const bool rev = tr ? dr < 0 : dc < 0;      // walk from the receiver
-                const int y = r - a.zr0 + (rev ? dr : 0), x = c + (rev ? dc : 0);   // start post
-                if (rev) { dr = -dr; dc = -dc; }
-                const int nM = tr ? dr : dc, nm = tr ? abs(dc) : abs(dr);
-                const bool mneg = (tr ? dc : dr) < 0;
-                const int64_t n = (int64_t)H * a.wp, nT = (int64_t)ncols * a.hp;
-                const int stride = tr ? a.hp : a.wp;
-                const int Es = rev ? Zt : E;
-                g.f.Q = qp + (tr ? 2 * n + (int64_t)x * a.hp + y + (mneg ? nT : 0) : (int64_t)y * a.wp + x + (mneg ? n : 0));
-                g.f.Es = Es;
-                g.f.msm = nm | ((nm == 0 ? 0 : (mneg ? -stride : stride)) * 256);
-                // skip map (k_skipmap): padded 4x4-block indices of the start post,
-                // SV row-major for column-major walks, ST column-major for row-major ones
-                const int maj = tr ? y : x, mnr = tr ? x : y;
-                const int mag = nM ? (nm * 65536 + nM - 1) / nM : 0;
-                g.c.soff = tr ? a.st_off + ((maj >> 2) + 1) + ((mnr >> 2) + 1) * a.pt
-                              : ((maj >> 2) + 1) + ((mnr >> 2) + 1) * a.pv;
-                const int D = rev ? E - Zt : Zt - E;
-                g.c.LE2 = Es * nM + min(0, 4 * D);
-                g.c.D4 = 4 * D;
-                g.c.w = nM | ((mneg ? 7 - (mnr & 3) : (mnr & 3)) << 8) | ((int)tr << 11) | ((int)mneg << 12) | (mag << 13);
-            }
-            if (SKIP == 1) {
-                vis += batch_skip(g, ns, lane, s_geo, s_pre, s_fail, smap, PQ);
-            } else {
-                s_geo[lane] = g;
-                __syncwarp();
-                for (int sidx = 0; sidx < ns; ++sidx)
-                    vis += (SKIP == 2 ? quad_walk_skip(s_geo + sidx, PQ, smap, s_fail, lane) : quad_walk(s_geo + sidx, lane)) ? 0 : 1;
-            }
+            nacc += take;
+            qn += take;
             __syncwarp();
+            if (qn >= 32) {
+                run_batch(32);
+                const int rest = qn - 32;   // < 16
+                const int t = lane < rest ? s_q[32 + lane] : 0;
+                __syncwarp();
+                if (lane < rest) s_q[lane] = t;
+                __syncwarp();
+                qn = rest;
+            }
         }
-        if (lane == 0) out[(int64_t)r * ncols + c] = (uint8_t)vis;
-        ++n_posts;
+    }
+    if (qn > 0) run_batch(qn);
+    for (int j = 0; j < kPPW; ++j) {
+        int r, c;
+        post_rc(j, r, c);
+        if (lane == j && r < a.row_end && c < ncols) out[(int64_t)r * ncols + c] = (uint8_t)mycnt;
     }
     for (int o = 16; o; o >>= 1) n_cross += __shfl_down_sync(kFull, n_cross, o);
     if (lane == 0 && n_posts) {
@@ -867,7 +915,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         }
         const uint2* qp = (const uint2*)c->d_pairs;
         set_zbounds(c->d_z, c->d_z + n, c->stream, (const int16_t*)qp, (const int16_t*)(qp + nq));
-        const size_t qsm = samp + (sizeof(QuadGeom) + (kVixUnit + 1) * sizeof(int)) * kVixWarps * 32;
+        const size_t qsm = (sizeof(QuadGeom) + (kVixUnit + 1) * sizeof(int)) * kVixWarps * 32 + sizeof(int) * 64 * kVixWarps;
         auto kq = skip == 1 ? k_vix_quads<1> : skip == 2 ? k_vix_quads<2> : k_vix_quads<0>;
         if (qsm > 48 * 1024)
             TXS_CUDA(c, "vix", cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm));
