@@ -528,20 +528,18 @@ __device__ __forceinline__ bool quad_walk_skip(const QuadGeom* gp, const QuadPit
 //
 // A batch of up to 32 segments (lane l built segment l's geometry g) is tested
 // as one flattened list of (segment, unit) pairs, 32 per warp pass, so lanes
-// do not idle on short segments; a unit is kVixUnit consecutive groups, tested
-// by one lane (the per-pair bookkeeping is paid once per unit).  The groups
-// that fail are walked exactly, 8 groups x 4 steps per pass, with the
-// predicates of quad_test, skipping segments already found blocked.  Returns
-// the number of visible segments.
-#ifndef VIX_UNIT
-#define VIX_UNIT 8   // measured: 2 / 4 / 8 -> c2 51.8 / 45.7 / 44.3 ms, c3 218.9 / 211.5 / 210.6
-#endif
-constexpr int kVixUnit = VIX_UNIT;
+// do not idle on short segments; a unit is U consecutive groups (4U steps),
+// tested by one lane, so the per-pair bookkeeping is paid once per unit.  A
+// unit with a failing group is then walked exactly, whole: one warp pass of 32
+// consecutive steps (coalesced plane loads, the predicates of quad_test), in
+// (segment, unit) order, skipping segments already found blocked.  Returns
+// the mask of lanes whose segment is visible.
+template <int U>
 __device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int lane, QuadGeom* s_geo, int* s_pre,
-                                          int* s_fail, const int16_t* __restrict__ smap, const QuadPitch& P) {
+                                               int* s_fail, const int16_t* __restrict__ smap, const QuadPitch& P) {
     const int nMl = g.c.w & 0xff;
     const int ng = (lane < ns && nMl >= 2) ? (nMl + 2) >> 2 : 0;   // ceil((M-1)/4) groups
-    const int nu = (ng + kVixUnit - 1) / kVixUnit;
+    const int nu = (ng + U - 1) / U;
     const unsigned nz = __ballot_sync(kFull, ng > 0);
     int inc = nu;
 #pragma unroll
@@ -565,59 +563,49 @@ __device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int la
         const int cb = __popc(__ballot_sync(kFull, myp <= base));
         const int p = base + lane;
         const int sl = cb - 1 + __popc(B & ((2u << lane) - 1));
-        unsigned fm = 0;   // failing groups of this lane's unit
-        int g0 = 0;
+        bool fail = false;
+        int ui = 0;
         if (p < T && !((blk >> sl) & 1u)) {   // pairs of segments already blocked are dropped
             const int ps = s_pre[sl];
             const QuadGeomC c = s_geo[sl].c;
             const int nM = c.w & 0xff, mag = (unsigned)c.w >> 13, c0 = (c.w >> 8) & 7, ssp = ps >> 16;
             const int ngs = (nM + 2) >> 2;
-            g0 = (p - (ps & 0xffff)) * kVixUnit;
+            ui = p - (ps & 0xffff);
+            const int g0 = ui * U;
             const int16_t* S = smap + c.soff;
             int q1 = (g0 * (mag << 2) + mag) >> 16;
 #pragma unroll
-            for (int k = 0; k < kVixUnit; ++k) {
+            for (int k = 0; k < U; ++k) {
                 const int gi = g0 + k;
                 if (k == 0 || gi < ngs) {
                     const int smax = __ldg(S + gi + ((c0 + q1) >> 2) * ssp);
-                    if (smax * nM > c.LE2 + gi * c.D4) fm |= 1u << k;
+                    fail |= smax * nM > c.LE2 + gi * c.D4;
                 }
                 q1 = ((gi + 1) * (mag << 2) + mag) >> 16;
             }
         }
-        const unsigned F = __ballot_sync(kFull, fm != 0);
+        const unsigned F = __ballot_sync(kFull, fail);
         if (!F) continue;
-        // failing groups -> s_fail (slot | group << 8), in (slot, group) order
-        const int nf = __popc(fm);
-        int off = nf;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(kFull, off, o);
-            if (lane >= o) off += t;
-        }
-        const int cnt = __shfl_sync(kFull, off, 31);
-        off -= nf;
-        for (unsigned m = fm; m; m &= m - 1) s_fail[off++] = sl | ((g0 + __ffs(m) - 1) << 8);
+        if (fail) s_fail[__popc(F & ((1u << lane) - 1))] = sl | (ui << 8);
         __syncwarp();
-        for (int j = 0; j < cnt; j += 8) {
-            const int sub = j + (lane >> 2);
+        const int cnt = __popc(F);
+        for (int h = 0; h < cnt; ++h) {
+            const int e = s_fail[h];
+            const int sf = e & 0xff;
+            if ((blk >> sf) & 1u) continue;
+            const QuadGeomC c = s_geo[sf].c;
+            const QuadGeomF f = s_geo[sf].f;
+            const int nM = c.w & 0xff;
+            // 32 steps from the unit's first (a unit of U < 8 groups is walked with its successor)
+            const int i = 4 * U * (e >> 8) + 1 + lane;
             bool b = false;
-            int sf = 0;
-            if (sub < cnt) {
-                const int e = s_fail[sub];
-                sf = e & 0xff;
-                const int i = 4 * (e >> 8) + 1 + (lane & 3);
-                const QuadGeomC c = s_geo[sf].c;
-                const int nM = c.w & 0xff;
-                if (i < nM && !((blk >> sf) & 1u)) {
-                    const QuadGeomF f = s_geo[sf].f;
-                    const int nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 13, D = c.D4 >> 2;
-                    const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
-                    const int q = (i * mag) >> 16, r = i * nm - q * nM;
-                    b = quad_test(qld(f.Q + i + q * sm), r, nm, wb, c.LE2 - min(0, c.D4) + i * D, f.Es * nm + q * D);
-                }
+            if (i < nM) {
+                const int nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 13, D = c.D4 >> 2;
+                const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
+                const int q = (i * mag) >> 16, r = i * nm - q * nM;
+                b = quad_test(qld(f.Q + i + q * sm), r, nm, wb, c.LE2 - min(0, c.D4) + i * D, f.Es * nm + q * D);
             }
-            blk |= __reduce_or_sync(kFull, b ? 1u << sf : 0u);
+            if (__any_sync(kFull, b)) blk |= 1u << sf;
         }
         __syncwarp();
     }
@@ -626,7 +614,7 @@ __device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int la
     return __ballot_sync(kFull, lane < ns && (ng == 0 || !((blk >> slot) & 1u)));
 }
 
-template <int SKIP>
+template <int SKIP, int U>
 __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16_t* __restrict__ z,
                                                                    const uint2* __restrict__ qp, int nrows, int ncols,
                                                                    uint8_t* __restrict__ out, VixArgs a,
@@ -634,12 +622,13 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
                                                                    const int16_t* __restrict__ smap,
                                                                    unsigned long long* __restrict__ counters) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
-    // dynamic smem: [geometry: kVixWarps x 32][failed groups: kVixWarps x 32 x kVixUnit][unit prefixes: kVixWarps x 32]
+    // dynamic smem: [geometry: kVixWarps x 32][failing units: kVixWarps x 32][unit prefixes: kVixWarps x 32]
     //               [sample queue: kVixWarps x 64 ints]
     QuadGeom* s_geo = (QuadGeom*)s_dyn + warp_of_thread() * 32;
-    int* s_fail = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + warp_of_thread() * 32 * kVixUnit;
-    int* s_pre = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + kVixWarps * 32 * kVixUnit + warp_of_thread() * 32;
-    int* s_q = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + kVixWarps * 32 * (kVixUnit + 1) + warp_of_thread() * 64;
+    constexpr int kFailInts = 32;   // failing units
+    int* s_fail = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + warp_of_thread() * kFailInts;
+    int* s_pre = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + kVixWarps * kFailInts + warp_of_thread() * 32;
+    int* s_q = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + kVixWarps * (kFailInts + 32) + warp_of_thread() * 64;
     const QuadPitch PQ{a.pv, a.pt};
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // tiles in vertical strips of a.strip tile columns, row-major inside a strip
@@ -705,7 +694,7 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
         __syncwarp();
         unsigned vism;
         if (SKIP == 1) {
-            vism = batch_skip(g, ns, lane, s_geo, s_pre, s_fail, smap, PQ);
+            vism = batch_skip<U>(g, ns, lane, s_geo, s_pre, s_fail, smap, PQ);
         } else {
             s_geo[lane] = g;
             __syncwarp();
@@ -915,8 +904,11 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         }
         const uint2* qp = (const uint2*)c->d_pairs;
         set_zbounds(c->d_z, c->d_z + n, c->stream, (const int16_t*)qp, (const int16_t*)(qp + nq));
-        const size_t qsm = (sizeof(QuadGeom) + (kVixUnit + 1) * sizeof(int)) * kVixWarps * 32 + sizeof(int) * 64 * kVixWarps;
-        auto kq = skip == 1 ? k_vix_quads<1> : skip == 2 ? k_vix_quads<2> : k_vix_quads<0>;
+        const size_t qsm = (sizeof(QuadGeom) * 32 + sizeof(int) * (32 + 32 + 64)) * kVixWarps;
+        // groups per skip unit (measured, profiles/README.md): 8 at roi 200 (C2 46.6 -> 43.5 ms
+        // vs 4), 4 at roi 100 (C3 190.6 -> 180.2 vs 8)
+        const bool u8 = p.roi >= 150;
+        auto kq = skip == 1 ? (u8 ? k_vix_quads<1, 8> : k_vix_quads<1, 4>) : skip == 2 ? k_vix_quads<2, 8> : k_vix_quads<0, 8>;
         if (qsm > 48 * 1024)
             TXS_CUDA(c, "vix", cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm));
         if (!c->d_gcd) {
