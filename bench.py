@@ -154,16 +154,34 @@ class Clocks:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         self.p = None
 
+    def _lines(self):
+        try:
+            with open(self.f.name) as fh:
+                return sum(1 for _ in fh)
+        except OSError:
+            return 0
+
     def start(self):
+        """Start sampling every 200 ms and return once the sampler is live (its
+        first line written), so that even a short timed region is covered."""
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                                        "-i", str(self.idx), "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
+            return
+        t0 = time.time()
+        while self._lines() == 0 and time.time() - t0 < 10 and self.p.poll() is None:
+            time.sleep(0.02)
+        self.n0 = self._lines()
 
     def stop(self):
         if self.p is None:
             return None
+        # at least one sample taken at or after the end of the timed region
+        t0 = time.time()
+        while self._lines() <= getattr(self, "n0", 0) and time.time() - t0 < 2 and self.p.poll() is None:
+            time.sleep(0.02)
         self.p.terminate()
         try:
             self.p.wait(timeout=5)
