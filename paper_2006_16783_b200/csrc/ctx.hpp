@@ -63,7 +63,9 @@ struct SiteState {
 
 // device counter slots
 enum Counter : int {
-    kVixLos = 0, kVixCrossFull, kVsCross, kVsCells, kSiteBytes, kNumCounters
+    kVixLos = 0, kVixCrossFull, kVsCross, kVsCells, kSiteBytes,
+    kVixNext,   // work counter of the persistent VIX kernel (reset per launch)
+    kNumCounters
 };
 
 }  // namespace txs

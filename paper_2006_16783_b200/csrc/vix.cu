@@ -630,42 +630,32 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
     int* s_pre = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + kVixWarps * kFailInts + warp_of_thread() * 32;
     int* s_q = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + kVixWarps * (kFailInts + 32) + warp_of_thread() * 64;
     const QuadPitch PQ{a.pv, a.pt};
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // tiles in vertical strips of a.strip tile columns, row-major inside a strip
-    int ty, tx;
-    {
-        const int strip_tiles = a.strip * a.tiles_y;
-        const int sidx = blockIdx.x / strip_tiles, rem = blockIdx.x - sidx * strip_tiles;
-        const int sw = min(a.strip, a.tiles_x - sidx * a.strip);
-        ty = rem / sw;
-        tx = sidx * a.strip + (rem - ty * sw);
-    }
-    const int ty0 = a.row0 + ty * kTileQ, tx0 = tx * kTileQ;
+    const int lane = threadIdx.x & 31;
     const int R2 = a.R * a.R;
     unsigned long long n_cross = 0;
     int n_posts = 0;
-    // The warp's posts are pi = warp + 16 j (j < kPPW).  Their receivers (D6)
-    // are drawn post by post into a per-warp queue of (dr, dc, j) and tested 32
-    // at a time, so a batch is full whatever S is; lane j keeps post j's
-    // observer elevation and visible count.
-    constexpr int kPPW = kTileQ * kTileQ / kVixWarps;
-    int myE = 0, mycnt = 0, qn = 0;
-    auto post_rc = [&](int j, int& r, int& c) {
-        const int pi = warp + kVixWarps * j;
-        r = ty0 + pi / kTileQ;
-        c = tx0 + pi % kTileQ;
-    };
+    // Persistent CTAs (grid = resident CTAs) whose warps pull tile rows of
+    // kTileQ posts from one global counter, in tile order (vertical strips of
+    // a.strip tile columns, row-major inside a strip): a warp that finishes
+    // early takes more work instead of idling until its CTA's slowest warp is
+    // done, and the rows in flight stay a compact window of the grid (the L2
+    // working set of the quad planes).  Each post's S receivers (D6) are drawn into a
+    // per-warp FIFO of (dr, dc, ring slot) and tested 32 at a time; post p of
+    // the warp (in draw order) owns FIFO samples [p S, p S + S) and ring slot
+    // p & 15, whose lane holds its position, observer elevation and count.
+    constexpr int kRing = 16;
+    int myE = 0, myR = 0, myC = 0, mycnt = 0;
+    int qn = 0;                      // queued samples
+    int p_next = 0, p_open = 0;      // posts drawn / posts finished
+    int tq = 0;                      // samples of the open posts already tested
     auto run_batch = [&](int ns) {
         QuadGeom g{};
-        int pj = 0;
+        const int pk = lane < ns ? s_q[lane] : 0;
+        const int pj = (pk >> 18) & (kRing - 1);
+        const int E = __shfl_sync(kFull, myE, pj), r = __shfl_sync(kFull, myR, pj), c = __shfl_sync(kFull, myC, pj);
         if (lane < ns) {
             const int H = a.zr1 - a.zr0;
-            const int pk = s_q[lane];
             int dr = (pk & 0x1ff) - 256, dc = ((pk >> 9) & 0x1ff) - 256;
-            pj = pk >> 18;
-            int r, c;
-            post_rc(pj, r, c);
-            const int E = __shfl_sync(__activemask(), myE, pj);
             const int Zt = zld(z + (int64_t)(r + dr) * ncols + (c + dc)) + a.hr;
             n_cross += crossings_tab(dr, dc, gcdt);
             const bool tr = abs(dr) > abs(dc);
@@ -705,55 +695,77 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
             }
             vism = __ballot_sync(kFull, vis);
         }
-#pragma unroll
-        for (int j = 0; j < kPPW; ++j) {
-            const int cj = __popc(vism & __ballot_sync(kFull, lane < ns && pj == j));
-            if (lane == j) mycnt += cj;
+        // visible counts of the ring slots in this batch (posts p0 .. p1)
+        const int p0 = p_open + tq / a.S, p1 = p_open + (tq + ns - 1) / a.S;
+        for (int pp = p0; pp <= p1; ++pp) {
+            const int cj = __popc(vism & __ballot_sync(kFull, lane < ns && pj == (pp & (kRing - 1))));
+            if (lane == (pp & (kRing - 1))) mycnt += cj;
         }
+        tq += ns;
+        // posts whose S samples are all tested: write their score, free the slot
+        for (; p_open < p_next && a.S <= tq; ++p_open, tq -= a.S) {
+            if (lane == (p_open & (kRing - 1))) {
+                out[(int64_t)myR * ncols + myC] = (uint8_t)mycnt;
+                mycnt = 0;
+            }
+        }
+        // drop the tested samples from the FIFO
+        const int rest = qn - ns;
+        const int t0 = lane < rest ? s_q[ns + lane] : 0, t1 = lane + 32 < rest ? s_q[ns + lane + 32] : 0;
         __syncwarp();
+        if (lane < rest) s_q[lane] = t0;
+        if (lane + 32 < rest) s_q[lane + 32] = t1;
+        __syncwarp();
+        qn = rest;
     };
-    for (int j = 0; j < kPPW; ++j) {
-        int r, c;
-        post_rc(j, r, c);
-        if (r >= a.row_end || c >= ncols) continue;
-        ++n_posts;
-        const uint64_t base = mix_seed(a.seed, (uint64_t)r, (uint64_t)c);
-        const int E = zld(z + (int64_t)r * ncols + c) + a.ht;
-        if (lane == j) myE = E;
-        // ---- draw S receivers (D6) into the queue ----
-        int nacc = 0;
-        for (uint64_t k = 0; nacc < a.S; k += 32) {
-            const int v = (int)fm_mod(a.span, sm_draw(base, k + lane)) - a.R;
-            const int dc = __shfl_down_sync(kFull, v, 1);
-            const int dr = v;
-            const bool ok = !(lane & 1) && dr * dr + dc * dc <= R2 && r + dr >= 0 && r + dr < nrows &&
-                            c + dc >= 0 && c + dc < ncols;
-            const unsigned mask = __ballot_sync(kFull, ok);
-            const int take = min(__popc(mask), a.S - nacc);
-            if (ok) {
-                const int rank = __popc(mask & ((1u << lane) - 1));
-                if (rank < take) s_q[qn + rank] = (dr + 256) | ((dc + 256) << 9) | (j << 18);
-            }
-            nacc += take;
-            qn += take;
-            __syncwarp();
-            if (qn >= 32) {
-                run_batch(32);
-                const int rest = qn - 32;   // < 16
-                const int t = lane < rest ? s_q[32 + lane] : 0;
+    const int strip_tiles = a.strip * a.tiles_y;
+    for (;;) {
+        long long item = 0;
+        if (lane == 0) item = (long long)atomicAdd(counters + kVixNext, 1ull);
+        item = __shfl_sync(kFull, item, 0);
+        const int64_t tile = item / kTileQ;
+        if (tile >= (int64_t)a.tiles_x * a.tiles_y) break;
+        int ty, tx;
+        {
+            const int sidx = (int)(tile / strip_tiles), rem = (int)(tile - (int64_t)sidx * strip_tiles);
+            const int sw = min(a.strip, a.tiles_x - sidx * a.strip);
+            ty = rem / sw;
+            tx = sidx * a.strip + (rem - ty * sw);
+        }
+        const int r = a.row0 + ty * kTileQ + item % kTileQ;
+        if (r >= a.row_end) continue;
+        for (int j = 0; j < kTileQ; ++j) {
+            const int c = tx * kTileQ + j;
+            if (c >= ncols) break;
+            if (p_next - p_open == kRing) run_batch(qn);   // ring full (S < 3): drain
+            ++n_posts;
+            const uint64_t base = mix_seed(a.seed, (uint64_t)r, (uint64_t)c);
+            const int E = zld(z + (int64_t)r * ncols + c) + a.ht;
+            const int slot = p_next & (kRing - 1);
+            if (lane == slot) { myE = E; myR = r; myC = c; }
+            ++p_next;
+            // ---- draw S receivers (D6) into the FIFO ----
+            int nacc = 0;
+            for (uint64_t k = 0; nacc < a.S; k += 32) {
+                const int v = (int)fm_mod(a.span, sm_draw(base, k + lane)) - a.R;
+                const int dc = __shfl_down_sync(kFull, v, 1);
+                const int dr = v;
+                const bool ok = !(lane & 1) && dr * dr + dc * dc <= R2 && r + dr >= 0 && r + dr < nrows &&
+                                c + dc >= 0 && c + dc < ncols;
+                const unsigned mask = __ballot_sync(kFull, ok);
+                const int take = min(__popc(mask), a.S - nacc);
+                if (ok) {
+                    const int rank = __popc(mask & ((1u << lane) - 1));
+                    if (rank < take) s_q[qn + rank] = (dr + 256) | ((dc + 256) << 9) | (slot << 18);
+                }
+                nacc += take;
+                qn += take;
                 __syncwarp();
-                if (lane < rest) s_q[lane] = t;
-                __syncwarp();
-                qn = rest;
+                if (qn >= 32) run_batch(32);
             }
         }
     }
-    if (qn > 0) run_batch(qn);
-    for (int j = 0; j < kPPW; ++j) {
-        int r, c;
-        post_rc(j, r, c);
-        if (lane == j && r < a.row_end && c < ncols) out[(int64_t)r * ncols + c] = (uint8_t)mycnt;
-    }
+    while (qn > 0) run_batch(min(qn, 32));
     for (int o = 16; o; o >>= 1) n_cross += __shfl_down_sync(kFull, n_cross, o);
     if (lane == 0 && n_posts) {
         atomicAdd(counters + kVixLos, (unsigned long long)n_posts * a.S);
@@ -923,7 +935,14 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         if (const char* e = getenv("TXS_VIX_STRIP")) aq.strip = std::max(1, std::min(aq.tiles_x, atoi(e)));
         const int64_t tiles_q = (int64_t)aq.tiles_x * aq.tiles_y;
         if (tiles_q > 0x7fffffff) return fail(c, TXS_ERR_RANGE, "vix", "grid too large");
-        kq<<<(unsigned)tiles_q, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols,
+        // persistent: as many CTAs as are resident (tiles are pulled in a loop)
+        int per_sm = 0;
+        TXS_CUDA(c, "vix", cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kq, kVixThreads, qsm));
+        int64_t grid_q = std::min<int64_t>(tiles_q, (int64_t)std::max(1, per_sm) * c->num_sms);
+        if (const char* e = getenv("TXS_VIX_GRID")) grid_q = std::min<int64_t>(tiles_q, std::max(1, atoi(e)));
+        TXS_CUDA(c, "vix", cudaMemsetAsync(c->d_counters + kVixNext, 0, sizeof(unsigned long long), c->stream));
+        if (getenv("TXS_VIX_VERBOSE")) fprintf(stderr, "[vix] per_sm %d grid %lld tiles %lld smem %zu\n", per_sm, (long long)grid_q, (long long)tiles_q, qsm);
+        kq<<<(unsigned)grid_q, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols,
                                                                 c->d_vix - c->band_r0 * c->ncols, aq, c->d_gcd, smap,
                                                                 c->d_counters);
         st = TXS_OK;
