@@ -80,7 +80,9 @@ class Engine:
 
     def close(self):
         if getattr(self, "_h", None):
-            N.lib.txs_destroy(self._h)
+            lib = getattr(N, "lib", None)   # None during interpreter teardown
+            if lib is not None:
+                lib.txs_destroy(self._h)
             self._h = None
 
     def __del__(self):

@@ -129,6 +129,8 @@ struct txs_ctx {
     double shard_target = 1.0;           // sharded SITE: stop rules of txs_site_shard_begin
     int64_t shard_max_sel = 0;
     uint64_t* d_cum = nullptr;
+    uint64_t* d_cum_dense = nullptr;     // SPEC-dense staging of txs_get_cumulative
+    size_t cum_dense_cap = 0;
     // per-round delta: newly covered words over the winner window (row pitch
     // dpitch words) and per-row [lo, hi] spans of non-zero words
     uint64_t* d_dwin = nullptr;

@@ -850,13 +850,15 @@ txs_status time_gain_pass(txs_ctx* c, int32_t reps, double* ms, int64_t* bytes) 
 
 txs_status download_cum(txs_ctx* c, uint64_t* host_dense) {
     const int64_t nw = (c->nrows * c->ncols + 63) / 64;
-    uint64_t* dense = nullptr;
-    TXS_CUDA(c, "site", cudaMallocAsync((void**)&dense, sizeof(uint64_t) * nw, c->stream));
+    // persistent staging buffer (a stream-ordered malloc/free per call stalled
+    // the download for up to hundreds of ms when the pool returned its memory)
+    if (ensure(c, "site", (void**)&c->d_cum_dense, &c->cum_dense_cap, sizeof(uint64_t) * (size_t)std::max<int64_t>(1, nw)) != TXS_OK)
+        return TXS_ERR_OUT_OF_MEMORY;
+    uint64_t* dense = c->d_cum_dense;
     k_padded_to_dense<<<blocks_for(nw, 256, c->num_sms * 16), 256, 0, c->stream>>>(
         c->d_cum - c->cum_r0 * c->wpr, dense, c->nrows, c->ncols, c->wpr, c->cum_r0, c->cum_r1);
     TXS_LAUNCHED(c, "site");
     TXS_CUDA(c, "site", cudaMemcpyAsync(host_dense, dense, sizeof(uint64_t) * nw, cudaMemcpyDeviceToHost, c->stream));
-    TXS_CUDA(c, "site", cudaFreeAsync(dense, c->stream));
     TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
     return TXS_OK;
 }

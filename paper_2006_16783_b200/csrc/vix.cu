@@ -867,9 +867,11 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     // HBM -- they beat the shared-memory tile at roi 100 and the column-major
     // copy at roi 200; else the shared-memory tile when two CTAs fit; else the
     // column-major copy.  TXS_VIX_PATH=smem|pairs|zt overrides (measurement).
-    size_t freeb = 0, totalb = 0;
-    cudaMemGetInfo(&freeb, &totalb);
     const size_t qbytes = sizeof(uint2) * (size_t)(2 * c->z_rows * (int64_t)a.wp + 2 * c->ncols * (int64_t)a.hp);
+    // the free-memory query only when the scratch must grow (it can stall the
+    // host inside the timed stage)
+    size_t freeb = 0, totalb = 0;
+    if (p.roi <= 255 && qbytes > c->pairs_cap) cudaMemGetInfo(&freeb, &totalb);
     const bool quads_ok = p.roi <= 255 && (qbytes <= c->pairs_cap || qbytes <= freeb / 2);
     int path = quads_ok ? 1 : (smem <= 110 * 1024 ? 0 : 2);
     if (const char* e = getenv("TXS_VIX_PATH")) {

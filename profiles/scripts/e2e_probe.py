@@ -1,3 +1,5 @@
+"""Per-phase timing of the bench e2e step (device events + host wall clock):
+python profiles/scripts/e2e_probe.py c2 [iters]"""
 import sys, time, ctypes
 sys.path.insert(0, '.')
 import numpy as np, torch
@@ -12,13 +14,19 @@ z_host = torch.empty((cfg.nrows, cfg.ncols), dtype=torch.int16, pin_memory=True)
 z_host[:] = e.terrain()
 nw = (cfg.nrows * cfg.ncols + 63) // 64
 cum_host = torch.empty(nw * 8, dtype=torch.uint8, pin_memory=True).numpy().view(np.uint64)
-for i in range(4):
+for i in range(int(sys.argv[2]) if len(sys.argv) > 2 else 4):
     e.synchronize()
+    t0 = time.perf_counter()
     e.event_record(2); e.set_terrain(z_host); e.event_record(3)
+    t1 = time.perf_counter()
     r = run(e, cfg, p); e.event_record(4)
+    t2 = time.perf_counter()
     e._chk(N.lib.txs_get_cumulative(e.handle, ctypes.c_void_p(cum_host.ctypes.data))); e.event_record(5)
+    t3 = time.perf_counter()
     st = e.stats()
-    print(i, "h2d", round(e.event_elapsed(2, 3), 2), "run", round(e.event_elapsed(3, 4), 2), "cum", round(e.event_elapsed(4, 5), 2), flush=True)
+    sm = {k: round(v, 2) for k, v in r.get("stage_ms", {}).items()}
+    print(i, "h2d", round(e.event_elapsed(2, 3), 2), "run", round(e.event_elapsed(3, 4), 2), "cum", round(e.event_elapsed(4, 5), 2),
+          "wall", round((t1 - t0) * 1e3, 2), round((t2 - t1) * 1e3, 2), round((t3 - t2) * 1e3, 2), "stages", sm, flush=True)
     e.reset_stats()
 for i in range(2):
     e.event_record(3); r = run(e, cfg, p); e.event_record(4)
