@@ -139,6 +139,21 @@ def test_vix_skip_map_matches_full_walk(engine, monkeypatch, nr, nc, rough, zmin
         assert np.array_equal(skip[rb:re], o[rb:re]), rb
 
 
+@pytest.mark.parametrize("samples", [1, 2, 3, 64])
+def test_vix_sample_counts_queue_paths(engine, monkeypatch, samples):
+    """Receiver-queue bookkeeping of the quad path: S = 1 and 2 fill the
+    16-post ring (drained with partial batches), S = 3 just fits it, S = 64
+    spreads each post over several 32-segment batches."""
+    T = _T()
+    z = O.generate_fractal(90, 77, 0.6, 13, 0, 2000)
+    engine.set_terrain(z)
+    monkeypatch.setenv("TXS_VIX_PATH", "pairs")
+    p = T.make_params(30, 5, 5, samples=samples, seed=17)
+    g = engine.estimate_vix(p)
+    o = O.estimate_vix(z, 30, 5, 5, samples, 17)
+    assert np.array_equal(g, o), int((g != o).sum())
+
+
 def test_vix_flat_and_tiny(engine):
     T = _T()
     engine.set_terrain(np.full((70, 45), 3, np.int16))
