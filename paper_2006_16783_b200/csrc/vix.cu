@@ -412,9 +412,9 @@ __device__ __forceinline__ int dp2hi(uint32_t pair, uint32_t w) {
 // 2^16 m/M)/2^16 < 255/2^16 < 1/M cannot carry past the next integer).
 struct __align__(16) QuadGeomC {   // skip test
     int soff;         // skip-map entry of the start post's block (padded block indices)
-    int LE2;          // Es*M + min(0, 4D)  (Es = LOS height at the start post, D = LOS rise)
-    int D4;           // 4D
-    int w;            // M | c0 << 8 | tr << 11 | mneg << 12 | mag << 13   (M = 0: nothing to walk)
+    int LE2;          // Es*M + min(0, G D)  (Es = LOS height at the start post, D = LOS rise, G = group steps)
+    int DG;           // G D
+    int w;            // M | c0 << 8 | tr << 13 | mneg << 14 | mag << 15   (M = 0: nothing to walk)
 };
 struct __align__(16) QuadGeomF {   // exact walk
     const uint2* Q;   // start post's entry in its plane
@@ -440,18 +440,19 @@ struct QuadPitch {
 // Full walk: one segment per warp, lane l taking major steps l+1, l+33, ...;
 // a vote after every 32 steps.  Returns true (uniform) iff the segment is
 // blocked.  (TXS_VIX_SKIP=0: every step of every segment is evaluated.)
+template <int GS>
 __device__ __forceinline__ bool quad_walk(const QuadGeom* gp, int lane) {
     const QuadGeomC c = gp->c;
     const int nM = c.w & 0xff, steps = nM - 1;
     if (steps <= 0) return false;
     const QuadGeomF f = gp->f;
-    const int nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 13, D = c.D4 >> 2;
+    const int nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 15, D = c.DG >> GS;
     const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
     const int q32 = (32 * mag) >> 16, r32 = 32 * nm - q32 * nM;
     int i = 1 + lane;
     int q = (i * mag) >> 16, r = i * nm - q * nM;
     int off = i + q * sm;
-    int rhsM = c.LE2 - min(0, c.D4) + i * D, rhsm = f.Es * nm + q * D;
+    int rhsM = c.LE2 - min(0, c.DG) + i * D, rhsm = f.Es * nm + q * D;
     const int dOff = 32 + q32 * sm, dRhsM = 32 * D, dRhsm = q32 * D;
     for (int k = steps >> 5; k; --k) {
         if (__any_sync(kFull, quad_test(qld(f.Q + off), r, nm, wb, rhsM, rhsm))) return true;
@@ -466,53 +467,54 @@ __device__ __forceinline__ bool quad_walk(const QuadGeom* gp, int lane) {
 }
 
 // Hierarchical walk with a conservative skip test (exact: it only ever skips
-// steps that cannot block).  Steps are taken in groups of 4: group g holds
-// major steps 4g+1..4g+4, whose crossings lie at t in (4g/M, (4g+4)/M] and use
-// posts with major offsets 4g..4g+4 and minor offsets q(4g+1)..q(4g+1)+4 -- a
-// 5x5 window, so inside the 8x8 posts of two-by-two 4x4 blocks at the window's
-// corner block.  The skip map holds, per block corner, the maximum elevation of
-// those 8x8 posts (k_skipmap).  The interpolated terrain at any crossing of the
-// group is at most that maximum, and the LOS over the group is at least its
-// value at one end, so
-//     smax * M  <=  Es*M + 4g*D + min(0, 4D)  =  LE2 + g*D4
+// steps that cannot block).  Steps are taken in groups of G = 2^GS (4 or 16):
+// group g holds major steps Gg+1..Gg+G, whose crossings lie at t in (Gg/M,
+// (Gg+G)/M] and use posts with major offsets Gg..Gg+G and minor offsets
+// q(Gg+1)..q(Gg+1)+G -- a (G+1)x(G+1) window, so inside the 2G x 2G posts of
+// two-by-two GxG blocks at the window's corner block.  The skip map holds, per
+// block corner, the maximum elevation of those 2G x 2G posts (k_skipmap).  The
+// interpolated terrain at any crossing of the group is at most that maximum,
+// and the LOS over the group is at least its value at one end, so
+//     smax * M  <=  Es*M + Gg*D + min(0, G D)  =  LE2 + g*DG
 // proves that no crossing of the group is blocked.  The window's minor corner
-// block, relative to the start post's, is mb = (c0 + q(4g+1)) >> 2 for a
-// positive minor direction (c0 = the start post's minor offset in its block),
-// and -((c0 + q(4g+1)) >> 2) for a negative one (c0 = 7 - that offset), so the
-// map index is soff + g + ((c0 + q(4g+1)) >> 2) * ssp with a signed pitch ssp.
+// block, relative to the start post's, is (c0 + q(Gg+1)) >> GS for a positive
+// minor direction (c0 = the start post's minor offset in its block) and
+// -((c0 + q(Gg+1)) >> GS) for a negative one (c0 = 2G-1 - that offset), so the
+// map index is soff + g + ((c0 + q(Gg+1)) >> GS) * ssp with a signed pitch ssp.
 //
 // Sequential form (TXS_VIX_SKIP=2): one segment per warp pass, lane l testing
 // group 32k+l, failing groups walked in order with an exit at the first block.
+template <int GS>
 __device__ __forceinline__ bool quad_walk_skip(const QuadGeom* gp, const QuadPitch& P, const int16_t* __restrict__ smap,
                                                int* s_fail, int lane) {
     const QuadGeomC c = gp->c;
     const int nM = c.w & 0xff, steps = nM - 1;
     if (steps <= 0) return false;
-    const int mag = (unsigned)c.w >> 13, mag4 = mag << 2, c0 = (c.w >> 8) & 7;
-    const int sp = (c.w & 0x800) ? P.pt : P.pv, ssp = (c.w & 0x1000) ? -sp : sp;
-    const int ngroups = (steps + 3) >> 2;
+    const int mag = (unsigned)c.w >> 15, magG = mag << GS, c0 = (c.w >> 8) & 31;
+    const int sp = (c.w & 0x2000) ? P.pt : P.pv, ssp = (c.w & 0x4000) ? -sp : sp;
+    const int ngroups = (steps + (1 << GS) - 1) >> GS;
     const int16_t* S = smap + c.soff;
     for (int g0 = 0; g0 < ngroups; g0 += 32) {
         const int gi = g0 + lane;
         bool fail = false;
         if (gi < ngroups) {
-            const int q1 = (gi * mag4 + mag) >> 16;
-            const int smax = __ldg(S + gi + ((c0 + q1) >> 2) * ssp);
-            fail = smax * nM > c.LE2 + gi * c.D4;
+            const int q1 = (gi * magG + mag) >> 16;
+            const int smax = __ldg(S + gi + ((c0 + q1) >> GS) * ssp);
+            fail = smax * nM > c.LE2 + gi * c.DG;
         }
         const unsigned F = __ballot_sync(kFull, fail);
         if (!F) continue;
         if (fail) s_fail[__popc(F & ((1u << lane) - 1))] = gi;
         __syncwarp();
         const QuadGeomF f = gp->f;
-        const int nm = f.msm & 0xff, sm = f.msm >> 8, D = c.D4 >> 2, LE = c.LE2 - min(0, c.D4);
+        const int nm = f.msm & 0xff, sm = f.msm >> 8, D = c.DG >> GS, LE = c.LE2 - min(0, c.DG);
         const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
         const int cnt = __popc(F);
-        for (int j = 0; j < cnt; j += 8) {
-            const int sub = j + (lane >> 2);
+        for (int j = 0; j < cnt; j += 32 >> GS) {   // 32/G groups x G steps per pass
+            const int sub = j + (lane >> GS);
             bool b = false;
             if (sub < cnt) {
-                const int i = 4 * s_fail[sub] + 1 + (lane & 3);
+                const int i = (s_fail[sub] << GS) + 1 + (lane & ((1 << GS) - 1));
                 if (i <= steps) {
                     const int q = (i * mag) >> 16, r = i * nm - q * nM;
                     b = quad_test(qld(f.Q + i + q * sm), r, nm, wb, LE + i * D, f.Es * nm + q * D);
@@ -534,11 +536,11 @@ __device__ __forceinline__ bool quad_walk_skip(const QuadGeom* gp, const QuadPit
 // consecutive steps (coalesced plane loads, the predicates of quad_test), in
 // (segment, unit) order, skipping segments already found blocked.  Returns
 // the mask of lanes whose segment is visible.
-template <int U>
+template <int U, int GS>
 __device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int lane, QuadGeom* s_geo, int* s_pre,
                                                int* s_fail, const int16_t* __restrict__ smap, const QuadPitch& P) {
     const int nMl = g.c.w & 0xff;
-    const int ng = (lane < ns && nMl >= 2) ? (nMl + 2) >> 2 : 0;   // ceil((M-1)/4) groups
+    const int ng = (lane < ns && nMl >= 2) ? (nMl + (1 << GS) - 2) >> GS : 0;   // ceil((M-1)/G) groups
     const int nu = (ng + U - 1) / U;
     const unsigned nz = __ballot_sync(kFull, ng > 0);
     int inc = nu;
@@ -551,8 +553,8 @@ __device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int la
     if (ng > 0) {   // compacted: segments with groups, in lane order; prefixes strictly increase
         const int slot = __popc(nz & ((1u << lane) - 1));
         s_geo[slot] = g;
-        const int sp = (g.c.w & 0x800) ? P.pt : P.pv;
-        s_pre[slot] = (inc - nu) | (((g.c.w & 0x1000) ? -sp : sp) << 16);   // unit prefix | signed map pitch
+        const int sp = (g.c.w & 0x2000) ? P.pt : P.pv;
+        s_pre[slot] = (inc - nu) | (((g.c.w & 0x4000) ? -sp : sp) << 16);   // unit prefix | signed map pitch
     }
     __syncwarp();
     const int myp = lane < __popc(nz) ? s_pre[lane] & 0xffff : 0x7fffffff;
@@ -568,20 +570,20 @@ __device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int la
         if (p < T && !((blk >> sl) & 1u)) {   // pairs of segments already blocked are dropped
             const int ps = s_pre[sl];
             const QuadGeomC c = s_geo[sl].c;
-            const int nM = c.w & 0xff, mag = (unsigned)c.w >> 13, c0 = (c.w >> 8) & 7, ssp = ps >> 16;
-            const int ngs = (nM + 2) >> 2;
+            const int nM = c.w & 0xff, mag = (unsigned)c.w >> 15, c0 = (c.w >> 8) & 31, ssp = ps >> 16;
+            const int ngs = (nM + (1 << GS) - 2) >> GS;
             ui = p - (ps & 0xffff);
             const int g0 = ui * U;
             const int16_t* S = smap + c.soff;
-            int q1 = (g0 * (mag << 2) + mag) >> 16;
+            int q1 = (g0 * (mag << GS) + mag) >> 16;
 #pragma unroll
             for (int k = 0; k < U; ++k) {
                 const int gi = g0 + k;
                 if (k == 0 || gi < ngs) {
-                    const int smax = __ldg(S + gi + ((c0 + q1) >> 2) * ssp);
-                    fail |= smax * nM > c.LE2 + gi * c.D4;
+                    const int smax = __ldg(S + gi + ((c0 + q1) >> GS) * ssp);
+                    fail |= smax * nM > c.LE2 + gi * c.DG;
                 }
-                q1 = ((gi + 1) * (mag << 2) + mag) >> 16;
+                q1 = ((gi + 1) * (mag << GS) + mag) >> 16;
             }
         }
         const unsigned F = __ballot_sync(kFull, fail);
@@ -596,14 +598,14 @@ __device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int la
             const QuadGeomC c = s_geo[sf].c;
             const QuadGeomF f = s_geo[sf].f;
             const int nM = c.w & 0xff;
-            // 32 steps from the unit's first (a unit of U < 8 groups is walked with its successor)
-            const int i = 4 * U * (e >> 8) + 1 + lane;
+            // 32 steps from the unit's first (a unit of U G < 32 steps is walked with its successor)
+            const int i = ((U * (e >> 8)) << GS) + 1 + lane;
             bool b = false;
             if (i < nM) {
-                const int nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 13, D = c.D4 >> 2;
+                const int nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 15, D = c.DG >> GS;
                 const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
                 const int q = (i * mag) >> 16, r = i * nm - q * nM;
-                b = quad_test(qld(f.Q + i + q * sm), r, nm, wb, c.LE2 - min(0, c.D4) + i * D, f.Es * nm + q * D);
+                b = quad_test(qld(f.Q + i + q * sm), r, nm, wb, c.LE2 - min(0, c.DG) + i * D, f.Es * nm + q * D);
             }
             if (__any_sync(kFull, b)) blk |= 1u << sf;
         }
@@ -614,7 +616,7 @@ __device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int la
     return __ballot_sync(kFull, lane < ns && (ng == 0 || !((blk >> slot) & 1u)));
 }
 
-template <int SKIP, int U>
+template <int SKIP, int U, int GS>
 __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16_t* __restrict__ z,
                                                                    const uint2* __restrict__ qp, int nrows, int ncols,
                                                                    uint8_t* __restrict__ out, VixArgs a,
@@ -674,23 +676,25 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
             // SV row-major for column-major walks, ST column-major for row-major ones
             const int maj = tr ? y : x, mnr = tr ? x : y;
             const int mag = nM ? (nm * 65536 + nM - 1) / nM : 0;
-            g.c.soff = tr ? a.st_off + ((maj >> 2) + 1) + ((mnr >> 2) + 1) * a.pt
-                          : ((maj >> 2) + 1) + ((mnr >> 2) + 1) * a.pv;
+            g.c.soff = tr ? a.st_off + ((maj >> GS) + 1) + ((mnr >> GS) + 1) * a.pt
+                          : ((maj >> GS) + 1) + ((mnr >> GS) + 1) * a.pv;
             const int D = rev ? E - Zt : Zt - E;
-            g.c.LE2 = Es * nM + min(0, 4 * D);
-            g.c.D4 = 4 * D;
-            g.c.w = nM | ((mneg ? 7 - (mnr & 3) : (mnr & 3)) << 8) | ((int)tr << 11) | ((int)mneg << 12) | (mag << 13);
+            constexpr int G = 1 << GS;
+            g.c.LE2 = Es * nM + min(0, G * D);
+            g.c.DG = G * D;
+            const int mo = mnr & (G - 1);
+            g.c.w = nM | ((mneg ? 2 * G - 1 - mo : mo) << 8) | ((int)tr << 13) | ((int)mneg << 14) | (mag << 15);
         }
         __syncwarp();
         unsigned vism;
         if (SKIP == 1) {
-            vism = batch_skip<U>(g, ns, lane, s_geo, s_pre, s_fail, smap, PQ);
+            vism = batch_skip<U, GS>(g, ns, lane, s_geo, s_pre, s_fail, smap, PQ);
         } else {
             s_geo[lane] = g;
             __syncwarp();
             bool vis = false;
             for (int sidx = 0; sidx < ns; ++sidx) {
-                const bool blk = SKIP == 2 ? quad_walk_skip(s_geo + sidx, PQ, smap, s_fail, lane) : quad_walk(s_geo + sidx, lane);
+                const bool blk = SKIP == 2 ? quad_walk_skip<GS>(s_geo + sidx, PQ, smap, s_fail, lane) : quad_walk<GS>(s_geo + sidx, lane);
                 if (lane == sidx) vis = !blk;
             }
             vism = __ballot_sync(kFull, vis);
@@ -773,21 +777,21 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
     }
 }
 
-// Skip map of quad_walk_skip.  Pass 1: per 4x4 block the maximum elevation,
+// Skip map of the skip tests.  Pass 1: per GxG block the maximum elevation,
 // stored with one block of padding on every side (padded index = block + 1;
 // padding blocks hold no posts: -32768).  Pass 2: per padded block corner
-// (pr, pc) the maximum of blocks pr..pr+1 x pc..pc+1 -- the 8x8 posts from
-// post (4(pr-1), 4(pc-1)) -- written row-major (SV) and column-major (ST) so
+// (pr, pc) the maximum of blocks pr..pr+1 x pc..pc+1 -- the 2G x 2G posts from
+// post (G(pr-1), G(pc-1)) -- written row-major (SV) and column-major (ST) so
 // that lanes stepping along a walk's major axis read consecutive entries.
-__global__ void k_blockmax(const int16_t* __restrict__ z, int H, int W, int16_t* __restrict__ bp, int Hb, int Wb) {
+__global__ void k_blockmax(const int16_t* __restrict__ z, int H, int W, int16_t* __restrict__ bp, int Hb, int Wb, int G) {
     const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (idx >= (int64_t)(Hb + 2) * (Wb + 2)) return;
     const int pr = (int)(idx / (Wb + 2)), pc = (int)(idx - (int64_t)pr * (Wb + 2));
     const int br = pr - 1, bc = pc - 1;
     int m = -32768;
     if (br >= 0 && br < Hb && bc >= 0 && bc < Wb) {
-        for (int y = 4 * br; y < min(4 * br + 4, H); ++y)
-            for (int x = 4 * bc; x < min(4 * bc + 4, W); ++x) m = max(m, (int)z[(int64_t)y * W + x]);
+        for (int y = G * br; y < min(G * br + G, H); ++y)
+            for (int x = G * bc; x < min(G * bc + G, W); ++x) m = max(m, (int)z[(int64_t)y * W + x]);
     }
     bp[idx] = (int16_t)m;
 }
@@ -884,8 +888,15 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         st = go(k_vix<true, 1>, smem);
     } else if (path == 1) {
         const int64_t n = c->z_rows * c->ncols, nq = 2 * c->z_rows * (int64_t)a.wp + 2 * c->ncols * (int64_t)a.hp;
+        // skip-test group size G = 2^gs (measured, profiles/README.md): 16 at roi < 150,
+        // where the smooth C3/C4 terrain passes 16-step tests 99.97 % of the time
+        // (one map load per 16 steps), 4 at roi >= 150 (C2: 59 % of 16-step groups
+        // fail, 19 % of 4-step ones); TXS_VIX_GROUP=4|16 overrides
+        int gs = p.roi >= 150 ? 2 : 4;
+        if (const char* e = getenv("TXS_VIX_GROUP")) gs = atoi(e) >= 16 ? 4 : 2;
+        const int G = 1 << gs;
         // skip map (k_skipmap) behind the quad planes: SV, ST, then the block maxima
-        const int Hb = (int)((c->z_rows + 3) / 4), Wb = (int)((c->ncols + 3) / 4);
+        const int Hb = (int)((c->z_rows + G - 1) / G), Wb = (int)((c->ncols + G - 1) / G);
         a.pv = ((Wb + 1) + 7) & ~7;
         a.pt = ((Hb + 1) + 7) & ~7;
         const int64_t nsv = (int64_t)(Hb + 1) * a.pv, nst = (int64_t)(Wb + 1) * a.pt;
@@ -910,7 +921,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         int16_t* smap = skip ? (int16_t*)((uint2*)c->d_pairs + nq) : nullptr;
         if (skip) {
             int16_t* bp = smap + nsv + nst;
-            k_blockmax<<<(unsigned)((nbp + 255) / 256), 256, 0, c->stream>>>(c->d_z, (int)c->z_rows, (int)c->ncols, bp, Hb, Wb);
+            k_blockmax<<<(unsigned)((nbp + 255) / 256), 256, 0, c->stream>>>(c->d_z, (int)c->z_rows, (int)c->ncols, bp, Hb, Wb, G);
             TXS_LAUNCHED(c, "vix");
             const int64_t ns = (int64_t)(Hb + 1) * (Wb + 1);
             k_skipmap<<<(unsigned)((ns + 255) / 256), 256, 0, c->stream>>>(bp, Hb, Wb, smap, a.pv, smap + nsv, a.pt);
@@ -921,8 +932,18 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         const size_t qsm = (sizeof(QuadGeom) * 32 + sizeof(int) * (32 + 32 + 64)) * kVixWarps;
         // groups per skip unit (measured, profiles/README.md): 8 at roi 200 (C2 46.6 -> 43.5 ms
         // vs 4), 4 at roi 100 (C3 190.6 -> 180.2 vs 8)
-        const bool u8 = p.roi >= 150;
-        auto kq = skip == 1 ? (u8 ? k_vix_quads<1, 8> : k_vix_quads<1, 4>) : skip == 2 ? k_vix_quads<2, 8> : k_vix_quads<0, 8>;
+        // G = 16: units of 2 groups (32 steps, TXS_VIX_UNIT=1 for 16)
+        int unit = gs == 4 ? 2 : (p.roi >= 150 ? 8 : 4);
+        if (const char* e = getenv("TXS_VIX_UNIT")) unit = atoi(e);
+        decltype(&k_vix_quads<1, 8, 2>) kq;
+        if (skip == 1) {
+            if (gs == 4) kq = unit == 1 ? k_vix_quads<1, 1, 4> : k_vix_quads<1, 2, 4>;
+            else kq = unit == 8 ? k_vix_quads<1, 8, 2> : k_vix_quads<1, 4, 2>;
+        } else if (skip == 2) {
+            kq = gs == 4 ? k_vix_quads<2, 8, 4> : k_vix_quads<2, 8, 2>;
+        } else {
+            kq = gs == 4 ? k_vix_quads<0, 8, 4> : k_vix_quads<0, 8, 2>;
+        }
         if (qsm > 48 * 1024)
             TXS_CUDA(c, "vix", cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm));
         if (!c->d_gcd) {

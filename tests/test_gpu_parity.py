@@ -130,10 +130,19 @@ def test_vix_skip_map_matches_full_walk(engine, monkeypatch, nr, nc, rough, zmin
     monkeypatch.setenv("TXS_VIX_PATH", "pairs")
     monkeypatch.setenv("TXS_VIX_SKIP", "0")
     full = engine.estimate_vix(p)
-    for mode in ("2", "1"):   # per-segment, flattened (default)
+    # per-segment / flattened (default) skip tests, 4- and 16-step groups, every unit size
+    for mode, group, unit in [("2", "4", ""), ("2", "16", ""), ("1", "4", "4"), ("1", "4", "8"),
+                              ("1", "16", "1"), ("1", "16", "2")]:
         monkeypatch.setenv("TXS_VIX_SKIP", mode)
+        monkeypatch.setenv("TXS_VIX_GROUP", group)
+        monkeypatch.setenv("TXS_VIX_UNIT", unit or "8")
         skip = engine.estimate_vix(p)
-        assert np.array_equal(full, skip), (mode, int((full != skip).sum()))
+        assert np.array_equal(full, skip), (mode, group, unit, int((full != skip).sum()))
+    monkeypatch.delenv("TXS_VIX_GROUP")
+    monkeypatch.delenv("TXS_VIX_UNIT")
+    monkeypatch.setenv("TXS_VIX_SKIP", "1")
+    skip = engine.estimate_vix(p)   # the defaults
+    assert np.array_equal(full, skip)
     for rb, re in [(0, 3), (nr - 3, nr)]:
         o = O.estimate_vix(z, roi, ht, hr, samples, 9, rows=(rb, re))
         assert np.array_equal(skip[rb:re], o[rb:re]), rb
