@@ -424,7 +424,7 @@ struct __align__(16) QuadGeomF {   // exact walk
 struct QuadGeom { QuadGeomC c; QuadGeomF f; };
 
 #ifndef VIX_MINB
-#define VIX_MINB 4    // CTAs per SM: 64 warps hide the L2 latency of the plane loads
+#define VIX_MINB 2    // CTAs per SM: 64 registers, no spills (measured: 4 / 3 / 2 / 1 -> c2 43.1 / 42.0 / 38.8 / 57.1 ms, c3 144.3 / 137.9 / 126.1 / 150.8)
 #endif
 
 __device__ __forceinline__ bool quad_test(uint2 v, int r, int nm, uint32_t wb, int rhsM, int rhsm) {
@@ -539,6 +539,7 @@ __device__ __forceinline__ bool quad_walk_skip(const QuadGeom* gp, const QuadPit
 template <int U, int GS>
 __device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int lane, QuadGeom* s_geo, int* s_pre,
                                                int* s_fail, const int16_t* __restrict__ smap, const QuadPitch& P) {
+    static_assert((U << GS) <= 32, "a failing unit is walked by one 32-step pass");
     const int nMl = g.c.w & 0xff;
     const int ng = (lane < ns && nMl >= 2) ? (nMl + (1 << GS) - 2) >> GS : 0;   // ceil((M-1)/G) groups
     const int nu = (ng + U - 1) / U;
