@@ -688,7 +688,7 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
         }
         __syncwarp();
         unsigned vism;
-        if (SKIP == 1) {
+        if constexpr (SKIP == 1) {
             vism = batch_skip<U, GS>(g, ns, lane, s_geo, s_pre, s_fail, smap, PQ);
         } else {
             s_geo[lane] = g;
