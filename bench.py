@@ -506,8 +506,8 @@ def run_b200_sharded(args, cfg):
             "data": "synthetic (seeded diamond-square terrain, BASELINE shapes)",
             "config": {"workload": cfg.name, "nrows": cfg.nrows, "ncols": cfg.ncols, "roi": cfg.roi,
                        "sited": int(len(res["index"])), "stop": res["stop"],
-                       "parallelism": f"rowband{world} (halo roi+1; SITE rounds device-resident, two "
-                                      f"stream-ordered NCCL allreduces per round, {res.get('rounds_mode')})",
+                       "parallelism": f"rowband{world} (halo roi+1; SITE rounds device-resident, "
+                                      f"stream-ordered NCCL: {res.get('exchange')}, {res.get('rounds_mode')})",
                        "l2": "flushed between steps (256 MB write outside the timed events)"},
             "e2e": {"value": round(e2e / 1e3, 5), "unit": "s", "h2d_bytes_per_step": cfg.posts * 2,
                     "d2h_bytes_per_step": ((cfg.posts + 63) // 64) * 8 + len(r2["index"]) * 32},

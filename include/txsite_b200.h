@@ -214,6 +214,20 @@ txs_status txs_site_shard_export_dev(txs_ctx* ctx, const uint64_t* d_key, uint64
 txs_status txs_site_shard_apply_dev(txs_ctx* ctx, const uint64_t* d_key, const uint64_t* d_payload,
                                     int64_t total_candidates);
 int64_t txs_site_shard_payload_words(const txs_ctx* ctx);
+/* One-collective form of the same round (one allgather instead of the two
+ * allreduces above):
+ *   txs_site_shard_best_dev
+ *   txs_site_shard_export_keyed_dev  d_out[0] = d_key[0] (this rank's best key),
+ *                                    d_out[1..] = that candidate's payload
+ *                                    (1 + txs_site_shard_payload_words() u64)
+ *   -- caller: allgather of d_out over the ranks, rank-major --
+ *   txs_site_shard_select_dev        d_key / d_payload = the entry with the largest
+ *                                    key (gain desc, global id asc: the allreduce(MAX)
+ *                                    winner), its payload
+ *   txs_site_shard_apply_dev */
+txs_status txs_site_shard_export_keyed_dev(txs_ctx* ctx, const uint64_t* d_key, uint64_t* d_out);
+txs_status txs_site_shard_select_dev(txs_ctx* ctx, const uint64_t* d_gathered, int32_t nranks, uint64_t* d_key,
+                                     uint64_t* d_payload);
 txs_status txs_site_shard_result(txs_ctx* ctx, txs_step* steps, int64_t cap, int64_t* nsteps, int32_t* stop_reason);
 /* The context's CUDA stream (a cudaStream_t), for ordering external work with it. */
 void* txs_stream(txs_ctx* ctx);

@@ -266,6 +266,13 @@ class Engine:
     def site_shard_apply_dev(self, d_key, d_payload, total_candidates):
         self._chk(N.lib.txs_site_shard_apply_dev(self._h, C.c_void_p(d_key), C.c_void_p(d_payload), total_candidates))
 
+    def site_shard_export_keyed_dev(self, d_key, d_out):
+        self._chk(N.lib.txs_site_shard_export_keyed_dev(self._h, C.c_void_p(d_key), C.c_void_p(d_out)))
+
+    def site_shard_select_dev(self, d_gathered, nranks, d_key, d_payload):
+        self._chk(N.lib.txs_site_shard_select_dev(self._h, C.c_void_p(d_gathered), nranks, C.c_void_p(d_key),
+                                                  C.c_void_p(d_payload)))
+
     def site_shard_payload_words(self):
         return int(N.lib.txs_site_shard_payload_words(self._h))
 

@@ -772,6 +772,22 @@ txs_status txs_site_shard_apply_dev(txs_ctx* c, const uint64_t* d_key, const uin
 
 int64_t txs_site_shard_payload_words(const txs_ctx* c) { return c ? shard_payload_words(c) : 0; }
 
+txs_status txs_site_shard_export_keyed_dev(txs_ctx* c, const uint64_t* d_key, uint64_t* d_out) {
+    if (!c || !d_key || !d_out) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->site_valid) return fail(c, TXS_ERR_STATE, "site", "call txs_site_shard_begin first");
+    cudaSetDevice(c->device);
+    TXS_CUDA(c, "site", cudaMemcpyAsync(d_out, d_key, sizeof(uint64_t), cudaMemcpyDeviceToDevice, c->stream));
+    return shard_site_export_dev(c, d_key, d_out + 1);
+}
+
+txs_status txs_site_shard_select_dev(txs_ctx* c, const uint64_t* d_gathered, int32_t nranks, uint64_t* d_key,
+                                     uint64_t* d_payload) {
+    if (!c || !d_gathered || nranks < 1 || !d_key || !d_payload) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->site_valid) return fail(c, TXS_ERR_STATE, "site", "call txs_site_shard_begin first");
+    cudaSetDevice(c->device);
+    return shard_site_select_dev(c, d_gathered, nranks, d_key, d_payload);
+}
+
 txs_status txs_site_shard_result(txs_ctx* c, txs_step* steps, int64_t cap, int64_t* nsteps, int32_t* stop) {
     if (!c || !nsteps || !stop || (cap > 0 && !steps)) return TXS_ERR_INVALID_ARGUMENT;
     if (!c->site_valid) return fail(c, TXS_ERR_STATE, "site", "call txs_site_shard_begin first");

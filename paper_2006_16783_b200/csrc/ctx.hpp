@@ -206,6 +206,8 @@ txs_status shard_site_best_dev(txs_ctx*, uint64_t* d_key);
 txs_status shard_site_export_dev(txs_ctx*, const uint64_t* d_key, uint64_t* d_payload);
 txs_status shard_site_apply_dev(txs_ctx*, const uint64_t* d_key, const uint64_t* d_payload, int64_t total);
 int64_t shard_payload_words(const txs_ctx*);
+txs_status shard_site_select_dev(txs_ctx*, const uint64_t* d_gathered, int32_t nranks, uint64_t* d_key,
+                                 uint64_t* d_payload);
 
 }  // namespace txs
 

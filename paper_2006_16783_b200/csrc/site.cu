@@ -1111,6 +1111,31 @@ txs_status shard_site_apply(txs_ctx* c, int32_t row, int32_t col, const txs_wind
 
 int64_t shard_payload_words(const txs_ctx* c) { return 6 + aligned_stride(c->vs_roi); }
 
+// The gathered {key, payload} entries of every rank: the largest key (the
+// allreduce(MAX) winner) and its payload, copied for txs_site_shard_apply_dev.
+__global__ void k_shard_select_dev(const uint64_t* __restrict__ g, int nranks, int64_t pw,
+                                   unsigned long long* __restrict__ key, uint64_t* __restrict__ payload) {
+    __shared__ int s_best;
+    if (threadIdx.x == 0) {
+        int b = 0;
+        for (int k = 1; k < nranks; ++k)
+            if (g[(int64_t)k * (pw + 1)] > g[(int64_t)b * (pw + 1)]) b = k;
+        s_best = b;
+        *key = g[(int64_t)b * (pw + 1)];
+    }
+    __syncthreads();
+    const uint64_t* src = g + (int64_t)s_best * (pw + 1) + 1;
+    for (int64_t t = threadIdx.x; t < pw; t += blockDim.x) payload[t] = src[t];
+}
+
+txs_status shard_site_select_dev(txs_ctx* c, const uint64_t* d_gathered, int32_t nranks, uint64_t* d_key,
+                                 uint64_t* d_payload) {
+    k_shard_select_dev<<<1, 256, 0, c->stream>>>(d_gathered, nranks, shard_payload_words(c),
+                                                 (unsigned long long*)d_key, d_payload);
+    TXS_LAUNCHED(c, "site");
+    return TXS_OK;
+}
+
 txs_status shard_site_best_dev(txs_ctx* c, uint64_t* d_key) {
     const int64_t n = c->vs_n;
     TXS_CUDA(c, "site", cudaMemsetAsync(d_key, 0, sizeof(uint64_t), c->stream));

@@ -5,18 +5,23 @@ band +- (roi+1) rows.  VIX, FINDMAX and VIEWSHED run independently per rank
 (no data-path collective).  Global candidate ids are the exclusive prefix of
 the per-band counts plus the local index, which reproduces single-GPU block
 order.  SITE is the one exchange: every round each rank
-reports its best (gain << 32 | ~gid) key, the max is reduced across ranks
-(allreduce MAX), the owner of the winner contributes its window and packed
+reports its best (gain << 32 | ~gid) key.  Host rounds reduce the keys
+(allreduce MAX) and the owner of the winner contributes its window and packed
 words to an allreduce SUM that every other rank feeds zeros into (a broadcast
-whose root is data-dependent), and every rank ORs the window into its held
-cumulative rows and updates its local gains.  Stop rules (decision D9) are
-evaluated identically on every rank from the reduced key.
+whose root is data-dependent).  Device rounds use one collective instead: each
+rank contributes {its best key, that candidate's window and words}, one
+allgather delivers every rank's entry, and each rank selects the largest key
+(TXS_SHARD_EXCHANGE=reduce keeps the two-allreduce form).  Every rank then ORs
+the window into its held cumulative rows and updates its local gains.  Stop
+rules (decision D9) are evaluated identically on every rank from that key.
 
 `ranks` is the list of (engine, band index) pairs this process drives: one per
 process with TorchComm over NCCL (one GPU each), or several on one device with
 LocalComm (the single-GPU emulation the tests use).  An "engine" is anything
 with the shard methods of paper_2006_16783_b200.Engine.
 """
+import os
+
 import numpy as np
 
 STOP_TARGET, STOP_ZERO, STOP_EXHAUSTED, STOP_MAX = "target-reached", "zero-gain", "exhausted", "max-selected"
@@ -56,6 +61,15 @@ class LocalComm:
 
     def sum_dev(self, tensors, engines):
         return self._reduce_dev(tensors, engines, "sum")
+
+    def allgather_dev(self, sends, recvs, engines):
+        import torch
+        for e in engines:
+            e.synchronize()
+        cat = torch.cat(sends)
+        for r in recvs:
+            r.copy_(cat)
+        torch.cuda.synchronize()
 
     @staticmethod
     def _reduce_dev(tensors, engines, op):
@@ -106,6 +120,11 @@ class TorchComm:
 
     def sum_dev(self, tensors, engines):
         self._on_stream(tensors[0], engines[0], self.dist.ReduceOp.SUM)
+
+    def allgather_dev(self, sends, recvs, engines):
+        s = self.torch.cuda.ExternalStream(engines[0].stream(), device=sends[0].device)
+        with self.torch.cuda.stream(s):
+            self.dist.all_gather_into_tensor(recvs[0], sends[0])
 
     def _on_stream(self, t, eng, op):
         s = self.torch.cuda.ExternalStream(eng.stream(), device=t.device)
@@ -257,9 +276,25 @@ def _device_rounds(active, comm, total_cand, poll_every=16):
     dev = torch.device("cuda", torch.cuda.current_device())
     keys = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in engines]
     pays = [torch.zeros(pw, dtype=torch.int64, device=dev) for _ in engines]
+    nranks = getattr(comm, "world", 1) if len(engines) == 1 else len(engines)
+    sends = [torch.zeros(pw + 1, dtype=torch.int64, device=dev) for _ in engines]
+    recvs = [torch.zeros(nranks * (pw + 1), dtype=torch.int64, device=dev) for _ in engines]
     torch.cuda.synchronize()
 
-    def one_round():
+    def round_gather():
+        # one collective: every rank contributes {its best key, that candidate's
+        # payload}; the largest key among the gathered entries is the winner
+        for e, k, sd in zip(engines, keys, sends):
+            e.site_shard_best_dev(k.data_ptr())
+            e.site_shard_export_keyed_dev(k.data_ptr(), sd.data_ptr())
+        comm.allgather_dev(sends, recvs, engines)
+        for e, k, p, rv in zip(engines, keys, pays, recvs):
+            e.site_shard_select_dev(rv.data_ptr(), nranks, k.data_ptr(), p.data_ptr())
+            e.site_shard_apply_dev(k.data_ptr(), p.data_ptr(), total_cand)
+
+    def round_reduce():
+        # two collectives: allreduce(MAX) of the keys, then the owner's payload
+        # broadcast as an allreduce(SUM) with zeros
         for e, k in zip(engines, keys):
             e.site_shard_best_dev(k.data_ptr())
         comm.max_dev(keys, engines)
@@ -268,6 +303,12 @@ def _device_rounds(active, comm, total_cand, poll_every=16):
         comm.sum_dev(pays, engines)
         for e, k, p in zip(engines, keys, pays):
             e.site_shard_apply_dev(k.data_ptr(), p.data_ptr(), total_cand)
+
+    # one allgather beats two allreduces once there are peers; a world of one
+    # has nothing to exchange and the two local allreduces are cheaper
+    # (c2, NCCL world 1: 18.1 vs 21.1 ms of rounds)
+    mode = os.environ.get("TXS_SHARD_EXCHANGE") or ("gather" if nranks > 1 else "reduce")
+    one_round = round_reduce if mode == "reduce" else round_gather
 
     engines[0].event_record(14)
     one_round()                                   # eager: sizes the device step log
@@ -301,4 +342,6 @@ def _device_rounds(active, comm, total_cand, poll_every=16):
         raise RuntimeError("sharded SITE did not stop")
     res["site_ms"] = engines[0].event_elapsed(14, 15)   # device time of the rounds (rank-local)
     res["rounds_mode"] = "graph" if graph is not None else "eager"
+    res["exchange"] = ("one allgather of {key, payload} per round" if mode != "reduce"
+                       else "two allreduces per round (MAX of keys, SUM broadcast of the payload)")
     return res

@@ -445,13 +445,16 @@ def test_cli_matches_oracle_and_is_deterministic(tmp_path):
 
 
 # ---- row-band shards on one device (virtual ranks) ---------------
-@pytest.mark.parametrize("device_rounds", [False, True])
+@pytest.mark.parametrize("device_rounds", [False, "gather", "reduce"])
 @pytest.mark.parametrize("kind,nb", [("findmax", 1), ("findmax", 2), ("findmax", 3), ("observers", 2),
                                      ("observers", 4)])
-def test_sharded_engine_matches_single(kind, nb, device_rounds):
+def test_sharded_engine_matches_single(monkeypatch, kind, nb, device_rounds):
     """Row bands on virtual ranks (one device) == the single-context run, with
-    the SITE rounds host-driven or device-resident (txs_site_shard_*_dev)."""
+    the SITE rounds host-driven or device-resident (txs_site_shard_*_dev), the
+    latter with the one-allgather or the two-allreduce exchange."""
     T = _T()
+    if device_rounds:
+        monkeypatch.setenv("TXS_SHARD_EXCHANGE", device_rounds)
     from paper_2006_16783_b200.configs import Config, params_for, run, setup_terrain
     from paper_2006_16783_b200.shard import LocalComm, run_sharded
     if kind == "findmax":
@@ -462,7 +465,7 @@ def test_sharded_engine_matches_single(kind, nb, device_rounds):
     params = params_for(cfg)
     engines = [T.Engine(0) for _ in range(nb)]
     res = run_sharded([(e, k) for k, e in enumerate(engines)], LocalComm(), cfg, params, nb,
-                      device_rounds=device_rounds)
+                      device_rounds=bool(device_rounds))
     with T.Engine(0) as e:
         setup_terrain(e, cfg)
         single = run(e, cfg, params)
