@@ -257,6 +257,13 @@ def stage_figures(st, K, cfg, site_mode):
                 "peak_kind": peak_kind,
                 "bytes_model": "VIX/VIEWSHED: 4 B (two int16 posts) per grid-line crossing, no early exit; "
                                "SITE: packed viewshed bytes streamed; FINDMAX: VixMap read twice"}
+    if dom == "vix":
+        roofline["note"] = ("algorithmic LOS-sample bytes (SURVEY 8(d)); the VIX skip map proves most crossings "
+                            "unblockable without reading them, so DRAM traffic per launch (traffic) is ~1 % of them and "
+                            "frac can exceed 1: the kernel is issue-bound, not HBM-bound (DESIGN.md 3, 5)")
+    elif dom == "viewshed":
+        roofline["note"] = ("algorithmic LOS-sample bytes (SURVEY 8(d)), served from L1/L2; the R2 sweep is "
+                            "ALU-bound (DESIGN.md 3)")
     return stages, roofline, peak
 
 
