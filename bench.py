@@ -223,9 +223,11 @@ def load_traffic(kernel):
         return None
 
 
-def stage_figures(st, K, cfg, site_mode):
+def stage_figures(st, K, cfg, site_mode, l2_gbs=None):
     """Per-stage device times and algorithmic throughputs from the engine's
-    stats over K steps, and the roofline of the dominant stage's kernel."""
+    stats over K steps, and the roofline of the dominant stage's kernel.
+    l2_gbs: measured L2-resident read bandwidth, the peak SURVEY 8(d) sets the
+    VIX / VIEWSHED LOS-sample figures against (reported beside the HBM one)."""
     peak, peak_kind = load_peaks()
     stages = {}
     if cfg.samples:
@@ -257,6 +259,14 @@ def stage_figures(st, K, cfg, site_mode):
                 "peak_kind": peak_kind,
                 "bytes_model": "VIX/VIEWSHED: 4 B (two int16 posts) per grid-line crossing, no early exit; "
                                "SITE: packed viewshed bytes streamed; FINDMAX: VixMap read twice"}
+    if l2_gbs:
+        for k in ("vix", "viewshed"):
+            if k in stages and stages[k].get("achieved_gbs"):
+                stages[k]["l2_peak_gbs"] = round(l2_gbs, 1)
+                stages[k]["frac_of_l2"] = round(stages[k]["achieved_gbs"] / l2_gbs, 4)
+        if dom in ("vix", "viewshed"):
+            roofline["l2_peak_gbs"] = round(l2_gbs, 1)
+            roofline["frac_of_l2"] = round(ach / l2_gbs, 4)
     if dom == "vix":
         roofline["note"] = ("algorithmic LOS-sample bytes (SURVEY 8(d)); the VIX skip map proves most crossings "
                             "unblockable without reading them, so DRAM traffic per launch (traffic) is ~1 % of them and "
@@ -378,7 +388,7 @@ def run_b200(args, cfg):
 
     # ---- per-stage figures and the roofline of the dominant kernel -------
     K = args.steps
-    stages, roofline, peak = stage_figures(st, K, cfg, args.site_mode)
+    stages, roofline, peak = stage_figures(st, K, cfg, args.site_mode, l2_gbs=eng.measure_l2())
     site_stream["frac_of_hbm"] = round(site_stream["gbs"] / peak, 4) if site_stream["gbs"] else None
     site_stream["kernel_frac_of_hbm"] = round(site_stream["kernel_gbs"] / peak, 4) if site_stream["kernel_gbs"] else None
     stages["site_stream"] = site_stream
@@ -505,7 +515,7 @@ def run_b200_sharded(args, cfg):
     launches = torch.tensor([st["kernel_launches"]], device=dev, dtype=torch.int64)
     dist.all_reduce(launches, op=dist.ReduceOp.SUM)
     if rank == 0:
-        stages, roofline, _ = stage_figures(agg, args.steps, cfg, args.site_mode)
+        stages, roofline, _ = stage_figures(agg, args.steps, cfg, args.site_mode, l2_gbs=eng.measure_l2())
         line = {
             "metric": METRIC, "value": round(ms / 1e3, 5), "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",

@@ -161,6 +161,11 @@ txs_status txs_marginal_gains(txs_ctx* ctx, const uint64_t* cum_dense, int64_t* 
  * are overwritten.  ms_per_pass = mean device time of one pass, bytes_per_pass =
  * packed viewshed bytes streamed (SPEC layout, algorithmic). */
 txs_status txs_time_gain_pass(txs_ctx* ctx, int32_t reps, double* ms_per_pass, int64_t* bytes_per_pass);
+/* Measurement: L2-resident read bandwidth (GB/s) -- `reps` passes of 16-byte
+ * loads over a `bytes` buffer that fits the L2, timed with CUDA events on the
+ * context stream (the peak the VIX / VIEWSHED LOS-sample figures are set
+ * against). */
+txs_status txs_measure_cache_read(txs_ctx* ctx, int64_t bytes, int32_t reps, double* gbs);
 
 /* ---- cli module (SPEC.md:433 run_pipeline) ---------------------------------- */
 /* vix -> findmax -> viewshed -> site on the resident terrain, device-resident

@@ -108,6 +108,7 @@ _sig("txs_site_shard_select_dev", C.c_int, [vp, vp, i32, vp, vp])
 _sig("txs_site_shard_result", C.c_int, [vp, vp, i64, C.POINTER(i64), C.POINTER(i32)])
 _sig("txs_stream", vp, [vp])
 _sig("txs_time_gain_pass", C.c_int, [vp, i32, C.POINTER(dbl), C.POINTER(i64)])
+_sig("txs_measure_cache_read", C.c_int, [vp, i64, i32, C.POINTER(dbl)])
 _sig("txs_ray_template", i64, [i32, vp, vp, vp, vp, vp, i64, i64, C.POINTER(i64)])
 _sig("txs_selftest", C.c_int, [])
 _sig("txs_event_template_info", C.c_int, [i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(i32)])
@@ -124,5 +125,5 @@ EXPORTS = [
     "txs_site_shard_export", "txs_site_shard_apply", "txs_event_template_info",
     "txs_site_shard_best_dev", "txs_site_shard_export_dev", "txs_site_shard_apply_dev",
     "txs_site_shard_payload_words", "txs_site_shard_result", "txs_stream", "txs_time_gain_pass",
-    "txs_site_shard_export_keyed_dev", "txs_site_shard_select_dev",
+    "txs_site_shard_export_keyed_dev", "txs_site_shard_select_dev", "txs_measure_cache_read",
 ]

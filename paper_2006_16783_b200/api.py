@@ -293,6 +293,12 @@ class Engine:
         self._chk(N.lib.txs_time_gain_pass(self._h, reps, C.byref(ms), C.byref(b)))
         return ms.value, b.value
 
+    def measure_l2(self, nbytes=64 << 20, reps=20):
+        """L2-resident read bandwidth in GB/s (txs_measure_cache_read)."""
+        g = C.c_double()
+        self._chk(N.lib.txs_measure_cache_read(self._h, nbytes, reps, C.byref(g)))
+        return g.value
+
     def stats(self):
         s = N.Stats()
         self._chk(N.lib.txs_get_stats(self._h, C.byref(s)))

@@ -619,6 +619,41 @@ txs_status txs_get_cumulative(txs_ctx* c, uint64_t* out) {
     return download_cum(c, out);
 }
 
+namespace {
+// every thread reads 16-byte words with a grid stride; the xor keeps the loads live
+__global__ void k_l2_read(const uint4* __restrict__ buf, int64_t n, int reps, unsigned* __restrict__ sink) {
+    uint32_t acc = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int k = 0; k < reps; ++k)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+            const uint4 v = __ldcg(buf + i);
+            acc ^= v.x ^ v.y ^ v.z ^ v.w;
+        }
+    if (acc == 0x9e3779b9u) *sink = acc;
+}
+}  // namespace
+
+txs_status txs_measure_cache_read(txs_ctx* c, int64_t bytes, int32_t reps, double* gbs) {
+    if (!c || !gbs || bytes < 4096 || reps < 1) return TXS_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(c->device);
+    uint4* buf = nullptr;
+    TXS_CUDA(c, "stats", cudaMalloc(&buf, (size_t)bytes + 16));
+    TXS_CUDA(c, "stats", cudaMemsetAsync(buf, 1, (size_t)bytes, c->stream));
+    const int64_t n = bytes / 16;
+    const int grid = c->num_sms * 8;
+    k_l2_read<<<grid, 256, 0, c->stream>>>(buf, n, 1, (unsigned*)(buf + n));   // warm the L2
+    cudaEventRecord(c->ev_r0, c->stream);
+    k_l2_read<<<grid, 256, 0, c->stream>>>(buf, n, reps, (unsigned*)(buf + n));
+    cudaEventRecord(c->ev_r1, c->stream);
+    const cudaError_t e = cudaEventSynchronize(c->ev_r1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev_r0, c->ev_r1);
+    cudaFree(buf);
+    if (e != cudaSuccess) return cuda_fail(c, "stats", e);
+    *gbs = ms > 0.f ? (double)n * 16.0 * reps / (ms * 1e-3) / 1e9 : 0.0;
+    return TXS_OK;
+}
+
 txs_status txs_time_gain_pass(txs_ctx* c, int32_t reps, double* ms, int64_t* bytes) {
     if (!c || !ms || !bytes || reps < 1) return TXS_ERR_INVALID_ARGUMENT;
     if (!c->site_valid || !c->vs_valid) return fail(c, TXS_ERR_STATE, "site", "run txs_site first");
