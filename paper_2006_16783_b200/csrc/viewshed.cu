@@ -642,17 +642,19 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
         for (const uint2& e : Et.events) { const uint32_t t = e.x & 7u; cr += t <= kEvPost; ce += t == kEvCell; }
         a.tmpl_cross = cr; a.tmpl_cells = ce;
     }
-    // observers per CTA (measured on B200 with the cum-aligned output, profiles/):
-    // 2 (C2 20.1 ms vs 21.8 / 25.3 for K=1 / 4; C5 1.85 s vs 1.96 / 2.91 s),
-    // 1 when the grid would not fill the SMs
+    // observers per CTA (measured on B200, profiles/README.md): 3 below roi 225
+    // (C2 16.2 -> 15.3 ms, C3 27.0 -> 23.5, C4 50.4 -> 44.5 against K = 2), 2 at
+    // roi >= 225 (C5 1324 ms vs 1519+ for K = 3), fewer when the grid would not
+    // fill the SMs (C1's 1000 observers: K = 2)
     int kobs = 1;
     if (2 * smem <= 100 * 1024 && n >= (int64_t)2 * c->num_sms * 4) kobs = 2;
+    if (p.roi < 225 && 3 * smem <= 100 * 1024 && n >= (int64_t)3 * c->num_sms * 8) kobs = 3;
     if (const char* kenv = getenv("TXS_VS_K")) kobs = atoi(kenv);
-    if (T->events && smem_bits && (kobs == 2 || kobs == 4) && (size_t)kobs * smem <= 200 * 1024) {
+    if (T->events && smem_bits && (kobs == 2 || kobs == 3 || kobs == 4) && (size_t)kobs * smem <= 200 * 1024) {
         // warps per CTA (measured, profiles/README.md; resident warps vs ray-group
         // balance): 15 at roi >= 225 (C5 1496 -> 1325 ms), 8 at roi >= 150 (C2
         // 16.5 -> 15.9), else 6 (C3 34.3 -> 27.0); TXS_VS_WARPS overrides
-        int best = p.roi >= 225 ? 15 : (p.roi >= 150 ? 8 : 6);
+        int best = p.roi >= 225 ? 15 : (p.roi >= 150 ? (kobs == 3 ? 12 : 8) : 6);   // K=3, roi 200: 12 (C2 15.3 vs 16.5 at 9)
         best = std::min(best, T->ngroups);
         if (const char* e = getenv("TXS_VS_WARPS")) best = std::max(1, std::min(32, atoi(e)));
         const int threads = 32 * best;
@@ -677,7 +679,12 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
         set_zbounds(c->d_z, c->d_z + c->z_rows * c->ncols, c->stream, (const int16_t*)a.pairs,
                     (const int16_t*)(a.pairs + pwords));
         }
-        if (kobs == 2) {
+        if (kobs == 3) {
+            if (sm > 48 * 1024)
+                TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(k_viewshed_evk<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            k_viewshed_evk<3><<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
+                                                                 T->ngroups, a, c->d_words, c->d_win, c->d_pop, c->d_counters);
+        } else if (kobs == 2) {
             if (sm > 48 * 1024)
                 TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(k_viewshed_evk<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             k_viewshed_evk<2><<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
