@@ -739,13 +739,21 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
         }
         const int r = a.row0 + ty * kTileQ + item % kTileQ;
         if (r >= a.row_end) continue;
+        // the row's stream seeds (D6) and observer elevations, one post per lane
+        // (measured: c3 126.1 -> 113.3 ms; a wash at 32 registers, profiles/README.md)
+        uint64_t rseed = 0;
+        int rE = 0;
+        if (lane < kTileQ && tx * kTileQ + lane < ncols) {
+            rseed = mix_seed(a.seed, (uint64_t)r, (uint64_t)(tx * kTileQ + lane));
+            rE = zld(z + (int64_t)r * ncols + tx * kTileQ + lane) + a.ht;
+        }
         for (int j = 0; j < kTileQ; ++j) {
             const int c = tx * kTileQ + j;
             if (c >= ncols) break;
             if (p_next - p_open == kRing) run_batch(qn);   // ring full (S < 3): drain
             ++n_posts;
-            const uint64_t base = mix_seed(a.seed, (uint64_t)r, (uint64_t)c);
-            const int E = zld(z + (int64_t)r * ncols + c) + a.ht;
+            const uint64_t base = __shfl_sync(kFull, rseed, j);
+            const int E = __shfl_sync(kFull, rE, j);
             const int slot = p_next & (kRing - 1);
             if (lane == slot) { myE = E; myR = r; myC = c; }
             ++p_next;
