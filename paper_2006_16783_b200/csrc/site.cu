@@ -268,7 +268,10 @@ __global__ void __launch_bounds__(kUpdThreads) k_update(SiteArgs a, const SiteSt
 // Phase C: neighbour gains -= popc(v_i & delta)                      -> grid sync
 // Delta spans are double-buffered so the next round's buffer is reset during
 // the current commit.
-constexpr int kLoopThreads = 256;
+#ifndef SITE_LOOP_THREADS
+#define SITE_LOOP_THREADS 256
+#endif
+constexpr int kLoopThreads = SITE_LOOP_THREADS;
 
 __global__ void __launch_bounds__(kLoopThreads) k_site_loop(SiteArgs a, SiteState* st, LoopPtrs lp,
                                                              int32_t* __restrict__ gain, const int32_t* __restrict__ items,
