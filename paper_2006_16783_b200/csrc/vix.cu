@@ -417,9 +417,10 @@ struct __align__(16) QuadGeomC {   // skip test
     int w;            // M | c0 << 8 | tr << 13 | mneg << 14 | mag << 15   (M = 0: nothing to walk)
 };
 struct __align__(16) QuadGeomF {   // exact walk
-    const uint2* Q;   // start post's entry in its plane
+    const uint2* Q;   // start post's entry in its plane (terrain-walk kernels: the start post's
+                      // int16 terrain address, reinterpreted)
     int Es;           // LOS height at the start post (E, or Zt when reversed)
-    int msm;          // m | sm << 8 (sm = minor step in plane words, 0 for axis-aligned segments)
+    int msm;          // m | sm << 8 (sm = minor step in plane words / terrain posts, 0 for axis-aligned)
 };
 struct QuadGeom { QuadGeomC c; QuadGeomF f; };
 
@@ -435,7 +436,22 @@ __device__ __forceinline__ bool quad_test(uint2 v, int r, int nm, uint32_t wb, i
 // Plane geometry shared by every walk of a launch.
 struct QuadPitch {
     int pv, pt;       // skip map: SV row pitch, ST column pitch (int16)
+    int zs;           // terrain row pitch (terrain-walk kernels)
 };
+
+// One exact step of a failing unit, read from the int16 terrain instead of the
+// quad planes (the kernels whose skip test passes almost every group -- 16-step
+// groups -- do not build the planes): posts A = P[i stepM + q sm], B = A one
+// minor step on, C = A one major step back; the predicates of quad_test.
+__device__ __forceinline__ bool terrain_test(const int16_t* P, int i, int q, int r, int nM, int nm, int sm, int stepM,
+                                             int rhsM, int rhsm) {
+    const int o = i * stepM + q * sm;
+    const bool minor = (unsigned)(r - 1) < (unsigned)(nm - 1);
+    const int zA = zld(P + o);
+    const int zB = r ? zld(P + o + sm) : 0;
+    const int zC = minor ? zld(P + o - stepM) : 0;
+    return (zA * (nM - r) + zB * r > rhsM) | (minor & (zC * r + zA * (nm - r) > rhsm));
+}
 
 // Full walk: one segment per warp, lane l taking major steps l+1, l+33, ...;
 // a vote after every 32 steps.  Returns true (uniform) iff the segment is
@@ -536,7 +552,7 @@ __device__ __forceinline__ bool quad_walk_skip(const QuadGeom* gp, const QuadPit
 // consecutive steps (coalesced plane loads, the predicates of quad_test), in
 // (segment, unit) order, skipping segments already found blocked.  Returns
 // the mask of lanes whose segment is visible.
-template <int U, int GS>
+template <int U, int GS, bool TERR>
 __device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int lane, QuadGeom* s_geo, int* s_pre,
                                                int* s_fail, const int16_t* __restrict__ smap, const QuadPitch& P) {
     static_assert((U << GS) <= 32, "a failing unit is walked by one 32-step pass");
@@ -604,9 +620,14 @@ __device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int la
             bool b = false;
             if (i < nM) {
                 const int nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 15, D = c.DG >> GS;
-                const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
                 const int q = (i * mag) >> 16, r = i * nm - q * nM;
-                b = quad_test(qld(f.Q + i + q * sm), r, nm, wb, c.LE2 - min(0, c.DG) + i * D, f.Es * nm + q * D);
+                const int rhsM = c.LE2 - min(0, c.DG) + i * D, rhsm = f.Es * nm + q * D;
+                if (TERR) {
+                    b = terrain_test((const int16_t*)f.Q, i, q, r, nM, nm, sm, (c.w & 0x2000) ? P.zs : 1, rhsM, rhsm);
+                } else {
+                    const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
+                    b = quad_test(qld(f.Q + i + q * sm), r, nm, wb, rhsM, rhsm);
+                }
             }
             if (__any_sync(kFull, b)) blk |= 1u << sf;
         }
@@ -632,7 +653,9 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
     int* s_fail = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + warp_of_thread() * kFailInts;
     int* s_pre = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + kVixWarps * kFailInts + warp_of_thread() * 32;
     int* s_q = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + kVixWarps * (kFailInts + 32) + warp_of_thread() * 64;
-    const QuadPitch PQ{a.pv, a.pt};
+    const QuadPitch PQ{a.pv, a.pt, ncols};
+    // 16-step skip groups (roi < 150): failing units walk the terrain, no quad planes
+    constexpr bool TERR = SKIP == 1 && GS == 4;
     const int lane = threadIdx.x & 31;
     const int R2 = a.R * a.R;
     unsigned long long n_cross = 0;
@@ -670,9 +693,15 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
             const int64_t n = (int64_t)H * a.wp, nT = (int64_t)ncols * a.hp;
             const int stride = tr ? a.hp : a.wp;
             const int Es = rev ? Zt : E;
-            g.f.Q = qp + (tr ? 2 * n + (int64_t)x * a.hp + y + (mneg ? nT : 0) : (int64_t)y * a.wp + x + (mneg ? n : 0));
+            if (TERR) {
+                g.f.Q = (const uint2*)(z + (int64_t)(y + a.zr0) * ncols + x);
+                const int zstep = tr ? 1 : ncols;   // minor axis: columns for row-major walks
+                g.f.msm = nm | ((nm == 0 ? 0 : (mneg ? -zstep : zstep)) * 256);
+            } else {
+                g.f.Q = qp + (tr ? 2 * n + (int64_t)x * a.hp + y + (mneg ? nT : 0) : (int64_t)y * a.wp + x + (mneg ? n : 0));
+                g.f.msm = nm | ((nm == 0 ? 0 : (mneg ? -stride : stride)) * 256);
+            }
             g.f.Es = Es;
-            g.f.msm = nm | ((nm == 0 ? 0 : (mneg ? -stride : stride)) * 256);
             // skip map (k_skipmap): padded 4x4-block indices of the start post,
             // SV row-major for column-major walks, ST column-major for row-major ones
             const int maj = tr ? y : x, mnr = tr ? x : y;
@@ -689,7 +718,7 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
         __syncwarp();
         unsigned vism;
         if constexpr (SKIP == 1) {
-            vism = batch_skip<U, GS>(g, ns, lane, s_geo, s_pre, s_fail, smap, PQ);
+            vism = batch_skip<U, GS, TERR>(g, ns, lane, s_geo, s_pre, s_fail, smap, PQ);
         } else {
             s_geo[lane] = g;
             __syncwarp();
@@ -884,8 +913,11 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     // the free-memory query only when the scratch must grow (it can stall the
     // host inside the timed stage)
     size_t freeb = 0, totalb = 0;
-    if (p.roi <= 255 && qbytes > c->pairs_cap) cudaMemGetInfo(&freeb, &totalb);
-    const bool quads_ok = p.roi <= 255 && (qbytes <= c->pairs_cap || qbytes <= freeb / 2);
+    // (the default roi < 150 kernel walks the terrain and needs only the skip map)
+    const bool terr_default = p.roi < 150 && !getenv("TXS_VIX_GROUP") && !getenv("TXS_VIX_SKIP");
+    const size_t qneed = terr_default ? 0 : qbytes;
+    if (p.roi <= 255 && qneed > c->pairs_cap) cudaMemGetInfo(&freeb, &totalb);
+    const bool quads_ok = p.roi <= 255 && (qneed <= c->pairs_cap || qneed <= freeb / 2);
     int path = quads_ok ? 1 : (smem <= 110 * 1024 ? 0 : 2);
     if (const char* e = getenv("TXS_VIX_PATH")) {
         if (!strcmp(e, "smem") && smem <= 200 * 1024) path = 0;
@@ -896,7 +928,8 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     if (path == 0) {
         st = go(k_vix<true, 1>, smem);
     } else if (path == 1) {
-        const int64_t n = c->z_rows * c->ncols, nq = 2 * c->z_rows * (int64_t)a.wp + 2 * c->ncols * (int64_t)a.hp;
+        const int64_t n = c->z_rows * c->ncols;
+        int64_t nq = 2 * c->z_rows * (int64_t)a.wp + 2 * c->ncols * (int64_t)a.hp;
         // skip-test group size G = 2^gs (measured, profiles/README.md): 16 at roi < 150,
         // where the smooth C3/C4 terrain passes 16-step tests 99.97 % of the time
         // (one map load per 16 steps), 4 at roi >= 150 (C2: 59 % of 16-step groups
@@ -919,10 +952,14 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         if (a.pv >= 32768 || a.pt >= 32768) skip = 0;   // signed 16-bit map pitches (batch_skip)
         if (const char* e = getenv("TXS_VIX_SKIP")) skip = std::max(0, std::min(2, atoi(e)));
         const size_t map_bytes = skip ? sizeof(int16_t) * (size_t)(nsv + nst + nbp) : 0;
+        // with 16-step skip groups the flattened kernel walks failing units on the
+        // terrain itself: no quad planes (69 GB at C4) and no plane build
+        const bool terr = skip == 1 && gs == 4;
+        if (terr) nq = 0;
         // rebuilt on every call (part of the timed stage; ~1 HBM pass of 34 B/post)
         if (ensure(c, "vix", (void**)&c->d_pairs, &c->pairs_cap, sizeof(uint2) * nq + map_bytes) != TXS_OK)
             return TXS_ERR_OUT_OF_MEMORY;
-        {
+        if (!terr) {
             dim3 tb(32, 8), tg((unsigned)((c->ncols + 31) / 32), (unsigned)((c->z_rows + 31) / 32));
             k_quads<<<tg, tb, 0, c->stream>>>(c->d_z, (uint2*)c->d_pairs, (int)c->z_rows, a.hp, a.wp, (int)c->ncols);
             TXS_LAUNCHED(c, "vix");
