@@ -1010,7 +1010,6 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         int64_t grid_q = std::min<int64_t>(tiles_q, (int64_t)std::max(1, per_sm) * c->num_sms);
         if (const char* e = getenv("TXS_VIX_GRID")) grid_q = std::min<int64_t>(tiles_q, std::max(1, atoi(e)));
         TXS_CUDA(c, "vix", cudaMemsetAsync(c->d_counters + kVixNext, 0, sizeof(unsigned long long), c->stream));
-        if (getenv("TXS_VIX_VERBOSE")) fprintf(stderr, "[vix] per_sm %d grid %lld tiles %lld smem %zu\n", per_sm, (long long)grid_q, (long long)tiles_q, qsm);
         kq<<<(unsigned)grid_q, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols,
                                                                 c->d_vix - c->band_r0 * c->ncols, aq, c->d_gcd, smap,
                                                                 c->d_counters);
