@@ -542,3 +542,31 @@ def test_time_gain_pass_counts_packed_bytes(engine):
     cum = engine.cumulative()
     exp = [O.marginal_gain(wins[i], words[i], cum, 300, 300) for i in range(len(rows))]
     assert np.array_equal(engine.marginal_gains(cum), np.array(exp))
+
+
+def test_bench_json_contract_and_cache_read(engine):
+    """bench.py's default-arm JSON line carries every key of the driver
+    contract (roofline, cpu_baseline, e2e with copy bytes, clocks sampled
+    during the timed region, launches); txs_measure_cache_read reports a
+    positive L2-resident read bandwidth."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "c1", "--steps", "2",
+                        "--warmup", "3"], cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["steps"] == 2 and d["warmup"] == 3 and d["value"] > 0 and d["gpu_launches"] > 0
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in d["roofline"], k
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["kind"] in ("port", "reference")
+    assert d["clocks"] and d["clocks"]["samples"] >= 1 and d["clocks"]["sm_mhz"] > 0
+    assert engine.measure_l2(16 << 20, 4) > 100.0
