@@ -322,12 +322,20 @@ __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, 
 // own horizon (NH, MH) and bitmap — K independent dependency chains per lane.
 // Interior observers have every post in the grid and an unclipped window, so
 // no bounds tests and no counting (the template's totals are added instead).
-template <int K, bool PAIRS>
+//
+// EDGE: the same sweep for CTAs holding observers near the grid edge (clipped
+// windows): per observer, an event counts only if its posts are in the grid
+// (a crossing that needs an off-grid post ends that observer's ray, cells
+// outside the grid are skipped -- the rules of vs_events<false>), the cell bit
+// uses the observer's own window pitch and origin, and the crossings / cells
+// actually evaluated are counted.
+template <int K, bool PAIRS, bool EDGE>
 __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const int* rk, const int* ck, const int* Ek,
                                             const int* RSk, const int* K0k,
                                             const VsArgs& a, const int4* __restrict__ rays,
                                             const int2* __restrict__ groups, const uint2* __restrict__ events,
-                                            int ngroups, uint32_t* s_bits, int bits_stride) {
+                                            int ngroups, uint32_t* s_bits, int bits_stride,
+                                            unsigned long long& n_cross, unsigned long long& n_cells) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const uint32_t* __restrict__ B[K];   // PAIRS: the observer's word in the pair planes
     const int16_t* __restrict__ P[K];    // else: the observer's post
@@ -360,14 +368,16 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
         // a cell's |X|*L2 <= 98302*L2 < 2^30*dot (an owned cell lies ahead of
         // its ray: dot >= 0.7*|(p,q)|, and |(p,q)| <= 354)
         int NH[K], MH[K], L2MH[K];
+        bool alive[K];
 #pragma unroll
-        for (int k = 0; k < K; ++k) { NH[k] = -(1 << 30); MH[k] = 1; L2MH[k] = L2; }
+        for (int k = 0; k < K; ++k) { NH[k] = -(1 << 30); MH[k] = 1; L2MH[k] = L2; alive[k] = true; }
         const uint2* ev = events + (int64_t)grp.x * 32 + lane;
         for (int st0 = 0; st0 < grp.y; st0 += 2) {
             uint2 ee[2];
             uint32_t pr[2][K];
             int z0[2][K], z1[2][K];
             int dru[2], dcu[2];
+            bool ok[2][K];
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 ee[u] = st0 + u < grp.y ? __ldg(ev + (int64_t)(st0 + u) * 32) : make_uint2((uint32_t)kEvNop, 0u);
@@ -375,17 +385,22 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
                 const int dr = ((int)(e << 20)) >> 23, dc = ((int)(e << 11)) >> 23;
                 const bool isrow = type == kEvRow, iscol = type == kEvCol;
                 dru[u] = dr; dcu[u] = dc;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {   // both interpolation posts (or the cell) in the grid
+                    ok[u][k] = !EDGE || (type != kEvNop && (unsigned)(rk[k] + dr) < (unsigned)(a.nrows - (iscol ? 1 : 0)) &&
+                                         (unsigned)(ck[k] + dc) < (unsigned)(a.ncols - (isrow ? 1 : 0)));
+                }
                 if (PAIRS) {   // the first post's H pair (its right neighbour) or, column crossing, V pair
                     const int off = type != kEvNop ? dr * a.p2 + dc + (iscol ? a.pw : 0) : 0;
 #pragma unroll
-                    for (int k = 0; k < K; ++k) pr[u][k] = vs_pld(B[k] + off);
+                    for (int k = 0; k < K; ++k) pr[u][k] = (!EDGE || ok[u][k]) ? vs_pld(B[k] + off) : 0u;
                 } else {
                     const int off0 = type != kEvNop ? dr * a.ncols + dc : 0;
                     const int off1 = off0 + (iscol ? a.ncols : (isrow ? 1 : 0));
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
-                        z0[u][k] = zld(P[k] + off0);
-                        z1[u][k] = zld(P[k] + off1);
+                        z0[u][k] = (!EDGE || ok[u][k]) ? zld(P[k] + off0) : 0;
+                        z1[u][k] = (!EDGE || ok[u][k]) ? zld(P[k] + off1) : 0;
                     }
                 }
             }
@@ -406,11 +421,24 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
                     const int X = v - (iscell ? Ehr[k] : n * Ek[k]);
                     const long long lhs = mulw(X, iscell ? L2MH[k] : MH[k]);
                     const long long rhs = mulw(NH[k], y);
-                    const bool up = iscross & (lhs > rhs);
+                    bool upc = iscross, setc = iscell;
+                    if (EDGE) {
+                        if (iscross && !ok[u][k]) alive[k] = false;   // the ray needs an off-grid post: it ends
+                        upc = iscross && alive[k];
+                        setc = iscell && ok[u][k];
+                        n_cross += upc;
+                        n_cells += setc;
+                    }
+                    const bool up = upc & (lhs > rhs);
                     NH[k] = up ? X : NH[k];
                     MH[k] = up ? y : MH[k];
                     L2MH[k] = up ? L2 * y : L2MH[k];
-                    red_or_shared(sb[k] + cw4, cbit, iscell & (lhs >= rhs));
+                    if (EDGE) {
+                        const int kb = dru[u] * RSk[k] + dcu[u] + K0k[k];
+                        red_or_shared(sb[k] + ((uint32_t)(kb >> 5) << 2), 1u << (kb & 31), setc & (lhs >= rhs));
+                    } else {
+                        red_or_shared(sb[k] + cw4, cbit, setc & (lhs >= rhs));
+                    }
                 }
             }
         }
@@ -485,8 +513,8 @@ __global__ void k_viewshed_ev(const int16_t* __restrict__ z, const int32_t* __re
 
 // K observers per CTA (shared event stream, smem bitmaps); CTAs where some
 // observer is not interior fall back to one observer at a time.
-template <int K>
-__global__ void k_viewshed_evk(const int16_t* __restrict__ z, const int32_t* __restrict__ crow,
+template <int K, int MAXREG>
+__global__ void __maxnreg__(MAXREG) k_viewshed_evk(const int16_t* __restrict__ z, const int32_t* __restrict__ crow,
                                const int32_t* __restrict__ ccol, const int4* __restrict__ rays,
                                const int2* __restrict__ groups, const uint2* __restrict__ events, int ngroups,
                                VsArgs a, uint64_t* __restrict__ words, int4* __restrict__ wins,
@@ -523,9 +551,13 @@ __global__ void k_viewshed_evk(const int16_t* __restrict__ z, const int32_t* __r
     __syncthreads();
     unsigned long long n_cross = 0, n_cells = 0;
     if (all_int) {
-        if (a.pairs) vs_events_k<K, true>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride);
-        else vs_events_k<K, false>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride);
+        unsigned long long d0 = 0, d1 = 0;
+        if (a.pairs) vs_events_k<K, true, false>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride, d0, d1);
+        else vs_events_k<K, false, false>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride, d0, d1);
         if (threadIdx.x == 0) { n_cross = (unsigned long long)(K * a.tmpl_cross); n_cells = (unsigned long long)(K * a.tmpl_cells); }
+    } else if (a.pairs && nk == K) {   // edge observers: the same shared sweep with per-observer grid bounds
+        vs_events_k<K, true, true>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride,
+                                   n_cross, n_cells);
     } else {
         for (int k = 0; k < K; ++k) {
             if (cand[k] < 0) continue;
@@ -659,6 +691,10 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
         if (const char* e = getenv("TXS_VS_WARPS")) best = std::max(1, std::min(32, atoi(e)));
         const int threads = 32 * best;
         const size_t sm = (size_t)kobs * smem;
+        // registers (resident CTAs per SM at the chosen warps): 72 at roi 150..224
+        // (C2 13.5 ms vs 14.0 at 64), 64 elsewhere (C3 23.2 vs 24.3 at 68, C4 44.3 vs
+        // 46.6, C5 1276 vs 1717 at 72: 15-warp CTAs drop to one per SM)
+        const bool cap64 = p.roi < 150 || p.roi >= 225;
         const unsigned grid = (unsigned)((n + kobs - 1) / kobs);
         // pair planes of the held rows (rebuilt per call, part of the timed stage;
         // shares the VIX quad-plane scratch buffer) -- measured (profiles/README.md):
@@ -680,19 +716,22 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
                     (const int16_t*)(a.pairs + pwords));
         }
         if (kobs == 3) {
+            auto kern = cap64 ? k_viewshed_evk<3, 64> : k_viewshed_evk<3, 72>;
             if (sm > 48 * 1024)
-                TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(k_viewshed_evk<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            k_viewshed_evk<3><<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
+                TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            kern<<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
                                                                  T->ngroups, a, c->d_words, c->d_win, c->d_pop, c->d_counters);
         } else if (kobs == 2) {
+            auto kern = cap64 ? k_viewshed_evk<2, 64> : k_viewshed_evk<2, 72>;
             if (sm > 48 * 1024)
-                TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(k_viewshed_evk<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            k_viewshed_evk<2><<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
+                TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            kern<<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
                                                                  T->ngroups, a, c->d_words, c->d_win, c->d_pop, c->d_counters);
         } else {
+            auto kern = cap64 ? k_viewshed_evk<4, 64> : k_viewshed_evk<4, 72>;
             if (sm > 48 * 1024)
-                TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(k_viewshed_evk<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            k_viewshed_evk<4><<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
+                TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            kern<<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
                                                                  T->ngroups, a, c->d_words, c->d_win, c->d_pop, c->d_counters);
         }
     } else if (T->events) {
