@@ -273,7 +273,12 @@ __global__ void __launch_bounds__(kUpdThreads) k_update(SiteArgs a, const SiteSt
 #endif
 constexpr int kLoopThreads = SITE_LOOP_THREADS;
 
-__global__ void __launch_bounds__(kLoopThreads) k_site_loop(SiteArgs a, SiteState* st, LoopPtrs lp,
+#ifdef SITE_LOOP_MAXREG
+#define TXS_LOOP_REGS __maxnreg__(SITE_LOOP_MAXREG)
+#else
+#define TXS_LOOP_REGS __launch_bounds__(kLoopThreads)
+#endif
+__global__ void TXS_LOOP_REGS k_site_loop(SiteArgs a, SiteState* st, LoopPtrs lp,
                                                              int32_t* __restrict__ gain, const int32_t* __restrict__ items,
                                                              const uint64_t* __restrict__ words, uint64_t* __restrict__ cum,
                                                              uint64_t* __restrict__ dwin, int2* __restrict__ dspan0,
