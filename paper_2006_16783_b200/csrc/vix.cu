@@ -246,6 +246,7 @@ struct VixArgs {
     int row0, row_end;   // band rows [row0, row_end)
     int zr0, zr1;        // held terrain rows [zr0, zr1)
     int pv, pt, st_off;  // skip map: SV row pitch, ST column pitch, ST offset (int16 entries)
+    uint32_t s_mul;      // ceil(2^32 / S) (0: divide): floor(x / S) = umulhi(x, s_mul) while x S < 2^32
 };
 
 template <bool SMEM, int ILP>
@@ -657,6 +658,11 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
     // 16-step skip groups (roi < 150): failing units walk the terrain, no quad planes
     constexpr bool TERR = SKIP == 1 && GS == 4;
     const int lane = threadIdx.x & 31;
+    // mag = ceil(2^16 m / M) for every M <= 255: floor(x / M) = (x * ceil(2^40 / M)) >> 40
+    // exactly for x < 2^24 (the error x (ceil - 2^40/M) / 2^40 < 2^-16 < 1/M)
+    __shared__ unsigned long long s_rcp40[256];
+    for (int d = threadIdx.x; d < 256; d += blockDim.x) s_rcp40[d] = d ? ((1ull << 40) + d - 1) / d : 0ull;
+    __syncthreads();
     const int R2 = a.R * a.R;
     unsigned long long n_cross = 0;
     int n_posts = 0;
@@ -705,7 +711,7 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
             // skip map (k_skipmap): padded 4x4-block indices of the start post,
             // SV row-major for column-major walks, ST column-major for row-major ones
             const int maj = tr ? y : x, mnr = tr ? x : y;
-            const int mag = nM ? (nm * 65536 + nM - 1) / nM : 0;
+            const int mag = (int)(((unsigned long long)(nm * 65536 + nM - 1) * s_rcp40[nM]) >> 40);   // 0 when M = 0
             g.c.soff = tr ? a.st_off + ((maj >> GS) + 1) + ((mnr >> GS) + 1) * a.pt
                           : ((maj >> GS) + 1) + ((mnr >> GS) + 1) * a.pv;
             const int D = rev ? E - Zt : Zt - E;
@@ -730,7 +736,8 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
             vism = __ballot_sync(kFull, vis);
         }
         // visible counts of the ring slots in this batch (posts p0 .. p1)
-        const int p0 = p_open + tq / a.S, p1 = p_open + (tq + ns - 1) / a.S;
+        const int p0 = p_open + (a.s_mul ? (int)__umulhi((unsigned)tq, a.s_mul) : tq / a.S);
+        const int p1 = p_open + (a.s_mul ? (int)__umulhi((unsigned)(tq + ns - 1), a.s_mul) : (tq + ns - 1) / a.S);
         for (int pp = p0; pp <= p1; ++pp) {
             const int cj = __popc(vism & __ballot_sync(kFull, lane < ns && pj == (pp & (kRing - 1))));
             if (lane == (pp & (kRing - 1))) mycnt += cj;
@@ -878,6 +885,8 @@ __global__ void k_los_batch(const int16_t* __restrict__ z, int nrows, int ncols,
 txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     VixArgs a;
     a.R = p.roi; a.ht = p.tx_height; a.hr = p.rx_height; a.S = p.samples_per_point;
+    // exact while x S < 2^32 for the x < 16 S + 32 it is applied to; larger S divides
+    a.s_mul = a.S > 0 && a.S < 4096 ? (uint32_t)(((1ull << 32) + (uint64_t)a.S - 1) / (uint64_t)a.S) : 0u;
     a.seed = p.seed;
     a.span = make_fastmod((uint64_t)(2 * p.roi + 1));
     a.tiles_x = (int)((c->ncols + kTile - 1) / kTile);
