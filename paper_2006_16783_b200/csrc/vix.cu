@@ -795,12 +795,12 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
             ++p_next;
             // ---- draw S receivers (D6) into the FIFO ----
             int nacc = 0;
-            for (uint64_t k = 0; nacc < a.S; k += 32) {
-                const int v = (int)fm_mod(a.span, sm_draw(base, k + lane)) - a.R;
+            for (uint32_t k = 0; nacc < a.S; k += 32) {   // draw k + lane of the post's stream
+                const int v = (int)fm_mod(a.span, sm_finalize(base + (uint64_t)(k + lane + 1) * kGamma)) - a.R;
                 const int dc = __shfl_down_sync(kFull, v, 1);
                 const int dr = v;
-                const bool ok = !(lane & 1) && dr * dr + dc * dc <= R2 && r + dr >= 0 && r + dr < nrows &&
-                                c + dc >= 0 && c + dc < ncols;
+                const bool ok = !(lane & 1) && dr * dr + dc * dc <= R2 && (unsigned)(r + dr) < (unsigned)nrows &&
+                                (unsigned)(c + dc) < (unsigned)ncols;
                 const unsigned mask = __ballot_sync(kFull, ok);
                 const int take = min(__popc(mask), a.S - nacc);
                 if (ok) {
