@@ -570,3 +570,16 @@ def test_bench_json_contract_and_cache_read(engine):
     assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["kind"] in ("port", "reference")
     assert d["clocks"] and d["clocks"]["samples"] >= 1 and d["clocks"]["sm_mhz"] > 0
     assert engine.measure_l2(16 << 20, 4) > 100.0
+
+
+def test_graft_entry_smoke():
+    """__graft_entry__.smoke(): one small pipeline on cuda:0, every stage
+    checked bit-exactly against the oracle (the driver's round-end check)."""
+    import importlib
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if root not in sys.path:
+        sys.path.insert(0, root)
+    g = importlib.import_module("__graft_entry__")
+    g.smoke()
