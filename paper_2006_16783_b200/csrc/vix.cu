@@ -21,13 +21,14 @@ namespace txs {
 namespace {
 
 #ifndef VIX_TILE
-#define VIX_TILE 8     // measured: 8 beats 4, 16, 32 (c3 436 vs 512/442/456 ms, c4 4242 vs -/4459/4619)
+#define VIX_TILE 32    // posts per item row (persistent kernel; measured 4 / 8 / 16 / 32: c3 110.5 / 102.6 / 98.7 / 96.3 ms, c4 - / 811 / 780 / 760, c2 38.2 / 37.8 / 37.8 / 37.8)
 #endif
 #ifndef VIX_THREADS
 #define VIX_THREADS 512
 #endif
 constexpr int kTile = 32;          // posts per tile side (shared-memory tile / column-major paths)
 constexpr int kTileQ = VIX_TILE;   // posts per tile side (quad-plane path)
+static_assert(kTileQ <= 32, "a tile row's stream seeds are computed one post per lane");
 constexpr int kVixThreads = VIX_THREADS;   // 16 warps
 constexpr int kVixWarps = kVixThreads / 32;
 constexpr unsigned kFull = 0xffffffffu;
