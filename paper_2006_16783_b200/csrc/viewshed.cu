@@ -643,7 +643,7 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
     // read overlapping terrain windows (L2 reuse; config 5's observers are
     // random over a 537 MB terrain).  Output slots keep candidate order.
     if (n >= 4096) {
-        int tshift = 6;   // 64x64-post observer tiles
+        int tshift = 4;   // 16x16-post observer tiles (measured 4 / 5 / 6: c5 1262 / 1264 / 1276 ms, c2 / c3 flat)
         if (const char* e = getenv("TXS_VS_TILE_SHIFT")) tshift = std::max(0, std::min(12, atoi(e)));
         const int tiles_x = (int)((c->ncols + (1 << tshift) - 1) >> tshift);
         size_t tmp_bytes = 0;
