@@ -639,7 +639,7 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
     if (n == 0) return TXS_OK;
     VsArgs a{(int)c->nrows, (int)c->ncols, p.roi, p.tx_height, p.rx_height, T->nrays, mw, nullptr, n, 0, 0, 0,
              nullptr, 0, 0, 0};
-    // Process observers in 64x64-tile order so the CTAs resident at any moment
+    // Process observers in 16x16-tile order so the CTAs resident at any moment
     // read overlapping terrain windows (L2 reuse; config 5's observers are
     // random over a 537 MB terrain).  Output slots keep candidate order.
     if (n >= 4096) {
