@@ -380,7 +380,7 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
             bool ok[2][K];
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-                ee[u] = st0 + u < grp.y ? __ldg(ev + (int64_t)(st0 + u) * 32) : make_uint2((uint32_t)kEvNop, 0u);
+                ee[u] = __ldg(ev + (int64_t)(st0 + u) * 32);   // groups hold an even number of steps
                 const uint32_t e = ee[u].x, type = e & 7u;
                 const int dr = ((int)(e << 20)) >> 23, dc = ((int)(e << 11)) >> 23;
                 const bool isrow = type == kEvRow, iscol = type == kEvCol;
