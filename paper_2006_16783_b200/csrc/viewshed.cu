@@ -342,6 +342,7 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
     int Ehr[K];
     uint32_t sb[K];                      // shared byte address of bitmap k
     const int RS0 = RSk[0], K00 = K0k[0];   // identical for every interior observer
+    const int p2 = a.p2, pw = a.pw;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         if (PAIRS) {
@@ -372,7 +373,7 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
 #pragma unroll
         for (int k = 0; k < K; ++k) { NH[k] = -(1 << 30); MH[k] = 1; L2MH[k] = L2; alive[k] = true; }
         const uint2* ev = events + (int64_t)grp.x * 32 + lane;
-        for (int st0 = 0; st0 < grp.y; st0 += 2) {
+        for (int st0 = 0; st0 < grp.y; st0 += 2, ev += 64) {
             uint2 ee[2];
             uint32_t pr[2][K];
             int z0[2][K], z1[2][K];
@@ -380,7 +381,7 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
             bool ok[2][K];
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-                ee[u] = __ldg(ev + (int64_t)(st0 + u) * 32);   // groups hold an even number of steps
+                ee[u] = __ldg(ev + u * 32);   // groups hold an even number of steps
                 const uint32_t e = ee[u].x, type = e & 7u;
                 const int dr = ((int)(e << 20)) >> 23, dc = ((int)(e << 11)) >> 23;
                 const bool isrow = type == kEvRow, iscol = type == kEvCol;
@@ -391,7 +392,7 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
                                          (unsigned)(ck[k] + dc) < (unsigned)(a.ncols - (isrow ? 1 : 0)));
                 }
                 if (PAIRS) {   // the first post's H pair (its right neighbour) or, column crossing, V pair
-                    const int off = type != kEvNop ? dr * a.p2 + dc + (iscol ? a.pw : 0) : 0;
+                    const int off = dr * p2 + dc + (iscol ? pw : 0);   // Nop events carry dr = dc = 0
 #pragma unroll
                     for (int k = 0; k < K; ++k) pr[u][k] = (!EDGE || ok[u][k]) ? vs_pld(B[k] + off) : 0u;
                 } else {
