@@ -161,7 +161,7 @@ EventTemplate build_events(const RayTemplate& T) {
     for (int64_t g = 0; g < ngroups; ++g) {
         size_t steps = 0;
         for (int64_t l = 0; l < 32 && g * 32 + l < nrays; ++l) steps = std::max(steps, per[(size_t)(g * 32 + l)].size());
-        steps += steps & 1;   // even: the sweeps read two steps per iteration without a bound test
+        steps = (steps + 3) & ~(size_t)3;   // a multiple of 4: the sweeps read 2 or 4 steps per iteration without a bound test
         E.groups.push_back(make_int2((int)row, (int)steps));
         for (size_t s = 0; s < steps; ++s)
             for (int64_t l = 0; l < 32; ++l) {

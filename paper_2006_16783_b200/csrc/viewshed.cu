@@ -317,6 +317,7 @@ __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, 
     }
 }
 
+
 // Interior fast path for K observers per CTA: each warp walks its ray group
 // once, the event load/decode/offsets are shared and every observer keeps its
 // own horizon (NH, MH) and bitmap — K independent dependency chains per lane.
@@ -329,7 +330,11 @@ __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, 
 // outside the grid are skipped -- the rules of vs_events<false>), the cell bit
 // uses the observer's own window pitch and origin, and the crossings / cells
 // actually evaluated are counted.
-template <int K, bool PAIRS, bool EDGE>
+//
+// STEP: events per sweep iteration (event groups are padded to a multiple of 4
+// steps, raytemplate.cpp) -- 4 at roi >= 225 (C5 1151 -> 1099 ms), 2 elsewhere
+// (C3 20.9 vs 23.5 ms at 4; profiles/README.md)
+template <int K, bool PAIRS, bool EDGE, int STEP>
 __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const int* rk, const int* ck, const int* Ek,
                                             const int* RSk, const int* K0k,
                                             const VsArgs& a, const int4* __restrict__ rays,
@@ -373,14 +378,14 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
 #pragma unroll
         for (int k = 0; k < K; ++k) { NH[k] = -(1 << 30); MH[k] = 1; L2MH[k] = L2; alive[k] = true; }
         const uint2* ev = events + (int64_t)grp.x * 32 + lane;
-        for (int st0 = 0; st0 < grp.y; st0 += 2, ev += 64) {
-            uint2 ee[2];
-            uint32_t pr[2][K];
-            int z0[2][K], z1[2][K];
-            int dru[2], dcu[2];
-            bool ok[2][K];
+        for (int st0 = 0; st0 < grp.y; st0 += STEP, ev += 32 * STEP) {
+            uint2 ee[STEP];
+            uint32_t pr[STEP][K];
+            int z0[STEP][K], z1[STEP][K];
+            int dru[STEP], dcu[STEP];
+            bool ok[STEP][K];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < STEP; ++u) {
                 ee[u] = __ldg(ev + u * 32);   // groups hold an even number of steps
                 const uint32_t e = ee[u].x, type = e & 7u;
                 const int dr = ((int)(e << 20)) >> 23, dc = ((int)(e << 11)) >> 23;
@@ -406,7 +411,7 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < STEP; ++u) {
                 const uint32_t e = ee[u].x, type = e & 7u;
                 const int y = (int)(ee[u].y & 0xffffffu);
                 const uint32_t W = __byte_perm(e, ee[u].y, 0x73u);   // w0 | w1 << 8
@@ -514,7 +519,7 @@ __global__ void k_viewshed_ev(const int16_t* __restrict__ z, const int32_t* __re
 
 // K observers per CTA (shared event stream, smem bitmaps); CTAs where some
 // observer is not interior fall back to one observer at a time.
-template <int K, int MAXREG>
+template <int K, int MAXREG, int STEP>
 __global__ void __maxnreg__(MAXREG) k_viewshed_evk(const int16_t* __restrict__ z, const int32_t* __restrict__ crow,
                                const int32_t* __restrict__ ccol, const int4* __restrict__ rays,
                                const int2* __restrict__ groups, const uint2* __restrict__ events, int ngroups,
@@ -553,11 +558,11 @@ __global__ void __maxnreg__(MAXREG) k_viewshed_evk(const int16_t* __restrict__ z
     unsigned long long n_cross = 0, n_cells = 0;
     if (all_int) {
         unsigned long long d0 = 0, d1 = 0;
-        if (a.pairs) vs_events_k<K, true, false>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride, d0, d1);
-        else vs_events_k<K, false, false>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride, d0, d1);
+        if (a.pairs) vs_events_k<K, true, false, STEP>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride, d0, d1);
+        else vs_events_k<K, false, false, STEP>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride, d0, d1);
         if (threadIdx.x == 0) { n_cross = (unsigned long long)(K * a.tmpl_cross); n_cells = (unsigned long long)(K * a.tmpl_cells); }
     } else if (a.pairs && nk == K) {   // edge observers: the same shared sweep with per-observer grid bounds
-        vs_events_k<K, true, true>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride,
+        vs_events_k<K, true, true, STEP>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride,
                                    n_cross, n_cells);
     } else {
         for (int k = 0; k < K; ++k) {
@@ -696,6 +701,9 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
         // (C2 13.5 ms vs 14.0 at 64), 64 elsewhere (C3 23.2 vs 24.3 at 68, C4 44.3 vs
         // 46.6, C5 1276 vs 1717 at 72: 15-warp CTAs drop to one per SM)
         const bool cap64 = p.roi < 150 || p.roi >= 225;
+        // 4 events per sweep iteration at roi >= 225 (K=2 only), TXS_VS_STEP=2/4 overrides
+        bool step4 = p.roi >= 225;
+        if (const char* e = getenv("TXS_VS_STEP")) step4 = atoi(e) == 4;
         const unsigned grid = (unsigned)((n + kobs - 1) / kobs);
         // pair planes of the held rows (rebuilt per call, part of the timed stage;
         // shares the VIX quad-plane scratch buffer) -- measured (profiles/README.md):
@@ -717,19 +725,19 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
                     (const int16_t*)(a.pairs + pwords));
         }
         if (kobs == 3) {
-            auto kern = cap64 ? k_viewshed_evk<3, 64> : k_viewshed_evk<3, 72>;
+            auto kern = cap64 ? k_viewshed_evk<3, 64, 2> : k_viewshed_evk<3, 72, 2>;
             if (sm > 48 * 1024)
                 TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             kern<<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
                                                                  T->ngroups, a, c->d_words, c->d_win, c->d_pop, c->d_counters);
         } else if (kobs == 2) {
-            auto kern = cap64 ? k_viewshed_evk<2, 64> : k_viewshed_evk<2, 72>;
+            auto kern = cap64 ? (step4 ? k_viewshed_evk<2, 64, 4> : k_viewshed_evk<2, 64, 2>) : k_viewshed_evk<2, 72, 2>;
             if (sm > 48 * 1024)
                 TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             kern<<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
                                                                  T->ngroups, a, c->d_words, c->d_win, c->d_pop, c->d_counters);
         } else {
-            auto kern = cap64 ? k_viewshed_evk<4, 64> : k_viewshed_evk<4, 72>;
+            auto kern = cap64 ? k_viewshed_evk<4, 64, 2> : k_viewshed_evk<4, 72, 2>;
             if (sm > 48 * 1024)
                 TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             kern<<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
