@@ -115,7 +115,10 @@ RayTemplate build(int32_t R) {
 // row whatever the ray's direction, so the GPU can read it as one packed pair);
 // posts carry (n, 0), cells (1, 0).
 inline uint2 pack_ev(uint32_t type, int dr, int dc, int w0, int w1, int64_t y) {
-    return make_uint2(type | ((uint32_t)(dr & 0x1ff) << 3) | ((uint32_t)(dc & 0x1ff) << 12) | ((uint32_t)w0 << 24),
+    // bits 12..21 hold 2*dc + (column crossing): the word offset of the crossing's
+    // pair in the interleaved (H, V) pair planes, one IMAD from dr (viewshed.cu)
+    const uint32_t f = (uint32_t)(2 * dc + (type == kEvCol ? 1 : 0)) & 0x3ffu;
+    return make_uint2(type | ((uint32_t)(dr & 0x1ff) << 3) | (f << 12) | ((uint32_t)w0 << 24),
                       (uint32_t)y | ((uint32_t)w1 << 24));
 }
 

@@ -32,12 +32,13 @@ struct VsArgs {
     int sbits;            // smem bitmap u32 words per observer: (2R+1) rows x (2*Wmax+1) (odd pitch)
     long long tmpl_cross, tmpl_cells;   // template crossings / cells (interior observers)
     const uint32_t* pairs;  // pair planes of the held rows (interior K-observer path), or null
-    int p2, pw;             // pair-plane row pitch (words) and V-plane offset inside a row
+    int p2, pw;             // pair-plane row pitch (words, 2*pw) and posts per plane row
     int zoff;               // first held terrain row
 };
 
 // Pair planes for the interior K-observer sweep: held row y occupies p2 = 2*pw
-// words, [H pairs | V pairs], H[x] = z(y,x) | z(y,x+1) << 16 and
+// words, (H, V) interleaved per post (word 2x + 1 for a column crossing, so an
+// event's pair offset is dr*p2 + 2*dc + col), H[x] = z(y,x) | z(y,x+1) << 16 and
 // V[x] = z(y,x) | z(y+1,x) << 16 (0 past the last column / held row).  A grid
 // crossing interpolates between exactly such a pair, so one 32-bit load and one
 // dp2a (signed 16-bit halves x unsigned weight bytes, exact) replace two
@@ -55,8 +56,7 @@ __global__ void k_vs_pairs(const int16_t* __restrict__ z, uint32_t* __restrict__
             vv = a | ((y + 1 < H ? (uint32_t)(uint16_t)zr[x + ncols] : 0u) << 16);
         }
         uint32_t* row = out + (int64_t)y * 2 * pw;
-        row[x] = hv;
-        row[pw + x] = vv;
+        reinterpret_cast<uint2*>(row)[x] = make_uint2(hv, vv);   // interleaved: (H, V) per post
     }
 }
 
@@ -272,7 +272,7 @@ __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, 
 #pragma unroll
             for (int u = 0; u < kVsUnroll; ++u) {
                 const uint32_t e = ee[u].x, type = e & 7u;
-                const int dr = ((int)(e << 20)) >> 23, dc = ((int)(e << 11)) >> 23;
+                const int dr = ((int)(e << 20)) >> 23, F = ((int)(e << 10)) >> 22, dc = F >> 1;
                 const bool isrow = type == kEvRow, iscol = type == kEvCol;
                 bool inb = type != kEvNop;
                 if (!INTERIOR) {   // both interpolation posts in the grid
@@ -347,13 +347,13 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
     int Ehr[K];
     uint32_t sb[K];                      // shared byte address of bitmap k
     const int RS0 = RSk[0], K00 = K0k[0];   // identical for every interior observer
-    const int p2 = a.p2, pw = a.pw;
+    const int p2 = a.p2;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         if (PAIRS) {
             // (threadIdx.x >> 10) == 0 but not provably so: B lives in per-thread
             // registers, and B + off becomes one IMAD.WIDE instead of a 64-bit add chain
-            B[k] = a.pairs + (int64_t)(rk[k] - a.zoff) * a.p2 + ck[k] + (threadIdx.x >> 10);
+            B[k] = a.pairs + (int64_t)(rk[k] - a.zoff) * a.p2 + 2 * ck[k] + (threadIdx.x >> 10);
             asm("mov.b64 %0, %0;" : "+l"(B[k]));
         } else {
             P[k] = z + (int64_t)rk[k] * a.ncols + ck[k];
@@ -388,16 +388,16 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
             for (int u = 0; u < STEP; ++u) {
                 ee[u] = __ldg(ev + u * 32);   // groups hold an even number of steps
                 const uint32_t e = ee[u].x, type = e & 7u;
-                const int dr = ((int)(e << 20)) >> 23, dc = ((int)(e << 11)) >> 23;
+                const int dr = ((int)(e << 20)) >> 23, F = ((int)(e << 10)) >> 22, dc = F >> 1;
                 const bool isrow = type == kEvRow, iscol = type == kEvCol;
-                dru[u] = dr; dcu[u] = dc;
+                dru[u] = dr; dcu[u] = F;   // dc = F >> 1
 #pragma unroll
                 for (int k = 0; k < K; ++k) {   // both interpolation posts (or the cell) in the grid
                     ok[u][k] = !EDGE || (type != kEvNop && (unsigned)(rk[k] + dr) < (unsigned)(a.nrows - (iscol ? 1 : 0)) &&
                                          (unsigned)(ck[k] + dc) < (unsigned)(a.ncols - (isrow ? 1 : 0)));
                 }
                 if (PAIRS) {   // the first post's H pair (its right neighbour) or, column crossing, V pair
-                    const int off = dr * p2 + dc + (iscol ? pw : 0);   // Nop events carry dr = dc = 0
+                    const int off = dr * p2 + F;   // F = 2*dc + iscol; Nop events carry dr = F = 0
 #pragma unroll
                     for (int k = 0; k < K; ++k) pr[u][k] = (!EDGE || ok[u][k]) ? vs_pld(B[k] + off) : 0u;
                 } else {
@@ -419,7 +419,7 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
                 const bool iscell = type == kEvCell, iscross = type <= kEvPost;
                 // interior observers share the window geometry (pitch 2R+1, origin
                 // bit R*(2R+1)+R): the cell's word and bit are observer-independent
-                const int kk = dru[u] * RS0 + dcu[u] + K00;
+                const int kk = dru[u] * RS0 + (dcu[u] >> 1) + K00;
                 const uint32_t cw4 = (uint32_t)(kk >> 5) << 2, cbit = 1u << (kk & 31);
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
@@ -440,7 +440,7 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
                     MH[k] = up ? y : MH[k];
                     L2MH[k] = up ? L2 * y : L2MH[k];
                     if (EDGE) {
-                        const int kb = dru[u] * RSk[k] + dcu[u] + K0k[k];
+                        const int kb = dru[u] * RSk[k] + (dcu[u] >> 1) + K0k[k];
                         red_or_shared(sb[k] + ((uint32_t)(kb >> 5) << 2), 1u << (kb & 31), setc & (lhs >= rhs));
                     } else {
                         red_or_shared(sb[k] + cw4, cbit, setc & (lhs >= rhs));
