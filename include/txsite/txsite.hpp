@@ -15,7 +15,7 @@
 #include <string>
 #include <vector>
 
-struct txs_ctx;
+#include "../txsite_b200.h"
 
 namespace txsite {
 
@@ -43,7 +43,8 @@ double elevation_between(const TerrainGrid& g, GridPoint p, GridPoint q, double 
 struct ObserverSpec { GridPoint base; int32_t height = 0; };
 bool is_visible(const TerrainGrid& g, const ObserverSpec& tx, const ObserverSpec& rx);
 std::vector<uint8_t> is_visible_batch(const TerrainGrid& g, const std::vector<GridPoint>& tx,
-                                      const std::vector<GridPoint>& rx, int32_t ht, int32_t hr);
+                                      const std::vector<GridPoint>& rx, int32_t ht, int32_t hr,
+                                      int32_t los_arith = TXS_LOS_FP64);
 
 // ---- params ----------------------------------------------------------
 struct SiteParams {
@@ -55,6 +56,7 @@ struct SiteParams {
     int32_t block_width = 0;     // 0 => ceil(roi/3)
     int64_t max_selected = 0;    // 0 => unlimited
     int32_t site_mode = 0;       // 0 incremental exact gains, 1 full rescan
+    int32_t los_arith = TXS_LOS_FP64;   // SPEC.md:147 fp64 (default) or TXS_LOS_EXACT
 };
 
 // ---- vix ---------------------------------------------------------

@@ -50,6 +50,14 @@ typedef enum txs_stop {
     TXS_STOP_MAX_SELECTED = 3
 } txs_stop;
 
+/* LOS arithmetic (txs_params.los_arith; DESIGN.md §2 D2).  TXS_LOS_FP64 is
+ * SPEC.md:147's formula ("All LOS arithmetic in double-precision floating
+ * point"): VIX/LOS decisions and viewshed bits identical to the fp64 oracle.
+ * TXS_LOS_EXACT is SPEC.md:120's real-number predicate in exact integers; the
+ * two differ only where the terrain touches the LOS exactly (grazing ties,
+ * ~1e-4 of LOS decisions), which fp64 rounding decides either way. */
+typedef enum txs_los_arith { TXS_LOS_FP64 = 0, TXS_LOS_EXACT = 1 } txs_los_arith;
+
 /* SiteParams plus the knobs the BASELINE configs need. */
 typedef struct txs_params {
     int32_t roi;               /* radius of interest in posts, >= 1                       */
@@ -59,7 +67,7 @@ typedef struct txs_params {
     int32_t per_block;         /* FINDMAX top-k per block (default 20)                     */
     int32_t block_width;       /* 0 => ceil(roi/3); BASELINE fixes it        */
     int32_t site_mode;         /* 0 = exact incremental gains, 1 = full rescan each round  */
-    int32_t _reserved;
+    int32_t los_arith;         /* TXS_LOS_FP64 (0, default) or TXS_LOS_EXACT (1), below      */
     double target_coverage;    /* (0,1]                                                    */
     int64_t max_selected;      /* 0 => unlimited                             */
     uint64_t seed;             /* VIX sampling seed                          */
@@ -88,6 +96,11 @@ typedef struct txs_stats {
     int64_t candidates;
     int64_t kernel_launches;        /* every kernel this context launched since reset        */
     double ms_site_rounds;          /* device time of the SITE round loop alone (no setup)   */
+    /* fp64 LOS arithmetic (TXS_LOS_FP64): exact grazing ties found by the exact
+     * walks and re-decided with SPEC.md:147's formula, and how many of those
+     * decisions fp64 rounding changed (VIX: segments; VIEWSHED: rays / bits). */
+    int64_t vix_fp64_ties, vix_fp64_flips;
+    int64_t vs_fp64_ties, vs_fp64_flips;
 } txs_stats;
 
 typedef struct txs_ctx txs_ctx;
@@ -119,9 +132,10 @@ txs_status txs_get_terrain(txs_ctx* ctx, int16_t* z_out);
 txs_status txs_terrain_dims(const txs_ctx* ctx, int64_t* nrows, int64_t* ncols);
 
 /* ---- los module — batch form for parity tests --------------- */
-/* pairs: n x {tx_row, tx_col, rx_row, rx_col}; out: n bytes 0/1. */
+/* pairs: n x {tx_row, tx_col, rx_row, rx_col}; out: n bytes 0/1; los_arith as
+ * in txs_params. */
 txs_status txs_is_visible_batch(txs_ctx* ctx, const int32_t* pairs, int64_t n, int32_t tx_height,
-                                int32_t rx_height, uint8_t* out);
+                                int32_t rx_height, int32_t los_arith, uint8_t* out);
 
 /* ---- vix module (SPEC.md:176 estimate_vix) ------------------------------------ */
 txs_status txs_estimate_vix(txs_ctx* ctx, const txs_params* p, uint8_t* scores_out);

@@ -159,7 +159,7 @@ bool is_visible(const Grid& g, int64_t tr, int64_t tc, int64_t ht,
 // ---------------------------------------------------------------------------
 void estimate_vix(const Grid& g, int64_t roi, int64_t ht, int64_t hr, int64_t samples,
                   uint64_t seed, unsigned threads, uint8_t* scores,
-                  int64_t row_begin, int64_t row_end) {
+                  int64_t row_begin, int64_t row_end, int arith) {
     const int64_t rows = row_end - row_begin;
     const uint64_t span = (uint64_t)(2 * roi + 1);
     const int64_t R2 = roi * roi;
@@ -175,7 +175,7 @@ void estimate_vix(const Grid& g, int64_t roi, int64_t ht, int64_t hr, int64_t sa
                     dc = (int64_t)s.next_below(span) - roi;
                     if (dr * dr + dc * dc <= R2 && g.in(r + dr, c + dc)) break;
                 }
-                vis += is_visible(g, r, c, ht, r + dr, c + dc, hr) ? 1 : 0;
+                vis += is_visible_arith(g, r, c, ht, r + dr, c + dc, hr, arith) ? 1 : 0;
             }
             scores[r * g.ncols + c] = (uint8_t)vis;
         }
@@ -297,14 +297,15 @@ Window window_of(int64_t nrows, int64_t ncols, int64_t r, int64_t c, int64_t R) 
 // of terrain tangents (z-E)/(u_k*L) over in-grid crossings with u_k < u_c,
 // u_c = dot/L^2 its projection (exact cross-multiplied integers).
 void compute_viewshed(const Grid& g, int64_t r, int64_t c, int64_t R, int64_t ht, int64_t hr,
-                      Window* win_out, uint64_t* words) {
+                      Window* win_out, uint64_t* words, uint64_t* ties) {
     const RayTemplate& T = ray_template(R);
     const Window win = window_of(g.nrows, g.ncols, r, c, R);
     *win_out = win;
     std::fill(words, words + window_words(win), 0ull);
-    auto setbit = [&](int64_t rr, int64_t cc) {
+    if (ties) std::fill(ties, ties + window_words(win), 0ull);
+    auto setbit = [&](int64_t rr, int64_t cc, uint64_t* w = nullptr) {
         const int64_t k = (rr - win.row0) * win.w + (cc - win.col0);
-        words[k >> 6] |= 1ull << (k & 63);
+        (w ? w : words)[k >> 6] |= 1ull << (k & 63);
     };
     setbit(r, c);
     const int64_t E = g.at(r, c) + ht;
@@ -326,6 +327,7 @@ void compute_viewshed(const Grid& g, int64_t r, int64_t c, int64_t R, int64_t ht
             if (!g.in(rr, cc)) return;
             const int64_t P = g.at(rr, cc) + hr - E, dot = a * p + b * q;
             if (!has || P * L2 * MH >= NH * dot) setbit(rr, cc);
+            if (ties && has && P * L2 * MH == NH * dot) setbit(rr, cc, ties);   // tangent == horizon
         };
         const int64_t dr = K * p, dc = K * q;
         const int64_t nr = std::llabs(dr), nc = std::llabs(dc);
@@ -357,6 +359,112 @@ void compute_viewshed(const Grid& g, int64_t r, int64_t c, int64_t R, int64_t ht
             if (ci == ce || !ok) return false;   // done, or left the grid (prefix)
             const int64_t N = zn - E * n, M = K * idx;
             if (!has || N * MH > NH * M) { has = true; NH = N; MH = M; }
+            return true;
+        });
+        while (ci < ce) test(ci++);
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// fp64 forms ("All LOS arithmetic in double-precision floating
+// point"), the reference formula: the restated walk's doubles (bit-identical
+// to grid_walk.hpp:27-77, pinned in tests/test_oracle_kat.py), interpolation
+// z0*(1-f) + z1*f with f = frac(col), LOS height E + t*(Zt-E);
+// built -ffp-contract=off, so every operation is one IEEE rounding.
+// ---------------------------------------------------------------------------
+static inline bool interp_fp64(const Grid& g, int64_t tr, int64_t tc, const Crossing& x, double* zt) {
+    int64_t r0, c0, r1, c1;
+    double f;
+    if (x.kind == Post) {
+        r0 = r1 = tr + std::llround(x.row); c0 = c1 = tc + std::llround(x.col); f = 0.0;
+        if (!g.in(r0, c0)) return false;
+        *zt = (double)g.at(r0, c0);
+        return true;
+    }
+    if (x.kind == RowLine) {
+        const double cf = std::floor(x.col);
+        f = x.col - cf;
+        r0 = r1 = tr + std::llround(x.row); c0 = tc + (int64_t)cf; c1 = c0 + 1;
+    } else {
+        const double rf = std::floor(x.row);
+        f = x.row - rf;
+        c0 = c1 = tc + std::llround(x.col); r0 = tr + (int64_t)rf; r1 = r0 + 1;
+    }
+    if (!g.in(r0, c0) || !g.in(r1, c1)) return false;
+    *zt = (double)g.at(r0, c0) * (1.0 - f) + (double)g.at(r1, c1) * f;
+    return true;
+}
+
+bool is_visible_fp64(const Grid& g, int64_t tr, int64_t tc, int64_t ht,
+                     int64_t rr, int64_t rc, int64_t hr) {
+    const double E = (double)g.at(tr, tc) + (double)ht, Zt = (double)g.at(rr, rc) + (double)hr;
+    return walk(0, 0, rr - tr, rc - tc, false, [&](const Crossing& x) {
+        double zt = 0.0;
+        interp_fp64(g, tr, tc, x, &zt);
+        return !(zt > E + x.t * (Zt - E));
+    });
+}
+
+bool is_visible_arith(const Grid& g, int64_t tr, int64_t tc, int64_t ht,
+                      int64_t rr, int64_t rc, int64_t hr, int arith) {
+    return arith == ArithExact ? is_visible(g, tr, tc, ht, rr, rc, hr)
+                               : is_visible_fp64(g, tr, tc, ht, rr, rc, hr);
+}
+
+// compute_viewshed in fp64 (SPEC.md:321 tangent = rise over 2D
+// run).  A crossing's tangent is SURVEY Appendix A D4's key (z - eye) /
+// sqrt(row^2 + col^2) on the walk's own doubles; a cell's run is its distance
+// along its owner ray (D5), dot / sqrt(L2) -- so in real numbers this is exactly
+// compute_viewshed's predicate, and the two differ only where a cell's tangent
+// EQUALS the horizon (a grazing tie, decided by fp64 rounding).  euclid = true
+// takes the cell's own distance sqrt(a^2 + b^2) instead (D4 verbatim; used only
+// to count the bits that choice moves, tests/test_oracle_spec.py).  Horizon =
+// max over the owner ray's in-grid crossings before the cell (the exact u order
+// of compute_viewshed); cell visible iff its tangent >= the horizon.
+void compute_viewshed_fp64(const Grid& g, int64_t r, int64_t c, int64_t R, int64_t ht, int64_t hr,
+                           Window* win_out, uint64_t* words, bool euclid) {
+    const RayTemplate& T = ray_template(R);
+    const Window win = window_of(g.nrows, g.ncols, r, c, R);
+    *win_out = win;
+    std::fill(words, words + window_words(win), 0ull);
+    auto setbit = [&](int64_t rr, int64_t cc) {
+        const int64_t k = (rr - win.row0) * win.w + (cc - win.col0);
+        words[k >> 6] |= 1ull << (k & 63);
+    };
+    setbit(r, c);
+    const double E = (double)g.at(r, c) + (double)ht;
+    const int64_t nrays = (int64_t)T.p.size();
+    for (int64_t ri = 0; ri < nrays; ++ri) {
+        const int64_t cb = T.cell_begin[ri], ce = T.cell_begin[ri + 1];
+        if (cb == ce) continue;
+        const int64_t p = T.p[ri], q = T.q[ri], L2 = p * p + q * q;
+        int64_t K = 1;
+        for (int64_t i = cb; i < ce; ++i) {
+            const int64_t d = T.ca[i] * p + T.cb[i] * q;
+            K = std::max(K, (d + L2 - 1) / L2);
+        }
+        bool has = false;
+        double H = 0.0;
+        int64_t ci = cb;
+        auto test = [&](int64_t i) {
+            const int64_t a = T.ca[i], b = T.cb[i], rr = r + a, cc = c + b;
+            if (!g.in(rr, cc)) return;
+            const double run = euclid ? std::sqrt((double)(a * a + b * b))
+                                      : (double)(a * p + b * q) / std::sqrt((double)L2);
+            const double s = ((double)g.at(rr, cc) + (double)hr - E) / run;
+            if (!has || s >= H) setbit(rr, cc);
+        };
+        const int64_t dr = K * p, dc = K * q;
+        const int64_t nr = std::llabs(dr), nc = std::llabs(dc);
+        walk(0, 0, dr, dc, false, [&](const Crossing& x) {
+            const bool byc = x.kind == ColLine || (x.kind == Post && nr == 0);
+            const int64_t n = byc ? nc : nr, idx = byc ? x.ic : x.ir;
+            while (ci < ce && (T.ca[ci] * p + T.cb[ci] * q) * n <= K * idx * L2) test(ci++);
+            double zt = 0.0;
+            if (ci == ce || !interp_fp64(g, r, c, x, &zt)) return false;
+            const double s = (zt - E) / std::sqrt(x.row * x.row + x.col * x.col);
+            if (!has || s > H) { has = true; H = s; }
             return true;
         });
         while (ci < ce) test(ci++);

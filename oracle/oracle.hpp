@@ -114,10 +114,18 @@ int generate_fractal(int64_t nrows, int64_t ncols, double roughness, uint64_t se
 bool is_visible(const Grid& g, int64_t tr, int64_t tc, int64_t ht,
                 int64_t rr, int64_t rc, int64_t hr);
 
+// SPEC.md:147 fp64 form (the reference formula) and the selector; arith is
+// ArithFp64 (0, the default everywhere) or ArithExact (1, exact rationals).
+enum Arith : int { ArithFp64 = 0, ArithExact = 1, ArithFp64Euclid = 2 /* viewsheds only */ };
+bool is_visible_fp64(const Grid& g, int64_t tr, int64_t tc, int64_t ht,
+                     int64_t rr, int64_t rc, int64_t hr);
+bool is_visible_arith(const Grid& g, int64_t tr, int64_t tc, int64_t ht,
+                      int64_t rr, int64_t rc, int64_t hr, int arith);
+
 // ---- vix, decision D6 ---------------------------------------
 void estimate_vix(const Grid& g, int64_t roi, int64_t ht, int64_t hr, int64_t samples,
                   uint64_t seed, unsigned threads, uint8_t* scores,
-                  int64_t row_begin, int64_t row_end);
+                  int64_t row_begin, int64_t row_end, int arith = ArithFp64);
 
 // ---- candidates, decision D7 -----------------------------
 struct Cand { int32_t row, col, score; };
@@ -137,8 +145,11 @@ std::vector<std::pair<int32_t,int32_t>> midpoint_circle(int64_t roi);
 struct Window { int32_t row0, col0, h, w; };
 inline int64_t window_words(const Window& w) { return ((int64_t)w.h * w.w + 63) / 64; }
 Window window_of(int64_t nrows, int64_t ncols, int64_t r, int64_t c, int64_t roi);
+// ties (optional, window words): the cells whose tangent EQUALS their horizon
 void compute_viewshed(const Grid& g, int64_t r, int64_t c, int64_t roi, int64_t ht, int64_t hr,
-                      Window* win, uint64_t* words);
+                      Window* win, uint64_t* words, uint64_t* ties = nullptr);
+void compute_viewshed_fp64(const Grid& g, int64_t r, int64_t c, int64_t roi, int64_t ht, int64_t hr,
+                           Window* win, uint64_t* words, bool euclid = false);
 
 // ---- siting, decision D9 ---------------------------------
 enum Stop : int { TargetReached = 0, ZeroGain = 1, Exhausted = 2, MaxSelected = 3 };

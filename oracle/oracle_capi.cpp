@@ -93,27 +93,27 @@ int txo_generate_fractal(int64_t nrows, int64_t ncols, double roughness, uint64_
 }
 
 int txo_is_visible(const int16_t* z, int64_t nrows, int64_t ncols, int64_t tr, int64_t tc,
-                   int64_t ht, int64_t rr, int64_t rc, int64_t hr) {
+                   int64_t ht, int64_t rr, int64_t rc, int64_t hr, int arith) {
     Grid g{nrows, ncols, z};
-    return is_visible(g, tr, tc, ht, rr, rc, hr) ? 1 : 0;
+    return is_visible_arith(g, tr, tc, ht, rr, rc, hr, arith) ? 1 : 0;
 }
 
 void txo_is_visible_batch(const int16_t* z, int64_t nrows, int64_t ncols, const int32_t* pairs,
-                          int64_t n, int64_t ht, int64_t hr, uint8_t* out, unsigned threads) {
+                          int64_t n, int64_t ht, int64_t hr, uint8_t* out, unsigned threads, int arith) {
     Grid g{nrows, ncols, z};
     par(n, threads, [&](int64_t b, int64_t e) {
         for (int64_t i = b; i < e; ++i) {
             const int32_t* p = pairs + 4 * i;
-            out[i] = is_visible(g, p[0], p[1], ht, p[2], p[3], hr) ? 1 : 0;
+            out[i] = is_visible_arith(g, p[0], p[1], ht, p[2], p[3], hr, arith) ? 1 : 0;
         }
     });
 }
 
 void txo_estimate_vix(const int16_t* z, int64_t nrows, int64_t ncols, int64_t roi, int64_t ht,
                       int64_t hr, int64_t samples, uint64_t seed, unsigned threads,
-                      uint8_t* scores, int64_t row_begin, int64_t row_end) {
+                      uint8_t* scores, int64_t row_begin, int64_t row_end, int arith) {
     Grid g{nrows, ncols, z};
-    estimate_vix(g, roi, ht, hr, samples, seed, threads, scores, row_begin, row_end);
+    estimate_vix(g, roi, ht, hr, samples, seed, threads, scores, row_begin, row_end, arith);
 }
 
 int64_t txo_find_candidates(const uint8_t* scores, int64_t nrows, int64_t ncols, int64_t bw,
@@ -146,13 +146,14 @@ int64_t txo_template(int64_t roi, int32_t* p, int32_t* q, int64_t* cell_begin, i
 
 void txo_viewsheds(const int16_t* z, int64_t nrows, int64_t ncols, int64_t roi, int64_t ht,
                    int64_t hr, int64_t n, const int32_t* rows, const int32_t* cols,
-                   int32_t* wins, uint64_t* words, int64_t stride, unsigned threads) {
+                   int32_t* wins, uint64_t* words, int64_t stride, unsigned threads, int arith) {
     Grid g{nrows, ncols, z};
     ray_template(roi);  // build once before fanning out
     par(n, threads, [&](int64_t b, int64_t e) {
         for (int64_t i = b; i < e; ++i) {
             Window w;
-            compute_viewshed(g, rows[i], cols[i], roi, ht, hr, &w, words + i * stride);
+            if (arith == ArithExact) compute_viewshed(g, rows[i], cols[i], roi, ht, hr, &w, words + i * stride);
+            else compute_viewshed_fp64(g, rows[i], cols[i], roi, ht, hr, &w, words + i * stride, arith == ArithFp64Euclid);
             wins[4 * i] = w.row0; wins[4 * i + 1] = w.col0; wins[4 * i + 2] = w.h; wins[4 * i + 3] = w.w;
         }
     });
@@ -207,6 +208,14 @@ void txo_random_observers(int64_t nrows, int64_t ncols, int64_t n, uint64_t seed
 }  // extern "C"
 
 extern "C" {
+
+// Exact viewsheds plus the mask of their grazing-tie cells (tangent == horizon).
+void txo_viewshed_ties(const int16_t* z, int64_t nrows, int64_t ncols, int64_t roi, int64_t ht, int64_t hr,
+                       int64_t r, int64_t c, uint64_t* words, uint64_t* ties) {
+    Grid g{nrows, ncols, z};
+    Window w;
+    compute_viewshed(g, r, c, roi, ht, hr, &w, words, ties);
+}
 
 // LOS classification for tie accounting: 1 blocked, 0 visible with a crossing
 // exactly ON the LOS (grazing tie), -1 visible with clearance.

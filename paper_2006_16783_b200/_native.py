@@ -31,7 +31,7 @@ STOP = {0: "target-reached", 1: "zero-gain", 2: "exhausted", 3: "max-selected"}
 
 class Params(C.Structure):
     _fields_ = [("roi", i32), ("tx_height", i32), ("rx_height", i32), ("samples_per_point", i32),
-                ("per_block", i32), ("block_width", i32), ("site_mode", i32), ("_reserved", i32),
+                ("per_block", i32), ("block_width", i32), ("site_mode", i32), ("los_arith", i32),
                 ("target_coverage", dbl), ("max_selected", i64), ("seed", u64)]
 
 
@@ -52,7 +52,8 @@ class Stats(C.Structure):
                 ("ms_site", dbl), ("vix_los", i64), ("vix_crossings_full", i64),
                 ("viewshed_crossings", i64), ("viewshed_cells", i64), ("site_iterations", i64),
                 ("site_bytes", i64), ("site_launches", i64), ("candidates", i64),
-                ("kernel_launches", i64), ("ms_site_rounds", dbl)]
+                ("kernel_launches", i64), ("ms_site_rounds", dbl),
+                ("vix_fp64_ties", i64), ("vix_fp64_flips", i64), ("vs_fp64_ties", i64), ("vs_fp64_flips", i64)]
 
 
 def _sig(name, res, args):
@@ -77,7 +78,7 @@ _sig("txs_generate_fractal", C.c_int, [vp, i64, i64, dbl, u64, i32, i32])
 _sig("txs_fill_rows", C.c_int, [vp, i64, i64, C.c_int16])
 _sig("txs_get_terrain", C.c_int, [vp, vp])
 _sig("txs_terrain_dims", C.c_int, [vp, C.POINTER(i64), C.POINTER(i64)])
-_sig("txs_is_visible_batch", C.c_int, [vp, vp, i64, i32, i32, vp])
+_sig("txs_is_visible_batch", C.c_int, [vp, vp, i64, i32, i32, i32, vp])
 _sig("txs_estimate_vix", C.c_int, [vp, C.POINTER(Params), vp])
 _sig("txs_set_vix", C.c_int, [vp, vp])
 _sig("txs_partition", C.c_int, [i64, i64, i32, i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)])

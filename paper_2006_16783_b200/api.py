@@ -24,11 +24,16 @@ def _p(a):
     return C.c_void_p(a.ctypes.data) if a is not None else None
 
 
+LOS_ARITH = {"fp64": 0, "exact": 1}
+
+
 def make_params(roi, tx_height=10, rx_height=10, samples=10, per_block=20, block_width=0,
-                target=0.95, max_selected=0, seed=0, site_mode=0):
-    """SiteParams plus block_width / seed / max_selected / site_mode."""
+                target=0.95, max_selected=0, seed=0, site_mode=0, los_arith="fp64"):
+    """SiteParams plus block_width / seed / max_selected / site_mode /
+    los_arith ("fp64" = SPEC.md:147's formula, the default; "exact" = exact rationals)."""
     return N.Params(roi=roi, tx_height=tx_height, rx_height=rx_height, samples_per_point=samples,
-                    per_block=per_block, block_width=block_width, site_mode=site_mode, _reserved=0,
+                    per_block=per_block, block_width=block_width, site_mode=site_mode,
+                    los_arith=LOS_ARITH[los_arith],
                     target_coverage=target, max_selected=max_selected, seed=seed)
 
 
@@ -122,10 +127,11 @@ class Engine:
         return z
 
     # ---- los ------------------------------------------------------------------
-    def is_visible_batch(self, pairs, tx_height, rx_height):
+    def is_visible_batch(self, pairs, tx_height, rx_height, los_arith="fp64"):
         pairs = np.ascontiguousarray(pairs, np.int32).reshape(-1, 4)
         out = np.zeros(len(pairs), np.uint8)
-        self._chk(N.lib.txs_is_visible_batch(self._h, _p(pairs), len(pairs), tx_height, rx_height, _p(out)))
+        self._chk(N.lib.txs_is_visible_batch(self._h, _p(pairs), len(pairs), tx_height, rx_height,
+                                             LOS_ARITH[los_arith], _p(out)))
         return out
 
     # ---- vix ------------------------------------------------------------------

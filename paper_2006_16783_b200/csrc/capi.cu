@@ -36,6 +36,8 @@ txs_status check_params(txs_ctx* ctx, const char* stage, const txs_params* p, bo
     if (p->roi > 4000) return fail(ctx, TXS_ERR_RANGE, stage, "roi > 4000 exceeds the exact-arithmetic envelope");
     if (p->tx_height < 0 || p->rx_height < 0 || p->tx_height > 32767 || p->rx_height > 32767)
         return fail(ctx, TXS_ERR_INVALID_ARGUMENT, stage, "heights must be in [0, 32767]");
+    if (p->los_arith != TXS_LOS_FP64 && p->los_arith != TXS_LOS_EXACT)
+        return fail(ctx, TXS_ERR_INVALID_ARGUMENT, stage, "los_arith must be 0 (fp64) or 1 (exact)");
     if (need_vix && (p->samples_per_point < 1 || p->samples_per_point > 255))
         return fail(ctx, TXS_ERR_INVALID_ARGUMENT, stage, "samples_per_point must be in [1, 255]");
     if (!ctx->d_z) return fail(ctx, TXS_ERR_STATE, stage, "no terrain");
@@ -173,6 +175,8 @@ txs_status txs_get_stats(txs_ctx* c, txs_stats* out) {
     out->viewshed_crossings = (int64_t)h[kVsCross];
     out->viewshed_cells = (int64_t)h[kVsCells];
     out->site_bytes = (int64_t)h[kSiteBytes];
+    out->vix_fp64_flips = (int64_t)h[kVixTiesFlipped];
+    out->vs_fp64_flips = (int64_t)h[kVsTiesFlipped];
     out->candidates = c->ncand;
     out->kernel_launches = c->launches;
     return TXS_OK;
@@ -289,8 +293,9 @@ txs_status txs_terrain_dims(const txs_ctx* c, int64_t* nrows, int64_t* ncols) {
 
 // ---- los -------------------------------------------------------------------
 txs_status txs_is_visible_batch(txs_ctx* c, const int32_t* pairs, int64_t n, int32_t ht,
-                                int32_t hr, uint8_t* out) {
+                                int32_t hr, int32_t arith, uint8_t* out) {
     if (!c || (n > 0 && (!pairs || !out)) || n < 0) return TXS_ERR_INVALID_ARGUMENT;
+    if (arith != TXS_LOS_FP64 && arith != TXS_LOS_EXACT) return fail(c, TXS_ERR_INVALID_ARGUMENT, "los", "los_arith must be 0 (fp64) or 1 (exact)");
     if (!c->d_z) return fail(c, TXS_ERR_STATE, "los", "no terrain");
     if (ht < 0 || hr < 0 || ht > 32767 || hr > 32767) return fail(c, TXS_ERR_INVALID_ARGUMENT, "los", "bad heights");
     if (n == 0) return TXS_OK;
@@ -309,7 +314,7 @@ txs_status txs_is_visible_batch(txs_ctx* c, const int32_t* pairs, int64_t n, int
     TXS_CUDA(c, "los", cudaMalloc(&dp, sizeof(int32_t) * 4 * n));
     TXS_CUDA(c, "los", cudaMalloc(&dout, n));
     TXS_CUDA(c, "los", cudaMemcpyAsync(dp, pairs, sizeof(int32_t) * 4 * n, cudaMemcpyHostToDevice, c->stream));
-    txs_status st = launch_los_batch(c, dp, n, ht, hr, dout);
+    txs_status st = launch_los_batch(c, dp, n, ht, hr, arith, dout);
     if (st == TXS_OK) {
         cudaMemcpyAsync(out, dout, n, cudaMemcpyDeviceToHost, c->stream);
         cudaError_t e = cudaStreamSynchronize(c->stream);
@@ -332,11 +337,22 @@ txs_status txs_estimate_vix(txs_ctx* c, const txs_params* p, uint8_t* scores_out
     const int64_t band = c->band_r1 - c->band_r0;
     if (ensure(c, "vix", (void**)&c->d_vix, &c->vix_cap, (size_t)std::max<int64_t>(1, band * c->ncols)) != TXS_OK)
         return TXS_ERR_OUT_OF_MEMORY;
-    StageTimer t(c, &c->stats.ms_vix);
-    st = launch_vix(c, *p);
-    if (st != TXS_OK) return st;
-    st = t.stop("vix");
-    if (st != TXS_OK) return st;
+    for (int attempt = 0;; ++attempt) {
+        StageTimer t(c, &c->stats.ms_vix);
+        st = launch_vix(c, *p);
+        if (st != TXS_OK) return st;
+        st = t.stop("vix");
+        if (st != TXS_OK) return st;
+        // the fp64 tie list overflowed (never seen on the BASELINE terrains): re-run with room
+        unsigned long long nt = 0;
+        TXS_CUDA(c, "vix", cudaMemcpy(&nt, c->d_counters + kVixTies, sizeof(nt), cudaMemcpyDeviceToHost));
+        if ((size_t)nt <= c->ties_cap / sizeof(int4) || p->los_arith != TXS_LOS_FP64) {
+            if (p->los_arith == TXS_LOS_FP64) c->stats.vix_fp64_ties += (int64_t)nt;
+            break;
+        }
+        if (attempt > 0) return fail(c, TXS_ERR_OUT_OF_MEMORY, "vix", "fp64 tie list overflow");
+        c->vix_tie_min = (int64_t)nt + (int64_t)(nt / 4);
+    }
     c->vix_valid = true;
     if (scores_out) {
         TXS_CUDA(c, "vix", cudaMemcpyAsync(scores_out, c->d_vix, band * c->ncols, cudaMemcpyDeviceToHost, c->stream));
@@ -493,11 +509,23 @@ txs_status txs_compute_viewsheds(txs_ctx* c, const txs_params* p) {
     if (c->sharded && ((c->band_r0 - c->z_off < p->roi + 1 && c->z_off > 0) ||
                        (c->z_off + c->z_rows - c->band_r1 < p->roi + 1 && c->z_off + c->z_rows < c->nrows)))
         return fail(c, TXS_ERR_RANGE, "viewshed", "shard halo smaller than roi + 1");
-    StageTimer t(c, &c->stats.ms_viewshed);
-    st = launch_viewsheds(c, *p);
-    if (st != TXS_OK) return st;
-    st = t.stop("viewshed");
-    if (st != TXS_OK) return st;
+    for (int attempt = 0;; ++attempt) {
+        StageTimer t(c, &c->stats.ms_viewshed);
+        st = launch_viewsheds(c, *p);
+        if (st != TXS_OK) return st;
+        st = t.stop("viewshed");
+        if (st != TXS_OK) return st;
+        if (c->ncand == 0 || p->los_arith != TXS_LOS_FP64) break;
+        // the fp64 tie list overflowed (never seen on the BASELINE terrains): re-run with room
+        unsigned long long nt = 0;
+        TXS_CUDA(c, "viewshed", cudaMemcpy(&nt, c->d_counters + kVsTies, sizeof(nt), cudaMemcpyDeviceToHost));
+        if ((size_t)nt <= c->ties_cap / sizeof(int2)) {
+            c->stats.vs_fp64_ties += (int64_t)nt;
+            break;
+        }
+        if (attempt > 0) return fail(c, TXS_ERR_OUT_OF_MEMORY, "viewshed", "fp64 tie list overflow");
+        c->vs_tie_min = (int64_t)nt + (int64_t)(nt / 4);
+    }
     c->vs_valid = true;
     c->site_valid = false;
     return TXS_OK;

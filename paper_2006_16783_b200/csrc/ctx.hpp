@@ -65,6 +65,9 @@ struct SiteState {
 enum Counter : int {
     kVixLos = 0, kVixCrossFull, kVsCross, kVsCells, kSiteBytes,
     kVixNext,   // work counter of the persistent VIX kernel (reset per launch)
+    kVixTies,   // VIX segments visible with an exact grazing tie (fp64 tie list entries)
+    kVsTies,    // VIEWSHED (observer, ray) pairs with a grazing tie at a cell (fp64 tie list)
+    kVixTiesFlipped, kVsTiesFlipped,   // decisions the fp64 re-test changed
     kNumCounters
 };
 
@@ -89,6 +92,9 @@ struct txs_ctx {
     size_t zt_cap = 0;
     void* d_pairs = nullptr;      // VIX quad planes / VIEWSHED pair planes (per-call scratch)
     uint8_t* d_gcd = nullptr;     // 256x256 gcd table (VIX crossing statistic)
+    int4* d_ties = nullptr;       // fp64 tie lists (VIX segments / VIEWSHED rays), per-call scratch
+    size_t ties_cap = 0;
+    int64_t vix_tie_min = 0, vs_tie_min = 0;   // tie-list sizes after an overflow (re-run)
     size_t pairs_cap = 0;
 
     // VixMap: one byte per post
@@ -187,7 +193,7 @@ txs_status launch_generate(txs_ctx*, int64_t nrows, int64_t ncols, double roughn
 txs_status launch_fill_rows(txs_ctx*, int64_t rb, int64_t re, int16_t v);
 txs_status launch_vix(txs_ctx*, const txs_params& p);
 txs_status launch_los_batch(txs_ctx*, const int32_t* d_pairs, int64_t n, int32_t ht, int32_t hr,
-                            uint8_t* d_out);
+                            int32_t arith, uint8_t* d_out);
 txs_status launch_findmax(txs_ctx*, const txs_params& p, int64_t bw);
 txs_status launch_random_observers(txs_ctx*, int64_t n, uint64_t seed);
 txs_status launch_viewsheds(txs_ctx*, const txs_params& p);

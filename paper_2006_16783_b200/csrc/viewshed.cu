@@ -34,7 +34,19 @@ struct VsArgs {
     const uint32_t* pairs;  // pair planes of the held rows (interior K-observer path), or null
     int p2, pw;             // pair-plane row pitch (words, 2*pw) and posts per plane row
     int zoff;               // first held terrain row
+    int2* ties;             // fp64 tie list: {candidate, ray} with a cell whose tangent equals the horizon
+    long long tie_cap;
 };
+
+// A cell's receiver tangent EQUALS its horizon (an exact grazing tie, which
+// fp64 rounding decides either way): the observer's ray goes to the fp64 tie
+// list (k_vs_fp64_ties).  The sweeps flag candidates by the low 32 bits of the
+// two cross products -- a superset of the exact ties (the re-test recomputes
+// the whole ray, so a false positive costs time, not bits).
+__device__ __forceinline__ void push_vs_tie(const VsArgs& a, unsigned long long* counters, int64_t cand, int ray) {
+    const unsigned long long k = atomicAdd(counters + kVsTies, 1ull);
+    if ((long long)k < a.tie_cap) a.ties[k] = make_int2((int)cand, ray);
+}
 
 // Pair planes for the interior K-observer sweep: held row y occupies p2 = 2*pw
 // words, (H, V) interleaved per post (word 2x + 1 for a column crossing, so an
@@ -143,7 +155,7 @@ __global__ void k_viewshed(const int16_t* __restrict__ z, const int32_t* __restr
         const int dqr = ap ? aq / ap : 0, dmr = ap ? aq % ap : 0;
         const int dqc = aq ? ap / aq : 0, dmc = aq ? ap % aq : 0;
         int i = 1, j = 1, qr = dqr, mr = dmr, qc = dqc, mc = dmc;
-        bool has = false, alive = true;
+        bool has = false, alive = true, tied = false;
         int NH = 0, MH = 1;
         for (int k = 0; k < cnt; ++k) {
             const uint32_t cell = __ldg(cells + cb + k);
@@ -193,9 +205,12 @@ __global__ void k_viewshed(const int16_t* __restrict__ z, const int32_t* __restr
             if (rr < 0 || rr >= a.nrows || cc < 0 || cc >= a.ncols) continue;
             ++n_cells;
             const int P = Z(rr, cc) + a.hr - E;
-            if (!has || (long long)P * L2 * MH >= (long long)NH * dot)
+            const long long lhs = (long long)P * L2 * MH, rhs = (long long)NH * dot;
+            if (!has || lhs >= rhs)
                 set_bit((rr - row0) * RS + (cc - abase));
+            tied |= has && lhs == rhs;
         }
+        if (tied) push_vs_tie(a, counters, cand, ray);
     }
     if (threadIdx.x == 0) set_bit((r - row0) * RS + (c - abase));
     __syncthreads();
@@ -247,7 +262,8 @@ __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, 
                                           const VsArgs& a, const int4* __restrict__ rays,
                                           const int2* __restrict__ groups, const uint2* __restrict__ events,
                                           int ngroups, uint32_t* s_bits, uint64_t* gout, bool smem_bits,
-                                          unsigned long long& n_cross, unsigned long long& n_cells) {
+                                          unsigned long long& n_cross, unsigned long long& n_cells, int64_t cand,
+                                          unsigned long long* counters) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int16_t* __restrict__ P = z + (int64_t)r * a.ncols + c;
     const int Ehr = E - a.hr;
@@ -259,7 +275,7 @@ __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, 
         int p = 0, q = 0;
         if (ray < a.nrays) { const int4 rd = __ldg(rays + ray); p = rd.x; q = rd.y; }
         const int L2 = p * p + q * q;
-        bool has = false, alive = true;
+        bool has = false, alive = true, tied = false;
         int NH = 0, MH = 1, L2MH = L2;
         const uint2* ev = events + (int64_t)grp.x * 32 + lane;
         for (int st0 = 0; st0 < grp.y; st0 += kVsUnroll) {
@@ -311,9 +327,11 @@ __device__ __forceinline__ void vs_events(const int16_t* __restrict__ z, int r, 
                         if (smem_bits) atomicOr(&s_bits[k >> 5], 1u << (k & 31));
                         else atomicOr((unsigned long long*)&gout[k >> 6], 1ull << (k & 63));
                     }
+                    tied |= has && lhs == rhs;
                 }
             }
         }
+        if (tied) push_vs_tie(a, counters, cand, ray);
     }
 }
 
@@ -340,7 +358,8 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
                                             const VsArgs& a, const int4* __restrict__ rays,
                                             const int2* __restrict__ groups, const uint2* __restrict__ events,
                                             int ngroups, uint32_t* s_bits, int bits_stride,
-                                            unsigned long long& n_cross, unsigned long long& n_cells) {
+                                            unsigned long long& n_cross, unsigned long long& n_cells,
+                                            unsigned long long* counters) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const uint32_t* __restrict__ B[K];   // PAIRS: the observer's word in the pair planes
     const int16_t* __restrict__ P[K];    // else: the observer's post
@@ -375,6 +394,7 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
         // its ray: dot >= 0.7*|(p,q)|, and |(p,q)| <= 354)
         int NH[K], MH[K], L2MH[K];
         bool alive[K];
+        uint32_t tied = 0;   // bit k: observer k met a cell whose tangent may equal its horizon
 #pragma unroll
         for (int k = 0; k < K; ++k) { NH[k] = -(1 << 30); MH[k] = 1; L2MH[k] = L2; alive[k] = true; }
         const uint2* ev = events + (int64_t)grp.x * 32 + lane;
@@ -445,8 +465,17 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
                     } else {
                         red_or_shared(sb[k] + cw4, cbit, setc & (lhs >= rhs));
                     }
+                    tied |= (uint32_t)(setc & ((uint32_t)lhs == (uint32_t)rhs)) << k;
                 }
             }
+        }
+        if (tied) {
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                if ((tied >> k) & 1u) {   // observer k of this CTA (k_viewshed_evk's slot order)
+                    const int64_t slot = (int64_t)blockIdx.x * K + k;
+                    push_vs_tie(a, counters, a.perm ? a.perm[slot] : slot, g * 32 + lane);
+                }
         }
     }
 }
@@ -478,9 +507,11 @@ __global__ void k_viewshed_ev(const int16_t* __restrict__ z, const int32_t* __re
     // every crossing/cell post lies within roi+1 of the observer
     const bool interior = r - a.R - 1 >= 0 && r + a.R + 1 < a.nrows && c - a.R - 1 >= 0 && c + a.R + 1 < a.ncols;
     if (interior)
-        vs_events<true>(z, r, c, E, row0, abase, RS, a, rays, groups, events, ngroups, s_bits, out, SMEM_BITS, n_cross, n_cells);
+        vs_events<true>(z, r, c, E, row0, abase, RS, a, rays, groups, events, ngroups, s_bits, out, SMEM_BITS, n_cross, n_cells,
+                        cand, counters);
     else
-        vs_events<false>(z, r, c, E, row0, abase, RS, a, rays, groups, events, ngroups, s_bits, out, SMEM_BITS, n_cross, n_cells);
+        vs_events<false>(z, r, c, E, row0, abase, RS, a, rays, groups, events, ngroups, s_bits, out, SMEM_BITS, n_cross, n_cells,
+                         cand, counters);
     if (threadIdx.x == 0) {
         const int k = (r - row0) * RS + (c - abase);
         if (SMEM_BITS) atomicOr(&s_bits[k >> 5], 1u << (k & 31));
@@ -558,12 +589,14 @@ __global__ void __maxnreg__(MAXREG) k_viewshed_evk(const int16_t* __restrict__ z
     unsigned long long n_cross = 0, n_cells = 0;
     if (all_int) {
         unsigned long long d0 = 0, d1 = 0;
-        if (a.pairs) vs_events_k<K, true, false, STEP>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride, d0, d1);
-        else vs_events_k<K, false, false, STEP>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride, d0, d1);
+        if (a.pairs) vs_events_k<K, true, false, STEP>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride, d0, d1,
+                                                       counters);
+        else vs_events_k<K, false, false, STEP>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride, d0, d1,
+                                                counters);
         if (threadIdx.x == 0) { n_cross = (unsigned long long)(K * a.tmpl_cross); n_cells = (unsigned long long)(K * a.tmpl_cells); }
     } else if (a.pairs && nk == K) {   // edge observers: the same shared sweep with per-observer grid bounds
         vs_events_k<K, true, true, STEP>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride,
-                                   n_cross, n_cells);
+                                   n_cross, n_cells, counters);
     } else {
         for (int k = 0; k < K; ++k) {
             if (cand[k] < 0) continue;
@@ -571,10 +604,10 @@ __global__ void __maxnreg__(MAXREG) k_viewshed_evk(const int16_t* __restrict__ z
                             ck[k] + a.R + 1 < a.ncols;
             if (in)
                 vs_events<true>(z, rk[k], ck[k], Ek[k], row0[k], abk[k], RSk[k], a, rays, groups, events, ngroups,
-                                s_bits + k * bits_stride, nullptr, true, n_cross, n_cells);
+                                s_bits + k * bits_stride, nullptr, true, n_cross, n_cells, cand[k], counters);
             else
                 vs_events<false>(z, rk[k], ck[k], Ek[k], row0[k], abk[k], RSk[k], a, rays, groups, events, ngroups,
-                                 s_bits + k * bits_stride, nullptr, true, n_cross, n_cells);
+                                 s_bits + k * bits_stride, nullptr, true, n_cross, n_cells, cand[k], counters);
         }
     }
 #pragma unroll
@@ -618,6 +651,122 @@ __global__ void __maxnreg__(MAXREG) k_viewshed_evk(const int16_t* __restrict__ z
     }
 }
 
+// fp64 re-decision of the tie list (txs_params.los_arith == TXS_LOS_FP64): the
+// whole ray of each listed (observer, ray) is recomputed with SPEC.md:147's
+// arithmetic, operation for operation the oracle's compute_viewshed_fp64
+// (oracle/oracle.cpp): crossings of the walk (0,0) -> (Kp, Kq) in exact order
+// with the walk's doubles t, row, col (grid_walk.hpp:27-77), interpolation
+// z0*(1-f) + z1*f, crossing tangent (z - E) / sqrt(row^2 + col^2), cell tangent
+// (z + h_r - E) / (dot / sqrt(L2)), visible iff >= the running max; the ray
+// ends at the first crossing with an off-grid post.  Explicit _rn intrinsics
+// (no FMA contraction).  Changed bits are flipped in the resident cum-aligned
+// words and the popcount adjusted.
+__global__ void k_vs_fp64_ties(const int16_t* __restrict__ z, const int32_t* __restrict__ crow,
+                               const int32_t* __restrict__ ccol, const int4* __restrict__ rays,
+                               const uint32_t* __restrict__ cells, VsArgs a, unsigned long long* __restrict__ counters,
+                               uint64_t* __restrict__ words, int32_t* __restrict__ pops) {
+    const long long nt = min((long long)counters[kVsTies], a.tie_cap);
+    auto Z = [&](int rr, int cc) -> double { return (double)zld(z + (int64_t)rr * a.ncols + cc); };
+    auto in = [&](int rr, int cc) { return rr >= 0 && rr < a.nrows && cc >= 0 && cc < a.ncols; };
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nt; t += (long long)gridDim.x * blockDim.x) {
+        const int2 e = a.ties[t];
+        const int64_t cand = e.x;
+        const int r = crow[cand], c = ccol[cand];
+        const int row0 = max(0, r - a.R), col0 = max(0, c - a.R), w = min(a.ncols - 1, c + a.R) - col0 + 1;
+        const int RS = win_nwr(col0, w) << 6, abase = col0 & ~63;
+        uint64_t* out = words + cand * a.stride;
+        const int4 rd = __ldg(rays + e.y);
+        const int p = rd.x, q = rd.y, cb = rd.z, cnt = rd.w, L2 = p * p + q * q;
+        auto cell = [&](int i, int& ca, int& cbb) {
+            const uint32_t v = __ldg(cells + cb + i);
+            ca = (int)(int16_t)(v & 0xffffu); cbb = (int)(int16_t)(v >> 16);
+        };
+        int K = 1;
+        for (int i = 0; i < cnt; ++i) {
+            int ca, cbb;
+            cell(i, ca, cbb);
+            K = max(K, (ca * p + cbb * q + L2 - 1) / L2);
+        }
+        const int Ei = zld(z + (int64_t)r * a.ncols + c) + a.ht;
+        const double E = (double)Ei, rootL = __dsqrt_rn((double)L2);
+        bool has = false;
+        double H = 0.0;
+        int ci = 0;
+        auto test = [&](int i) {
+            int ca, cbb;
+            cell(i, ca, cbb);
+            const int rr = r + ca, cc = c + cbb;
+            if (!in(rr, cc)) return;
+            const double run = __ddiv_rn((double)(ca * p + cbb * q), rootL);
+            const double s = __ddiv_rn((double)(zld(z + (int64_t)rr * a.ncols + cc) + a.hr - Ei), run);
+            const bool vis = !has || s >= H;
+            const int64_t k = (int64_t)(rr - row0) * RS + (cc - abase);
+            const unsigned long long m = 1ull << (k & 63);
+            unsigned long long* wp = (unsigned long long*)out + (k >> 6);
+            const bool cur = (*(volatile unsigned long long*)wp & m) != 0ull;
+            if (vis != cur) {
+                if (vis) atomicOr(wp, m); else atomicAnd(wp, ~m);
+                atomicAdd(pops + cand, vis ? 1 : -1);
+                atomicAdd(counters + kVsTiesFlipped, 1ull);
+            }
+        };
+        const int dr = K * p, dc = K * q, nr = abs(dr), nc = abs(dc), sr = dr >= 0 ? 1 : -1, sc = dc >= 0 ? 1 : -1;
+        int ir = 1, ic = 1;
+        while (ci < cnt && (ir <= nr || ic <= nc)) {
+            int cmp;
+            if (ir > nr) cmp = 1;
+            else if (ic > nc) cmp = -1;
+            else {
+                const long long x = (long long)ir * nc, y = (long long)ic * nr;
+                cmp = x < y ? -1 : (x > y ? 1 : 0);
+            }
+            double t, row, col;
+            int n, idx, kind;   // kind: 0 row line, 1 column line, 2 post
+            bool at_end;
+            if (cmp < 0) {
+                t = __ddiv_rn((double)ir, (double)nr); row = (double)(sr * ir); col = dc == 0 ? 0.0 : __dmul_rn(t, (double)dc);
+                kind = dc == 0 ? 2 : 0; n = nr; idx = ir; at_end = ir == nr; ++ir;
+            } else if (cmp > 0) {
+                t = __ddiv_rn((double)ic, (double)nc); row = dr == 0 ? 0.0 : __dmul_rn(t, (double)dr); col = (double)(sc * ic);
+                kind = dr == 0 ? 2 : 1; n = nc; idx = ic; at_end = ic == nc; ++ic;
+            } else {
+                t = __ddiv_rn((double)ir, (double)nr); row = (double)(sr * ir); col = (double)(sc * ic);
+                kind = 2; n = nr; idx = ir; at_end = ir == nr; ++ir; ++ic;
+            }
+            (void)t;
+            if (at_end) break;
+            // cells with u_c <= u_k (dot / L2 <= K idx / n) do not see this crossing
+            for (;;) {
+                if (ci >= cnt) break;
+                int ca, cbb;
+                cell(ci, ca, cbb);
+                if ((long long)(ca * p + cbb * q) * n > (long long)K * idx * L2) break;
+                test(ci++);
+            }
+            if (ci >= cnt) break;
+            double zt;
+            if (kind == 2) {
+                const int rr = r + (int)row, cc = c + (int)col;
+                if (!in(rr, cc)) break;
+                zt = Z(rr, cc);
+            } else if (kind == 0) {
+                const double cf = floor(col), f = __dsub_rn(col, cf);
+                const int rr = r + (int)row, c0 = c + (int)cf;
+                if (!in(rr, c0) || !in(rr, c0 + 1)) break;
+                zt = __dadd_rn(__dmul_rn(Z(rr, c0), __dsub_rn(1.0, f)), __dmul_rn(Z(rr, c0 + 1), f));
+            } else {
+                const double rf = floor(row), f = __dsub_rn(row, rf);
+                const int r0 = r + (int)rf, cc = c + (int)col;
+                if (!in(r0, cc) || !in(r0 + 1, cc)) break;
+                zt = __dadd_rn(__dmul_rn(Z(r0, cc), __dsub_rn(1.0, f)), __dmul_rn(Z(r0 + 1, cc), f));
+            }
+            const double s = __ddiv_rn(__dsub_rn(zt, E), __dsqrt_rn(__dadd_rn(__dmul_rn(row, row), __dmul_rn(col, col))));
+            if (!has || s > H) { has = true; H = s; }
+        }
+        while (ci < cnt) test(ci++);
+    }
+}
+
 __global__ void k_tile_keys(const int32_t* __restrict__ crow, const int32_t* __restrict__ ccol, int64_t n, int tiles_x,
                             int tshift, uint32_t* __restrict__ keys, int32_t* __restrict__ idx) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -644,7 +793,18 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
     c->vs_stride = mw;
     if (n == 0) return TXS_OK;
     VsArgs a{(int)c->nrows, (int)c->ncols, p.roi, p.tx_height, p.rx_height, T->nrays, mw, nullptr, n, 0, 0, 0,
-             nullptr, 0, 0, 0};
+             nullptr, 0, 0, 0, nullptr, 0};
+    // fp64 tie list (rays with a cell exactly at its horizon: ~2e-5 of cells at
+    // roi 100, fewer at larger roi); txs_compute_viewsheds re-runs on overflow
+    {
+        const int64_t want = std::max<int64_t>(c->vs_tie_min,
+                                               std::min<int64_t>(1 << 26, std::max<int64_t>(1 << 20, n * T->nrays / 256)));
+        if (ensure(c, "viewshed", (void**)&c->d_ties, &c->ties_cap, sizeof(int2) * (size_t)want) != TXS_OK)
+            return TXS_ERR_OUT_OF_MEMORY;
+        a.ties = (int2*)c->d_ties;
+        a.tie_cap = (long long)(c->ties_cap / sizeof(int2));
+        TXS_CUDA(c, "viewshed", cudaMemsetAsync(c->d_counters + kVsTies, 0, sizeof(unsigned long long), c->stream));
+    }
     // Process observers in 16x16-tile order so the CTAs resident at any moment
     // read overlapping terrain windows (L2 reuse; config 5's observers are
     // random over a 537 MB terrain).  Output slots keep candidate order.
@@ -775,6 +935,11 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
         }
     }
     TXS_LAUNCHED(c, "viewshed");
+    if (p.los_arith == TXS_LOS_FP64) {   // re-decide the tied rays in fp64
+        k_vs_fp64_ties<<<(unsigned)(c->num_sms * 4), 128, 0, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->cells, a,
+                                                                         c->d_counters, c->d_words, c->d_pop);
+        TXS_LAUNCHED(c, "viewshed");
+    }
     return TXS_OK;
 }
 

@@ -62,13 +62,15 @@ __device__ __forceinline__ int load_z(const int16_t* base, int off) {
     return zld(base + off);
 }
 
+// Returns 1 (uniform) iff the segment is blocked, 2 iff it is visible but
+// touches the LOS at some crossing (an exact grazing tie), else 0.
 template <bool SMEM, int ILP>
-__device__ __forceinline__ bool warp_blocked(const int16_t* P, int stride, int dr, int dc, int E, int Zt, int lane) {
+__device__ __forceinline__ int warp_blocked(const int16_t* P, int stride, int dr, int dc, int E, int Zt, int lane) {
     const int nr = abs(dr), nc = abs(dc);
     const bool rows_major = nr >= nc;
     const int nM = rows_major ? nr : nc, nm = rows_major ? nc : nr;
     const int steps = nM - 1;
-    if (steps <= 0) return false;
+    if (steps <= 0) return 0;
     const int stepM = rows_major ? (dr >= 0 ? stride : -stride) : (dc >= 0 ? 1 : -1);
     const int stepm = rows_major ? (dc >= 0 ? 1 : -1) : (dr >= 0 ? stride : -stride);
     const int D = Zt - E;
@@ -90,6 +92,7 @@ __device__ __forceinline__ bool warp_blocked(const int16_t* P, int stride, int d
     int rhsM = E * nM + i * D;                       // major-line LOS numerator
     int rhsm = E * nm + q * D;                       // minor-line LOS numerator
     const int dOffM = 32 * stepM, dRhsM = 32 * D;
+    bool tie = false;
     for (int k0 = 0; k0 < steps; k0 += 32 * ILP) {
         bool b = false;
 #pragma unroll
@@ -102,9 +105,12 @@ __device__ __forceinline__ bool warp_blocked(const int16_t* P, int stride, int d
             const int zCl = (lane == 0 && valid) ? load_z<SMEM>(P, oA - stepM) : 0;
             const int nb = __shfl_up_sync(kFull, zB, 1);
             const int zC = lane == 0 ? zCl : nb;
-            b |= valid && zA * (nM - r) + zB * r > rhsM;
+            const int vM = zA * (nM - r) + zB * r, vm = zC * r + zA * (nm - r);
+            const bool minor = r > 0 && r < nm;
+            b |= valid && vM > rhsM;
             // minor line j = q between major lines i-1 and i: weight on A = nm - r
-            b |= valid && r > 0 && r < nm && zC * r + zA * (nm - r) > rhsm;
+            b |= valid && minor && vm > rhsm;
+            tie |= valid && (vM == rhsM || (minor && vm == rhsm));
             // advance 32 steps
             i += 32;
             off += dOffM;
@@ -112,9 +118,80 @@ __device__ __forceinline__ bool warp_blocked(const int16_t* P, int stride, int d
             r += r32; q += q32; off += q32 * stepm; rhsm += q32 * D;
             if (r >= nM) { r -= nM; ++q; off += stepm; rhsm += D; }
         }
-        if (__any_sync(kFull, b)) return true;
+        if (__any_sync(kFull, b)) return 1;
+    }
+    return __any_sync(kFull, tie) ? 2 : 0;
+}
+
+// SPEC.md:147's fp64 is_visible for one segment, operation for operation the
+// oracle's is_visible_fp64 (oracle/oracle.cpp) on the walk of grid_walk.hpp:27-77
+// (relative coordinates, D1): t = k/n, the minor coordinate t*d, f = its
+// fractional part, z0*(1-f) + z1*f against E + t*(Zt-E), blocked iff '>'.
+// Explicit _rn intrinsics: no FMA contraction (the oracle is built
+// -ffp-contract=off).  Run only for segments with an exact grazing tie.
+__device__ bool seg_blocked_fp64(const int16_t* __restrict__ z, int64_t ncols, int tr, int tc, int E, int Zt, int dr,
+                                 int dc) {
+    const int nr = abs(dr), nc = abs(dc), sr = dr >= 0 ? 1 : -1, sc = dc >= 0 ? 1 : -1;
+    const double Ed = (double)E, D = (double)(Zt - E);
+    auto Z = [&](int r, int c) -> double { return (double)zld(z + (int64_t)r * ncols + c); };
+    int ir = 1, ic = 1;
+    while (ir <= nr || ic <= nc) {
+        int cmp;
+        if (ir > nr) cmp = 1;
+        else if (ic > nc) cmp = -1;
+        else {
+            const long long x = (long long)ir * nc, y = (long long)ic * nr;
+            cmp = x < y ? -1 : (x > y ? 1 : 0);
+        }
+        double t, zt;
+        bool at_end;
+        if (cmp < 0 && dc != 0) {          // row line: row exact, col = t*dc
+            t = __ddiv_rn((double)ir, (double)nr);
+            const double col = __dmul_rn(t, (double)dc), cf = floor(col), f = __dsub_rn(col, cf);
+            const int r = tr + sr * ir, c = tc + (int)cf;
+            zt = __dadd_rn(__dmul_rn(Z(r, c), __dsub_rn(1.0, f)), __dmul_rn(Z(r, c + 1), f));
+            at_end = ir == nr;
+            ++ir;
+        } else if (cmp > 0 && dr != 0) {   // column line: col exact, row = t*dr
+            t = __ddiv_rn((double)ic, (double)nc);
+            const double row = __dmul_rn(t, (double)dr), rf = floor(row), f = __dsub_rn(row, rf);
+            const int r = tr + (int)rf, c = tc + sc * ic;
+            zt = __dadd_rn(__dmul_rn(Z(r, c), __dsub_rn(1.0, f)), __dmul_rn(Z(r + 1, c), f));
+            at_end = ic == nc;
+            ++ic;
+        } else {                            // through a post (axis-aligned, or both lines at once)
+            const bool byr = cmp <= 0;
+            t = byr ? __ddiv_rn((double)ir, (double)nr) : __ddiv_rn((double)ic, (double)nc);
+            const int r = byr ? tr + sr * ir : tr, c = cmp == 0 ? tc + sc * ic : (byr ? tc : tc + sc * ic);
+            zt = Z(r, c);
+            at_end = byr ? ir == nr : ic == nc;
+            if (cmp <= 0) ++ir;
+            if (cmp >= 0) ++ic;
+        }
+        if (at_end) return false;
+        if (zt > __dadd_rn(Ed, __dmul_rn(t, D))) return true;
     }
     return false;
+}
+
+// fp64 re-test of the tie list (txs_params.los_arith == TXS_LOS_FP64): a
+// segment the exact walk found visible with a grazing tie is re-decided by
+// SPEC.md:147's formula, and a block takes one off its post's score.
+__global__ void k_vix_fp64_ties(const int16_t* __restrict__ z, int64_t ncols, const int4* __restrict__ ties,
+                                unsigned long long* __restrict__ counters, long long cap, int ht, int hr,
+                                uint8_t* __restrict__ vix_rows) {
+    const long long n = min((long long)counters[kVixTies], cap);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int4 t = ties[i];
+        const int E = zld(z + (int64_t)t.x * ncols + t.y) + ht;
+        const int Zt = zld(z + (int64_t)(t.x + t.z) * ncols + t.y + t.w) + hr;
+        if (seg_blocked_fp64(z, ncols, t.x, t.y, E, Zt, t.z, t.w)) {
+            uint8_t* b = vix_rows + (int64_t)t.x * ncols + t.y;
+            unsigned* w = (unsigned*)((uintptr_t)b & ~(uintptr_t)3);
+            atomicSub(w, 1u << (8 * ((uintptr_t)b & 3)));   // the byte counted this segment: >= 1, no borrow
+            atomicAdd((unsigned long long*)counters + kVixTiesFlipped, 1ull);
+        }
+    }
 }
 
 // Per-sample walk geometry, computed by the lane that owns the sample and
@@ -176,9 +253,9 @@ __device__ __forceinline__ bool walk_round(const int16_t* P, int nM, int nm, int
 }
 
 template <bool SMEM>
-__device__ __forceinline__ bool warp_walk(const int16_t* P, const SegGeom& g, int E, int lane) {
+__device__ __forceinline__ int warp_walk(const int16_t* P, const SegGeom& g, int E, int lane) {
     const int nM = g.nM, nm = g.nm, steps = nM - 1;
-    if (steps <= 0) return false;
+    if (steps <= 0) return 0;
     const int stepM = g.stepM, stepm = g.stepm, D = g.D;
     int i = 1 + lane;
     const int num = i * nm;
@@ -186,13 +263,20 @@ __device__ __forceinline__ bool warp_walk(const int16_t* P, const SegGeom& g, in
     if (r >= nM) { ++q; r -= nM; }
     if (r < 0) { --q; r += nM; }
     int off = i * stepM + q * stepm;                 // post A = (i, q)
-    int rhsM = E * nM + i * D;                       // major-line LOS numerator
-    int rhsm = E * nm + q * D;                       // minor-line LOS numerator
+    // LOS numerators minus 1: the rounds test z >= LOS (blocks and grazing
+    // ties); a round with a hit is re-tested strictly (+1).  0 visible,
+    // 1 blocked, 2 visible with a tie (the segment goes to the fp64 tie list).
+    int rhsM = E * nM + i * D - 1;                   // major-line LOS numerator
+    int rhsm = E * nm + q * D - 1;                   // minor-line LOS numerator
     const int dOffM = 32 * stepM + g.q32 * stepm, dRhsM = 32 * D, dRhsm = g.q32 * D;
     const int full = steps >> 5;                     // rounds with every lane valid
+    int st = 0;
     for (int k = 0; k < full; ++k) {
-        if (__any_sync(kFull, walk_round<SMEM, false>(P, nM, nm, stepM, stepm, steps, lane, i, r, off, rhsM, rhsm)))
-            return true;
+        if (__any_sync(kFull, walk_round<SMEM, false>(P, nM, nm, stepM, stepm, steps, lane, i, r, off, rhsM, rhsm))) {
+            if (__any_sync(kFull, walk_round<SMEM, false>(P, nM, nm, stepM, stepm, steps, lane, i, r, off, rhsM + 1, rhsm + 1)))
+                return 1;
+            st = 2;
+        }
         i += 32;
         off += dOffM;
         rhsM += dRhsM;
@@ -200,9 +284,12 @@ __device__ __forceinline__ bool warp_walk(const int16_t* P, const SegGeom& g, in
         r += g.r32;
         if (r >= nM) { r -= nM; off += stepm; rhsm += D; }
     }
-    if (steps & 31)
-        return __any_sync(kFull, walk_round<SMEM, true>(P, nM, nm, stepM, stepm, steps, lane, i, r, off, rhsM, rhsm));
-    return false;
+    if ((steps & 31) && __any_sync(kFull, walk_round<SMEM, true>(P, nM, nm, stepM, stepm, steps, lane, i, r, off, rhsM, rhsm))) {
+        if (__any_sync(kFull, walk_round<SMEM, true>(P, nM, nm, stepM, stepm, steps, lane, i, r, off, rhsM + 1, rhsm + 1)))
+            return 1;
+        st = 2;
+    }
+    return st;
 }
 
 __device__ __forceinline__ int warp_of_thread() { return threadIdx.x >> 5; }
@@ -248,7 +335,16 @@ struct VixArgs {
     int zr0, zr1;        // held terrain rows [zr0, zr1)
     int pv, pt, st_off;  // skip map: SV row pitch, ST column pitch, ST offset (int16 entries)
     uint32_t s_mul;      // ceil(2^32 / S) (0: divide): floor(x / S) = umulhi(x, s_mul) while x S < 2^32
+    int4* ties;          // fp64 tie list: {tx row, tx col, dr, dc} of visible segments with a grazing tie
+    long long tie_cap;
 };
+
+// Record a visible segment with a grazing tie for the fp64 re-test (rare:
+// ~1e-4 of segments on the BASELINE terrains).
+__device__ __forceinline__ void push_tie(const VixArgs& a, unsigned long long* counters, int r, int c, int dr, int dc) {
+    const unsigned long long k = atomicAdd(counters + kVixTies, 1ull);
+    if ((long long)k < a.tie_cap) a.ties[k] = make_int4(r, c, dr, dc);
+}
 
 template <bool SMEM, int ILP>
 __global__ void __launch_bounds__(kVixThreads, 2) k_vix(const int16_t* __restrict__ z, const int16_t* __restrict__ zt, int nrows, int ncols,
@@ -317,8 +413,12 @@ __global__ void __launch_bounds__(kVixThreads, 2) k_vix(const int16_t* __restric
             const unsigned trmask = __ballot_sync(kFull, my_tr);
             for (int sidx = 0; sidx < ns; ++sidx) {
                 const SegGeom g = shfl_geom(my, sidx);
-                const bool blk = warp_walk<SMEM>(((trmask >> sidx) & 1u) ? PT : P, g, E, lane);
-                vis += blk ? 0 : 1;
+                const int stt = warp_walk<SMEM>(((trmask >> sidx) & 1u) ? PT : P, g, E, lane);
+                vis += stt == 1 ? 0 : 1;
+                if (stt == 2 && lane == 0) {
+                    const int pk = s_samp[s0 + sidx];
+                    push_tie(a, counters, r, c, (int)(int16_t)(pk & 0xffff), pk >> 16);
+                }
             }
         }
         __syncwarp();
@@ -412,16 +512,21 @@ __device__ __forceinline__ int dp2hi(uint32_t pair, uint32_t w) {
 // Divisions by M are exact fixed-point multiplies: with mag = ceil(2^16 m / M),
 // floor(x m / M) = (x mag) >> 16 for every 0 <= x <= 255 (the error x(mag -
 // 2^16 m/M)/2^16 < 255/2^16 < 1/M cannot carry past the next integer).
+// Grazing ties (DESIGN.md §2 D2): every hot test below is `z >= LOS` -- the
+// -1 of `z > LOS - 1` is folded into LE2 and Esn -- so the skip test only skips
+// groups strictly below the LOS, and a walked chunk reports exact blocks AND
+// exact ties; a chunk with a hit is re-tested strictly (bias +1), and a segment
+// that stays visible with a tie goes to the fp64 tie list (k_vix_fp64_ties).
 struct __align__(16) QuadGeomC {   // skip test
     int soff;         // skip-map entry of the start post's block (padded block indices)
-    int LE2;          // Es*M + min(0, G D)  (Es = LOS height at the start post, D = LOS rise, G = group steps)
+    int LE2;          // Es*M + min(0, G D) - 1  (Es = LOS height at the start post, D = LOS rise, G = group steps)
     int DG;           // G D
     int w;            // M | c0 << 8 | tr << 13 | mneg << 14 | mag << 15   (M = 0: nothing to walk)
 };
 struct __align__(16) QuadGeomF {   // exact walk
     const uint2* Q;   // start post's entry in its plane (terrain-walk kernels: the start post's
                       // int16 terrain address, reinterpreted)
-    int Es;           // LOS height at the start post (E, or Zt when reversed)
+    int Esn;          // Es*m - 1 (Es = LOS height at the start post: E, or Zt when reversed)
     int msm;          // m | sm << 8 (sm = minor step in plane words / terrain posts, 0 for axis-aligned)
 };
 struct QuadGeom { QuadGeomC c; QuadGeomF f; };
@@ -458,11 +563,14 @@ __device__ __forceinline__ bool terrain_test(const int16_t* P, int i, int q, int
 // Full walk: one segment per warp, lane l taking major steps l+1, l+33, ...;
 // a vote after every 32 steps.  Returns true (uniform) iff the segment is
 // blocked.  (TXS_VIX_SKIP=0: every step of every segment is evaluated.)
+// Segment states of the walks: visible, blocked, visible with a grazing tie.
+enum : int { kSegVis = 0, kSegBlk = 1, kSegTie = 2 };
+
 template <int GS>
-__device__ __forceinline__ bool quad_walk(const QuadGeom* gp, int lane) {
+__device__ __forceinline__ int quad_walk(const QuadGeom* gp, int lane) {
     const QuadGeomC c = gp->c;
     const int nM = c.w & 0xff, steps = nM - 1;
-    if (steps <= 0) return false;
+    if (steps <= 0) return kSegVis;
     const QuadGeomF f = gp->f;
     const int nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 15, D = c.DG >> GS;
     const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
@@ -470,18 +578,22 @@ __device__ __forceinline__ bool quad_walk(const QuadGeom* gp, int lane) {
     int i = 1 + lane;
     int q = (i * mag) >> 16, r = i * nm - q * nM;
     int off = i + q * sm;
-    int rhsM = c.LE2 - min(0, c.DG) + i * D, rhsm = f.Es * nm + q * D;
+    int rhsM = c.LE2 - min(0, c.DG) + i * D, rhsm = f.Esn + q * D;
     const int dOff = 32 + q32 * sm, dRhsM = 32 * D, dRhsm = q32 * D;
-    for (int k = steps >> 5; k; --k) {
-        if (__any_sync(kFull, quad_test(qld(f.Q + off), r, nm, wb, rhsM, rhsm))) return true;
+    int st = kSegVis;
+    for (int k = 0; k <= (steps >> 5); ++k) {
+        const bool valid = k < (steps >> 5) || (steps & ~31) + 1 + lane <= steps;
+        if (k == (steps >> 5) && !(steps & 31)) break;
+        const uint2 v = valid ? qld(f.Q + off) : make_uint2(0u, 0u);
+        const bool b = valid && quad_test(v, r, nm, wb, rhsM, rhsm);
+        if (__any_sync(kFull, b)) {   // >= hit: a block, or only ties
+            if (__any_sync(kFull, b && quad_test(v, r, nm, wb, rhsM + 1, rhsm + 1))) return kSegBlk;
+            st = kSegTie;
+        }
         off += dOff; rhsM += dRhsM; rhsm += dRhsm; r += r32;
         if (r >= nM) { r -= nM; off += sm; rhsm += D; }
     }
-    if (steps & 31) {
-        const bool valid = (steps & ~31) + 1 + lane <= steps;
-        return __any_sync(kFull, valid && quad_test(qld(f.Q + (valid ? off : 0)), r, nm, wb, rhsM, rhsm));
-    }
-    return false;
+    return st;
 }
 
 // Hierarchical walk with a conservative skip test (exact: it only ever skips
@@ -503,11 +615,12 @@ __device__ __forceinline__ bool quad_walk(const QuadGeom* gp, int lane) {
 // Sequential form (TXS_VIX_SKIP=2): one segment per warp pass, lane l testing
 // group 32k+l, failing groups walked in order with an exit at the first block.
 template <int GS>
-__device__ __forceinline__ bool quad_walk_skip(const QuadGeom* gp, const QuadPitch& P, const int16_t* __restrict__ smap,
-                                               int* s_fail, int lane) {
+__device__ __forceinline__ int quad_walk_skip(const QuadGeom* gp, const QuadPitch& P, const int16_t* __restrict__ smap,
+                                              int* s_fail, int lane) {
     const QuadGeomC c = gp->c;
     const int nM = c.w & 0xff, steps = nM - 1;
-    if (steps <= 0) return false;
+    if (steps <= 0) return kSegVis;
+    int st = kSegVis;
     const int mag = (unsigned)c.w >> 15, magG = mag << GS, c0 = (c.w >> 8) & 31;
     const int sp = (c.w & 0x2000) ? P.pt : P.pv, ssp = (c.w & 0x4000) ? -sp : sp;
     const int ngroups = (steps + (1 << GS) - 1) >> GS;
@@ -530,19 +643,24 @@ __device__ __forceinline__ bool quad_walk_skip(const QuadGeom* gp, const QuadPit
         const int cnt = __popc(F);
         for (int j = 0; j < cnt; j += 32 >> GS) {   // 32/G groups x G steps per pass
             const int sub = j + (lane >> GS);
-            bool b = false;
+            bool b = false, s = false;
             if (sub < cnt) {
                 const int i = (s_fail[sub] << GS) + 1 + (lane & ((1 << GS) - 1));
                 if (i <= steps) {
                     const int q = (i * mag) >> 16, r = i * nm - q * nM;
-                    b = quad_test(qld(f.Q + i + q * sm), r, nm, wb, LE + i * D, f.Es * nm + q * D);
+                    const uint2 v = qld(f.Q + i + q * sm);
+                    b = quad_test(v, r, nm, wb, LE + i * D, f.Esn + q * D);
+                    s = b && quad_test(v, r, nm, wb, LE + i * D + 1, f.Esn + q * D + 1);
                 }
             }
-            if (__any_sync(kFull, b)) return true;
+            if (__any_sync(kFull, b)) {
+                if (__any_sync(kFull, s)) return kSegBlk;
+                st = kSegTie;
+            }
         }
         __syncwarp();
     }
-    return false;
+    return st;
 }
 
 //
@@ -553,10 +671,12 @@ __device__ __forceinline__ bool quad_walk_skip(const QuadGeom* gp, const QuadPit
 // unit with a failing group is then walked exactly, whole: one warp pass of 32
 // consecutive steps (coalesced plane loads, the predicates of quad_test), in
 // (segment, unit) order, skipping segments already found blocked.  Returns
-// the mask of lanes whose segment is visible.
+// the mask of lanes whose segment is visible; *tiem = the visible lanes whose
+// segment touched the LOS at some crossing (an exact grazing tie).
 template <int U, int GS, bool TERR>
 __device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int lane, QuadGeom* s_geo, int* s_pre,
-                                               int* s_fail, const int16_t* __restrict__ smap, const QuadPitch& P) {
+                                               int* s_fail, const int16_t* __restrict__ smap, const QuadPitch& P,
+                                               unsigned* tiem) {
     static_assert((U << GS) <= 32, "a failing unit is walked by one 32-step pass");
     const int nMl = g.c.w & 0xff;
     const int ng = (lane < ns && nMl >= 2) ? (nMl + (1 << GS) - 2) >> GS : 0;   // ceil((M-1)/G) groups
@@ -577,7 +697,7 @@ __device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int la
     }
     __syncwarp();
     const int myp = lane < __popc(nz) ? s_pre[lane] & 0xffff : 0x7fffffff;
-    unsigned blk = 0;   // blocked slots
+    unsigned blk = 0, tie = 0;   // blocked slots, slots with a grazing tie
     for (int base = 0; base < T; base += 32) {
         // slot of pair base+lane: (slots starting at or before base) - 1 + (starts in (base, base+lane])
         const unsigned B = __reduce_or_sync(kFull, (myp > base && myp < base + 32) ? 1u << (myp - base) : 0u);
@@ -619,25 +739,30 @@ __device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int la
             const int nM = c.w & 0xff;
             // 32 steps from the unit's first (a unit of U G < 32 steps is walked with its successor)
             const int i = ((U * (e >> 8)) << GS) + 1 + lane;
-            bool b = false;
-            if (i < nM) {
+            // bias 0: z >= LOS (blocks and ties), bias 1: z > LOS (blocks)
+            auto test = [&](int bias) -> bool {
+                if (i >= nM) return false;
                 const int nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 15, D = c.DG >> GS;
                 const int q = (i * mag) >> 16, r = i * nm - q * nM;
-                const int rhsM = c.LE2 - min(0, c.DG) + i * D, rhsm = f.Es * nm + q * D;
-                if (TERR) {
-                    b = terrain_test((const int16_t*)f.Q, i, q, r, nM, nm, sm, (c.w & 0x2000) ? P.zs : 1, rhsM, rhsm);
-                } else {
-                    const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
-                    b = quad_test(qld(f.Q + i + q * sm), r, nm, wb, rhsM, rhsm);
-                }
+                const int rhsM = c.LE2 - min(0, c.DG) + i * D + bias, rhsm = f.Esn + q * D + bias;
+                if (TERR)
+                    return terrain_test((const int16_t*)f.Q, i, q, r, nM, nm, sm, (c.w & 0x2000) ? P.zs : 1, rhsM, rhsm);
+                const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
+                return quad_test(qld(f.Q + i + q * sm), r, nm, wb, rhsM, rhsm);
+            };
+            const bool b = test(0);
+            if (__any_sync(kFull, b)) {
+                if (__any_sync(kFull, b && test(1))) blk |= 1u << sf;
+                else tie |= 1u << sf;
             }
-            if (__any_sync(kFull, b)) blk |= 1u << sf;
         }
         __syncwarp();
     }
     // visible lanes (lane order): segments without groups, and slots not blocked
     const int slot = __popc(nz & ((1u << lane) - 1));
-    return __ballot_sync(kFull, lane < ns && (ng == 0 || !((blk >> slot) & 1u)));
+    const bool vis = lane < ns && (ng == 0 || !((blk >> slot) & 1u));
+    *tiem = __ballot_sync(kFull, vis && ng > 0 && ((tie >> slot) & 1u));
+    return __ballot_sync(kFull, vis);
 }
 
 template <int SKIP, int U, int GS>
@@ -686,9 +811,10 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
         const int pk = lane < ns ? s_q[lane] : 0;
         const int pj = (pk >> 18) & (kRing - 1);
         const int E = __shfl_sync(kFull, myE, pj), r = __shfl_sync(kFull, myR, pj), c = __shfl_sync(kFull, myC, pj);
+        const int dr0 = (pk & 0x1ff) - 256, dc0 = ((pk >> 9) & 0x1ff) - 256;   // transmitter frame
         if (lane < ns) {
             const int H = a.zr1 - a.zr0;
-            int dr = (pk & 0x1ff) - 256, dc = ((pk >> 9) & 0x1ff) - 256;
+            int dr = dr0, dc = dc0;
             const int Zt = zld(z + (int64_t)(r + dr) * ncols + (c + dc)) + a.hr;
             n_cross += crossings_tab(dr, dc, gcdt);
             const bool tr = abs(dr) > abs(dc);
@@ -708,7 +834,7 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
                 g.f.Q = qp + (tr ? 2 * n + (int64_t)x * a.hp + y + (mneg ? nT : 0) : (int64_t)y * a.wp + x + (mneg ? n : 0));
                 g.f.msm = nm | ((nm == 0 ? 0 : (mneg ? -stride : stride)) * 256);
             }
-            g.f.Es = Es;
+            g.f.Esn = Es * nm - 1;
             // skip map (k_skipmap): padded 4x4-block indices of the start post,
             // SV row-major for column-major walks, ST column-major for row-major ones
             const int maj = tr ? y : x, mnr = tr ? x : y;
@@ -717,25 +843,27 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
                           : ((maj >> GS) + 1) + ((mnr >> GS) + 1) * a.pv;
             const int D = rev ? E - Zt : Zt - E;
             constexpr int G = 1 << GS;
-            g.c.LE2 = Es * nM + min(0, G * D);
+            g.c.LE2 = Es * nM + min(0, G * D) - 1;
             g.c.DG = G * D;
             const int mo = mnr & (G - 1);
             g.c.w = nM | ((mneg ? 2 * G - 1 - mo : mo) << 8) | ((int)tr << 13) | ((int)mneg << 14) | (mag << 15);
         }
         __syncwarp();
-        unsigned vism;
+        unsigned vism, tiem;
         if constexpr (SKIP == 1) {
-            vism = batch_skip<U, GS, TERR>(g, ns, lane, s_geo, s_pre, s_fail, smap, PQ);
+            vism = batch_skip<U, GS, TERR>(g, ns, lane, s_geo, s_pre, s_fail, smap, PQ, &tiem);
         } else {
             s_geo[lane] = g;
             __syncwarp();
-            bool vis = false;
+            int mine = kSegVis;
             for (int sidx = 0; sidx < ns; ++sidx) {
-                const bool blk = SKIP == 2 ? quad_walk_skip<GS>(s_geo + sidx, PQ, smap, s_fail, lane) : quad_walk<GS>(s_geo + sidx, lane);
-                if (lane == sidx) vis = !blk;
+                const int stt = SKIP == 2 ? quad_walk_skip<GS>(s_geo + sidx, PQ, smap, s_fail, lane) : quad_walk<GS>(s_geo + sidx, lane);
+                if (lane == sidx) mine = stt;
             }
-            vism = __ballot_sync(kFull, vis);
+            vism = __ballot_sync(kFull, lane < ns && mine != kSegBlk);
+            tiem = __ballot_sync(kFull, lane < ns && mine == kSegTie);
         }
+        if ((tiem >> lane) & 1u) push_tie(a, counters, r, c, dr0, dc0);
         // visible counts of the ring slots in this batch (posts p0 .. p1)
         const int p0 = p_open + (a.s_mul ? (int)__umulhi((unsigned)tq, a.s_mul) : tq / a.S);
         const int p1 = p_open + (a.s_mul ? (int)__umulhi((unsigned)(tq + ns - 1), a.s_mul) : (tq + ns - 1) / a.S);
@@ -868,17 +996,21 @@ __global__ void k_transpose(const int16_t* __restrict__ z, int16_t* __restrict__
     }
 }
 
-// one warp per pair
+// one warp per pair; exact walk, tied segments re-decided in fp64 (fp64 = 1)
 __global__ void k_los_batch(const int16_t* __restrict__ z, int nrows, int ncols, const int4* __restrict__ pairs,
-                            int64_t n, int ht, int hr, uint8_t* __restrict__ out) {
+                            int64_t n, int ht, int hr, int fp64, uint8_t* __restrict__ out) {
     const int lane = threadIdx.x & 31;
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     if (w >= n) return;
     const int4 p = pairs[w];
     const int16_t* P = z + (int64_t)p.x * ncols + p.y;
     const int E = zld(P) + ht, Zt = zld(z + (int64_t)p.z * ncols + p.w) + hr;
-    const bool blocked = warp_blocked<false, 1>(P, ncols, p.z - p.x, p.w - p.y, E, Zt, lane);
-    if (lane == 0) out[w] = blocked ? 0 : 1;
+    const int st = warp_blocked<false, 1>(P, ncols, p.z - p.x, p.w - p.y, E, Zt, lane);
+    if (lane == 0) {
+        bool blocked = st == 1;
+        if (st == 2 && fp64) blocked = seg_blocked_fp64(z, ncols, p.x, p.y, E, Zt, p.z - p.x, p.w - p.y);
+        out[w] = blocked ? 0 : 1;
+    }
 }
 
 }  // namespace
@@ -890,6 +1022,17 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     a.s_mul = a.S > 0 && a.S < 4096 ? (uint32_t)(((1ull << 32) + (uint64_t)a.S - 1) / (uint64_t)a.S) : 0u;
     a.seed = p.seed;
     a.span = make_fastmod((uint64_t)(2 * p.roi + 1));
+    // fp64 tie list (grazing ties: ~1e-4 of segments on the BASELINE terrains);
+    // txs_estimate_vix re-runs the stage with a larger list on overflow
+    {
+        const int64_t los = (c->band_r1 - c->band_r0) * c->ncols * (int64_t)p.samples_per_point;
+        const int64_t want = std::max<int64_t>(c->vix_tie_min, std::min<int64_t>(1 << 26, std::max<int64_t>(1 << 20, los / 1024)));
+        if (ensure(c, "vix", (void**)&c->d_ties, &c->ties_cap, sizeof(int4) * (size_t)want) != TXS_OK)
+            return TXS_ERR_OUT_OF_MEMORY;
+        a.ties = c->d_ties;
+        a.tie_cap = (long long)(c->ties_cap / sizeof(int4));
+        TXS_CUDA(c, "vix", cudaMemsetAsync(c->d_counters + kVixTies, 0, sizeof(unsigned long long), c->stream));
+    }
     a.tiles_x = (int)((c->ncols + kTile - 1) / kTile);
     a.tiles_y = (int)((c->band_r1 - c->band_r0 + kTile - 1) / kTile);
     const int tq = kTileQ;   // the quad path's tiles (see path 1 below)
@@ -1037,14 +1180,22 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     }
     if (st != TXS_OK) return st;
     TXS_LAUNCHED(c, "vix");
+    if (p.los_arith == TXS_LOS_FP64) {   // re-decide the tied segments in fp64
+        k_vix_fp64_ties<<<(unsigned)(c->num_sms * 4), 256, 0, c->stream>>>(c->zv(), c->ncols, c->d_ties, c->d_counters,
+                                                                          a.tie_cap, p.tx_height, p.rx_height,
+                                                                          c->d_vix - c->band_r0 * c->ncols);
+        TXS_LAUNCHED(c, "vix");
+    }
     return TXS_OK;
 }
 
-txs_status launch_los_batch(txs_ctx* c, const int32_t* d_pairs, int64_t n, int32_t ht, int32_t hr, uint8_t* d_out) {
+txs_status launch_los_batch(txs_ctx* c, const int32_t* d_pairs, int64_t n, int32_t ht, int32_t hr, int32_t arith,
+                            uint8_t* d_out) {
     const int64_t threads = n * 32;
     const unsigned blocks = (unsigned)((threads + 255) / 256);
     set_zbounds(c->d_z, c->d_z + c->z_rows * c->ncols, c->stream);
-    k_los_batch<<<blocks, 256, 0, c->stream>>>(c->zv(), (int)c->nrows, (int)c->ncols, (const int4*)d_pairs, n, ht, hr, d_out);
+    k_los_batch<<<blocks, 256, 0, c->stream>>>(c->zv(), (int)c->nrows, (int)c->ncols, (const int4*)d_pairs, n, ht, hr,
+                                                 arith == TXS_LOS_FP64 ? 1 : 0, d_out);
     TXS_LAUNCHED(c, "los");
     return TXS_OK;
 }

@@ -30,6 +30,7 @@ txs_params to_params(const SiteParams& p, uint64_t seed = 0) {
     q.per_block = p.per_block;
     q.block_width = p.block_width;
     q.site_mode = p.site_mode;
+    q.los_arith = p.los_arith;
     q.target_coverage = p.target_coverage;
     q.max_selected = p.max_selected;
     q.seed = seed;
@@ -176,7 +177,8 @@ double elevation_between(const TerrainGrid& g, GridPoint p, GridPoint q, double 
 
 // ---- los -----------------------------------------------------------------------------
 std::vector<uint8_t> is_visible_batch(const TerrainGrid& g, const std::vector<GridPoint>& tx,
-                                      const std::vector<GridPoint>& rx, int32_t ht, int32_t hr) {
+                                      const std::vector<GridPoint>& rx, int32_t ht, int32_t hr,
+                                      int32_t los_arith) {
     if (tx.size() != rx.size()) throw Error(TXS_ERR_SIZE_MISMATCH, "[los] tx/rx size mismatch");
     std::vector<int32_t> pairs(4 * tx.size());
     for (size_t i = 0; i < tx.size(); ++i) {
@@ -187,7 +189,7 @@ std::vector<uint8_t> is_visible_batch(const TerrainGrid& g, const std::vector<Gr
     txs_ctx* c = shared_ctx();
     upload(c, g);
     std::vector<uint8_t> out(tx.size());
-    check(c, txs_is_visible_batch(c, pairs.data(), (int64_t)tx.size(), ht, hr, out.data()));
+    check(c, txs_is_visible_batch(c, pairs.data(), (int64_t)tx.size(), ht, hr, los_arith, out.data()));
     return out;
 }
 

@@ -29,3 +29,10 @@ def engine():
     e = T.Engine(0)
     yield e
     e.close()
+
+
+@pytest.fixture(scope="session")
+def c1_terrain():
+    """BASELINE config 1's terrain (1000x1000, roughness 0.5, 0..4000), oracle-generated."""
+    import oracle_lib as O
+    return O.generate_fractal(1000, 1000, 0.5, 1, 0, 4000)

@@ -75,6 +75,20 @@ def main():
     R.ref_estimate_vix_fp64(O._p(z), 96, 96, 20, 10, 10, 10, 99, 0, O._p(fp), 0, 96)
     kat["vix_fp64"] = {"terrain": "generate_fractal(96,96,0.5,7,0,4000)", "roi": 20, "ht": 10, "hr": 10,
                        "samples": 10, "seed": 99, "scores": fp.ravel().tolist()}
+    # SPEC.md:147 fp64 LOS decisions of the reference walk on a tie-heavy terrain:
+    # elevations quantized to multiples of 50 with a flat band, so the terrain
+    # often touches the LOS exactly (grazing ties that fp64 rounding decides).
+    zq = (O.generate_fractal(80, 80, 0.6, 31, 0, 600) // 50 * 50).astype(np.int16)
+    zq[30:40, :] = 100
+    rng = np.random.default_rng(1234)
+    pairs = rng.integers(0, 80, size=(6000, 4)).astype(np.int64)
+    vis = [int(R.ref_is_visible_fp64(O._p(zq), 80, 80, int(a), int(b), 0, int(c), int(d), 0))
+           for a, b, c, d in pairs]
+    kat["los_fp64_ties"] = {"terrain": "generate_fractal(80,80,0.6,31,0,600)//50*50, rows 30..39 = 100",
+                            "ht": 0, "hr": 0, "pairs": pairs.ravel().tolist(), "visible": vis}
+    fq = np.zeros((80, 80), np.uint8)
+    R.ref_estimate_vix_fp64(O._p(zq), 80, 80, 15, 0, 0, 12, 4242, 0, O._p(fq), 0, 80)
+    kat["vix_fp64_ties"] = {"roi": 15, "ht": 0, "hr": 0, "samples": 12, "seed": 4242, "scores": fq.ravel().tolist()}
     with open(os.path.join(HERE, "kat.json"), "w") as f:
         json.dump(kat, f, separators=(",", ":"))
     print("wrote", os.path.join(HERE, "kat.json"))

@@ -10,7 +10,7 @@ import os
 import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-ORACLE_SO = os.path.join(ROOT, "oracle", "liboracle.so")
+ORACLE_SO = os.environ.get("ORACLE_SO", os.path.join(ROOT, "oracle", "liboracle.so"))
 REF_SO = os.path.join(ROOT, "oracle", "_ref", "libtxs_ref.so")
 
 i64, u64, i32, dbl, vp = C.c_int64, C.c_uint64, C.c_int32, C.c_double, C.c_void_p
@@ -42,16 +42,16 @@ def lib():
         L.txo_generate_fractal.restype = C.c_int
         L.txo_generate_fractal.argtypes = [i64, i64, dbl, u64, i32, i32, vp, C.c_uint]
         L.txo_is_visible.restype = C.c_int
-        L.txo_is_visible.argtypes = [vp, i64, i64, i64, i64, i64, i64, i64, i64]
-        L.txo_is_visible_batch.argtypes = [vp, i64, i64, vp, i64, i64, i64, vp, C.c_uint]
-        L.txo_estimate_vix.argtypes = [vp, i64, i64, i64, i64, i64, i64, u64, C.c_uint, vp, i64, i64]
+        L.txo_is_visible.argtypes = [vp, i64, i64, i64, i64, i64, i64, i64, i64, C.c_int]
+        L.txo_is_visible_batch.argtypes = [vp, i64, i64, vp, i64, i64, i64, vp, C.c_uint, C.c_int]
+        L.txo_estimate_vix.argtypes = [vp, i64, i64, i64, i64, i64, i64, u64, C.c_uint, vp, i64, i64, C.c_int]
         L.txo_find_candidates.restype = i64
         L.txo_find_candidates.argtypes = [vp, i64, i64, i64, i64, vp, vp, vp, i64]
         L.txo_midpoint_circle_count.restype = i64
         L.txo_midpoint_circle_count.argtypes = [i64]
         L.txo_template.restype = i64
         L.txo_template.argtypes = [i64, vp, vp, vp, vp, vp, i64, i64, vp]
-        L.txo_viewsheds.argtypes = [vp, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp, i64, C.c_uint]
+        L.txo_viewsheds.argtypes = [vp, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp, i64, C.c_uint, C.c_int]
         L.txo_marginal_gain.restype = i64
         L.txo_marginal_gain.argtypes = [vp, vp, vp, i64, i64, C.c_int]
         L.txo_site.restype = C.c_int
@@ -121,24 +121,32 @@ def generate_fractal(nrows, ncols, roughness, seed, zmin, zmax, threads=0):
     return z
 
 
-def is_visible(z, tr, tc, ht, rr, rc, hr):
+# LOS arithmetic (txs_params.los_arith): "fp64" = SPEC.md:147's formula, the
+# reference's and the engine's default; "exact" = exact rationals (SPEC.md:120's
+# real-number predicate; differs from fp64 only at exact grazing ties).
+ARITH = {"fp64": 0, "exact": 1, "fp64-euclid": 2}   # fp64-euclid: viewsheds only (oracle.cpp)
+
+
+def is_visible(z, tr, tc, ht, rr, rc, hr, arith="fp64"):
     z = np.ascontiguousarray(z, np.int16)
-    return bool(lib().txo_is_visible(_p(z), z.shape[0], z.shape[1], tr, tc, ht, rr, rc, hr))
+    return bool(lib().txo_is_visible(_p(z), z.shape[0], z.shape[1], tr, tc, ht, rr, rc, hr, ARITH[arith]))
 
 
-def is_visible_batch(z, pairs, ht, hr, threads=0):
+def is_visible_batch(z, pairs, ht, hr, threads=0, arith="fp64"):
     z = np.ascontiguousarray(z, np.int16)
     pairs = np.ascontiguousarray(pairs, np.int32)
     out = np.zeros(len(pairs), np.uint8)
-    lib().txo_is_visible_batch(_p(z), z.shape[0], z.shape[1], _p(pairs), len(pairs), ht, hr, _p(out), threads)
+    lib().txo_is_visible_batch(_p(z), z.shape[0], z.shape[1], _p(pairs), len(pairs), ht, hr, _p(out), threads,
+                               ARITH[arith])
     return out
 
 
-def estimate_vix(z, roi, ht, hr, samples, seed, threads=0, rows=None):
+def estimate_vix(z, roi, ht, hr, samples, seed, threads=0, rows=None, arith="fp64"):
     z = np.ascontiguousarray(z, np.int16)
     out = np.zeros(z.shape, np.uint8)
     rb, re = rows if rows is not None else (0, z.shape[0])
-    lib().txo_estimate_vix(_p(z), z.shape[0], z.shape[1], roi, ht, hr, samples, seed, threads, _p(out), rb, re)
+    lib().txo_estimate_vix(_p(z), z.shape[0], z.shape[1], roi, ht, hr, samples, seed, threads, _p(out), rb, re,
+                           ARITH[arith])
     return out
 
 
@@ -166,7 +174,7 @@ def max_words(roi):
     return (s * s + 63) // 64
 
 
-def viewsheds(z, roi, ht, hr, rows, cols, threads=0):
+def viewsheds(z, roi, ht, hr, rows, cols, threads=0, arith="fp64"):
     z = np.ascontiguousarray(z, np.int16)
     rows = np.ascontiguousarray(rows, np.int32)
     cols = np.ascontiguousarray(cols, np.int32)
@@ -175,7 +183,7 @@ def viewsheds(z, roi, ht, hr, rows, cols, threads=0):
     wins = np.zeros((n, 4), np.int32)
     words = np.zeros((n, stride), np.uint64)
     lib().txo_viewsheds(_p(z), z.shape[0], z.shape[1], roi, ht, hr, n, _p(rows), _p(cols),
-                        _p(wins), _p(words), stride, threads)
+                        _p(wins), _p(words), stride, threads, ARITH[arith])
     return wins, words
 
 
@@ -242,6 +250,16 @@ def pack_dense(bits2d):
     pad = (-len(flat)) % 64
     flat = np.concatenate([flat, np.zeros(pad, np.uint8)])
     return np.packbits(flat, bitorder="little").view(np.uint64).copy()
+
+
+def viewshed_ties(z, roi, ht, hr, r, c):
+    """(exact words, tie-cell words) of one viewshed (window layout, D8)."""
+    L = lib()
+    L.txo_viewshed_ties.argtypes = [vp, i64, i64, i64, i64, i64, i64, i64, vp, vp]
+    z = np.ascontiguousarray(z, np.int16)
+    w, t = np.zeros(max_words(roi), np.uint64), np.zeros(max_words(roi), np.uint64)
+    L.txo_viewshed_ties(_p(z), z.shape[0], z.shape[1], roi, ht, hr, r, c, _p(w), _p(t))
+    return w, t
 
 
 def los_class(z, tr, tc, ht, rr, rc, hr):

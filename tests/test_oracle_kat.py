@@ -76,3 +76,82 @@ def test_live_reference_shim_random_segments():
         dr, dc = (int(x) for x in rng.integers(-300, 301, 2))
         e = int(rng.integers(0, 2))
         assert O.walk_hash(r0, c0, r0 + dr, c0 + dc, e) == O.walk_hash(r0, c0, r0 + dr, c0 + dc, e, R)
+
+
+# ---- SPEC.md:147 fp64 formula: the oracle's fp64 mode pinned to the reference walk ----
+def _tie_terrain():
+    zq = (O.generate_fractal(80, 80, 0.6, 31, 0, 600) // 50 * 50).astype(np.int16)
+    zq[30:40, :] = 100
+    return zq
+
+
+def test_fp64_los_pinned_on_tie_heavy_terrain(kat):
+    """Golden fp64 decisions of the REFERENCE walk_crossings (oracle/ref_shim.cpp)
+    on a terrain built to produce grazing ties: the oracle's fp64 is_visible and
+    estimate_vix match bit for bit; the exact predicate differs only at ties."""
+    zq = _tie_terrain()
+    g = kat["los_fp64_ties"]
+    pairs = np.array(g["pairs"], np.int32).reshape(-1, 4)
+    f = O.is_visible_batch(zq, pairs, g["ht"], g["hr"])
+    assert np.array_equal(f, np.array(g["visible"], np.uint8))
+    e = O.is_visible_batch(zq, pairs, g["ht"], g["hr"], arith="exact")
+    diff = np.nonzero(f != e)[0]
+    assert len(diff) > 0                                      # the fixture exercises ties
+    for i in diff:
+        a, b, c, d = (int(x) for x in pairs[i])
+        assert e[i] == 1 and O.los_class(zq, a, b, 0, c, d, 0) == 0
+    v = kat["vix_fp64_ties"]
+    s = O.estimate_vix(zq, v["roi"], v["ht"], v["hr"], v["samples"], v["seed"])
+    assert np.array_equal(s.ravel(), np.array(v["scores"], np.uint8))
+
+
+@pytest.mark.skipif(O.ref() is None, reason="oracle/_ref not built (no /root/reference here)")
+def test_fp64_vix_live_against_reference_walk():
+    """Fresh terrains, live: oracle fp64 estimate_vix == SPEC.md:147 on the
+    compiled reference walk_crossings (ref_estimate_vix_fp64)."""
+    R = O.ref()
+    for seed, (n, rough, roi, h, S) in enumerate([(120, 0.5, 30, 10, 10), (90, 0.6, 45, 20, 20), (100, 0.3, 12, 0, 8)]):
+        z = O.generate_fractal(n, n, rough, 500 + seed, 0, 4000)
+        if seed == 2:
+            z = (z // 100 * 100).astype(np.int16)
+        ref = np.zeros((n, n), np.uint8)
+        R.ref_estimate_vix_fp64(O._p(z), n, n, roi, h, h, S, 77 + seed, 0, O._p(ref), 0, n)
+        assert np.array_equal(O.estimate_vix(z, roi, h, h, S, 77 + seed), ref), seed
+
+
+def test_viewshed_fp64_differs_from_exact_only_at_ties():
+    """The fp64 R2 formula (oracle compute_viewshed_fp64) and the exact one agree
+    on every cell whose tangent is not EXACTLY its horizon."""
+    z = O.generate_fractal(300, 300, 0.5, 2006, 0, 4000)
+    rng = np.random.default_rng(3)
+    rows, cols = rng.integers(0, 300, 60).astype(np.int32), rng.integers(0, 300, 60).astype(np.int32)
+    for roi, h in ((40, 10), (100, 10), (60, 50)):
+        wf, vf = O.viewsheds(z, roi, h, h, rows, cols)
+        nties = nflip = 0
+        for i in range(len(rows)):
+            ve, vt = O.viewshed_ties(z, roi, h, h, int(rows[i]), int(cols[i]))
+            x = ve ^ vf[i]
+            assert not (x & ~vt).any(), (roi, i)              # differences only at tie cells
+            nties += int(np.unpackbits(vt.view(np.uint8)).sum())
+            nflip += int(np.unpackbits(x.view(np.uint8)).sum())
+        assert nflip <= nties
+        print(f"roi {roi}: {nties} tie cells, {nflip} decided differently by fp64")
+
+
+@pytest.mark.parametrize("roi,h,rough,zmax", [(100, 10, 0.5, 4000), (200, 20, 0.6, 3000), (250, 50, 0.5, 4000)])
+def test_viewshed_fp64_vs_d4_euclid_within_tolerance(roi, h, rough, zmax):
+    """SURVEY Appendix A D4 verbatim takes a cell's own Euclidean run
+    sqrt(a^2 + b^2); the engine's fp64 formula runs a cell along its owner ray
+    (D5, dot / |(p,q)|), which equals the exact predicate away from ties.  The
+    bits the choice moves are counted at the BASELINE ROIs / heights on
+    interior observers: <= 1e-5 of window bits (north_star tolerance)."""
+    z = O.generate_fractal(900, 900, rough, 2006 + roi, 0, zmax)
+    rng = np.random.default_rng(roi)
+    rows = rng.integers(roi, 900 - roi, 150).astype(np.int32)
+    cols = rng.integers(roi, 900 - roi, 150).astype(np.int32)
+    wf, vf = O.viewsheds(z, roi, h, h, rows, cols)
+    _, vd = O.viewsheds(z, roi, h, h, rows, cols, arith="fp64-euclid")
+    area = int((wf[:, 2] * wf[:, 3]).sum())
+    d4 = int(np.unpackbits((vf ^ vd).view(np.uint8)).sum())
+    print(f"roi {roi}: D4-euclid moves {d4} of {area} bits ({d4 / area:.2e})")
+    assert d4 <= 1e-5 * area

