@@ -101,6 +101,9 @@ typedef struct txs_stats {
      * decisions fp64 rounding changed (VIX: segments; VIEWSHED: rays / bits). */
     int64_t vix_fp64_ties, vix_fp64_flips;
     int64_t vs_fp64_ties, vs_fp64_flips;
+    /* device time of the stage's main kernel alone (k_vix_quads / k_vix, the
+     * VIEWSHED sweep), CUDA events on the context stream around that launch */
+    double ms_vix_kernel, ms_viewshed_kernel;
 } txs_stats;
 
 typedef struct txs_ctx txs_ctx;

@@ -187,24 +187,28 @@ void estimate_vix(const Grid& g, int64_t roi, int64_t ht, int64_t hr, int64_t sa
 // within a block score desc, then (row, col) asc; min(per_block, size) each.
 // ---------------------------------------------------------------------------
 std::vector<Cand> find_candidates(const uint8_t* scores, int64_t nrows, int64_t ncols,
-                                  int64_t bw, int64_t per_block) {
-    std::vector<Cand> out;
+                                  int64_t bw, int64_t per_block, unsigned threads) {
     const int64_t by = (nrows + bw - 1) / bw, bx = (ncols + bw - 1) / bw;
-    std::vector<Cand> tmp;
-    for (int64_t i = 0; i < by; ++i)
-        for (int64_t j = 0; j < bx; ++j) {
-            tmp.clear();
-            for (int64_t r = i * bw; r < std::min(nrows, (i + 1) * bw); ++r)
-                for (int64_t c = j * bw; c < std::min(ncols, (j + 1) * bw); ++c)
-                    tmp.push_back({(int32_t)r, (int32_t)c, scores[r * ncols + c]});
-            const int64_t k = std::min<int64_t>(per_block, (int64_t)tmp.size());
-            std::partial_sort(tmp.begin(), tmp.begin() + k, tmp.end(), [](const Cand& a, const Cand& b) {
-                if (a.score != b.score) return a.score > b.score;
-                if (a.row != b.row) return a.row < b.row;
-                return a.col < b.col;
-            });
-            out.insert(out.end(), tmp.begin(), tmp.begin() + k);
-        }
+    std::vector<std::vector<Cand>> rows_out((size_t)by);   // per block row, in block order
+    parallel_chunks(by, threads, [&](int64_t b, int64_t e) {
+        std::vector<Cand> tmp;
+        for (int64_t i = b; i < e; ++i)
+            for (int64_t j = 0; j < bx; ++j) {
+                tmp.clear();
+                for (int64_t r = i * bw; r < std::min(nrows, (i + 1) * bw); ++r)
+                    for (int64_t c = j * bw; c < std::min(ncols, (j + 1) * bw); ++c)
+                        tmp.push_back({(int32_t)r, (int32_t)c, scores[r * ncols + c]});
+                const int64_t k = std::min<int64_t>(per_block, (int64_t)tmp.size());
+                std::partial_sort(tmp.begin(), tmp.begin() + k, tmp.end(), [](const Cand& x, const Cand& y) {
+                    if (x.score != y.score) return x.score > y.score;
+                    if (x.row != y.row) return x.row < y.row;
+                    return x.col < y.col;
+                });
+                rows_out[(size_t)i].insert(rows_out[(size_t)i].end(), tmp.begin(), tmp.begin() + k);
+            }
+    });
+    std::vector<Cand> out;
+    for (auto& v : rows_out) out.insert(out.end(), v.begin(), v.end());
     return out;
 }
 

@@ -130,7 +130,7 @@ void estimate_vix(const Grid& g, int64_t roi, int64_t ht, int64_t hr, int64_t sa
 // ---- candidates, decision D7 -----------------------------
 struct Cand { int32_t row, col, score; };
 std::vector<Cand> find_candidates(const uint8_t* scores, int64_t nrows, int64_t ncols,
-                                  int64_t block_width, int64_t per_block);
+                                  int64_t block_width, int64_t per_block, unsigned threads = 0);
 
 // ---- viewshed, decision D5/D8 ----------------------------
 struct RayTemplate {

@@ -116,6 +116,21 @@ void txo_estimate_vix(const int16_t* z, int64_t nrows, int64_t ncols, int64_t ro
     estimate_vix(g, roi, ht, hr, samples, seed, threads, scores, row_begin, row_end, arith);
 }
 
+// estimate_vix on an arbitrary set of rows: out is len(rows) x ncols
+void txo_estimate_vix_rows(const int16_t* z, int64_t nrows, int64_t ncols, int64_t roi, int64_t ht,
+                           int64_t hr, int64_t samples, uint64_t seed, unsigned threads,
+                           const int64_t* rows, int64_t nsel, uint8_t* out, int arith) {
+    Grid g{nrows, ncols, z};
+    par(nsel, threads, [&](int64_t b, int64_t e) {
+        std::vector<uint8_t> full;
+        for (int64_t i = b; i < e; ++i) {
+            // scores lands at row rows[i] of a virtual full map: offset the pointer
+            estimate_vix(g, roi, ht, hr, samples, seed, 1, out + i * ncols - rows[i] * ncols, rows[i], rows[i] + 1,
+                         arith);
+        }
+    });
+}
+
 int64_t txo_find_candidates(const uint8_t* scores, int64_t nrows, int64_t ncols, int64_t bw,
                             int64_t per_block, int32_t* rows, int32_t* cols, int32_t* sc,
                             int64_t cap) {

@@ -53,7 +53,8 @@ class Stats(C.Structure):
                 ("viewshed_crossings", i64), ("viewshed_cells", i64), ("site_iterations", i64),
                 ("site_bytes", i64), ("site_launches", i64), ("candidates", i64),
                 ("kernel_launches", i64), ("ms_site_rounds", dbl),
-                ("vix_fp64_ties", i64), ("vix_fp64_flips", i64), ("vs_fp64_ties", i64), ("vs_fp64_flips", i64)]
+                ("vix_fp64_ties", i64), ("vix_fp64_flips", i64), ("vs_fp64_ties", i64), ("vs_fp64_flips", i64),
+                ("ms_vix_kernel", dbl), ("ms_viewshed_kernel", dbl)]
 
 
 def _sig(name, res, args):

@@ -101,6 +101,7 @@ txs_status txs_create(int device, txs_ctx** out) {
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
         cudaEventCreate(&c->ev_r0) != cudaSuccess || cudaEventCreate(&c->ev_r1) != cudaSuccess ||
+        cudaEventCreate(&c->ev_k0) != cudaSuccess || cudaEventCreate(&c->ev_k1) != cudaSuccess ||
         cudaMalloc(&c->d_counters, sizeof(unsigned long long) * kNumCounters) != cudaSuccess ||
         cudaMalloc(&c->d_state, sizeof(SiteState)) != cudaSuccess ||
         cudaMallocHost(&c->h_state, sizeof(SiteState)) != cudaSuccess) {
@@ -119,7 +120,7 @@ void txs_destroy(txs_ctx* c) {
     void* bufs[] = {c->d_shard_steps, c->d_z, c->d_zt, c->d_pairs, c->d_gcd, c->d_vix, c->d_crow, c->d_ccol, c->d_cscore, c->d_words, c->d_win,
                     c->d_pop, c->d_cum, c->d_dwin, c->d_dspan, c->d_partials, c->d_gain, c->d_state,
                     c->d_bucket_start, c->d_bucket_items, c->d_counters, c->d_scratch, c->d_cgid, c->d_xfer,
-                    c->d_cum_dense};
+                    c->d_cum_dense, c->d_ties};
     for (void* p : bufs) if (p) cudaFree(p);
     for (auto& kv : c->templates) {
         cudaFree(kv.second.rays); cudaFree(kv.second.cells);
@@ -132,6 +133,8 @@ void txs_destroy(txs_ctx* c) {
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->ev_r0) cudaEventDestroy(c->ev_r0);
     if (c->ev_r1) cudaEventDestroy(c->ev_r1);
+    if (c->ev_k0) cudaEventDestroy(c->ev_k0);
+    if (c->ev_k1) cudaEventDestroy(c->ev_k1);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -348,6 +351,8 @@ txs_status txs_estimate_vix(txs_ctx* c, const txs_params* p, uint8_t* scores_out
         TXS_CUDA(c, "vix", cudaMemcpy(&nt, c->d_counters + kVixTies, sizeof(nt), cudaMemcpyDeviceToHost));
         if ((size_t)nt <= c->ties_cap / sizeof(int4) || p->los_arith != TXS_LOS_FP64) {
             if (p->los_arith == TXS_LOS_FP64) c->stats.vix_fp64_ties += (int64_t)nt;
+            float f = 0.f;   // the main VIX kernel alone (launch_vix brackets it with ev_k0/ev_k1)
+            if (cudaEventElapsedTime(&f, c->ev_k0, c->ev_k1) == cudaSuccess) c->stats.ms_vix_kernel += f;
             break;
         }
         if (attempt > 0) return fail(c, TXS_ERR_OUT_OF_MEMORY, "vix", "fp64 tie list overflow");
@@ -515,6 +520,8 @@ txs_status txs_compute_viewsheds(txs_ctx* c, const txs_params* p) {
         if (st != TXS_OK) return st;
         st = t.stop("viewshed");
         if (st != TXS_OK) return st;
+        float f = 0.f;   // the sweep kernel alone (launch_viewsheds brackets it with ev_k0/ev_k1)
+        if (c->ncand > 0 && cudaEventElapsedTime(&f, c->ev_k0, c->ev_k1) == cudaSuccess) c->stats.ms_viewshed_kernel += f;
         if (c->ncand == 0 || p->los_arith != TXS_LOS_FP64) break;
         // the fp64 tie list overflowed (never seen on the BASELINE terrains): re-run with room
         unsigned long long nt = 0;

@@ -160,6 +160,7 @@ struct txs_ctx {
     unsigned long long* d_counters = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t ev_r0 = nullptr, ev_r1 = nullptr;   // SITE round-loop timer
+    cudaEvent_t ev_k0 = nullptr, ev_k1 = nullptr;   // the stage's main kernel alone (VIX / VIEWSHED)
     cudaEvent_t user_ev[16] = {};
     int64_t launches = 0;
 

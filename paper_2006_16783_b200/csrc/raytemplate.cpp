@@ -103,9 +103,11 @@ RayTemplate build(int32_t R) {
 // the crossings of its primitive direction interleaved with its owned cells,
 // a cell emitted before every crossing with u_k >= u_c, nothing after the
 // last cell.  Event (uint2):
-//   x: bits 0-2 type, 3-11 row offset, 12-20 col offset (9-bit two's
-//      complement) of the crossing's FIRST interpolation post, 24-31 its
-//      weight w0 (so that one byte permute yields the dp2a weight word);
+//   x: bits 0-2 type, 3-11 row offset dr (9-bit two's complement) of the
+//      crossing's FIRST interpolation post, 12-21 F = 2*dc + (column crossing)
+//      (10-bit two's complement; dc = F >> 1, and F is the word offset of the
+//      post's pair in the interleaved (H, V) pair planes), 24-31 its weight w0
+//      (so that one byte permute yields the dp2a weight word);
 //   y: bits 0-23 the crossing's line index (its slope's M) or, for a cell, its
 //      projection numerator dot = a*p + b*q; bits 24-31 the weight w1 of the
 //      second post, which lies one column right (row crossing) or one row down

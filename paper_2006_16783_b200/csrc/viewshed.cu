@@ -888,18 +888,21 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
             auto kern = cap64 ? k_viewshed_evk<3, 64, 2> : k_viewshed_evk<3, 72, 2>;
             if (sm > 48 * 1024)
                 TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            cudaEventRecord(c->ev_k0, c->stream);
             kern<<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
                                                                  T->ngroups, a, c->d_words, c->d_win, c->d_pop, c->d_counters);
         } else if (kobs == 2) {
             auto kern = cap64 ? (step4 ? k_viewshed_evk<2, 64, 4> : k_viewshed_evk<2, 64, 2>) : k_viewshed_evk<2, 72, 2>;
             if (sm > 48 * 1024)
                 TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            cudaEventRecord(c->ev_k0, c->stream);
             kern<<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
                                                                  T->ngroups, a, c->d_words, c->d_win, c->d_pop, c->d_counters);
         } else {
             auto kern = cap64 ? k_viewshed_evk<4, 64, 2> : k_viewshed_evk<4, 72, 2>;
             if (sm > 48 * 1024)
                 TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            cudaEventRecord(c->ev_k0, c->stream);
             kern<<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
                                                                  T->ngroups, a, c->d_words, c->d_win, c->d_pop, c->d_counters);
         }
@@ -913,10 +916,12 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
         if (smem_bits) {
             if (smem > 48 * 1024)
                 TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(k_viewshed_ev<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            cudaEventRecord(c->ev_k0, c->stream);
             k_viewshed_ev<true><<<(unsigned)n, threads, smem, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups,
                                                                           T->events, T->ngroups, a, c->d_words, c->d_win,
                                                                           c->d_pop, c->d_counters);
         } else {
+            cudaEventRecord(c->ev_k0, c->stream);
             k_viewshed_ev<false><<<(unsigned)n, threads, 0, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups,
                                                                         T->events, T->ngroups, a, c->d_words, c->d_win,
                                                                         c->d_pop, c->d_counters);
@@ -927,13 +932,16 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
         if (smem_bits) {
             if (smem > 48 * 1024)
                 TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(k_viewshed<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            cudaEventRecord(c->ev_k0, c->stream);
             k_viewshed<true><<<(unsigned)n, threads, smem, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->cells, a,
                                                                         c->d_words, c->d_win, c->d_pop, c->d_counters);
         } else {
+            cudaEventRecord(c->ev_k0, c->stream);
             k_viewshed<false><<<(unsigned)n, threads, 0, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->cells, a,
                                                                      c->d_words, c->d_win, c->d_pop, c->d_counters);
         }
     }
+    cudaEventRecord(c->ev_k1, c->stream);
     TXS_LAUNCHED(c, "viewshed");
     if (p.los_arith == TXS_LOS_FP64) {   // re-decide the tied rays in fp64
         k_vs_fp64_ties<<<(unsigned)(c->num_sms * 4), 128, 0, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->cells, a,

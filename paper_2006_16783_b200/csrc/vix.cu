@@ -1079,7 +1079,9 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     }
     set_zbounds(c->d_z, c->d_z + c->z_rows * c->ncols, c->stream);
     if (path == 0) {
+        cudaEventRecord(c->ev_k0, c->stream);
         st = go(k_vix<true, 1>, smem);
+        cudaEventRecord(c->ev_k1, c->stream);
     } else if (path == 1) {
         const int64_t n = c->z_rows * c->ncols;
         int64_t nq = 2 * c->z_rows * (int64_t)a.wp + 2 * c->ncols * (int64_t)a.hp;
@@ -1163,9 +1165,11 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         int64_t grid_q = std::min<int64_t>(tiles_q, (int64_t)std::max(1, per_sm) * c->num_sms);
         if (const char* e = getenv("TXS_VIX_GRID")) grid_q = std::min<int64_t>(tiles_q, std::max(1, atoi(e)));
         TXS_CUDA(c, "vix", cudaMemsetAsync(c->d_counters + kVixNext, 0, sizeof(unsigned long long), c->stream));
+        cudaEventRecord(c->ev_k0, c->stream);
         kq<<<(unsigned)grid_q, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols,
                                                                 c->d_vix - c->band_r0 * c->ncols, aq, c->d_gcd, smap,
                                                                 c->d_counters);
+        cudaEventRecord(c->ev_k1, c->stream);
         st = TXS_OK;
     } else {
         if (ensure(c, "vix", (void**)&c->d_zt, &c->zt_cap, sizeof(int16_t) * c->z_rows * c->ncols) != TXS_OK)
@@ -1176,7 +1180,9 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
             TXS_LAUNCHED(c, "vix");
         }
         set_zbounds(c->d_z, c->d_z + c->z_rows * c->ncols, c->stream, c->d_zt, c->d_zt + c->z_rows * c->ncols);
+        cudaEventRecord(c->ev_k0, c->stream);
         st = go(k_vix<false, 1>, samp);
+        cudaEventRecord(c->ev_k1, c->stream);
     }
     if (st != TXS_OK) return st;
     TXS_LAUNCHED(c, "vix");

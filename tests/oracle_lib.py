@@ -150,6 +150,23 @@ def estimate_vix(z, roi, ht, hr, samples, seed, threads=0, rows=None, arith="fp6
     return out
 
 
+def estimate_vix_rows(z, roi, ht, hr, samples, seed, rows, threads=0, arith="fp64"):
+    """VixMap rows `rows` only (len(rows) x ncols), same values as estimate_vix."""
+    L = lib()
+    L.txo_estimate_vix_rows.argtypes = [vp, i64, i64, i64, i64, i64, i64, u64, C.c_uint, vp, i64, vp, C.c_int]
+    z = np.ascontiguousarray(z, np.int16)
+    rows = np.ascontiguousarray(rows, np.int64)
+    out = np.zeros((len(rows), z.shape[1]), np.uint8)
+    L.txo_estimate_vix_rows(_p(z), z.shape[0], z.shape[1], roi, ht, hr, samples, seed, threads, _p(rows), len(rows),
+                            _p(out), ARITH[arith])
+    return out
+
+
+def popcounts(words):
+    """Per-row popcount of a 2-D uint64 array."""
+    return np.bitwise_count(np.ascontiguousarray(words, np.uint64)).sum(axis=-1, dtype=np.int64)
+
+
 def find_candidates(scores, block_width, per_block):
     scores = np.ascontiguousarray(scores, np.uint8)
     nr, nc = scores.shape

@@ -221,11 +221,12 @@ def test_viewsheds_c1_bit_exact(engine, c1):
     _vs_compare(engine, c1, 100, 10, 10, rows, cols)
 
 
-@pytest.mark.parametrize("k,pairs", [(1, 0), (2, 0), (2, 1), (4, 1)])
-def test_viewsheds_k_paths_bit_exact(engine, monkeypatch, k, pairs):
-    """Every VIEWSHED sweep: K observers per CTA (1/2/4, TXS_VS_K), int16 posts
-    or H/V pair planes (TXS_VS_PAIRS), tile-sorted order (n >= 4096), CTAs
-    mixing interior and edge observers -- all against the oracle."""
+@pytest.mark.parametrize("k,pairs,step", [(1, 0, 2), (2, 0, 2), (2, 1, 2), (4, 1, 2), (2, 1, 4), (3, 1, 2)])
+def test_viewsheds_k_paths_bit_exact(engine, monkeypatch, k, pairs, step):
+    """Every VIEWSHED sweep: K observers per CTA (1/2/3/4, TXS_VS_K), int16 posts
+    or H/V pair planes (TXS_VS_PAIRS), 2 or 4 events per sweep iteration
+    (TXS_VS_STEP), tile-sorted order (n >= 4096), CTAs mixing interior and edge
+    observers (corners, edges) -- all against the oracle."""
     rng = np.random.default_rng(100 + k)
     z = O.generate_fractal(700, 650, 0.6, 33, -200, 2500)
     n = 5000
@@ -233,7 +234,21 @@ def test_viewsheds_k_paths_bit_exact(engine, monkeypatch, k, pairs):
     rows[:6], cols[:6] = [0, 699, 0, 699, 41, 658], [0, 649, 649, 0, 41, 608]
     monkeypatch.setenv("TXS_VS_K", str(k))
     monkeypatch.setenv("TXS_VS_PAIRS", str(pairs))
+    monkeypatch.setenv("TXS_VS_STEP", str(step))
     _vs_compare(engine, z, 40, 15, 5, rows, cols)
+
+
+def test_viewsheds_c5_default_path(engine):
+    """The C5 production sweep with no overrides: roi 250 >= 225 selects K = 2
+    observers per CTA, 4 events per iteration and the interleaved pair planes
+    (>= 2 * SMs * 4 observers); interior, edge and corner observers of a grid
+    only a little larger than the window, compared in full."""
+    rng = np.random.default_rng(250)
+    z = O.generate_fractal(900, 1000, 0.5, 35, 0, 4000)
+    n = 2 * 148 * 4 + 321
+    rows, cols = rng.integers(0, 900, n).astype(np.int32), rng.integers(0, 1000, n).astype(np.int32)
+    rows[:8], cols[:8] = [0, 899, 0, 899, 251, 648, 450, 0], [0, 999, 999, 0, 251, 748, 0, 500]
+    _vs_compare(engine, z, 250, 50, 50, rows, cols)
 
 
 @pytest.mark.parametrize("roi,h", [(200, 20), (250, 50), (1, 0), (3, 5), (300, 10), (100, 10)])
