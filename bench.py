@@ -25,6 +25,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "end-to-end siting sec; VIEWSHED LOS samples/s; SITE GB/s vs HBM roofline"
+DTYPE = "int32 exact LOS walks + fp64 tie re-test (SPEC.md:147 decisions); int16 terrain; u64 bitmaps"
+DATA = "synthetic (seeded diamond-square terrain, BASELINE shapes)"
 
 
 def parse():
@@ -32,7 +34,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c3", help="BASELINE config c1..c5 (default c3: the largest "
+                    "single-GPU full pipeline)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--site-mode", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -47,72 +50,124 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------
-# CPU oracle leg (cpu_baseline and --impl reference): bounded sample,
-# linearly extrapolated to the full configuration.
+# CPU oracle leg (cpu_baseline and --impl reference).  Nothing here loads the
+# engine library: paper_2006_16783_b200.configs is pure Python (the package
+# resolves its engine names lazily).
 # ---------------------------------------------------------------------------
+# Per-config sample plan: VIX on every `vix_stride`-th row (offset rotating per
+# step), VIEWSHED on every `vs_stride`-th candidate (rotating), FINDMAX in full,
+# SITE in full (lazy greedy over every candidate's viewshed) except at C5,
+# where 1M R=250 viewsheds cannot be built on the host in minutes: there SITE
+# runs on the candidates of the top-left 1/16 sub-square with 1/16 of the picks.
+SAMPLE_PLAN = {"c1": (1, 1, True), "c2": (16, 16, True), "c3": (512, 64, True), "c4": (2048, 64, True),
+               "c5": (0, 1024, False)}
+
+
+def config_dict(cfg):
+    """The workload description both arms print (identical dicts)."""
+    return {"workload": cfg.name, "nrows": cfg.nrows, "ncols": cfg.ncols, "roi": cfg.roi, "height": cfg.height,
+            "vix_samples": cfg.samples, "block": cfg.block, "per_block": cfg.per_block,
+            "random_observers": cfg.random_observers, "max_selected": cfg.max_selected,
+            "target_coverage": cfg.target, "los_arith": "fp64 (SPEC.md:147)",
+            "l2": "flushed between steps (256 MB write outside the timed events)"}
+
+
 class CpuReference:
-    def __init__(self, cfg, threads):
+    """The oracle port (oracle/, std::thread workers like parallel.hpp) timed on
+    this host on a bounded sample of the configuration, extrapolated per stage:
+    est = VIX_sample * nrows / rows_sampled + FINDMAX + VIEWSHED_sample * n /
+    sampled + SITE (full).  `cand` / `views`: the GPU's candidate list and
+    downloaded viewsheds (cpu_baseline leg: the host work is then checked
+    against the GPU's); without them (reference arm) candidates come from a
+    seeded synthetic VixMap and the host builds every viewshed once at setup."""
+
+    def __init__(self, cfg, threads, cand=None, views=None):
         sys.path.insert(0, os.path.join(ROOT, "tests"))
         import numpy as np
         import oracle_lib as O
         self.O, self.np, self.cfg = O, np, cfg
         self.threads = threads or (os.cpu_count() or 1)
         c = cfg
+        t0 = time.perf_counter()
         self.z = O.generate_fractal(c.nrows, c.ncols, c.roughness, c.terrain_seed, c.zmin, c.zmax, self.threads)
         if c.water_rows:
             self.z[:c.water_rows] = 0
+        self.vix_stride, self.vs_stride, self.site_full = SAMPLE_PLAN.get(c.name[:2], (64, 64, True))
         rng = np.random.default_rng(c.terrain_seed)
-        budget = 1.5e7 * self.threads        # LOS crossings per sampled component (~0.3-1 s)
         if c.samples:
-            per_row = c.ncols * c.samples * 0.81 * c.roi
-            self.vix_rows = int(max(1, min(c.nrows, round(budget / per_row))))
+            # FINDMAX input for timing: a seeded synthetic VixMap (score levels 0..S)
             self.scores = rng.integers(0, c.samples + 1, (c.nrows, c.ncols)).astype(np.uint8)
+        if cand is not None:
+            self.cr, self.cc = cand
+        elif c.samples:
             self.cr, self.cc, _ = O.find_candidates(self.scores, c.block, c.per_block)
         else:
-            self.vix_rows = 0
             self.cr, self.cc = O.random_observers(c.nrows, c.ncols, c.random_observers, c.observer_seed)
         self.ncand = len(self.cr)
-        self.vs_n = int(max(8, min(self.ncand, round(budget / (7.0 * c.roi * c.roi)))))
-        # SITE: lazy greedy on the candidates of the top-left 1/16 sub-square
-        sub = (self.cr < c.nrows // 4) & (self.cc < c.ncols // 4)
-        self.sr, self.sc = self.cr[sub], self.cc[sub]
-        self.sw, self.sv = O.viewsheds(self.z, c.roi, c.height, c.height, self.sr, self.sc, self.threads)
-        self.sub_sel = max(1, c.max_selected // 16)
+        if self.site_full:
+            self.site_idx = np.arange(self.ncand)
+            self.site_sel = c.max_selected
+        else:
+            self.site_idx = np.nonzero((self.cr < c.nrows // 4) & (self.cc < c.ncols // 4))[0]
+            self.site_sel = max(1, c.max_selected // 16)
+        if views is not None and self.site_full:
+            self.sw, self.sv = views
+        else:
+            self.sw, self.sv = O.viewsheds(self.z, c.roi, c.height, c.height, self.cr[self.site_idx],
+                                           self.cc[self.site_idx], self.threads)
+        self.setup_s = time.perf_counter() - t0
+        self.full = self.vix_stride <= 1 and self.vs_stride == 1 and self.site_full
         self.k = 0
+        self.last = {}
 
     def step(self):
+        """One sampled step: (estimated full-configuration seconds, per-stage
+        estimates, measured wall seconds of the step)."""
         O, np, c = self.O, self.np, self.cfg
-        parts = {}
+        parts, out = {}, {}
+        w0 = time.perf_counter()
         if c.samples:
-            rb = (self.k * 977) % max(1, c.nrows - self.vix_rows)
+            rows = np.arange((self.k * 7919) % self.vix_stride, c.nrows, self.vix_stride)
             t0 = time.perf_counter()
-            O.estimate_vix(self.z, c.roi, c.height, c.height, c.samples, c.vix_seed, self.threads,
-                           rows=(rb, rb + self.vix_rows))
-            parts["vix"] = (time.perf_counter() - t0) * c.nrows / self.vix_rows
+            out["vix_rows"], out["vix"] = rows, O.estimate_vix_rows(self.z, c.roi, c.height, c.height, c.samples,
+                                                                     c.vix_seed, rows, self.threads)
+            parts["vix"] = (time.perf_counter() - t0) * c.nrows / len(rows)
             t0 = time.perf_counter()
             O.find_candidates(self.scores, c.block, c.per_block)
             parts["findmax"] = time.perf_counter() - t0
-        idx = np.linspace(0, self.ncand - 1, self.vs_n).astype(np.int64)
-        idx = (idx + self.k) % self.ncand
+        # runs of 64 consecutive candidates (block-order neighbours share terrain in the host caches, as in
+        # the full run), every vs_stride-th run
+        runs = np.arange((self.k * 104729) % self.vs_stride, -(-self.ncand // 64), self.vs_stride)
+        idx = (runs[:, None] * 64 + np.arange(64)[None, :]).ravel()
+        idx = idx[idx < self.ncand]
         t0 = time.perf_counter()
-        O.viewsheds(self.z, c.roi, c.height, c.height, self.cr[idx], self.cc[idx], self.threads)
-        parts["viewshed"] = (time.perf_counter() - t0) * self.ncand / self.vs_n
+        out["vs_idx"] = idx
+        out["vs_wins"], out["vs_words"] = O.viewsheds(self.z, c.roi, c.height, c.height, self.cr[idx], self.cc[idx],
+                                                      self.threads)
+        parts["viewshed"] = (time.perf_counter() - t0) * self.ncand / len(idx)
         t0 = time.perf_counter()
-        O.site(self.sr, self.sc, self.sw, self.sv, c.nrows, c.ncols, c.target, self.sub_sel)
-        parts["site"] = (time.perf_counter() - t0) * 16
+        out["site"] = O.site(self.cr[self.site_idx], self.cc[self.site_idx], self.sw, self.sv, c.nrows, c.ncols,
+                             c.target, self.site_sel)
+        parts["site"] = (time.perf_counter() - t0) * (1 if self.site_full else 16)
         self.k += 1
-        return sum(parts.values()), parts
+        self.last = out
+        return sum(parts.values()), parts, time.perf_counter() - w0
 
     def sample_desc(self):
         c = self.cfg
         s = []
         if c.samples:
-            s.append(f"VIX on {self.vix_rows}/{c.nrows} rows (x{c.nrows / self.vix_rows:.0f})")
-            s.append("FINDMAX full (synthetic VixMap)")
-        s.append(f"VIEWSHED on {self.vs_n}/{self.ncand} observers (x{self.ncand / self.vs_n:.1f})")
-        s.append(f"SITE lazy greedy on the {len(self.sr)} observers of the top-left 1/16 sub-square, "
-                 f"{self.sub_sel} picks (x16)")
-        return "; ".join(s) + "; extrapolated linearly to the full configuration"
+            s.append("VIX on every %d-th row (%d of %d rows, x%d)" % (self.vix_stride, -(-c.nrows // self.vix_stride),
+                                                                      c.nrows, self.vix_stride)
+                     if self.vix_stride > 1 else "VIX in full")
+            s.append("FINDMAX in full (seeded synthetic VixMap)")
+        s.append("VIEWSHED on every %d-th run of 64 consecutive of %d observers (x%d)" % (self.vs_stride, self.ncand,
+                                                                                        self.vs_stride)
+                 if self.vs_stride > 1 else f"VIEWSHED in full ({self.ncand} observers)")
+        s.append(f"SITE lazy greedy in full ({self.ncand} candidates, {self.site_sel} picks max)" if self.site_full
+                 else f"SITE lazy greedy on the {len(self.site_idx)} candidates of the top-left 1/16 sub-square, "
+                      f"{self.site_sel} picks (x16)")
+        return "; ".join(s) + "; per-stage linear extrapolation to the full configuration"
 
 
 def run_reference(args, cfg):
@@ -122,20 +177,28 @@ def run_reference(args, cfg):
     ref = CpuReference(cfg, args.threads)
     for _ in range(args.warmup):
         ref.step()
-    vals = []
+    vals, walls, parts_all = [], [], []
     for _ in range(args.steps):
-        v, parts = ref.step()
+        v, parts, wall = ref.step()
         vals.append(v)
+        walls.append(wall)
+        parts_all.append(parts)
     value = statistics.mean(vals)
+    stages = {k: round(statistics.mean(p[k] for p in parts_all), 4) for k in parts_all[0]}
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(value * 1e3, 2), "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int32 (exact integer LOS arithmetic)", "data": "synthetic",
-        "config": {"workload": cfg.name, "nrows": cfg.nrows, "ncols": cfg.ncols, "roi": cfg.roi},
+        "ms_per_step": round(statistics.mean(walls) * 1e3, 2), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp64 (SPEC.md:147 LOS arithmetic, oracle port)", "data": DATA,
+        "config": config_dict(cfg),
         "cpu_baseline": {"value": round(value, 4), "unit": "s", "cores": ref.threads, "kind": "port",
                          "sample": ref.sample_desc()},
-        "stages_s": {k: round(v, 4) for k, v in parts.items()},
+        "estimated": {"what": ("value = the measured full-configuration step (every stage in full)" if ref.full else
+                               "value = full-configuration seconds estimated from each step's sample "
+                               "(per-stage linear extrapolation); ms_per_step = the measured wall time of a "
+                               "sampled step"), "extrapolated": not ref.full, "steps_s": [round(v, 3) for v in vals],
+                      "stdev_s": round(statistics.pstdev(vals), 3), "setup_s": round(ref.setup_s, 1)},
+        "stages_s": stages,
         "e2e": {"value": round(value, 4), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -205,76 +268,100 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def load_peaks():
+def _load_json(*path):
     try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
-    except (OSError, KeyError, ValueError):
-        return 6650.0, "fallback"
-
-
-def load_traffic(kernel):
-    """dram bytes per launch from the committed ncu --set full summary, if any."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f).get(kernel)
+        with open(os.path.join(ROOT, *path)) as f:
+            return json.load(f)
     except (OSError, ValueError):
-        return None
+        return {}
 
 
-def stage_figures(st, K, cfg, site_mode, l2_gbs=None):
-    """Per-stage device times and algorithmic throughputs from the engine's
-    stats over K steps, and the roofline of the dominant stage's kernel.
-    l2_gbs: measured L2-resident read bandwidth, the peak SURVEY 8(d) sets the
-    VIX / VIEWSHED LOS-sample figures against (reported beside the HBM one)."""
-    peak, peak_kind = load_peaks()
+def load_peaks():
+    """HBM copy peak (MEASURED_PEAKS.json, driver-written; else the profiling
+    recipe's fallback), the L2-resident read peak (profiles/l2_peak.json, a
+    committed measurement -- fixed, not re-measured per run) and the warp
+    instruction issue peak: 148 SMs x 4 schedulers x 1 warp-instruction/clk at
+    the max SM clock."""
+    d = _load_json("MEASURED_PEAKS.json")
+    hbm = (float(d["hbm_gbs"]), "measured") if "hbm_gbs" in d else (6650.0, "fallback (B200_PROFILING.md)")
+    mhz = float(d.get("sm_max_mhz", 1965.0))
+    l2 = _load_json("profiles", "l2_peak.json")
+    return {"hbm": hbm, "l2": (float(l2["gbs"]), l2.get("source", "profiles/l2_peak.json")) if "gbs" in l2 else (None, None),
+            "issue": (148 * 4 * mhz * 1e6 / 1e9, f"148 SMs x 4 SMSPs x 1 warp-inst/clk x {mhz:.0f} MHz")}
+
+
+def kernel_counts(cfg, kernel):
+    """Per-launch ncu counters of `kernel` at this config (profiles/kernel_counts.json,
+    from profiles/scripts/kernel_counts.sh: same config, same seeds, so the same
+    data-dependent work as the live run)."""
+    return _load_json("profiles", "kernel_counts.json").get(cfg.name[:2], {}).get(kernel)
+
+
+def los_roof(name, kernel, kernel_ms, units, cfg, peaks):
+    """VIX / VIEWSHED: issue-bound LOS walks.  achieved = ncu warp
+    instructions per launch / the live kernel time; l2 = L2 bytes the kernel
+    actually read (ncu) / live time against the committed L2 read peak; los =
+    SURVEY §8(d)'s algorithmic LOS samples (every crossing, no early exit)."""
+    r = {"stage": name, "kernel": kernel, "kernel_ms": round(kernel_ms, 3), "bound": "issue",
+         "unit": "Gwarp-inst/s", "peak": round(peaks["issue"][0], 1), "peak_kind": peaks["issue"][1],
+         "los": {"samples_per_launch": int(units),
+                 "samples_per_s": round(units / (kernel_ms / 1e3), 1) if kernel_ms else None,
+                 "algorithmic_gbs": round(4 * units / (kernel_ms / 1e3) / 1e9, 1) if kernel_ms else None}}
+    k = kernel_counts(cfg, kernel)
+    if k and kernel_ms:
+        r["achieved"] = round(k["inst"] / (kernel_ms / 1e3) / 1e9, 1)
+        r["frac"] = round(r["achieved"] / r["peak"], 4)
+        r["inst_per_launch"] = int(k["inst"])
+        r["inst_per_los_sample"] = round(k["inst"] / units, 3) if units else None
+        r["traffic"] = int(k["dram_bytes"])
+        l2p = peaks["l2"][0]
+        r["l2"] = {"read_bytes_per_launch": int(k["l2_read_bytes"]),
+                   "achieved_gbs": round(k["l2_read_bytes"] / (kernel_ms / 1e3) / 1e9, 1),
+                   "peak_gbs": l2p, "frac": round(k["l2_read_bytes"] / (kernel_ms / 1e3) / 1e9 / l2p, 4) if l2p else None}
+        r["ncu_issue_active_pct"] = k.get("issue_active_pct")
+    else:
+        r["achieved"] = r["frac"] = r["traffic"] = None
+    return r
+
+
+def stage_figures(st, K, cfg, site_mode, site_stream=None):
+    """Per-stage device times and work figures from the engine's stats over K
+    steps, and the roofline of the dominant stage's kernel."""
+    peaks = load_peaks()
     stages = {}
     if cfg.samples:
-        vix_ms = st["ms_vix"] / K
-        units = st["vix_crossings_full"] / K
-        stages["vix"] = {"ms": round(vix_ms, 3), "los_crossings": int(units),
-                         "los_samples_per_s": units / (vix_ms / 1e3) if vix_ms else None,
-                         "kernel": "k_vix_quads" if cfg.roi <= 255 else "k_vix", "bytes_per_launch": 4 * units}
-        fm_ms = st["ms_findmax"] / K
-        stages["findmax"] = {"ms": round(fm_ms, 3), "kernel": "k_findmax", "bytes_per_launch": 2 * cfg.posts}
-    vs_ms = st["ms_viewshed"] / K
-    vunits = st["viewshed_crossings"] / K
-    stages["viewshed"] = {"ms": round(vs_ms, 3), "los_crossings": int(vunits),
-                          "los_samples_per_s": vunits / (vs_ms / 1e3) if vs_ms else None,
-                          "kernel": "k_viewshed_evk" if cfg.roi <= 250 else "k_viewshed",
-                          "bytes_per_launch": 4 * vunits}
+        kern = "k_vix_quads" if cfg.roi <= 255 else "k_vix"
+        stages["vix"] = {"ms": round(st["ms_vix"] / K, 3),
+                         **los_roof("vix", kern, st["ms_vix_kernel"] / K, st["vix_crossings_full"] / K, cfg, peaks)}
+        stages["findmax"] = {"ms": round(st["ms_findmax"] / K, 3), "kernel": "k_findmax"}
+    kern = "k_viewshed_evk" if cfg.roi <= 250 else "k_viewshed"
+    stages["viewshed"] = {"ms": round(st["ms_viewshed"] / K, 3),
+                          **los_roof("viewshed", kern, st["ms_viewshed_kernel"] / K, st["viewshed_crossings"] / K,
+                                     cfg, peaks)}
     site_ms = st["ms_site"] / K
-    sbytes = st["site_bytes"] / K
     stages["site"] = {"ms": round(site_ms, 3), "iterations": int(st["site_iterations"] // K),
-                      "site_gbs": sbytes / (site_ms / 1e3) / 1e9 if site_ms else None,
-                      "kernel": "k_site_loop/k_update" if site_mode == 0 else "k_gain_full",
-                      "bytes_per_launch": sbytes, "mode": "incremental" if site_mode == 0 else "full-rescan"}
-    for s_ in stages.values():
-        s_["achieved_gbs"] = round(s_["bytes_per_launch"] / (s_["ms"] / 1e3) / 1e9, 2) if s_["ms"] else None
-    dom = max(stages, key=lambda k: stages[k]["ms"])
-    ach = stages[dom]["achieved_gbs"] or 0.0
-    roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
-                "traffic": load_traffic(stages[dom]["kernel"]), "kernel": stages[dom]["kernel"], "stage": dom,
-                "peak_kind": peak_kind,
-                "bytes_model": "VIX/VIEWSHED: 4 B (two int16 posts) per grid-line crossing, no early exit; "
-                               "SITE: packed viewshed bytes streamed; FINDMAX: VixMap read twice"}
-    if l2_gbs:
-        for k in ("vix", "viewshed"):
-            if k in stages and stages[k].get("achieved_gbs"):
-                stages[k]["l2_peak_gbs"] = round(l2_gbs, 1)
-                stages[k]["frac_of_l2"] = round(stages[k]["achieved_gbs"] / l2_gbs, 4)
-        if dom in ("vix", "viewshed"):
-            roofline["l2_peak_gbs"] = round(l2_gbs, 1)
-            roofline["frac_of_l2"] = round(ach / l2_gbs, 4)
-    if dom == "vix":
-        roofline["note"] = ("algorithmic LOS-sample bytes (SURVEY 8(d)); the VIX skip map proves most crossings "
-                            "unblockable without reading them, so DRAM traffic per launch (traffic) is ~1 % of them and "
-                            "frac can exceed 1: the kernel is issue-bound, not HBM-bound (DESIGN.md 3, 5)")
-    elif dom == "viewshed":
-        roofline["note"] = ("algorithmic LOS-sample bytes (SURVEY 8(d)), served from L1/L2; the R2 sweep is "
-                            "ALU-bound (DESIGN.md 3)")
-    return stages, roofline, peak
+                      "kernel": "k_site_loop / k_argmax+k_commit+k_update" if site_mode == 0 else "k_gain_full",
+                      "mode": "exact incremental" if site_mode == 0 else "full-rescan"}
+    if site_stream:
+        hbm = peaks["hbm"][0]
+        site_stream["frac_of_hbm"] = round(site_stream["gbs"] / hbm, 4) if site_stream.get("gbs") else None
+        site_stream["kernel_frac_of_hbm"] = (round(site_stream["kernel_gbs"] / hbm, 4)
+                                             if site_stream.get("kernel_gbs") else None)
+        k = kernel_counts(cfg, site_stream["kernel"])
+        site_stream["traffic"] = int(k["dram_bytes"]) if k else None
+        stages["site_stream"] = site_stream
+    dom = max(("vix", "viewshed", "site"), key=lambda x: stages.get(x, {}).get("ms", -1))
+    if dom in ("vix", "viewshed"):
+        roofline = {k: v for k, v in stages[dom].items() if k != "ms"}
+    else:   # SITE: the streaming gain pass against HBM
+        ss = stages.get("site_stream", {})
+        roofline = {"stage": "site", "kernel": ss.get("kernel"), "bound": "hbm", "unit": "GB/s",
+                    "achieved": ss.get("kernel_gbs"), "peak": peaks["hbm"][0], "peak_kind": peaks["hbm"][1],
+                    "frac": ss.get("kernel_frac_of_hbm"), "traffic": ss.get("traffic")}
+    roofline["note"] = ("VIX/VIEWSHED are issue-bound exact LOS walks (DESIGN.md §3, §5): the roof is warp-instruction "
+                        "issue; l2 = bytes the kernel actually read against the committed L2 read peak; SITE's "
+                        "streaming gain pass is the HBM-bound kernel (stages.site_stream)")
+    return stages, roofline, peaks
 
 
 def run_b200(args, cfg):
@@ -388,37 +475,70 @@ def run_b200(args, cfg):
 
     # ---- per-stage figures and the roofline of the dominant kernel -------
     K = args.steps
-    stages, roofline, peak = stage_figures(st, K, cfg, args.site_mode, l2_gbs=eng.measure_l2())
-    site_stream["frac_of_hbm"] = round(site_stream["gbs"] / peak, 4) if site_stream["gbs"] else None
-    site_stream["kernel_frac_of_hbm"] = round(site_stream["kernel_gbs"] / peak, 4) if site_stream["kernel_gbs"] else None
-    stages["site_stream"] = site_stream
+    stages, roofline, peaks = stage_figures(st, K, cfg, args.site_mode, site_stream)
     line = {
         "metric": METRIC, "value": round(ms / 1e3, 5), "unit": "s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int32 (exact integer LOS arithmetic)",
-        "data": "synthetic (seeded diamond-square terrain, BASELINE shapes)",
-        "config": {"workload": cfg.name, "nrows": cfg.nrows, "ncols": cfg.ncols, "roi": cfg.roi,
-                   "height": cfg.height, "vix_samples": cfg.samples, "block": cfg.block, "per_block": cfg.per_block,
-                   "max_selected": cfg.max_selected, "candidates": st["candidates"],
-                   "sited": int(len(res["index"])), "stop": res["stop"],
-                   "parallelism": f"replicas{world}" if world > 1 else "single-gpu",
-                   "l2": "flushed between steps (256 MB write outside the timed events)"},
+        "vs_baseline": None, "dtype": DTYPE, "data": DATA, "config": config_dict(cfg),
+        "result": {"candidates": st["candidates"], "sited": int(len(res["index"])), "stop": res["stop"],
+                   "coverage": float(res["coverage"][-1]) if len(res["coverage"]) else 0.0,
+                   "parallelism": f"replicas{world}" if world > 1 else "single-gpu"},
         "stages": stages,
         "roofline": roofline,
         "e2e": {"value": round(e2e / 1e3, 5), "unit": "s", "h2d_bytes_per_step": cfg.posts * 2,
                 "d2h_bytes_per_step": d2h, "kernel_launches_per_step": launches_e2e,
                 "steps_ms": [round(x, 3) for x in e2e_ms], "statistic": "median"},
         "gpu_launches": st["kernel_launches"],
+        "fp64_ties": {"vix_segments_retested": st["vix_fp64_ties"] // K, "vix_decisions_changed": st["vix_fp64_flips"] // K,
+                      "viewshed_rays_retested": st["vs_fp64_ties"] // K, "viewshed_bits_changed": st["vs_fp64_flips"] // K},
         "clocks": clk,
     }
     if world == 1 and not args.no_cpu_baseline:
-        ref = CpuReference(cfg, args.threads)
-        v, parts = ref.step()
-        line["cpu_baseline"] = {"value": round(v, 3), "unit": "s", "cores": ref.threads, "kind": "port",
-                                "sample": ref.sample_desc(), "stages_s": {k: round(x, 3) for k, x in parts.items()}}
+        line["cpu_baseline"], line["differing_bits"] = cpu_baseline_leg(args, cfg, eng, res)
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def cpu_baseline_leg(args, cfg, eng, res):
+    """The oracle on this host on the bounded sample (rank 0, N = 1), fed with
+    the GPU's candidate list and viewsheds; its sample outputs double as a live
+    parity check of the timed run: differing VixMap scores on the sampled rows,
+    differing bits of the sampled viewsheds, and the oracle's SITE sequence /
+    cumulative bitmap against the GPU's."""
+    import numpy as np
+    rows, cols, _ = eng.candidates()
+    plan = SAMPLE_PLAN.get(cfg.name[:2], (64, 64, True))
+    views = eng.viewsheds(cfg.roi)[:2] if plan[2] else None
+    ref = CpuReference(cfg, args.threads, cand=(rows, cols), views=views)
+    v, parts, wall = ref.step()
+    out = ref.last
+    diff = {}
+    if cfg.samples:
+        g = np.concatenate([eng.vix(int(r), int(r) + 1) for r in out["vix_rows"]])
+        diff["vix"] = {"rows_compared": int(len(out["vix_rows"])), "posts_compared": int(g.size),
+                       "scores_differing": int((g != out["vix"]).sum())}
+    idx = out["vs_idx"]
+    if views is not None:
+        gw, gv = views[0][idx], views[1][idx]
+    else:
+        got = [eng.viewsheds(cfg.roi, first=int(i), count=1)[:2] for i in idx]
+        gw, gv = np.concatenate([x[0] for x in got]), np.concatenate([x[1] for x in got])
+    area = int((out["vs_wins"][:, 2].astype(np.int64) * out["vs_wins"][:, 3]).sum())
+    diff["viewshed"] = {"viewsheds_compared": int(len(idx)), "bits_compared": area,
+                        "windows_differing": int((gw != out["vs_wins"]).any(1).sum()),
+                        "bits_differing": int(np.bitwise_count(gv ^ out["vs_words"]).sum())}
+    o = out["site"]
+    if plan[2]:
+        same = (o["stop"] == res["stop"] and len(o["index"]) == len(res["index"])
+                and bool(np.array_equal(o["index"], res["index"])) and bool(np.array_equal(o["gain"], res["gain"])))
+        diff["site"] = {"picks_compared": int(len(res["index"])), "sequence_identical": same,
+                        "cum_bits_differing": int(np.bitwise_count(eng.cumulative() ^ o["cum"]).sum())}
+    diff["reference"] = ("the cpu_baseline sample's own oracle outputs (SPEC.md:147 fp64 formula, oracle pinned to the "
+                         "reference walk_crossings) against this run's GPU results")
+    cpu = {"value": round(v, 3), "unit": "s", "cores": ref.threads, "kind": "port", "sample": ref.sample_desc(),
+           "measured_wall_s": round(wall, 3), "stages_s": {k: round(x, 3) for k, x in parts.items()}}
+    return cpu, diff
 
 
 def run_b200_sharded(args, cfg):
@@ -486,14 +606,16 @@ def run_b200_sharded(args, cfg):
     st = eng.stats()
     # stage times: max over ranks; work units: summed over the bands
     tm = torch.tensor([st["ms_vix"], st["ms_findmax"], st["ms_viewshed"], st["ms_site"] + site_ms,
-                       st["site_iterations"] + args.steps * len(res["index"])], device=dev, dtype=torch.float64)
+                       st["site_iterations"] + args.steps * len(res["index"]), st["ms_vix_kernel"],
+                       st["ms_viewshed_kernel"]], device=dev, dtype=torch.float64)
     dist.all_reduce(tm, op=dist.ReduceOp.MAX)
     tc = torch.tensor([st["vix_crossings_full"], st["viewshed_crossings"], st["site_bytes"]], device=dev,
                       dtype=torch.float64)
     dist.all_reduce(tc, op=dist.ReduceOp.SUM)
     agg = dict(st)
     agg.update(ms_vix=tm[0].item(), ms_findmax=tm[1].item(), ms_viewshed=tm[2].item(), ms_site=tm[3].item(),
-               site_iterations=int(tm[4].item()), vix_crossings_full=tc[0].item(), viewshed_crossings=tc[1].item(),
+               site_iterations=int(tm[4].item()), ms_vix_kernel=tm[5].item(), ms_viewshed_kernel=tm[6].item(),
+               vix_crossings_full=tc[0].item(), viewshed_crossings=tc[1].item(),
                site_bytes=tc[2].item())
     t = torch.tensor([sum(step_ms) / args.steps], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -515,17 +637,14 @@ def run_b200_sharded(args, cfg):
     launches = torch.tensor([st["kernel_launches"]], device=dev, dtype=torch.int64)
     dist.all_reduce(launches, op=dist.ReduceOp.SUM)
     if rank == 0:
-        stages, roofline, _ = stage_figures(agg, args.steps, cfg, args.site_mode, l2_gbs=eng.measure_l2())
+        stages, roofline, _ = stage_figures(agg, args.steps, cfg, args.site_mode)
         line = {
             "metric": METRIC, "value": round(ms / 1e3, 5), "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "int32 (exact integer LOS arithmetic)",
-            "data": "synthetic (seeded diamond-square terrain, BASELINE shapes)",
-            "config": {"workload": cfg.name, "nrows": cfg.nrows, "ncols": cfg.ncols, "roi": cfg.roi,
-                       "sited": int(len(res["index"])), "stop": res["stop"],
+            "vs_baseline": None, "dtype": DTYPE, "data": DATA, "config": config_dict(cfg),
+            "result": {"sited": int(len(res["index"])), "stop": res["stop"],
                        "parallelism": f"rowband{world} (halo roi+1; SITE rounds device-resident, "
-                                      f"stream-ordered NCCL: {res.get('exchange')}, {res.get('rounds_mode')})",
-                       "l2": "flushed between steps (256 MB write outside the timed events)"},
+                                      f"stream-ordered NCCL: {res.get('exchange')}, {res.get('rounds_mode')})"},
             "e2e": {"value": round(e2e / 1e3, 5), "unit": "s", "h2d_bytes_per_step": cfg.posts * 2,
                     "d2h_bytes_per_step": ((cfg.posts + 63) // 64) * 8 + len(r2["index"]) * 32},
             "gpu_launches": int(launches.item()),

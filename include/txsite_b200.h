@@ -143,6 +143,8 @@ txs_status txs_is_visible_batch(txs_ctx* ctx, const int32_t* pairs, int64_t n, i
 /* ---- vix module (SPEC.md:176 estimate_vix) ------------------------------------ */
 txs_status txs_estimate_vix(txs_ctx* ctx, const txs_params* p, uint8_t* scores_out);
 txs_status txs_set_vix(txs_ctx* ctx, const uint8_t* scores);  /* inject a VixMap */
+/* copy rows [row_begin, row_end) of the resident VixMap (band rows when sharded) */
+txs_status txs_get_vix(txs_ctx* ctx, int64_t row_begin, int64_t row_end, uint8_t* scores_out);
 
 /* ---- candidates module (SPEC.md:228 partition, :238 find_candidates) ------- */
 txs_status txs_partition(int64_t nrows, int64_t ncols, int32_t roi, int32_t block_width,

@@ -157,29 +157,40 @@ bool is_visible(const Grid& g, int64_t tr, int64_t tc, int64_t ht,
 // SplitMix64(mix_seed(seed,row,col)); per sample draw dr then dc with
 // next_below(2R+1)-R, reject outside the lattice disk or the grid; self allowed.
 // ---------------------------------------------------------------------------
+// The VixMap score of one post (D6 draw order).
+static uint8_t vix_score(const Grid& g, int64_t roi, int64_t ht, int64_t hr, int64_t samples, uint64_t seed,
+                         int64_t r, int64_t c, int arith) {
+    const uint64_t span = (uint64_t)(2 * roi + 1);
+    const int64_t R2 = roi * roi;
+    SplitMix64 s(mix_seed(seed, (uint64_t)r, (uint64_t)c));
+    int64_t vis = 0;
+    for (int64_t k = 0; k < samples; ++k) {
+        int64_t dr, dc;
+        for (;;) {
+            dr = (int64_t)s.next_below(span) - roi;
+            dc = (int64_t)s.next_below(span) - roi;
+            if (dr * dr + dc * dc <= R2 && g.in(r + dr, c + dc)) break;
+        }
+        vis += is_visible_arith(g, r, c, ht, r + dr, c + dc, hr, arith) ? 1 : 0;
+    }
+    return (uint8_t)vis;
+}
+
 void estimate_vix(const Grid& g, int64_t roi, int64_t ht, int64_t hr, int64_t samples,
                   uint64_t seed, unsigned threads, uint8_t* scores,
                   int64_t row_begin, int64_t row_end, int arith) {
     const int64_t rows = row_end - row_begin;
-    const uint64_t span = (uint64_t)(2 * roi + 1);
-    const int64_t R2 = roi * roi;
     parallel_chunks(rows * g.ncols, threads, [&](int64_t b, int64_t e) {
         for (int64_t idx = b; idx < e; ++idx) {
             const int64_t r = row_begin + idx / g.ncols, c = idx % g.ncols;
-            SplitMix64 s(mix_seed(seed, (uint64_t)r, (uint64_t)c));
-            int64_t vis = 0;
-            for (int64_t k = 0; k < samples; ++k) {
-                int64_t dr, dc;
-                for (;;) {
-                    dr = (int64_t)s.next_below(span) - roi;
-                    dc = (int64_t)s.next_below(span) - roi;
-                    if (dr * dr + dc * dc <= R2 && g.in(r + dr, c + dc)) break;
-                }
-                vis += is_visible_arith(g, r, c, ht, r + dr, c + dc, hr, arith) ? 1 : 0;
-            }
-            scores[r * g.ncols + c] = (uint8_t)vis;
+            scores[r * g.ncols + c] = vix_score(g, roi, ht, hr, samples, seed, r, c, arith);
         }
     });
+}
+
+void estimate_vix_cols(const Grid& g, int64_t roi, int64_t ht, int64_t hr, int64_t samples, uint64_t seed,
+                       int64_t r, int64_t c0, int64_t c1, uint8_t* row_out, int arith) {
+    for (int64_t c = c0; c < c1; ++c) row_out[c] = vix_score(g, roi, ht, hr, samples, seed, r, c, arith);
 }
 
 // ---------------------------------------------------------------------------

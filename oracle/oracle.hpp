@@ -126,6 +126,9 @@ bool is_visible_arith(const Grid& g, int64_t tr, int64_t tc, int64_t ht,
 void estimate_vix(const Grid& g, int64_t roi, int64_t ht, int64_t hr, int64_t samples,
                   uint64_t seed, unsigned threads, uint8_t* scores,
                   int64_t row_begin, int64_t row_end, int arith = ArithFp64);
+// columns [c0, c1) of row r, written to row_out[c] (single-threaded)
+void estimate_vix_cols(const Grid& g, int64_t roi, int64_t ht, int64_t hr, int64_t samples, uint64_t seed,
+                       int64_t r, int64_t c0, int64_t c1, uint8_t* row_out, int arith = ArithFp64);
 
 // ---- candidates, decision D7 -----------------------------
 struct Cand { int32_t row, col, score; };

@@ -116,17 +116,19 @@ void txo_estimate_vix(const int16_t* z, int64_t nrows, int64_t ncols, int64_t ro
     estimate_vix(g, roi, ht, hr, samples, seed, threads, scores, row_begin, row_end, arith);
 }
 
-// estimate_vix on an arbitrary set of rows: out is len(rows) x ncols
+// estimate_vix on an arbitrary set of rows: out is len(rows) x ncols.  Work is
+// split over posts (not rows) so a few expensive rows do not serialise.
 void txo_estimate_vix_rows(const int16_t* z, int64_t nrows, int64_t ncols, int64_t roi, int64_t ht,
                            int64_t hr, int64_t samples, uint64_t seed, unsigned threads,
                            const int64_t* rows, int64_t nsel, uint8_t* out, int arith) {
     Grid g{nrows, ncols, z};
-    par(nsel, threads, [&](int64_t b, int64_t e) {
-        std::vector<uint8_t> full;
-        for (int64_t i = b; i < e; ++i) {
-            // scores lands at row rows[i] of a virtual full map: offset the pointer
-            estimate_vix(g, roi, ht, hr, samples, seed, 1, out + i * ncols - rows[i] * ncols, rows[i], rows[i] + 1,
-                         arith);
+    const int64_t span = 1024;   // posts per work item
+    const int64_t per_row = (ncols + span - 1) / span;
+    par(nsel * per_row, threads, [&](int64_t b, int64_t e) {
+        for (int64_t it = b; it < e; ++it) {
+            // rows interleaved, so every worker's static chunk mixes all sampled rows
+            const int64_t i = it % nsel, c0 = (it / nsel) * span, c1 = std::min(ncols, c0 + span);
+            estimate_vix_cols(g, roi, ht, hr, samples, seed, rows[i], c0, c1, out + i * ncols, arith);
         }
     });
 }

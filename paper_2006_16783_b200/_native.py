@@ -82,6 +82,7 @@ _sig("txs_terrain_dims", C.c_int, [vp, C.POINTER(i64), C.POINTER(i64)])
 _sig("txs_is_visible_batch", C.c_int, [vp, vp, i64, i32, i32, i32, vp])
 _sig("txs_estimate_vix", C.c_int, [vp, C.POINTER(Params), vp])
 _sig("txs_set_vix", C.c_int, [vp, vp])
+_sig("txs_get_vix", C.c_int, [vp, i64, i64, vp])
 _sig("txs_partition", C.c_int, [i64, i64, i32, i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)])
 _sig("txs_find_candidates", C.c_int, [vp, C.POINTER(Params), C.POINTER(i64), vp, i64])
 _sig("txs_set_candidates", C.c_int, [vp, vp, i64])
@@ -119,7 +120,7 @@ _sig("txs_event_template_info", C.c_int, [i32, C.POINTER(i64), C.POINTER(i64), C
 EXPORTS = [
     "txs_abi_version", "txs_device_ok", "txs_create", "txs_destroy", "txs_last_error", "txs_get_stats",
     "txs_reset_stats", "txs_synchronize", "txs_event_record", "txs_event_elapsed", "txs_set_terrain", "txs_generate_fractal", "txs_fill_rows",
-    "txs_get_terrain", "txs_terrain_dims", "txs_is_visible_batch", "txs_estimate_vix", "txs_set_vix",
+    "txs_get_terrain", "txs_terrain_dims", "txs_is_visible_batch", "txs_estimate_vix", "txs_set_vix", "txs_get_vix",
     "txs_partition", "txs_find_candidates", "txs_set_candidates", "txs_random_observers",
     "txs_get_candidates", "txs_compute_viewsheds", "txs_get_viewsheds", "txs_set_viewsheds", "txs_site",
     "txs_get_cumulative", "txs_marginal_gains", "txs_run_pipeline", "txs_ray_template", "txs_selftest",

@@ -140,6 +140,15 @@ class Engine:
         self._chk(N.lib.txs_estimate_vix(self._h, C.byref(params), _p(out)))
         return out
 
+    def vix(self, row_begin=None, row_end=None):
+        """Rows [row_begin, row_end) of the resident VixMap (default: all)."""
+        nr, nc = self.dims
+        rb = 0 if row_begin is None else row_begin
+        re = nr if row_end is None else row_end
+        out = np.empty((re - rb, nc), np.uint8)
+        self._chk(N.lib.txs_get_vix(self._h, rb, re, _p(out)))
+        return out
+
     def set_vix(self, scores):
         scores = np.ascontiguousarray(scores, np.uint8)
         self._chk(N.lib.txs_set_vix(self._h, _p(scores)))

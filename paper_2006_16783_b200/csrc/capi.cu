@@ -366,6 +366,17 @@ txs_status txs_estimate_vix(txs_ctx* c, const txs_params* p, uint8_t* scores_out
     return TXS_OK;
 }
 
+txs_status txs_get_vix(txs_ctx* c, int64_t rb, int64_t re, uint8_t* out) {
+    if (!c || !out) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->vix_valid) return fail(c, TXS_ERR_STATE, "vix", "no VixMap (run estimate_vix first)");
+    if (rb < c->band_r0 || re > c->band_r1 || rb > re) return fail(c, TXS_ERR_INVALID_ARGUMENT, "vix", "rows outside the band");
+    cudaSetDevice(c->device);
+    TXS_CUDA(c, "vix", cudaMemcpyAsync(out, c->d_vix + (rb - c->band_r0) * c->ncols, (re - rb) * c->ncols,
+                                       cudaMemcpyDeviceToHost, c->stream));
+    TXS_CUDA(c, "vix", cudaStreamSynchronize(c->stream));
+    return TXS_OK;
+}
+
 txs_status txs_set_vix(txs_ctx* c, const uint8_t* scores) {
     if (!c || !scores) return TXS_ERR_INVALID_ARGUMENT;
     if (!c->d_z) return fail(c, TXS_ERR_STATE, "vix", "no terrain");
@@ -655,15 +666,24 @@ txs_status txs_get_cumulative(txs_ctx* c, uint64_t* out) {
 }
 
 namespace {
-// every thread reads 16-byte words with a grid stride; the xor keeps the loads live
+// every thread keeps 4 independent 16-byte loads in flight per iteration (grid
+// stride); the xor keeps the loads live
 __global__ void k_l2_read(const uint4* __restrict__ buf, int64_t n, int reps, unsigned* __restrict__ sink) {
     uint32_t acc = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int k = 0; k < reps; ++k)
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t n4 = n - 3 * stride;
+    for (int k = 0; k < reps; ++k) {
+        int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        for (; i < n4; i += 4 * stride) {
+            const uint4 a = __ldcg(buf + i), b = __ldcg(buf + i + stride), c = __ldcg(buf + i + 2 * stride),
+                        d = __ldcg(buf + i + 3 * stride);
+            acc ^= a.x ^ a.y ^ a.z ^ a.w ^ b.x ^ b.y ^ b.z ^ b.w ^ c.x ^ c.y ^ c.z ^ c.w ^ d.x ^ d.y ^ d.z ^ d.w;
+        }
+        for (; i < n; i += stride) {
             const uint4 v = __ldcg(buf + i);
             acc ^= v.x ^ v.y ^ v.z ^ v.w;
         }
+    }
     if (acc == 0x9e3779b9u) *sink = acc;
 }
 }  // namespace
@@ -677,15 +697,21 @@ txs_status txs_measure_cache_read(txs_ctx* c, int64_t bytes, int32_t reps, doubl
     const int64_t n = bytes / 16;
     const int grid = c->num_sms * 8;
     k_l2_read<<<grid, 256, 0, c->stream>>>(buf, n, 1, (unsigned*)(buf + n));   // warm the L2
-    cudaEventRecord(c->ev_r0, c->stream);
-    k_l2_read<<<grid, 256, 0, c->stream>>>(buf, n, reps, (unsigned*)(buf + n));
-    cudaEventRecord(c->ev_r1, c->stream);
-    const cudaError_t e = cudaEventSynchronize(c->ev_r1);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, c->ev_r0, c->ev_r1);
+    // best of 5 timed launches (the figure is a peak, committed in profiles/l2_peak.json)
+    float best = 0.f;
+    cudaError_t e = cudaSuccess;
+    for (int t = 0; t < 5 && e == cudaSuccess; ++t) {
+        cudaEventRecord(c->ev_r0, c->stream);
+        k_l2_read<<<grid, 256, 0, c->stream>>>(buf, n, reps, (unsigned*)(buf + n));
+        cudaEventRecord(c->ev_r1, c->stream);
+        e = cudaEventSynchronize(c->ev_r1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->ev_r0, c->ev_r1);
+        if (ms > 0.f && (best == 0.f || ms < best)) best = ms;
+    }
     cudaFree(buf);
     if (e != cudaSuccess) return cuda_fail(c, "stats", e);
-    *gbs = ms > 0.f ? (double)n * 16.0 * reps / (ms * 1e-3) / 1e9 : 0.0;
+    *gbs = best > 0.f ? (double)n * 16.0 * reps / (best * 1e-3) / 1e9 : 0.0;
     return TXS_OK;
 }
 
