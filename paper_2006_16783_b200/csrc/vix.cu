@@ -535,9 +535,24 @@ struct QuadGeom { QuadGeomC c; QuadGeomF f; };
 #define VIX_MINB 2    // CTAs per SM: 64 registers, no spills (measured: 4 / 3 / 2 / 1 -> c2 43.1 / 42.0 / 38.8 / 57.1 ms, c3 144.3 / 137.9 / 126.1 / 150.8)
 #endif
 
-__device__ __forceinline__ bool quad_test(uint2 v, int r, int nm, uint32_t wb, int rhsM, int rhsm) {
+// The larger margin z*n - (LOS numerator - 1) of a step's two crossings (the
+// dp2a accumulators take the negated numerators): d > 0 iff some crossing
+// touches or rises above the LOS (z >= LOS), d > 1 iff one is strictly above
+// it (z > LOS: blocked).  The minor-line crossing exists only for 0 < r < m.
+__device__ __forceinline__ int dp2lo_acc(uint32_t pair, uint32_t w, int acc) {
+    int d;
+    asm("dp2a.lo.s32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(pair), "r"(w), "r"(acc));
+    return d;
+}
+__device__ __forceinline__ int dp2hi_acc(uint32_t pair, uint32_t w, int acc) {
+    int d;
+    asm("dp2a.hi.s32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(pair), "r"(w), "r"(acc));
+    return d;
+}
+__device__ __forceinline__ int quad_margin(uint2 v, int r, int nm, uint32_t wb, int rhsM, int rhsm) {
     const uint32_t W = wb + (uint32_t)r * 0xFF0100FFu;   // (+255 lo, -255 hi) per unit r
-    return (dp2lo(v.x, W) > rhsM) | (((unsigned)(r - 1) < (unsigned)(nm - 1)) & (dp2hi(v.y, W) > rhsm));
+    const int dM = dp2lo_acc(v.x, W, -rhsM), dm = dp2hi_acc(v.y, W, -rhsm);
+    return ((unsigned)(r - 1) < (unsigned)(nm - 1)) ? max(dM, dm) : dM;
 }
 
 // Plane geometry shared by every walk of a launch.
@@ -550,14 +565,15 @@ struct QuadPitch {
 // quad planes (the kernels whose skip test passes almost every group -- 16-step
 // groups -- do not build the planes): posts A = P[i stepM + q sm], B = A one
 // minor step on, C = A one major step back; the predicates of quad_test.
-__device__ __forceinline__ bool terrain_test(const int16_t* P, int i, int q, int r, int nM, int nm, int sm, int stepM,
-                                             int rhsM, int rhsm) {
+__device__ __forceinline__ int terrain_margin(const int16_t* P, int i, int q, int r, int nM, int nm, int sm, int stepM,
+                                              int rhsM, int rhsm) {
     const int o = i * stepM + q * sm;
     const bool minor = (unsigned)(r - 1) < (unsigned)(nm - 1);
     const int zA = zld(P + o);
     const int zB = r ? zld(P + o + sm) : 0;
     const int zC = minor ? zld(P + o - stepM) : 0;
-    return (zA * (nM - r) + zB * r > rhsM) | (minor & (zC * r + zA * (nm - r) > rhsm));
+    const int dM = zA * (nM - r) + zB * r - rhsM;
+    return minor ? max(dM, zC * r + zA * (nm - r) - rhsm) : dM;
 }
 
 // Full walk: one segment per warp, lane l taking major steps l+1, l+33, ...;
@@ -584,10 +600,9 @@ __device__ __forceinline__ int quad_walk(const QuadGeom* gp, int lane) {
     for (int k = 0; k <= (steps >> 5); ++k) {
         const bool valid = k < (steps >> 5) || (steps & ~31) + 1 + lane <= steps;
         if (k == (steps >> 5) && !(steps & 31)) break;
-        const uint2 v = valid ? qld(f.Q + off) : make_uint2(0u, 0u);
-        const bool b = valid && quad_test(v, r, nm, wb, rhsM, rhsm);
-        if (__any_sync(kFull, b)) {   // >= hit: a block, or only ties
-            if (__any_sync(kFull, b && quad_test(v, r, nm, wb, rhsM + 1, rhsm + 1))) return kSegBlk;
+        const int d = valid ? quad_margin(qld(f.Q + off), r, nm, wb, rhsM, rhsm) : 0;
+        if (__any_sync(kFull, d > 0)) {   // z >= LOS somewhere: a block, or only ties
+            if (__any_sync(kFull, d > 1)) return kSegBlk;
             st = kSegTie;
         }
         off += dOff; rhsM += dRhsM; rhsm += dRhsm; r += r32;
@@ -643,18 +658,16 @@ __device__ __forceinline__ int quad_walk_skip(const QuadGeom* gp, const QuadPitc
         const int cnt = __popc(F);
         for (int j = 0; j < cnt; j += 32 >> GS) {   // 32/G groups x G steps per pass
             const int sub = j + (lane >> GS);
-            bool b = false, s = false;
+            int d = 0;
             if (sub < cnt) {
                 const int i = (s_fail[sub] << GS) + 1 + (lane & ((1 << GS) - 1));
                 if (i <= steps) {
                     const int q = (i * mag) >> 16, r = i * nm - q * nM;
-                    const uint2 v = qld(f.Q + i + q * sm);
-                    b = quad_test(v, r, nm, wb, LE + i * D, f.Esn + q * D);
-                    s = b && quad_test(v, r, nm, wb, LE + i * D + 1, f.Esn + q * D + 1);
+                    d = quad_margin(qld(f.Q + i + q * sm), r, nm, wb, LE + i * D, f.Esn + q * D);
                 }
             }
-            if (__any_sync(kFull, b)) {
-                if (__any_sync(kFull, s)) return kSegBlk;
+            if (__any_sync(kFull, d > 0)) {
+                if (__any_sync(kFull, d > 1)) return kSegBlk;
                 st = kSegTie;
             }
         }
@@ -739,20 +752,20 @@ __device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int la
             const int nM = c.w & 0xff;
             // 32 steps from the unit's first (a unit of U G < 32 steps is walked with its successor)
             const int i = ((U * (e >> 8)) << GS) + 1 + lane;
-            // bias 0: z >= LOS (blocks and ties), bias 1: z > LOS (blocks)
-            auto test = [&](int bias) -> bool {
-                if (i >= nM) return false;
+            int d = 0;   // margin: > 0 z >= LOS (a block or a grazing tie), > 1 z > LOS (a block)
+            if (i < nM) {
                 const int nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 15, D = c.DG >> GS;
                 const int q = (i * mag) >> 16, r = i * nm - q * nM;
-                const int rhsM = c.LE2 - min(0, c.DG) + i * D + bias, rhsm = f.Esn + q * D + bias;
-                if (TERR)
-                    return terrain_test((const int16_t*)f.Q, i, q, r, nM, nm, sm, (c.w & 0x2000) ? P.zs : 1, rhsM, rhsm);
-                const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
-                return quad_test(qld(f.Q + i + q * sm), r, nm, wb, rhsM, rhsm);
-            };
-            const bool b = test(0);
-            if (__any_sync(kFull, b)) {
-                if (__any_sync(kFull, b && test(1))) blk |= 1u << sf;
+                const int rhsM = c.LE2 - min(0, c.DG) + i * D, rhsm = f.Esn + q * D;
+                if (TERR) {
+                    d = terrain_margin((const int16_t*)f.Q, i, q, r, nM, nm, sm, (c.w & 0x2000) ? P.zs : 1, rhsM, rhsm);
+                } else {
+                    const uint32_t wb = (uint32_t)nM | ((uint32_t)nm << 24);
+                    d = quad_margin(qld(f.Q + i + q * sm), r, nm, wb, rhsM, rhsm);
+                }
+            }
+            if (__any_sync(kFull, d > 0)) {
+                if (__any_sync(kFull, d > 1)) blk |= 1u << sf;
                 else tie |= 1u << sf;
             }
         }
