@@ -126,6 +126,7 @@ void txs_destroy(txs_ctx* c) {
         cudaFree(kv.second.rays); cudaFree(kv.second.cells);
         if (kv.second.groups) cudaFree(kv.second.groups);
         if (kv.second.events) cudaFree(kv.second.events);
+        if (kv.second.events3) cudaFree(kv.second.events3);
     }
     if (c->h_state) cudaFreeHost(c->h_state);
     for (cudaEvent_t e : c->user_ev) if (e) cudaEventDestroy(e);

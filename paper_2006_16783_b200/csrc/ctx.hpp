@@ -34,13 +34,17 @@ struct RayTemplateDev {
     int32_t ngroups = 0;
     int2* groups = nullptr;      // {first event row (x32 lanes), steps}
     uint2* events = nullptr;
+    uint2* events3 = nullptr;    // the same stream in the interior-sweep encoding (raytemplate.cpp, pack_ev3)
     int64_t nevents = 0;
 };
 // host-side event stream (exposed for tests through txs_event_template)
 struct EventTemplate {
     std::vector<int2> groups;
     std::vector<uint2> events;
+    std::vector<uint2> events3;   // interior encoding (pack_ev3), same order
 };
+// interior-sweep event types (events3)
+enum Ev3Type : uint32_t { kEv3Cross = 0, kEv3Cell = 1, kEv3Nop = 2 };
 const EventTemplate& event_template(int32_t roi);
 
 // Device-side SITE loop state (one struct, read/written by the loop kernels).

@@ -16,6 +16,7 @@
 #include <map>
 #include <mutex>
 #include <numeric>
+#include <stdexcept>
 #include <tuple>
 
 #include "ctx.hpp"
@@ -124,6 +125,38 @@ inline uint2 pack_ev(uint32_t type, int dr, int dc, int w0, int w1, int64_t y) {
                       (uint32_t)y | ((uint32_t)w1 << 24));
 }
 
+// Interior-sweep encoding of the same event (k_viewshed_evk's interior
+// observers share the window pitch 2R+1, so a cell's bitmap bit is a template
+// constant):
+//   x: bits 0-1 type (kEv3Cross / kEv3Cell / kEv3Nop), 2-10 dr, 11-20 F =
+//      2*dc + (column crossing) (two's complement; the pair offset is
+//      dr*p2 + F), 21-31 aux bits 0-10;
+//   y: bits 0-24 yv, 25-31 aux bits 11-17.
+// crossing: aux = w0 | w1 << 8 (the dp2a weight word), yv = line index * L2
+//   (the horizon then keeps M' = L2*M, so cells and crossings share one
+//   product X*M' and no select); cell: aux = its bit in the interior window
+//   bitmap, (dr + R)*(2R+1) + dc + R, yv = dot.  Bounds (R <= 250): line
+//   index * L2 <= 2R^3 < 2^25, bit index < (2R+1)^2 < 2^18.
+inline uint2 pack_ev3(uint2 e, int64_t R, int64_t L2) {
+    const uint32_t t2 = e.x & 7u;
+    const int dr = ((int)(e.x << 20)) >> 23, F = ((int)(e.x << 10)) >> 22, dc = F >> 1;
+    uint32_t type, aux;
+    uint64_t yv;
+    if (t2 == kEvNop) return make_uint2(kEv3Nop, 0u);
+    if (t2 == kEvCell) {
+        type = kEv3Cell;
+        aux = (uint32_t)((dr + R) * (2 * R + 1) + dc + R);
+        yv = e.y & 0xffffffu;
+    } else {
+        type = kEv3Cross;
+        aux = (e.x >> 24) | ((e.y >> 24) << 8);
+        yv = (uint64_t)(e.y & 0xffffffu) * (uint64_t)L2;
+    }
+    if (yv >= (1u << 25) || aux >= (1u << 18)) throw std::runtime_error("event3 field overflow");
+    return make_uint2(type | ((uint32_t)(dr & 0x1ff) << 2) | ((uint32_t)(F & 0x3ff) << 11) | ((aux & 0x7ffu) << 21),
+                      (uint32_t)yv | ((aux >> 11) << 25));
+}
+
 EventTemplate build_events(const RayTemplate& T) {
     EventTemplate E;
     const int64_t nrays = (int64_t)T.p.size();
@@ -171,8 +204,12 @@ EventTemplate build_events(const RayTemplate& T) {
         for (size_t s = 0; s < steps; ++s)
             for (int64_t l = 0; l < 32; ++l) {
                 const int64_t r = g * 32 + l;
-                E.events.push_back(r < nrays && s < per[(size_t)r].size() ? per[(size_t)r][s]
-                                                                         : make_uint2((uint32_t)kEvNop, 0u));
+                const uint2 e = r < nrays && s < per[(size_t)r].size() ? per[(size_t)r][s]
+                                                                       : make_uint2((uint32_t)kEvNop, 0u);
+                E.events.push_back(e);
+                const int64_t L2 = r < nrays ? (int64_t)T.p[(size_t)r] * T.p[(size_t)r] +
+                                                   (int64_t)T.q[(size_t)r] * T.q[(size_t)r] : 1;
+                E.events3.push_back(pack_ev3(e, T.roi, L2));
             }
         row += (int64_t)steps;
     }
@@ -222,9 +259,12 @@ txs_status get_template(txs_ctx* ctx, int32_t roi, RayTemplateDev** out) {
         D.nevents = (int64_t)E.events.size();
         TXS_CUDA(ctx, "viewshed", cudaMalloc(&D.groups, sizeof(int2) * E.groups.size()));
         TXS_CUDA(ctx, "viewshed", cudaMalloc(&D.events, sizeof(uint2) * std::max<size_t>(1, E.events.size())));
+        TXS_CUDA(ctx, "viewshed", cudaMalloc(&D.events3, sizeof(uint2) * std::max<size_t>(1, E.events3.size())));
         TXS_CUDA(ctx, "viewshed", cudaMemcpy(D.groups, E.groups.data(), sizeof(int2) * E.groups.size(), cudaMemcpyHostToDevice));
         if (!E.events.empty())
             TXS_CUDA(ctx, "viewshed", cudaMemcpy(D.events, E.events.data(), sizeof(uint2) * E.events.size(), cudaMemcpyHostToDevice));
+        if (!E.events3.empty())
+            TXS_CUDA(ctx, "viewshed", cudaMemcpy(D.events3, E.events3.data(), sizeof(uint2) * E.events3.size(), cudaMemcpyHostToDevice));
     }
     TXS_CUDA(ctx, "viewshed", cudaMalloc(&D.rays, sizeof(int4) * rays.size()));
     TXS_CUDA(ctx, "viewshed", cudaMalloc(&D.cells, sizeof(uint32_t) * std::max<size_t>(1, cells.size())));

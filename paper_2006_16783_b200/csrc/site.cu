@@ -370,6 +370,222 @@ __global__ void TXS_LOOP_REGS k_site_loop(SiteArgs a, SiteState* st, LoopPtrs lp
     }
 }
 
+// ---- persistent SITE loop with ONE grid barrier per round (site_mode 0) ---------
+// Candidate i is owned by CTA i mod G, which keeps its gain and window in
+// shared memory, so a gain is only ever updated by its owner and the per-CTA
+// partial argmax needs no barrier after the updates.  Per round r (after the
+// barrier):
+//   1. every CTA reduces the G partials {key = gain << 32 | ~idx, position,
+//      window} of round r-1 (double-buffered by parity): identical winner w_r
+//      and stop decisions (decision D9) everywhere;
+//   2. the previous winner's bits are ORed into cum, rows spread over the CTAs
+//      (the commit of w_{r-1} happens one round late);
+//   3. every CTA updates its owned candidates whose window overlaps w_r's:
+//      gain_i -= popc(v_i & v_w & ~cum & ~v_{w_{r-1}}).  The reads of cum race
+//      with step 2's writes, and either value of a word gives the same result:
+//      cum through w_{r-2} | v_{w_{r-1}} is exactly cum through w_{r-1};
+//   4. it writes its new partial -> barrier.
+// The winner overlaps itself, so its gain drops to 0 (taken).  Exact: the same
+// picks, gains and cum as the three-barrier loop and naive greedy.
+struct __align__(16) SitePart {
+    unsigned long long key;
+    int r, c, row0, col0, h, w;
+};
+
+__device__ __forceinline__ void part_max(SitePart& a, const SitePart& b) {
+    if (b.key > a.key) a = b;
+}
+
+__device__ __forceinline__ SitePart shfl_part(const SitePart& p, int o) {
+    SitePart q;
+    q.key = __shfl_xor_sync(kFull, p.key, o);
+    q.r = __shfl_xor_sync(kFull, p.r, o); q.c = __shfl_xor_sync(kFull, p.c, o);
+    q.row0 = __shfl_xor_sync(kFull, p.row0, o); q.col0 = __shfl_xor_sync(kFull, p.col0, o);
+    q.h = __shfl_xor_sync(kFull, p.h, o); q.w = __shfl_xor_sync(kFull, p.w, o);
+    return q;
+}
+
+#ifndef SITE_L1_THREADS
+#define SITE_L1_THREADS 256
+#endif
+constexpr int kL1Threads = SITE_L1_THREADS;
+
+// cum |= v over the window rows slot, slot + nslots, ... (the commit of one winner)
+__device__ __forceinline__ void flush_rows(const SiteArgs& a, const SitePart& w, const uint64_t* __restrict__ v,
+                                           uint64_t* __restrict__ cum, int slot, int nslots) {
+    const int nwr = win_nwr(w.col0, w.w), wlo = w.col0 >> 6;
+    const int nrow = (w.h + nslots - 1 - slot) / nslots;   // rows of this slot
+    for (int t = threadIdx.x; t < nrow * nwr; t += blockDim.x) {
+        const int y = slot + (t / nwr) * nslots, b = t % nwr;
+        const uint64_t x = v[y * nwr + b];
+        if (x) {
+            uint64_t* o = cum + (int64_t)(w.row0 + y) * a.wpr + wlo + b;
+            *o |= x;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kL1Threads, 1) k_site_loop1(SiteArgs a, SiteState* st, LoopPtrs lp,
+                                                         const int32_t* __restrict__ pop, int32_t* __restrict__ gain,
+                                                         const uint64_t* __restrict__ words, uint64_t* __restrict__ cum,
+                                                         SitePart* __restrict__ parts,
+                                                         unsigned long long* __restrict__ counters) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int m = (int)((a.n - cta + G - 1) / G);   // owned: i = cta + G j, j < m
+    int4* s_win = (int4*)s_dyn;
+    int2* s_rc = (int2*)(s_win + m);
+    int* s_gain = (int*)(s_rc + m);
+    int* s_nb = s_gain + m;                          // owned candidates overlapping the winner
+    __shared__ SitePart s_part[kL1Threads / 32];
+    __shared__ int s_nnb, s_nrows[kL1Threads];
+    for (int j = tid; j < m; j += blockDim.x) {
+        const int64_t i = cta + (int64_t)G * j;
+        s_win[j] = lp.wins[i];
+        s_rc[j] = make_int2(lp.crow[i], lp.ccol[i]);
+        s_gain[j] = pop[i];
+    }
+    __syncthreads();
+    // partial argmax of the owned gains -> parts[buf][cta]
+    auto write_partial = [&](SitePart* buf) {
+        SitePart b{0ull, 0, 0, 0, 0, 0, 0};
+        for (int j = tid; j < m; j += blockDim.x) {
+            const int64_t i = cta + (int64_t)G * j;
+            const unsigned long long key = ((unsigned long long)(uint32_t)s_gain[j] << 32) | (0xffffffffull - (uint64_t)i);
+            if (key > b.key) {
+                const int4 wv = s_win[j];
+                b = SitePart{key, s_rc[j].x, s_rc[j].y, wv.x, wv.y, wv.z, wv.w};
+            }
+        }
+        for (int o = 16; o; o >>= 1) part_max(b, shfl_part(b, o));
+        if (lane == 0) s_part[warp] = b;
+        __syncthreads();
+        if (tid == 0) {
+            SitePart x = s_part[0];
+            for (int k = 1; k < kL1Threads / 32; ++k) part_max(x, s_part[k]);
+            buf[cta] = x;
+        }
+    };
+    write_partial(parts);
+    grid.sync();
+    long long nsel = 0, covered = 0;
+    int stop = TXS_STOP_EXHAUSTED;
+    bool have_prev = false;
+    SitePart prev{};
+    int64_t prev_idx = 0;
+    unsigned long long bytes_all = 0;
+    for (int it = 0;; ++it) {
+        const SitePart* pb = parts + (size_t)(it & 1) * G;
+        SitePart* pn = parts + (size_t)((it + 1) & 1) * G;
+        // ---- 1. global winner (redundantly in every CTA)
+        SitePart best{0ull, 0, 0, 0, 0, 0, 0};
+        for (int k = tid; k < G; k += blockDim.x) part_max(best, pb[k]);
+        for (int o = 16; o; o >>= 1) part_max(best, shfl_part(best, o));
+        __syncthreads();   // s_part reuse
+        if (lane == 0) s_part[warp] = best;
+        __syncthreads();
+        best = s_part[0];
+        for (int k = 1; k < kL1Threads / 32; ++k) part_max(best, s_part[k]);
+        // ---- 2. commit of the previous winner (rows spread over the CTAs)
+        if (have_prev) flush_rows(a, prev, words + prev_idx * a.stride, cum, cta, G);
+        const int g = (int)(best.key >> 32);
+        const int64_t idx = (int64_t)(0xffffffffull - (best.key & 0xffffffffull));
+        if (nsel >= a.n) { stop = TXS_STOP_EXHAUSTED; break; }
+        if (g <= 0) { stop = TXS_STOP_ZERO_GAIN; break; }
+        covered += g;
+        const double cov = (double)covered / a.total;
+        if (cta == 0 && tid == 0) lp.steps[nsel] = txs_step{idx, best.r, best.c, (int64_t)g, cov};
+        ++nsel;
+        const uint64_t* vw = words + idx * a.stride;
+        if (cov >= a.target || (a.max_sel > 0 && nsel >= a.max_sel)) {
+            stop = cov >= a.target ? TXS_STOP_TARGET_REACHED : TXS_STOP_MAX_SELECTED;
+            flush_rows(a, best, vw, cum, cta, G);   // the final commit
+            break;
+        }
+        // ---- 3. owned neighbours: gain -= popc(v_i & v_w & ~cum & ~v_prev)
+        if (tid == 0) s_nnb = 0;
+        __syncthreads();
+        const int wr1 = best.row0 + best.h - 1, wc1 = best.col0 + best.w - 1;
+        for (int j = tid; j < m; j += blockDim.x) {
+            const int4 wv = s_win[j];
+            if (wv.x <= wr1 && wv.x + wv.z - 1 >= best.row0 && wv.y <= wc1 && wv.y + wv.w - 1 >= best.col0)
+                s_nb[atomicAdd(&s_nnb, 1)] = j;
+        }
+        __syncthreads();
+        const int nnb = s_nnb;
+        if (nnb > 0) {
+            // (neighbour, overlap row) pairs flattened over the CTA
+            const int nwr_w = win_nwr(best.col0, best.w), wlo_w = best.col0 >> 6;
+            const int nwr_p = have_prev ? win_nwr(prev.col0, prev.w) : 0, wlo_p = prev.col0 >> 6;
+            const uint64_t* vp = have_prev ? words + prev_idx * a.stride : nullptr;
+            int total = 0;   // pairs (the overlap row counts of the neighbours, prefix in s_nrows)
+            for (int k0 = 0; k0 < nnb; k0 += blockDim.x) {
+                // rows per neighbour of this chunk, then a CTA prefix scan (chunk <= blockDim.x neighbours)
+                int rows = 0;
+                if (k0 + tid < nnb) {
+                    const int4 wv = s_win[s_nb[k0 + tid]];
+                    rows = min(wv.x + wv.z - 1, wr1) - max(wv.x, best.row0) + 1;
+                }
+                int incl = rows;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                __syncthreads();
+                if (lane == 31) s_part[warp].r = incl;   // warp totals (s_part is free here)
+                __syncthreads();
+                int woff = 0;
+                for (int q = 0; q < warp; ++q) woff += s_part[q].r;
+                int ctot = 0;
+                for (int q = 0; q < kL1Threads / 32; ++q) ctot += s_part[q].r;
+                s_nrows[tid] = woff + incl;   // inclusive prefix of the chunk's neighbours
+                __syncthreads();
+                const int cn = min((int)blockDim.x, nnb - k0);
+                for (int t = tid; t < ctot; t += blockDim.x) {
+                    int lo = 0, hi = cn - 1;     // the neighbour holding pair t
+                    while (lo < hi) { const int mid = (lo + hi) >> 1; if (s_nrows[mid] > t) hi = mid; else lo = mid + 1; }
+                    const int j = s_nb[k0 + lo];
+                    const int4 wv = s_win[j];
+                    const int y = max(wv.x, best.row0) + t - (lo ? s_nrows[lo - 1] : 0);
+                    const int cl = max(wv.y, best.col0), ch = min(wv.y + wv.w - 1, wc1);
+                    const int64_t i = cta + (int64_t)G * j;
+                    const uint64_t* vi = words + i * a.stride + (int64_t)(y - wv.x) * win_nwr(wv.y, wv.w) - (wv.y >> 6);
+                    const uint64_t* vwr = vw + (int64_t)(y - best.row0) * nwr_w - wlo_w;
+                    const bool prow = have_prev && y >= prev.row0 && y < prev.row0 + prev.h;
+                    const uint64_t* vpr = prow ? vp + (int64_t)(y - prev.row0) * nwr_p - wlo_p : nullptr;
+                    const uint64_t* cr = cum + (int64_t)y * a.wpr;
+                    int acc = 0;
+                    for (int B = cl >> 6; B <= (ch >> 6); ++B) {
+                        const uint64_t x = __ldg(vi + B) & __ldg(vwr + B) & ~(*(volatile const uint64_t*)(cr + B));
+                        const uint64_t pv = (prow && B >= wlo_p && B < wlo_p + nwr_p) ? __ldg(vpr + B) : 0ull;
+                        acc += __popcll(x & ~pv);
+                    }
+                    if (acc) atomicSub(&s_gain[j], acc);
+                }
+                total += ctot;
+                __syncthreads();
+            }
+            bytes_all += 16ull * (unsigned long long)total;
+        }
+        __syncthreads();
+        // ---- 4. new partial -> barrier
+        write_partial(pn);
+        prev = best;
+        prev_idx = idx;
+        have_prev = true;
+        grid.sync();
+    }
+    for (int j = tid; j < m; j += blockDim.x) gain[cta + (int64_t)G * j] = s_gain[j];
+    if (tid == 0 && bytes_all) atomicAdd(counters + kSiteBytes, bytes_all);
+    if (cta == 0 && tid == 0) {
+        st->nsel = nsel;
+        st->covered = covered;
+        st->stop = stop;
+        st->done = 1;
+    }
+}
+
 // Streaming form over the cum-aligned layout: lane t of the candidate's warp
 // reads word t (one coalesced, L1-bypassing load; the viewshed words are the
 // only HBM stream) = word b of window row y, whose cum counterpart is the
@@ -724,6 +940,54 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
     const double expected_nb = (double)n * span * span / ((double)c->nrows * (double)c->ncols);
     const bool persistent = p.site_mode == 0 && (expected_nb <= 1000.0 || getenv("TXS_SITE_PERSISTENT")) &&
                             !getenv("TXS_SITE_GRAPH");
+    if (persistent && !getenv("TXS_SITE_LOOP3")) {
+        // one-barrier persistent loop (k_site_loop1): owned gains/windows in shared memory
+        int want = 2;
+        if (const char* e = getenv("TXS_SITE_LOOP_CTAS")) want = std::max(1, atoi(e));
+        int grid = 0, per_sm = 0;
+        size_t smem = 0;
+        for (int w = want; w >= 1; --w) {
+            const int g = w * sms;
+            const int64_t m = (n + g - 1) / g;
+            smem = (size_t)m * (sizeof(int4) + sizeof(int2) + 2 * sizeof(int));
+            if (smem > 200 * 1024) continue;
+            if (smem > 48 * 1024)
+                TXS_CUDA(c, "site", cudaFuncSetAttribute(k_site_loop1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            TXS_CUDA(c, "site", cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_site_loop1, kL1Threads, smem));
+            if (per_sm >= w) { grid = g; break; }
+        }
+        if (grid > 0) {
+            if (ensure(c, "site", (void**)&c->d_partials, &c->partials_cap, 2 * sizeof(SitePart) * (size_t)grid) != TXS_OK)
+                return TXS_ERR_OUT_OF_MEMORY;
+            SiteArgs aa = a;
+            LoopPtrs lpp = lp0;
+            SiteState* st_ = c->d_state;
+            const int32_t* pop_ = c->d_pop;
+            int32_t* g_ = c->d_gain;
+            const uint64_t* w_ = c->d_words;
+            uint64_t* cu_ = cumv;
+            SitePart* pa_ = (SitePart*)c->d_partials;
+            unsigned long long* co_ = c->d_counters;
+            void* args[] = {&aa, &st_, &lpp, &pop_, &g_, &w_, &cu_, &pa_, &co_};
+            cudaEventRecord(c->ev_r0, c->stream);
+            TXS_CUDA(c, "site", cudaLaunchCooperativeKernel((void*)k_site_loop1, grid, kL1Threads, args, smem, c->stream));
+            TXS_LAUNCHED(c, "site");
+            cudaEventRecord(c->ev_r1, c->stream);
+            c->stats.site_launches += 1;
+            TXS_CUDA(c, "site", cudaMemcpyAsync(c->h_state, c->d_state, sizeof(SiteState), cudaMemcpyDeviceToHost, c->stream));
+            TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+            add_round_time(c);
+            const int64_t ns = c->h_state->nsel;
+            c->stats.site_iterations += ns;
+            out.resize((size_t)ns);
+            if (ns > 0) {
+                TXS_CUDA(c, "site", cudaMemcpyAsync(out.data(), d_steps, sizeof(txs_step) * ns, cudaMemcpyDeviceToHost, c->stream));
+                TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+            }
+            *stop = c->h_state->stop;
+            return TXS_OK;
+        }
+    }
     if (persistent) {
         // persistent cooperative loop: as many co-resident CTAs as fit, <= 2 per SM
         int per_sm = 0;

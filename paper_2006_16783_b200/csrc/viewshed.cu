@@ -480,6 +480,90 @@ __device__ __forceinline__ void vs_events_k(const int16_t* __restrict__ z, const
     }
 }
 
+// Interior K-observer sweep on the interior event encoding (events3,
+// raytemplate.cpp pack_ev3): per event one shared decode -- pair offset
+// dr*p2 + F, weight word W, denominator n = w0 + w1 (a dp2a of W with
+// (1, 1)), the receiver-height term, the cell's bitmap word and bit straight
+// from the event -- then per observer
+//     X   = dp2a(pair, W, hrc) - n*E          (crossing: z*n - E*n; cell: z + h_r - E)
+//     lhs = X * M',  rhs = N * yv              (M' = L2*M: one product for both kinds)
+//     crossing: horizon <- (X, yv) iff lhs > rhs;  cell: visible iff lhs >= rhs
+// and a flag when the two products' low words agree (a superset of the exact
+// ties, re-decided in fp64 by k_vs_fp64_ties).
+template <int K, int STEP>
+__device__ __forceinline__ void vs_events_k3(const int* rk, const int* ck, const int* Ek, const VsArgs& a,
+                                             const int4* __restrict__ rays, const int2* __restrict__ groups,
+                                             const uint2* __restrict__ events, int ngroups, uint32_t* s_bits,
+                                             int bits_stride, unsigned long long* counters) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const uint32_t* __restrict__ B[K];
+    int nE[K];
+    uint32_t sb[K];
+    const int p2 = a.p2, hr = a.hr;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        B[k] = a.pairs + (int64_t)(rk[k] - a.zoff) * a.p2 + 2 * ck[k] + (threadIdx.x >> 10);
+        asm("mov.b64 %0, %0;" : "+l"(B[k]));
+        nE[k] = -Ek[k];
+        sb[k] = (uint32_t)__cvta_generic_to_shared(s_bits + k * bits_stride);
+    }
+    for (int g = warp; g < ngroups; g += nwarps) {
+        const int2 grp = __ldg(groups + g);
+        const int ray = g * 32 + lane;
+        int p = 0, q = 0;
+        if (ray < a.nrays) { const int4 rd = __ldg(rays + ray); p = rd.x; q = rd.y; }
+        const int L2 = p * p + q * q;
+        // horizon N/M' (M' = L2*M) from a sentinel below every real tangent (see vs_events_k)
+        int NH[K], MH[K];
+        bool tied[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) { NH[k] = -(1 << 30); MH[k] = L2; tied[k] = false; }
+        const uint2* ev = events + (int64_t)grp.x * 32 + lane;
+        for (int st0 = 0; st0 < grp.y; st0 += STEP, ev += 32 * STEP) {
+            uint2 ee[STEP];
+            uint32_t pr[STEP][K];
+#pragma unroll
+            for (int u = 0; u < STEP; ++u) {
+                ee[u] = __ldg(ev + u * 32);
+                const int dr = ((int)(ee[u].x << 21)) >> 23, F = ((int)(ee[u].x << 11)) >> 22;
+                const int off = dr * p2 + F;   // Nop events carry dr = F = 0
+#pragma unroll
+                for (int k = 0; k < K; ++k) pr[u][k] = vs_pld(B[k] + off);
+            }
+#pragma unroll
+            for (int u = 0; u < STEP; ++u) {
+                const uint32_t x = ee[u].x, type = x & 3u;
+                const bool iscell = type == kEv3Cell, iscross = type == kEv3Cross;
+                const uint32_t aux = (x >> 21) | ((ee[u].y >> 25) << 11);
+                const int yv = (int)(ee[u].y & 0x1ffffffu);
+                const uint32_t W = iscell ? 1u : aux;
+                const int n = vs_dp2(0x00010001u, W);   // w0 + w1 (1 for a cell)
+                const int hrc = iscell ? hr : 0;
+                const uint32_t cw4 = (aux >> 5) << 2, cbit = 1u << (aux & 31u);
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    int v;
+                    asm("dp2a.lo.s32.u32 %0, %1, %2, %3;" : "=r"(v) : "r"(pr[u][k]), "r"(W), "r"(hrc));
+                    const int X = v + n * nE[k];
+                    const long long lhs = mulw(X, MH[k]);
+                    const long long rhs = mulw(NH[k], yv);
+                    const bool up = iscross & (lhs > rhs);
+                    NH[k] = up ? X : NH[k];
+                    MH[k] = up ? yv : MH[k];
+                    red_or_shared(sb[k] + cw4, cbit, iscell & (lhs >= rhs));
+                    tied[k] |= iscell & ((uint32_t)lhs == (uint32_t)rhs);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            if (tied[k]) {   // observer k of this CTA (k_viewshed_evk's slot order)
+                const int64_t slot = (int64_t)blockIdx.x * K + k;
+                push_vs_tie(a, counters, a.perm ? a.perm[slot] : slot, ray);
+            }
+    }
+}
+
 template <bool SMEM_BITS>
 __global__ void k_viewshed_ev(const int16_t* __restrict__ z, const int32_t* __restrict__ crow,
                               const int32_t* __restrict__ ccol, const int4* __restrict__ rays,
@@ -555,7 +639,8 @@ __global__ void __maxnreg__(MAXREG) k_viewshed_evk(const int16_t* __restrict__ z
                                const int32_t* __restrict__ ccol, const int4* __restrict__ rays,
                                const int2* __restrict__ groups, const uint2* __restrict__ events, int ngroups,
                                VsArgs a, uint64_t* __restrict__ words, int4* __restrict__ wins,
-                               int32_t* __restrict__ pops, unsigned long long* __restrict__ counters) {
+                               int32_t* __restrict__ pops, unsigned long long* __restrict__ counters,
+                               const uint2* __restrict__ events3) {
     extern __shared__ __align__(16) uint32_t s_bits[];
     __shared__ int s_red[32];
     const int bits_stride = a.sbits;
@@ -589,7 +674,8 @@ __global__ void __maxnreg__(MAXREG) k_viewshed_evk(const int16_t* __restrict__ z
     unsigned long long n_cross = 0, n_cells = 0;
     if (all_int) {
         unsigned long long d0 = 0, d1 = 0;
-        if (a.pairs) vs_events_k<K, true, false, STEP>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride, d0, d1,
+        if (a.pairs && events3) vs_events_k3<K, STEP>(rk, ck, Ek, a, rays, groups, events3, ngroups, s_bits, bits_stride, counters);
+        else if (a.pairs) vs_events_k<K, true, false, STEP>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride, d0, d1,
                                                        counters);
         else vs_events_k<K, false, false, STEP>(z, rk, ck, Ek, RSk, K0k, a, rays, groups, events, ngroups, s_bits, bits_stride, d0, d1,
                                                 counters);
@@ -884,27 +970,33 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
         set_zbounds(c->d_z, c->d_z + c->z_rows * c->ncols, c->stream, (const int16_t*)a.pairs,
                     (const int16_t*)(a.pairs + pwords));
         }
+        // interior observers sweep the interior event encoding (TXS_VS_EV3=0: the generic one)
+        const uint2* ev3 = T->events3;
+        if (const char* e = getenv("TXS_VS_EV3")) ev3 = atoi(e) ? T->events3 : nullptr;
         if (kobs == 3) {
             auto kern = cap64 ? k_viewshed_evk<3, 64, 2> : k_viewshed_evk<3, 72, 2>;
             if (sm > 48 * 1024)
                 TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             cudaEventRecord(c->ev_k0, c->stream);
             kern<<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
-                                                                 T->ngroups, a, c->d_words, c->d_win, c->d_pop, c->d_counters);
+                                                                 T->ngroups, a, c->d_words, c->d_win, c->d_pop, c->d_counters,
+                                                                 ev3);
         } else if (kobs == 2) {
             auto kern = cap64 ? (step4 ? k_viewshed_evk<2, 64, 4> : k_viewshed_evk<2, 64, 2>) : k_viewshed_evk<2, 72, 2>;
             if (sm > 48 * 1024)
                 TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             cudaEventRecord(c->ev_k0, c->stream);
             kern<<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
-                                                                 T->ngroups, a, c->d_words, c->d_win, c->d_pop, c->d_counters);
+                                                                 T->ngroups, a, c->d_words, c->d_win, c->d_pop, c->d_counters,
+                                                                 ev3);
         } else {
             auto kern = cap64 ? k_viewshed_evk<4, 64, 2> : k_viewshed_evk<4, 72, 2>;
             if (sm > 48 * 1024)
                 TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             cudaEventRecord(c->ev_k0, c->stream);
             kern<<<grid, threads, sm, c->stream>>>(c->zv(), c->d_crow, c->d_ccol, T->rays, T->groups, T->events,
-                                                                 T->ngroups, a, c->d_words, c->d_win, c->d_pop, c->d_counters);
+                                                                 T->ngroups, a, c->d_words, c->d_win, c->d_pop, c->d_counters,
+                                                                 ev3);
         }
     } else if (T->events) {
         // warps per CTA: the divisor of the group count closest to 12 (balanced strides)
