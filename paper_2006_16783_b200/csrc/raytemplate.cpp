@@ -213,6 +213,11 @@ EventTemplate build_events(const RayTemplate& T) {
             }
         row += (int64_t)steps;
     }
+    // 4 rows of Nops past the last group: the sweeps prefetch one iteration ahead
+    for (int s = 0; s < 4 * 32; ++s) {
+        E.events.push_back(make_uint2((uint32_t)kEvNop, 0u));
+        E.events3.push_back(make_uint2((uint32_t)kEv3Nop, 0u));
+    }
     return E;
 }
 

@@ -519,16 +519,27 @@ __device__ __forceinline__ void vs_events_k3(const int* rk, const int* ck, const
 #pragma unroll
         for (int k = 0; k < K; ++k) { NH[k] = -(1 << 30); MH[k] = L2; tied[k] = false; }
         const uint2* ev = events + (int64_t)grp.x * 32 + lane;
+        // software pipeline: the next iteration's events are loaded while this
+        // one computes (the stream is padded by STEP rows of Nops at its end)
+        // (two-event iterations only: at STEP 4 the extra registers cost more, c5 1027 -> 1055 ms)
+        constexpr bool kPre = STEP == 2;
+        uint2 en[STEP];
+#pragma unroll
+        for (int u = 0; u < STEP; ++u) en[u] = kPre ? __ldg(ev + u * 32) : make_uint2(0u, 0u);
         for (int st0 = 0; st0 < grp.y; st0 += STEP, ev += 32 * STEP) {
             uint2 ee[STEP];
             uint32_t pr[STEP][K];
 #pragma unroll
             for (int u = 0; u < STEP; ++u) {
-                ee[u] = __ldg(ev + u * 32);
+                ee[u] = kPre ? en[u] : __ldg(ev + u * 32);
                 const int dr = ((int)(ee[u].x << 21)) >> 23, F = ((int)(ee[u].x << 11)) >> 22;
                 const int off = dr * p2 + F;   // Nop events carry dr = F = 0
 #pragma unroll
                 for (int k = 0; k < K; ++k) pr[u][k] = vs_pld(B[k] + off);
+            }
+            if (kPre) {
+#pragma unroll
+                for (int u = 0; u < STEP; ++u) en[u] = __ldg(ev + 32 * STEP + u * 32);
             }
 #pragma unroll
             for (int u = 0; u < STEP; ++u) {
