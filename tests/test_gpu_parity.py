@@ -531,7 +531,7 @@ def test_sharded_bench_torchrun_world1():
     lines = [l for l in r.stdout.splitlines() if l.strip()]
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
-    assert "graph" in d["config"]["parallelism"] and d["roofline"] and d["stages"]["site"]["ms"] > 0
+    assert "graph" in d["result"]["parallelism"] and d["roofline"] and d["stages"]["site"]["ms"] > 0
     r1 = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "c1", "--steps", "1",
                          "--warmup", "1", "--no-cpu-baseline"], cwd=root, capture_output=True, text=True, timeout=600)
     assert r1.returncode == 0, r1.stderr[-3000:]
