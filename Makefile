@@ -29,7 +29,7 @@ $(BUILD)/%.cpp.o: $(PKG)/csrc/%.cpp $(HDRS) | $(BUILD)
 	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
 
 $(LIB): $(OBJ)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lnccl
 
 # bounds-checked variant for the tests (terrain loads trap when out of range)
 $(BUILD)/chk_%.o: $(PKG)/csrc/%.cu $(HDRS) | $(BUILD)
@@ -37,7 +37,7 @@ $(BUILD)/chk_%.o: $(PKG)/csrc/%.cu $(HDRS) | $(BUILD)
 $(BUILD)/chk_%.cpp.o: $(PKG)/csrc/%.cpp $(HDRS) | $(BUILD)
 	$(NVCC) $(NVFLAGS) -DTXS_BOUNDS_CHECK -x cu -c $< -o $@
 $(CHECKED): $(CHK_OBJ)
-	$(NVCC) $(ARCH) -shared -o $@ $(CHK_OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(CHK_OBJ) -lnccl
 
 $(HOSTLIB): $(PKG)/host/txsite.cpp include/txsite/txsite.hpp include/txsite_b200.h $(LIB)
 	g++ -std=c++17 -O2 -fPIC -shared -Wall -Wextra -Iinclude -o $@ $(PKG)/host/txsite.cpp -L$(PKG) -ltxsite_b200 -Wl,-rpath,'$$ORIGIN'

@@ -255,6 +255,98 @@ txs_status txs_site_shard_select_dev(txs_ctx* ctx, const uint64_t* d_gathered, i
 txs_status txs_site_shard_result(txs_ctx* ctx, txs_step* steps, int64_t cap, int64_t* nsteps, int32_t* stop_reason);
 /* The context's CUDA stream (a cudaStream_t), for ordering external work with it. */
 void* txs_stream(txs_ctx* ctx);
+/* OR the bits of global rows [row_begin, row_end) of the context's cumulative
+ * viewshed (the held cum rows; rows outside them read as 0) into `dense_out`,
+ * the caller's SPEC-dense bitmap of the WHOLE grid ((nrows*ncols+63)/64 words,
+ * SPEC.md:351).  Words wholly inside the rows are overwritten, the (at most two)
+ * words shared with neighbouring rows are OR-ed atomically, so row bands of
+ * several contexts may be assembled into one buffer concurrently.  The dense
+ * words are formed on the device; only the band's words cross PCIe. */
+txs_status txs_get_cumulative_rows(txs_ctx* ctx, int64_t row_begin, int64_t row_end, uint64_t* dense_out);
+
+/* ---- native multi-GPU group (SURVEY §8(b) txs_create(ngpus, devices)) ----
+ * One process, one host thread per call, N contexts (one per device, or several
+ * on one device for testing).  The group plans the row bands (FINDMAX block rows,
+ * roi+1 halo), runs VIX / FINDMAX / VIEWSHED on every band concurrently (one
+ * worker thread per rank: no collective), assigns global candidate ids by the
+ * prefix of band counts, and drives the SITE rounds with one of three winner
+ * exchanges:
+ *   TXS_XCHG_P2P   (default) every rank writes {its best key, payload} into its
+ *                  own device mailbox; every rank's select kernel reads the N
+ *                  keys and then the winner's window words straight out of the
+ *                  winner rank's mailbox over NVLink peer memory (cross-device
+ *                  ordering by CUDA events, double-buffered mailboxes); the
+ *                  rounds of all ranks are captured as ONE multi-device CUDA
+ *                  graph of 16 rounds and replayed until the device stop flag;
+ *   TXS_XCHG_NCCL  one ncclAllGather of {key, payload} per round over the
+ *                  group's communicators (ncclCommInitAll; distinct devices),
+ *                  also graph-captured;
+ *   TXS_XCHG_HOST  host-staged rounds (keys and the owner's window through host
+ *                  memory; txs_site_shard_best/export/apply) -- the reference
+ *                  formulation, and the only exchange available with custom ops.
+ * All three give the single-context pick sequence and cumulative bitmap. */
+typedef enum txs_exchange { TXS_XCHG_P2P = 0, TXS_XCHG_NCCL = 1, TXS_XCHG_HOST = 2 } txs_exchange;
+
+/* Stage entry points the group drives (defaults: the functions above).  A test
+ * may substitute a CPU stand-in; only TXS_XCHG_HOST works with substituted ops. */
+typedef struct txs_engine_ops {
+    txs_status (*create)(int device, txs_ctx** out);
+    void (*destroy)(txs_ctx* ctx);
+    const char* (*last_error)(const txs_ctx* ctx);
+    txs_status (*set_shard)(txs_ctx*, int64_t nrows, int64_t ncols, int64_t row_begin, int64_t row_end, int32_t halo);
+    txs_status (*shard_info)(const txs_ctx*, int64_t* held_row0, int64_t* held_rows, int64_t* band_begin, int64_t* band_end);
+    txs_status (*set_terrain)(txs_ctx*, const int16_t* z, int64_t nrows, int64_t ncols);
+    txs_status (*generate_fractal)(txs_ctx*, int64_t nrows, int64_t ncols, double roughness, uint64_t seed,
+                                   int32_t zmin, int32_t zmax);
+    txs_status (*fill_rows)(txs_ctx*, int64_t row_begin, int64_t row_end, int16_t value);
+    txs_status (*estimate_vix)(txs_ctx*, const txs_params* p, uint8_t* scores_out);
+    txs_status (*find_candidates)(txs_ctx*, const txs_params* p, int64_t* n_out, txs_candidate* out, int64_t cap);
+    txs_status (*random_observers)(txs_ctx*, int64_t n, uint64_t seed);
+    txs_status (*get_candidates)(txs_ctx*, txs_candidate* out, int64_t cap, int64_t* n_out);
+    txs_status (*set_candidate_base)(txs_ctx*, int64_t gid0);
+    txs_status (*compute_viewsheds)(txs_ctx*, const txs_params* p);
+    txs_status (*site_shard_begin)(txs_ctx*, const txs_params* p);
+    txs_status (*site_shard_best)(txs_ctx*, uint64_t* key);
+    txs_status (*site_shard_export)(txs_ctx*, int64_t gid, int32_t* owned, int32_t* row, int32_t* col,
+                                    txs_window* win, uint64_t* words, int64_t words_stride);
+    txs_status (*site_shard_apply)(txs_ctx*, int32_t row, int32_t col, const txs_window* win, const uint64_t* words);
+    txs_status (*get_cumulative_rows)(txs_ctx*, int64_t row_begin, int64_t row_end, uint64_t* dense_out);
+    txs_status (*get_stats)(txs_ctx*, txs_stats* out);
+} txs_engine_ops;
+const txs_engine_ops* txs_default_ops(void);
+
+typedef struct txs_group txs_group;
+/* Row bands of nrows over `world` ranks by whole FINDMAX block rows (the split
+ * of shard.py's plan_bands): out[2k], out[2k+1] = rank k's [row_begin, row_end).
+ * Host-only.  TXS_ERR_INVALID_ARGUMENT when world exceeds the block rows. */
+txs_status txs_plan_bands(int64_t nrows, int64_t block, int32_t world, int64_t* out);
+txs_status txs_group_create(int ngpus, const int* devices, txs_group** out);
+txs_status txs_group_create_with_ops(int ngpus, const int* devices, const txs_engine_ops* ops, txs_group** out);
+void txs_group_destroy(txs_group* g);
+const char* txs_group_last_error(const txs_group* g);
+int32_t txs_group_size(const txs_group* g);
+txs_ctx* txs_group_context(txs_group* g, int32_t rank);
+txs_status txs_group_set_exchange(txs_group* g, int32_t exchange);
+/* Plan the bands (block = p->block_width, or ceil(roi/3); halo roi+1) and make
+ * every rank a shard of the nrows x ncols grid.  Call before the terrain. */
+txs_status txs_group_set_grid(txs_group* g, int64_t nrows, int64_t ncols, const txs_params* p);
+txs_status txs_group_band(const txs_group* g, int32_t rank, int64_t* row_begin, int64_t* row_end);
+/* Terrain: the whole row-major grid from the host (each rank copies its band +
+ * halo rows), or the D10 generator on every rank's device (cropped). */
+txs_status txs_group_set_terrain(txs_group* g, const int16_t* z);
+txs_status txs_group_generate_fractal(txs_group* g, double roughness, uint64_t seed, int32_t zmin, int32_t zmax);
+txs_status txs_group_fill_rows(txs_group* g, int64_t row_begin, int64_t row_end, int16_t value);
+/* Config 5: the n global draws of decision D11; every rank keeps its band's
+ * observers (ids = draw index).  The next txs_group_run_pipeline then skips
+ * VIX/FINDMAX. */
+txs_status txs_group_random_observers(txs_group* g, int64_t n, uint64_t seed);
+/* VIX -> FINDMAX -> VIEWSHED on every band, then the SITE rounds; stage_ms[4] =
+ * device ms of {vix, findmax, viewshed, site} (max over ranks; site = the
+ * rounds incl. the exchange). */
+txs_status txs_group_run_pipeline(txs_group* g, const txs_params* p, txs_step* steps, int64_t cap,
+                                  int64_t* nsteps, int32_t* stop_reason, double* stage_ms);
+/* Global dense cumulative bitmap, assembled from every rank's band rows. */
+txs_status txs_group_get_cumulative(txs_group* g, uint64_t* dense_out);
 
 /* ---- host-only helpers (no GPU needed; used by the CPU test-suite) -------- */
 /* The frozen D5 ray template for roi: returns ray count; arrays filled when the

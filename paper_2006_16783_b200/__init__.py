@@ -8,7 +8,7 @@ as ``paper_2006_16783_b200.configs`` does not map libtxsite_b200.so, so
 bench.py's CPU reference arm runs without the engine library in the process.
 Touching any engine name loads the library (and fails loudly without it).
 """
-__all__ = ["Engine", "TxsError", "STOP", "LOS_ARITH", "device_ok", "make_params", "max_words", "partition",
+__all__ = ["Engine", "Group", "plan_bands", "TxsError", "STOP", "LOS_ARITH", "device_ok", "make_params", "max_words", "partition",
            "ray_template", "selftest"]
 
 

@@ -116,6 +116,27 @@ _sig("txs_ray_template", i64, [i32, vp, vp, vp, vp, vp, i64, i64, C.POINTER(i64)
 _sig("txs_selftest", C.c_int, [])
 _sig("txs_event_template_info", C.c_int, [i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(i32)])
 
+_sig("txs_get_cumulative_rows", C.c_int, [vp, i64, i64, vp])
+_sig("txs_default_ops", vp, [])
+_sig("txs_plan_bands", C.c_int, [i64, i64, i32, vp])
+_sig("txs_group_create", C.c_int, [C.c_int, vp, C.POINTER(vp)])
+_sig("txs_group_create_with_ops", C.c_int, [C.c_int, vp, vp, C.POINTER(vp)])
+_sig("txs_group_destroy", None, [vp])
+_sig("txs_group_last_error", C.c_char_p, [vp])
+_sig("txs_group_size", i32, [vp])
+_sig("txs_group_context", vp, [vp, i32])
+_sig("txs_group_set_exchange", C.c_int, [vp, i32])
+_sig("txs_group_set_grid", C.c_int, [vp, i64, i64, C.POINTER(Params)])
+_sig("txs_group_band", C.c_int, [vp, i32, C.POINTER(i64), C.POINTER(i64)])
+_sig("txs_group_set_terrain", C.c_int, [vp, vp])
+_sig("txs_group_generate_fractal", C.c_int, [vp, dbl, u64, i32, i32])
+_sig("txs_group_fill_rows", C.c_int, [vp, i64, i64, C.c_int16])
+_sig("txs_group_random_observers", C.c_int, [vp, i64, u64])
+_sig("txs_group_run_pipeline", C.c_int, [vp, C.POINTER(Params), vp, i64, C.POINTER(i64), C.POINTER(i32), vp])
+_sig("txs_group_get_cumulative", C.c_int, [vp, vp])
+
+EXCHANGE = {"p2p": 0, "nccl": 1, "host": 2}
+
 # every symbol the header declares (checked by the CPU test-suite)
 EXPORTS = [
     "txs_abi_version", "txs_device_ok", "txs_create", "txs_destroy", "txs_last_error", "txs_get_stats",
@@ -129,4 +150,8 @@ EXPORTS = [
     "txs_site_shard_best_dev", "txs_site_shard_export_dev", "txs_site_shard_apply_dev",
     "txs_site_shard_payload_words", "txs_site_shard_result", "txs_stream", "txs_time_gain_pass",
     "txs_site_shard_export_keyed_dev", "txs_site_shard_select_dev", "txs_measure_cache_read",
+    "txs_get_cumulative_rows", "txs_default_ops", "txs_plan_bands", "txs_group_create", "txs_group_create_with_ops",
+    "txs_group_destroy", "txs_group_last_error", "txs_group_size", "txs_group_context", "txs_group_set_exchange",
+    "txs_group_set_grid", "txs_group_band", "txs_group_set_terrain", "txs_group_generate_fractal",
+    "txs_group_fill_rows", "txs_group_random_observers", "txs_group_run_pipeline", "txs_group_get_cumulative",
 ]

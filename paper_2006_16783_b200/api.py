@@ -338,6 +338,102 @@ class Engine:
         return self._h
 
 
+def plan_bands(nrows, block, world):
+    """txs_plan_bands: [(row_begin, row_end)] per rank over whole FINDMAX block rows."""
+    out = np.zeros(2 * world, np.int64)
+    st = N.lib.txs_plan_bands(nrows, block, world, _p(out))
+    if st:
+        raise TxsError(st, f"plan_bands: {world} ranks > block rows of {nrows} / {block}")
+    return [(int(out[2 * k]), int(out[2 * k + 1])) for k in range(world)]
+
+
+class Group:
+    """Native multi-GPU group (txs_group, csrc/group.cu): N contexts as row-band
+    shards of one grid, driven from this one process; SITE rounds exchange the
+    winner over peer memory ("p2p", default), NCCL ("nccl") or the host ("host").
+    `devices` may repeat a device (virtual ranks, tests).  `ops` (an address of a
+    txs_engine_ops table) substitutes the stage entry points (CPU stand-in tests;
+    host exchange only)."""
+
+    def __init__(self, devices=(0,), exchange=None, ops=None):
+        devs = np.ascontiguousarray(devices, np.int32)
+        h = C.c_void_p()
+        if ops is None:
+            st = N.lib.txs_group_create(len(devs), _p(devs), C.byref(h))
+        else:
+            st = N.lib.txs_group_create_with_ops(len(devs), _p(devs), C.c_void_p(ops), C.byref(h))
+        if st:
+            raise TxsError(st, f"txs_group_create(devices={list(devices)}) failed")
+        self._h = h
+        self.n = len(devs)
+        if exchange is not None:
+            self._chk(N.lib.txs_group_set_exchange(self._h, N.EXCHANGE[exchange]))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib = getattr(N, "lib", None)
+            if lib is not None:
+                lib.txs_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _chk(self, st):
+        if st:
+            raise TxsError(st, N.lib.txs_group_last_error(self._h).decode())
+
+    def set_exchange(self, name):
+        self._chk(N.lib.txs_group_set_exchange(self._h, N.EXCHANGE[name]))
+
+    def set_grid(self, nrows, ncols, params):
+        self.dims = (nrows, ncols)
+        self._chk(N.lib.txs_group_set_grid(self._h, nrows, ncols, C.byref(params)))
+
+    def band(self, rank):
+        a, b = C.c_int64(), C.c_int64()
+        self._chk(N.lib.txs_group_band(self._h, rank, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def set_terrain(self, z):
+        z = np.ascontiguousarray(z, np.int16)
+        assert z.shape == tuple(self.dims)
+        self._chk(N.lib.txs_group_set_terrain(self._h, _p(z)))
+
+    def generate_fractal(self, roughness, seed, zmin, zmax):
+        self._chk(N.lib.txs_group_generate_fractal(self._h, roughness, seed, zmin, zmax))
+
+    def fill_rows(self, row_begin, row_end, value):
+        self._chk(N.lib.txs_group_fill_rows(self._h, row_begin, row_end, value))
+
+    def random_observers(self, n, seed):
+        self._chk(N.lib.txs_group_random_observers(self._h, n, seed))
+
+    def run_pipeline(self, params, cap=1 << 20):
+        steps = (N.Step * cap)()
+        ns, stop = C.c_int64(), C.c_int32()
+        ms = (C.c_double * 4)()
+        self._chk(N.lib.txs_group_run_pipeline(self._h, C.byref(params), steps, cap, C.byref(ns), C.byref(stop), ms))
+        d = _steps_dict(steps, min(ns.value, cap), stop.value)
+        d["stage_ms"] = dict(vix=ms[0], findmax=ms[1], viewshed=ms[2], site=ms[3])
+        return d
+
+    def cumulative(self):
+        nr, nc = self.dims
+        out = np.zeros((nr * nc + 63) // 64, np.uint64)
+        self._chk(N.lib.txs_group_get_cumulative(self._h, _p(out)))
+        return out
+
+    def context(self, rank):
+        return N.lib.txs_group_context(self._h, rank)
+
+
 _STEP_DT = np.dtype([("index", "<i8"), ("row", "<i4"), ("col", "<i4"), ("gain", "<i8"), ("coverage", "<f8")])
 
 

@@ -904,6 +904,14 @@ txs_status txs_site_shard_result(txs_ctx* c, txs_step* steps, int64_t cap, int64
 
 void* txs_stream(txs_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
+txs_status txs_get_cumulative_rows(txs_ctx* c, int64_t rb, int64_t re, uint64_t* out) {
+    if (!c || !out) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->site_valid) return fail(c, TXS_ERR_STATE, "site", "no cumulative viewshed (run site first)");
+    if (rb < 0 || re > c->nrows || rb > re) return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "bad row range");
+    cudaSetDevice(c->device);
+    return download_cum_rows(c, rb, re, out);
+}
+
 int txs_selftest(void) {
     // exact 64-bit modulo magic vs the hardware '%', divisors of the shapes
     // the engine uses (2roi+1, 2A+1, grid dims) plus random ones

@@ -219,6 +219,10 @@ txs_status shard_site_apply_dev(txs_ctx*, const uint64_t* d_key, const uint64_t*
 int64_t shard_payload_words(const txs_ctx*);
 txs_status shard_site_select_dev(txs_ctx*, const uint64_t* d_gathered, int32_t nranks, uint64_t* d_key,
                                  uint64_t* d_payload);
+// txs_group's peer-memory exchange: d_mail = device array of the N ranks' mailboxes
+txs_status shard_site_select_peers(txs_ctx*, const uint64_t* const* d_mail, int32_t nranks, uint64_t* d_key,
+                                   uint64_t* d_payload);
+txs_status download_cum_rows(txs_ctx*, int64_t row_begin, int64_t row_end, uint64_t* host_dense);
 
 }  // namespace txs
 

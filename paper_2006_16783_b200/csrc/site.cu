@@ -790,10 +790,11 @@ __global__ void k_dense_to_padded(const uint64_t* __restrict__ dense, uint64_t* 
 }
 
 // pad is indexed by global row; rows outside [cr0, cr1) read as zero
+// dense words [t0, t1) of the whole grid are written to dense[0 .. t1-t0)
 __global__ void k_padded_to_dense(const uint64_t* __restrict__ pad, uint64_t* __restrict__ dense, int64_t nrows,
-                                  int64_t ncols, int64_t wpr, int64_t cr0, int64_t cr1) {
-    const int64_t total = nrows * ncols, nw = (total + 63) >> 6;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nw; t += (int64_t)gridDim.x * blockDim.x) {
+                                  int64_t ncols, int64_t wpr, int64_t cr0, int64_t cr1, int64_t t0, int64_t t1) {
+    const int64_t total = nrows * ncols;
+    for (int64_t t = t0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < t1; t += (int64_t)gridDim.x * blockDim.x) {
         uint64_t v = 0;
         const int64_t b0 = t * 64, b1 = min(b0 + 64, total);
         int64_t b = b0;
@@ -811,7 +812,7 @@ __global__ void k_padded_to_dense(const uint64_t* __restrict__ pad, uint64_t* __
             v |= seg << (b - b0);
             b += len;
         }
-        dense[t] = v;
+        dense[t - t0] = v;
     }
 }
 
@@ -1131,10 +1132,39 @@ txs_status download_cum(txs_ctx* c, uint64_t* host_dense) {
         return TXS_ERR_OUT_OF_MEMORY;
     uint64_t* dense = c->d_cum_dense;
     k_padded_to_dense<<<blocks_for(nw, 256, c->num_sms * 16), 256, 0, c->stream>>>(
-        c->d_cum - c->cum_r0 * c->wpr, dense, c->nrows, c->ncols, c->wpr, c->cum_r0, c->cum_r1);
+        c->d_cum - c->cum_r0 * c->wpr, dense, c->nrows, c->ncols, c->wpr, c->cum_r0, c->cum_r1, 0, nw);
     TXS_LAUNCHED(c, "site");
     TXS_CUDA(c, "site", cudaMemcpyAsync(host_dense, dense, sizeof(uint64_t) * nw, cudaMemcpyDeviceToHost, c->stream));
     TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+    return TXS_OK;
+}
+
+// Rows [rb, re) of the cum into the caller's whole-grid dense bitmap: the
+// interior words by one D2H straight into place, the two shared edge words
+// OR-ed atomically (row bands of several contexts assemble concurrently).
+txs_status download_cum_rows(txs_ctx* c, int64_t rb, int64_t re, uint64_t* host_dense) {
+    const int64_t total = c->nrows * c->ncols;
+    const int64_t b0 = rb * c->ncols, b1 = re * c->ncols;
+    if (b1 <= b0) return TXS_OK;
+    const int64_t t0 = b0 >> 6, t1 = (b1 + 63) >> 6, m = t1 - t0;
+    if (ensure(c, "site", (void**)&c->d_cum_dense, &c->cum_dense_cap, sizeof(uint64_t) * (size_t)m) != TXS_OK)
+        return TXS_ERR_OUT_OF_MEMORY;
+    k_padded_to_dense<<<blocks_for(m, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+        c->d_cum - c->cum_r0 * c->wpr, c->d_cum_dense, c->nrows, c->ncols, c->wpr, std::max(rb, c->cum_r0),
+        std::min(re, c->cum_r1), t0, t1);
+    TXS_LAUNCHED(c, "site");
+    // words shared with rows outside [rb, re) (the last word's tail past the grid is padding)
+    const bool e0 = (b0 & 63) != 0, e1 = (b1 & 63) != 0 && b1 < total;
+    const int64_t i0 = e0 ? 1 : 0, i1 = e1 ? m - 1 : m;
+    if (i1 > i0)
+        TXS_CUDA(c, "site", cudaMemcpyAsync(host_dense + t0 + i0, c->d_cum_dense + i0, sizeof(uint64_t) * (i1 - i0),
+                                            cudaMemcpyDeviceToHost, c->stream));
+    uint64_t edge[2] = {0, 0};
+    if (e0) TXS_CUDA(c, "site", cudaMemcpyAsync(&edge[0], c->d_cum_dense, 8, cudaMemcpyDeviceToHost, c->stream));
+    if (e1) TXS_CUDA(c, "site", cudaMemcpyAsync(&edge[1], c->d_cum_dense + m - 1, 8, cudaMemcpyDeviceToHost, c->stream));
+    TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+    if (e0) __atomic_fetch_or(&host_dense[t0], edge[0], __ATOMIC_RELAXED);       // OR is idempotent: m == 1
+    if (e1) __atomic_fetch_or(&host_dense[t1 - 1], edge[1], __ATOMIC_RELAXED);   // with both edges is fine
     return TXS_OK;
 }
 
@@ -1407,6 +1437,39 @@ txs_status shard_site_select_dev(txs_ctx* c, const uint64_t* d_gathered, int32_t
                                  uint64_t* d_payload) {
     k_shard_select_dev<<<1, 256, 0, c->stream>>>(d_gathered, nranks, shard_payload_words(c),
                                                  (unsigned long long*)d_key, d_payload);
+    TXS_LAUNCHED(c, "site");
+    return TXS_OK;
+}
+
+// Peer-memory exchange (txs_group, TXS_XCHG_P2P): mail[k] points at rank k's
+// mailbox {key, payload} -- on its own device, read here over NVLink.  All N keys
+// are read, then only the winner's header and window rows (h * nwr aligned words,
+// not the whole payload stride) cross the link.
+__global__ void k_shard_select_peers(const uint64_t* const* __restrict__ mail, int nranks,
+                                     unsigned long long* __restrict__ key, uint64_t* __restrict__ payload) {
+    __shared__ int s_best;
+    __shared__ int64_t s_len;
+    if (threadIdx.x == 0) {
+        int b = 0;
+        uint64_t bk = *(volatile const uint64_t*)mail[0];
+        for (int k = 1; k < nranks; ++k) {
+            const uint64_t v = *(volatile const uint64_t*)mail[k];
+            if (v > bk) { bk = v; b = k; }
+        }
+        s_best = b;
+        *key = bk;
+        const uint64_t* src = mail[b] + 1;
+        const int h = (int)(uint32_t)src[4], c0 = (int)(uint32_t)src[3], w = (int)(uint32_t)src[5];
+        s_len = bk ? 6 + (int64_t)h * win_nwr(c0, w) : 6;
+    }
+    __syncthreads();
+    const uint64_t* src = mail[s_best] + 1;
+    for (int64_t t = threadIdx.x; t < s_len; t += blockDim.x) payload[t] = src[t];
+}
+
+txs_status shard_site_select_peers(txs_ctx* c, const uint64_t* const* d_mail, int32_t nranks, uint64_t* d_key,
+                                   uint64_t* d_payload) {
+    k_shard_select_peers<<<1, 256, 0, c->stream>>>(d_mail, nranks, (unsigned long long*)d_key, d_payload);
     TXS_LAUNCHED(c, "site");
     return TXS_OK;
 }

@@ -536,7 +536,7 @@ def test_sharded_bench_torchrun_world1():
                          "--warmup", "1", "--no-cpu-baseline"], cwd=root, capture_output=True, text=True, timeout=600)
     assert r1.returncode == 0, r1.stderr[-3000:]
     d1 = json.loads(r1.stdout.strip().splitlines()[-1])
-    assert d["config"]["sited"] == d1["config"]["sited"] and d["config"]["stop"] == d1["config"]["stop"]
+    assert d["result"]["sited"] == d1["result"]["sited"] and d["result"]["stop"] == d1["result"]["stop"]
 
 
 def test_time_gain_pass_counts_packed_bytes(engine):
