@@ -16,8 +16,9 @@ CHK_OBJ := $(CU_SRC:$(PKG)/csrc/%.cu=$(BUILD)/chk_%.o) $(CPP_SRC:$(PKG)/csrc/%.c
 
 HOSTLIB := $(PKG)/libtxsite_host.so
 CLI := $(PKG)/bin/txsite
+APICHK := $(PKG)/bin/txsite_api_check
 
-all: $(LIB) $(CHECKED) $(HOSTLIB) $(CLI) oracle
+all: $(LIB) $(CHECKED) $(HOSTLIB) $(CLI) $(APICHK) oracle
 
 $(BUILD):
 	mkdir -p $(BUILD)
@@ -29,7 +30,7 @@ $(BUILD)/%.cpp.o: $(PKG)/csrc/%.cpp $(HDRS) | $(BUILD)
 	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
 
 $(LIB): $(OBJ)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lnccl
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -ldl
 
 # bounds-checked variant for the tests (terrain loads trap when out of range)
 $(BUILD)/chk_%.o: $(PKG)/csrc/%.cu $(HDRS) | $(BUILD)
@@ -37,7 +38,7 @@ $(BUILD)/chk_%.o: $(PKG)/csrc/%.cu $(HDRS) | $(BUILD)
 $(BUILD)/chk_%.cpp.o: $(PKG)/csrc/%.cpp $(HDRS) | $(BUILD)
 	$(NVCC) $(NVFLAGS) -DTXS_BOUNDS_CHECK -x cu -c $< -o $@
 $(CHECKED): $(CHK_OBJ)
-	$(NVCC) $(ARCH) -shared -o $@ $(CHK_OBJ) -lnccl
+	$(NVCC) $(ARCH) -shared -o $@ $(CHK_OBJ) -ldl
 
 $(HOSTLIB): $(PKG)/host/txsite.cpp include/txsite/txsite.hpp include/txsite_b200.h $(LIB)
 	g++ -std=c++17 -O2 -fPIC -shared -Wall -Wextra -Iinclude -o $@ $(PKG)/host/txsite.cpp -L$(PKG) -ltxsite_b200 -Wl,-rpath,'$$ORIGIN'
@@ -46,11 +47,16 @@ $(CLI): $(PKG)/host/txsite_main.cpp $(HOSTLIB)
 	mkdir -p $(PKG)/bin
 	g++ -std=c++17 -O2 -Wall -Wextra -Iinclude -o $@ $(PKG)/host/txsite_main.cpp -L$(PKG) -ltxsite_host -ltxsite_b200 -Wl,-rpath,'$$ORIGIN/..'
 
+# the reference-shaped C++ value-type API exercised end to end (tests/test_gpu_cli.py)
+$(APICHK): tests/cpp/api_check.cpp $(HOSTLIB)
+	mkdir -p $(PKG)/bin
+	g++ -std=c++17 -O2 -Wall -Wextra -Iinclude -o $@ tests/cpp/api_check.cpp -L$(PKG) -ltxsite_host -ltxsite_b200 -Wl,-rpath,'$$ORIGIN/..'
+
 oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -rf $(BUILD) $(LIB) $(CHECKED) $(HOSTLIB) $(CLI)
+	rm -rf $(BUILD) $(LIB) $(CHECKED) $(HOSTLIB) $(CLI) $(APICHK)
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean

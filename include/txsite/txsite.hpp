@@ -111,15 +111,28 @@ struct RunConfig {
     uint64_t seed = 1;
     double roughness = 0.5;
     int32_t zmin = 0, zmax = 4000;
+    int64_t water_rows = 0;     // rows [0, water_rows) clamped to 0 (BASELINE config 3)
+    int64_t observers_random = 0;   // > 0: that many random observers (decision D11) replace VIX + FINDMAX (config 5)
+    uint64_t observer_seed = 0;
     SiteParams params;
     uint64_t vix_seed = 1;
     std::string out_dir;        // result CSV, report, PGMs when non-empty
     std::vector<int64_t> snapshots;
+    bool images = true;             // out_dir/cumshed.pgm; --no-images skips it
+    bool dump_vix = false;          // out_dir/vix.u8: row-major score bytes
+    bool dump_candidates = false;   // out_dir/candidates.csv: "row,col,score"
+    bool dump_viewsheds = false;    // out_dir/viewsheds.bin: per viewshed {row0, col0, w, h} int32 + packed u64 words, LE
     int device = 0;
+    std::vector<int> devices;   // > 1 entries: the native multi-GPU group (row bands, txs_group_*)
+    int32_t exchange = TXS_XCHG_P2P;   // group SITE winner exchange
 };
 struct RunReport {
     double read_s = 0, vix_s = 0, findmax_s = 0, viewshed_s = 0, site_s = 0, total_s = 0;
     int64_t candidates = 0;
+    int32_t gpus = 1;
+    int64_t device_bytes_peak = 0;   // peak memory estimate: max over GPUs of resident HBM buffers
+    int64_t host_bytes_peak = 0;     // process max RSS
+    std::string params_echo;         // parameter echo
     SitingResult result;
     std::string to_string() const;
 };
@@ -139,6 +152,8 @@ public:
     void generate_fractal(int64_t nrows, int64_t ncols, double roughness, uint64_t seed, int32_t zmin, int32_t zmax);
     void estimate_vix(const SiteParams& p, uint64_t seed);
     int64_t find_candidates(const SiteParams& p);
+    void fill_rows(int64_t row_begin, int64_t row_end, int16_t value);
+    int64_t random_observers(int64_t n, uint64_t seed);
     void compute_all_viewsheds(const SiteParams& p);
     SitingResult site(const SiteParams& p, bool with_cumulative = true);
     txs_ctx* handle() const { return ctx_; }

@@ -104,6 +104,10 @@ typedef struct txs_stats {
     /* device time of the stage's main kernel alone (k_vix_quads / k_vix, the
      * VIEWSHED sweep), CUDA events on the context stream around that launch */
     double ms_vix_kernel, ms_viewshed_kernel;
+    /* HBM held by the context's resident buffers (terrain, planes, VixMap,
+     * candidates, viewsheds, bitmaps, SITE state): now, and the high-water mark
+     * since creation (RunReport's peak memory estimate) */
+    int64_t device_bytes, device_bytes_peak;
 } txs_stats;
 
 typedef struct txs_ctx txs_ctx;
@@ -156,6 +160,9 @@ txs_status txs_set_candidates(txs_ctx* ctx, const txs_candidate* c, int64_t n);
  * col = next_below(ncols) from SplitMix64(seed) (decision D11). */
 txs_status txs_random_observers(txs_ctx* ctx, int64_t n, uint64_t seed);
 txs_status txs_get_candidates(txs_ctx* ctx, txs_candidate* out, int64_t cap, int64_t* n_out);
+/* Global candidate ids of the resident candidates (index i -> base + i, or the
+ * draw index of a sharded random observer): the ids SITE steps report. */
+txs_status txs_get_candidate_ids(txs_ctx* ctx, int64_t* ids_out, int64_t cap, int64_t* n_out);
 
 /* ---- viewshed module (SPEC.md:305 compute_all_viewsheds) ------------------- */
 txs_status txs_compute_viewsheds(txs_ctx* ctx, const txs_params* p);

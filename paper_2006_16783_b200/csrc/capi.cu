@@ -21,10 +21,12 @@ txs_status cuda_fail(txs_ctx* ctx, const char* stage, cudaError_t e) {
 
 txs_status ensure(txs_ctx* ctx, const char* stage, void** p, size_t* cap, size_t bytes) {
     if (bytes <= *cap && *p) return TXS_OK;
-    if (*p) { cudaFree(*p); *p = nullptr; *cap = 0; }
+    if (*p) { cudaFree(*p); *p = nullptr; ctx->dev_bytes -= (int64_t)*cap; *cap = 0; }
     if (bytes == 0) bytes = 16;
     TXS_CUDA(ctx, stage, cudaMalloc(p, bytes));
     *cap = bytes;
+    ctx->dev_bytes += (int64_t)bytes;   // RunReport's peak memory estimate
+    ctx->dev_bytes_peak = std::max(ctx->dev_bytes_peak, ctx->dev_bytes);
     return TXS_OK;
 }
 
@@ -183,6 +185,8 @@ txs_status txs_get_stats(txs_ctx* c, txs_stats* out) {
     out->vs_fp64_flips = (int64_t)h[kVsTiesFlipped];
     out->candidates = c->ncand;
     out->kernel_launches = c->launches;
+    out->device_bytes = c->dev_bytes;
+    out->device_bytes_peak = c->dev_bytes_peak;
     return TXS_OK;
 }
 
@@ -439,6 +443,15 @@ txs_status txs_get_candidates(txs_ctx* c, txs_candidate* out, int64_t cap, int64
     TXS_CUDA(c, "findmax", cudaMemcpyAsync(s.data(), c->d_cscore, 4 * n, cudaMemcpyDeviceToHost, c->stream));
     TXS_CUDA(c, "findmax", cudaStreamSynchronize(c->stream));
     for (int64_t i = 0; i < n; ++i) out[i] = txs_candidate{r[i], cc[i], s[i], 0};
+    return TXS_OK;
+}
+
+txs_status txs_get_candidate_ids(txs_ctx* c, int64_t* out, int64_t cap, int64_t* n_out) {
+    if (!c || (cap > 0 && !out)) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->cand_valid) return fail(c, TXS_ERR_STATE, "findmax", "no candidates");
+    if (n_out) *n_out = c->ncand;
+    const int64_t m = std::min(cap, c->ncand);
+    for (int64_t i = 0; i < m; ++i) out[i] = c->h_cgid.empty() ? c->cand_gid0 + i : (int64_t)c->h_cgid[(size_t)i];
     return TXS_OK;
 }
 

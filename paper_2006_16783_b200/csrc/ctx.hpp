@@ -167,6 +167,7 @@ struct txs_ctx {
     cudaEvent_t ev_k0 = nullptr, ev_k1 = nullptr;   // the stage's main kernel alone (VIX / VIEWSHED)
     cudaEvent_t user_ev[16] = {};
     int64_t launches = 0;
+    int64_t dev_bytes = 0, dev_bytes_peak = 0;   // context buffers (txs::ensure), live and high-water
 
     // scratch
     void* d_scratch = nullptr;

@@ -19,6 +19,7 @@
 // replayed until the device stop flag (decision D9, evaluated identically on
 // every rank from the exchanged key) is set.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -33,6 +34,36 @@
 namespace {
 
 constexpr int kGraphRounds = 16;
+
+// NCCL is opened on first use of TXS_XCHG_NCCL, not linked: a load-time
+// dependency would bind the soname libnccl.so.2 to whichever copy loads first
+// and break a torch imported later in the same process (torch ships its own,
+// newer libnccl.so.2; when torch is already loaded, dlopen returns that copy).
+struct NcclApi {
+    bool tried = false, ok = false;
+    ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi a;
+    if (a.tried) return a;
+    a.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) return a;
+    a.CommInitAll = (decltype(a.CommInitAll))dlsym(h, "ncclCommInitAll");
+    a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
+    a.GroupStart = (decltype(a.GroupStart))dlsym(h, "ncclGroupStart");
+    a.GroupEnd = (decltype(a.GroupEnd))dlsym(h, "ncclGroupEnd");
+    a.AllGather = (decltype(a.AllGather))dlsym(h, "ncclAllGather");
+    a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
+    a.ok = a.CommInitAll && a.CommDestroy && a.GroupStart && a.GroupEnd && a.AllGather && a.GetErrorString;
+    return a;
+}
 
 const txs_engine_ops kDefaultOps = {
     txs_create, txs_destroy, txs_last_error, txs_set_shard, txs_shard_info, txs_set_terrain,
@@ -181,11 +212,12 @@ txs_status enable_peers(txs_group* g) {
 txs_status ensure_comms(txs_group* g) {
     if (!g->comms.empty()) return TXS_OK;
     if (!distinct_devices(g)) return gfail(g, TXS_ERR_INVALID_ARGUMENT, "[site] group: NCCL needs one rank per device");
+    if (!nccl().ok) return gfail(g, TXS_ERR_CUDA, "[site] group: libnccl.so.2 not loadable");
     g->comms.assign((size_t)g->n, nullptr);
-    const ncclResult_t r = ncclCommInitAll(g->comms.data(), g->n, g->dev.data());
+    const ncclResult_t r = nccl().CommInitAll(g->comms.data(), g->n, g->dev.data());
     if (r != ncclSuccess) {
         g->comms.clear();
-        return gfail(g, TXS_ERR_CUDA, std::string("[site] group: ncclCommInitAll: ") + ncclGetErrorString(r));
+        return gfail(g, TXS_ERR_CUDA, std::string("[site] group: ncclCommInitAll: ") + nccl().GetErrorString(r));
     }
     return TXS_OK;
 }
@@ -233,16 +265,17 @@ txs_status enqueue_round(txs_group* g, int parity, int64_t total) {
         if (g->exchange == TXS_XCHG_P2P) G_CUDA(g, "round", cudaEventRecord(g->ev_mail[parity][(size_t)k], c->stream));
     }
     if (g->exchange == TXS_XCHG_NCCL) {
-        ncclResult_t r = ncclGroupStart();
+        NcclApi& N = nccl();
+        ncclResult_t r = N.GroupStart();
         for (int k = 0; k < n && r == ncclSuccess; ++k) {
             cudaSetDevice(g->dev[(size_t)k]);
-            r = ncclAllGather(g->d_mail[0][(size_t)k], g->d_gather[(size_t)k], (size_t)(g->pw + 1), ncclUint64,
-                              g->comms[(size_t)k], g->ctx[(size_t)k]->stream);
+            r = N.AllGather(g->d_mail[0][(size_t)k], g->d_gather[(size_t)k], (size_t)(g->pw + 1), ncclUint64,
+                            g->comms[(size_t)k], g->ctx[(size_t)k]->stream);
         }
-        const ncclResult_t r2 = ncclGroupEnd();
+        const ncclResult_t r2 = N.GroupEnd();
         if (r != ncclSuccess || r2 != ncclSuccess)
             return gfail(g, TXS_ERR_CUDA, std::string("[site] group: ncclAllGather: ") +
-                                              ncclGetErrorString(r != ncclSuccess ? r : r2));
+                                              N.GetErrorString(r != ncclSuccess ? r : r2));
     }
     for (int k = 0; k < n; ++k) {
         txs_ctx* c = g->ctx[(size_t)k];
@@ -428,7 +461,7 @@ void txs_group_destroy(txs_group* g) {
     if (g->native) {
         free_round_buffers(g);
         destroy_events(g);
-        for (ncclComm_t c : g->comms) if (c) ncclCommDestroy(c);
+        for (ncclComm_t c : g->comms) if (c) nccl().CommDestroy(c);
     }
     for (txs_ctx* c : g->ctx) if (c) g->ops.destroy(c);
     delete g;

@@ -339,6 +339,11 @@ int64_t Pipeline::find_candidates(const SiteParams& p) {
     check(ctx_, txs_find_candidates(ctx_, &q, &n, nullptr, 0));
     return n;
 }
+void Pipeline::fill_rows(int64_t rb, int64_t re, int16_t v) { check(ctx_, txs_fill_rows(ctx_, rb, re, v)); }
+int64_t Pipeline::random_observers(int64_t n, uint64_t seed) {
+    check(ctx_, txs_random_observers(ctx_, n, seed));
+    return n;
+}
 void Pipeline::compute_all_viewsheds(const SiteParams& p) {
     const txs_params q = to_params(p);
     check(ctx_, txs_compute_viewsheds(ctx_, &q));
@@ -355,7 +360,10 @@ std::string RunReport::to_string() const {
     o << "stage_seconds read=" << read_s << " vix=" << vix_s << " findmax=" << findmax_s
       << " viewshed=" << viewshed_s << " site=" << site_s << " total=" << total_s << "\n"
       << "candidates=" << candidates << " selected=" << result.selected.size()
-      << " final_coverage=" << result.final_coverage << " stop=" << stop_reason_name(result.stop_reason) << "\n";
+      << " final_coverage=" << result.final_coverage << " stop=" << stop_reason_name(result.stop_reason) << "\n"
+      << "peak_memory_estimate device_bytes=" << device_bytes_peak << " (max over " << gpus
+      << " GPU(s) of resident HBM buffers) host_bytes=" << host_bytes_peak << "\n"
+      << "params " << params_echo << "\n";
     return o.str();
 }
 
@@ -399,17 +407,192 @@ void render_snapshots(const SitingResult& r, const std::vector<Viewshed>& v, int
     }
 }
 
-RunReport run_pipeline(const RunConfig& cfg) {
+namespace {
+
+std::string params_echo(const RunConfig& c, int gpus) {
+    std::ostringstream o;
+    o << "input=" << (c.synth || c.input.empty() ? std::string("synth") : c.input) << " nrows=" << c.nrows
+      << " ncols=" << c.ncols << " seed=" << c.seed << " roughness=" << c.roughness << " zmin=" << c.zmin
+      << " zmax=" << c.zmax << " water_rows=" << c.water_rows << " observers_random=" << c.observers_random
+      << " observer_seed=" << c.observer_seed << " roi=" << c.params.roi << " tx_height=" << c.params.tx_height
+      << " rx_height=" << c.params.rx_height << " coverage=" << c.params.target_coverage
+      << " samples=" << c.params.samples_per_point << " per_block=" << c.params.per_block
+      << " block_width=" << c.params.block_width << " max_selected=" << c.params.max_selected
+      << " site_mode=" << c.params.site_mode << " los_arith=" << (c.params.los_arith == TXS_LOS_EXACT ? "exact" : "fp64")
+      << " vix_seed=" << c.vix_seed << " gpus=" << gpus;
+    if (gpus > 1) o << " exchange=" << (c.exchange == TXS_XCHG_NCCL ? "nccl" : c.exchange == TXS_XCHG_HOST ? "host" : "p2p");
+    return o.str();
+}
+
+int64_t host_rss_peak() {
+    std::ifstream f("/proc/self/status");
+    std::string line;
+    while (std::getline(f, line))
+        if (line.rfind("VmHWM:", 0) == 0) return std::atoll(line.c_str() + 6) * 1024;
+    return 0;
+}
+
+// the resident candidates of each context in global-id order, plus the owner
+// (context, local index) of every global id a step may name
+struct Owners {
+    std::vector<txs_ctx*> ctx;
+    std::vector<std::vector<int64_t>> ids;      // per context, sorted global ids
+    std::vector<std::vector<txs_candidate>> cand;
+    bool find(int64_t gid, size_t* k, int64_t* li) const {
+        for (size_t i = 0; i < ids.size(); ++i) {
+            auto it = std::lower_bound(ids[i].begin(), ids[i].end(), gid);
+            if (it != ids[i].end() && *it == gid) { *k = i; *li = it - ids[i].begin(); return true; }
+        }
+        return false;
+    }
+};
+
+Owners owners_of(const std::vector<txs_ctx*>& ctxs) {
+    Owners o;
+    o.ctx = ctxs;
+    for (txs_ctx* c : ctxs) {
+        int64_t n = 0;
+        check(c, txs_get_candidate_ids(c, nullptr, 0, &n));
+        std::vector<int64_t> ids((size_t)n);
+        std::vector<txs_candidate> cand((size_t)n);
+        if (n) {
+            check(c, txs_get_candidate_ids(c, ids.data(), n, nullptr));
+            check(c, txs_get_candidates(c, cand.data(), n, nullptr));
+        }
+        o.ids.push_back(std::move(ids));
+        o.cand.push_back(std::move(cand));
+    }
+    return o;
+}
+
+SitingResult to_result(const std::vector<txs_step>& steps, int32_t stop, const Owners& o) {
+    SitingResult r;
+    for (const txs_step& s : steps) {
+        size_t k = 0;
+        int64_t li = 0;
+        const int32_t score = o.find(s.index, &k, &li) ? o.cand[k][(size_t)li].score : 0;
+        r.selected.push_back({s.index, {{s.row, s.col}, score}, s.gain, s.coverage});
+    }
+    r.stop_reason = (StopReason)stop;
+    r.final_coverage = r.selected.empty() ? 0.0 : r.selected.back().cumulative_coverage;
+    return r;
+}
+
+// the selected transmitters' viewsheds only (SPEC layout), in step order
+std::vector<Viewshed> selected_viewsheds(const SitingResult& r, const Owners& o, int32_t roi) {
+    const int64_t stride = ((2 * (int64_t)roi + 1) * (2 * (int64_t)roi + 1) + 63) / 64;
+    std::vector<Viewshed> out;
+    std::vector<uint64_t> words((size_t)stride);
+    for (const Selected& s : r.selected) {
+        size_t k = 0;
+        int64_t li = 0;
+        if (!o.find(s.index, &k, &li)) throw Error(TXS_ERR_STATE, "[render] selected id not resident");
+        txs_window w{};
+        check(o.ctx[k], txs_get_viewsheds(o.ctx[k], li, 1, &w, words.data(), stride, nullptr));
+        Viewshed v;
+        v.origin = s.candidate.base;
+        v.roi = roi;
+        v.row0 = w.row0; v.col0 = w.col0; v.h = w.h; v.w = w.w;
+        v.words.assign(words.begin(), words.begin() + ((int64_t)w.h * w.w + 63) / 64);
+        out.push_back(std::move(v));
+    }
+    return out;
+}
+
+void write_dumps(const RunConfig& cfg, const Owners& o, const std::vector<std::pair<int64_t, int64_t>>& bands) {
+    const std::string& d = cfg.out_dir;
+    if (cfg.dump_vix && cfg.observers_random == 0) {   // SPEC.md:201 row-major score bytes
+        std::vector<uint8_t> v((size_t)(cfg.nrows * cfg.ncols));
+        for (size_t k = 0; k < o.ctx.size(); ++k)
+            check(o.ctx[k], txs_get_vix(o.ctx[k], bands[k].first, bands[k].second,
+                                        v.data() + bands[k].first * cfg.ncols));
+        std::ofstream(d + "/vix.u8", std::ios::binary).write(reinterpret_cast<const char*>(v.data()), (std::streamsize)v.size());
+    }
+    // candidates / viewsheds in global id order (ranks hold contiguous id ranges
+    // in band order, or interleaved draw indices: merge by id)
+    std::vector<std::pair<int64_t, std::pair<size_t, int64_t>>> order;
+    for (size_t k = 0; k < o.ids.size(); ++k)
+        for (size_t i = 0; i < o.ids[k].size(); ++i) order.push_back({o.ids[k][i], {k, (int64_t)i}});
+    std::sort(order.begin(), order.end());
+    if (cfg.dump_candidates) {
+        std::ofstream f(d + "/candidates.csv");
+        f << "row,col,score\n";
+        for (const auto& e : order) {
+            const txs_candidate& c = o.cand[e.second.first][(size_t)e.second.second];
+            f << c.row << "," << c.col << "," << c.score << "\n";
+        }
+    }
+    if (cfg.dump_viewsheds) {    // window header + packed words, little-endian
+        const int32_t roi = cfg.params.roi;
+        const int64_t stride = ((2 * (int64_t)roi + 1) * (2 * (int64_t)roi + 1) + 63) / 64;
+        const int64_t chunk = std::max<int64_t>(1, (int64_t)(64 << 20) / (8 * stride));
+        std::ofstream f(d + "/viewsheds.bin", std::ios::binary);
+        std::vector<txs_window> wins;
+        std::vector<uint64_t> words;
+        // ranks' id ranges are each sorted: stream every rank in chunks, emit in id order
+        std::vector<std::vector<std::pair<txs_window, std::vector<uint64_t>>>> cache(o.ctx.size());
+        std::vector<int64_t> cached_from(o.ctx.size(), -1);
+        for (const auto& e : order) {
+            const size_t k = e.second.first;
+            const int64_t li = e.second.second;
+            if (cached_from[k] < 0 || li >= cached_from[k] + (int64_t)cache[k].size()) {
+                const int64_t m = std::min<int64_t>(chunk, (int64_t)o.ids[k].size() - li);
+                wins.resize((size_t)m);
+                words.resize((size_t)(m * stride));
+                check(o.ctx[k], txs_get_viewsheds(o.ctx[k], li, m, wins.data(), words.data(), stride, nullptr));
+                cache[k].clear();
+                for (int64_t i = 0; i < m; ++i) {
+                    const int64_t nw = ((int64_t)wins[(size_t)i].h * wins[(size_t)i].w + 63) / 64;
+                    cache[k].push_back({wins[(size_t)i], std::vector<uint64_t>(words.begin() + i * stride,
+                                                                               words.begin() + i * stride + nw)});
+                }
+                cached_from[k] = li;
+            }
+            const auto& v = cache[k][(size_t)(li - cached_from[k])];
+            const int32_t hdr[4] = {v.first.row0, v.first.col0, v.first.w, v.first.h};
+            f.write(reinterpret_cast<const char*>(hdr), sizeof hdr);
+            f.write(reinterpret_cast<const char*>(v.second.data()), (std::streamsize)(8 * v.second.size()));
+        }
+    }
+}
+
+void write_outputs(const RunConfig& cfg, RunReport& rep, const Owners& o,
+                   const std::vector<std::pair<int64_t, int64_t>>& bands) {
+    if (cfg.out_dir.empty()) return;
+    std::ofstream csv(cfg.out_dir + "/result.csv");
+    if (!csv) throw Error(TXS_ERR_INVALID_ARGUMENT, "[render] unwritable out-dir: " + cfg.out_dir);
+    csv << "rank,row,col,marginal_gain,cumulative_coverage\n";
+    for (size_t k = 0; k < rep.result.selected.size(); ++k) {
+        const Selected& s = rep.result.selected[k];
+        char line[160];
+        std::snprintf(line, sizeof line, "%zu,%lld,%lld,%lld,%.17g\n", k + 1, (long long)s.candidate.base.row,
+                      (long long)s.candidate.base.col, (long long)s.marginal_gain, s.cumulative_coverage);
+        csv << line;
+    }
+    if (cfg.images) render_cumshed(rep.result.cumulative, cfg.out_dir + "/cumshed.pgm");
+    if (!cfg.snapshots.empty()) {
+        SitingResult byrank = rep.result;   // snapshot k = union of the first k selected viewsheds
+        for (size_t k = 0; k < byrank.selected.size(); ++k) byrank.selected[k].index = (int64_t)k;
+        render_snapshots(byrank, selected_viewsheds(rep.result, o, cfg.params.roi), cfg.nrows, cfg.ncols,
+                         cfg.snapshots, cfg.out_dir);
+    }
+    write_dumps(cfg, o, bands);
+    std::ofstream(cfg.out_dir + "/report.txt") << rep.to_string();
+}
+
+RunReport run_single(const RunConfig& cfg) {
     RunReport rep;
     Pipeline pl(cfg.device);
     const double t0 = now_s();
     if (cfg.synth || cfg.input.empty()) pl.generate_fractal(cfg.nrows, cfg.ncols, cfg.roughness, cfg.seed, cfg.zmin, cfg.zmax);
     else pl.set_terrain(load_binary(cfg.input, cfg.nrows, cfg.ncols));
+    if (cfg.water_rows > 0) pl.fill_rows(0, std::min(cfg.water_rows, cfg.nrows), 0);
     txs_synchronize(pl.handle());
     const double t1 = now_s();
-    pl.estimate_vix(cfg.params, cfg.vix_seed);
+    if (cfg.observers_random == 0) pl.estimate_vix(cfg.params, cfg.vix_seed);
     const double t2 = now_s();
-    rep.candidates = pl.find_candidates(cfg.params);
+    rep.candidates = cfg.observers_random > 0 ? pl.random_observers(cfg.observers_random, cfg.observer_seed)
+                                              : pl.find_candidates(cfg.params);
     const double t3 = now_s();
     pl.compute_all_viewsheds(cfg.params);
     const double t4 = now_s();
@@ -417,26 +600,81 @@ RunReport run_pipeline(const RunConfig& cfg) {
     const double t5 = now_s();
     rep.read_s = t1 - t0; rep.vix_s = t2 - t1; rep.findmax_s = t3 - t2; rep.viewshed_s = t4 - t3; rep.site_s = t5 - t4;
     rep.total_s = t5 - t0;
-    if (!cfg.out_dir.empty()) {
-        std::ofstream csv(cfg.out_dir + "/result.csv");
-        csv << "rank,row,col,marginal_gain,cumulative_coverage\n";
-        for (size_t k = 0; k < rep.result.selected.size(); ++k) {
-            const Selected& s = rep.result.selected[k];
-            char line[160];
-            std::snprintf(line, sizeof line, "%zu,%lld,%lld,%lld,%.17g\n", k + 1, (long long)s.candidate.base.row,
-                          (long long)s.candidate.base.col, (long long)s.marginal_gain, s.cumulative_coverage);
-            csv << line;
-        }
-        std::ofstream(cfg.out_dir + "/report.txt") << rep.to_string();
-        render_cumshed(rep.result.cumulative, cfg.out_dir + "/cumshed.pgm");
-        if (!cfg.snapshots.empty()) {
-            int64_t n = 0;
-            txs_get_candidates(pl.handle(), nullptr, 0, &n);
-            render_snapshots(rep.result, download_viewsheds(pl.handle(), cfg.params.roi, n), cfg.nrows, cfg.ncols,
-                             cfg.snapshots, cfg.out_dir);
-        }
-    }
+    const Owners o = owners_of({pl.handle()});
+    txs_stats st{};
+    check(pl.handle(), txs_get_stats(pl.handle(), &st));
+    rep.gpus = 1;
+    rep.device_bytes_peak = st.device_bytes_peak;
+    rep.params_echo = params_echo(cfg, 1);
+    rep.host_bytes_peak = host_rss_peak();
+    write_outputs(cfg, rep, o, {{0, cfg.nrows}});
     return rep;
+}
+
+RunReport run_group(const RunConfig& cfg) {
+    RunReport rep;
+    const int n = (int)cfg.devices.size();
+    txs_group* g = nullptr;
+    txs_status st0 = txs_group_create(n, cfg.devices.data(), &g);
+    if (st0 != TXS_OK) throw Error((int)st0, "txsite: txs_group_create failed (no usable sm_100 devices?)");
+    struct Guard { txs_group* g; ~Guard() { txs_group_destroy(g); } } guard{g};
+    auto gchk = [&](txs_status st) { if (st != TXS_OK) throw Error((int)st, txs_group_last_error(g)); };
+    gchk(txs_group_set_exchange(g, cfg.exchange));
+    const txs_params q = to_params(cfg.params, cfg.vix_seed);
+    const double t0 = now_s();
+    gchk(txs_group_set_grid(g, cfg.nrows, cfg.ncols, &q));
+    if (cfg.synth || cfg.input.empty()) gchk(txs_group_generate_fractal(g, cfg.roughness, cfg.seed, cfg.zmin, cfg.zmax));
+    else gchk(txs_group_set_terrain(g, load_binary(cfg.input, cfg.nrows, cfg.ncols).elevations.data()));
+    if (cfg.water_rows > 0) gchk(txs_group_fill_rows(g, 0, std::min(cfg.water_rows, cfg.nrows), 0));
+    if (cfg.observers_random > 0) gchk(txs_group_random_observers(g, cfg.observers_random, cfg.observer_seed));
+    const double t1 = now_s();
+    std::vector<txs_step> steps;
+    int64_t ns = 0;
+    int32_t stop = 0;
+    double ms[4] = {0, 0, 0, 0};
+    int64_t cap = cfg.params.max_selected > 0 ? cfg.params.max_selected + 1 : 1 << 20;
+    steps.resize((size_t)cap);
+    gchk(txs_group_run_pipeline(g, &q, steps.data(), cap, &ns, &stop, ms));
+    const double t2 = now_s();
+    steps.resize((size_t)std::min(ns, cap));
+    std::vector<txs_ctx*> ctxs;
+    std::vector<std::pair<int64_t, int64_t>> bands;
+    for (int k = 0; k < n; ++k) {
+        ctxs.push_back(txs_group_context(g, k));
+        int64_t a = 0, b = 0;
+        gchk(txs_group_band(g, k, &a, &b));
+        bands.push_back({a, b});
+    }
+    const Owners o = owners_of(ctxs);
+    rep.result = to_result(steps, stop, o);
+    rep.result.cumulative.nrows = cfg.nrows;
+    rep.result.cumulative.ncols = cfg.ncols;
+    rep.result.cumulative.words.resize((size_t)((cfg.nrows * cfg.ncols + 63) / 64));
+    gchk(txs_group_get_cumulative(g, rep.result.cumulative.words.data()));
+    for (const auto& ids : o.ids) rep.candidates += (int64_t)ids.size();
+    // stage times: device time of each stage's slowest band; total: wall clock
+    rep.read_s = t1 - t0; rep.vix_s = ms[0] / 1e3; rep.findmax_s = ms[1] / 1e3; rep.viewshed_s = ms[2] / 1e3;
+    rep.site_s = ms[3] / 1e3;
+    rep.total_s = t2 - t0;
+    rep.gpus = n;
+    for (txs_ctx* c : ctxs) {
+        txs_stats st{};
+        check(c, txs_get_stats(c, &st));
+        rep.device_bytes_peak = std::max(rep.device_bytes_peak, st.device_bytes_peak);
+    }
+    rep.params_echo = params_echo(cfg, n);
+    rep.host_bytes_peak = host_rss_peak();
+    write_outputs(cfg, rep, o, bands);
+    return rep;
+}
+
+}  // namespace
+
+RunReport run_pipeline(const RunConfig& cfg) {
+    if (cfg.devices.size() > 1) return run_group(cfg);
+    RunConfig c = cfg;
+    if (c.devices.size() == 1) c.device = c.devices[0];
+    return run_single(c);
 }
 
 }  // namespace txsite

@@ -13,7 +13,10 @@ static void usage() {
                  "usage: txsite (--input FILE --nrows N --ncols M | --synth [--nrows N --ncols M --seed S --roughness R "
                  "--zmin A --zmax B]) [--roi R] [--tx-height H] [--rx-height H] [--coverage F] [--samples K] "
                  "[--per-block K] [--block-width W] [--max-selected N] [--vix-seed S] [--site-mode 0|1] "
-                 "[--out-dir DIR] [--snapshots a,b,c|pow2] [--threads T (ignored: GPU engine)] [--device D]\n");
+                 "[--out-dir DIR] [--snapshots a,b,c|pow2] [--threads T (ignored: GPU engine)] [--device D] "
+                 "[--water-rows K] [--observers-random N --observer-seed S] [--los-arith fp64|exact] "
+                 "[--gpus N | --devices a,b,...] [--exchange p2p|nccl|host] [--dump-vix] [--dump-candidates] "
+                 "[--dump-viewsheds] [--no-images]\n");
 }
 
 int main(int argc, char** argv) {
@@ -45,6 +48,38 @@ int main(int argc, char** argv) {
         else if (a == "--vix-seed") cfg.vix_seed = std::strtoull(val(), nullptr, 10);
         else if (a == "--out-dir") cfg.out_dir = val();
         else if (a == "--device") cfg.device = std::atoi(val());
+        else if (a == "--water-rows") cfg.water_rows = std::atoll(val());
+        else if (a == "--observers-random") cfg.observers_random = std::atoll(val());
+        else if (a == "--observer-seed") cfg.observer_seed = std::strtoull(val(), nullptr, 10);
+        else if (a == "--los-arith") {
+            const std::string m = val();
+            if (m != "fp64" && m != "exact") { usage(); return 2; }
+            cfg.params.los_arith = m == "exact" ? TXS_LOS_EXACT : TXS_LOS_FP64;
+        } else if (a == "--gpus") {
+            const int n = std::atoi(val());
+            cfg.devices.clear();
+            for (int k = 0; k < n; ++k) cfg.devices.push_back(k);
+        } else if (a == "--devices") {   // e.g. 0,0 : two row bands on device 0 (testing)
+            const std::string d = val();
+            cfg.devices.clear();
+            size_t p = 0;
+            while (p < d.size()) {
+                size_t q = d.find(',', p);
+                if (q == std::string::npos) q = d.size();
+                cfg.devices.push_back(std::atoi(d.substr(p, q - p).c_str()));
+                p = q + 1;
+            }
+        } else if (a == "--exchange") {
+            const std::string m = val();
+            if (m == "p2p") cfg.exchange = TXS_XCHG_P2P;
+            else if (m == "nccl") cfg.exchange = TXS_XCHG_NCCL;
+            else if (m == "host") cfg.exchange = TXS_XCHG_HOST;
+            else { usage(); return 2; }
+        }
+        else if (a == "--no-images") cfg.images = false;
+        else if (a == "--dump-vix") cfg.dump_vix = true;
+        else if (a == "--dump-candidates") cfg.dump_candidates = true;
+        else if (a == "--dump-viewsheds") cfg.dump_viewsheds = true;
         else if (a == "--threads") (void)val();
         else if (a == "--snapshots") {
             const std::string s = val();
