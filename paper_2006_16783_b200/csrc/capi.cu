@@ -612,12 +612,20 @@ txs_status txs_set_viewsheds(txs_ctx* c, int32_t roi, int64_t n, const int32_t* 
     std::vector<int32_t> pop(n);
     for (int64_t i = 0; i < n; ++i) {
         const txs_window& x = wins[i];
-        if (x.row0 < 0 || x.col0 < 0 || x.h < 1 || x.w < 1 || x.row0 + x.h > c->nrows || x.col0 + x.w > c->ncols ||
-            x.h > 2 * roi + 1 || x.w > 2 * roi + 1)
-            return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "window out of bounds");
+        if (rows[i] < 0 || rows[i] >= c->nrows || cols[i] < 0 || cols[i] >= c->ncols)
+            return fail(c, TXS_ERR_OFF_GRID, "site", "viewshed origin off the grid");
+        // the window must be the origin's clipped disk box: the SITE
+        // neighbour search (buckets of side roi, +-2roi around a winner) relies on it
+        const int64_t r0 = std::max<int64_t>(0, rows[i] - roi), c0 = std::max<int64_t>(0, cols[i] - roi);
+        const int64_t r1 = std::min<int64_t>(c->nrows - 1, rows[i] + roi), c1 = std::min<int64_t>(c->ncols - 1, cols[i] + roi);
+        if (x.row0 != r0 || x.col0 != c0 || x.h != r1 - r0 + 1 || x.w != c1 - c0 + 1)
+            return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "window is not the origin's clipped roi box");
         cand[i] = txs_candidate{rows[i], cols[i], 0, 0};
         w[i] = make_int4(x.row0, x.col0, x.h, x.w);
         const int64_t nw = ((int64_t)x.h * x.w + 63) / 64;
+        const int tail = (int)(((int64_t)x.h * x.w) & 63);
+        if (tail && (words[i * stride + nw - 1] >> tail) != 0)
+            return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "padding bits past h*w must be zero");
         int64_t pc = 0;
         for (int64_t k = 0; k < nw; ++k) pc += __builtin_popcountll(words[i * stride + k]);
         pop[i] = (int32_t)pc;

@@ -848,14 +848,21 @@ int blocks_for(int64_t work, int per_block, int cap) {
 // bucket's cum region fits two CTAs per SM (roi <= ~280) -- measured: C5 (244
 // per bucket) 4.26 -> 4.97 TB/s; C2 (39) and C3 (5) stream faster with
 // k_gain_full, which reads each candidate's cum words from L2.
-template <typename G>
-static void launch_gain_pass(txs_ctx* c, const SiteArgs& a, const SiteState* st, const uint64_t* cum, G* gain,
-                             unsigned long long* counters, bool buckets) {
+static bool gain_tiled(const SiteArgs& a, bool buckets, size_t* smem_out) {
     const int64_t rows = (int64_t)a.bsize + 2 * a.R;
     const int64_t pw = (a.bsize + 2 * (int64_t)a.R + 63) / 64 + 1;
     const size_t smem = sizeof(uint64_t) * (size_t)(rows * pw);
     const bool dense = a.n >= 64 * (int64_t)a.nbx * a.nby;
-    if (buckets && dense && smem <= 110 * 1024 && !getenv("TXS_GAIN_REG")) {
+    *smem_out = smem;
+    return buckets && dense && smem <= 110 * 1024 && !getenv("TXS_GAIN_REG");
+}
+
+template <typename G>
+static void launch_gain_pass(txs_ctx* c, const SiteArgs& a, const SiteState* st, const uint64_t* cum, G* gain,
+                             unsigned long long* counters, bool buckets) {
+    size_t smem = 0;
+    const bool tiled = gain_tiled(a, buckets, &smem);
+    if (tiled) {
         auto kern = k_gain_tiled<G>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         const int64_t nbk = (int64_t)a.nbx * a.nby;

@@ -29,9 +29,12 @@ STOP_TARGET, STOP_ZERO, STOP_EXHAUSTED, STOP_MAX = "target-reached", "zero-gain"
 
 def plan_bands(nrows, block, world):
     """Split the ceil(nrows/block) FINDMAX block rows over `world` ranks as
-    evenly as possible; returns [(row_begin, row_end)] (empty when world exceeds
-    the block rows)."""
+    evenly as possible; returns [(row_begin, row_end)].  A world larger than
+    the block rows is rejected: a rank without a band would leave its peers
+    blocked in the per-round collectives (txs_plan_bands refuses it likewise)."""
     nb = -(-nrows // block)
+    if world < 1 or world > nb:
+        raise ValueError(f"{world} ranks > {nb} FINDMAX block rows ({nrows} rows / block {block})")
     base, extra = divmod(nb, world)
     out, b = [], 0
     for k in range(world):

@@ -394,6 +394,29 @@ def test_set_viewsheds_then_site(engine):
     assert np.array_equal(engine.cumulative(), o["cum"])
 
 
+def test_set_viewsheds_rejects_malformed_windows(engine):
+    """Injected windows must be the origin's clipped roi box (the
+    SITE neighbour search relies on it) with zero padding bits."""
+    T = _T()
+    z = O.generate_fractal(128, 128, 0.5, 3, 0, 1000)
+    rows, cols = np.array([5, 64], np.int32), np.array([70, 64], np.int32)
+    ow, ov = O.viewsheds(z, 10, 5, 5, rows, cols)
+    engine.set_terrain(z)
+    engine.set_viewsheds(10, rows, cols, ow, ov)          # well-formed: accepted
+    shifted = ow.copy()
+    shifted[1, 1] += 1                                     # off-centre window
+    with pytest.raises(T.TxsError, match="clipped roi box"):
+        engine.set_viewsheds(10, rows, cols, shifted, ov)
+    dirty = ov.copy()
+    nbits = int(ow[0, 2]) * int(ow[0, 3])
+    assert nbits % 64
+    dirty[0, nbits // 64] |= np.uint64(1) << np.uint64(63)   # a padding bit past h*w
+    with pytest.raises(T.TxsError, match="padding bits"):
+        engine.set_viewsheds(10, rows, cols, ow, dirty)
+    with pytest.raises(T.TxsError, match="off the grid"):
+        engine.set_viewsheds(10, np.array([128], np.int32), np.array([3], np.int32), ow[:1], ov[:1])
+
+
 # ---- pipeline ---------------------------------------------------------------------
 def test_run_pipeline_c1_matches_oracle(engine, c1):
     """run_pipeline on config 1 end to end vs the oracle stages."""

@@ -30,6 +30,8 @@ def test_plan_bands_matches_python(nrows, block, world):
 def test_plan_bands_rejects_empty_bands():
     with pytest.raises(T.TxsError):
         T.plan_bands(1000, 100, 11)   # 10 block rows, 11 ranks: a rank would own nothing
+    with pytest.raises(ValueError):
+        py_plan_bands(1000, 100, 11)   # shard.py refuses it too (its peers would block in the collectives)
 
 
 def _oracle_pipeline(z, roi, h, S, bw, k, target, max_sel, seed, observers=None):

@@ -65,7 +65,8 @@ def test_plan_bands():
     assert plan_bands(46400, 400, 8) == [(0, 6000), (6000, 12000), (12000, 18000), (18000, 24000),
                                         (24000, 29600), (29600, 35200), (35200, 40800), (40800, 46400)]
     assert plan_bands(1000, 100, 8)[-1] == (900, 1000)
-    assert plan_bands(100, 100, 3) == [(0, 100), (100, 100), (100, 100)]
+    with pytest.raises(ValueError):           # a rank without a band is refused
+        plan_bands(100, 100, 3)
     for nr, b, w in [(4096, 128, 8), (16384, 256, 5), (1000, 7, 6)]:
         bands = plan_bands(nr, b, w)
         assert bands[0][0] == 0 and bands[-1][1] == nr
