@@ -367,7 +367,7 @@ class Group:
         self._h = h
         self.n = len(devs)
         if exchange is not None:
-            self._chk(N.lib.txs_group_set_exchange(self._h, N.EXCHANGE[exchange]))
+            self.set_exchange(exchange)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -390,6 +390,14 @@ class Group:
             raise TxsError(st, N.lib.txs_group_last_error(self._h).decode())
 
     def set_exchange(self, name):
+        if name == "nccl":
+            # the engine dlopens libnccl.so.2 on first NCCL use and reuses a copy
+            # already in the process: load torch's (newer) one first where torch is
+            # installed, so a later `import torch` does not meet an older NCCL
+            try:
+                import torch  # noqa: F401
+            except ImportError:
+                pass
         self._chk(N.lib.txs_group_set_exchange(self._h, N.EXCHANGE[name]))
 
     def set_grid(self, nrows, ncols, params):

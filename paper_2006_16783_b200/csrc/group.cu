@@ -53,7 +53,12 @@ NcclApi& nccl() {
     static NcclApi a;
     if (a.tried) return a;
     a.tried = true;
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    // TXS_NCCL_LIB names a library explicitly; else a libnccl.so.2 already in the
+    // process (torch's) is reused; else the system one is loaded
+    void* h = nullptr;
+    if (const char* e = getenv("TXS_NCCL_LIB")) h = dlopen(e, RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
     if (!h) return a;
     a.CommInitAll = (decltype(a.CommInitAll))dlsym(h, "ncclCommInitAll");
     a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
