@@ -108,6 +108,10 @@ typedef struct txs_stats {
      * candidates, viewsheds, bitmaps, SITE state): now, and the high-water mark
      * since creation (RunReport's peak memory estimate) */
     int64_t device_bytes, device_bytes_peak;
+    /* persistent SITE loop, CTA 0's device time per phase over the whole loop
+     * (set with TXS_SITE_PROFILE=1, else 0): winner reduction, commit of the
+     * previous winner, neighbour updates, partial argmax, grid barrier */
+    int64_t site_phase_ns[5];
 } txs_stats;
 
 typedef struct txs_ctx txs_ctx;

@@ -54,7 +54,8 @@ class Stats(C.Structure):
                 ("site_bytes", i64), ("site_launches", i64), ("candidates", i64),
                 ("kernel_launches", i64), ("ms_site_rounds", dbl),
                 ("vix_fp64_ties", i64), ("vix_fp64_flips", i64), ("vs_fp64_ties", i64), ("vs_fp64_flips", i64),
-                ("ms_vix_kernel", dbl), ("ms_viewshed_kernel", dbl), ("device_bytes", i64), ("device_bytes_peak", i64)]
+                ("ms_vix_kernel", dbl), ("ms_viewshed_kernel", dbl), ("device_bytes", i64), ("device_bytes_peak", i64),
+                ("site_phase_ns", i64 * 5)]
 
 
 def _sig(name, res, args):

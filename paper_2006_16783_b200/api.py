@@ -317,7 +317,8 @@ class Engine:
     def stats(self):
         s = N.Stats()
         self._chk(N.lib.txs_get_stats(self._h, C.byref(s)))
-        return {k: getattr(s, k) for k, _ in N.Stats._fields_}
+        return {k: (list(getattr(s, k)) if isinstance(getattr(s, k), C.Array) else getattr(s, k))
+                for k, _ in N.Stats._fields_}
 
     def reset_stats(self):
         self._chk(N.lib.txs_reset_stats(self._h))

@@ -111,6 +111,7 @@ txs_status txs_create(int device, txs_ctx** out) {
         return TXS_ERR_CUDA;
     }
     cudaMemset(c->d_counters, 0, sizeof(unsigned long long) * kNumCounters);
+    std::memset(c->h_state, 0, sizeof(SiteState));
     *out = c;
     return TXS_OK;
 }
@@ -185,6 +186,7 @@ txs_status txs_get_stats(txs_ctx* c, txs_stats* out) {
     out->vs_fp64_flips = (int64_t)h[kVsTiesFlipped];
     out->candidates = c->ncand;
     out->kernel_launches = c->launches;
+    for (int k = 0; k < 5; ++k) out->site_phase_ns[k] = (int64_t)c->h_state->phase_ns[k];
     out->device_bytes = c->dev_bytes;
     out->device_bytes_peak = c->dev_bytes_peak;
     return TXS_OK;

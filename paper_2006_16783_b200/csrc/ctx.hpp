@@ -63,6 +63,7 @@ struct SiteState {
     int nb_start[kMaxNb];
     int nb_pref[kMaxNb + 1];
     unsigned long long shard_key;  // sharded SITE: local best key
+    unsigned long long phase_ns[5];   // k_site_loop1 phases (TXS_SITE_PROFILE=1): winner, commit, update, partial, barrier
 };
 
 // device counter slots

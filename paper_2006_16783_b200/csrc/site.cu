@@ -44,7 +44,14 @@ struct SiteArgs {
     int dpitch;                       // delta window row pitch (words)
     int64_t wpr, n, stride, max_sel;
     double target, total;
+    int prof;                         // k_site_loop1: accumulate per-phase device time (TXS_SITE_PROFILE=1)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 __global__ void k_init_gains(const int32_t* __restrict__ pop, int32_t* __restrict__ gain, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -475,6 +482,11 @@ __global__ void __launch_bounds__(kL1Threads, 1) k_site_loop1(SiteArgs a, SiteSt
     SitePart prev{};
     int64_t prev_idx = 0;
     unsigned long long bytes_all = 0;
+    const bool prof = a.prof && cta == 0 && tid == 0;
+    unsigned long long ph[5] = {0, 0, 0, 0, 0}, tp = prof ? gtimer() : 0;
+    auto mark = [&](int k) {
+        if (prof) { const unsigned long long t = gtimer(); ph[k] += t - tp; tp = t; }
+    };
     for (int it = 0;; ++it) {
         const SitePart* pb = parts + (size_t)(it & 1) * G;
         SitePart* pn = parts + (size_t)((it + 1) & 1) * G;
@@ -487,8 +499,10 @@ __global__ void __launch_bounds__(kL1Threads, 1) k_site_loop1(SiteArgs a, SiteSt
         __syncthreads();
         best = s_part[0];
         for (int k = 1; k < kL1Threads / 32; ++k) part_max(best, s_part[k]);
+        mark(0);
         // ---- 2. commit of the previous winner (rows spread over the CTAs)
         if (have_prev) flush_rows(a, prev, words + prev_idx * a.stride, cum, cta, G);
+        mark(1);
         const int g = (int)(best.key >> 32);
         const int64_t idx = (int64_t)(0xffffffffull - (best.key & 0xffffffffull));
         if (nsel >= a.n) { stop = TXS_STOP_EXHAUSTED; break; }
@@ -569,13 +583,18 @@ __global__ void __launch_bounds__(kL1Threads, 1) k_site_loop1(SiteArgs a, SiteSt
             bytes_all += 16ull * (unsigned long long)total;
         }
         __syncthreads();
+        mark(2);
         // ---- 4. new partial -> barrier
         write_partial(pn);
+        mark(3);
         prev = best;
         prev_idx = idx;
         have_prev = true;
         grid.sync();
+        mark(4);
     }
+    if (prof)
+        for (int k = 0; k < 5; ++k) st->phase_ns[k] = ph[k];
     for (int j = tid; j < m; j += blockDim.x) gain[cta + (int64_t)G * j] = s_gain[j];
     if (tid == 0 && bytes_all) atomicAdd(counters + kSiteBytes, bytes_all);
     if (cta == 0 && tid == 0) {
@@ -830,6 +849,7 @@ SiteArgs make_args(txs_ctx* c, const txs_params& p) {
     a.total = (double)c->nrows * (double)c->ncols;
     a.cr0 = (int)c->cum_r0; a.cr1 = (int)c->cum_r1;
     a.dpitch = (int)c->dpitch;
+    a.prof = getenv("TXS_SITE_PROFILE") ? 1 : 0;
     return a;
 }
 
