@@ -455,23 +455,36 @@ __global__ void __launch_bounds__(kL1Threads, 1) k_site_loop1(SiteArgs a, SiteSt
     }
     __syncthreads();
     // partial argmax of the owned gains -> parts[buf][cta]
+    // (keys alone travel through the shuffles; the owner of the best key then
+    // writes the payload from shared memory)
+    __shared__ unsigned long long s_key[kL1Threads / 32];
+    __shared__ int s_kj[kL1Threads / 32];
     auto write_partial = [&](SitePart* buf) {
-        SitePart b{0ull, 0, 0, 0, 0, 0, 0};
+        unsigned long long bk = 0ull;
+        int bj = -1;
         for (int j = tid; j < m; j += blockDim.x) {
             const int64_t i = cta + (int64_t)G * j;
             const unsigned long long key = ((unsigned long long)(uint32_t)s_gain[j] << 32) | (0xffffffffull - (uint64_t)i);
-            if (key > b.key) {
-                const int4 wv = s_win[j];
-                b = SitePart{key, s_rc[j].x, s_rc[j].y, wv.x, wv.y, wv.z, wv.w};
-            }
+            if (key > bk) { bk = key; bj = j; }
         }
-        for (int o = 16; o; o >>= 1) part_max(b, shfl_part(b, o));
-        if (lane == 0) s_part[warp] = b;
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long k2 = __shfl_xor_sync(kFull, bk, o);
+            const int j2 = __shfl_xor_sync(kFull, bj, o);
+            if (k2 > bk) { bk = k2; bj = j2; }
+        }
+        if (lane == 0) { s_key[warp] = bk; s_kj[warp] = bj; }
         __syncthreads();
         if (tid == 0) {
-            SitePart x = s_part[0];
-            for (int k = 1; k < kL1Threads / 32; ++k) part_max(x, s_part[k]);
-            buf[cta] = x;
+            unsigned long long x = s_key[0];
+            int xj = s_kj[0];
+            for (int k = 1; k < kL1Threads / 32; ++k)
+                if (s_key[k] > x) { x = s_key[k]; xj = s_kj[k]; }
+            SitePart out{0ull, 0, 0, 0, 0, 0, 0};
+            if (xj >= 0) {
+                const int4 wv = s_win[xj];
+                out = SitePart{x, s_rc[xj].x, s_rc[xj].y, wv.x, wv.y, wv.z, wv.w};
+            }
+            buf[cta] = out;
         }
     };
     write_partial(parts);
@@ -492,19 +505,34 @@ __global__ void __launch_bounds__(kL1Threads, 1) k_site_loop1(SiteArgs a, SiteSt
         SitePart* pn = parts + (size_t)((it + 1) & 1) * G;
         // ---- 1. global winner (redundantly in every CTA)
         SitePart best{0ull, 0, 0, 0, 0, 0, 0};
-        for (int k = tid; k < G; k += blockDim.x) part_max(best, pb[k]);
-        for (int o = 16; o; o >>= 1) part_max(best, shfl_part(best, o));
-        __syncthreads();   // s_part reuse
-        if (lane == 0) s_part[warp] = best;
-        __syncthreads();
-        best = s_part[0];
-        for (int k = 1; k < kL1Threads / 32; ++k) part_max(best, s_part[k]);
+        {
+            unsigned long long bk = 0ull;
+            int bk_k = -1;
+            for (int k = tid; k < G; k += blockDim.x) {
+                const unsigned long long key = pb[k].key;
+                if (key > bk) { bk = key; bk_k = k; }
+            }
+            for (int o = 16; o; o >>= 1) {
+                const unsigned long long k2 = __shfl_xor_sync(kFull, bk, o);
+                const int i2 = __shfl_xor_sync(kFull, bk_k, o);
+                if (k2 > bk) { bk = k2; bk_k = i2; }
+            }
+            __syncthreads();   // s_key / s_part reuse
+            if (lane == 0) { s_key[warp] = bk; s_kj[warp] = bk_k; }
+            __syncthreads();
+            unsigned long long x = s_key[0];
+            int xk = s_kj[0];
+            for (int k = 1; k < kL1Threads / 32; ++k)
+                if (s_key[k] > x) { x = s_key[k]; xk = s_kj[k]; }
+            if (xk >= 0) best = pb[xk];   // one 32-byte read, L1/L2 hit (the partials were just read)
+        }
         mark(0);
-        // ---- 2. commit of the previous winner (rows spread over the CTAs)
-        if (have_prev) flush_rows(a, prev, words + prev_idx * a.stride, cum, cta, G);
         mark(1);
         const int g = (int)(best.key >> 32);
         const int64_t idx = (int64_t)(0xffffffffull - (best.key & 0xffffffffull));
+        // a stop ends the loop before this round's end-of-round commit of w_{r-1}: do it here
+        const bool stop_now = nsel >= a.n || g <= 0;
+        if (stop_now && have_prev) flush_rows(a, prev, words + prev_idx * a.stride, cum, cta, G);
         if (nsel >= a.n) { stop = TXS_STOP_EXHAUSTED; break; }
         if (g <= 0) { stop = TXS_STOP_ZERO_GAIN; break; }
         covered += g;
@@ -514,6 +542,7 @@ __global__ void __launch_bounds__(kL1Threads, 1) k_site_loop1(SiteArgs a, SiteSt
         const uint64_t* vw = words + idx * a.stride;
         if (cov >= a.target || (a.max_sel > 0 && nsel >= a.max_sel)) {
             stop = cov >= a.target ? TXS_STOP_TARGET_REACHED : TXS_STOP_MAX_SELECTED;
+            if (have_prev) flush_rows(a, prev, words + prev_idx * a.stride, cum, cta, G);
             flush_rows(a, best, vw, cum, cta, G);   // the final commit
             break;
         }
@@ -584,8 +613,12 @@ __global__ void __launch_bounds__(kL1Threads, 1) k_site_loop1(SiteArgs a, SiteSt
         }
         __syncthreads();
         mark(2);
-        // ---- 4. new partial -> barrier
+        // ---- 4. new partial, then the commit of the previous winner (its rows
+        // spread over the CTAs; it overlaps the wait for the slowest CTA, and
+        // every commit of w_{r-1} lands before barrier r, ahead of round r+1's
+        // updates, which compensate only for w_r) -> barrier
         write_partial(pn);
+        if (have_prev) flush_rows(a, prev, words + prev_idx * a.stride, cum, cta, G);
         mark(3);
         prev = best;
         prev_idx = idx;
