@@ -605,8 +605,9 @@ def run_b200_sharded(args, cfg):
     clk = clocks.stop()
     st = eng.stats()
     # stage times: max over ranks; work units: summed over the bands
+    extra_iters = 0 if res.get("rounds_mode") == "replicated" else args.steps * len(res["index"])
     tm = torch.tensor([st["ms_vix"], st["ms_findmax"], st["ms_viewshed"], st["ms_site"] + site_ms,
-                       st["site_iterations"] + args.steps * len(res["index"]), st["ms_vix_kernel"],
+                       st["site_iterations"] + extra_iters, st["ms_vix_kernel"],
                        st["ms_viewshed_kernel"]], device=dev, dtype=torch.float64)
     dist.all_reduce(tm, op=dist.ReduceOp.MAX)
     tc = torch.tensor([st["vix_crossings_full"], st["viewshed_crossings"], st["site_bytes"]], device=dev,

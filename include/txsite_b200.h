@@ -266,6 +266,26 @@ txs_status txs_site_shard_select_dev(txs_ctx* ctx, const uint64_t* d_gathered, i
 txs_status txs_site_shard_result(txs_ctx* ctx, txs_step* steps, int64_t cap, int64_t* nsteps, int32_t* stop_reason);
 /* The context's CUDA stream (a cudaStream_t), for ordering external work with it. */
 void* txs_stream(txs_ctx* ctx);
+
+/* ---- replicated SITE over gathered viewsheds -------------------
+ * The other multi-GPU SITE form: one allgather of every band's candidates and
+ * packed viewsheds, then the single-GPU SITE loop (no collective per round) on
+ * the gathered set -- the same picks, bit for bit, since the gathered set IS the
+ * single-GPU candidate list.  A record is txs_viewshed_record_words(roi) u64:
+ *   [0] global candidate id (-1: padding)   [1] row | col << 32
+ *   [2..3] window {row0, col0, h, w} (int32) [4] popcount
+ *   [5..] the engine's cum-aligned row words (txs_viewsheds_device layout)
+ * txs_viewsheds_pack writes the context's resident viewsheds as `slots`
+ * records into a device buffer (padding past its count), stream-ordered on
+ * txs_stream (for collectives issued there). */
+int64_t txs_viewshed_record_words(int32_t roi);
+txs_status txs_viewsheds_pack(txs_ctx* ctx, int64_t slots, uint64_t* d_records, int64_t* n_out);
+/* SITE (p's stop rules) on `nrec` gathered records holding the
+ * n_total candidates of the whole grid (each placed at its global id).  The
+ * context's own candidates and viewsheds are replaced; afterwards
+ * txs_get_cumulative returns the whole grid's cumulative viewshed. */
+txs_status txs_site_gathered(txs_ctx* ctx, const txs_params* p, int64_t nrec, int64_t n_total, const uint64_t* d_records,
+                             txs_step* steps, int64_t cap, int64_t* nsteps, int32_t* stop_reason);
 /* OR the bits of global rows [row_begin, row_end) of the context's cumulative
  * viewshed (the held cum rows; rows outside them read as 0) into `dense_out`,
  * the caller's SPEC-dense bitmap of the WHOLE grid ((nrows*ncols+63)/64 words,

@@ -67,6 +67,11 @@ def device_ok():
     return bool(N.lib.txs_device_ok())
 
 
+def record_words(roi):
+    """u64 words per gathered viewshed record (txs_viewshed_record_words)."""
+    return int(N.lib.txs_viewshed_record_words(roi))
+
+
 def max_words(roi):
     s = 2 * roi + 1
     return (s * s + 63) // 64
@@ -158,6 +163,11 @@ class Engine:
         n = C.c_int64()
         self._chk(N.lib.txs_find_candidates(self._h, C.byref(params), C.byref(n), None, 0))
         return self.candidates() if copy else n.value
+
+    def num_candidates(self):
+        n = C.c_int64()
+        self._chk(N.lib.txs_get_candidates(self._h, None, 0, C.byref(n)))
+        return n.value
 
     def candidates(self):
         n = C.c_int64()
@@ -298,6 +308,23 @@ class Engine:
         d = _steps_dict(steps, min(ns.value, cap), 0)
         d["stop"] = STOP[stop.value] if stop.value >= 0 else None
         return d
+
+    # ---- replicated SITE over gathered viewsheds ---------------------
+    def viewsheds_pack(self, slots, d_records):
+        """Resident viewsheds as `slots` records (txs_viewshed_record_words u64
+        each) into the device buffer at d_records (stream-ordered); returns the
+        record count."""
+        n = C.c_int64()
+        self._chk(N.lib.txs_viewsheds_pack(self._h, slots, C.c_void_p(d_records), C.byref(n)))
+        return n.value
+
+    def site_gathered(self, params, nrec, n_total, d_records, cap=None):
+        cap = n_total + 1 if cap is None else cap
+        steps = (N.Step * max(cap, 1))()
+        ns, stop = C.c_int64(), C.c_int32()
+        self._chk(N.lib.txs_site_gathered(self._h, C.byref(params), nrec, n_total, C.c_void_p(d_records), steps, cap,
+                                          C.byref(ns), C.byref(stop)))
+        return _steps_dict(steps, min(ns.value, cap), stop.value)
 
     def stream(self):
         return N.lib.txs_stream(self._h)

@@ -927,6 +927,63 @@ txs_status txs_site_shard_result(txs_ctx* c, txs_step* steps, int64_t cap, int64
 
 void* txs_stream(txs_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
+int64_t txs_viewshed_record_words(int32_t roi) { return roi >= 1 ? kRecHead + aligned_stride(roi) : 0; }
+
+txs_status txs_viewsheds_pack(txs_ctx* c, int64_t slots, uint64_t* d_rec, int64_t* n_out) {
+    if (!c || slots < 0 || (slots > 0 && !d_rec)) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->vs_valid) return fail(c, TXS_ERR_STATE, "viewshed", "no viewsheds");
+    if (slots < c->vs_n) return fail(c, TXS_ERR_INVALID_ARGUMENT, "viewshed", "fewer record slots than viewsheds");
+    cudaSetDevice(c->device);
+    if (!c->h_cgid.empty()) {   // sharded observers: their global draw indices on the device
+        if (ensure(c, "site", (void**)&c->d_cgid, &c->cgid_cap, sizeof(int32_t) * c->h_cgid.size()) != TXS_OK)
+            return TXS_ERR_OUT_OF_MEMORY;
+        TXS_CUDA(c, "site", cudaMemcpyAsync(c->d_cgid, c->h_cgid.data(), sizeof(int32_t) * c->h_cgid.size(),
+                                            cudaMemcpyHostToDevice, c->stream));
+    }
+    if (n_out) *n_out = c->vs_n;
+    return pack_records(c, slots, d_rec);
+}
+
+txs_status txs_site_gathered(txs_ctx* c, const txs_params* p, int64_t nrec, int64_t n_total, const uint64_t* d_rec,
+                             txs_step* steps, int64_t cap, int64_t* nsteps, int32_t* stop) {
+    if (!c || !p || nrec < 0 || n_total < 0 || (nrec > 0 && !d_rec)) return TXS_ERR_INVALID_ARGUMENT;
+    if (!c->d_z) return fail(c, TXS_ERR_STATE, "site", "no grid");
+    if (p->roi < 1 || p->roi > 4000) return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "roi out of range");
+    if (!(p->target_coverage > 0.0) || p->target_coverage > 1.0)
+        return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "target_coverage must be in (0,1]");
+    if (p->max_selected < 0) return fail(c, TXS_ERR_INVALID_ARGUMENT, "site", "max_selected < 0");
+    if (n_total >= 0x7fffffff) return fail(c, TXS_ERR_RANGE, "site", "too many candidates");
+    cudaSetDevice(c->device);
+    TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+    StageTimer t(c, &c->stats.ms_site);
+    const int64_t stride = aligned_stride(p->roi);
+    if (alloc_cands(c, n_total) != TXS_OK ||
+        ensure(c, "site", (void**)&c->d_words, &c->words_cap, sizeof(uint64_t) * (size_t)(n_total * stride + 8)) != TXS_OK ||
+        ensure(c, "site", (void**)&c->d_win, &c->win_cap, sizeof(int4) * (size_t)std::max<int64_t>(1, n_total)) != TXS_OK ||
+        ensure(c, "site", (void**)&c->d_pop, &c->pop_cap, sizeof(int32_t) * (size_t)std::max<int64_t>(1, n_total)) != TXS_OK)
+        return fail(c, TXS_ERR_OUT_OF_MEMORY, "site", "cannot hold the gathered viewsheds");
+    c->ncand = n_total;
+    c->cand_gid0 = 0;
+    c->h_cgid.clear();
+    c->vs_roi = p->roi;
+    c->vs_n = n_total;
+    c->vs_stride = stride;
+    c->cand_valid = c->vs_valid = true;
+    txs_status st = unpack_records(c, nrec, d_rec);
+    if (st != TXS_OK) return st;
+    std::vector<txs_step> v;
+    int32_t sr = 0;
+    st = run_site(c, *p, v, &sr);   // the whole grid's cum, the single-GPU loop
+    if (st != TXS_OK) return st;
+    st = t.stop("site");
+    if (st != TXS_OK) return st;
+    c->site_valid = true;
+    if (nsteps) *nsteps = (int64_t)v.size();
+    if (stop) *stop = sr;
+    if (steps) std::copy(v.begin(), v.begin() + std::min<int64_t>(cap, (int64_t)v.size()), steps);
+    return TXS_OK;
+}
+
 txs_status txs_get_cumulative_rows(txs_ctx* c, int64_t rb, int64_t re, uint64_t* out) {
     if (!c || !out) return TXS_ERR_INVALID_ARGUMENT;
     if (!c->site_valid) return fail(c, TXS_ERR_STATE, "site", "no cumulative viewshed (run site first)");

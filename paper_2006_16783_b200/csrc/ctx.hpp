@@ -225,6 +225,11 @@ txs_status shard_site_select_dev(txs_ctx*, const uint64_t* d_gathered, int32_t n
 txs_status shard_site_select_peers(txs_ctx*, const uint64_t* const* d_mail, int32_t nranks, uint64_t* d_key,
                                    uint64_t* d_payload);
 txs_status download_cum_rows(txs_ctx*, int64_t row_begin, int64_t row_end, uint64_t* host_dense);
+// replicated SITE: resident viewsheds -> records; gathered records -> the
+// context's candidate / viewshed arrays at their global ids
+constexpr int kRecHead = 5;
+txs_status pack_records(txs_ctx*, int64_t slots, uint64_t* d_rec);
+txs_status unpack_records(txs_ctx*, int64_t nrec, const uint64_t* d_rec);
 
 }  // namespace txs
 

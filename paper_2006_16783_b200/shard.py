@@ -15,6 +15,11 @@ allgather delivers every rank's entry, and each rank selects the largest key
 the window into its held cumulative rows and updates its local gains.  Stop
 rules (decision D9) are evaluated identically on every rank from that key.
 
+The default with device rounds (TXS_SHARD_EXCHANGE=replicate) needs no
+collective per round at all: one allgather of every band's packed viewsheds,
+then every rank runs the single-GPU SITE loop (~6 us per round at roi 100,
+against a collective's latency per round) on the gathered set.
+
 `ranks` is the list of (engine, band index) pairs this process drives: one per
 process with TorchComm over NCCL (one GPU each), or several on one device with
 LocalComm (the single-GPU emulation the tests use).  An "engine" is anything
@@ -196,12 +201,20 @@ def run_sharded(ranks, comm, cfg, params, nbands, setup=True, with_cum=True, dev
             eng.set_candidate_base(int(prefix[k]))
         total_cand = int(counts.sum())
     # ---- VIEWSHED per band --------------------------------------------------------
+    mode = os.environ.get("TXS_SHARD_EXCHANGE") or "replicate"
+    replicate = device_rounds and mode == "replicate"
     for eng, _ in active:
         eng.compute_all_viewsheds(params)
-        eng.site_shard_begin(params)
-    # ---- SITE rounds ----------------------------------------------------------------
+        if not replicate:
+            eng.site_shard_begin(params)
+    # ---- SITE ---------------------------------------------------------------------------
+    if replicate:
+        out = _replicated_site(active, comm, params, total_cand)
+        if with_cum:
+            out["cum"] = active[0][0].cumulative()   # every rank holds the whole grid's cum
+        return out
     if device_rounds:
-        out = _device_rounds(active, comm, total_cand)
+        out = _device_rounds(active, comm, total_cand, mode)
         if not with_cum:
             return out
         return _with_cum(out, active, comm, bands, nr, nc)
@@ -268,7 +281,43 @@ def _with_cum(out, active, comm, bands, nr, nc):
     return out
 
 
-def _device_rounds(active, comm, total_cand, poll_every=16):
+def _replicated_site(active, comm, params, total_cand):
+    """SITE without a collective per round: one allgather of every band's
+    candidates and packed viewsheds (records of txs_viewshed_record_words), then
+    the single-GPU SITE loop on the gathered set on every rank -- the same picks
+    bit for bit (the gathered set is the single-GPU candidate list, each entry
+    at its global id).  site_ms = device time of the pack + allgather (the
+    engine's own SITE stage timer covers the rest)."""
+    import torch
+    from .api import record_words
+    engines = [e for e, _ in active]
+    rw = record_words(params.roi)
+    n_local = max(e.num_candidates() for e in engines)
+    n_max = max(1, int(comm.allgather_i64(np.array([n_local], np.int64)).max()))
+    nranks = getattr(comm, "world", 1) if len(engines) == 1 else len(engines)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    torch.cuda.synchronize()
+    engines[0].event_record(12)
+    sends = [torch.empty(n_max * rw, dtype=torch.int64, device=dev) for _ in engines]
+    for e, sd in zip(engines, sends):
+        e.viewsheds_pack(n_max, sd.data_ptr())
+    recvs = [torch.empty(nranks * n_max * rw, dtype=torch.int64, device=dev) for _ in engines]
+    comm.allgather_dev(sends, recvs, engines)
+    engines[0].event_record(13)
+    gather_ms = engines[0].event_elapsed(12, 13)
+    del sends
+    res = None
+    for e, rv in zip(engines, recvs):
+        r = e.site_gathered(params, nranks * n_max, total_cand, rv.data_ptr())
+        res = res or r
+    del recvs
+    res["site_ms"] = gather_ms
+    res["rounds_mode"] = "replicated"
+    res["exchange"] = "one allgather of every band's packed viewsheds, then the single-GPU SITE loop on every rank"
+    return res
+
+
+def _device_rounds(active, comm, total_cand, mode="gather", poll_every=16):
     """SITE rounds with the keys and payloads in device buffers (see run_sharded).
     With one engine per process (TorchComm) a block of `poll_every` rounds --
     engine kernels and NCCL collectives, all on the engine's stream -- is
@@ -307,10 +356,8 @@ def _device_rounds(active, comm, total_cand, poll_every=16):
         for e, k, p in zip(engines, keys, pays):
             e.site_shard_apply_dev(k.data_ptr(), p.data_ptr(), total_cand)
 
-    # one allgather beats two allreduces once there are peers; a world of one
-    # has nothing to exchange and the two local allreduces are cheaper
-    # (c2, NCCL world 1: 18.1 vs 21.1 ms of rounds)
-    mode = os.environ.get("TXS_SHARD_EXCHANGE") or ("gather" if nranks > 1 else "reduce")
+    # per-round exchange (TXS_SHARD_EXCHANGE=gather|reduce): one allgather of
+    # {key, payload}, or two allreduces (MAX of keys, SUM broadcast of the payload)
     one_round = round_reduce if mode == "reduce" else round_gather
 
     engines[0].event_record(14)

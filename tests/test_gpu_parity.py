@@ -483,13 +483,14 @@ def test_cli_matches_oracle_and_is_deterministic(tmp_path):
 
 
 # ---- row-band shards on one device (virtual ranks) ---------------
-@pytest.mark.parametrize("device_rounds", [False, "gather", "reduce"])
+@pytest.mark.parametrize("device_rounds", [False, "gather", "reduce", "replicate"])
 @pytest.mark.parametrize("kind,nb", [("findmax", 1), ("findmax", 2), ("findmax", 3), ("observers", 2),
                                      ("observers", 4)])
 def test_sharded_engine_matches_single(monkeypatch, kind, nb, device_rounds):
     """Row bands on virtual ranks (one device) == the single-context run, with
     the SITE rounds host-driven or device-resident (txs_site_shard_*_dev), the
-    latter with the one-allgather or the two-allreduce exchange."""
+    latter with the one-allgather or the two-allreduce exchange per round, or
+    replicated (one allgather of the packed viewsheds, then the single-GPU loop)."""
     T = _T()
     if device_rounds:
         monkeypatch.setenv("TXS_SHARD_EXCHANGE", device_rounds)
@@ -554,7 +555,8 @@ def test_sharded_bench_torchrun_world1():
     lines = [l for l in r.stdout.splitlines() if l.strip()]
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
-    assert "graph" in d["result"]["parallelism"] and d["roofline"] and d["stages"]["site"]["ms"] > 0
+    par = d["result"]["parallelism"]
+    assert ("replicated" in par or "graph" in par) and d["roofline"] and d["stages"]["site"]["ms"] > 0
     r1 = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "c1", "--steps", "1",
                          "--warmup", "1", "--no-cpu-baseline"], cwd=root, capture_output=True, text=True, timeout=600)
     assert r1.returncode == 0, r1.stderr[-3000:]
