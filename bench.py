@@ -644,8 +644,8 @@ def run_b200_sharded(args, cfg):
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": DTYPE, "data": DATA, "config": config_dict(cfg),
             "result": {"sited": int(len(res["index"])), "stop": res["stop"],
-                       "parallelism": f"rowband{world} (halo roi+1; SITE rounds device-resident, "
-                                      f"stream-ordered NCCL: {res.get('exchange')}, {res.get('rounds_mode')})"},
+                       "parallelism": f"rowband{world} (halo roi+1; SITE {res.get('rounds_mode')}: "
+                                      f"{res.get('exchange')})"},
             "e2e": {"value": round(e2e / 1e3, 5), "unit": "s", "h2d_bytes_per_step": cfg.posts * 2,
                     "d2h_bytes_per_step": ((cfg.posts + 63) // 64) * 8 + len(r2["index"]) * 32},
             "gpu_launches": int(launches.item()),

@@ -124,7 +124,7 @@ struct RunConfig {
     bool dump_viewsheds = false;    // out_dir/viewsheds.bin: per viewshed {row0, col0, w, h} int32 + packed u64 words, LE
     int device = 0;
     std::vector<int> devices;   // > 1 entries: the native multi-GPU group (row bands, txs_group_*)
-    int32_t exchange = TXS_XCHG_P2P;   // group SITE winner exchange
+    int32_t exchange = TXS_XCHG_REPLICATE;   // group SITE: gathered viewsheds (default) or a per-round exchange
 };
 struct RunReport {
     double read_s = 0, vix_s = 0, findmax_s = 0, viewshed_s = 0, site_s = 0, total_s = 0;

@@ -273,7 +273,7 @@ void* txs_stream(txs_ctx* ctx);
  * the gathered set -- the same picks, bit for bit, since the gathered set IS the
  * single-GPU candidate list.  A record is txs_viewshed_record_words(roi) u64:
  *   [0] global candidate id (-1: padding)   [1] row | col << 32
- *   [2..3] window {row0, col0, h, w} (int32) [4] popcount
+ *   [2..3] window {row0, col0, h, w} (int32) [4] popcount | FINDMAX score << 32
  *   [5..] the engine's cum-aligned row words (txs_viewsheds_device layout)
  * txs_viewsheds_pack writes the context's resident viewsheds as `slots`
  * records into a device buffer (padding past its count), stream-ordered on
@@ -302,7 +302,7 @@ txs_status txs_get_cumulative_rows(txs_ctx* ctx, int64_t row_begin, int64_t row_
  * worker thread per rank: no collective), assigns global candidate ids by the
  * prefix of band counts, and drives the SITE rounds with one of three winner
  * exchanges:
- *   TXS_XCHG_P2P   (default) every rank writes {its best key, payload} into its
+ *   TXS_XCHG_P2P   every rank writes {its best key, payload} into its
  *                  own device mailbox; every rank's select kernel reads the N
  *                  keys and then the winner's window words straight out of the
  *                  winner rank's mailbox over NVLink peer memory (cross-device
@@ -314,9 +314,17 @@ txs_status txs_get_cumulative_rows(txs_ctx* ctx, int64_t row_begin, int64_t row_
  *                  also graph-captured;
  *   TXS_XCHG_HOST  host-staged rounds (keys and the owner's window through host
  *                  memory; txs_site_shard_best/export/apply) -- the reference
- *                  formulation, and the only exchange available with custom ops.
+ *                  formulation, and the only exchange available with custom ops;
+ *   TXS_XCHG_REPLICATE (default, below) gathers the viewsheds once instead.
  * All three give the single-context pick sequence and cumulative bitmap. */
-typedef enum txs_exchange { TXS_XCHG_P2P = 0, TXS_XCHG_NCCL = 1, TXS_XCHG_HOST = 2 } txs_exchange;
+typedef enum txs_exchange {
+    TXS_XCHG_P2P = 0, TXS_XCHG_NCCL = 1, TXS_XCHG_HOST = 2,
+    /* no exchange per round: every band's packed viewsheds are copied once to
+     * rank 0 (peer copies) and rank 0 runs the single-GPU SITE loop on them
+     * (txs_site_gathered) -- the default: ~6 us per round at roi 100 against
+     * a cross-GPU exchange's latency per round */
+    TXS_XCHG_REPLICATE = 3
+} txs_exchange;
 
 /* Stage entry points the group drives (defaults: the functions above).  A test
  * may substitute a CPU stand-in; only TXS_XCHG_HOST works with substituted ops. */

@@ -140,7 +140,7 @@ _sig("txs_group_random_observers", C.c_int, [vp, i64, u64])
 _sig("txs_group_run_pipeline", C.c_int, [vp, C.POINTER(Params), vp, i64, C.POINTER(i64), C.POINTER(i32), vp])
 _sig("txs_group_get_cumulative", C.c_int, [vp, vp])
 
-EXCHANGE = {"p2p": 0, "nccl": 1, "host": 2}
+EXCHANGE = {"p2p": 0, "nccl": 1, "host": 2, "replicate": 3}
 
 # every symbol the header declares (checked by the CPU test-suite)
 EXPORTS = [

@@ -86,7 +86,7 @@ struct txs_group {
     std::vector<int> dev;
     std::vector<txs_ctx*> ctx;
     std::string err;
-    int32_t exchange = TXS_XCHG_P2P;
+    int32_t exchange = TXS_XCHG_REPLICATE;
     int64_t nrows = 0, ncols = 0, block = 0;
     int32_t roi = 0;
     std::vector<int64_t> r0, r1;
@@ -100,6 +100,7 @@ struct txs_group {
     std::vector<ncclComm_t> comms;
     bool peers_enabled = false;
     cudaGraphExec_t graph = nullptr;
+    bool replicated = false;            // the last SITE ran on rank 0 over the gathered viewsheds
 };
 
 namespace {
@@ -378,6 +379,65 @@ txs_status device_rounds(txs_group* g, int64_t total, std::vector<txs_step>& ste
     return TXS_OK;
 }
 
+// TXS_XCHG_REPLICATE: every band's viewsheds packed as records on its own
+// device, copied once into rank 0's HBM (peer copies over NVLink), then rank 0
+// runs the single-GPU SITE loop on the gathered set (txs_site_gathered)
+txs_status replicated_site(txs_group* g, const txs_params& p, int64_t total, std::vector<txs_step>& steps,
+                           int32_t* stop, double* ms) {
+    const int n = g->n;
+    const int64_t rw = txs_viewshed_record_words(p.roi);
+    std::vector<int64_t> cnt((size_t)n, 0);
+    int64_t nmax = 1;
+    for (int k = 0; k < n; ++k) {
+        cnt[(size_t)k] = g->ctx[(size_t)k]->vs_n;
+        nmax = std::max(nmax, cnt[(size_t)k]);
+    }
+    G_CUDA(g, "gather", cudaSetDevice(g->dev[0]));
+    uint64_t* d_all = nullptr;
+    G_CUDA(g, "gather", cudaMalloc(&d_all, sizeof(uint64_t) * (size_t)(n * nmax * rw)));
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, g->ctx[0]->stream);
+    txs_status st = for_ranks(g, [&](int k) {   // pack on each device, then one peer copy into rank 0
+        txs_ctx* c = g->ctx[(size_t)k];
+        uint64_t* dst = d_all + (size_t)k * nmax * rw;
+        if (g->dev[(size_t)k] == g->dev[0]) return txs_viewsheds_pack(c, nmax, dst, nullptr);
+        cudaSetDevice(g->dev[(size_t)k]);
+        uint64_t* tmp = nullptr;
+        if (cudaMalloc(&tmp, sizeof(uint64_t) * (size_t)(nmax * rw)) != cudaSuccess) return TXS_ERR_OUT_OF_MEMORY;
+        txs_status s2 = txs_viewsheds_pack(c, nmax, tmp, nullptr);
+        if (s2 == TXS_OK &&
+            (cudaMemcpyPeerAsync(dst, g->dev[0], tmp, g->dev[(size_t)k], sizeof(uint64_t) * (size_t)(nmax * rw), c->stream) !=
+                 cudaSuccess ||
+             cudaStreamSynchronize(c->stream) != cudaSuccess))
+            s2 = TXS_ERR_CUDA;
+        cudaFree(tmp);
+        return s2;
+    });
+    if (st == TXS_OK) {
+        for (int k = 0; k < n; ++k) cudaStreamSynchronize(g->ctx[(size_t)k]->stream);
+        cudaSetDevice(g->dev[0]);
+        cudaEventRecord(e1, g->ctx[0]->stream);
+        cudaEventSynchronize(e1);
+        float f = 0.f;
+        cudaEventElapsedTime(&f, e0, e1);
+        steps.resize((size_t)total + 1);
+        int64_t ns = 0;
+        const txs_stats before = g->ctx[0]->stats;
+        st = txs_site_gathered(g->ctx[0], &p, n * nmax, total, d_all, steps.data(), (int64_t)steps.size(), &ns, stop);
+        if (st != TXS_OK) st = rank_fail(g, 0, st);
+        steps.resize((size_t)std::max<int64_t>(0, ns));
+        *ms = f + (g->ctx[0]->stats.ms_site - before.ms_site);
+    }
+    cudaSetDevice(g->dev[0]);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d_all);
+    if (st == TXS_OK) g->replicated = true;
+    return st;
+}
+
 // host-staged rounds (TXS_XCHG_HOST): shard.py's host loop, stop rules D9
 txs_status host_rounds(txs_group* g, const txs_params& p, int64_t total, std::vector<txs_step>& steps,
                        int32_t* stop) {
@@ -441,7 +501,7 @@ txs_status txs_group_create_with_ops(int ngpus, const int* devices, const txs_en
     txs_group* g = new txs_group();
     g->ops = *ops;
     g->native = ops == &kDefaultOps;
-    g->exchange = g->native ? TXS_XCHG_P2P : TXS_XCHG_HOST;
+    g->exchange = g->native ? TXS_XCHG_REPLICATE : TXS_XCHG_HOST;
     g->n = ngpus;
     for (int k = 0; k < ngpus; ++k) g->dev.push_back(devices ? devices[k] : k);
     for (int k = 0; k < ngpus; ++k) {
@@ -480,7 +540,7 @@ txs_ctx* txs_group_context(txs_group* g, int32_t rank) {
 
 txs_status txs_group_set_exchange(txs_group* g, int32_t x) {
     if (!g) return TXS_ERR_INVALID_ARGUMENT;
-    if (x != TXS_XCHG_P2P && x != TXS_XCHG_NCCL && x != TXS_XCHG_HOST)
+    if (x != TXS_XCHG_P2P && x != TXS_XCHG_NCCL && x != TXS_XCHG_HOST && x != TXS_XCHG_REPLICATE)
         return gfail(g, TXS_ERR_INVALID_ARGUMENT, "[site] group: unknown exchange");
     if (!g->native && x != TXS_XCHG_HOST)
         return gfail(g, TXS_ERR_INVALID_ARGUMENT, "[site] group: substituted ops support the host exchange only");
@@ -580,16 +640,20 @@ txs_status txs_group_run_pipeline(txs_group* g, const txs_params* p, txs_step* s
         }
     }
     // ---- VIEWSHED per band ----
+    const bool repl = g->exchange == TXS_XCHG_REPLICATE;
+    g->replicated = false;
     st = for_ranks(g, [&](int k) {
         txs_status s = g->ops.compute_viewsheds(g->ctx[(size_t)k], p);
-        return s != TXS_OK ? s : g->ops.site_shard_begin(g->ctx[(size_t)k], p);
+        return (s != TXS_OK || repl) ? s : g->ops.site_shard_begin(g->ctx[(size_t)k], p);
     });
     if (st != TXS_OK) return st;
     // ---- SITE rounds ----
     std::vector<txs_step> v;
     int32_t sr = TXS_STOP_EXHAUSTED;
     double site_ms = 0.0;
-    if (g->exchange == TXS_XCHG_HOST) {
+    if (repl) {
+        st = replicated_site(g, *p, total, v, &sr, &site_ms);
+    } else if (g->exchange == TXS_XCHG_HOST) {
         const auto t0 = std::chrono::steady_clock::now();
         st = host_rounds(g, *p, total, v, &sr);
         site_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -618,6 +682,10 @@ txs_status txs_group_get_cumulative(txs_group* g, uint64_t* dense_out) {
     if (!g || !dense_out) return TXS_ERR_INVALID_ARGUMENT;
     if (g->r0.empty()) return gfail(g, TXS_ERR_STATE, "[site] group: no grid");
     std::memset(dense_out, 0, sizeof(uint64_t) * (size_t)((g->nrows * g->ncols + 63) / 64));
+    if (g->replicated) {   // rank 0 holds the whole grid's cum
+        const txs_status st = txs_get_cumulative(g->ctx[0], dense_out);
+        return st == TXS_OK ? st : rank_fail(g, 0, st);
+    }
     return for_ranks(g, [&](int k) {
         return g->ops.get_cumulative_rows(g->ctx[(size_t)k], g->r0[(size_t)k], g->r1[(size_t)k], dense_out);
     });

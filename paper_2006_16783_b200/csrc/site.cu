@@ -1231,7 +1231,8 @@ txs_status download_cum_rows(txs_ctx* c, int64_t rb, int64_t re, uint64_t* host_
 // ---- replicated SITE: records <-> resident candidates (one warp per record) -----------
 __global__ void k_pack_records(int64_t n, int64_t slots, int64_t gid0, const int32_t* __restrict__ cgid,
                                const int32_t* __restrict__ crow, const int32_t* __restrict__ ccol,
-                               const int4* __restrict__ cwin, const int32_t* __restrict__ cpop,
+                               const int32_t* __restrict__ cscore, const int4* __restrict__ cwin,
+                               const int32_t* __restrict__ cpop,
                                const uint64_t* __restrict__ words, int64_t stride, uint64_t* __restrict__ rec) {
     const int lane = threadIdx.x & 31;
     const int64_t rw = kRecHead + stride;
@@ -1248,7 +1249,7 @@ __global__ void k_pack_records(int64_t n, int64_t slots, int64_t gid0, const int
             r[1] = (uint64_t)(uint32_t)crow[s] | ((uint64_t)(uint32_t)ccol[s] << 32);
             r[2] = (uint64_t)(uint32_t)w.x | ((uint64_t)(uint32_t)w.y << 32);
             r[3] = (uint64_t)(uint32_t)w.z | ((uint64_t)(uint32_t)w.w << 32);
-            r[4] = (uint64_t)(uint32_t)cpop[s];
+            r[4] = (uint64_t)(uint32_t)cpop[s] | ((uint64_t)(uint32_t)cscore[s] << 32);
         }
         const int64_t nw = (int64_t)w.z * win_nwr(w.y, w.w);
         for (int64_t t = lane; t < nw; t += 32) r[kRecHead + t] = words[s * stride + t];
@@ -1256,8 +1257,8 @@ __global__ void k_pack_records(int64_t n, int64_t slots, int64_t gid0, const int
 }
 
 __global__ void k_unpack_records(int64_t nrec, int64_t n_total, const uint64_t* __restrict__ rec, int64_t stride,
-                                 int32_t* __restrict__ crow, int32_t* __restrict__ ccol, int4* __restrict__ cwin,
-                                 int32_t* __restrict__ cpop, uint64_t* __restrict__ words) {
+                                 int32_t* __restrict__ crow, int32_t* __restrict__ ccol, int32_t* __restrict__ cscore,
+                                 int4* __restrict__ cwin, int32_t* __restrict__ cpop, uint64_t* __restrict__ words) {
     const int lane = threadIdx.x & 31;
     const int64_t rw = kRecHead + stride;
     for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nrec;
@@ -1272,6 +1273,7 @@ __global__ void k_unpack_records(int64_t nrec, int64_t n_total, const uint64_t* 
             ccol[g] = (int32_t)(uint32_t)(r[1] >> 32);
             cwin[g] = w;
             cpop[g] = (int32_t)(uint32_t)r[4];
+            cscore[g] = (int32_t)(uint32_t)(r[4] >> 32);
         }
         const int64_t nw = (int64_t)w.z * win_nwr(w.y, w.w);
         for (int64_t t = lane; t < nw; t += 32) words[g * stride + t] = __ldcs(r + kRecHead + t);
@@ -1281,8 +1283,8 @@ __global__ void k_unpack_records(int64_t nrec, int64_t n_total, const uint64_t* 
 txs_status pack_records(txs_ctx* c, int64_t slots, uint64_t* d_rec) {
     if (slots <= 0) return TXS_OK;
     k_pack_records<<<blocks_for(slots * 32, 256, c->num_sms * 16), 256, 0, c->stream>>>(
-        c->vs_n, slots, c->cand_gid0, c->h_cgid.empty() ? nullptr : c->d_cgid, c->d_crow, c->d_ccol, c->d_win, c->d_pop,
-        c->d_words, c->vs_stride, d_rec);
+        c->vs_n, slots, c->cand_gid0, c->h_cgid.empty() ? nullptr : c->d_cgid, c->d_crow, c->d_ccol, c->d_cscore, c->d_win,
+        c->d_pop, c->d_words, c->vs_stride, d_rec);
     TXS_LAUNCHED(c, "site");
     return TXS_OK;
 }
@@ -1290,7 +1292,7 @@ txs_status pack_records(txs_ctx* c, int64_t slots, uint64_t* d_rec) {
 txs_status unpack_records(txs_ctx* c, int64_t nrec, const uint64_t* d_rec) {
     if (nrec <= 0) return TXS_OK;
     k_unpack_records<<<blocks_for(nrec * 32, 256, c->num_sms * 16), 256, 0, c->stream>>>(
-        nrec, c->vs_n, d_rec, c->vs_stride, c->d_crow, c->d_ccol, c->d_win, c->d_pop, c->d_words);
+        nrec, c->vs_n, d_rec, c->vs_stride, c->d_crow, c->d_ccol, c->d_cscore, c->d_win, c->d_pop, c->d_words);
     TXS_LAUNCHED(c, "site");
     return TXS_OK;
 }

@@ -420,7 +420,9 @@ std::string params_echo(const RunConfig& c, int gpus) {
       << " block_width=" << c.params.block_width << " max_selected=" << c.params.max_selected
       << " site_mode=" << c.params.site_mode << " los_arith=" << (c.params.los_arith == TXS_LOS_EXACT ? "exact" : "fp64")
       << " vix_seed=" << c.vix_seed << " gpus=" << gpus;
-    if (gpus > 1) o << " exchange=" << (c.exchange == TXS_XCHG_NCCL ? "nccl" : c.exchange == TXS_XCHG_HOST ? "host" : "p2p");
+    if (gpus > 1)
+        o << " exchange=" << (c.exchange == TXS_XCHG_NCCL ? "nccl" : c.exchange == TXS_XCHG_HOST ? "host"
+                              : c.exchange == TXS_XCHG_P2P ? "p2p" : "replicate");
     return o.str();
 }
 
@@ -645,7 +647,8 @@ RunReport run_group(const RunConfig& cfg) {
         gchk(txs_group_band(g, k, &a, &b));
         bands.push_back({a, b});
     }
-    const Owners o = owners_of(ctxs);
+    // replicated SITE: rank 0 holds every candidate (at its global id); else the bands do
+    const Owners o = cfg.exchange == TXS_XCHG_REPLICATE ? owners_of({ctxs[0]}) : owners_of(ctxs);
     rep.result = to_result(steps, stop, o);
     rep.result.cumulative.nrows = cfg.nrows;
     rep.result.cumulative.ncols = cfg.ncols;

@@ -15,7 +15,7 @@ static void usage() {
                  "[--per-block K] [--block-width W] [--max-selected N] [--vix-seed S] [--site-mode 0|1] "
                  "[--out-dir DIR] [--snapshots a,b,c|pow2] [--threads T (ignored: GPU engine)] [--device D] "
                  "[--water-rows K] [--observers-random N --observer-seed S] [--los-arith fp64|exact] "
-                 "[--gpus N | --devices a,b,...] [--exchange p2p|nccl|host] [--dump-vix] [--dump-candidates] "
+                 "[--gpus N | --devices a,b,...] [--exchange replicate|p2p|nccl|host] [--dump-vix] [--dump-candidates] "
                  "[--dump-viewsheds] [--no-images]\n");
 }
 
@@ -74,6 +74,7 @@ int main(int argc, char** argv) {
             if (m == "p2p") cfg.exchange = TXS_XCHG_P2P;
             else if (m == "nccl") cfg.exchange = TXS_XCHG_NCCL;
             else if (m == "host") cfg.exchange = TXS_XCHG_HOST;
+            else if (m == "replicate") cfg.exchange = TXS_XCHG_REPLICATE;
             else { usage(); return 2; }
         }
         else if (a == "--no-images") cfg.images = false;

@@ -114,7 +114,7 @@ def test_cli_random_observers(tmp_path, devices):
 def test_cli_exchanges_agree(tmp_path):
     outs = []
     for k, extra in enumerate([[], ["--devices", "0,0", "--exchange", "host"], ["--devices", "0,0,0,0"],
-                               ["--gpus", "1", "--exchange", "nccl"]]):
+                               ["--devices", "0,0,0", "--exchange", "p2p"], ["--gpus", "1", "--exchange", "nccl"]]):
         d = tmp_path / f"r{k}"
         d.mkdir()
         _run(BASE + extra + ["--no-images"], d)

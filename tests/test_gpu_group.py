@@ -53,7 +53,8 @@ def _same(a, b):
 
 
 @pytest.mark.parametrize("devs,xchg", [([0], "p2p"), ([0, 0], "p2p"), ([0, 0, 0], "p2p"), ([0, 0, 0, 0], "p2p"),
-                                       ([0, 0], "host"), ([0, 0, 0], "host"), ([0], "nccl")])
+                                       ([0, 0], "host"), ([0, 0, 0], "host"), ([0], "nccl"), ([0], "replicate"),
+                                       ([0, 0, 0], "replicate")])
 def test_group_matches_single_context(devs, xchg):
     p = T.make_params(30, 10, 10, samples=8, per_block=6, block_width=40, target=0.9, max_selected=120, seed=5)
     ref = _single(480, 400, 0.5, 3, p)
@@ -61,22 +62,25 @@ def test_group_matches_single_context(devs, xchg):
     _same(_group(devs, xchg, 480, 400, 0.5, 3, p), ref)
 
 
-@pytest.mark.parametrize("devs", [[0, 0], [0, 0, 0]])
-def test_group_random_observers_and_water(devs):
+@pytest.mark.parametrize("devs,xchg", [([0, 0], "p2p"), ([0, 0, 0], "p2p"), ([0, 0], "replicate"),
+                                       ([0, 0, 0, 0], "replicate")])
+def test_group_random_observers_and_water(devs, xchg):
     p = T.make_params(40, 20, 10, target=1.0, max_selected=200, block_width=48)
     ref = _single(512, 448, 0.6, 8, p, water=60, observers=(3000, 17))
-    _same(_group(devs, "p2p", 512, 448, 0.6, 8, p, water=60, observers=(3000, 17)), ref)
+    _same(_group(devs, xchg, 512, 448, 0.6, 8, p, water=60, observers=(3000, 17)), ref)
 
 
 def test_group_config2_four_ranks():
     """BASELINE config 2 (4096^2, R200, 16384 candidates, 1024 picks max) on 4
-    row bands exchanging over peer memory == the single context."""
+    row bands, exchanging winners over peer memory or gathering the viewsheds
+    once (replicated SITE) == the single context."""
     cfg = CONFIGS["c2"]
     p = params_for(cfg)
     ref = _single(cfg.nrows, cfg.ncols, cfg.roughness, cfg.terrain_seed, p, zmax=cfg.zmax)
-    got = _group([0, 0, 0, 0], "p2p", cfg.nrows, cfg.ncols, cfg.roughness, cfg.terrain_seed, p, zmax=cfg.zmax)
-    _same(got, ref)
-    assert got[0]["stage_ms"]["site"] > 0
+    for xchg in ("p2p", "replicate"):
+        got = _group([0, 0, 0, 0], xchg, cfg.nrows, cfg.ncols, cfg.roughness, cfg.terrain_seed, p, zmax=cfg.zmax)
+        _same(got, ref)
+        assert got[0]["stage_ms"]["site"] > 0
 
 
 def test_group_rejects_bad_use():
