@@ -501,13 +501,16 @@ std::vector<Viewshed> selected_viewsheds(const SitingResult& r, const Owners& o,
     return out;
 }
 
-void write_dumps(const RunConfig& cfg, const Owners& o, const std::vector<std::pair<int64_t, int64_t>>& bands) {
+// band_ctx[k] holds VixMap rows bands[k] (every context of a group; the owners
+// of the candidates may be fewer: a replicated SITE gathers them on rank 0)
+void write_dumps(const RunConfig& cfg, const Owners& o, const std::vector<txs_ctx*>& band_ctx,
+                 const std::vector<std::pair<int64_t, int64_t>>& bands) {
     const std::string& d = cfg.out_dir;
     if (cfg.dump_vix && cfg.observers_random == 0) {   // SPEC.md:201 row-major score bytes
         std::vector<uint8_t> v((size_t)(cfg.nrows * cfg.ncols));
-        for (size_t k = 0; k < o.ctx.size(); ++k)
-            check(o.ctx[k], txs_get_vix(o.ctx[k], bands[k].first, bands[k].second,
-                                        v.data() + bands[k].first * cfg.ncols));
+        for (size_t k = 0; k < band_ctx.size(); ++k)
+            check(band_ctx[k], txs_get_vix(band_ctx[k], bands[k].first, bands[k].second,
+                                           v.data() + bands[k].first * cfg.ncols));
         std::ofstream(d + "/vix.u8", std::ios::binary).write(reinterpret_cast<const char*>(v.data()), (std::streamsize)v.size());
     }
     // candidates / viewsheds in global id order (ranks hold contiguous id ranges
@@ -558,7 +561,7 @@ void write_dumps(const RunConfig& cfg, const Owners& o, const std::vector<std::p
     }
 }
 
-void write_outputs(const RunConfig& cfg, RunReport& rep, const Owners& o,
+void write_outputs(const RunConfig& cfg, RunReport& rep, const Owners& o, const std::vector<txs_ctx*>& band_ctx,
                    const std::vector<std::pair<int64_t, int64_t>>& bands) {
     if (cfg.out_dir.empty()) return;
     std::ofstream csv(cfg.out_dir + "/result.csv");
@@ -578,7 +581,7 @@ void write_outputs(const RunConfig& cfg, RunReport& rep, const Owners& o,
         render_snapshots(byrank, selected_viewsheds(rep.result, o, cfg.params.roi), cfg.nrows, cfg.ncols,
                          cfg.snapshots, cfg.out_dir);
     }
-    write_dumps(cfg, o, bands);
+    write_dumps(cfg, o, band_ctx, bands);
     std::ofstream(cfg.out_dir + "/report.txt") << rep.to_string();
 }
 
@@ -609,7 +612,7 @@ RunReport run_single(const RunConfig& cfg) {
     rep.device_bytes_peak = st.device_bytes_peak;
     rep.params_echo = params_echo(cfg, 1);
     rep.host_bytes_peak = host_rss_peak();
-    write_outputs(cfg, rep, o, {{0, cfg.nrows}});
+    write_outputs(cfg, rep, o, {pl.handle()}, {{0, cfg.nrows}});
     return rep;
 }
 
@@ -667,7 +670,7 @@ RunReport run_group(const RunConfig& cfg) {
     }
     rep.params_echo = params_echo(cfg, n);
     rep.host_bytes_peak = host_rss_peak();
-    write_outputs(cfg, rep, o, bands);
+    write_outputs(cfg, rep, o, ctxs, bands);
     return rep;
 }
 
