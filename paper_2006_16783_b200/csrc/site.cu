@@ -425,14 +425,12 @@ __device__ __forceinline__ void flush_rows(const SiteArgs& a, const SitePart& w,
     for (int t = threadIdx.x; t < nrow * nwr; t += blockDim.x) {
         const int y = slot + (t / nwr) * nslots, b = t % nwr;
         const uint64_t x = v[y * nwr + b];
-        if (x) {
-            uint64_t* o = cum + (int64_t)(w.row0 + y) * a.wpr + wlo + b;
-            *o |= x;
-        }
+        if (x)   // a reduction, not load-or-store: no round trip before the barrier
+            atomicOr((unsigned long long*)(cum + (int64_t)(w.row0 + y) * a.wpr + wlo + b), (unsigned long long)x);
     }
 }
 
-__global__ void __launch_bounds__(kL1Threads, 1) k_site_loop1(SiteArgs a, SiteState* st, LoopPtrs lp,
+__global__ void __launch_bounds__(kL1Threads, 2) k_site_loop1(SiteArgs a, SiteState* st, LoopPtrs lp,
                                                          const int32_t* __restrict__ pop, int32_t* __restrict__ gain,
                                                          const uint64_t* __restrict__ words, uint64_t* __restrict__ cum,
                                                          SitePart* __restrict__ parts,
@@ -524,7 +522,9 @@ __global__ void __launch_bounds__(kL1Threads, 1) k_site_loop1(SiteArgs a, SiteSt
             int xk = s_kj[0];
             for (int k = 1; k < kL1Threads / 32; ++k)
                 if (s_key[k] > x) { x = s_key[k]; xk = s_kj[k]; }
-            if (xk >= 0) best = pb[xk];   // one 32-byte read, L1/L2 hit (the partials were just read)
+            // one 32-byte read of the winning partial (measured: cheaper than every
+            // thread loading whole partials and handing the winner over in smem)
+            if (xk >= 0) best = pb[xk];
         }
         mark(0);
         mark(1);
@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(kL1Threads, 1) k_site_loop1(SiteArgs a, SiteSt
                     const uint64_t* cr = cum + (int64_t)y * a.wpr;
                     int acc = 0;
                     for (int B = cl >> 6; B <= (ch >> 6); ++B) {
-                        const uint64_t x = __ldg(vi + B) & __ldg(vwr + B) & ~(*(volatile const uint64_t*)(cr + B));
+                        const uint64_t x = __ldg(vi + B) & __ldg(vwr + B) & ~__ldcg(cr + B);
                         const uint64_t pv = (prow && B >= wlo_p && B < wlo_p + nwr_p) ? __ldg(vpr + B) : 0ull;
                         acc += __popcll(x & ~pv);
                     }
