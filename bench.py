@@ -368,7 +368,7 @@ def run_b200(args, cfg):
     import numpy as np
     import torch
     import paper_2006_16783_b200 as T
-    from paper_2006_16783_b200.configs import params_for, run, setup_terrain
+    from paper_2006_16783_b200.configs import params_for, run, run_from_host, setup_terrain
 
     rank, world, local = dist_env()
     if world > 1:
@@ -452,8 +452,7 @@ def run_b200(args, cfg):
         torch.cuda.synchronize()
         before = eng.stats()["kernel_launches"]
         eng.event_record(2)
-        eng.set_terrain(z_host)
-        r2 = run(eng, cfg, params)
+        r2 = run_from_host(eng, cfg, params, z_host)   # upload overlapped with VIX (public API)
         eng._chk(N.lib.txs_get_cumulative(eng.handle, ctypes.c_void_p(cum_host.ctypes.data)))
         eng.event_record(3)
         e2e_ms.append(eng.event_elapsed(2, 3))
@@ -461,6 +460,7 @@ def run_b200(args, cfg):
     # median over the e2e steps: a host-side stall (seen as an occasional
     # 200-400 ms gap between the step's device events) does not set the figure;
     # every step's time is reported beside it
+    assert np.array_equal(r2["index"], res["index"]) and r2["stop"] == res["stop"], "e2e picks differ"
     e2e = statistics.median(e2e_ms)
     if world > 1:
         t = torch.tensor([e2e], device=f"cuda:{local}", dtype=torch.float64)

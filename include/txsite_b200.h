@@ -203,6 +203,15 @@ txs_status txs_measure_cache_read(txs_ctx* ctx, int64_t bytes, int32_t reps, dou
 txs_status txs_run_pipeline(txs_ctx* ctx, const txs_params* p, txs_step* steps, int64_t cap,
                             int64_t* nsteps, int32_t* stop_reason, double* stage_ms);
 
+/* run_pipeline straight from a host terrain (load_binary's result, SPEC.md:41 +
+ * :433): the rows go up in ~16 chunks on a copy stream while VIX runs band by
+ * band behind them (each band waits only for the rows its walks and skip-map
+ * corners reach), so the upload overlaps the dominant stage; NODATA is checked
+ * once the rows are in.  Same results as txs_set_terrain + txs_run_pipeline
+ * (which it is, on a sharded context).  z should be pinned for the overlap. */
+txs_status txs_run_pipeline_host(txs_ctx* ctx, const int16_t* z, int64_t nrows, int64_t ncols, const txs_params* p,
+                                 txs_step* steps, int64_t cap, int64_t* nsteps, int32_t* stop_reason, double* stage_ms);
+
 /* ---- multi-GPU row-band shards ---------------------------------
  * A sharded context owns rows [row_begin,row_end) of a global nrows x ncols grid
  * and holds terrain rows [max(0,row_begin-halo), min(nrows,row_end+halo)).

@@ -120,6 +120,7 @@ _sig("txs_event_template_info", C.c_int, [i32, C.POINTER(i64), C.POINTER(i64), C
 _sig("txs_get_cumulative_rows", C.c_int, [vp, i64, i64, vp])
 _sig("txs_get_candidate_ids", C.c_int, [vp, vp, i64, C.POINTER(i64)])
 _sig("txs_viewshed_record_words", i64, [i32])
+_sig("txs_run_pipeline_host", C.c_int, [vp, vp, i64, i64, C.POINTER(Params), vp, i64, C.POINTER(i64), C.POINTER(i32), vp])
 _sig("txs_viewsheds_pack", C.c_int, [vp, i64, vp, C.POINTER(i64)])
 _sig("txs_site_gathered", C.c_int, [vp, C.POINTER(Params), i64, i64, vp, vp, i64, C.POINTER(i64), C.POINTER(i32)])
 _sig("txs_default_ops", vp, [])
@@ -156,7 +157,7 @@ EXPORTS = [
     "txs_site_shard_payload_words", "txs_site_shard_result", "txs_stream", "txs_time_gain_pass",
     "txs_site_shard_export_keyed_dev", "txs_site_shard_select_dev", "txs_measure_cache_read",
     "txs_get_cumulative_rows", "txs_get_candidate_ids", "txs_default_ops", "txs_viewshed_record_words",
-    "txs_viewsheds_pack", "txs_site_gathered", "txs_plan_bands", "txs_group_create", "txs_group_create_with_ops",
+    "txs_viewsheds_pack", "txs_site_gathered", "txs_run_pipeline_host", "txs_plan_bands", "txs_group_create", "txs_group_create_with_ops",
     "txs_group_destroy", "txs_group_last_error", "txs_group_size", "txs_group_context", "txs_group_set_exchange",
     "txs_group_set_grid", "txs_group_band", "txs_group_set_terrain", "txs_group_generate_fractal",
     "txs_group_fill_rows", "txs_group_random_observers", "txs_group_run_pipeline", "txs_group_get_cumulative",

@@ -246,6 +246,19 @@ class Engine:
         d["stage_ms"] = dict(vix=ms[0], findmax=ms[1], viewshed=ms[2], site=ms[3])
         return d
 
+    def run_pipeline_host(self, z, params, cap=1 << 20):
+        """run_pipeline from a host terrain (row-major int16, ideally pinned):
+        the upload overlaps VIX (txs_run_pipeline_host)."""
+        z = np.ascontiguousarray(z, np.int16)
+        steps = (N.Step * cap)()
+        ns, stop = C.c_int64(), C.c_int32()
+        ms = (C.c_double * 4)()
+        self._chk(N.lib.txs_run_pipeline_host(self._h, _p(z), z.shape[0], z.shape[1], C.byref(params), steps, cap,
+                                              C.byref(ns), C.byref(stop), ms))
+        d = _steps_dict(steps, min(ns.value, cap), stop.value)
+        d["stage_ms"] = dict(vix=ms[0], findmax=ms[1], viewshed=ms[2], site=ms[3])
+        return d
+
     # ---- row-band shards (DESIGN.md §6) --------------------------------------------
     def set_shard(self, nrows, ncols, row_begin, row_end, halo):
         self._chk(N.lib.txs_set_shard(self._h, nrows, ncols, row_begin, row_end, halo))

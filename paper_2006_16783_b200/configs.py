@@ -66,3 +66,14 @@ def run(engine, cfg, params):
         engine.compute_all_viewsheds(params)
         return engine.site(params, cap=min(cap, cfg.random_observers + 1))
     return engine.run_pipeline(params, cap=cap)
+
+
+def run_from_host(engine, cfg, params, z_host):
+    """The same siting from a host terrain through the public API: the upload
+    overlaps VIX (txs_run_pipeline_host); configuration 5 (no VIX) uploads, then
+    runs."""
+    cap = cfg.max_selected + 1 if cfg.max_selected > 0 else 1 << 20
+    if cfg.random_observers:
+        engine.set_terrain(z_host)
+        return run(engine, cfg, params)
+    return engine.run_pipeline_host(z_host, params, cap=cap)

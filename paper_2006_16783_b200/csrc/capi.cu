@@ -46,6 +46,13 @@ txs_status check_params(txs_ctx* ctx, const char* stage, const txs_params* p, bo
     return TXS_OK;
 }
 
+txs_status wait_terrain_rows(txs_ctx* c, int64_t row_end) {
+    if (!c->up_pending || row_end <= 0 || c->up_ev.empty()) return TXS_OK;
+    const size_t k = (size_t)std::min<int64_t>((int64_t)c->up_ev.size() - 1, (row_end - 1) / c->up_chunk);
+    TXS_CUDA(c, "read", cudaStreamWaitEvent(c->stream, c->up_ev[k], 0));
+    return TXS_OK;
+}
+
 }  // namespace txs
 
 using namespace txs;
@@ -139,6 +146,8 @@ void txs_destroy(txs_ctx* c) {
     if (c->ev_r1) cudaEventDestroy(c->ev_r1);
     if (c->ev_k0) cudaEventDestroy(c->ev_k0);
     if (c->ev_k1) cudaEventDestroy(c->ev_k1);
+    for (cudaEvent_t e : c->up_ev) if (e) cudaEventDestroy(e);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -783,6 +792,76 @@ txs_status txs_run_pipeline(txs_ctx* c, const txs_params* p, txs_step* steps, in
     if (st != TXS_OK) return st;
     if (stage_ms) {
         stage_ms[0] = c->stats.ms_vix - before.ms_vix;
+        stage_ms[1] = c->stats.ms_findmax - before.ms_findmax;
+        stage_ms[2] = c->stats.ms_viewshed - before.ms_viewshed;
+        stage_ms[3] = c->stats.ms_site - before.ms_site;
+    }
+    return TXS_OK;
+}
+
+txs_status txs_run_pipeline_host(txs_ctx* c, const int16_t* z, int64_t nrows, int64_t ncols, const txs_params* p,
+                                 txs_step* steps, int64_t cap, int64_t* nsteps, int32_t* stop, double* stage_ms) {
+    if (!c || !z || !p) return TXS_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(c->device);
+    if (c->sharded) {   // a shard holds band + halo rows: no overlapped form
+        txs_status st = txs_set_terrain(c, z, nrows, ncols);
+        return st != TXS_OK ? st : txs_run_pipeline(c, p, steps, cap, nsteps, stop, stage_ms);
+    }
+    txs_status st = check_params(c, "vix", p, true);   // (before the upload replaces the terrain)
+    if (st != TXS_OK && st != TXS_ERR_STATE) return st;
+    st = set_dims(c, nrows, ncols);
+    if (st != TXS_OK) return st;
+    if (!c->copy_stream) TXS_CUDA(c, "read", cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    // ~16 chunks of whole 64-row multiples, on the copy stream, one event each
+    const int64_t ch = std::max<int64_t>(64, ((nrows + 15) / 16 + 63) / 64 * 64);
+    const size_t nch = (size_t)((nrows + ch - 1) / ch);
+    while (c->up_ev.size() < nch) {
+        cudaEvent_t e = nullptr;
+        TXS_CUDA(c, "read", cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->up_ev.push_back(e);
+    }
+    const txs_stats before = c->stats;
+    // the copies start after everything already on the context stream (device order)
+    TXS_CUDA(c, "read", cudaEventRecord(c->ev_r0, c->stream));
+    TXS_CUDA(c, "read", cudaStreamWaitEvent(c->copy_stream, c->ev_r0, 0));
+    for (size_t k = 0; k < nch; ++k) {
+        const int64_t r0 = (int64_t)k * ch, r1 = std::min(nrows, r0 + ch);
+        TXS_CUDA(c, "read", cudaMemcpyAsync(c->d_z + r0 * ncols, z + r0 * ncols, sizeof(int16_t) * (r1 - r0) * ncols,
+                                            cudaMemcpyHostToDevice, c->copy_stream));
+        TXS_CUDA(c, "read", cudaEventRecord(c->up_ev[k], c->copy_stream));
+    }
+    std::vector<cudaEvent_t> evs(c->up_ev.begin(), c->up_ev.begin() + (int64_t)nch);
+    std::swap(c->up_ev, evs);   // exactly this upload's chunks while it is pending
+    c->up_chunk = ch;
+    c->up_pending = true;
+    st = txs_estimate_vix(c, p, nullptr);   // VIX bands start behind the arriving rows
+    c->up_pending = false;
+    std::swap(c->up_ev, evs);
+    TXS_CUDA(c, "read", cudaStreamWaitEvent(c->stream, c->up_ev[nch - 1], 0));   // the whole terrain in any case
+    if (st != TXS_OK) return st;
+    {   // NODATA, checked once the rows are in
+        if (ensure(c, "read", &c->d_scratch, &c->scratch_cap, 64) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
+        int* flag = (int*)c->d_scratch;
+        TXS_CUDA(c, "read", cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
+        k_nodata_check<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_z, nrows * ncols, flag);
+        TXS_LAUNCHED(c, "read");
+        int h = 0;
+        TXS_CUDA(c, "read", cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        TXS_CUDA(c, "read", cudaStreamSynchronize(c->stream));
+        if (h) {
+            c->nrows = c->ncols = 0;
+            invalidate(c);
+            return fail(c, TXS_ERR_NODATA, "read", "NODATA sentinel -32768 in terrain");
+        }
+    }
+    st = txs_find_candidates(c, p, nullptr, nullptr, 0);
+    if (st != TXS_OK) return st;
+    st = txs_compute_viewsheds(c, p);
+    if (st != TXS_OK) return st;
+    st = txs_site(c, p, steps, cap, nsteps, stop);
+    if (st != TXS_OK) return st;
+    if (stage_ms) {
+        stage_ms[0] = c->stats.ms_vix - before.ms_vix;   // includes the waits for the first rows
         stage_ms[1] = c->stats.ms_findmax - before.ms_findmax;
         stage_ms[2] = c->stats.ms_viewshed - before.ms_viewshed;
         stage_ms[3] = c->stats.ms_site - before.ms_site;

@@ -160,6 +160,14 @@ struct txs_ctx {
     size_t bucket_cap = 0, bucket_items_cap = 0;
     bool site_valid = false;
 
+    // txs_run_pipeline_host: terrain rows arriving on copy_stream in chunks of
+    // up_chunk rows (event up_ev[k] after chunk k); VIX starts on the first
+    // row bands while the rest is still in flight
+    cudaStream_t copy_stream = nullptr;
+    std::vector<cudaEvent_t> up_ev;
+    int64_t up_chunk = 0;
+    bool up_pending = false;
+
     // stats
     txs_stats stats{};
     unsigned long long* d_counters = nullptr;
@@ -199,6 +207,8 @@ txs_status launch_generate(txs_ctx*, int64_t nrows, int64_t ncols, double roughn
                            int32_t zmin, int32_t zmax);   // writes held rows [z_off, z_off+z_rows)
 txs_status launch_fill_rows(txs_ctx*, int64_t rb, int64_t re, int16_t v);
 txs_status launch_vix(txs_ctx*, const txs_params& p);
+// txs_run_pipeline_host: make the context stream wait until terrain rows [0, row_end) have arrived
+txs_status wait_terrain_rows(txs_ctx*, int64_t row_end);
 txs_status launch_los_batch(txs_ctx*, const int32_t* d_pairs, int64_t n, int32_t ht, int32_t hr,
                             int32_t arith, uint8_t* d_out);
 txs_status launch_findmax(txs_ctx*, const txs_params& p, int64_t bw);

@@ -970,9 +970,11 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
 // (pr, pc) the maximum of blocks pr..pr+1 x pc..pc+1 -- the 2G x 2G posts from
 // post (G(pr-1), G(pc-1)) -- written row-major (SV) and column-major (ST) so
 // that lanes stepping along a walk's major axis read consecutive entries.
-__global__ void k_blockmax(const int16_t* __restrict__ z, int H, int W, int16_t* __restrict__ bp, int Hb, int Wb, int G) {
-    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (idx >= (int64_t)(Hb + 2) * (Wb + 2)) return;
+// padded block rows [pr0, pr1) of the (Hb+2) x (Wb+2) block maxima
+__global__ void k_blockmax(const int16_t* __restrict__ z, int H, int W, int16_t* __restrict__ bp, int Hb, int Wb, int G,
+                           int pr0, int pr1) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + (int64_t)pr0 * (Wb + 2);
+    if (idx >= (int64_t)pr1 * (Wb + 2)) return;
     const int pr = (int)(idx / (Wb + 2)), pc = (int)(idx - (int64_t)pr * (Wb + 2));
     const int br = pr - 1, bc = pc - 1;
     int m = -32768;
@@ -983,10 +985,11 @@ __global__ void k_blockmax(const int16_t* __restrict__ z, int H, int W, int16_t*
     bp[idx] = (int16_t)m;
 }
 
+// block-corner rows [q0, q1) of the skip map (from padded block rows q0 .. q1)
 __global__ void k_skipmap(const int16_t* __restrict__ bp, int Hb, int Wb, int16_t* __restrict__ sv, int pv,
-                          int16_t* __restrict__ st, int pt) {
-    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (idx >= (int64_t)(Hb + 1) * (Wb + 1)) return;
+                          int16_t* __restrict__ st, int pt, int q0, int q1) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + (int64_t)q0 * (Wb + 1);
+    if (idx >= (int64_t)q1 * (Wb + 1)) return;
     const int pr = (int)(idx / (Wb + 1)), pc = (int)(idx - (int64_t)pr * (Wb + 1));
     const int16_t* b = bp + (int64_t)pr * (Wb + 2) + pc;
     const int16_t m = max(max(b[0], b[1]), max(b[Wb + 2], b[Wb + 3]));
@@ -1091,6 +1094,12 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         if (!strcmp(e, "zt")) path = 2;
     }
     set_zbounds(c->d_z, c->d_z + c->z_rows * c->ncols, c->stream);
+    // an overlapped upload (txs_run_pipeline_host) has a banded form only on the
+    // 16-step terrain-walk path; every other path waits for the whole terrain
+    if (c->up_pending && path != 1) {
+        txs_status w = wait_terrain_rows(c, c->z_rows);
+        if (w != TXS_OK) return w;
+    }
     if (path == 0) {
         cudaEventRecord(c->ev_k0, c->stream);
         st = go(k_vix<true, 1>, smem);
@@ -1127,18 +1136,26 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         // rebuilt on every call (part of the timed stage; ~1 HBM pass of 34 B/post)
         if (ensure(c, "vix", (void**)&c->d_pairs, &c->pairs_cap, sizeof(uint2) * nq + map_bytes) != TXS_OK)
             return TXS_ERR_OUT_OF_MEMORY;
+        const bool banded = c->up_pending && terr && !c->sharded;
+        if (c->up_pending && !banded) {
+            txs_status w = wait_terrain_rows(c, c->z_rows);
+            if (w != TXS_OK) return w;
+        }
         if (!terr) {
             dim3 tb(32, 8), tg((unsigned)((c->ncols + 31) / 32), (unsigned)((c->z_rows + 31) / 32));
             k_quads<<<tg, tb, 0, c->stream>>>(c->d_z, (uint2*)c->d_pairs, (int)c->z_rows, a.hp, a.wp, (int)c->ncols);
             TXS_LAUNCHED(c, "vix");
         }
         int16_t* smap = skip ? (int16_t*)((uint2*)c->d_pairs + nq) : nullptr;
-        if (skip) {
-            int16_t* bp = smap + nsv + nst;
-            k_blockmax<<<(unsigned)((nbp + 255) / 256), 256, 0, c->stream>>>(c->d_z, (int)c->z_rows, (int)c->ncols, bp, Hb, Wb, G);
+        // overlapped terrain upload (txs_run_pipeline_host): the map and the walk go
+        // band by band behind the arriving rows (16-step terrain walks only)
+        int16_t* bp = skip ? smap + nsv + nst : nullptr;
+        if (skip && !banded) {
+            k_blockmax<<<(unsigned)((nbp + 255) / 256), 256, 0, c->stream>>>(c->d_z, (int)c->z_rows, (int)c->ncols, bp, Hb, Wb, G,
+                                                                           0, Hb + 2);
             TXS_LAUNCHED(c, "vix");
             const int64_t ns = (int64_t)(Hb + 1) * (Wb + 1);
-            k_skipmap<<<(unsigned)((ns + 255) / 256), 256, 0, c->stream>>>(bp, Hb, Wb, smap, a.pv, smap + nsv, a.pt);
+            k_skipmap<<<(unsigned)((ns + 255) / 256), 256, 0, c->stream>>>(bp, Hb, Wb, smap, a.pv, smap + nsv, a.pt, 0, Hb + 1);
             TXS_LAUNCHED(c, "vix");
         }
         const uint2* qp = (const uint2*)c->d_pairs;
@@ -1177,12 +1194,54 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         TXS_CUDA(c, "vix", cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kq, kVixThreads, qsm));
         int64_t grid_q = std::min<int64_t>(tiles_q, (int64_t)std::max(1, per_sm) * c->num_sms);
         if (const char* e = getenv("TXS_VIX_GRID")) grid_q = std::min<int64_t>(tiles_q, std::max(1, atoi(e)));
-        TXS_CUDA(c, "vix", cudaMemsetAsync(c->d_counters + kVixNext, 0, sizeof(unsigned long long), c->stream));
-        cudaEventRecord(c->ev_k0, c->stream);
-        kq<<<(unsigned)grid_q, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols,
-                                                                c->d_vix - c->band_r0 * c->ncols, aq, c->d_gcd, smap,
-                                                                c->d_counters);
-        cudaEventRecord(c->ev_k1, c->stream);
+        if (!banded) {
+            TXS_CUDA(c, "vix", cudaMemsetAsync(c->d_counters + kVixNext, 0, sizeof(unsigned long long), c->stream));
+            cudaEventRecord(c->ev_k0, c->stream);
+            kq<<<(unsigned)grid_q, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols,
+                                                                    c->d_vix - c->band_r0 * c->ncols, aq, c->d_gcd, smap,
+                                                                    c->d_counters);
+            cudaEventRecord(c->ev_k1, c->stream);
+        } else {
+            // band b = upload chunk b's rows; it needs the rows up to r1 + R + 4G (its
+            // walks, and the map corners of their groups), so it waits for that
+            // chunk; block-max rows and map corner rows are built once each, as
+            // soon as their terrain rows are in
+            const int64_t H = c->z_rows, CH = c->up_chunk;
+            int pr_done = 0, q_done = 0;
+            cudaEventRecord(c->ev_k0, c->stream);
+            for (int64_t r0 = 0; r0 < H; r0 += CH) {
+                const int64_t r1 = std::min(H, r0 + CH);
+                const int64_t need = std::min(H, r1 + p.roi + 4 * (int64_t)G);
+                const int64_t loaded = std::min(H, ((need - 1) / CH + 1) * CH);
+                if ((st = wait_terrain_rows(c, need)) != TXS_OK) return st;
+                const int pr_new = loaded >= H ? Hb + 2 : (int)(loaded / G) + 1;
+                if (pr_new > pr_done) {
+                    const int64_t cnt = (int64_t)(pr_new - pr_done) * (Wb + 2);
+                    k_blockmax<<<(unsigned)((cnt + 255) / 256), 256, 0, c->stream>>>(c->d_z, (int)H, (int)c->ncols, bp, Hb, Wb,
+                                                                                   G, pr_done, pr_new);
+                    TXS_LAUNCHED(c, "vix");
+                    pr_done = pr_new;
+                }
+                const int q_new = std::min(Hb + 1, pr_done - 1);
+                if (q_new > q_done) {
+                    const int64_t cnt = (int64_t)(q_new - q_done) * (Wb + 1);
+                    k_skipmap<<<(unsigned)((cnt + 255) / 256), 256, 0, c->stream>>>(bp, Hb, Wb, smap, a.pv, smap + nsv, a.pt,
+                                                                                  q_done, q_new);
+                    TXS_LAUNCHED(c, "vix");
+                    q_done = q_new;
+                }
+                VixArgs ab = aq;
+                ab.row0 = (int)r0; ab.row_end = (int)r1;
+                ab.tiles_y = (int)((r1 - r0 + tq - 1) / tq);
+                const int64_t tb = (int64_t)ab.tiles_x * ab.tiles_y;
+                const int64_t gb = std::min<int64_t>(tb, (int64_t)std::max(1, per_sm) * c->num_sms);
+                TXS_CUDA(c, "vix", cudaMemsetAsync(c->d_counters + kVixNext, 0, sizeof(unsigned long long), c->stream));
+                kq<<<(unsigned)gb, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols, c->d_vix, ab,
+                                                                  c->d_gcd, smap, c->d_counters);
+                TXS_LAUNCHED(c, "vix");
+            }
+            cudaEventRecord(c->ev_k1, c->stream);
+        }
         st = TXS_OK;
     } else {
         if (ensure(c, "vix", (void**)&c->d_zt, &c->zt_cap, sizeof(int16_t) * c->z_rows * c->ncols) != TXS_OK)
