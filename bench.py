@@ -59,7 +59,7 @@ def dist_env():
 # SITE in full (lazy greedy over every candidate's viewshed) except at C5,
 # where 1M R=250 viewsheds cannot be built on the host in minutes: there SITE
 # runs on the candidates of the top-left 1/16 sub-square with 1/16 of the picks.
-SAMPLE_PLAN = {"c1": (1, 1, True), "c2": (16, 16, True), "c3": (256, 64, True), "c4": (1024, 64, True),
+SAMPLE_PLAN = {"c1": (1, 1, True), "c2": (1, 1, True), "c3": (256, 64, True), "c4": (1024, 64, True),
                "c5": (0, 1024, False)}
 
 
