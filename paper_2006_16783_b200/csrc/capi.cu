@@ -812,8 +812,13 @@ txs_status txs_run_pipeline_host(txs_ctx* c, const int16_t* z, int64_t nrows, in
     st = set_dims(c, nrows, ncols);
     if (st != TXS_OK) return st;
     if (!c->copy_stream) TXS_CUDA(c, "read", cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-    // ~16 chunks of whole 64-row multiples, on the copy stream, one event each
-    const int64_t ch = std::max<int64_t>(64, ((nrows + 15) / 16 + 63) / 64 * 64);
+    // ~16 chunks of whole 64-row multiples, on the copy stream, one event each;
+    // below 128 MB one chunk (the upload is short, and VIX bands over a small
+    // grid would each fill only part of the GPU: c1 e2e 4.1 -> 10.9 ms banded)
+    const bool small = (double)nrows * (double)ncols * sizeof(int16_t) < (double)(128 << 20);
+    int64_t ch = small ? std::max<int64_t>(1, nrows) : std::max<int64_t>(64, ((nrows + 15) / 16 + 63) / 64 * 64);
+    if (const char* e = getenv("TXS_UPLOAD_CHUNK_ROWS"))   // tests / A/B (whole 64-row multiples)
+        ch = std::max<int64_t>(64, (atoll(e) + 63) / 64 * 64);
     const size_t nch = (size_t)((nrows + ch - 1) / ch);
     while (c->up_ev.size() < nch) {
         cudaEvent_t e = nullptr;
