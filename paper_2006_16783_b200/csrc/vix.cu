@@ -778,6 +778,75 @@ __device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int la
     return __ballot_sync(kFull, vis);
 }
 
+// Per-lane form of the skip test (16-step groups, where almost every group
+// passes): each lane runs the skip test over its own segment's groups, with no
+// cross-lane compaction.  The walk position is carried incrementally: the
+// minor offset of step gi*G + 1 plus the start block's offset c0 sits in the
+// high bits of acc (acc >> 16 = c0 + floor((gi G + 1) m / M)), and the LOS
+// bound grows by G D per group.  Lanes with failing groups (rare) are then
+// walked one at a time: one coalesced 32-step pass from each failing group
+// (32 >> GS groups per pass), stopping at the first block.
+template <int GS, bool TERR>
+__device__ __forceinline__ unsigned batch_skip_lane(const QuadGeom& g, int ns, int lane, QuadGeom* s_geo,
+                                                    const int16_t* __restrict__ smap, const QuadPitch& P,
+                                                    unsigned* tiem) {
+    constexpr int kSpan = 32 >> GS;   // groups covered by one 32-step pass
+    const int nM = g.c.w & 0xff;
+    const int ng = (lane < ns && nM >= 2) ? (nM + (1 << GS) - 2) >> GS : 0;
+    unsigned fm = 0;   // failing groups of this lane's segment
+    if (ng > 0) {
+        const int mag = (unsigned)g.c.w >> 15, c0 = (g.c.w >> 8) & 31;
+        const int sp = (g.c.w & 0x2000) ? P.pt : P.pv;
+        const int ssp = (g.c.w & 0x4000) ? -sp : sp;
+        const int16_t* S = smap + g.c.soff;
+        int acc = mag + (c0 << 16), rhs = g.c.LE2;
+        for (int gi = 0; gi < ng; ++gi) {
+            const int smax = __ldg(S + gi + (acc >> (16 + GS)) * ssp);
+            fm |= (unsigned)(smax * nM > rhs) << gi;
+            acc += mag << GS;
+            rhs += g.c.DG;
+        }
+    }
+    unsigned F = __ballot_sync(kFull, fm != 0u);
+    unsigned blk = 0, tie = 0;   // bit l: lane l's segment blocked / has a grazing tie
+    if (F) {
+        if (fm) s_geo[lane] = g;
+        __syncwarp();
+        while (F) {
+            const int sl = __ffs(F) - 1;
+            F &= F - 1;
+            unsigned m = __shfl_sync(kFull, fm, sl);
+            const QuadGeomC c = s_geo[sl].c;
+            const QuadGeomF f = s_geo[sl].f;
+            const int sM = c.w & 0xff, nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 15, D = c.DG >> GS;
+            while (m) {
+                const int gi = __ffs(m) - 1;
+                m &= ~(((1u << kSpan) - 1u) << gi);
+                const int i = (gi << GS) + 1 + lane;
+                int d = 0;   // margin: > 0 z >= LOS (a block or a grazing tie), > 1 z > LOS (a block)
+                if (i < sM) {
+                    const int q = (i * mag) >> 16, r = i * nm - q * sM;
+                    const int rhsM = c.LE2 - min(0, c.DG) + i * D, rhsm = f.Esn + q * D;
+                    if (TERR) {
+                        d = terrain_margin((const int16_t*)f.Q, i, q, r, sM, nm, sm, (c.w & 0x2000) ? P.zs : 1, rhsM, rhsm);
+                    } else {
+                        const uint32_t wb = (uint32_t)sM | ((uint32_t)nm << 24);
+                        d = quad_margin(qld(f.Q + i + q * sm), r, nm, wb, rhsM, rhsm);
+                    }
+                }
+                if (__any_sync(kFull, d > 0)) {
+                    if (__any_sync(kFull, d > 1)) { blk |= 1u << sl; break; }
+                    tie |= 1u << sl;
+                }
+            }
+        }
+        __syncwarp();
+    }
+    const bool vis = lane < ns && !((blk >> lane) & 1u);
+    *tiem = __ballot_sync(kFull, vis && ((tie >> lane) & 1u));
+    return __ballot_sync(kFull, vis);
+}
+
 template <int SKIP, int U, int GS>
 __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16_t* __restrict__ z,
                                                                    const uint2* __restrict__ qp, int nrows, int ncols,
@@ -795,7 +864,7 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
     int* s_q = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + kVixWarps * (kFailInts + 32) + warp_of_thread() * 64;
     const QuadPitch PQ{a.pv, a.pt, ncols};
     // 16-step skip groups (roi < 150): failing units walk the terrain, no quad planes
-    constexpr bool TERR = SKIP == 1 && GS == 4;
+    constexpr bool TERR = (SKIP == 1 || SKIP == 3) && GS == 4;
     const int lane = threadIdx.x & 31;
     // mag = ceil(2^16 m / M) for every M <= 255: floor(x / M) = (x * ceil(2^40 / M)) >> 40
     // exactly for x < 2^24 (the error x (ceil - 2^40/M) / 2^40 < 2^-16 < 1/M)
@@ -865,6 +934,8 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
         unsigned vism, tiem;
         if constexpr (SKIP == 1) {
             vism = batch_skip<U, GS, TERR>(g, ns, lane, s_geo, s_pre, s_fail, smap, PQ, &tiem);
+        } else if constexpr (SKIP == 3) {
+            vism = batch_skip_lane<GS, TERR>(g, ns, lane, s_geo, smap, PQ, &tiem);
         } else {
             s_geo[lane] = g;
             __syncwarp();
@@ -1168,7 +1239,9 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         if (const char* e = getenv("TXS_VIX_UNIT")) unit = atoi(e);
         decltype(&k_vix_quads<1, 8, 2>) kq;
         if (skip == 1) {
-            if (gs == 4) kq = unit == 1 ? k_vix_quads<1, 1, 4> : k_vix_quads<1, 2, 4>;
+            // per-lane skip tests (batch_skip_lane) at 16-step groups; TXS_VIX_LANESKIP=0: flattened units
+            static const bool lane_skip = !getenv("TXS_VIX_LANESKIP") || atoi(getenv("TXS_VIX_LANESKIP")) != 0;
+            if (gs == 4) kq = lane_skip ? k_vix_quads<3, 2, 4> : (unit == 1 ? k_vix_quads<1, 1, 4> : k_vix_quads<1, 2, 4>);
             else kq = unit == 8 ? k_vix_quads<1, 8, 2> : k_vix_quads<1, 4, 2>;
         } else if (skip == 2) {
             kq = gs == 4 ? k_vix_quads<2, 8, 4> : k_vix_quads<2, 8, 2>;
