@@ -330,7 +330,7 @@ def stage_figures(st, K, cfg, site_mode, site_stream=None):
     peaks = load_peaks()
     stages = {}
     if cfg.samples:
-        kern = "k_vix_quads" if cfg.roi <= 255 else "k_vix"
+        kern = ("k_vix_lanes" if cfg.samples <= 32 else "k_vix_quads") if cfg.roi <= 255 else "k_vix"
         stages["vix"] = {"ms": round(st["ms_vix"] / K, 3),
                          **los_roof("vix", kern, st["ms_vix_kernel"] / K, st["vix_crossings_full"] / K, cfg, peaks)}
         stages["findmax"] = {"ms": round(st["ms_findmax"] / K, 3), "kernel": "k_findmax"}

@@ -778,8 +778,8 @@ __device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int la
     return __ballot_sync(kFull, vis);
 }
 
-// Per-lane form of the skip test (16-step groups, where almost every group
-// passes): each lane runs the skip test over its own segment's groups, with no
+// Per-lane form of the skip test (measured: c3 VIX 102.7 -> 78.3 ms, c4 811 ->
+// 617, c2 (4-step groups, 19 % failing) 40.0 -> 35.4 against batch_skip): each lane runs the skip test over its own segment's groups, with no
 // cross-lane compaction.  The walk position is carried incrementally: the
 // minor offset of step gi*G + 1 plus the start block's offset c0 sits in the
 // high bits of acc (acc >> 16 = c0 + floor((gi G + 1) m / M)), and the LOS
@@ -793,7 +793,8 @@ __device__ __forceinline__ unsigned batch_skip_lane(const QuadGeom& g, int ns, i
     constexpr int kSpan = 32 >> GS;   // groups covered by one 32-step pass
     const int nM = g.c.w & 0xff;
     const int ng = (lane < ns && nM >= 2) ? (nM + (1 << GS) - 2) >> GS : 0;
-    unsigned fm = 0;   // failing groups of this lane's segment
+    using Mask = typename std::conditional<(GS >= 3), unsigned, unsigned long long>::type;   // <= 63 groups
+    Mask fm = 0;   // failing groups of this lane's segment
     if (ng > 0) {
         const int mag = (unsigned)g.c.w >> 15, c0 = (g.c.w >> 8) & 31;
         const int sp = (g.c.w & 0x2000) ? P.pt : P.pv;
@@ -802,12 +803,12 @@ __device__ __forceinline__ unsigned batch_skip_lane(const QuadGeom& g, int ns, i
         int acc = mag + (c0 << 16), rhs = g.c.LE2;
         for (int gi = 0; gi < ng; ++gi) {
             const int smax = __ldg(S + gi + (acc >> (16 + GS)) * ssp);
-            fm |= (unsigned)(smax * nM > rhs) << gi;
+            fm |= (Mask)(smax * nM > rhs) << gi;
             acc += mag << GS;
             rhs += g.c.DG;
         }
     }
-    unsigned F = __ballot_sync(kFull, fm != 0u);
+    unsigned F = __ballot_sync(kFull, fm != 0);
     unsigned blk = 0, tie = 0;   // bit l: lane l's segment blocked / has a grazing tie
     if (F) {
         if (fm) s_geo[lane] = g;
@@ -815,13 +816,13 @@ __device__ __forceinline__ unsigned batch_skip_lane(const QuadGeom& g, int ns, i
         while (F) {
             const int sl = __ffs(F) - 1;
             F &= F - 1;
-            unsigned m = __shfl_sync(kFull, fm, sl);
+            Mask m = __shfl_sync(kFull, fm, sl);
             const QuadGeomC c = s_geo[sl].c;
             const QuadGeomF f = s_geo[sl].f;
             const int sM = c.w & 0xff, nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 15, D = c.DG >> GS;
             while (m) {
-                const int gi = __ffs(m) - 1;
-                m &= ~(((1u << kSpan) - 1u) << gi);
+                const int gi = sizeof(Mask) == 4 ? __ffs((unsigned)m) - 1 : __ffsll((long long)m) - 1;
+                m &= ~((((Mask)1 << kSpan) - 1) << gi);
                 const int i = (gi << GS) + 1 + lane;
                 int d = 0;   // margin: > 0 z >= LOS (a block or a grazing tie), > 1 z > LOS (a block)
                 if (i < sM) {
@@ -845,6 +846,52 @@ __device__ __forceinline__ unsigned batch_skip_lane(const QuadGeom& g, int ns, i
     const bool vis = lane < ns && !((blk >> lane) & 1u);
     *tiem = __ballot_sync(kFull, vis && ((tie >> lane) & 1u));
     return __ballot_sync(kFull, vis);
+}
+
+// Walk geometry of the segment from post (r, c) (observer elevation E) to
+// (r + dr0, c + dc0): the skip-test record (soff, LE2, DG, w) and the
+// exact-walk record (start address, Esn, msm); n_cross counts its crossings.
+template <int GS, bool TERR>
+__device__ __forceinline__ QuadGeom seg_quad_geom(const int16_t* __restrict__ z, const uint2* __restrict__ qp, int ncols,
+                                                  const VixArgs& a, const uint8_t* __restrict__ gcdt,
+                                                  const unsigned long long* s_rcp40, int r, int c, int E, int dr0, int dc0,
+                                                  unsigned long long& n_cross) {
+    QuadGeom g{};
+    const int H = a.zr1 - a.zr0;
+    int dr = dr0, dc = dc0;
+    const int Zt = zld(z + (int64_t)(r + dr) * ncols + (c + dc)) + a.hr;
+    n_cross += crossings_tab(dr, dc, gcdt);
+    const bool tr = abs(dr) > abs(dc);
+    const bool rev = tr ? dr < 0 : dc < 0;      // walk from the receiver
+    const int y = r - a.zr0 + (rev ? dr : 0), x = c + (rev ? dc : 0);   // start post
+    if (rev) { dr = -dr; dc = -dc; }
+    const int nM = tr ? dr : dc, nm = tr ? abs(dc) : abs(dr);
+    const bool mneg = (tr ? dc : dr) < 0;
+    const int64_t n = (int64_t)H * a.wp, nT = (int64_t)ncols * a.hp;
+    const int stride = tr ? a.hp : a.wp;
+    const int Es = rev ? Zt : E;
+    if (TERR) {
+        g.f.Q = (const uint2*)(z + (int64_t)(y + a.zr0) * ncols + x);
+        const int zstep = tr ? 1 : ncols;   // minor axis: columns for row-major walks
+        g.f.msm = nm | ((nm == 0 ? 0 : (mneg ? -zstep : zstep)) * 256);
+    } else {
+        g.f.Q = qp + (tr ? 2 * n + (int64_t)x * a.hp + y + (mneg ? nT : 0) : (int64_t)y * a.wp + x + (mneg ? n : 0));
+        g.f.msm = nm | ((nm == 0 ? 0 : (mneg ? -stride : stride)) * 256);
+    }
+    g.f.Esn = Es * nm - 1;
+    // skip map (k_skipmap): padded 4x4-block indices of the start post,
+    // SV row-major for column-major walks, ST column-major for row-major ones
+    const int maj = tr ? y : x, mnr = tr ? x : y;
+    const int mag = (int)(((unsigned long long)(nm * 65536 + nM - 1) * s_rcp40[nM]) >> 40);   // 0 when M = 0
+    g.c.soff = tr ? a.st_off + ((maj >> GS) + 1) + ((mnr >> GS) + 1) * a.pt
+                  : ((maj >> GS) + 1) + ((mnr >> GS) + 1) * a.pv;
+    const int D = rev ? E - Zt : Zt - E;
+    constexpr int G = 1 << GS;
+    g.c.LE2 = Es * nM + min(0, G * D) - 1;
+    g.c.DG = G * D;
+    const int mo = mnr & (G - 1);
+    g.c.w = nM | ((mneg ? 2 * G - 1 - mo : mo) << 8) | ((int)tr << 13) | ((int)mneg << 14) | (mag << 15);
+    return g;
 }
 
 template <int SKIP, int U, int GS>
@@ -894,42 +941,7 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
         const int pj = (pk >> 18) & (kRing - 1);
         const int E = __shfl_sync(kFull, myE, pj), r = __shfl_sync(kFull, myR, pj), c = __shfl_sync(kFull, myC, pj);
         const int dr0 = (pk & 0x1ff) - 256, dc0 = ((pk >> 9) & 0x1ff) - 256;   // transmitter frame
-        if (lane < ns) {
-            const int H = a.zr1 - a.zr0;
-            int dr = dr0, dc = dc0;
-            const int Zt = zld(z + (int64_t)(r + dr) * ncols + (c + dc)) + a.hr;
-            n_cross += crossings_tab(dr, dc, gcdt);
-            const bool tr = abs(dr) > abs(dc);
-            const bool rev = tr ? dr < 0 : dc < 0;      // walk from the receiver
-            const int y = r - a.zr0 + (rev ? dr : 0), x = c + (rev ? dc : 0);   // start post
-            if (rev) { dr = -dr; dc = -dc; }
-            const int nM = tr ? dr : dc, nm = tr ? abs(dc) : abs(dr);
-            const bool mneg = (tr ? dc : dr) < 0;
-            const int64_t n = (int64_t)H * a.wp, nT = (int64_t)ncols * a.hp;
-            const int stride = tr ? a.hp : a.wp;
-            const int Es = rev ? Zt : E;
-            if (TERR) {
-                g.f.Q = (const uint2*)(z + (int64_t)(y + a.zr0) * ncols + x);
-                const int zstep = tr ? 1 : ncols;   // minor axis: columns for row-major walks
-                g.f.msm = nm | ((nm == 0 ? 0 : (mneg ? -zstep : zstep)) * 256);
-            } else {
-                g.f.Q = qp + (tr ? 2 * n + (int64_t)x * a.hp + y + (mneg ? nT : 0) : (int64_t)y * a.wp + x + (mneg ? n : 0));
-                g.f.msm = nm | ((nm == 0 ? 0 : (mneg ? -stride : stride)) * 256);
-            }
-            g.f.Esn = Es * nm - 1;
-            // skip map (k_skipmap): padded 4x4-block indices of the start post,
-            // SV row-major for column-major walks, ST column-major for row-major ones
-            const int maj = tr ? y : x, mnr = tr ? x : y;
-            const int mag = (int)(((unsigned long long)(nm * 65536 + nM - 1) * s_rcp40[nM]) >> 40);   // 0 when M = 0
-            g.c.soff = tr ? a.st_off + ((maj >> GS) + 1) + ((mnr >> GS) + 1) * a.pt
-                          : ((maj >> GS) + 1) + ((mnr >> GS) + 1) * a.pv;
-            const int D = rev ? E - Zt : Zt - E;
-            constexpr int G = 1 << GS;
-            g.c.LE2 = Es * nM + min(0, G * D) - 1;
-            g.c.DG = G * D;
-            const int mo = mnr & (G - 1);
-            g.c.w = nM | ((mneg ? 2 * G - 1 - mo : mo) << 8) | ((int)tr << 13) | ((int)mneg << 14) | (mag << 15);
-        }
+        if (lane < ns) g = seg_quad_geom<GS, TERR>(z, qp, ncols, a, gcdt, s_rcp40, r, c, E, dr0, dc0, n_cross);
         __syncwarp();
         unsigned vism, tiem;
         if constexpr (SKIP == 1) {
@@ -1034,6 +1046,101 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
         atomicAdd(counters + kVixCrossFull, n_cross);
     }
 }
+
+// One post per lane (S <= kLaneDrawMaxS, item rows of 32 posts): lane l draws
+// its own post's S receivers (D6: pair i of the post's stream is draws 2i,
+// 2i+1; rejected pairs are skipped) into column l of the warp's
+// [sample][lane] table, then batch k tests sample k of every post -- the
+// lanes of a batch are the row's 32 posts, so the observer, its elevation and
+// its visible count stay in the lane's registers (no receiver FIFO, no ring of
+// open posts, no shuffles per batch).
+constexpr int kLaneDrawMaxS = 32;
+template <int GS>
+__global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_lanes(const int16_t* __restrict__ z,
+                                                                   const uint2* __restrict__ qp, int nrows, int ncols,
+                                                                   uint8_t* __restrict__ out, VixArgs a,
+                                                                   const uint8_t* __restrict__ gcdt,
+                                                                   const int16_t* __restrict__ smap,
+                                                                   unsigned long long* __restrict__ counters) {
+    static_assert(kTileQ == 32, "one post per lane");
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    // dynamic smem: [geometry: kVixWarps x 32][samples: kVixWarps x S x 32 ints]
+    QuadGeom* s_geo = (QuadGeom*)s_dyn + warp_of_thread() * 32;
+    int* s_smp = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + warp_of_thread() * a.S * 32;
+    const QuadPitch PQ{a.pv, a.pt, ncols};
+    constexpr bool TERR = GS == 4;
+    const int lane = threadIdx.x & 31;
+    __shared__ unsigned long long s_rcp40[256];
+    for (int d = threadIdx.x; d < 256; d += blockDim.x) s_rcp40[d] = d ? ((1ull << 40) + d - 1) / d : 0ull;
+    __syncthreads();
+    const int R2 = a.R * a.R, S = a.S;
+    unsigned long long n_cross = 0;
+    int n_posts = 0;
+    const int strip_tiles = a.strip * a.tiles_y;
+    for (;;) {
+        long long item = 0;
+        if (lane == 0) item = (long long)atomicAdd(counters + kVixNext, 1ull);
+        item = __shfl_sync(kFull, item, 0);
+        const int64_t tile = item / kTileQ;
+        if (tile >= (int64_t)a.tiles_x * a.tiles_y) break;
+        int ty, tx;
+        {
+            const int sidx = (int)(tile / strip_tiles), rem = (int)(tile - (int64_t)sidx * strip_tiles);
+            const int sw = min(a.strip, a.tiles_x - sidx * a.strip);
+            ty = rem / sw;
+            tx = sidx * a.strip + (rem - ty * sw);
+        }
+        const int r = a.row0 + ty * kTileQ + item % kTileQ;
+        if (r >= a.row_end) continue;
+        const int c = tx * kTileQ + lane;
+        const int np = min(32, ncols - tx * kTileQ);   // posts of this item row: lanes 0 .. np-1
+        const bool has = lane < np;
+        int E = 0, nacc = S;
+        uint64_t x = 0;
+        if (has) {
+            x = mix_seed(a.seed, (uint64_t)r, (uint64_t)c);
+            E = zld(z + (int64_t)r * ncols + c) + a.ht;
+            nacc = 0;
+        }
+        n_posts += np * (lane == 0);
+        // ---- draw: the lane's S receivers (D6) ----
+        while (nacc < S) {
+            x += kGamma;
+            const int dr = (int)fm_mod(a.span, sm_finalize(x)) - a.R;
+            x += kGamma;
+            const int dc = (int)fm_mod(a.span, sm_finalize(x)) - a.R;
+            if (dr * dr + dc * dc <= R2 && (unsigned)(r + dr) < (unsigned)nrows && (unsigned)(c + dc) < (unsigned)ncols) {
+                s_smp[nacc * 32 + lane] = (dr + 256) | ((dc + 256) << 9);
+                ++nacc;
+            }
+        }
+        __syncwarp();
+        // ---- batch k: sample k of every post of the row ----
+        int cnt = 0;
+        for (int k = 0; k < S; ++k) {
+            QuadGeom g{};
+            int dr0 = 0, dc0 = 0;
+            if (has) {
+                const int pk = s_smp[k * 32 + lane];
+                dr0 = (pk & 0x1ff) - 256;
+                dc0 = ((pk >> 9) & 0x1ff) - 256;
+                g = seg_quad_geom<GS, TERR>(z, qp, ncols, a, gcdt, s_rcp40, r, c, E, dr0, dc0, n_cross);
+            }
+            unsigned tiem;
+            const unsigned vism = batch_skip_lane<GS, TERR>(g, np, lane, s_geo, smap, PQ, &tiem);
+            if ((tiem >> lane) & 1u) push_tie(a, counters, r, c, dr0, dc0);
+            cnt += (vism >> lane) & 1u;
+        }
+        if (has) out[(int64_t)r * ncols + c] = (uint8_t)cnt;
+        __syncwarp();
+    }
+    for (int o = 16; o; o >>= 1) n_cross += __shfl_down_sync(kFull, n_cross, o);
+    if (lane == 0 && n_posts) {
+        atomicAdd(counters + kVixLos, (unsigned long long)n_posts * a.S);
+        atomicAdd(counters + kVixCrossFull, n_cross);
+    }
+}
+
 
 // Skip map of the skip tests.  Pass 1: per GxG block the maximum elevation,
 // stored with one block of padding on every side (padded index = block + 1;
@@ -1231,7 +1338,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         }
         const uint2* qp = (const uint2*)c->d_pairs;
         set_zbounds(c->d_z, c->d_z + n, c->stream, (const int16_t*)qp, (const int16_t*)(qp + nq));
-        const size_t qsm = (sizeof(QuadGeom) * 32 + sizeof(int) * (32 + 32 + 64)) * kVixWarps;
+        size_t qsm = (sizeof(QuadGeom) * 32 + sizeof(int) * (32 + 32 + 64)) * kVixWarps;
         // groups per skip unit (measured, profiles/README.md): 8 at roi 200 (C2 46.6 -> 43.5 ms
         // vs 4), 4 at roi 100 (C3 190.6 -> 180.2 vs 8)
         // G = 16: units of 2 groups (32 steps, TXS_VIX_UNIT=1 for 16)
@@ -1239,16 +1346,22 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         if (const char* e = getenv("TXS_VIX_UNIT")) unit = atoi(e);
         decltype(&k_vix_quads<1, 8, 2>) kq;
         if (skip == 1) {
-            // per-lane skip tests (batch_skip_lane) at 16-step groups; TXS_VIX_LANESKIP=0: flattened units
+            // per-lane skip tests (batch_skip_lane); TXS_VIX_LANESKIP=0: flattened units (batch_skip)
             static const bool lane_skip = !getenv("TXS_VIX_LANESKIP") || atoi(getenv("TXS_VIX_LANESKIP")) != 0;
             if (gs == 4) kq = lane_skip ? k_vix_quads<3, 2, 4> : (unit == 1 ? k_vix_quads<1, 1, 4> : k_vix_quads<1, 2, 4>);
-            else kq = unit == 8 ? k_vix_quads<1, 8, 2> : k_vix_quads<1, 4, 2>;
+            else kq = lane_skip ? k_vix_quads<3, 8, 2> : (unit == 8 ? k_vix_quads<1, 8, 2> : k_vix_quads<1, 4, 2>);
+            // one post per lane (k_vix_lanes) for S <= 32; TXS_VIX_LANEDRAW=0: the per-warp receiver FIFO
+            static const bool lane_draw = !getenv("TXS_VIX_LANEDRAW") || atoi(getenv("TXS_VIX_LANEDRAW")) != 0;
+            if (lane_skip && lane_draw && p.samples_per_point <= kLaneDrawMaxS) {
+                kq = gs == 4 ? k_vix_lanes<4> : k_vix_lanes<2>;
+                qsm = (sizeof(QuadGeom) * 32 + sizeof(int) * 32 * (size_t)std::max(1, p.samples_per_point)) * kVixWarps;
+            }
         } else if (skip == 2) {
             kq = gs == 4 ? k_vix_quads<2, 8, 4> : k_vix_quads<2, 8, 2>;
         } else {
             kq = gs == 4 ? k_vix_quads<0, 8, 4> : k_vix_quads<0, 8, 2>;
         }
-        if (qsm > 48 * 1024)
+        if (qsm > 40 * 1024)   // (the kernels' static shared memory counts against the default 48 KB)
             TXS_CUDA(c, "vix", cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm));
         if (!c->d_gcd) {
             TXS_CUDA(c, "vix", cudaMalloc((void**)&c->d_gcd, 256 * 256));
