@@ -779,54 +779,89 @@ __device__ __forceinline__ unsigned batch_skip(const QuadGeom& g, int ns, int la
 }
 
 // Per-lane form of the skip test (measured: c3 VIX 102.7 -> 78.3 ms, c4 811 ->
-// 617, c2 (4-step groups, 19 % failing) 40.0 -> 35.4 against batch_skip): each lane runs the skip test over its own segment's groups, with no
-// cross-lane compaction.  The walk position is carried incrementally: the
-// minor offset of step gi*G + 1 plus the start block's offset c0 sits in the
-// high bits of acc (acc >> 16 = c0 + floor((gi G + 1) m / M)), and the LOS
-// bound grows by G D per group.  Lanes with failing groups (rare) are then
-// walked one at a time: one coalesced 32-step pass from each failing group
+// 617, c2 (4-step groups, 19 % failing) 40.0 -> 35.4 against batch_skip): each
+// lane runs the skip test over its own segment's groups, with no cross-lane
+// compaction, keeping one "some group failed" flag.  The walk position is
+// carried incrementally: the minor offset of step gi*G + 1 plus the start
+// block's offset c0 sits in the high bits of acc (acc >> 16 = c0 +
+// floor((gi G + 1) m / M)), and the LOS bound grows by G D per group.  Lanes
+// with a failing group (rare) build their exact-walk record (walk_rec) and are
+// walked one at a time: the warp re-tests that segment's groups (lane =
+// group), then runs one coalesced 32-step pass from each failing group
 // (32 >> GS groups per pass), stopping at the first block.
-template <int GS, bool TERR>
-__device__ __forceinline__ unsigned batch_skip_lane(const QuadGeom& g, int ns, int lane, QuadGeom* s_geo,
+template <int GS, bool TERR, bool MASK, class WalkRec>
+__device__ __forceinline__ unsigned batch_skip_lane(const QuadGeomC& gc, int ns, int lane, QuadGeom* s_geo,
                                                     const int16_t* __restrict__ smap, const QuadPitch& P,
-                                                    unsigned* tiem) {
+                                                    unsigned* tiem, WalkRec walk_rec) {
     constexpr int kSpan = 32 >> GS;   // groups covered by one 32-step pass
-    const int nM = g.c.w & 0xff;
-    const int ng = (lane < ns && nM >= 2) ? (nM + (1 << GS) - 2) >> GS : 0;
     using Mask = typename std::conditional<(GS >= 3), unsigned, unsigned long long>::type;   // <= 63 groups
-    Mask fm = 0;   // failing groups of this lane's segment
-    if (ng > 0) {
-        const int mag = (unsigned)g.c.w >> 15, c0 = (g.c.w >> 8) & 31;
-        const int sp = (g.c.w & 0x2000) ? P.pt : P.pv;
-        const int ssp = (g.c.w & 0x4000) ? -sp : sp;
-        const int16_t* S = smap + g.c.soff;
-        int acc = mag + (c0 << 16), rhs = g.c.LE2;
-        for (int gi = 0; gi < ng; ++gi) {
-            const int smax = __ldg(S + gi + (acc >> (16 + GS)) * ssp);
-            fm |= (Mask)(smax * nM > rhs) << gi;
-            acc += mag << GS;
-            rhs += g.c.DG;
+    const int nM = gc.w & 0xff;
+    const int ng = (lane < ns && nM >= 2) ? (nM + (1 << GS) - 2) >> GS : 0;
+    // map entry of group gi: soff + gi + ((acc0 + gi G mag) >> (16 + GS)) * ssp
+    const int mag = (unsigned)gc.w >> 15, acc0 = mag + (((gc.w >> 8) & 31) << 16);
+    const int sp = (gc.w & 0x2000) ? P.pt : P.pv;
+    const int ssp = (gc.w & 0x4000) ? -sp : sp;
+    bool fail = false;
+    Mask fm = 0;   // (MASK) the failing groups themselves
+    {
+        // 4-step groups (up to 63 per segment): four groups per iteration, their map
+        // loads issued together (c2 40.6 -> 34.0 ms); 16-step groups (<= 10): one
+        // per iteration (c3 49.9 -> 45.6 against four)
+        constexpr int kU = GS >= 4 ? 1 : 4;
+        int acc = acc0, rhs = gc.LE2, idx = gc.soff;
+        for (int g0 = 0; g0 < ng; g0 += kU) {
+            int sv[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u)
+                sv[u] = (kU == 1 || g0 + u < ng) ? __ldg(smap + (idx + u + ((acc + u * (mag << GS)) >> (16 + GS)) * ssp)) : 0;
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const bool f = (kU == 1 || g0 + u < ng) && sv[u] * nM > rhs + u * gc.DG;
+                if (MASK) fm |= (Mask)f << (g0 + u);
+                else fail |= f;
+            }
+            acc += kU * (mag << GS);
+            rhs += kU * gc.DG;
+            idx += kU;
         }
     }
-    unsigned F = __ballot_sync(kFull, fm != 0);
+    if (MASK) fail = fm != 0;
+    unsigned F = __ballot_sync(kFull, fail);
     unsigned blk = 0, tie = 0;   // bit l: lane l's segment blocked / has a grazing tie
     if (F) {
-        if (fm) s_geo[lane] = g;
+        if (fail) s_geo[lane] = QuadGeom{gc, walk_rec()};   // the walk record, built only when needed
         __syncwarp();
         while (F) {
             const int sl = __ffs(F) - 1;
             F &= F - 1;
-            Mask m = __shfl_sync(kFull, fm, sl);
             const QuadGeomC c = s_geo[sl].c;
             const QuadGeomF f = s_geo[sl].f;
-            const int sM = c.w & 0xff, nm = f.msm & 0xff, sm = f.msm >> 8, mag = (unsigned)c.w >> 15, D = c.DG >> GS;
+            const int sM = c.w & 0xff, nm = f.msm & 0xff, sm = f.msm >> 8, cmag = (unsigned)c.w >> 15, D = c.DG >> GS;
+            // the segment's failing groups, re-tested cooperatively (lane = group)
+            Mask m = 0;
+            if (MASK) {
+                m = __shfl_sync(kFull, fm, sl);
+            } else {
+                const int sng = (sM + (1 << GS) - 2) >> GS;
+                const int csp = (c.w & 0x2000) ? P.pt : P.pv, cssp = (c.w & 0x4000) ? -csp : csp;
+                const int cacc0 = cmag + (((c.w >> 8) & 31) << 16);
+                for (int base = 0; base < sng; base += 32) {
+                    const int gi = base + lane;
+                    bool fl = false;
+                    if (gi < sng) {
+                        const int smax = __ldg(smap + (c.soff + gi + ((cacc0 + gi * (cmag << GS)) >> (16 + GS)) * cssp));
+                        fl = smax * sM > c.LE2 + gi * c.DG;
+                    }
+                    m |= (Mask)__ballot_sync(kFull, fl) << base;
+                }
+            }
             while (m) {
                 const int gi = sizeof(Mask) == 4 ? __ffs((unsigned)m) - 1 : __ffsll((long long)m) - 1;
                 m &= ~((((Mask)1 << kSpan) - 1) << gi);
                 const int i = (gi << GS) + 1 + lane;
                 int d = 0;   // margin: > 0 z >= LOS (a block or a grazing tie), > 1 z > LOS (a block)
                 if (i < sM) {
-                    const int q = (i * mag) >> 16, r = i * nm - q * sM;
+                    const int q = (i * cmag) >> 16, r = i * nm - q * sM;
                     const int rhsM = c.LE2 - min(0, c.DG) + i * D, rhsm = f.Esn + q * D;
                     if (TERR) {
                         d = terrain_margin((const int16_t*)f.Q, i, q, r, sM, nm, sm, (c.w & 0x2000) ? P.zs : 1, rhsM, rhsm);
@@ -851,7 +886,7 @@ __device__ __forceinline__ unsigned batch_skip_lane(const QuadGeom& g, int ns, i
 // Walk geometry of the segment from post (r, c) (observer elevation E) to
 // (r + dr0, c + dc0): the skip-test record (soff, LE2, DG, w) and the
 // exact-walk record (start address, Esn, msm); n_cross counts its crossings.
-template <int GS, bool TERR>
+template <int GS, bool TERR, bool WALK = true>
 __device__ __forceinline__ QuadGeom seg_quad_geom(const int16_t* __restrict__ z, const uint2* __restrict__ qp, int ncols,
                                                   const VixArgs& a, const uint8_t* __restrict__ gcdt,
                                                   const unsigned long long* s_rcp40, int r, int c, int E, int dr0, int dc0,
@@ -870,7 +905,8 @@ __device__ __forceinline__ QuadGeom seg_quad_geom(const int16_t* __restrict__ z,
     const int64_t n = (int64_t)H * a.wp, nT = (int64_t)ncols * a.hp;
     const int stride = tr ? a.hp : a.wp;
     const int Es = rev ? Zt : E;
-    if (TERR) {
+    if (!WALK) {
+    } else if (TERR) {
         g.f.Q = (const uint2*)(z + (int64_t)(y + a.zr0) * ncols + x);
         const int zstep = tr ? 1 : ncols;   // minor axis: columns for row-major walks
         g.f.msm = nm | ((nm == 0 ? 0 : (mneg ? -zstep : zstep)) * 256);
@@ -878,7 +914,7 @@ __device__ __forceinline__ QuadGeom seg_quad_geom(const int16_t* __restrict__ z,
         g.f.Q = qp + (tr ? 2 * n + (int64_t)x * a.hp + y + (mneg ? nT : 0) : (int64_t)y * a.wp + x + (mneg ? n : 0));
         g.f.msm = nm | ((nm == 0 ? 0 : (mneg ? -stride : stride)) * 256);
     }
-    g.f.Esn = Es * nm - 1;
+    if (WALK) g.f.Esn = Es * nm - 1;
     // skip map (k_skipmap): padded 4x4-block indices of the start post,
     // SV row-major for column-major walks, ST column-major for row-major ones
     const int maj = tr ? y : x, mnr = tr ? x : y;
@@ -947,7 +983,7 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
         if constexpr (SKIP == 1) {
             vism = batch_skip<U, GS, TERR>(g, ns, lane, s_geo, s_pre, s_fail, smap, PQ, &tiem);
         } else if constexpr (SKIP == 3) {
-            vism = batch_skip_lane<GS, TERR>(g, ns, lane, s_geo, smap, PQ, &tiem);
+            vism = batch_skip_lane<GS, TERR, true>(g.c, ns, lane, s_geo, smap, PQ, &tiem, [&] { return g.f; });
         } else {
             s_geo[lane] = g;
             __syncwarp();
@@ -1055,7 +1091,7 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
 // its visible count stay in the lane's registers (no receiver FIFO, no ring of
 // open posts, no shuffles per batch).
 constexpr int kLaneDrawMaxS = 32;
-template <int GS>
+template <int GS, bool MASK, bool LAZY>
 __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_lanes(const int16_t* __restrict__ z,
                                                                    const uint2* __restrict__ qp, int nrows, int ncols,
                                                                    uint8_t* __restrict__ out, VixArgs a,
@@ -1067,6 +1103,7 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_lanes(const int16
     // dynamic smem: [geometry: kVixWarps x 32][samples: kVixWarps x S x 32 ints]
     QuadGeom* s_geo = (QuadGeom*)s_dyn + warp_of_thread() * 32;
     int* s_smp = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + warp_of_thread() * a.S * 32;
+    const uint32_t smp_lane = (uint32_t)__cvta_generic_to_shared(s_smp) + 4u * (threadIdx.x & 31);   // column of this lane
     const QuadPitch PQ{a.pv, a.pt, ncols};
     constexpr bool TERR = GS == 4;
     const int lane = threadIdx.x & 31;
@@ -1110,7 +1147,8 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_lanes(const int16
             x += kGamma;
             const int dc = (int)fm_mod(a.span, sm_finalize(x)) - a.R;
             if (dr * dr + dc * dc <= R2 && (unsigned)(r + dr) < (unsigned)nrows && (unsigned)(c + dc) < (unsigned)ncols) {
-                s_smp[nacc * 32 + lane] = (dr + 256) | ((dc + 256) << 9);
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(smp_lane + (uint32_t)nacc * 128u),
+                             "r"((dr + 256) | ((dc + 256) << 9)));
                 ++nacc;
             }
         }
@@ -1124,10 +1162,14 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_lanes(const int16
                 const int pk = s_smp[k * 32 + lane];
                 dr0 = (pk & 0x1ff) - 256;
                 dc0 = ((pk >> 9) & 0x1ff) - 256;
-                g = seg_quad_geom<GS, TERR>(z, qp, ncols, a, gcdt, s_rcp40, r, c, E, dr0, dc0, n_cross);
+                g = seg_quad_geom<GS, TERR, !LAZY>(z, qp, ncols, a, gcdt, s_rcp40, r, c, E, dr0, dc0, n_cross);
             }
             unsigned tiem;
-            const unsigned vism = batch_skip_lane<GS, TERR>(g, np, lane, s_geo, smap, PQ, &tiem);
+            const unsigned vism = batch_skip_lane<GS, TERR, MASK>(g.c, np, lane, s_geo, smap, PQ, &tiem, [&] {
+                if (!LAZY) return g.f;
+                unsigned long long unused = 0;
+                return seg_quad_geom<GS, TERR, true>(z, qp, ncols, a, gcdt, s_rcp40, r, c, E, dr0, dc0, unused).f;
+            });
             if ((tiem >> lane) & 1u) push_tie(a, counters, r, c, dr0, dc0);
             cnt += (vism >> lane) & 1u;
         }
@@ -1353,7 +1395,14 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
             // one post per lane (k_vix_lanes) for S <= 32; TXS_VIX_LANEDRAW=0: the per-warp receiver FIFO
             static const bool lane_draw = !getenv("TXS_VIX_LANEDRAW") || atoi(getenv("TXS_VIX_LANEDRAW")) != 0;
             if (lane_skip && lane_draw && p.samples_per_point <= kLaneDrawMaxS) {
-                kq = gs == 4 ? k_vix_lanes<4> : k_vix_lanes<2>;
+                // failing-group mask vs one flag + cooperative re-test; walk record eager vs
+                // built only for failing lanes (TXS_VIX_LMODE = mask | lazy << 1)
+                int lm = gs == 4 ? 3 : 1;   // measured: profiles/README.md (VIX one post per lane)
+                if (const char* e = getenv("TXS_VIX_LMODE")) lm = atoi(e) & 3;
+                if (gs == 4) kq = lm == 0 ? k_vix_lanes<4, false, false> : lm == 1 ? k_vix_lanes<4, true, false>
+                                : lm == 2 ? k_vix_lanes<4, false, true> : k_vix_lanes<4, true, true>;
+                else kq = lm == 0 ? k_vix_lanes<2, false, false> : lm == 1 ? k_vix_lanes<2, true, false>
+                        : lm == 2 ? k_vix_lanes<2, false, true> : k_vix_lanes<2, true, true>;
                 qsm = (sizeof(QuadGeom) * 32 + sizeof(int) * 32 * (size_t)std::max(1, p.samples_per_point)) * kVixWarps;
             }
         } else if (skip == 2) {
