@@ -807,7 +807,10 @@ __device__ __forceinline__ unsigned batch_skip_lane(const QuadGeomC& gc, int ns,
         // 4-step groups (up to 63 per segment): four groups per iteration, their map
         // loads issued together (c2 40.6 -> 34.0 ms); 16-step groups (<= 10): one
         // per iteration (c3 49.9 -> 45.6 against four)
-        constexpr int kU = GS >= 4 ? 1 : 4;
+#ifndef VIX_SKIP_U16
+#define VIX_SKIP_U16 1
+#endif
+        constexpr int kU = GS >= 4 ? VIX_SKIP_U16 : 4;
         int acc = acc0, rhs = gc.LE2, idx = gc.soff;
         for (int g0 = 0; g0 < ng; g0 += kU) {
             int sv[kU];
