@@ -324,6 +324,40 @@ __device__ __forceinline__ int crossings_tab(int dr, int dc, const uint8_t* __re
     return a + b - (int)__ldg(gt + (a << 8) + b) - 1;
 }
 
+// x % d for a 64-bit x and a small d (<= 511: 2R+1 with R <= 255) in 32-bit
+// steps: t = hi*(2^32 mod d) + lo < 2^41 (one wide multiply-add), n = (t >> 20)*
+// (2^20 mod d) + (t mod 2^20) < 2^12 d^2 + 2^20 <= 2^30, then
+// floor(n / d) = umulhi(n, m) >> sh with m = ceil(2^(32+sh) / d) < 2^32, exact
+// for every n <= n_max because e n_max < 2^(32+sh), e = m d - 2^(32+sh)
+// (make_smallmod checks it; the identities keep t and n congruent to x mod d).
+struct SmallMod {
+    uint32_t d, k32, k20, m, sh;
+};
+
+inline SmallMod make_smallmod(uint32_t d) {
+    SmallMod f{d, (uint32_t)((1ull << 32) % d), (uint32_t)((1ull << 20) % d), 0, 0};
+    if (d < 2 || d > 511) return SmallMod{0, 0, 0, 0, 0};
+    const uint64_t nmax = ((((uint64_t)d << 32) >> 20) + 1) * (d - 1) + (1u << 20);
+    for (uint32_t sh = 31; sh > 0; --sh) {   // the largest sh with m < 2^32
+        const unsigned __int128 P = (unsigned __int128)1 << (32 + sh);
+        const unsigned __int128 m = (P + d - 1) / d;
+        if (m >= ((unsigned __int128)1 << 32)) continue;
+        const unsigned __int128 e = m * d - P;
+        if (e * nmax >= P) return SmallMod{0, 0, 0, 0, 0};
+        f.m = (uint32_t)m;
+        f.sh = sh;
+        return f;
+    }
+    return SmallMod{0, 0, 0, 0, 0};
+}
+
+__device__ __forceinline__ int small_mod(const SmallMod& f, uint64_t x) {
+    const uint64_t t = (uint64_t)(uint32_t)(x >> 32) * f.k32 + (uint32_t)x;
+    const uint32_t n = (uint32_t)(t >> 20) * f.k20 + ((uint32_t)t & 0xfffffu);
+    const uint32_t q = __umulhi(n, f.m) >> f.sh;
+    return (int)(n - q * f.d);
+}
+
 struct VixArgs {
     int R, ht, hr, S;
     uint64_t seed;
@@ -335,6 +369,7 @@ struct VixArgs {
     int zr0, zr1;        // held terrain rows [zr0, zr1)
     int pv, pt, st_off;  // skip map: SV row pitch, ST column pitch, ST offset (int16 entries)
     uint32_t s_mul;      // ceil(2^32 / S) (0: divide): floor(x / S) = umulhi(x, s_mul) while x S < 2^32
+    SmallMod smod;       // x % (2R+1) for 64-bit x by 32-bit folds (k_vix_lanes)
     int4* ties;          // fp64 tie list: {tx row, tx col, dr, dc} of visible segments with a grazing tie
     long long tie_cap;
 };
@@ -1146,9 +1181,9 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_lanes(const int16
         // ---- draw: the lane's S receivers (D6) ----
         while (nacc < S) {
             x += kGamma;
-            const int dr = (int)fm_mod(a.span, sm_finalize(x)) - a.R;
+            const int dr = small_mod(a.smod, sm_finalize(x)) - a.R;
             x += kGamma;
-            const int dc = (int)fm_mod(a.span, sm_finalize(x)) - a.R;
+            const int dc = small_mod(a.smod, sm_finalize(x)) - a.R;
             if (dr * dr + dc * dc <= R2 && (unsigned)(r + dr) < (unsigned)nrows && (unsigned)(c + dc) < (unsigned)ncols) {
                 asm volatile("st.shared.u32 [%0], %1;" ::"r"(smp_lane + (uint32_t)nacc * 128u),
                              "r"((dr + 256) | ((dc + 256) << 9)));
@@ -1261,6 +1296,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     a.s_mul = a.S > 0 && a.S < 4096 ? (uint32_t)(((1ull << 32) + (uint64_t)a.S - 1) / (uint64_t)a.S) : 0u;
     a.seed = p.seed;
     a.span = make_fastmod((uint64_t)(2 * p.roi + 1));
+    a.smod = make_smallmod((uint32_t)(2 * p.roi + 1));   // (d = 0: not usable; k_vix_lanes needs roi <= 255)
     // fp64 tie list (grazing ties: ~1e-4 of segments on the BASELINE terrains);
     // txs_estimate_vix re-runs the stage with a larger list on overflow
     {
@@ -1397,7 +1433,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
             else kq = lane_skip ? k_vix_quads<3, 8, 2> : (unit == 8 ? k_vix_quads<1, 8, 2> : k_vix_quads<1, 4, 2>);
             // one post per lane (k_vix_lanes) for S <= 32; TXS_VIX_LANEDRAW=0: the per-warp receiver FIFO
             static const bool lane_draw = !getenv("TXS_VIX_LANEDRAW") || atoi(getenv("TXS_VIX_LANEDRAW")) != 0;
-            if (lane_skip && lane_draw && p.samples_per_point <= kLaneDrawMaxS) {
+            if (lane_skip && lane_draw && p.samples_per_point <= kLaneDrawMaxS && a.smod.d != 0) {
                 // failing-group mask vs one flag + cooperative re-test; walk record eager vs
                 // built only for failing lanes (TXS_VIX_LMODE = mask | lazy << 1)
                 int lm = gs == 4 ? 3 : 1;   // measured: profiles/README.md (VIX one post per lane)
