@@ -1003,7 +1003,10 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
                             !getenv("TXS_SITE_GRAPH");
     if (persistent && !getenv("TXS_SITE_LOOP3")) {
         // one-barrier persistent loop (k_site_loop1): owned gains/windows in shared memory
-        int want = 2;
+        // CTAs per SM (measured, profiles/README.md): one when few neighbours change per
+        // round (fewer partials to reduce: c3 23.2 -> 21.9 ms, c4 23.8 -> 23.0), two
+        // when the neighbour updates dominate (c2, ~630 per round: 6.8 vs 9.3 ms)
+        int want = expected_nb < 300.0 ? 1 : 2;
         if (const char* e = getenv("TXS_SITE_LOOP_CTAS")) want = std::max(1, atoi(e));
         int grid = 0, per_sm = 0;
         size_t smem = 0;
