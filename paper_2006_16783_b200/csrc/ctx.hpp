@@ -177,6 +177,12 @@ struct txs_ctx {
     cudaEvent_t user_ev[16] = {};
     int64_t launches = 0;
     int64_t dev_bytes = 0, dev_bytes_peak = 0;   // context buffers (txs::ensure), live and high-water
+    // VIX crossing statistic (txs_stats.vix_crossings_full): a function of the grid,
+    // band, roi, S and seed only, so it is counted on the first launch with a
+    // given key and added from this cache afterwards (k_vix_lanes)
+    uint64_t vix_cross_key = 0;
+    unsigned long long vix_cross_count = 0;
+    bool vix_cross_valid = false;
 
     // scratch
     void* d_scratch = nullptr;

@@ -311,6 +311,8 @@ __device__ __forceinline__ int crossings_of(int dr, int dc) {
 
 // gcd table for |dr|,|dc| <= 255 (the quad path's crossing statistic: one L2
 // load per sample instead of a binary-gcd loop)
+__global__ void k_add_counter(unsigned long long* __restrict__ p, unsigned long long v) { *p += v; }
+
 __global__ void k_gcd_table(uint8_t* __restrict__ t) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= 256 * 256) return;
@@ -370,6 +372,7 @@ struct VixArgs {
     int pv, pt, st_off;  // skip map: SV row pitch, ST column pitch, ST offset (int16 entries)
     uint32_t s_mul;      // ceil(2^32 / S) (0: divide): floor(x / S) = umulhi(x, s_mul) while x S < 2^32
     SmallMod smod;       // x % (2R+1) for 64-bit x by 32-bit folds (k_vix_lanes)
+    int count_cross;     // k_vix_lanes: accumulate the crossing statistic (first launch per key)
     int4* ties;          // fp64 tie list: {tx row, tx col, dr, dc} of visible segments with a grazing tie
     long long tie_cap;
 };
@@ -924,7 +927,7 @@ __device__ __forceinline__ unsigned batch_skip_lane(const QuadGeomC& gc, int ns,
 // Walk geometry of the segment from post (r, c) (observer elevation E) to
 // (r + dr0, c + dc0): the skip-test record (soff, LE2, DG, w) and the
 // exact-walk record (start address, Esn, msm); n_cross counts its crossings.
-template <int GS, bool TERR, bool WALK = true>
+template <int GS, bool TERR, bool WALK = true, bool COUNT = true>
 __device__ __forceinline__ QuadGeom seg_quad_geom(const int16_t* __restrict__ z, const uint2* __restrict__ qp, int ncols,
                                                   const VixArgs& a, const uint8_t* __restrict__ gcdt,
                                                   const unsigned long long* s_rcp40, int r, int c, int E, int dr0, int dc0,
@@ -933,7 +936,7 @@ __device__ __forceinline__ QuadGeom seg_quad_geom(const int16_t* __restrict__ z,
     const int H = a.zr1 - a.zr0;
     int dr = dr0, dc = dc0;
     const int Zt = zld(z + (int64_t)(r + dr) * ncols + (c + dc)) + a.hr;
-    n_cross += crossings_tab(dr, dc, gcdt);
+    if (COUNT) n_cross += crossings_tab(dr, dc, gcdt);
     const bool tr = abs(dr) > abs(dc);
     const bool rev = tr ? dr < 0 : dc < 0;      // walk from the receiver
     const int y = r - a.zr0 + (rev ? dr : 0), x = c + (rev ? dc : 0);   // start post
@@ -1200,7 +1203,8 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_lanes(const int16
                 const int pk = s_smp[k * 32 + lane];
                 dr0 = (pk & 0x1ff) - 256;
                 dc0 = ((pk >> 9) & 0x1ff) - 256;
-                g = seg_quad_geom<GS, TERR, !LAZY>(z, qp, ncols, a, gcdt, s_rcp40, r, c, E, dr0, dc0, n_cross);
+                g = a.count_cross ? seg_quad_geom<GS, TERR, !LAZY, true>(z, qp, ncols, a, gcdt, s_rcp40, r, c, E, dr0, dc0, n_cross)
+                                  : seg_quad_geom<GS, TERR, !LAZY, false>(z, qp, ncols, a, gcdt, s_rcp40, r, c, E, dr0, dc0, n_cross);
             }
             unsigned tiem;
             const unsigned vism = batch_skip_lane<GS, TERR, MASK>(g.c, np, lane, s_geo, smap, PQ, &tiem, [&] {
@@ -1296,7 +1300,8 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     a.s_mul = a.S > 0 && a.S < 4096 ? (uint32_t)(((1ull << 32) + (uint64_t)a.S - 1) / (uint64_t)a.S) : 0u;
     a.seed = p.seed;
     a.span = make_fastmod((uint64_t)(2 * p.roi + 1));
-    a.smod = make_smallmod((uint32_t)(2 * p.roi + 1));   // (d = 0: not usable; k_vix_lanes needs roi <= 255)
+    a.smod = make_smallmod((uint32_t)(2 * p.roi + 1));
+    a.count_cross = 1;   // (d = 0: not usable; k_vix_lanes needs roi <= 255)
     // fp64 tie list (grazing ties: ~1e-4 of segments on the BASELINE terrains);
     // txs_estimate_vix re-runs the stage with a larger list on overflow
     {
@@ -1426,6 +1431,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         int unit = gs == 4 ? 2 : (p.roi >= 150 ? 8 : 4);
         if (const char* e = getenv("TXS_VIX_UNIT")) unit = atoi(e);
         decltype(&k_vix_quads<1, 8, 2>) kq;
+        bool lanes_kernel = false;
         if (skip == 1) {
             // per-lane skip tests (batch_skip_lane); TXS_VIX_LANESKIP=0: flattened units (batch_skip)
             static const bool lane_skip = !getenv("TXS_VIX_LANESKIP") || atoi(getenv("TXS_VIX_LANESKIP")) != 0;
@@ -1443,6 +1449,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
                 else kq = lm == 0 ? k_vix_lanes<2, false, false> : lm == 1 ? k_vix_lanes<2, true, false>
                         : lm == 2 ? k_vix_lanes<2, false, true> : k_vix_lanes<2, true, true>;
                 qsm = (sizeof(QuadGeom) * 32 + sizeof(int) * 32 * (size_t)std::max(1, p.samples_per_point)) * kVixWarps;
+                lanes_kernel = true;
             }
         } else if (skip == 2) {
             kq = gs == 4 ? k_vix_quads<2, 8, 4> : k_vix_quads<2, 8, 2>;
@@ -1470,11 +1477,35 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         if (const char* e = getenv("TXS_VIX_GRID")) grid_q = std::min<int64_t>(tiles_q, std::max(1, atoi(e)));
         if (!banded) {
             TXS_CUDA(c, "vix", cudaMemsetAsync(c->d_counters + kVixNext, 0, sizeof(unsigned long long), c->stream));
+            // the crossing statistic depends only on this key: counted once, then cached
+            const uint64_t key = mix_seed(mix_seed(p.seed, (uint64_t)p.roi * 4099 + (uint64_t)p.samples_per_point,
+                                                   (uint64_t)c->nrows * 1000003 + (uint64_t)c->ncols),
+                                          (uint64_t)c->band_r0 * 1000003 + (uint64_t)c->band_r1,
+                                          (uint64_t)c->z_off * 1000003 + (uint64_t)c->z_rows);
+            const bool lanes = lanes_kernel;
+            const bool cached = lanes && c->vix_cross_valid && c->vix_cross_key == key;
+            aq.count_cross = cached ? 0 : 1;
+            unsigned long long before = 0;
+            if (lanes && !cached)
+                TXS_CUDA(c, "vix", cudaMemcpyAsync(&before, c->d_counters + kVixCrossFull, sizeof(before),
+                                                   cudaMemcpyDeviceToHost, c->stream));
             cudaEventRecord(c->ev_k0, c->stream);
             kq<<<(unsigned)grid_q, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols,
                                                                     c->d_vix - c->band_r0 * c->ncols, aq, c->d_gcd, smap,
                                                                     c->d_counters);
             cudaEventRecord(c->ev_k1, c->stream);
+            if (cached) {
+                k_add_counter<<<1, 1, 0, c->stream>>>(c->d_counters + kVixCrossFull, c->vix_cross_count);
+                TXS_LAUNCHED(c, "vix");
+            } else if (lanes) {
+                unsigned long long after = 0;
+                TXS_CUDA(c, "vix", cudaMemcpyAsync(&after, c->d_counters + kVixCrossFull, sizeof(after),
+                                                   cudaMemcpyDeviceToHost, c->stream));
+                TXS_CUDA(c, "vix", cudaStreamSynchronize(c->stream));
+                c->vix_cross_count = after - before;
+                c->vix_cross_key = key;
+                c->vix_cross_valid = true;
+            }
         } else {
             // band b = upload chunk b's rows; it needs the rows up to r1 + R + 4G (its
             // walks, and the map corners of their groups), so it waits for that
