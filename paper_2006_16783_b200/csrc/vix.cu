@@ -1132,7 +1132,11 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_quads(const int16
 // its visible count stay in the lane's registers (no receiver FIFO, no ring of
 // open posts, no shuffles per batch).
 constexpr int kLaneDrawMaxS = 32;
-template <int GS, bool MASK, bool LAZY>
+// P posts per lane (P = 2: the warp takes two item rows; each lane draws its
+// first post's S receivers, then its second's, in one loop, so the warp's draw
+// iterations are the max over lanes of the two posts' pair counts together --
+// less divergence than twice the max of one).
+template <int GS, bool MASK, bool LAZY, int P>
 __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_lanes(const int16_t* __restrict__ z,
                                                                    const uint2* __restrict__ qp, int nrows, int ncols,
                                                                    uint8_t* __restrict__ out, VixArgs a,
@@ -1140,10 +1144,11 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_lanes(const int16
                                                                    const int16_t* __restrict__ smap,
                                                                    unsigned long long* __restrict__ counters) {
     static_assert(kTileQ == 32, "one post per lane");
+    static_assert(P == 1 || P == 2, "one or two posts per lane");
     extern __shared__ __align__(16) unsigned char s_dyn[];
-    // dynamic smem: [geometry: kVixWarps x 32][samples: kVixWarps x S x 32 ints]
+    // dynamic smem: [geometry: kVixWarps x 32][samples: kVixWarps x P S x 32 ints]
     QuadGeom* s_geo = (QuadGeom*)s_dyn + warp_of_thread() * 32;
-    int* s_smp = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + warp_of_thread() * a.S * 32;
+    int* s_smp = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + warp_of_thread() * a.S * 32 * P;
     const uint32_t smp_lane = (uint32_t)__cvta_generic_to_shared(s_smp) + 4u * (threadIdx.x & 31);   // column of this lane
     const QuadPitch PQ{a.pv, a.pt, ncols};
     constexpr bool TERR = GS == 4;
@@ -1155,67 +1160,85 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_lanes(const int16
     unsigned long long n_cross = 0;
     int n_posts = 0;
     const int strip_tiles = a.strip * a.tiles_y;
+    const int64_t ntiles = (int64_t)a.tiles_x * a.tiles_y;
     for (;;) {
-        long long item = 0;
-        if (lane == 0) item = (long long)atomicAdd(counters + kVixNext, 1ull);
-        item = __shfl_sync(kFull, item, 0);
-        const int64_t tile = item / kTileQ;
-        if (tile >= (int64_t)a.tiles_x * a.tiles_y) break;
-        int ty, tx;
-        {
+        long long item0 = 0;
+        if (lane == 0) item0 = (long long)atomicAdd(counters + kVixNext, (unsigned long long)P);
+        item0 = __shfl_sync(kFull, item0, 0);
+        if (item0 / kTileQ >= ntiles) break;
+        int rq[P], cq[P], Eq[P], npq[P];
+        bool hq[P];
+        uint64_t xq[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const long long item = item0 + q;
+            const int64_t tile = item / kTileQ;
+            rq[q] = 0; cq[q] = 0; Eq[q] = 0; npq[q] = 0; hq[q] = false; xq[q] = 0;
+            if (tile >= ntiles) continue;
             const int sidx = (int)(tile / strip_tiles), rem = (int)(tile - (int64_t)sidx * strip_tiles);
             const int sw = min(a.strip, a.tiles_x - sidx * a.strip);
-            ty = rem / sw;
-            tx = sidx * a.strip + (rem - ty * sw);
+            const int ty = rem / sw;
+            const int tx = sidx * a.strip + (rem - ty * sw);
+            const int r = a.row0 + ty * kTileQ + (int)(item % kTileQ);
+            if (r >= a.row_end) continue;
+            rq[q] = r;
+            cq[q] = tx * kTileQ + lane;
+            npq[q] = min(32, ncols - tx * kTileQ);   // posts of this item row: lanes 0 .. np-1
+            hq[q] = lane < npq[q];
+            if (hq[q]) {
+                xq[q] = mix_seed(a.seed, (uint64_t)r, (uint64_t)cq[q]);
+                Eq[q] = zld(z + (int64_t)r * ncols + cq[q]) + a.ht;
+            }
+            n_posts += npq[q] * (lane == 0);
         }
-        const int r = a.row0 + ty * kTileQ + item % kTileQ;
-        if (r >= a.row_end) continue;
-        const int c = tx * kTileQ + lane;
-        const int np = min(32, ncols - tx * kTileQ);   // posts of this item row: lanes 0 .. np-1
-        const bool has = lane < np;
-        int E = 0, nacc = S;
-        uint64_t x = 0;
-        if (has) {
-            x = mix_seed(a.seed, (uint64_t)r, (uint64_t)c);
-            E = zld(z + (int64_t)r * ncols + c) + a.ht;
-            nacc = 0;
-        }
-        n_posts += np * (lane == 0);
-        // ---- draw: the lane's S receivers (D6) ----
-        while (nacc < S) {
-            x += kGamma;
-            const int dr = small_mod(a.smod, sm_finalize(x)) - a.R;
-            x += kGamma;
-            const int dc = small_mod(a.smod, sm_finalize(x)) - a.R;
-            if (dr * dr + dc * dc <= R2 && (unsigned)(r + dr) < (unsigned)nrows && (unsigned)(c + dc) < (unsigned)ncols) {
-                asm volatile("st.shared.u32 [%0], %1;" ::"r"(smp_lane + (uint32_t)nacc * 128u),
-                             "r"((dr + 256) | ((dc + 256) << 9)));
-                ++nacc;
+        // ---- draw: the lane's posts' S receivers each (D6), rows q S .. q S + S - 1 ----
+        {
+            int row = hq[0] ? 0 : S;
+            const int limit = (P == 2 && hq[P - 1]) ? P * S : (hq[0] ? S : 0);
+            uint64_t x = hq[0] ? xq[0] : xq[P - 1];
+            int rr = hq[0] ? rq[0] : rq[P - 1], cc = hq[0] ? cq[0] : cq[P - 1];
+            while (row < limit) {
+                x += kGamma;
+                const int dr = small_mod(a.smod, sm_finalize(x)) - a.R;
+                x += kGamma;
+                const int dc = small_mod(a.smod, sm_finalize(x)) - a.R;
+                if (dr * dr + dc * dc <= R2 && (unsigned)(rr + dr) < (unsigned)nrows && (unsigned)(cc + dc) < (unsigned)ncols) {
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(smp_lane + (uint32_t)row * 128u),
+                                 "r"((dr + 256) | ((dc + 256) << 9)));
+                    ++row;
+                    if (P == 2 && row == S) { x = xq[P - 1]; rr = rq[P - 1]; cc = cq[P - 1]; }   // the second post
+                }
             }
         }
         __syncwarp();
-        // ---- batch k: sample k of every post of the row ----
-        int cnt = 0;
-        for (int k = 0; k < S; ++k) {
-            QuadGeom g{};
-            int dr0 = 0, dc0 = 0;
-            if (has) {
-                const int pk = s_smp[k * 32 + lane];
-                dr0 = (pk & 0x1ff) - 256;
-                dc0 = ((pk >> 9) & 0x1ff) - 256;
-                g = a.count_cross ? seg_quad_geom<GS, TERR, !LAZY, true>(z, qp, ncols, a, gcdt, s_rcp40, r, c, E, dr0, dc0, n_cross)
-                                  : seg_quad_geom<GS, TERR, !LAZY, false>(z, qp, ncols, a, gcdt, s_rcp40, r, c, E, dr0, dc0, n_cross);
+        // ---- batch k of post q: sample k of the q-th row's 32 posts ----
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            if (npq[q] == 0) continue;   // (warp-uniform)
+            const int r = rq[q], c = cq[q], E = Eq[q], np = npq[q];
+            const bool has = hq[q];
+            int cnt = 0;
+            for (int k = 0; k < S; ++k) {
+                QuadGeom g{};
+                int dr0 = 0, dc0 = 0;
+                if (has) {
+                    const int pk = s_smp[(q * S + k) * 32 + lane];
+                    dr0 = (pk & 0x1ff) - 256;
+                    dc0 = ((pk >> 9) & 0x1ff) - 256;
+                    g = a.count_cross ? seg_quad_geom<GS, TERR, !LAZY, true>(z, qp, ncols, a, gcdt, s_rcp40, r, c, E, dr0, dc0, n_cross)
+                                      : seg_quad_geom<GS, TERR, !LAZY, false>(z, qp, ncols, a, gcdt, s_rcp40, r, c, E, dr0, dc0, n_cross);
+                }
+                unsigned tiem;
+                const unsigned vism = batch_skip_lane<GS, TERR, MASK>(g.c, np, lane, s_geo, smap, PQ, &tiem, [&] {
+                    if (!LAZY) return g.f;
+                    unsigned long long unused = 0;
+                    return seg_quad_geom<GS, TERR, true>(z, qp, ncols, a, gcdt, s_rcp40, r, c, E, dr0, dc0, unused).f;
+                });
+                if ((tiem >> lane) & 1u) push_tie(a, counters, r, c, dr0, dc0);
+                cnt += (vism >> lane) & 1u;
             }
-            unsigned tiem;
-            const unsigned vism = batch_skip_lane<GS, TERR, MASK>(g.c, np, lane, s_geo, smap, PQ, &tiem, [&] {
-                if (!LAZY) return g.f;
-                unsigned long long unused = 0;
-                return seg_quad_geom<GS, TERR, true>(z, qp, ncols, a, gcdt, s_rcp40, r, c, E, dr0, dc0, unused).f;
-            });
-            if ((tiem >> lane) & 1u) push_tie(a, counters, r, c, dr0, dc0);
-            cnt += (vism >> lane) & 1u;
+            if (has) out[(int64_t)r * ncols + c] = (uint8_t)cnt;
         }
-        if (has) out[(int64_t)r * ncols + c] = (uint8_t)cnt;
         __syncwarp();
     }
     for (int o = 16; o; o >>= 1) n_cross += __shfl_down_sync(kFull, n_cross, o);
@@ -1224,7 +1247,6 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_lanes(const int16
         atomicAdd(counters + kVixCrossFull, n_cross);
     }
 }
-
 
 // Skip map of the skip tests.  Pass 1: per GxG block the maximum elevation,
 // stored with one block of padding on every side (padded index = block + 1;
@@ -1444,11 +1466,24 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
                 // built only for failing lanes (TXS_VIX_LMODE = mask | lazy << 1)
                 int lm = gs == 4 ? 3 : 1;   // measured: profiles/README.md (VIX one post per lane)
                 if (const char* e = getenv("TXS_VIX_LMODE")) lm = atoi(e) & 3;
-                if (gs == 4) kq = lm == 0 ? k_vix_lanes<4, false, false> : lm == 1 ? k_vix_lanes<4, true, false>
-                                : lm == 2 ? k_vix_lanes<4, false, true> : k_vix_lanes<4, true, true>;
-                else kq = lm == 0 ? k_vix_lanes<2, false, false> : lm == 1 ? k_vix_lanes<2, true, false>
-                        : lm == 2 ? k_vix_lanes<2, false, true> : k_vix_lanes<2, true, true>;
-                qsm = (sizeof(QuadGeom) * 32 + sizeof(int) * 32 * (size_t)std::max(1, p.samples_per_point)) * kVixWarps;
+                // posts per lane (TXS_VIX_PPL=1|2; measured, profiles/README.md): two on large
+                // grids with few samples (c3 41.8 -> 40.2 ms, c4 322 -> 309), one otherwise
+                // (c2, S = 20: 32.5 vs 53.6; c1, 1000^2: 1.87 vs 2.03)
+                int ppl = p.samples_per_point <= 12 && (double)c->nrows * (double)c->ncols >= (double)(1 << 24) ? 2 : 1;
+                if (const char* e = getenv("TXS_VIX_PPL")) ppl = atoi(e) == 2 && p.samples_per_point <= 20 ? 2 : 1;
+                if (ppl == 2) {
+                    if (gs == 4) kq = lm == 0 ? k_vix_lanes<4, false, false, 2> : lm == 1 ? k_vix_lanes<4, true, false, 2>
+                                    : lm == 2 ? k_vix_lanes<4, false, true, 2> : k_vix_lanes<4, true, true, 2>;
+                    else kq = lm == 0 ? k_vix_lanes<2, false, false, 2> : lm == 1 ? k_vix_lanes<2, true, false, 2>
+                            : lm == 2 ? k_vix_lanes<2, false, true, 2> : k_vix_lanes<2, true, true, 2>;
+                } else {
+                    if (gs == 4) kq = lm == 0 ? k_vix_lanes<4, false, false, 1> : lm == 1 ? k_vix_lanes<4, true, false, 1>
+                                    : lm == 2 ? k_vix_lanes<4, false, true, 1> : k_vix_lanes<4, true, true, 1>;
+                    else kq = lm == 0 ? k_vix_lanes<2, false, false, 1> : lm == 1 ? k_vix_lanes<2, true, false, 1>
+                            : lm == 2 ? k_vix_lanes<2, false, true, 1> : k_vix_lanes<2, true, true, 1>;
+                }
+                qsm = (sizeof(QuadGeom) * 32 + sizeof(int) * 32 * (size_t)ppl * (size_t)std::max(1, p.samples_per_point)) *
+                      kVixWarps;
                 lanes_kernel = true;
             }
         } else if (skip == 2) {
