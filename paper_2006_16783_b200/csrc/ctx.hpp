@@ -158,6 +158,10 @@ struct txs_ctx {
     int32_t* d_bucket_start = nullptr;   // CSR over candidate buckets
     int32_t* d_bucket_items = nullptr;
     size_t bucket_cap = 0, bucket_items_cap = 0;
+    int4* d_strip_tasks = nullptr;       // k_gain_strips task list (site.cu), grouped by tile
+    int32_t* d_strip_start = nullptr;    // tiles+1 (+ tiles+1 fill cursors)
+    size_t strip_tasks_cap = 0, strip_start_cap = 0;
+    unsigned long long site_alg_bytes = 0;   // SPEC-layout bytes of the candidate set's viewsheds
     bool site_valid = false;
 
     // txs_run_pipeline_host: terrain rows arriving on copy_stream in chunks of

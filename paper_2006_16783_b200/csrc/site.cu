@@ -23,6 +23,7 @@
 #include <cub/cub.cuh>
 
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "ctx.hpp"
@@ -767,6 +768,183 @@ __global__ void __launch_bounds__(kTiledThreads, 2) k_gain_tiled(SiteArgs a, con
     if (counters && lane == 0 && bytes) atomicAdd(counters + kSiteBytes, bytes);
 }
 
+// Strip-tile form of the full gain pass: a tile is SH terrain rows x TX
+// candidate buckets (side roi).  A task is one candidate's window rows inside
+// one strip -- contiguous words of its cum-aligned viewshed; the task list,
+// grouped by tile, is built once per candidate set (k_strip_count /
+// k_strip_fill: the windows do not change between rounds).  Per tile a CTA
+// stages the cum words its tasks can reach (the tile's rows, its bucket
+// columns +- roi) in shared memory once, then its warps stream the tasks:
+// each viewshed word is read from HBM once per pass and each cum word from L2
+// a few times per pass (the per-candidate form reads a window of cum per
+// candidate: at roi 100 as many L2 bytes as HBM bytes).  A task's words arrive
+// by one bulk copy (cp.async.bulk, completion on an mbarrier) into one of
+// kStripSlots slots of the warp's staging ring, so every warp keeps
+// kStripSlots tasks in flight whatever their length; partial popcounts go to
+// the gains by atomics (zeroed first by k_zero_gains).  Warp w takes the
+// tile's tasks w, w + W, w + 2W, ... (even shares).
+constexpr int kStripThreads = 256;
+constexpr int kStripSlots = 4;
+
+struct StripGeo {
+    int SH, TX, ntx, nstrips, r_lo, r_hi;
+};
+__device__ __forceinline__ void strip_tile_box(const SiteArgs& a, const StripGeo& g, int tile, int* s0, int* s1,
+                                               int* wx0, int* pw) {
+    const int s = tile / g.ntx, tx = tile - s * g.ntx;
+    *s0 = g.r_lo + s * g.SH;
+    *s1 = min(g.r_hi, *s0 + g.SH);
+    const int bx0 = tx * g.TX, bx1 = min(a.nbx, bx0 + g.TX);
+    *wx0 = max(0, bx0 * a.bsize - a.R) >> 6;
+    *pw = ((min(a.ncols - 1, bx1 * a.bsize - 1 + a.R) >> 6) + 1) - *wx0;
+}
+
+// tasks of candidate i: one per strip its window rows (held rows) meet
+template <bool FILL>
+__global__ void k_strip_tasks(SiteArgs a, StripGeo g, const int4* __restrict__ wins, const int32_t* __restrict__ ccol,
+                              int32_t* __restrict__ cursor, int4* __restrict__ tasks, unsigned long long* alg) {
+    unsigned long long bytes = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int4 win = wins[i];
+        if (!FILL) bytes += 8ull * (((unsigned long long)win.z * win.w + 63) >> 6);   // SPEC-layout (algorithmic) bytes
+        const int ya0 = max(win.x, g.r_lo), yb0 = min(win.x + win.z, g.r_hi);
+        if (ya0 >= yb0) continue;
+        const int tx = (ccol[i] / a.bsize) / g.TX;
+        const int nwr = win_nwr(win.y, win.w);
+        for (int s = (ya0 - g.r_lo) / g.SH; s <= (yb0 - 1 - g.r_lo) / g.SH; ++s) {
+            const int tile = s * g.ntx + tx;
+            if (!FILL) { atomicAdd(cursor + tile, 1); continue; }
+            int s0, s1, wx0, pw;
+            strip_tile_box(a, g, tile, &s0, &s1, &wx0, &pw);
+            const int ya = max(ya0, s0), yb = min(yb0, s1);
+            const int k = atomicAdd(cursor + tile, 1);
+            tasks[k] = make_int4((int)i, (ya - win.x) * nwr, (ya - s0) * pw + (win.y >> 6) - wx0,
+                                 ((yb - ya) * nwr) | (nwr << 20));
+        }
+    }
+    if (!FILL) {
+        for (int o = 16; o; o >>= 1) bytes += __shfl_down_sync(kFull, bytes, o);
+        if ((threadIdx.x & 31) == 0 && bytes) atomicAdd(alg, bytes);
+    }
+}
+
+template <typename G>
+__global__ void k_zero_gains(const SiteState* st, G* __restrict__ gain, int64_t n) {
+    if (st && (st->done || st->finish)) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        gain[i] = 0;
+}
+
+__device__ __forceinline__ void gain_add(int32_t* g, int v) { atomicAdd(g, v); }
+__device__ __forceinline__ void gain_add(int64_t* g, int v) {
+    atomicAdd((unsigned long long*)g, (unsigned long long)(long long)v);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+// arm the barrier with the copy's byte count and start the copy (one lane)
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n @!p bra W;\n}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+template <typename G>
+__global__ void __launch_bounds__(kStripThreads) k_gain_strips(SiteArgs a, StripGeo geo, const SiteState* st,
+                                                              const uint64_t* __restrict__ words,
+                                                              const uint64_t* __restrict__ cum,
+                                                              const int32_t* __restrict__ tstart,
+                                                              const int4* __restrict__ tasks,
+                                                              G* __restrict__ gain,
+                                                              unsigned long long* __restrict__ counters,
+                                                              unsigned long long alg_bytes, int tile_words, int SW) {
+    if (st && (st->done || st->finish)) return;
+    extern __shared__ __align__(16) uint64_t s_cum[];   // cum tile (tile_words, even), then the staging rings
+    __shared__ __align__(8) uint64_t s_bar[kStripThreads / 32][kStripSlots];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int W = kStripThreads / 32, S = kStripSlots;
+    uint64_t* ring = s_cum + tile_words + (int64_t)warp * S * SW;
+    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+    const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(&s_bar[warp][0]);
+    if (lane == 0)
+        for (int k = 0; k < S; ++k) mbar_init(bar_s + 8 * k, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    if (counters && blockIdx.x == 0 && tid == 0) atomicAdd(counters + kSiteBytes, alg_bytes);
+    uint32_t phase = 0;   // bit k: parity of slot k's next completion
+    int head = 0;         // oldest slot in flight
+    const int wpr = (int)a.wpr;
+    for (int tile = blockIdx.x; tile < geo.nstrips * geo.ntx; tile += gridDim.x) {
+        const int t0 = tstart[tile], t1 = tstart[tile + 1];
+        if (t0 == t1) continue;
+        int s0, s1, wx0, pw;
+        strip_tile_box(a, geo, tile, &s0, &s1, &wx0, &pw);
+        for (int t = tid; t < (s1 - s0) * pw; t += kStripThreads) {
+            const int y = t / pw, x = t - y * pw;
+            s_cum[t] = __ldg(cum + (int64_t)(s0 + y) * wpr + wx0 + x);
+        }
+        __syncthreads();
+        int4 fd = make_int4(0, 0, 0, 0);   // this lane's fetched task
+        int fbase = t0 + warp, fcur = 32, fn = 0;   // lane l of a fetch: task fbase + W*l
+        int si = 0, scb = 0, snwr = 1, soff = 0, snw = 0;   // slot info held by lane k
+        int inflight = 0;
+        for (;;) {
+            while (inflight < S) {   // producer: keep S copies in flight
+                if (fcur >= fn) {
+                    if (fbase >= t1) break;
+                    fn = min(32, (t1 - fbase + W - 1) / W);
+                    if (lane < fn) fd = __ldg(tasks + fbase + W * lane);
+                    fbase += W * 32;
+                    fcur = 0;
+                }
+                const int j = fcur++;
+                const int ij = __shfl_sync(kFull, fd.x, j), fwj = __shfl_sync(kFull, fd.y, j);
+                const int cbj = __shfl_sync(kFull, fd.z, j), pk = __shfl_sync(kFull, fd.w, j);
+                const int nwj = pk & 0xfffff;
+                const int64_t src = (int64_t)ij * a.stride + fwj;
+                const int64_t a0 = src & ~(int64_t)1;
+                const int off = (int)(src - a0), span = (off + nwj + 1) & ~1;
+                const int slot = (head + inflight) & (S - 1);
+                if (lane == 0) bulk_load(ring_s + 8u * slot * SW, words + a0, 8u * span, bar_s + 8 * slot);
+                if (lane == slot) { si = ij; scb = cbj; snwr = pk >> 20; soff = off; snw = nwj; }
+                ++inflight;
+            }
+            if (inflight == 0) break;
+            const int slot = head;   // consumer: the oldest slot
+            const int ij = __shfl_sync(kFull, si, slot), cbj = __shfl_sync(kFull, scb, slot);
+            const int nwrj = __shfl_sync(kFull, snwr, slot), offj = __shfl_sync(kFull, soff, slot);
+            const int nwj = __shfl_sync(kFull, snw, slot);
+            mbar_wait(bar_s + 8 * slot, (phase >> slot) & 1u);
+            phase ^= 1u << slot;
+            const uint64_t* v = ring + slot * SW + offj;
+            const uint64_t* cr = s_cum + cbj;
+            int y = lane / nwrj, b = lane - y * nwrj;
+            const int dy = 32 / nwrj, db = 32 - dy * nwrj;
+            int acc = 0;
+            for (int t = lane; t < nwj; t += 32) {
+                acc += __popcll(v[t] & ~cr[y * pw + b]);
+                y += dy; b += db;
+                if (b >= nwrj) { b -= nwrj; ++y; }
+            }
+            acc = __reduce_add_sync(kFull, acc);
+            if (lane == 0 && acc) gain_add(gain + ij, acc);
+            __syncwarp();
+            head = (head + 1) & (S - 1);
+            --inflight;
+        }
+        __syncthreads();
+    }
+}
+
 // ---- layout conversion: SPEC dense rows <-> cum-aligned rows ------------------------
 __global__ void k_aligned_to_dense(const uint64_t* __restrict__ al, int64_t astride, const int4* __restrict__ wins,
                                    int64_t count, uint64_t* __restrict__ dense, int64_t dstride) {
@@ -910,12 +1088,103 @@ static bool gain_tiled(const SiteArgs& a, bool buckets, size_t* smem_out) {
     return buckets && dense && smem <= 110 * 1024 && !getenv("TXS_GAIN_REG");
 }
 
+// Tile of k_gain_strips: SH rows (TXS_STRIP_ROWS, default 32, <= 128) x TX
+// buckets (TXS_STRIP_TX, default 8); the staging ring slot holds the longest
+// task (SH window rows, even).  0 when the shared memory would pass 110 KB.
+struct StripShape {
+    int sh, tx, tile_words, sw;
+    size_t smem;
+};
+static int strip_rows(const SiteArgs& a, StripShape* sp) {
+    int sh = 32, t = 8;
+    if (const char* e = getenv("TXS_STRIP_ROWS")) sh = std::min(1 << 12, std::max(1, atoi(e)));
+    if (const char* e = getenv("TXS_STRIP_TX")) t = std::max(1, atoi(e));
+    const int64_t pw = ((int64_t)t * a.bsize + 2 * (int64_t)a.R + 63) / 64 + 2;
+    const int64_t nwr_max = (2 * (int64_t)a.R + 63) / 64 + 1;
+    const int64_t tile_words = (pw * sh + 1) & ~(int64_t)1;
+    const int64_t sw = (std::min<int64_t>(sh, 2 * (int64_t)a.R + 1) * nwr_max + 3) & ~(int64_t)1;
+    const int64_t bytes = 8 * (tile_words + (int64_t)(kStripThreads / 32) * kStripSlots * sw);
+    if (bytes > 110 * 1024 || nwr_max >= 4096 || sw > (1 << 20)) return 0;
+    sp->sh = sh; sp->tx = t; sp->tile_words = (int)tile_words; sp->sw = (int)sw; sp->smem = (size_t)bytes;
+    return sh;
+}
+
+static StripGeo strip_geo(const SiteArgs& a, const StripShape& sp) {
+    StripGeo g;
+    g.SH = sp.sh; g.TX = sp.tx;
+    g.r_lo = std::max(0, a.cr0); g.r_hi = std::min(a.nrows, a.cr1);
+    g.nstrips = std::max(0, (g.r_hi - g.r_lo + g.SH - 1) / g.SH);
+    g.ntx = (a.nbx + g.TX - 1) / g.TX;
+    return g;
+}
+
+// the task list of the current candidate set for this shape (count, scan, fill)
+static txs_status build_strip_tasks(txs_ctx* c, const SiteArgs& a, const StripShape& sp) {
+    const StripGeo g = strip_geo(a, sp);
+    const int64_t tiles = (int64_t)g.nstrips * g.ntx;
+    const int64_t cap = a.n * ((2 * (int64_t)a.R + 1 + g.SH - 1) / g.SH + 1);
+    const int64_t alg_at = (2 * (tiles + 1) + 1) & ~(int64_t)1;   // u64 slot after the two int arrays
+    if (ensure(c, "site", (void**)&c->d_strip_start, &c->strip_start_cap, sizeof(int32_t) * (size_t)(alg_at + 2)) != TXS_OK ||
+        ensure(c, "site", (void**)&c->d_strip_tasks, &c->strip_tasks_cap, sizeof(int4) * (size_t)std::max<int64_t>(1, cap)) != TXS_OK)
+        return TXS_ERR_OUT_OF_MEMORY;
+    if (cap > INT32_MAX) return fail(c, TXS_ERR_RANGE, "site", "strip task list too long");
+    int32_t* start = c->d_strip_start;
+    int32_t* cursor = c->d_strip_start + tiles + 1;
+    unsigned long long* alg = (unsigned long long*)(c->d_strip_start + alg_at);
+    TXS_CUDA(c, "site", cudaMemsetAsync(cursor, 0, sizeof(int32_t) * (size_t)(tiles + 1), c->stream));
+    TXS_CUDA(c, "site", cudaMemsetAsync(alg, 0, sizeof(unsigned long long), c->stream));
+    const int blocks = blocks_for(a.n, 256, c->num_sms * 8);
+    k_strip_tasks<false><<<blocks, 256, 0, c->stream>>>(a, g, c->d_win, c->d_ccol, cursor, nullptr, alg);
+    TXS_LAUNCHED(c, "site");
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, cursor, start, (int)(tiles + 1), c->stream);
+    void* tmp = nullptr;
+    TXS_CUDA(c, "site", cudaMallocAsync(&tmp, tb, c->stream));
+    TXS_CUDA(c, "site", cub::DeviceScan::ExclusiveSum(tmp, tb, cursor, start, (int)(tiles + 1), c->stream));
+    TXS_CUDA(c, "site", cudaFreeAsync(tmp, c->stream));
+    TXS_CUDA(c, "site", cudaMemcpyAsync(cursor, start, sizeof(int32_t) * (size_t)(tiles + 1), cudaMemcpyDeviceToDevice, c->stream));
+    k_strip_tasks<true><<<blocks, 256, 0, c->stream>>>(a, g, c->d_win, c->d_ccol, cursor, c->d_strip_tasks, nullptr);
+    TXS_LAUNCHED(c, "site");
+    TXS_CUDA(c, "site", cudaMemcpyAsync(&c->site_alg_bytes, alg, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+    return TXS_OK;
+}
+
+// TXS_GAIN_PASS=full|tiled|strips overrides the measured choice (A/B only;
+// k_gain_strips measured slower than k_gain_full at c2-c4 and equal to
+// k_gain_tiled at c5, profiles/README.md)
+static int gain_pass_kind(const SiteArgs& a, bool buckets, size_t* smem, StripShape* sp) {
+    size_t ts = 0;
+    const bool tiled = gain_tiled(a, buckets, &ts);
+    const int rows = buckets ? strip_rows(a, sp) : 0;
+    int kind = tiled ? 1 : 0;   // strips: A/B only (slower at c2-c5, profiles/README.md)
+    if (const char* e = getenv("TXS_GAIN_PASS")) {
+        if (!strcmp(e, "full")) kind = 0;
+        else if (!strcmp(e, "tiled") && buckets) kind = 1;
+        else if (!strcmp(e, "strips") && rows > 0) kind = 2;
+    }
+    *smem = kind == 1 ? ts : kind == 2 ? sp->smem : 0;
+    return kind;
+}
+
 template <typename G>
 static void launch_gain_pass(txs_ctx* c, const SiteArgs& a, const SiteState* st, const uint64_t* cum, G* gain,
                              unsigned long long* counters, bool buckets) {
     size_t smem = 0;
-    const bool tiled = gain_tiled(a, buckets, &smem);
-    if (tiled) {
+    StripShape sp{};
+    const int kind = gain_pass_kind(a, buckets, &smem, &sp);
+    if (kind == 2) {
+        k_zero_gains<G><<<blocks_for(a.n, 256, c->num_sms * 4), 256, 0, c->stream>>>(st, gain, a.n);
+        auto kern = k_gain_strips<G>;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const StripGeo g = strip_geo(a, sp);
+        const int64_t tiles = (int64_t)g.nstrips * g.ntx;
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStripThreads, smem);
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)c->num_sms * std::max(1, per_sm)));
+        kern<<<grid, kStripThreads, smem, c->stream>>>(a, g, st, c->d_words, cum, c->d_strip_start, c->d_strip_tasks,
+                                                       gain, counters, c->site_alg_bytes, sp.tile_words, sp.sw);
+    } else if (kind == 1) {
         auto kern = k_gain_tiled<G>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         const int64_t nbk = (int64_t)a.nbx * a.nby;
@@ -1100,6 +1369,13 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
     const LoopPtrs lp{c->d_crow, c->d_ccol, c->d_win, c->d_bucket_start, d_steps};
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
+    size_t gp_smem = 0;
+    StripShape gp_shape{};
+    const int gp_kind = p.site_mode == 1 ? gain_pass_kind(a, true, &gp_smem, &gp_shape) : -1;
+    if (gp_kind == 2) {
+        const txs_status bs = build_strip_tasks(c, a, gp_shape);
+        if (bs != TXS_OK) return bs;
+    }
     TXS_CUDA(c, "site", cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     for (int r = 0; r < kRoundsPerGraph; ++r) {
         if (p.site_mode == 1) launch_gain_pass<int32_t>(c, a, c->d_state, cumv, c->d_gain, c->d_counters, true);
@@ -1113,7 +1389,7 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
     if (ce != cudaSuccess) return cuda_fail(c, "site", ce);
     ce = cudaGraphInstantiate(&exec, graph, 0);
     if (ce != cudaSuccess) { cudaGraphDestroy(graph); return cuda_fail(c, "site", ce); }
-    const int per_round = (p.site_mode == 1 ? 3 : 3);
+    const int per_round = gp_kind == 2 ? 4 : 3;
     txs_status st = TXS_OK;
     int64_t graphs = 0;
     for (;;) {
@@ -1168,6 +1444,12 @@ txs_status time_gain_pass(txs_ctx* c, int32_t reps, double* ms, int64_t* bytes) 
     p.target_coverage = 1.0;
     const SiteArgs a = make_args(c, p);
     uint64_t* cumv = c->d_cum - c->cum_r0 * c->wpr;
+    size_t gp_smem = 0;
+    StripShape gp_shape{};
+    if (gain_pass_kind(a, true, &gp_smem, &gp_shape) == 2) {
+        const txs_status bs = build_strip_tasks(c, a, gp_shape);
+        if (bs != TXS_OK) return bs;
+    }
     TXS_CUDA(c, "site", cudaMemsetAsync(c->d_counters + kSiteBytes, 0, sizeof(unsigned long long), c->stream));
     launch_gain_pass<int32_t>(c, a, nullptr, cumv, c->d_gain, c->d_counters, true);   // warm-up (+ byte count)
     TXS_LAUNCHED(c, "site");

@@ -329,6 +329,32 @@ def test_site_bucket_tiled_bit_exact(engine, mode):
     _site_compare(engine, 20, rows, cols, 200, 256, 1.0, 0, mode)
 
 
+@pytest.mark.parametrize("kind,shape", [("full", None), ("tiled", None), ("strips", None), ("strips", "8x1"),
+                                        ("strips", "40x3")])
+def test_site_full_rescan_gain_pass_forms(engine, monkeypatch, kind, shape):
+    """Mode-1 rounds through every gain-pass kernel (per-candidate, bucket-tiled,
+    strip-tile task list with bulk copies; A/B knob TXS_GAIN_PASS) and strip
+    shapes whose tiles cut windows at many rows and bucket columns; grid edges
+    and a duplicate included."""
+    T = _T()
+    z = O.generate_fractal(230, 300, 0.6, 13, 0, 3000)
+    rng = np.random.default_rng(5)
+    n = 900
+    rows, cols = rng.integers(0, 230, n).astype(np.int32), rng.integers(0, 300, n).astype(np.int32)
+    rows[:5], cols[:5] = [0, 229, 0, 229, 0], [0, 299, 299, 0, 0]
+    engine.set_terrain(z)
+    engine.set_candidates(rows, cols)
+    engine.compute_all_viewsheds(T.make_params(33, 10, 10))
+    monkeypatch.setenv("TXS_GAIN_PASS", kind)
+    if shape:
+        sh, tx = shape.split("x")
+        monkeypatch.setenv("TXS_STRIP_ROWS", sh)
+        monkeypatch.setenv("TXS_STRIP_TX", tx)
+    _site_compare(engine, 33, rows, cols, 230, 300, 0.99, 0, 1)
+    ms, nbytes = engine.time_gain_pass(2)
+    assert ms > 0 and nbytes == sum(8 * ((int(w[2]) * int(w[3]) + 63) // 64) for w in engine.viewsheds(33)[0])
+
+
 @pytest.mark.parametrize("ctas", ["", "1", "3"])
 def test_site_persistent_loop_widths(engine, monkeypatch, ctas):
     """Persistent SITE loop with 400-1000 expected neighbours per round (4 CTAs
