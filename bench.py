@@ -437,7 +437,8 @@ def run_b200(args, cfg):
     site_stream = {"ms": round(rms, 3), "ms_with_setup": round(st1["ms_site"], 3),
                    "iterations": int(st1["site_iterations"]), "bytes": int(st1["site_bytes"]),
                    "gbs": round(st1["site_bytes"] / (rms / 1e3) / 1e9, 1) if rms else None,
-                   "kernel": "k_gain_tiled" if cfg.random_observers else "k_gain_full",
+                   "kernel": "k_gain_full",
+                   "layout": os.environ.get("TXS_GAIN_PASS") or "t8 (8x8-tile shadow of the viewsheds and the cum, DESIGN.md §3)",
                    "mode": "full-rescan (same picks as incremental)",
                    "kernel_ms_per_pass": round(gp_ms, 4), "kernel_bytes_per_pass": int(gp_bytes),
                    "kernel_gbs": round(gp_bytes / (gp_ms / 1e3) / 1e9, 1) if gp_ms else None}

@@ -130,7 +130,7 @@ void txs_destroy(txs_ctx* c) {
     void* bufs[] = {c->d_shard_steps, c->d_z, c->d_zt, c->d_pairs, c->d_gcd, c->d_vix, c->d_crow, c->d_ccol, c->d_cscore, c->d_words, c->d_win,
                     c->d_pop, c->d_cum, c->d_dwin, c->d_dspan, c->d_partials, c->d_gain, c->d_state,
                     c->d_bucket_start, c->d_bucket_items, c->d_counters, c->d_scratch, c->d_cgid, c->d_xfer,
-                    c->d_cum_dense, c->d_ties, c->d_strip_tasks, c->d_strip_start};
+                    c->d_cum_dense, c->d_ties, c->d_strip_tasks, c->d_strip_start, c->d_t8_words, c->d_t8_win, c->d_t8_cum};
     for (void* p : bufs) if (p) cudaFree(p);
     for (auto& kv : c->templates) {
         cudaFree(kv.second.rays); cudaFree(kv.second.cells);
@@ -570,6 +570,7 @@ txs_status txs_compute_viewsheds(txs_ctx* c, const txs_params* p) {
         c->vs_tie_min = (int64_t)nt + (int64_t)(nt / 4);
     }
     c->vs_valid = true;
+    c->t8_valid = false;
     c->site_valid = false;
     return TXS_OK;
 }
@@ -664,6 +665,7 @@ txs_status txs_set_viewsheds(txs_ctx* c, int32_t roi, int64_t n, const int32_t* 
     c->vs_n = n;
     c->vs_stride = astr;
     c->vs_valid = true;
+    c->t8_valid = false;
     c->site_valid = false;
     return TXS_OK;
 }
@@ -1053,6 +1055,7 @@ txs_status txs_site_gathered(txs_ctx* c, const txs_params* p, int64_t nrec, int6
     c->vs_n = n_total;
     c->vs_stride = stride;
     c->cand_valid = c->vs_valid = true;
+    c->t8_valid = false;
     txs_status st = unpack_records(c, nrec, d_rec);
     if (st != TXS_OK) return st;
     std::vector<txs_step> v;

@@ -162,6 +162,13 @@ struct txs_ctx {
     int32_t* d_strip_start = nullptr;    // tiles+1 (+ tiles+1 fill cursors)
     size_t strip_tasks_cap = 0, strip_start_cap = 0;
     unsigned long long site_alg_bytes = 0;   // SPEC-layout bytes of the candidate set's viewsheds
+    // 8x8-tile shadow of the viewsheds and the cum for the streaming gain pass
+    // (site.cu, "t8" layout); t8_valid: d_t8_words / d_t8_win match d_words
+    uint64_t* d_t8_words = nullptr;
+    int4* d_t8_win = nullptr;
+    uint64_t* d_t8_cum = nullptr;
+    size_t t8_words_cap = 0, t8_win_cap = 0, t8_cum_cap = 0;
+    bool t8_valid = false;
     bool site_valid = false;
 
     // txs_run_pipeline_host: terrain rows arriving on copy_stream in chunks of

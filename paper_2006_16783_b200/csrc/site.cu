@@ -645,31 +645,60 @@ __global__ void __launch_bounds__(kL1Threads, 2) k_site_loop1(SiteArgs a, SiteSt
 // L2-resident cum word (row0+y, (col0>>6)+b): gain = sum popc(v & ~cum).
 // (measured: 4 loads in flight per lane at 46 registers beat 8 or 16 in flight
 // and tighter register bounds, profiles/README.md)
-template <typename G>
+// T8: the same pass over the 8x8-tile shadow layout (below): `wins` holds the
+// window in tile units (ty0, tx0, nty, ntx), word t is tile (t / ntx, t % ntx)
+// and its cum counterpart is word (ty0 + t / ntx, tx0 + t % ntx) of the tile
+// cum (pitch a.wpr tiles); `wins_alg` (the windows in posts) only feeds the
+// algorithmic byte count.
+#ifndef GAIN_T8_U
+#define GAIN_T8_U 5   // (stream, cum) load pairs in flight per lane of the t8 pass; measured 4 / 5 / 6 / 8: c3 4.34 / 4.39 / 3.65 / 3.91 TB/s, c4 3.94 / 4.18 / 3.54 / 3.81
+#endif
+template <typename G, bool T8>
 __global__ void k_gain_full(SiteArgs a, const SiteState* st, const int4* __restrict__ wins,
                             const uint64_t* __restrict__ words, const uint64_t* __restrict__ cum,
-                            G* __restrict__ gain, unsigned long long* __restrict__ counters) {
+                            G* __restrict__ gain, unsigned long long* __restrict__ counters,
+                            const int4* __restrict__ wins_alg, int64_t pf_ahead) {
     if (st && (st->done || st->finish)) return;
     const int lane = threadIdx.x & 31;
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long bytes = 0;
     for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < a.n; i += warps) {
         const int4 win = wins[i];
-        const int nwr = win_nwr(win.y, win.w), total = win.z * nwr;
+        const int nwr = T8 ? win.w : win_nwr(win.y, win.w), total = win.z * nwr;
         const uint64_t* v = words + i * a.stride;
-        const uint64_t* crow = cum + (int64_t)win.x * a.wpr + (win.y >> 6);
+        const uint64_t* crow = cum + (int64_t)win.x * a.wpr + (T8 ? win.y : (win.y >> 6));
+        if (T8 && pf_ahead >= 0 && i + pf_ahead < a.n) {
+            // a tile cum larger than L2 (c4: 269 MB) misses on every pass, and a warp
+            // stalled on scattered cum sectors holds back its stream loads: the
+            // candidate's tile rows (lane = tile row, <= 3 lines each) go to L2 first
+            // (measured at c4, look-ahead 0 / 8 / 148 / 1184 candidates: 3.94 / 3.84 /
+            // 3.89 / 3.84 TB/s against 3.54 without; with the cum resident in L2 the
+            // prefetches only cost issue slots, c3 4.34 -> 4.11)
+            const int4 wf = pf_ahead ? wins[i + pf_ahead] : win;
+            if (lane < wf.z) {
+                const uint64_t* q = cum + (int64_t)(wf.x + lane) * a.wpr + wf.y;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(q + 16));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(q + wf.w - 1));
+            }
+        }
         // word t -> (y, b): y = t / nwr via incremental steps of 32 words
         int y = lane / nwr, b = lane - y * nwr;
         const int dy = 32 / nwr, db = 32 - dy * nwr;
         int acc = 0;
-        constexpr int U = 4;
+        constexpr int U = T8 ? GAIN_T8_U : 4;
+#ifdef GAIN_PROBE_FOLD
+        const int ymask = (a.prof & 2) ? 1 : -1;   // timing probe: cum reads folded onto two rows (wrong gains)
+#else
+        constexpr int ymask = -1;
+#endif
         for (int t0 = lane; t0 < total; t0 += 32 * U) {
             uint64_t vw[U], cw[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const bool ok = t0 + 32 * u < total;
                 vw[u] = ok ? __ldcs(v + t0 + 32 * u) : 0ull;
-                cw[u] = ok ? __ldg(crow + (int64_t)y * a.wpr + b) : 0ull;
+                cw[u] = ok ? __ldg(crow + (int64_t)(y & ymask) * a.wpr + b) : 0ull;
                 y += dy; b += db;
                 if (b >= nwr) { b -= nwr; ++y; }
             }
@@ -679,10 +708,82 @@ __global__ void k_gain_full(SiteArgs a, const SiteState* st, const int4* __restr
         for (int o = 16; o; o >>= 1) acc += __shfl_down_sync(kFull, acc, o);
         if (lane == 0) {
             gain[i] = (G)acc;
-            bytes += 8ull * (((unsigned long long)win.z * win.w + 63) >> 6);   // SPEC-layout (algorithmic) bytes
+            if (counters) {   // SPEC-layout (algorithmic) bytes
+                const int4 wa = T8 ? wins_alg[i] : win;
+                bytes += 8ull * (((unsigned long long)wa.z * wa.w + 63) >> 6);
+            }
         }
     }
     if (counters && lane == 0 && bytes) atomicAdd(counters + kSiteBytes, bytes);
+}
+
+// ---- 8x8-tile ("t8") shadow layout of the streaming gain pass ---------------
+// Word (TY, TX) of a tile bitmap holds terrain rows 8TY..8TY+7 x columns
+// 8TX..8TX+7, bit (r & 7) * 8 + (c & 7).  A (2R+1)^2 window touches at most
+// ((2R+7)/8 + 1)^2 tiles: 1.07x its packed size at roi 100 (1.04x at 200),
+// where the cum-aligned rows -- padded to 64-bit terrain words in ONE
+// dimension -- take 1.32x (1.16x).  The streaming pass reads exactly these
+// words, so the padding is HBM traffic; the tile words keep the property the
+// pass needs: word t of a candidate has ONE cum counterpart (no shifts).
+// Tile columns are bytes of the cum-aligned words (8 | 64), so the conversion
+// gathers one byte from each of 8 rows.
+__host__ __device__ inline int t8_span(int lo, int len) { return ((lo + len - 1) >> 3) - (lo >> 3) + 1; }
+inline int64_t t8_stride(int64_t roi) { const int64_t m = ((2 * roi + 7) >> 3) + 1; return m * m; }
+
+__global__ void k_words_to_t8(int64_t n, const int4* __restrict__ wins, const uint64_t* __restrict__ words,
+                              int64_t stride, uint64_t* __restrict__ t8, int64_t t8stride, int4* __restrict__ t8win) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+        const int4 win = wins[i];   // row0, col0, h, w
+        const int nwr = win_nwr(win.y, win.w), wlo = win.y >> 6;
+        const int ty0 = win.x >> 3, tx0 = win.y >> 3;
+        const int nty = t8_span(win.x, win.z), ntx = t8_span(win.y, win.w);
+        if (lane == 0) t8win[i] = make_int4(ty0, tx0, nty, ntx);
+        const uint64_t* v = words + i * stride;
+        uint64_t* o = t8 + i * t8stride;
+        for (int t = lane; t < nty * ntx; t += 32) {
+            const int ty = t / ntx, TX = tx0 + (t - ty * ntx);
+            const int b = (TX >> 3) - wlo, sh = (TX & 7) * 8;
+            uint64_t out = 0;
+#pragma unroll
+            for (int rr = 0; rr < 8; ++rr) {
+                const int y = (ty0 + ty) * 8 + rr - win.x;
+                if (y >= 0 && y < win.z) out |= ((v[y * nwr + b] >> sh) & 0xffull) << (rr * 8);
+            }
+            o[t] = out;
+        }
+    }
+}
+
+// row-padded cum (rows [cr0, cr1) held) -> tile cum of the whole grid
+__global__ void k_cum_to_t8(const uint64_t* __restrict__ cum, int64_t wpr, int cr0, int cr1, int th, int tw,
+                            uint64_t* __restrict__ t8cum) {
+    const int64_t total = (int64_t)th * tw;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int TY = (int)(t / tw), TX = (int)(t - (int64_t)TY * tw);
+        const int sh = (TX & 7) * 8;
+        uint64_t out = 0;
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) {
+            const int r = TY * 8 + rr;
+            if (r >= cr0 && r < cr1) out |= ((cum[(int64_t)r * wpr + (TX >> 3)] >> sh) & 0xffull) << (rr * 8);
+        }
+        t8cum[t] = out;
+    }
+}
+
+// the round's winner into the tile cum (beside k_commit's row-padded cum)
+__global__ void k_commit_t8(const SiteState* st, const int4* __restrict__ t8win, const uint64_t* __restrict__ t8,
+                            int64_t t8stride, uint64_t* __restrict__ t8cum, int tw) {
+    if (st->done) return;
+    const int4 win = t8win[st->w_idx];
+    const uint64_t* v = t8 + (int64_t)st->w_idx * t8stride;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < win.z * win.w; t += gridDim.x * blockDim.x) {
+        const int ty = t / win.w, tx = t - ty * win.w;
+        const uint64_t x = v[t];
+        if (x) t8cum[(int64_t)(win.x + ty) * tw + win.y + tx] |= x;
+    }
 }
 
 // Bucket-tiled form of k_gain_full (mode-1 rounds): one CTA per candidate
@@ -1060,7 +1161,7 @@ SiteArgs make_args(txs_ctx* c, const txs_params& p) {
     a.total = (double)c->nrows * (double)c->ncols;
     a.cr0 = (int)c->cum_r0; a.cr1 = (int)c->cum_r1;
     a.dpitch = (int)c->dpitch;
-    a.prof = getenv("TXS_SITE_PROFILE") ? 1 : 0;
+    a.prof = (getenv("TXS_SITE_PROFILE") ? 1 : 0) | (getenv("TXS_GAIN_FOLD") ? 2 : 0);
     return a;
 }
 
@@ -1150,21 +1251,73 @@ static txs_status build_strip_tasks(txs_ctx* c, const SiteArgs& a, const StripSh
     return TXS_OK;
 }
 
-// TXS_GAIN_PASS=full|tiled|strips overrides the measured choice (A/B only;
+// The t8 shadow (tile words of every viewshed + the tile cum) for the current
+// candidate set; built once per viewshed set (t8_valid), the tile cum zeroed or
+// converted from the row-padded cum by the caller.  false when HBM is short.
+static bool t8_fits(txs_ctx* c, const SiteArgs& a) {
+    if (c->t8_valid) return true;
+    const size_t need = sizeof(uint64_t) * (size_t)(std::max<int64_t>(1, a.n) * t8_stride(a.R));
+    if (c->t8_words_cap >= need) return true;
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return false;
+    return fr > need + (need >> 3) + ((size_t)1 << 30);
+}
+
+static txs_status build_t8(txs_ctx* c, const SiteArgs& a) {
+    const int th = (a.nrows + 7) >> 3, tw = (a.ncols + 7) >> 3;
+    if (ensure(c, "site", (void**)&c->d_t8_cum, &c->t8_cum_cap, sizeof(uint64_t) * (size_t)((int64_t)th * tw + 1)) != TXS_OK)
+        return TXS_ERR_OUT_OF_MEMORY;
+    if (c->t8_valid) return TXS_OK;
+    const int64_t ts = t8_stride(a.R);
+    if (ensure(c, "site", (void**)&c->d_t8_words, &c->t8_words_cap, sizeof(uint64_t) * (size_t)(std::max<int64_t>(1, a.n) * ts)) != TXS_OK ||
+        ensure(c, "site", (void**)&c->d_t8_win, &c->t8_win_cap, sizeof(int4) * (size_t)std::max<int64_t>(1, a.n)) != TXS_OK)
+        return TXS_ERR_OUT_OF_MEMORY;
+    if (a.n > 0) {
+        k_words_to_t8<<<blocks_for(a.n * 32, 256, c->num_sms * 16), 256, 0, c->stream>>>(a.n, c->d_win, c->d_words, a.stride,
+                                                                                       c->d_t8_words, ts, c->d_t8_win);
+        TXS_LAUNCHED(c, "site");
+    }
+    c->t8_valid = true;
+    return TXS_OK;
+}
+
+// TXS_GAIN_PASS=full|tiled|strips|t8 overrides the measured choice (A/B only;
 // k_gain_strips measured slower than k_gain_full at c2-c4 and equal to
-// k_gain_tiled at c5, profiles/README.md)
-static int gain_pass_kind(const SiteArgs& a, bool buckets, size_t* smem, StripShape* sp) {
+// k_gain_tiled at c5, profiles/README.md).  Kinds: 0 cum-aligned rows, 1
+// bucket-tiled cum in shared memory, 2 strips, 3 the 8x8-tile shadow.
+static int gain_pass_kind(txs_ctx* c, const SiteArgs& a, bool buckets, size_t* smem, StripShape* sp) {
     size_t ts = 0;
     const bool tiled = gain_tiled(a, buckets, &ts);
     const int rows = buckets ? strip_rows(a, sp) : 0;
-    int kind = tiled ? 1 : 0;   // strips: A/B only (slower at c2-c5, profiles/README.md)
+    // t8: SITE rounds on a whole-grid cum only (the shadow is per viewshed set)
+    const bool t8ok = buckets && a.cr0 == 0 && a.cr1 == a.nrows && a.n > 0 && t8_fits(c, a);
+    int kind = t8ok ? 3 : (tiled ? 1 : 0);   // measured: t8 >= tiled at c5 (5.41 vs 5.15 TB/s), >= rows at c2-c4
     if (const char* e = getenv("TXS_GAIN_PASS")) {
         if (!strcmp(e, "full")) kind = 0;
         else if (!strcmp(e, "tiled") && buckets) kind = 1;
         else if (!strcmp(e, "strips") && rows > 0) kind = 2;
+        else if (!strcmp(e, "t8") && t8ok) kind = 3;
     }
     *smem = kind == 1 ? ts : kind == 2 ? sp->smem : 0;
     return kind;
+}
+
+// CTAs per SM of the per-candidate passes' grid (TXS_GAIN_GRID, A/B).  Five
+// 256-thread CTAs are resident per SM: 16 per SM made 3.2 waves with an idle
+// tail; measured 5 / 16 / 64 / 256 per SM, TB/s: c3 t8 4.09 / 4.10 / 4.34 /
+// 4.21, c4 rows 3.44 / 3.32 / 3.65 / 3.54, c5 t8 5.17 / 4.94 / 5.41 / 5.46
+static int gain_grid_mult() {
+    const char* e = getenv("TXS_GAIN_GRID");
+    return e ? std::max(1, atoi(e)) : 64;
+}
+
+// t8 pass: candidates of look-ahead for the tile-cum L2 prefetch (< 0 = none):
+// only when the tile cum cannot stay in L2 between passes (c4: 269 MB);
+// TXS_GAIN_PF_AHEAD overrides (A/B)
+static int64_t t8_prefetch_ahead(txs_ctx*, const SiteArgs& a) {
+    if (const char* e = getenv("TXS_GAIN_PF_AHEAD")) return std::max<long long>(-1, atoll(e));
+    const int64_t cum_bytes = (int64_t)((a.nrows + 7) >> 3) * ((a.ncols + 7) >> 3) * 8;
+    return cum_bytes > (int64_t)96 << 20 ? 0 : -1;
 }
 
 template <typename G>
@@ -1172,8 +1325,14 @@ static void launch_gain_pass(txs_ctx* c, const SiteArgs& a, const SiteState* st,
                              unsigned long long* counters, bool buckets) {
     size_t smem = 0;
     StripShape sp{};
-    const int kind = gain_pass_kind(a, buckets, &smem, &sp);
-    if (kind == 2) {
+    const int kind = gain_pass_kind(c, a, buckets, &smem, &sp);
+    if (kind == 3) {   // `cum` is not read: the tile cum shadows it (build_t8 / k_commit_t8 / k_cum_to_t8)
+        SiteArgs t = a;
+        t.stride = t8_stride(a.R);
+        t.wpr = (a.ncols + 7) >> 3;
+        k_gain_full<G, true><<<blocks_for(a.n * 32, 256, c->num_sms * gain_grid_mult()), 256, 0, c->stream>>>(
+            t, st, c->d_t8_win, c->d_t8_words, c->d_t8_cum, gain, counters, c->d_win, t8_prefetch_ahead(c, a));
+    } else if (kind == 2) {
         k_zero_gains<G><<<blocks_for(a.n, 256, c->num_sms * 4), 256, 0, c->stream>>>(st, gain, a.n);
         auto kern = k_gain_strips<G>;
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1192,8 +1351,8 @@ static void launch_gain_pass(txs_ctx* c, const SiteArgs& a, const SiteState* st,
         kern<<<grid, kTiledThreads, smem, c->stream>>>(a, st, c->d_win, c->d_words, cum, c->d_bucket_start,
                                                        c->d_bucket_items, gain, counters);
     } else {
-        k_gain_full<G><<<blocks_for(a.n * 32, 256, c->num_sms * 16), 256, 0, c->stream>>>(a, st, c->d_win, c->d_words,
-                                                                                          cum, gain, counters);
+        k_gain_full<G, false><<<blocks_for(a.n * 32, 256, c->num_sms * gain_grid_mult()), 256, 0, c->stream>>>(
+            a, st, c->d_win, c->d_words, cum, gain, counters, nullptr, -1);
     }
 }
 
@@ -1371,16 +1530,24 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
     cudaGraphExec_t exec = nullptr;
     size_t gp_smem = 0;
     StripShape gp_shape{};
-    const int gp_kind = p.site_mode == 1 ? gain_pass_kind(a, true, &gp_smem, &gp_shape) : -1;
+    const int gp_kind = p.site_mode == 1 ? gain_pass_kind(c, a, true, &gp_smem, &gp_shape) : -1;
     if (gp_kind == 2) {
         const txs_status bs = build_strip_tasks(c, a, gp_shape);
         if (bs != TXS_OK) return bs;
+    }
+    const int t8w = (a.ncols + 7) >> 3, t8h = (a.nrows + 7) >> 3;
+    if (gp_kind == 3) {
+        const txs_status bs = build_t8(c, a);
+        if (bs != TXS_OK) return bs;
+        TXS_CUDA(c, "site", cudaMemsetAsync(c->d_t8_cum, 0, sizeof(uint64_t) * (size_t)((int64_t)t8h * t8w), c->stream));
     }
     TXS_CUDA(c, "site", cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     for (int r = 0; r < kRoundsPerGraph; ++r) {
         if (p.site_mode == 1) launch_gain_pass<int32_t>(c, a, c->d_state, cumv, c->d_gain, c->d_counters, true);
         k_argmax<<<am_blocks, 256, 0, c->stream>>>(c->d_gain, a, c->d_state, lp, c->d_dspan);
         k_commit<<<cm_blocks, 256, 0, c->stream>>>(a, c->d_state, c->d_words, cumv, c->d_dwin, c->d_dspan, nullptr);
+        if (gp_kind == 3)
+            k_commit_t8<<<cm_blocks, 256, 0, c->stream>>>(c->d_state, c->d_t8_win, c->d_t8_words, t8_stride(a.R), c->d_t8_cum, t8w);
         if (p.site_mode != 1)
             k_update<<<up_blocks, kUpdThreads, 0, c->stream>>>(a, c->d_state, c->d_win, c->d_words, c->d_dwin,
                                                                c->d_dspan, c->d_bucket_items, c->d_gain, c->d_counters);
@@ -1389,7 +1556,7 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
     if (ce != cudaSuccess) return cuda_fail(c, "site", ce);
     ce = cudaGraphInstantiate(&exec, graph, 0);
     if (ce != cudaSuccess) { cudaGraphDestroy(graph); return cuda_fail(c, "site", ce); }
-    const int per_round = gp_kind == 2 ? 4 : 3;
+    const int per_round = (gp_kind == 2 || gp_kind == 3) ? 4 : 3;
     txs_status st = TXS_OK;
     int64_t graphs = 0;
     for (;;) {
@@ -1446,9 +1613,18 @@ txs_status time_gain_pass(txs_ctx* c, int32_t reps, double* ms, int64_t* bytes) 
     uint64_t* cumv = c->d_cum - c->cum_r0 * c->wpr;
     size_t gp_smem = 0;
     StripShape gp_shape{};
-    if (gain_pass_kind(a, true, &gp_smem, &gp_shape) == 2) {
+    const int gp_kind = gain_pass_kind(c, a, true, &gp_smem, &gp_shape);
+    if (gp_kind == 2) {
         const txs_status bs = build_strip_tasks(c, a, gp_shape);
         if (bs != TXS_OK) return bs;
+    }
+    if (gp_kind == 3) {   // the tile cum from the current row-padded cum
+        const txs_status bs = build_t8(c, a);
+        if (bs != TXS_OK) return bs;
+        const int t8w = (a.ncols + 7) >> 3, t8h = (a.nrows + 7) >> 3;
+        k_cum_to_t8<<<blocks_for((int64_t)t8h * t8w, 256, c->num_sms * 16), 256, 0, c->stream>>>(cumv, a.wpr, a.cr0, a.cr1, t8h,
+                                                                                                t8w, c->d_t8_cum);
+        TXS_LAUNCHED(c, "site");
     }
     TXS_CUDA(c, "site", cudaMemsetAsync(c->d_counters + kSiteBytes, 0, sizeof(unsigned long long), c->stream));
     launch_gain_pass<int32_t>(c, a, nullptr, cumv, c->d_gain, c->d_counters, true);   // warm-up (+ byte count)

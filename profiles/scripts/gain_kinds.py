@@ -1,4 +1,4 @@
-"""SITE streaming gain pass: every kernel form (TXS_GAIN_PASS=full|tiled|strips)
+"""SITE streaming gain pass: every kernel form (TXS_GAIN_PASS=full|tiled|strips|t8)
 on a BASELINE config, timed alone (txs_time_gain_pass) and checked by running
 64 full-rescan SITE rounds with it against the incremental SITE's picks.
 python profiles/scripts/gain_kinds.py c3 [kinds...]"""
@@ -12,7 +12,7 @@ from paper_2006_16783_b200 import Engine, make_params  # noqa: E402
 from paper_2006_16783_b200.configs import CONFIGS, params_for, setup_terrain  # noqa: E402
 
 cfg = CONFIGS[sys.argv[1]]
-kinds = sys.argv[2:] or ["full", "tiled", "strips"]
+kinds = sys.argv[2:] or ["full", "tiled", "strips", "t8"]
 e = Engine()
 setup_terrain(e, cfg)
 p0 = params_for(cfg)

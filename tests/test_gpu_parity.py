@@ -329,11 +329,12 @@ def test_site_bucket_tiled_bit_exact(engine, mode):
     _site_compare(engine, 20, rows, cols, 200, 256, 1.0, 0, mode)
 
 
-@pytest.mark.parametrize("kind,shape", [("full", None), ("tiled", None), ("strips", None), ("strips", "8x1"),
-                                        ("strips", "40x3")])
+@pytest.mark.parametrize("kind,shape", [("full", None), ("tiled", None), ("t8", None), ("t8", "pf0"), ("t8", "pf7"),
+                                        ("strips", None), ("strips", "8x1"), ("strips", "40x3")])
 def test_site_full_rescan_gain_pass_forms(engine, monkeypatch, kind, shape):
     """Mode-1 rounds through every gain-pass kernel (per-candidate, bucket-tiled,
-    strip-tile task list with bulk copies; A/B knob TXS_GAIN_PASS) and strip
+    the 8x8-tile shadow layout with its own cum, strip-tile task list with bulk
+    copies; A/B knob TXS_GAIN_PASS) and strip
     shapes whose tiles cut windows at many rows and bucket columns; grid edges
     and a duplicate included."""
     T = _T()
@@ -346,7 +347,10 @@ def test_site_full_rescan_gain_pass_forms(engine, monkeypatch, kind, shape):
     engine.set_candidates(rows, cols)
     engine.compute_all_viewsheds(T.make_params(33, 10, 10))
     monkeypatch.setenv("TXS_GAIN_PASS", kind)
-    if shape:
+    if shape and shape.startswith("pf"):   # the tile-cum L2 prefetch of grids whose cum exceeds L2
+        monkeypatch.setenv("TXS_GAIN_PF_AHEAD", shape[2:])
+        monkeypatch.setenv("TXS_GAIN_GRID", "1")   # several candidates per warp
+    elif shape:
         sh, tx = shape.split("x")
         monkeypatch.setenv("TXS_STRIP_ROWS", sh)
         monkeypatch.setenv("TXS_STRIP_TX", tx)
