@@ -639,6 +639,276 @@ __global__ void __launch_bounds__(kL1Threads, 2) k_site_loop1(SiteArgs a, SiteSt
     }
 }
 
+// ---- the same loop inside ONE thread-block cluster (site_mode 0, few neighbours per round) --
+// When a round updates only tens of neighbours (roi 100: c3, c4) the round is
+// the latency of its barrier and of its scans: a grid barrier costs ~1.2 us
+// before any waiting (profiles/scripts/gridsync_bench.cu) and the 148-CTA loop
+// spent 2.7 of its 5.3 us per round there.  A cluster of CS CTAs (16,
+// non-portable size) runs the identical round structure with a hardware
+// cluster barrier, and the per-CTA partial winners travel through distributed
+// shared memory: CTA k stores its {key, position, window} into slot k of every
+// peer's s_parts[parity], so the winner reduction reads local shared memory.
+// Ownership follows the neighbour-bucket order (d_bucket_items, buckets of
+// side R sorted row-major): the candidate at sorted position s belongs to CTA
+// s mod CS, local slot s / CS, so the winner's neighbours are <= 5 contiguous
+// local ranges (one per bucket row) instead of a scan of every owned
+// candidate, and the per-CTA argmax keeps a maximum per chunk of 32 slots,
+// recomputed only for the chunks those ranges touch (gains only change
+// there).  Per candidate in shared memory: position (2 x u16), index, gain, a
+// u16 neighbour-list slot.  Same picks, gains and cum as k_site_loop1 (commit
+// of w_{r-1} one round late, racing cum reads compensated by ~v_prev).
+#ifndef SITE_LC_THREADS
+#define SITE_LC_THREADS 512
+#endif
+constexpr int kLcThreads = SITE_LC_THREADS;
+constexpr int kLcMaxCluster = 16;
+constexpr int kLcMaxRanges = 8;   // bucket rows within 2R of a winner: <= 5 at bucket side R
+
+__device__ __forceinline__ int4 roi_box(const SiteArgs& a, int r, int c) {
+    const int row0 = max(0, r - a.R), col0 = max(0, c - a.R);
+    return make_int4(row0, col0, min(a.nrows - 1, r + a.R) - row0 + 1, min(a.ncols - 1, c + a.R) - col0 + 1);
+}
+
+__global__ void __launch_bounds__(kLcThreads, 1) k_site_loopc(SiteArgs a, SiteState* st, LoopPtrs lp,
+                                                              const int32_t* __restrict__ pop, int32_t* __restrict__ gain,
+                                                              const int32_t* __restrict__ items,
+                                                              const uint64_t* __restrict__ words, uint64_t* __restrict__ cum,
+                                                              unsigned long long* __restrict__ counters) {
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    const int G = (int)cluster.num_blocks(), cta = (int)cluster.block_rank(), tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int kWarps = kLcThreads / 32;
+    const int m = (int)((a.n - cta + G - 1) / G);   // owned: sorted positions s = cta + G j, j < m
+    const int mmax = (int)((a.n + G - 1) / G);      // the same carve-up in every CTA
+    const int nchunk = (mmax + 31) >> 5;
+    uint32_t* s_pos = (uint32_t*)s_dyn;             // row << 16 | col
+    int* s_idx = (int*)(s_pos + mmax);              // candidate index
+    int* s_gain = s_idx + mmax;
+    unsigned long long* s_ckey = (unsigned long long*)(s_gain + mmax + (mmax & 1));   // per chunk of 32 slots: best key
+    int* s_cj = (int*)(s_ckey + nchunk);                                               // ... and its slot
+    uint16_t* s_nb = (uint16_t*)(s_cj + nchunk);    // owned candidates overlapping the winner (mmax <= 65535)
+    __shared__ SitePart s_parts[2][kLcMaxCluster];  // [parity][writer rank], written by the peers
+    __shared__ unsigned long long s_key[kWarps];
+    __shared__ int s_kj[kWarps], s_wsum[kWarps];
+    __shared__ int s_nnb, s_nrows[kLcThreads];
+    __shared__ int s_rng[2 * kLcMaxRanges];         // local slot ranges [lo, hi) of the winner's bucket rows
+    for (int j = tid; j < m; j += blockDim.x) {
+        const int i = items[cta + (int64_t)G * j];
+        s_pos[j] = ((uint32_t)lp.crow[i] << 16) | (uint32_t)lp.ccol[i];
+        s_idx[j] = i;
+        s_gain[j] = pop[i];
+    }
+    __syncthreads();
+    // best key of chunk ch (slots 32 ch .. 32 ch + 31), by one warp
+    auto chunk_max = [&](int ch) {
+        const int j = ch * 32 + lane;
+        unsigned long long bk = 0ull;
+        int bj = -1;
+        if (j < m) { bk = ((unsigned long long)(uint32_t)s_gain[j] << 32) | (0xffffffffull - (uint64_t)(uint32_t)s_idx[j]); bj = j; }
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long k2 = __shfl_xor_sync(kFull, bk, o);
+            const int j2 = __shfl_xor_sync(kFull, bj, o);
+            if (k2 > bk) { bk = k2; bj = j2; }
+        }
+        if (lane == 0) { s_ckey[ch] = bk; s_cj[ch] = bj; }
+    };
+    // the CTA's best over its chunk maxima -> slot `cta` of every peer's s_parts[buf]
+    auto write_partial = [&](int buf) {
+        unsigned long long bk = 0ull;
+        int bj = -1;
+        for (int ch = tid; ch < nchunk; ch += blockDim.x) {
+            const unsigned long long key = s_ckey[ch];
+            if (key > bk) { bk = key; bj = s_cj[ch]; }
+        }
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long k2 = __shfl_xor_sync(kFull, bk, o);
+            const int j2 = __shfl_xor_sync(kFull, bj, o);
+            if (k2 > bk) { bk = k2; bj = j2; }
+        }
+        if (lane == 0) { s_key[warp] = bk; s_kj[warp] = bj; }
+        __syncthreads();
+        if (tid < G) {   // thread k delivers this CTA's partial to peer k
+            unsigned long long x = s_key[0];
+            int xj = s_kj[0];
+            for (int k = 1; k < kWarps; ++k)
+                if (s_key[k] > x) { x = s_key[k]; xj = s_kj[k]; }
+            SitePart out{0ull, 0, 0, 0, 0, 0, 0};
+            if (xj >= 0) {
+                const uint32_t rc = s_pos[xj];
+                const int4 wv = roi_box(a, (int)(rc >> 16), (int)(rc & 0xffffu));
+                out = SitePart{x, (int)(rc >> 16), (int)(rc & 0xffffu), wv.x, wv.y, wv.z, wv.w};
+            }
+            SitePart* peer = cluster.map_shared_rank(&s_parts[buf][cta], tid);
+            *peer = out;
+        }
+    };
+    for (int ch = warp; ch < nchunk; ch += kWarps) chunk_max(ch);
+    __syncthreads();
+    write_partial(0);
+    cluster.sync();
+    long long nsel = 0, covered = 0;
+    int stop = TXS_STOP_EXHAUSTED;
+    bool have_prev = false;
+    SitePart prev{};
+    int64_t prev_idx = 0;
+    unsigned long long bytes_all = 0;
+    const bool prof = a.prof && cta == 0 && tid == 0;
+    unsigned long long ph[5] = {0, 0, 0, 0, 0}, tp = prof ? gtimer() : 0;
+    auto mark = [&](int k) {
+        if (prof) { const unsigned long long t = gtimer(); ph[k] += t - tp; tp = t; }
+    };
+    for (int it = 0;; ++it) {
+        // ---- 1. global winner from the local copies of the G partials (every warp, by shuffles)
+        SitePart best;
+        {
+            unsigned long long bk = lane < G ? s_parts[it & 1][lane].key : 0ull;
+            int bw = lane < G ? lane : 0;
+            for (int o = 16; o; o >>= 1) {
+                const unsigned long long k2 = __shfl_xor_sync(kFull, bk, o);
+                const int w2 = __shfl_xor_sync(kFull, bw, o);
+                if (k2 > bk) { bk = k2; bw = w2; }
+            }
+            best = s_parts[it & 1][bw];
+        }
+        const int g = (int)(best.key >> 32);
+        const int64_t idx = (int64_t)(0xffffffffull - (best.key & 0xffffffffull));
+        // the winner's neighbour buckets: rows by0..by1, columns bx0..bx1 -> one sorted range per
+        // bucket row -> local slots [ceil((s0 - cta) / G), ceil((s1 - cta) / G))
+        const int by0 = max(0, (best.r - 2 * a.R) / a.bsize), by1 = min(a.nby - 1, (best.r + 2 * a.R) / a.bsize);
+        const int bx0 = max(0, (best.c - 2 * a.R) / a.bsize), bx1 = min(a.nbx - 1, (best.c + 2 * a.R) / a.bsize);
+        const int nrng = min(kLcMaxRanges, by1 - by0 + 1);
+        if (g > 0 && tid < 2 * nrng) {
+            const int by = by0 + (tid >> 1);
+            const int sp = __ldg(lp.bstart + by * a.nbx + ((tid & 1) ? bx1 + 1 : bx0));
+            s_rng[tid] = max(0, (sp - cta + G - 1) / G);
+        }
+        mark(0);
+        mark(1);
+        // a stop ends the loop before this round's end-of-round commit of w_{r-1}: do it here
+        const bool stop_now = nsel >= a.n || g <= 0;
+        if (stop_now && have_prev) flush_rows(a, prev, words + prev_idx * a.stride, cum, cta, G);
+        if (nsel >= a.n) { stop = TXS_STOP_EXHAUSTED; break; }
+        if (g <= 0) { stop = TXS_STOP_ZERO_GAIN; break; }
+        covered += g;
+        const double cov = (double)covered / a.total;
+        if (cta == 0 && tid == 0) lp.steps[nsel] = txs_step{idx, best.r, best.c, (int64_t)g, cov};
+        ++nsel;
+        const uint64_t* vw = words + idx * a.stride;
+        if (cov >= a.target || (a.max_sel > 0 && nsel >= a.max_sel)) {
+            stop = cov >= a.target ? TXS_STOP_TARGET_REACHED : TXS_STOP_MAX_SELECTED;
+            if (have_prev) flush_rows(a, prev, words + prev_idx * a.stride, cum, cta, G);
+            flush_rows(a, best, vw, cum, cta, G);   // the final commit
+            break;
+        }
+        // ---- 3. owned neighbours: gain -= popc(v_i & v_w & ~cum & ~v_prev)
+        if (tid == 0) s_nnb = 0;
+        __syncthreads();
+        const int wr1 = best.row0 + best.h - 1, wc1 = best.col0 + best.w - 1;
+        // windows overlap iff the origins are within 2R of each other in both axes
+        // (clipping at the grid edge shortens both boxes on the same side)
+        for (int q = 0; q < nrng; ++q) {
+            const int lo = s_rng[2 * q], hi = min(m, s_rng[2 * q + 1]);
+            for (int j = lo + tid; j < hi; j += blockDim.x) {
+                const uint32_t rc = s_pos[j];
+                if (abs((int)(rc >> 16) - best.r) <= 2 * a.R && abs((int)(rc & 0xffffu) - best.c) <= 2 * a.R)
+                    s_nb[atomicAdd(&s_nnb, 1)] = (uint16_t)j;
+            }
+        }
+        __syncthreads();
+        const int nnb = s_nnb;
+        if (nnb > 0) {
+            const int nwr_w = win_nwr(best.col0, best.w), wlo_w = best.col0 >> 6;
+            const int nwr_p = have_prev ? win_nwr(prev.col0, prev.w) : 0, wlo_p = prev.col0 >> 6;
+            const uint64_t* vp = have_prev ? words + prev_idx * a.stride : nullptr;
+            int total = 0;
+            for (int k0 = 0; k0 < nnb; k0 += blockDim.x) {
+                int rows = 0;
+                if (k0 + tid < nnb) {
+                    const uint32_t rc = s_pos[s_nb[k0 + tid]];
+                    const int4 wv = roi_box(a, (int)(rc >> 16), (int)(rc & 0xffffu));
+                    rows = max(0, min(wv.x + wv.z - 1, wr1) - max(wv.x, best.row0) + 1);
+                }
+                int incl = rows;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                __syncthreads();
+                if (lane == 31) s_wsum[warp] = incl;
+                __syncthreads();
+                int woff = 0, ctot = 0;
+                for (int q = 0; q < kWarps; ++q) {
+                    const int v = s_wsum[q];
+                    if (q < warp) woff += v;
+                    ctot += v;
+                }
+                s_nrows[tid] = woff + incl;   // inclusive prefix of the chunk's neighbours
+                __syncthreads();
+                const int cn = min((int)blockDim.x, nnb - k0);
+                for (int t = tid; t < ctot; t += blockDim.x) {
+                    int lo = 0, hi = cn - 1;     // the neighbour holding pair t
+                    while (lo < hi) { const int mid = (lo + hi) >> 1; if (s_nrows[mid] > t) hi = mid; else lo = mid + 1; }
+                    const int j = s_nb[k0 + lo];
+                    const uint32_t rc = s_pos[j];
+                    const int4 wv = roi_box(a, (int)(rc >> 16), (int)(rc & 0xffffu));
+                    const int y = max(wv.x, best.row0) + t - (lo ? s_nrows[lo - 1] : 0);
+                    const int cl = max(wv.y, best.col0), ch = min(wv.y + wv.w - 1, wc1);
+                    const int64_t i = s_idx[j];
+                    const uint64_t* vi = words + i * a.stride + (int64_t)(y - wv.x) * win_nwr(wv.y, wv.w) - (wv.y >> 6);
+                    const uint64_t* vwr = vw + (int64_t)(y - best.row0) * nwr_w - wlo_w;
+                    const bool prow = have_prev && y >= prev.row0 && y < prev.row0 + prev.h;
+                    const uint64_t* vpr = prow ? vp + (int64_t)(y - prev.row0) * nwr_p - wlo_p : nullptr;
+                    const uint64_t* cr = cum + (int64_t)y * a.wpr;
+                    int acc = 0;
+                    for (int B = cl >> 6; B <= (ch >> 6); ++B) {
+                        const uint64_t x = __ldg(vi + B) & __ldg(vwr + B) & ~__ldcg(cr + B);
+                        const uint64_t pv = (prow && B >= wlo_p && B < wlo_p + nwr_p) ? __ldg(vpr + B) : 0ull;
+                        acc += __popcll(x & ~pv);
+                    }
+                    if (acc) atomicSub(&s_gain[j], acc);
+                }
+                total += ctot;
+                __syncthreads();
+            }
+            bytes_all += 16ull * (unsigned long long)total;
+        }
+        __syncthreads();
+        mark(2);
+        // ---- 4. chunk maxima of the touched ranges, the new partial to every peer, the commit
+        // of the previous winner -> cluster barrier
+        {
+            int base = 0;   // (range, chunk) pairs flattened over the warps
+            for (int q = 0; q < nrng; ++q) {
+                const int lo = s_rng[2 * q], hi = min(m, s_rng[2 * q + 1]);
+                if (hi <= lo) continue;
+                const int c0 = lo >> 5, c1 = (hi - 1) >> 5;
+                for (int ch = c0 + ((warp - base) % kWarps + kWarps) % kWarps; ch <= c1; ch += kWarps) chunk_max(ch);
+                base += c1 - c0 + 1;
+            }
+        }
+        __syncthreads();
+        write_partial((it + 1) & 1);
+        if (have_prev) flush_rows(a, prev, words + prev_idx * a.stride, cum, cta, G);
+        mark(3);
+        prev = best;
+        prev_idx = idx;
+        have_prev = true;
+        cluster.sync();
+        mark(4);
+    }
+    if (prof)
+        for (int k = 0; k < 5; ++k) st->phase_ns[k] = ph[k];
+    for (int j = tid; j < m; j += blockDim.x) gain[s_idx[j]] = s_gain[j];
+    if (tid == 0 && bytes_all) atomicAdd(counters + kSiteBytes, bytes_all);
+    if (cta == 0 && tid == 0) {
+        st->nsel = nsel;
+        st->covered = covered;
+        st->stop = stop;
+        st->done = 1;
+    }
+    cluster.sync();   // no CTA exits while a peer may still address its shared memory
+}
+
 // Streaming form over the cum-aligned layout: lane t of the candidate's warp
 // reads word t (one coalesced, L1-bypassing load; the viewshed words are the
 // only HBM stream) = word b of window row y, whose cum counterpart is the
@@ -1429,6 +1699,64 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
     const double expected_nb = (double)n * span * span / ((double)c->nrows * (double)c->ncols);
     const bool persistent = p.site_mode == 0 && (expected_nb <= 1000.0 || getenv("TXS_SITE_PERSISTENT")) &&
                             !getenv("TXS_SITE_GRAPH");
+    // the loop inside one thread-block cluster (cluster barrier + partials through
+    // distributed shared memory): A/B only, TXS_SITE_CLUSTER=8|16.  Measured slower
+    // than the grid loop (profiles/README.md: the barrier drops from 2.7 to 0.75 us
+    // per round, but 16 SMs carry the neighbour updates 3x slower: c3 27.1 vs 21.9 ms,
+    // c4 24.2 vs 23.0)
+    if (persistent && !getenv("TXS_SITE_LOOP3") && n > 0) {
+        int want_cs = 0;
+        if (const char* e = getenv("TXS_SITE_CLUSTER")) want_cs = std::max(0, std::min(kLcMaxCluster, atoi(e)));
+        for (int cs = want_cs; cs >= 8; cs >>= 1) {
+            const int64_t mmax = (n + cs - 1) / cs;
+            const int64_t nchunk = (mmax + 31) / 32;
+            const size_t smem = (size_t)(mmax + 1) * 12 + (size_t)nchunk * 12 + (size_t)mmax * 2 + 32;
+            if (mmax > 65535 || smem > 216 * 1024 || c->nrows > 65535 || c->ncols > 65535 ||
+                4 * (int64_t)a.R / a.bsize + 2 > kLcMaxRanges)
+                continue;
+            if (cs > 8 && cudaFuncSetAttribute(k_site_loopc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+                cudaGetLastError();
+                continue;
+            }
+            if (cudaFuncSetAttribute(k_site_loopc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+                cudaGetLastError();
+                continue;
+            }
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3((unsigned)cs);
+            cfg.blockDim = dim3(kLcThreads);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = c->stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = (unsigned)cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+            cfg.attrs = at; cfg.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, k_site_loopc, &cfg) != cudaSuccess || nclusters < 1) {
+                cudaGetLastError();
+                continue;
+            }
+            cudaEventRecord(c->ev_r0, c->stream);
+            TXS_CUDA(c, "site", cudaLaunchKernelEx(&cfg, k_site_loopc, a, c->d_state, lp0, (const int32_t*)c->d_pop, c->d_gain,
+                                                   (const int32_t*)c->d_bucket_items, (const uint64_t*)c->d_words, cumv,
+                                                   c->d_counters));
+            TXS_LAUNCHED(c, "site");
+            cudaEventRecord(c->ev_r1, c->stream);
+            c->stats.site_launches += 1;
+            TXS_CUDA(c, "site", cudaMemcpyAsync(c->h_state, c->d_state, sizeof(SiteState), cudaMemcpyDeviceToHost, c->stream));
+            TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+            add_round_time(c);
+            const int64_t ns = c->h_state->nsel;
+            c->stats.site_iterations += ns;
+            out.resize((size_t)ns);
+            if (ns > 0) {
+                TXS_CUDA(c, "site", cudaMemcpyAsync(out.data(), d_steps, sizeof(txs_step) * ns, cudaMemcpyDeviceToHost, c->stream));
+                TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+            }
+            *stop = c->h_state->stop;
+            return TXS_OK;
+        }
+    }
     if (persistent && !getenv("TXS_SITE_LOOP3")) {
         // one-barrier persistent loop (k_site_loop1): owned gains/windows in shared memory
         // CTAs per SM (measured, profiles/README.md): one when few neighbours change per

@@ -522,7 +522,10 @@ __device__ __forceinline__ void vs_events_k3(const int* rk, const int* ck, const
         // software pipeline: the next iteration's events are loaded while this
         // one computes (the stream is padded by STEP rows of Nops at its end)
         // (two-event iterations only: at STEP 4 the extra registers cost more, c5 1027 -> 1055 ms)
-        constexpr bool kPre = STEP == 2;
+#ifndef VS_PRE4
+#define VS_PRE4 0
+#endif
+        constexpr bool kPre = STEP == 2 || VS_PRE4;
         uint2 en[STEP];
 #pragma unroll
         for (int u = 0; u < STEP; ++u) en[u] = kPre ? __ldg(ev + u * 32) : make_uint2(0u, 0u);
@@ -994,6 +997,11 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
                                                                  ev3);
         } else if (kobs == 2) {
             auto kern = cap64 ? (step4 ? k_viewshed_evk<2, 64, 4> : k_viewshed_evk<2, 64, 2>) : k_viewshed_evk<2, 72, 2>;
+            if (const char* e = getenv("TXS_VS_REGS")) {   // A/B: register cap x events per iteration
+                const int rg = atoi(e);
+                if (rg == 80) kern = step4 ? k_viewshed_evk<2, 80, 4> : k_viewshed_evk<2, 80, 2>;
+                else if (rg == 96) kern = step4 ? k_viewshed_evk<2, 96, 4> : k_viewshed_evk<2, 96, 2>;
+            }
             if (sm > 48 * 1024)
                 TXS_CUDA(c, "viewshed", cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             cudaEventRecord(c->ev_k0, c->stream);

@@ -376,6 +376,31 @@ def test_site_persistent_loop_widths(engine, monkeypatch, ctas):
     _site_compare(engine, 20, rows, cols, 300, 300, 0.97, 0, 0)
 
 
+@pytest.mark.parametrize("cs", ["16", "8", "0"])
+@pytest.mark.parametrize("case", ["sparse", "tiny", "maxsel"])
+def test_site_cluster_loop(engine, monkeypatch, cs, case):
+    """The SITE loop inside one thread-block cluster (cluster barrier, partial
+    winners through distributed shared memory; A/B knob TXS_SITE_CLUSTER) at
+    both cluster sizes and off, against the oracle:
+    sparse candidates with grid corners and a duplicate run to exhaustion, fewer
+    candidates than CTAs, and a max_selected stop."""
+    T = _T()
+    nr, nc, roi = 420, 380, 25
+    z = O.generate_fractal(nr, nc, 0.6, 31, 0, 3000)
+    rng = np.random.default_rng(77)
+    n = {"sparse": 700, "tiny": 5, "maxsel": 300}[case]
+    rows, cols = rng.integers(0, nr, n).astype(np.int32), rng.integers(0, nc, n).astype(np.int32)
+    if n > 5:
+        rows[:5], cols[:5] = [0, nr - 1, 0, nr - 1, 0], [0, nc - 1, nc - 1, 0, 0]
+    engine.set_terrain(z)
+    engine.set_candidates(rows, cols)
+    engine.compute_all_viewsheds(T.make_params(roi, 10, 10))
+    monkeypatch.setenv("TXS_SITE_CLUSTER", cs)
+    before = engine.stats()["site_launches"]
+    _site_compare(engine, roi, rows, cols, nr, nc, 1.0 if case != "maxsel" else 0.9, 40 if case == "maxsel" else 0, 0)
+    assert engine.stats()["site_launches"] == before + 1   # one persistent kernel either way
+
+
 def test_site_edge_cases(engine):
     T = _T()
     z = O.generate_fractal(64, 64, 0.5, 2, 0, 4000)
