@@ -11,6 +11,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 python profiles/scripts/vix_once.py c3 > $O/vix_once.log 2>&1 && \
 ncu --set full --import-source on --clock-control none -k regex:k_vix_lanes -c 1 -o $O/r02_vix_c3 -f \
     python profiles/scripts/vix_once.py c3 > $O/ncu_vix_full.log 2>&1
+profiles/scripts/gain_ncu.sh c3 c4
 for c in c3 c1 c2 c4 c5; do timeout 900 python bench.py --config $c > $O/final_bench_$c.log 2>&1; done
 timeout 900 python bench.py --impl reference > $O/final_ref_c3.log 2>&1
 echo done > $O/refresh_done.txt
