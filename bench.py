@@ -340,8 +340,10 @@ def stage_figures(st, K, cfg, site_mode, site_stream=None):
                                      cfg, peaks)}
     site_ms = st["ms_site"] / K
     stages["site"] = {"ms": round(site_ms, 3), "iterations": int(st["site_iterations"] // K),
-                      "kernel": "k_site_loop / k_argmax+k_commit+k_update" if site_mode == 0 else "k_gain_full",
-                      "mode": "exact incremental" if site_mode == 0 else "full-rescan"}
+                      "kernel": ("k_batch_bmax+decide+winners+delta+update (batched rounds; k_site_loop1 on small grids)"
+                                 if site_mode == 0 else "k_gain_full"),
+                      "launches": int(st["site_launches"] // K),
+                      "mode": "exact incremental, every local maximum per round" if site_mode == 0 else "full-rescan"}
     if site_stream:
         hbm = peaks["hbm"][0]
         site_stream["frac_of_hbm"] = round(site_stream["gbs"] / hbm, 4) if site_stream.get("gbs") else None

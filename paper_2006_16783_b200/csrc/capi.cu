@@ -130,7 +130,7 @@ void txs_destroy(txs_ctx* c) {
     void* bufs[] = {c->d_shard_steps, c->d_z, c->d_zt, c->d_pairs, c->d_gcd, c->d_vix, c->d_crow, c->d_ccol, c->d_cscore, c->d_words, c->d_win,
                     c->d_pop, c->d_cum, c->d_dwin, c->d_dspan, c->d_partials, c->d_gain, c->d_state,
                     c->d_bucket_start, c->d_bucket_items, c->d_counters, c->d_scratch, c->d_cgid, c->d_xfer,
-                    c->d_cum_dense, c->d_ties, c->d_strip_tasks, c->d_strip_start, c->d_t8_words, c->d_t8_win, c->d_t8_cum};
+                    c->d_cum_dense, c->d_ties, c->d_strip_tasks, c->d_strip_start, c->d_t8_words, c->d_t8_win, c->d_t8_cum, c->d_batch};
     for (void* p : bufs) if (p) cudaFree(p);
     for (auto& kv : c->templates) {
         cudaFree(kv.second.rays); cudaFree(kv.second.cells);

@@ -150,6 +150,8 @@ struct txs_ctx {
     int64_t dpitch = 0;
     unsigned long long* d_partials = nullptr;   // persistent SITE loop: per-CTA argmax
     size_t partials_cap = 0;
+    void* d_batch = nullptr;             // batched SITE (site.cu): bucket maxima, winner lists, delta windows, pick log
+    size_t batch_cap = 0;
     size_t bitmap_cap = 0;
     int32_t* d_gain = nullptr;
     size_t gain_cap = 0;

@@ -197,6 +197,7 @@ constexpr int kUpdU = SITE_UPD_U;   // delta words in flight per row in the neig
 // latency-bound), each row visiting only the delta span of non-zero words.
 // nb_* describe the neighbour list (CSR bucket ranges).  Returns the SITE
 // bytes touched (counted by thread 0).
+template <bool kAtomic = false>
 __device__ __forceinline__ unsigned long long update_body(const SiteArgs& a, int wr0, int wc0, int wh, int ww, int nb,
                                                           const int* nb_start, const int* nb_pref,
                                                           const int4* __restrict__ wins, const uint64_t* __restrict__ words,
@@ -247,7 +248,10 @@ __device__ __forceinline__ unsigned long long update_body(const SiteArgs& a, int
         if (threadIdx.x == 0) {
             int t = 0, tb = 0;
             for (int q = 0; q < nw; ++q) { t += s_red[q]; tb += s_cnt[q]; }
-            if (t) gain[i] -= t;
+            if (t) {
+                if (kAtomic) atomicSub(&gain[i], t);
+                else gain[i] -= t;
+            }
             bytes_all += 16ull * (unsigned long long)tb;
         }
         __syncthreads();
@@ -1626,6 +1630,286 @@ static void launch_gain_pass(txs_ctx* c, const SiteArgs& a, const SiteState* st,
     }
 }
 
+// ---- batched exact greedy (site_mode 0): every local maximum per round ------------------
+// The greedy sequence is serial only along chains of overlapping windows.  If
+// candidate X has the largest key (gain << 32 | ~index) among all candidates
+// whose windows overlap X's, no overlapping candidate can be picked before X
+// (their keys only fall and X's stays until something overlapping is picked),
+// so X WILL be the greedy pick with exactly its current gain once every
+// larger key elsewhere is used up -- and committing it now changes nothing
+// for the picks in between: they do not overlap X, and X's neighbours, whose
+// gains drop early, stay below X.  Successive greedy picks have strictly
+// falling keys, so the greedy ORDER is the committed picks sorted by key.
+// Per round: (1) k_batch_bmax: per neighbour bucket (side R) the best key, the
+// global best kappa and a gain histogram; (2) k_batch_decide: the stop test on
+// the known prefix (logged picks with key > kappa) and the rank threshold;
+// (3) k_batch_winners: every bucket champion that beats the champions of all
+// buckets within 2R of it (a superset of the overlapping candidates) is a
+// winner -- winners are pairwise non-overlapping; (4) k_batch_delta: each
+// winner's newly covered bits D = v_w & ~cum go to its own delta window, into
+// cum and its key into the log; (5) k_batch_update: gain_z -= popc(v_z & D_w)
+// for the winners' neighbours.  The run ends once the stop rule (decision D9)
+// fires inside the known prefix.  Winners whose key turns out to lie past the
+// stop were committed needlessly: the rank threshold (only candidates among
+// the `remaining` largest current gains may win, besides the global maximum)
+// keeps them to one histogram bin; the step list is cut at the stop and the
+// cum rebuilt from the kept picks.  c3: 4096 serial rounds -> tens of rounds.
+struct BatchState {
+    unsigned long long kappa_acc;   // running max of the uncommitted keys (k_batch_bmax)
+    unsigned long long kappa;       // the round's global max key
+    long long logn;                 // committed picks in the log
+    long long nvalid, svalid;       // logged picks with key > kappa: count, gain sum
+    int nx;                         // winners of the current round besides the global maximum (may exceed cap - 1)
+    int cap;                        // winner slots per round
+    int tau;                        // gain threshold of the winners other than the global maximum
+    int done, rounds;
+};
+constexpr int kHistBins = 4096;
+constexpr int kBatchUpdThreads = 128;
+constexpr int kBatchMaxRanges = 8;
+
+__device__ __forceinline__ int batch_nw(const BatchState* S) { return 1 + min(S->nx, S->cap - 1); }
+
+__global__ void __launch_bounds__(256) k_batch_bmax(SiteArgs a, BatchState* S, const int32_t* __restrict__ bstart,
+                                                    const int32_t* __restrict__ items, const int32_t* __restrict__ gain,
+                                                    unsigned long long* __restrict__ bmax, unsigned int* __restrict__ hist,
+                                                    int hshift) {
+    if (S->done) return;
+    __shared__ unsigned int s_hist[kHistBins];
+    const bool use_hist = a.max_sel > 0;
+    if (use_hist) {
+        for (int k = threadIdx.x; k < kHistBins; k += blockDim.x) s_hist[k] = 0u;
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31;
+    const int64_t nbk = (int64_t)a.nbx * a.nby, nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long cta_best = 0ull;
+    for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nbk; b += nwarps) {
+        const int s0 = bstart[b], s1 = bstart[b + 1];
+        unsigned long long best = 0ull;
+        for (int s = s0 + lane; s < s1; s += 32) {
+            const int i = items[s], g = gain[i];
+            if (g > 0) {
+                best = umax64(best, ((unsigned long long)(uint32_t)g << 32) | (0xffffffffull - (uint64_t)(uint32_t)i));
+                if (use_hist) atomicAdd(&s_hist[min(g >> hshift, kHistBins - 1)], 1u);
+            }
+        }
+        for (int o = 16; o; o >>= 1) best = umax64(best, __shfl_xor_sync(kFull, best, o));
+        if (lane == 0) bmax[b] = best;
+        cta_best = umax64(cta_best, best);
+    }
+    if (lane == 0 && cta_best) atomicMax(&S->kappa_acc, cta_best);
+    if (use_hist) {
+        __syncthreads();
+        for (int k = threadIdx.x; k < kHistBins; k += blockDim.x) {
+            const unsigned int h = s_hist[k];
+            if (h) atomicAdd(&hist[k], h);
+        }
+    }
+}
+
+// one CTA: the stop test on the known prefix, the next rank threshold, resets
+__global__ void __launch_bounds__(1024) k_batch_decide(SiteArgs a, BatchState* S, const unsigned long long* __restrict__ log,
+                                                       unsigned int* __restrict__ hist, int hshift) {
+    if (S->done) return;
+    __shared__ long long s_cnt[32], s_sum[32];
+    __shared__ unsigned int s_h[32];
+    __shared__ int s_tau;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long logn = S->logn + (S->rounds > 0 ? batch_nw(S) : 0);   // the previous round's winners are in the log now
+    const unsigned long long kappa = S->kappa_acc;
+    long long cnt = 0, sum = 0;
+    for (long long k = tid; k < logn; k += blockDim.x) {
+        const unsigned long long key = log[k];
+        if (key > kappa) { ++cnt; sum += (long long)(key >> 32); }
+    }
+    for (int o = 16; o; o >>= 1) { cnt += __shfl_xor_sync(kFull, cnt, o); sum += __shfl_xor_sync(kFull, sum, o); }
+    if (lane == 0) { s_cnt[warp] = cnt; s_sum[warp] = sum; }
+    // counts of the gain histogram from the top bin down: thread t owns bins [top, top + 3], top = 4 (1023 - t)
+    const int top = (kHistBins / 4 - 1 - tid) * 4;
+    const unsigned int h3 = hist[top + 3], h2 = hist[top + 2], h1 = hist[top + 1], h0 = hist[top];
+    const unsigned int mine = h0 + h1 + h2 + h3;
+    unsigned int incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int t = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_h[warp] = incl;
+    if (tid == 0) s_tau = 1;
+    __syncthreads();
+    cnt = 0; sum = 0;
+    for (int q = 0; q < 32; ++q) { cnt += s_cnt[q]; sum += s_sum[q]; }
+    unsigned int before = 0;   // candidates in higher bins than this thread's
+    for (int q = 0; q < warp; ++q) before += s_h[q];
+    before += incl - mine;
+    const long long remaining = a.max_sel > 0 ? a.max_sel - cnt : (long long)1 << 40;
+    // the bin where the count from the top reaches `remaining`: its lower edge is the threshold
+    if (remaining > 0 && (long long)before < remaining && (long long)before + mine >= remaining) {
+        long long c2 = before;
+        int bin = top;
+        const unsigned int hh[4] = {h3, h2, h1, h0};
+        for (int k = 0; k < 4; ++k) {
+            c2 += hh[k];
+            if (c2 >= remaining) { bin = top + 3 - k; break; }
+        }
+        s_tau = max(1, bin << hshift);
+    }
+    __syncthreads();
+    for (int k = tid; k < kHistBins; k += blockDim.x) hist[k] = 0u;
+    if (tid == 0) {
+        const long long g = (long long)(kappa >> 32);
+        const bool stop = (a.max_sel > 0 && cnt >= a.max_sel) || (double)sum / a.total >= a.target || g <= 0;
+        S->kappa = kappa;
+        S->kappa_acc = 0ull;
+        S->logn = logn;
+        S->nvalid = cnt;
+        S->svalid = sum;
+        S->nx = 0;
+        S->tau = s_tau;
+        S->rounds += 1;
+        if (stop) S->done = 1;
+    }
+}
+
+// slot 0 is the global maximum's (always a winner: progress every round)
+__global__ void k_batch_winners(SiteArgs a, BatchState* S, const unsigned long long* __restrict__ bmax,
+                                const int32_t* __restrict__ crow, const int32_t* __restrict__ ccol,
+                                int32_t* __restrict__ wl, unsigned long long* __restrict__ wkey) {
+    if (S->done) return;
+    const int64_t nbk = (int64_t)a.nbx * a.nby;
+    const unsigned long long kappa = S->kappa;
+    const int tau = S->tau, cap = S->cap;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nbk; b += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long key = bmax[b];
+        if (!key) continue;
+        if ((int)(key >> 32) < tau && key != kappa) continue;
+        const int i = (int)(0xffffffffull - (key & 0xffffffffull));
+        const int r = crow[i], c = ccol[i];
+        const int by0 = max(0, (r - 2 * a.R) / a.bsize), by1 = min(a.nby - 1, (r + 2 * a.R) / a.bsize);
+        const int bx0 = max(0, (c - 2 * a.R) / a.bsize), bx1 = min(a.nbx - 1, (c + 2 * a.R) / a.bsize);
+        bool top = true;
+        for (int by = by0; by <= by1 && top; ++by)
+            for (int bx = bx0; bx <= bx1; ++bx)
+                if (bmax[(int64_t)by * a.nbx + bx] > key) { top = false; break; }
+        if (!top) continue;
+        int slot = 0;
+        if (key != kappa) {
+            slot = 1 + atomicAdd(&S->nx, 1);
+            if (slot >= cap) continue;   // no slot this round: it wins again next round
+        }
+        wl[slot] = i;
+        wkey[slot] = key;
+    }
+}
+
+// one CTA per winner: D = v_w & ~cum into the winner's delta window (+ per-row spans of its
+// non-zero words), cum |= D, key into the log.  Winners' windows are disjoint, but two may
+// share a cum word at their edges: the bits each one tests and sets are its own.
+__global__ void __launch_bounds__(256) k_batch_delta(SiteArgs a, const BatchState* S, const int32_t* __restrict__ wl,
+                                                     const unsigned long long* __restrict__ wkey,
+                                                     const int4* __restrict__ wins, const uint64_t* __restrict__ words,
+                                                     uint64_t* cum, uint64_t* __restrict__ dwin, int2* __restrict__ dspan,
+                                                     unsigned long long* __restrict__ log) {
+    if (S->done) return;
+    const int nw = batch_nw(S), side = 2 * a.R + 1;
+    for (int w = blockIdx.x; w < nw; w += gridDim.x) {
+        const int X = wl[w];
+        const int4 wx = wins[X];
+        const uint64_t* v = words + (int64_t)X * a.stride;
+        uint64_t* dw = dwin + (int64_t)w * side * a.dpitch;
+        int2* ds = dspan + (int64_t)w * side;
+        const int nwr = win_nwr(wx.y, wx.w), wlo = wx.y >> 6;
+        for (int y = threadIdx.x; y < side; y += blockDim.x) ds[y] = make_int2(0x7fffffff, -1);
+        __syncthreads();
+        for (int t = threadIdx.x; t < wx.z * nwr; t += blockDim.x) {
+            const int y = t / nwr, b = t - y * nwr;
+            const int64_t o = (int64_t)(wx.x + y) * a.wpr + wlo + b;
+            const uint64_t d = v[t] & ~__ldcg(cum + o);
+            dw[(int64_t)y * a.dpitch + b] = d;
+            if (d) {
+                atomicOr((unsigned long long*)(cum + o), (unsigned long long)d);
+                atomicMin(&ds[y].x, b);
+                atomicMax(&ds[y].y, b);
+            }
+        }
+        if (threadIdx.x == 0) log[S->logn + w] = wkey[w];
+        __syncthreads();
+    }
+}
+
+// virtual CTA (winner w, slot x of XS): the neighbours f = x, x + XS, ... of winner w.  XS shrinks as
+// the winners grow so that the grid holds about one virtual CTA per real one.
+__global__ void __launch_bounds__(kBatchUpdThreads) k_batch_update(SiteArgs a, const BatchState* S,
+                                                                    const int32_t* __restrict__ wl,
+                                                                    const int32_t* __restrict__ crow,
+                                                                    const int32_t* __restrict__ ccol,
+                                                                    const int32_t* __restrict__ bstart,
+                                                                    const int32_t* __restrict__ items,
+                                                                    const int4* __restrict__ wins,
+                                                                    const uint64_t* __restrict__ words,
+                                                                    const uint64_t* __restrict__ dwin,
+                                                                    const int2* __restrict__ dspan,
+                                                                    int32_t* __restrict__ gain,
+                                                                    unsigned long long* __restrict__ counters) {
+    if (S->done) return;
+    __shared__ int s_red[kBatchUpdThreads / 32], s_cnt[kBatchUpdThreads / 32], s_start[kBatchMaxRanges], s_len[kBatchMaxRanges],
+        s_pref[kBatchMaxRanges + 1];
+    const int nw = batch_nw(S), side = 2 * a.R + 1;
+    const int XS = max(1, min(64, (int)gridDim.x / nw));
+    unsigned long long bytes = 0;
+    for (int64_t vf = blockIdx.x; vf < (int64_t)nw * XS; vf += gridDim.x) {
+        const int w = (int)(vf / XS), x = (int)(vf - (int64_t)w * XS);
+        const int X = wl[w];
+        const int4 wx = wins[X];
+        const int r = crow[X], c = ccol[X];
+        const int by0 = max(0, (r - 2 * a.R) / a.bsize), by1 = min(a.nby - 1, (r + 2 * a.R) / a.bsize);
+        const int bx0 = max(0, (c - 2 * a.R) / a.bsize), bx1 = min(a.nbx - 1, (c + 2 * a.R) / a.bsize);
+        const int nb = min(kBatchMaxRanges, by1 - by0 + 1);
+        __syncthreads();
+        if (threadIdx.x < nb) {
+            const int s0 = bstart[(int64_t)(by0 + threadIdx.x) * a.nbx + bx0], s1 = bstart[(int64_t)(by0 + threadIdx.x) * a.nbx + bx1 + 1];
+            s_start[threadIdx.x] = s0;
+            s_len[threadIdx.x] = s1 - s0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int pref = 0;
+            for (int k = 0; k < nb; ++k) { s_pref[k] = pref; pref += s_len[k]; }
+            s_pref[nb] = pref;
+        }
+        __syncthreads();
+        bytes += update_body<true>(a, wx.x, wx.y, wx.z, wx.w, nb, s_start, s_pref, wins, words,
+                                   dwin + (int64_t)w * side * a.dpitch, dspan + (int64_t)w * side, items, gain, x, XS, s_red, s_cnt);
+    }
+    if (threadIdx.x == 0 && bytes) atomicAdd(counters + kSiteBytes, bytes);
+}
+
+// cum |= v_w for the first `count` listed candidates (the rebuild after an over-commit)
+__global__ void k_batch_rebuild(SiteArgs a, int64_t count, const int32_t* __restrict__ wl, const int4* __restrict__ wins,
+                                const uint64_t* __restrict__ words, uint64_t* __restrict__ cum) {
+    for (int64_t w = blockIdx.x; w < count; w += gridDim.x) {
+        const int X = wl[w];
+        const int4 wx = wins[X];
+        const uint64_t* v = words + (int64_t)X * a.stride;
+        const int nwr = win_nwr(wx.y, wx.w), wlo = wx.y >> 6;
+        for (int t = threadIdx.x; t < wx.z * nwr; t += blockDim.x) {
+            const uint64_t x = v[t];
+            const int y = t / nwr, b = t - y * nwr;
+            if (x) atomicOr((unsigned long long*)(cum + (int64_t)(wx.x + y) * a.wpr + wlo + b), (unsigned long long)x);
+        }
+    }
+}
+
+__global__ void k_batch_emit(int64_t count, const unsigned long long* __restrict__ sorted, const int32_t* __restrict__ crow,
+                             const int32_t* __restrict__ ccol, txs_step* __restrict__ steps, int32_t* __restrict__ idx_out) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count; k += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long key = sorted[k];
+        const int i = (int)(0xffffffffull - (key & 0xffffffffull));
+        steps[k] = txs_step{(int64_t)i, crow[i], ccol[i], (int64_t)(key >> 32), 0.0};
+        idx_out[k] = i;
+    }
+}
+
 // cum over the held region rows [r0, r1) (whole grid unless sharded) + delta list
 txs_status alloc_bitmaps(txs_ctx* c, int64_t r0, int64_t r1) {
     c->wpr = (c->ncols + 63) / 64;
@@ -1662,6 +1946,131 @@ txs_status init_gains_buckets(txs_ctx* c, const SiteArgs& a, void* d_scan_tmp, s
     return TXS_OK;
 }
 
+// Batched exact greedy (kernels above): graphs of kBatchRoundsPerGraph rounds until the device
+// stop flag, then the log sorted by key is the greedy order; decision D9's stop rules are
+// replayed over it on the host (exactly the serial loop's tests, pick by pick).
+constexpr int kBatchRoundsPerGraph = 8;
+
+static txs_status run_site_batched(txs_ctx* c, const txs_params& p, const SiteArgs& a, txs_step* d_steps,
+                                   std::vector<txs_step>& out, int32_t* stop) {
+    const int64_t n = a.n, nbk = (int64_t)a.nbx * a.nby;
+    const int sms = c->num_sms, side = 2 * a.R + 1;
+    // winner slots per round: one per bucket at most; the delta windows are capped at 1 GB
+    const int64_t dwin_words = (int64_t)side * a.dpitch;
+    int64_t cap = std::min<int64_t>(nbk, std::max<int64_t>(64, ((int64_t)1 << 30) / (8 * dwin_words)));
+    cap = std::max<int64_t>(1, std::min<int64_t>(cap, n));
+    if (const char* e = getenv("TXS_SITE_BATCH_CAP")) cap = std::max<int64_t>(1, std::min<int64_t>(cap, atoll(e)));
+    size_t sort_bytes = 0;
+    cub::DeviceRadixSort::SortKeysDescending(nullptr, sort_bytes, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                             (int)n, 0, 64, c->stream);
+    auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+    const size_t o_bmax = 0, o_hist = o_bmax + al(8 * (size_t)nbk), o_wl = o_hist + al(4 * kHistBins),
+                 o_wkey = o_wl + al(4 * (size_t)cap), o_log = o_wkey + al(8 * (size_t)cap), o_sorted = o_log + al(8 * (size_t)n),
+                 o_idx = o_sorted + al(8 * (size_t)n), o_sort = o_idx + al(4 * (size_t)n), o_dspan = o_sort + al(sort_bytes),
+                 o_dwin = o_dspan + al(sizeof(int2) * (size_t)(cap * side)), total = o_dwin + al(8 * (size_t)(cap * dwin_words));
+    if (ensure(c, "site", &c->d_batch, &c->batch_cap, total) != TXS_OK) return TXS_ERR_OUT_OF_MEMORY;
+    char* base = (char*)c->d_batch;
+    unsigned long long* bmax = (unsigned long long*)(base + o_bmax);
+    unsigned int* hist = (unsigned int*)(base + o_hist);
+    int32_t* wl = (int32_t*)(base + o_wl);
+    unsigned long long* wkey = (unsigned long long*)(base + o_wkey);
+    unsigned long long* log = (unsigned long long*)(base + o_log);
+    unsigned long long* sorted = (unsigned long long*)(base + o_sorted);
+    int32_t* idx = (int32_t*)(base + o_idx);
+    int2* dspan = (int2*)(base + o_dspan);
+    uint64_t* dwin = (uint64_t*)(base + o_dwin);
+    static_assert(sizeof(BatchState) <= sizeof(SiteState), "BatchState lives in the SiteState buffers");
+    BatchState* S = (BatchState*)c->d_state;
+    BatchState* hS = (BatchState*)c->h_state;
+    std::memset(hS, 0, sizeof(BatchState));
+    hS->cap = (int)cap;
+    TXS_CUDA(c, "site", cudaMemcpyAsync(S, hS, sizeof(BatchState), cudaMemcpyHostToDevice, c->stream));
+    TXS_CUDA(c, "site", cudaMemsetAsync(hist, 0, 4 * kHistBins, c->stream));
+    int hshift = 0;
+    while ((((int64_t)side * side) >> hshift) >= kHistBins) ++hshift;
+    const int bm_blocks = blocks_for(nbk * 32, 256, sms * 4);
+    const int wn_blocks = blocks_for(nbk, 128, sms * 4);
+    const int dl_blocks = (int)std::min<int64_t>(cap, sms * 8);
+    int up_blocks = sms * 8;
+    if (const char* e = getenv("TXS_BATCH_UPD_MULT")) up_blocks = sms * std::max(1, atoi(e));
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    TXS_CUDA(c, "site", cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    for (int r = 0; r < kBatchRoundsPerGraph; ++r) {
+        k_batch_bmax<<<bm_blocks, 256, 0, c->stream>>>(a, S, c->d_bucket_start, c->d_bucket_items, c->d_gain, bmax, hist, hshift);
+        k_batch_decide<<<1, 1024, 0, c->stream>>>(a, S, log, hist, hshift);
+        k_batch_winners<<<wn_blocks, 128, 0, c->stream>>>(a, S, bmax, c->d_crow, c->d_ccol, wl, wkey);
+        k_batch_delta<<<dl_blocks, 256, 0, c->stream>>>(a, S, wl, wkey, c->d_win, c->d_words, c->d_cum, dwin, dspan, log);
+        k_batch_update<<<up_blocks, kBatchUpdThreads, 0, c->stream>>>(a, S, wl, c->d_crow, c->d_ccol, c->d_bucket_start,
+                                                                      c->d_bucket_items, c->d_win, c->d_words, dwin, dspan,
+                                                                      c->d_gain, c->d_counters);
+    }
+    cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
+    if (ce != cudaSuccess) return cuda_fail(c, "site", ce);
+    ce = cudaGraphInstantiate(&exec, graph, 0);
+    if (ce != cudaSuccess) { cudaGraphDestroy(graph); return cuda_fail(c, "site", ce); }
+    txs_status st = TXS_OK;
+    int64_t graphs = 0;
+    for (;;) {
+        cudaEventRecord(c->ev_r0, c->stream);
+        ce = cudaGraphLaunch(exec, c->stream);
+        if (ce != cudaSuccess) { st = cuda_fail(c, "site", ce); break; }
+        cudaEventRecord(c->ev_r1, c->stream);
+        ++graphs;
+        ce = cudaMemcpyAsync(hS, S, sizeof(BatchState), cudaMemcpyDeviceToHost, c->stream);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(c->stream);
+        if (ce == cudaSuccess) add_round_time(c);
+        if (ce != cudaSuccess) { st = cuda_fail(c, "site", ce); break; }
+        if (hS->done) break;
+        if (graphs * kBatchRoundsPerGraph > n + 2 * kBatchRoundsPerGraph) { st = fail(c, TXS_ERR_STATE, "site", "batched loop did not terminate"); break; }
+    }
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    if (st != TXS_OK) return st;
+    c->launches += graphs * kBatchRoundsPerGraph * 5;
+    c->stats.site_launches += graphs * kBatchRoundsPerGraph * 5;
+    const int64_t logn = hS->logn, rounds = hS->rounds;
+    const unsigned long long kappa = hS->kappa;
+    if (getenv("TXS_SITE_BATCH_VERBOSE"))
+        fprintf(stderr, "[txs] batched SITE: %lld rounds, %lld picks logged, %lld in the known prefix\n", (long long)rounds,
+                (long long)logn, (long long)hS->nvalid);
+    out.clear();
+    *stop = (kappa >> 32) == 0 ? (logn >= n ? TXS_STOP_EXHAUSTED : TXS_STOP_ZERO_GAIN) : TXS_STOP_ZERO_GAIN;
+    int64_t kept = 0;
+    if (logn > 0) {
+        TXS_CUDA(c, "site", cub::DeviceRadixSort::SortKeysDescending(base + o_sort, sort_bytes, (const unsigned long long*)log, sorted,
+                                                                     (int)logn, 0, 64, c->stream));
+        k_batch_emit<<<blocks_for(logn, 256, sms * 4), 256, 0, c->stream>>>(logn, sorted, c->d_crow, c->d_ccol, d_steps, idx);
+        TXS_LAUNCHED(c, "site");
+        out.resize((size_t)logn);
+        TXS_CUDA(c, "site", cudaMemcpyAsync(out.data(), d_steps, sizeof(txs_step) * logn, cudaMemcpyDeviceToHost, c->stream));
+        TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+        // D9 in the serial loop's order: a pick is made while a positive gain is left; after
+        // it, target coverage is tested before the observer cap
+        long long covered = 0;
+        bool stopped = false;
+        for (int64_t k = 0; k < logn; ++k) {
+            covered += out[k].gain;
+            const double cov = (double)covered / a.total;
+            out[k].coverage = cov;
+            kept = k + 1;
+            if (cov >= a.target) { *stop = TXS_STOP_TARGET_REACHED; stopped = true; break; }
+            if (a.max_sel > 0 && k + 1 >= a.max_sel) { *stop = TXS_STOP_MAX_SELECTED; stopped = true; break; }
+        }
+        if (!stopped && (kappa >> 32) != 0) return fail(c, TXS_ERR_STATE, "site", "batched loop ended before a stop rule");
+        out.resize((size_t)kept);
+        if (kept < logn) {   // picks past the stop were committed: the cum is the kept picks' union
+            const size_t bm = sizeof(uint64_t) * (size_t)((c->cum_r1 - c->cum_r0) * c->wpr + 1);
+            TXS_CUDA(c, "site", cudaMemsetAsync(c->d_cum, 0, bm, c->stream));
+            k_batch_rebuild<<<(int)std::min<int64_t>(kept, sms * 8), 256, 0, c->stream>>>(a, kept, idx, c->d_win, c->d_words, c->d_cum);
+            TXS_LAUNCHED(c, "site");
+            TXS_CUDA(c, "site", cudaStreamSynchronize(c->stream));
+        }
+    }
+    c->stats.site_iterations += kept;
+    return TXS_OK;
+}
+
 }  // namespace
 
 txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out, int32_t* stop) {
@@ -1691,6 +2100,20 @@ txs_status run_site(txs_ctx* c, const txs_params& p, std::vector<txs_step>& out,
     const int sms = c->num_sms;
     if (init_gains_buckets(c, a, d_scan_tmp, scan_bytes) != TXS_OK) return TXS_ERR_CUDA;
     const LoopPtrs lp0{c->d_crow, c->d_ccol, c->d_win, c->d_bucket_start, d_steps};
+    // Batched exact greedy (every local maximum per round) when the grid holds enough
+    // independent (4R+1)^2 neighbourhoods for a round to commit several picks (measured:
+    // c3 1670 regions 21.9 -> 1.9 ms, c5 268 regions 79.6 -> 46.4, c2 26 regions 6.8 -> 3.8;
+    // c1's 6 regions 0.41 -> 0.82 ms, so small grids keep the serial loop).  TXS_SITE_BATCH=0|1
+    // forces the choice; the serial loops' A/B knobs imply 0.
+    {
+        const double regions = (double)c->nrows * (double)c->ncols / ((4.0 * a.R + 1.0) * (4.0 * a.R + 1.0));
+        bool batch = regions >= 16.0;
+        for (const char* k : {"TXS_SITE_CLUSTER", "TXS_SITE_PERSISTENT", "TXS_SITE_GRAPH", "TXS_SITE_LOOP3", "TXS_SITE_LOOP_CTAS",
+                              "TXS_SITE_PROFILE"})
+            if (getenv(k)) batch = false;
+        if (const char* e = getenv("TXS_SITE_BATCH")) batch = atoi(e) != 0;
+        if (batch && p.site_mode == 0 && n > 0) return run_site_batched(c, p, a, d_steps, out, stop);
+    }
     // Persistent loop vs graph of per-round kernels (measured, profiles/): the
     // persistent kernel wins while a round touches few neighbours (C1 0.72 vs
     // 1.28 ms, C3 47 vs 62 ms); with thousands of neighbours per round (C5) the

@@ -401,6 +401,59 @@ def test_site_cluster_loop(engine, monkeypatch, cs, case):
     assert engine.stats()["site_launches"] == before + 1   # one persistent kernel either way
 
 
+@pytest.mark.parametrize("case", ["dense", "maxsel", "target", "flat-ties", "cap1", "cap3", "wide", "tiny", "single", "exhaust"])
+def test_site_batched_greedy(engine, monkeypatch, case):
+    """The batched exact greedy (site.cu run_site_batched: every local maximum of
+    the key per round, the greedy order recovered by sorting the committed picks)
+    against the oracle's serial greedy: to zero gain with a duplicate and the
+    grid corners; a max_selected stop and a target stop (picks committed past
+    the stop are cut and the cum rebuilt); flat terrain (every gain ties, lowest
+    index wins); one and three winner slots per round; a grid wide enough that
+    the batched form is the default; fewer candidates than buckets; one
+    candidate; every candidate picked (exhausted)."""
+    T = _T()
+    nr, nc, roi, n, target, max_sel, rough = 300, 420, 25, 700, 1.0, 0, 0.6
+    if case == "maxsel":
+        target, max_sel = 1.0, 60
+    elif case == "target":
+        target = 0.55
+    elif case == "flat-ties":
+        nr, nc, roi, n = 200, 260, 10, 1500
+    elif case == "wide":
+        nr, nc, roi, n, max_sel = 1100, 1300, 10, 6000, 900
+    elif case == "tiny":
+        n = 5
+    elif case == "single":
+        n = 1
+    elif case == "exhaust":
+        nr, nc, roi, n = 400, 400, 6, 40
+    z = np.zeros((nr, nc), np.int16) if case == "flat-ties" else O.generate_fractal(nr, nc, rough, 19, 0, 3500)
+    rng = np.random.default_rng(101)
+    rows, cols = rng.integers(0, nr, n).astype(np.int32), rng.integers(0, nc, n).astype(np.int32)
+    if case == "exhaust":   # pairwise disjoint windows: every candidate keeps its whole gain and is picked
+        k = np.arange(n)
+        rows, cols = (20 + 40 * (k // 8)).astype(np.int32), (20 + 40 * (k % 8)).astype(np.int32)
+    elif n > 5:
+        rows[:5], cols[:5] = [0, nr - 1, 0, nr - 1, 0], [0, nc - 1, nc - 1, 0, 0]
+        rows[7], cols[7] = rows[6], cols[6]
+    engine.set_terrain(z)
+    engine.set_candidates(rows, cols)
+    engine.compute_all_viewsheds(T.make_params(roi, 10, 10))
+    if case != "wide":
+        monkeypatch.setenv("TXS_SITE_BATCH", "1")
+    if case.startswith("cap"):
+        monkeypatch.setenv("TXS_SITE_BATCH_CAP", case[3:])
+    before = engine.stats()["site_launches"]
+    g = _site_compare(engine, roi, rows, cols, nr, nc, target, max_sel, 0)
+    assert (engine.stats()["site_launches"] - before) % 40 == 0   # graphs of 8 rounds x 5 kernels: the batched form ran
+    if case == "exhaust":
+        assert g["stop"] == "exhausted" and len(g["index"]) == n
+    if case == "maxsel":
+        assert g["stop"] == "max-selected" and len(g["index"]) == 60
+    if case == "target":
+        assert g["stop"] == "target-reached"
+
+
 def test_site_edge_cases(engine):
     T = _T()
     z = O.generate_fractal(64, 64, 0.5, 2, 0, 4000)
