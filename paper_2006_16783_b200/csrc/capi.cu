@@ -48,7 +48,8 @@ txs_status check_params(txs_ctx* ctx, const char* stage, const txs_params* p, bo
 
 txs_status wait_terrain_rows(txs_ctx* c, int64_t row_end) {
     if (!c->up_pending || row_end <= 0 || c->up_ev.empty()) return TXS_OK;
-    const size_t k = (size_t)std::min<int64_t>((int64_t)c->up_ev.size() - 1, (row_end - 1) / c->up_chunk);
+    size_t k = 0;
+    while (k + 1 < c->up_end.size() && c->up_end[k] < row_end) ++k;
     TXS_CUDA(c, "read", cudaStreamWaitEvent(c->stream, c->up_ev[k], 0));
     return TXS_OK;
 }
@@ -814,14 +815,39 @@ txs_status txs_run_pipeline_host(txs_ctx* c, const int16_t* z, int64_t nrows, in
     st = set_dims(c, nrows, ncols);
     if (st != TXS_OK) return st;
     if (!c->copy_stream) TXS_CUDA(c, "read", cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-    // ~16 chunks of whole 64-row multiples, on the copy stream, one event each;
-    // below 128 MB one chunk (the upload is short, and VIX bands over a small
-    // grid would each fill only part of the GPU: c1 e2e 4.1 -> 10.9 ms banded)
+    // Chunks of whole 64-row multiples on the copy stream, one event each.  Below 128 MB one
+    // chunk (the upload is short, and VIX bands over a small grid would each fill only part
+    // of the GPU: c1 e2e 4.1 -> 10.9 ms banded).  When a row's walks cost well over its
+    // upload (S * roi >= 500: c3 / c4's rows take ~4x their PCIe time) the chunks grow
+    // geometrically -- ~16 MB, the same again, then each as large as everything before it,
+    // up to a quarter of the grid -- so the first VIX band starts after ~32 MB instead of
+    // two sixteenths of the terrain (c4: 1 ms instead of 10.8) and the later bands are few
+    // and long; otherwise 16 uniform chunks (a band must never wait for half the upload).
     const bool small = (double)nrows * (double)ncols * sizeof(int16_t) < (double)(128 << 20);
-    int64_t ch = small ? std::max<int64_t>(1, nrows) : std::max<int64_t>(64, ((nrows + 15) / 16 + 63) / 64 * 64);
-    if (const char* e = getenv("TXS_UPLOAD_CHUNK_ROWS"))   // tests / A/B (whole 64-row multiples)
-        ch = std::max<int64_t>(64, (atoll(e) + 63) / 64 * 64);
-    const size_t nch = (size_t)((nrows + ch - 1) / ch);
+    bool grow = !small && (int64_t)p->samples_per_point * p->roi >= 500;
+    if (const char* e = getenv("TXS_UPLOAD_BANDS")) grow = e[0] == 'g';   // grow | uniform (A/B, tests)
+    auto up64 = [](int64_t x) { return std::max<int64_t>(64, (x + 63) / 64 * 64); };
+    int64_t ch = small ? std::max<int64_t>(1, nrows) : up64((nrows + 15) / 16);
+    if (const char* e = getenv("TXS_UPLOAD_CHUNK_ROWS")) {   // tests / A/B (uniform, whole 64-row multiples)
+        ch = up64(atoll(e));
+        grow = false;
+    }
+    c->up_end.clear();
+    if (grow) {
+        int64_t first = up64(std::max<int64_t>(((int64_t)16 << 20) / (int64_t)(ncols * sizeof(int16_t)), p->roi + 128));
+        if (const char* e = getenv("TXS_UPLOAD_FIRST_ROWS")) first = up64(atoll(e));   // tests
+        const int64_t cap_rows = up64(nrows / 4);
+        for (int64_t done = 0; done < nrows;) {
+            done = std::min(nrows, done + std::min(cap_rows, std::max(first, done)));
+            c->up_end.push_back(done);
+        }
+    } else {
+        for (int64_t done = 0; done < nrows;) {
+            done = std::min(nrows, done + ch);
+            c->up_end.push_back(done);
+        }
+    }
+    const size_t nch = c->up_end.size();
     while (c->up_ev.size() < nch) {
         cudaEvent_t e = nullptr;
         TXS_CUDA(c, "read", cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -832,14 +858,13 @@ txs_status txs_run_pipeline_host(txs_ctx* c, const int16_t* z, int64_t nrows, in
     TXS_CUDA(c, "read", cudaEventRecord(c->ev_r0, c->stream));
     TXS_CUDA(c, "read", cudaStreamWaitEvent(c->copy_stream, c->ev_r0, 0));
     for (size_t k = 0; k < nch; ++k) {
-        const int64_t r0 = (int64_t)k * ch, r1 = std::min(nrows, r0 + ch);
+        const int64_t r0 = k ? c->up_end[k - 1] : 0, r1 = c->up_end[k];
         TXS_CUDA(c, "read", cudaMemcpyAsync(c->d_z + r0 * ncols, z + r0 * ncols, sizeof(int16_t) * (r1 - r0) * ncols,
                                             cudaMemcpyHostToDevice, c->copy_stream));
         TXS_CUDA(c, "read", cudaEventRecord(c->up_ev[k], c->copy_stream));
     }
     std::vector<cudaEvent_t> evs(c->up_ev.begin(), c->up_ev.begin() + (int64_t)nch);
     std::swap(c->up_ev, evs);   // exactly this upload's chunks while it is pending
-    c->up_chunk = ch;
     c->up_pending = true;
     st = txs_estimate_vix(c, p, nullptr);   // VIX bands start behind the arriving rows
     c->up_pending = false;

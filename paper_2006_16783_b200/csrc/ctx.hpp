@@ -173,12 +173,12 @@ struct txs_ctx {
     bool t8_valid = false;
     bool site_valid = false;
 
-    // txs_run_pipeline_host: terrain rows arriving on copy_stream in chunks of
-    // up_chunk rows (event up_ev[k] after chunk k); VIX starts on the first
+    // txs_run_pipeline_host: terrain rows arriving on copy_stream in chunks
+    // (event up_ev[k] after chunk k, which ends at row up_end[k]); VIX starts on the first
     // row bands while the rest is still in flight
     cudaStream_t copy_stream = nullptr;
     std::vector<cudaEvent_t> up_ev;
-    int64_t up_chunk = 0;
+    std::vector<int64_t> up_end;   // chunk k holds rows [up_end[k-1], up_end[k])
     bool up_pending = false;
 
     // stats

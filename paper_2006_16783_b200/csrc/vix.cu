@@ -1510,25 +1510,20 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         TXS_CUDA(c, "vix", cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kq, kVixThreads, qsm));
         int64_t grid_q = std::min<int64_t>(tiles_q, (int64_t)std::max(1, per_sm) * c->num_sms);
         if (const char* e = getenv("TXS_VIX_GRID")) grid_q = std::min<int64_t>(tiles_q, std::max(1, atoi(e)));
-        if (!banded) {
-            TXS_CUDA(c, "vix", cudaMemsetAsync(c->d_counters + kVixNext, 0, sizeof(unsigned long long), c->stream));
-            // the crossing statistic depends only on this key: counted once, then cached
-            const uint64_t key = mix_seed(mix_seed(p.seed, (uint64_t)p.roi * 4099 + (uint64_t)p.samples_per_point,
-                                                   (uint64_t)c->nrows * 1000003 + (uint64_t)c->ncols),
-                                          (uint64_t)c->band_r0 * 1000003 + (uint64_t)c->band_r1,
-                                          (uint64_t)c->z_off * 1000003 + (uint64_t)c->z_rows);
-            const bool lanes = lanes_kernel;
-            const bool cached = lanes && c->vix_cross_valid && c->vix_cross_key == key;
-            aq.count_cross = cached ? 0 : 1;
-            unsigned long long before = 0;
-            if (lanes && !cached)
-                TXS_CUDA(c, "vix", cudaMemcpyAsync(&before, c->d_counters + kVixCrossFull, sizeof(before),
-                                                   cudaMemcpyDeviceToHost, c->stream));
-            cudaEventRecord(c->ev_k0, c->stream);
-            kq<<<(unsigned)grid_q, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols,
-                                                                    c->d_vix - c->band_r0 * c->ncols, aq, c->d_gcd, smap,
-                                                                    c->d_counters);
-            cudaEventRecord(c->ev_k1, c->stream);
+        // the crossing statistic depends only on this key: counted once (over one launch or
+        // the upload bands' launches), then cached
+        const uint64_t key = mix_seed(mix_seed(p.seed, (uint64_t)p.roi * 4099 + (uint64_t)p.samples_per_point,
+                                               (uint64_t)c->nrows * 1000003 + (uint64_t)c->ncols),
+                                      (uint64_t)c->band_r0 * 1000003 + (uint64_t)c->band_r1,
+                                      (uint64_t)c->z_off * 1000003 + (uint64_t)c->z_rows);
+        const bool lanes = lanes_kernel;
+        const bool cached = lanes && c->vix_cross_valid && c->vix_cross_key == key;
+        aq.count_cross = cached ? 0 : 1;
+        unsigned long long before = 0;
+        if (lanes && !cached)
+            TXS_CUDA(c, "vix", cudaMemcpyAsync(&before, c->d_counters + kVixCrossFull, sizeof(before),
+                                               cudaMemcpyDeviceToHost, c->stream));
+        auto finish_cross = [&]() -> txs_status {
             if (cached) {
                 k_add_counter<<<1, 1, 0, c->stream>>>(c->d_counters + kVixCrossFull, c->vix_cross_count);
                 TXS_LAUNCHED(c, "vix");
@@ -1541,18 +1536,30 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
                 c->vix_cross_key = key;
                 c->vix_cross_valid = true;
             }
+            return TXS_OK;
+        };
+        if (!banded) {
+            TXS_CUDA(c, "vix", cudaMemsetAsync(c->d_counters + kVixNext, 0, sizeof(unsigned long long), c->stream));
+            cudaEventRecord(c->ev_k0, c->stream);
+            kq<<<(unsigned)grid_q, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols,
+                                                                    c->d_vix - c->band_r0 * c->ncols, aq, c->d_gcd, smap,
+                                                                    c->d_counters);
+            cudaEventRecord(c->ev_k1, c->stream);
+            if ((st = finish_cross()) != TXS_OK) return st;
         } else {
             // band b = upload chunk b's rows; it needs the rows up to r1 + R + 4G (its
-            // walks, and the map corners of their groups), so it waits for that
-            // chunk; block-max rows and map corner rows are built once each, as
+            // walks, and the map corners of their groups), so it waits for the chunk
+            // holding them; block-max rows and map corner rows are built once each, as
             // soon as their terrain rows are in
-            const int64_t H = c->z_rows, CH = c->up_chunk;
+            const int64_t H = c->z_rows;
             int pr_done = 0, q_done = 0;
             cudaEventRecord(c->ev_k0, c->stream);
-            for (int64_t r0 = 0; r0 < H; r0 += CH) {
-                const int64_t r1 = std::min(H, r0 + CH);
+            for (size_t b = 0; b < c->up_end.size(); ++b) {
+                const int64_t r0 = b ? c->up_end[b - 1] : 0, r1 = c->up_end[b];
                 const int64_t need = std::min(H, r1 + p.roi + 4 * (int64_t)G);
-                const int64_t loaded = std::min(H, ((need - 1) / CH + 1) * CH);
+                int64_t loaded = H;
+                for (size_t k = b; k < c->up_end.size(); ++k)
+                    if (c->up_end[k] >= need) { loaded = c->up_end[k]; break; }
                 if ((st = wait_terrain_rows(c, need)) != TXS_OK) return st;
                 const int pr_new = loaded >= H ? Hb + 2 : (int)(loaded / G) + 1;
                 if (pr_new > pr_done) {
@@ -1581,6 +1588,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
                 TXS_LAUNCHED(c, "vix");
             }
             cudaEventRecord(c->ev_k1, c->stream);
+            if ((st = finish_cross()) != TXS_OK) return st;
         }
         st = TXS_OK;
     } else {

@@ -20,10 +20,13 @@ def _ref(e, z, p):
                                                     ((2300, 700), 100, 100, 4, 6, 300),      # banded, water rows
                                                     ((900, 800), 30, 40, 3, 8, 0),           # many small bands
                                                     ((1100, 900), 160, 128, 4, 5, 0)])       # quad planes: no bands
-@pytest.mark.parametrize("chunk", [None, "64"])   # default (one chunk below 128 MB) / forced bands
+@pytest.mark.parametrize("chunk", [None, "64", "grow"])   # default (one chunk below 128 MB) / forced bands / growing chunks
 def test_host_pipeline_matches(engine, monkeypatch, shape, roi, bw, k, S, water, chunk):
     import torch
-    if chunk:
+    if chunk == "grow":   # chunks of 64, 64, 128, 256 ... rows, at most a quarter of the grid each
+        monkeypatch.setenv("TXS_UPLOAD_BANDS", "grow")
+        monkeypatch.setenv("TXS_UPLOAD_FIRST_ROWS", "64")
+    elif chunk:
         monkeypatch.setenv("TXS_UPLOAD_CHUNK_ROWS", chunk)
     import paper_2006_16783_b200 as T
     nr, nc = shape
