@@ -73,6 +73,7 @@ enum Counter : int {
     kVixTies,   // VIX segments visible with an exact grazing tie (fp64 tie list entries)
     kVsTies,    // VIEWSHED (observer, ray) pairs with a grazing tie at a cell (fp64 tie list)
     kVixTiesFlipped, kVsTiesFlipped,   // decisions the fp64 re-test changed
+    kVixSelFail, kVixSelTotal, kVixSel,   // k_vix_sample: sampled segments failing a 32-step skip test / sampled; chosen log2 group size
     kNumCounters
 };
 

@@ -373,6 +373,8 @@ struct VixArgs {
     uint32_t s_mul;      // ceil(2^32 / S) (0: divide): floor(x / S) = umulhi(x, s_mul) while x S < 2^32
     SmallMod smod;       // x % (2R+1) for 64-bit x by 32-bit folds (k_vix_lanes)
     int count_cross;     // k_vix_lanes: accumulate the crossing statistic (first launch per key)
+    const unsigned long long* sel;   // k_vix_lanes: run only if *sel == sel_want (k_vix_sample's choice of group size); null: run
+    int sel_want;
     int4* ties;          // fp64 tie list: {tx row, tx col, dr, dc} of visible segments with a grazing tie
     long long tie_cap;
 };
@@ -960,14 +962,16 @@ __device__ __forceinline__ QuadGeom seg_quad_geom(const int16_t* __restrict__ z,
     // SV row-major for column-major walks, ST column-major for row-major ones
     const int maj = tr ? y : x, mnr = tr ? x : y;
     const int mag = (int)(((unsigned long long)(nm * 65536 + nM - 1) * s_rcp40[nM]) >> 40);   // 0 when M = 0
-    g.c.soff = tr ? a.st_off + ((maj >> GS) + 1) + ((mnr >> GS) + 1) * a.pt
-                  : ((maj >> GS) + 1) + ((mnr >> GS) + 1) * a.pv;
+    // (a negative minor direction starts one block further on, G - 1 - mo posts into it: folded
+    // into soff so that the in-block offset c0 stays below G -- 5 bits up to 32-step groups)
+    g.c.soff = tr ? a.st_off + ((maj >> GS) + 1) + ((mnr >> GS) + 1 - (int)mneg) * a.pt
+                  : ((maj >> GS) + 1) + ((mnr >> GS) + 1 - (int)mneg) * a.pv;
     const int D = rev ? E - Zt : Zt - E;
     constexpr int G = 1 << GS;
     g.c.LE2 = Es * nM + min(0, G * D) - 1;
     g.c.DG = G * D;
     const int mo = mnr & (G - 1);
-    g.c.w = nM | ((mneg ? 2 * G - 1 - mo : mo) << 8) | ((int)tr << 13) | ((int)mneg << 14) | (mag << 15);
+    g.c.w = nM | ((mneg ? G - 1 - mo : mo) << 8) | ((int)tr << 13) | ((int)mneg << 14) | (mag << 15);
     return g;
 }
 
@@ -1145,13 +1149,14 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_lanes(const int16
                                                                    unsigned long long* __restrict__ counters) {
     static_assert(kTileQ == 32, "one post per lane");
     static_assert(P == 1 || P == 2, "one or two posts per lane");
+    if (a.sel && (int)*a.sel != a.sel_want) return;   // the other group size was chosen for these rows
     extern __shared__ __align__(16) unsigned char s_dyn[];
     // dynamic smem: [geometry: kVixWarps x 32][samples: kVixWarps x P S x 32 ints]
     QuadGeom* s_geo = (QuadGeom*)s_dyn + warp_of_thread() * 32;
     int* s_smp = (int*)((QuadGeom*)s_dyn + kVixWarps * 32) + warp_of_thread() * a.S * 32 * P;
     const uint32_t smp_lane = (uint32_t)__cvta_generic_to_shared(s_smp) + 4u * (threadIdx.x & 31);   // column of this lane
     const QuadPitch PQ{a.pv, a.pt, ncols};
-    constexpr bool TERR = GS == 4;
+    constexpr bool TERR = GS >= 4;
     const int lane = threadIdx.x & 31;
     __shared__ unsigned long long s_rcp40[256];
     for (int d = threadIdx.x; d < 256; d += blockDim.x) s_rcp40[d] = d ? ((1ull << 40) + d - 1) / d : 0ull;
@@ -1248,6 +1253,51 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_lanes(const int16
     }
 }
 
+// Group-size choice for k_vix_lanes (16- or 32-step skip groups).  32-step groups halve the
+// skip tests of a segment, but a failing group costs a serial exact walk, so they pay only
+// where nearly every group passes (c4's 46400^2 terrain: VIX 311 -> 263 ms; c3's rougher
+// 16384^2: 40 -> 70).  k_vix_sample runs the 32-step test on pseudo-random segments of the
+// launch's rows; k_vix_select picks 5 (32 steps) when at most thr/1024 of them have a failing
+// group, else 4.  Both kernels are then launched and the one not chosen returns at once.
+__global__ void k_vix_sample(const int16_t* __restrict__ z, int ncols, VixArgs a, const int16_t* __restrict__ smap,
+                             unsigned long long* __restrict__ counters, int nsamp) {
+    __shared__ unsigned long long s_rcp40[256];
+    for (int d = threadIdx.x; d < 256; d += blockDim.x) s_rcp40[d] = d ? ((1ull << 40) + d - 1) / d : 0ull;
+    __syncthreads();
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    bool counted = false, failed = false;
+    if (t < nsamp && a.row_end > a.row0) {
+        const uint64_t h = sm_finalize(a.seed ^ ((uint64_t)(t + 1) * kGamma)), h2 = sm_finalize(h + kGamma);
+        const int r = a.row0 + (int)((uint32_t)h % (uint32_t)(a.row_end - a.row0)), c = (int)((uint32_t)(h >> 32) % (uint32_t)ncols);
+        const int span = 2 * a.R + 1;
+        const int dr = (int)((uint32_t)(h2 & 0xffffu) % (uint32_t)span) - a.R, dc = (int)((uint32_t)((h2 >> 16) & 0xffffu) % (uint32_t)span) - a.R;
+        if (dr * dr + dc * dc <= a.R * a.R && (dr | dc) != 0 && r + dr >= a.zr0 && r + dr < a.zr1 && (unsigned)(c + dc) < (unsigned)ncols) {
+            unsigned long long unused = 0;
+            const int E = zld(z + (int64_t)r * ncols + c) + a.ht;
+            const QuadGeomC gc = seg_quad_geom<5, true, false, false>(z, nullptr, ncols, a, nullptr, s_rcp40, r, c, E, dr, dc, unused).c;
+            const int nM = gc.w & 0xff, ng = nM >= 2 ? (nM + 30) >> 5 : 0;
+            const int mag = (unsigned)gc.w >> 15, sp = (gc.w & 0x2000) ? a.pt : a.pv, ssp = (gc.w & 0x4000) ? -sp : sp;
+            int acc = mag + (((gc.w >> 8) & 31) << 16), rhs = gc.LE2;
+            for (int gi = 0; gi < ng; ++gi) {
+                failed |= (int)__ldg(smap + (gc.soff + gi + (acc >> 21) * ssp)) * nM > rhs;
+                acc += mag << 5;
+                rhs += gc.DG;
+            }
+            counted = true;
+        }
+    }
+    const unsigned cm = __ballot_sync(0xffffffffu, counted), fm = __ballot_sync(0xffffffffu, failed);
+    if ((threadIdx.x & 31) == 0 && cm) {
+        atomicAdd(counters + kVixSelTotal, (unsigned long long)__popc(cm));
+        if (fm) atomicAdd(counters + kVixSelFail, (unsigned long long)__popc(fm));
+    }
+}
+
+__global__ void k_vix_select(unsigned long long* __restrict__ counters, int thr) {
+    const unsigned long long fail = counters[kVixSelFail], total = counters[kVixSelTotal];
+    counters[kVixSel] = (total >= 1024 && fail * 1024ull <= total * (unsigned long long)thr) ? 5ull : 4ull;
+}
+
 // Skip map of the skip tests.  Pass 1: per GxG block the maximum elevation,
 // stored with one block of padding on every side (padded index = block + 1;
 // padding blocks hold no posts: -32768).  Pass 2: per padded block corner
@@ -1324,6 +1374,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     a.span = make_fastmod((uint64_t)(2 * p.roi + 1));
     a.smod = make_smallmod((uint32_t)(2 * p.roi + 1));
     a.count_cross = 1;   // (d = 0: not usable; k_vix_lanes needs roi <= 255)
+    a.sel = nullptr; a.sel_want = 0;
     // fp64 tie list (grazing ties: ~1e-4 of segments on the BASELINE terrains);
     // txs_estimate_vix re-runs the stage with a larger list on overflow
     {
@@ -1398,7 +1449,13 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         // (one map load per 16 steps), 4 at roi >= 150 (C2: 59 % of 16-step groups
         // fail, 19 % of 4-step ones); TXS_VIX_GROUP=4|16 overrides
         int gs = p.roi >= 150 ? 2 : 4;
-        if (const char* e = getenv("TXS_VIX_GROUP")) gs = atoi(e) >= 16 ? 4 : 2;
+        // k_vix_lanes also has 32-step groups: TXS_VIX_GROUP=32 forces them; by default both
+        // the 16- and the 32-step maps are built and k_vix_sample picks per launch (`dual`)
+        const bool lanes_ok = p.samples_per_point <= kLaneDrawMaxS && a.smod.d != 0 && !getenv("TXS_VIX_SKIP") &&
+                              !getenv("TXS_VIX_LANESKIP") && !getenv("TXS_VIX_LANEDRAW");
+        bool dual = gs == 4 && lanes_ok && !getenv("TXS_VIX_GROUP") && !getenv("TXS_VIX_LMODE");
+        if (const char* e = getenv("TXS_VIX_DUAL")) dual = dual && atoi(e) != 0;
+        if (const char* e = getenv("TXS_VIX_GROUP")) gs = atoi(e) >= 32 && lanes_ok ? 5 : atoi(e) >= 16 ? 4 : 2;
         const int G = 1 << gs;
         // skip map (k_skipmap) behind the quad planes: SV, ST, then the block maxima
         const int Hb = (int)((c->z_rows + G - 1) / G), Wb = (int)((c->ncols + G - 1) / G);
@@ -1414,10 +1471,17 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         int skip = 1;
         if (a.pv >= 32768 || a.pt >= 32768) skip = 0;   // signed 16-bit map pitches (batch_skip)
         if (const char* e = getenv("TXS_VIX_SKIP")) skip = std::max(0, std::min(2, atoi(e)));
-        const size_t map_bytes = skip ? sizeof(int16_t) * (size_t)(nsv + nst + nbp) : 0;
+        // the 32-step maps (dual) sit behind the 16-step ones
+        constexpr int G2 = 32;
+        const int Hb2 = (int)((c->z_rows + G2 - 1) / G2), Wb2 = (int)((c->ncols + G2 - 1) / G2);
+        const int pv2 = ((Wb2 + 1) + 7) & ~7, pt2 = ((Hb2 + 1) + 7) & ~7;
+        const int64_t nsv2 = (int64_t)(Hb2 + 1) * pv2, nst2 = (int64_t)(Wb2 + 1) * pt2, nbp2 = (int64_t)(Hb2 + 2) * (Wb2 + 2);
+        const int64_t n_fine = nsv + nst + nbp;
+        dual = dual && skip == 1;
+        const size_t map_bytes = skip ? sizeof(int16_t) * (size_t)(n_fine + (dual ? nsv2 + nst2 + nbp2 : 0)) : 0;
         // with 16-step skip groups the flattened kernel walks failing units on the
         // terrain itself: no quad planes (69 GB at C4) and no plane build
-        const bool terr = skip == 1 && gs == 4;
+        const bool terr = skip == 1 && gs >= 4;
         if (terr) nq = 0;
         // rebuilt on every call (part of the timed stage; ~1 HBM pass of 34 B/post)
         if (ensure(c, "vix", (void**)&c->d_pairs, &c->pairs_cap, sizeof(uint2) * nq + map_bytes) != TXS_OK)
@@ -1443,6 +1507,17 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
             const int64_t ns = (int64_t)(Hb + 1) * (Wb + 1);
             k_skipmap<<<(unsigned)((ns + 255) / 256), 256, 0, c->stream>>>(bp, Hb, Wb, smap, a.pv, smap + nsv, a.pt, 0, Hb + 1);
             TXS_LAUNCHED(c, "vix");
+            if (dual) {
+                int16_t* smap2 = smap + n_fine;
+                int16_t* bp2 = smap2 + nsv2 + nst2;
+                k_blockmax<<<(unsigned)((nbp2 + 255) / 256), 256, 0, c->stream>>>(c->d_z, (int)c->z_rows, (int)c->ncols, bp2, Hb2,
+                                                                                Wb2, G2, 0, Hb2 + 2);
+                TXS_LAUNCHED(c, "vix");
+                const int64_t ns2 = (int64_t)(Hb2 + 1) * (Wb2 + 1);
+                k_skipmap<<<(unsigned)((ns2 + 255) / 256), 256, 0, c->stream>>>(bp2, Hb2, Wb2, smap2, pv2, smap2 + nsv2, pt2, 0,
+                                                                               Hb2 + 1);
+                TXS_LAUNCHED(c, "vix");
+            }
         }
         const uint2* qp = (const uint2*)c->d_pairs;
         set_zbounds(c->d_z, c->d_z + n, c->stream, (const int16_t*)qp, (const int16_t*)(qp + nq));
@@ -1450,28 +1525,30 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         // groups per skip unit (measured, profiles/README.md): 8 at roi 200 (C2 46.6 -> 43.5 ms
         // vs 4), 4 at roi 100 (C3 190.6 -> 180.2 vs 8)
         // G = 16: units of 2 groups (32 steps, TXS_VIX_UNIT=1 for 16)
-        int unit = gs == 4 ? 2 : (p.roi >= 150 ? 8 : 4);
+        int unit = gs >= 4 ? 2 : (p.roi >= 150 ? 8 : 4);
         if (const char* e = getenv("TXS_VIX_UNIT")) unit = atoi(e);
-        decltype(&k_vix_quads<1, 8, 2>) kq;
+        decltype(&k_vix_quads<1, 8, 2>) kq, kq32 = nullptr;   // kq32: the 32-step kernel of a dual launch
         bool lanes_kernel = false;
         if (skip == 1) {
             // per-lane skip tests (batch_skip_lane); TXS_VIX_LANESKIP=0: flattened units (batch_skip)
             static const bool lane_skip = !getenv("TXS_VIX_LANESKIP") || atoi(getenv("TXS_VIX_LANESKIP")) != 0;
-            if (gs == 4) kq = lane_skip ? k_vix_quads<3, 2, 4> : (unit == 1 ? k_vix_quads<1, 1, 4> : k_vix_quads<1, 2, 4>);
+            if (gs >= 4) kq = lane_skip ? k_vix_quads<3, 2, 4> : (unit == 1 ? k_vix_quads<1, 1, 4> : k_vix_quads<1, 2, 4>);
             else kq = lane_skip ? k_vix_quads<3, 8, 2> : (unit == 8 ? k_vix_quads<1, 8, 2> : k_vix_quads<1, 4, 2>);
             // one post per lane (k_vix_lanes) for S <= 32; TXS_VIX_LANEDRAW=0: the per-warp receiver FIFO
             static const bool lane_draw = !getenv("TXS_VIX_LANEDRAW") || atoi(getenv("TXS_VIX_LANEDRAW")) != 0;
             if (lane_skip && lane_draw && p.samples_per_point <= kLaneDrawMaxS && a.smod.d != 0) {
                 // failing-group mask vs one flag + cooperative re-test; walk record eager vs
                 // built only for failing lanes (TXS_VIX_LMODE = mask | lazy << 1)
-                int lm = gs == 4 ? 3 : 1;   // measured: profiles/README.md (VIX one post per lane)
+                int lm = gs >= 4 ? 3 : 1;   // measured: profiles/README.md (VIX one post per lane)
                 if (const char* e = getenv("TXS_VIX_LMODE")) lm = atoi(e) & 3;
                 // posts per lane (TXS_VIX_PPL=1|2; measured, profiles/README.md): two on large
                 // grids with few samples (c3 41.8 -> 40.2 ms, c4 322 -> 309), one otherwise
                 // (c2, S = 20: 32.5 vs 53.6; c1, 1000^2: 1.87 vs 2.03)
                 int ppl = p.samples_per_point <= 12 && (double)c->nrows * (double)c->ncols >= (double)(1 << 24) ? 2 : 1;
                 if (const char* e = getenv("TXS_VIX_PPL")) ppl = atoi(e) == 2 && p.samples_per_point <= 20 ? 2 : 1;
-                if (ppl == 2) {
+                if (gs == 5) {   // (failing-group mask + lazy walk record only)
+                    kq = ppl == 2 ? k_vix_lanes<5, true, true, 2> : k_vix_lanes<5, true, true, 1>;
+                } else if (ppl == 2) {
                     if (gs == 4) kq = lm == 0 ? k_vix_lanes<4, false, false, 2> : lm == 1 ? k_vix_lanes<4, true, false, 2>
                                     : lm == 2 ? k_vix_lanes<4, false, true, 2> : k_vix_lanes<4, true, true, 2>;
                     else kq = lm == 0 ? k_vix_lanes<2, false, false, 2> : lm == 1 ? k_vix_lanes<2, true, false, 2>
@@ -1485,14 +1562,18 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
                 qsm = (sizeof(QuadGeom) * 32 + sizeof(int) * 32 * (size_t)ppl * (size_t)std::max(1, p.samples_per_point)) *
                       kVixWarps;
                 lanes_kernel = true;
+                if (dual) kq32 = ppl == 2 ? k_vix_lanes<5, true, true, 2> : k_vix_lanes<5, true, true, 1>;
             }
         } else if (skip == 2) {
             kq = gs == 4 ? k_vix_quads<2, 8, 4> : k_vix_quads<2, 8, 2>;
         } else {
             kq = gs == 4 ? k_vix_quads<0, 8, 4> : k_vix_quads<0, 8, 2>;
         }
-        if (qsm > 40 * 1024)   // (the kernels' static shared memory counts against the default 48 KB)
+        dual = dual && kq32 != nullptr;
+        if (qsm > 40 * 1024) {   // (the kernels' static shared memory counts against the default 48 KB)
             TXS_CUDA(c, "vix", cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm));
+            if (dual) TXS_CUDA(c, "vix", cudaFuncSetAttribute(kq32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm));
+        }
         if (!c->d_gcd) {
             TXS_CUDA(c, "vix", cudaMalloc((void**)&c->d_gcd, 256 * 256));
             k_gcd_table<<<256, 256, 0, c->stream>>>(c->d_gcd);
@@ -1538,12 +1619,48 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
             }
             return TXS_OK;
         };
-        if (!banded) {
+        // one launch over args' rows; dual: sample the 32-step test on those rows, then both
+        // group sizes' kernels, of which the one not chosen returns at once
+        int dual_thr = 8;   // of 1024 sampled segments with a failing 32-step group (TXS_VIX_DUAL_THR)
+        if (const char* e = getenv("TXS_VIX_DUAL_THR")) dual_thr = std::max(0, atoi(e));
+        auto launch_rows = [&](VixArgs args, int64_t grid, uint8_t* out) -> txs_status {
+            if (dual) {
+                VixArgs a32 = args;
+                a32.pv = pv2; a32.pt = pt2; a32.st_off = (int)nsv2;
+                const int16_t* smap2 = smap + n_fine;
+                constexpr int kSamples = 1 << 16;
+                TXS_CUDA(c, "vix", cudaMemsetAsync(c->d_counters + kVixSelFail, 0, 3 * sizeof(unsigned long long), c->stream));
+                k_vix_sample<<<kSamples / 256, 256, 0, c->stream>>>(c->zv(), (int)c->ncols, a32, smap2, c->d_counters, kSamples);
+                TXS_LAUNCHED(c, "vix");
+                k_vix_select<<<1, 1, 0, c->stream>>>(c->d_counters, dual_thr);
+                TXS_LAUNCHED(c, "vix");
+                if (getenv("TXS_VIX_VERBOSE")) {
+                    unsigned long long h[3] = {0, 0, 0};
+                    TXS_CUDA(c, "vix", cudaMemcpyAsync(h, c->d_counters + kVixSelFail, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+                    TXS_CUDA(c, "vix", cudaStreamSynchronize(c->stream));
+                    fprintf(stderr, "[txs] VIX rows [%d, %d): %llu of %llu sampled segments fail a 32-step group -> %llu-step groups\n",
+                            args.row0, args.row_end, h[0], h[1], 1ull << h[2]);
+                }
+                args.sel = c->d_counters + kVixSel; args.sel_want = 4;
+                a32.sel = args.sel; a32.sel_want = 5;
+                TXS_CUDA(c, "vix", cudaMemsetAsync(c->d_counters + kVixNext, 0, sizeof(unsigned long long), c->stream));
+                kq<<<(unsigned)grid, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols, out, args, c->d_gcd,
+                                                                   smap, c->d_counters);
+                TXS_LAUNCHED(c, "vix");
+                TXS_CUDA(c, "vix", cudaMemsetAsync(c->d_counters + kVixNext, 0, sizeof(unsigned long long), c->stream));
+                kq32<<<(unsigned)grid, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols, out, a32, c->d_gcd,
+                                                                     smap2, c->d_counters);
+                return TXS_OK;
+            }
+            args.sel = nullptr; args.sel_want = 0;
             TXS_CUDA(c, "vix", cudaMemsetAsync(c->d_counters + kVixNext, 0, sizeof(unsigned long long), c->stream));
+            kq<<<(unsigned)grid, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols, out, args, c->d_gcd, smap,
+                                                               c->d_counters);
+            return TXS_OK;
+        };
+        if (!banded) {
             cudaEventRecord(c->ev_k0, c->stream);
-            kq<<<(unsigned)grid_q, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols,
-                                                                    c->d_vix - c->band_r0 * c->ncols, aq, c->d_gcd, smap,
-                                                                    c->d_counters);
+            if ((st = launch_rows(aq, grid_q, c->d_vix - c->band_r0 * c->ncols)) != TXS_OK) return st;
             cudaEventRecord(c->ev_k1, c->stream);
             if ((st = finish_cross()) != TXS_OK) return st;
         } else {
@@ -1552,11 +1669,12 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
             // holding them; block-max rows and map corner rows are built once each, as
             // soon as their terrain rows are in
             const int64_t H = c->z_rows;
-            int pr_done = 0, q_done = 0;
+            int pr_done = 0, q_done = 0, pr2_done = 0, q2_done = 0;
+            const int Gneed = dual ? G2 : G;
             cudaEventRecord(c->ev_k0, c->stream);
             for (size_t b = 0; b < c->up_end.size(); ++b) {
                 const int64_t r0 = b ? c->up_end[b - 1] : 0, r1 = c->up_end[b];
-                const int64_t need = std::min(H, r1 + p.roi + 4 * (int64_t)G);
+                const int64_t need = std::min(H, r1 + p.roi + 4 * (int64_t)Gneed);
                 int64_t loaded = H;
                 for (size_t k = b; k < c->up_end.size(); ++k)
                     if (c->up_end[k] >= need) { loaded = c->up_end[k]; break; }
@@ -1577,14 +1695,32 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
                     TXS_LAUNCHED(c, "vix");
                     q_done = q_new;
                 }
+                if (dual) {
+                    int16_t* smap2 = smap + n_fine;
+                    int16_t* bp2 = smap2 + nsv2 + nst2;
+                    const int pr2_new = loaded >= H ? Hb2 + 2 : (int)(loaded / G2) + 1;
+                    if (pr2_new > pr2_done) {
+                        const int64_t cnt = (int64_t)(pr2_new - pr2_done) * (Wb2 + 2);
+                        k_blockmax<<<(unsigned)((cnt + 255) / 256), 256, 0, c->stream>>>(c->d_z, (int)H, (int)c->ncols, bp2, Hb2,
+                                                                                       Wb2, G2, pr2_done, pr2_new);
+                        TXS_LAUNCHED(c, "vix");
+                        pr2_done = pr2_new;
+                    }
+                    const int q2_new = std::min(Hb2 + 1, pr2_done - 1);
+                    if (q2_new > q2_done) {
+                        const int64_t cnt = (int64_t)(q2_new - q2_done) * (Wb2 + 1);
+                        k_skipmap<<<(unsigned)((cnt + 255) / 256), 256, 0, c->stream>>>(bp2, Hb2, Wb2, smap2, pv2, smap2 + nsv2, pt2,
+                                                                                      q2_done, q2_new);
+                        TXS_LAUNCHED(c, "vix");
+                        q2_done = q2_new;
+                    }
+                }
                 VixArgs ab = aq;
                 ab.row0 = (int)r0; ab.row_end = (int)r1;
                 ab.tiles_y = (int)((r1 - r0 + tq - 1) / tq);
                 const int64_t tb = (int64_t)ab.tiles_x * ab.tiles_y;
                 const int64_t gb = std::min<int64_t>(tb, (int64_t)std::max(1, per_sm) * c->num_sms);
-                TXS_CUDA(c, "vix", cudaMemsetAsync(c->d_counters + kVixNext, 0, sizeof(unsigned long long), c->stream));
-                kq<<<(unsigned)gb, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols, c->d_vix, ab,
-                                                                  c->d_gcd, smap, c->d_counters);
+                if ((st = launch_rows(ab, gb, c->d_vix)) != TXS_OK) return st;
                 TXS_LAUNCHED(c, "vix");
             }
             cudaEventRecord(c->ev_k1, c->stream);
