@@ -373,8 +373,6 @@ struct VixArgs {
     uint32_t s_mul;      // ceil(2^32 / S) (0: divide): floor(x / S) = umulhi(x, s_mul) while x S < 2^32
     SmallMod smod;       // x % (2R+1) for 64-bit x by 32-bit folds (k_vix_lanes)
     int count_cross;     // k_vix_lanes: accumulate the crossing statistic (first launch per key)
-    const unsigned long long* sel;   // k_vix_lanes: run only if *sel == sel_want (k_vix_sample's choice of group size); null: run
-    int sel_want;
     int4* ties;          // fp64 tie list: {tx row, tx col, dr, dc} of visible segments with a grazing tie
     long long tie_cap;
 };
@@ -964,14 +962,19 @@ __device__ __forceinline__ QuadGeom seg_quad_geom(const int16_t* __restrict__ z,
     const int mag = (int)(((unsigned long long)(nm * 65536 + nM - 1) * s_rcp40[nM]) >> 40);   // 0 when M = 0
     // (a negative minor direction starts one block further on, G - 1 - mo posts into it: folded
     // into soff so that the in-block offset c0 stays below G -- 5 bits up to 32-step groups)
-    g.c.soff = tr ? a.st_off + ((maj >> GS) + 1) + ((mnr >> GS) + 1 - (int)mneg) * a.pt
-                  : ((maj >> GS) + 1) + ((mnr >> GS) + 1 - (int)mneg) * a.pv;
+#ifndef VIX_REPACK_ALL
+#define VIX_REPACK_ALL 0
+#endif
+    constexpr bool kFold = GS >= 5 || VIX_REPACK_ALL;   // (only 32-step groups need it)
+    const int mfold = kFold ? (int)mneg : 0;
+    g.c.soff = tr ? a.st_off + ((maj >> GS) + 1) + ((mnr >> GS) + 1 - mfold) * a.pt
+                  : ((maj >> GS) + 1) + ((mnr >> GS) + 1 - mfold) * a.pv;
     const int D = rev ? E - Zt : Zt - E;
     constexpr int G = 1 << GS;
     g.c.LE2 = Es * nM + min(0, G * D) - 1;
     g.c.DG = G * D;
     const int mo = mnr & (G - 1);
-    g.c.w = nM | ((mneg ? G - 1 - mo : mo) << 8) | ((int)tr << 13) | ((int)mneg << 14) | (mag << 15);
+    g.c.w = nM | ((mneg ? (kFold ? G : 2 * G) - 1 - mo : mo) << 8) | ((int)tr << 13) | ((int)mneg << 14) | (mag << 15);
     return g;
 }
 
@@ -1149,7 +1152,6 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_lanes(const int16
                                                                    unsigned long long* __restrict__ counters) {
     static_assert(kTileQ == 32, "one post per lane");
     static_assert(P == 1 || P == 2, "one or two posts per lane");
-    if (a.sel && (int)*a.sel != a.sel_want) return;   // the other group size was chosen for these rows
     extern __shared__ __align__(16) unsigned char s_dyn[];
     // dynamic smem: [geometry: kVixWarps x 32][samples: kVixWarps x P S x 32 ints]
     QuadGeom* s_geo = (QuadGeom*)s_dyn + warp_of_thread() * 32;
@@ -1258,7 +1260,8 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_lanes(const int16
 // where nearly every group passes (c4's 46400^2 terrain: VIX 311 -> 263 ms; c3's rougher
 // 16384^2: 40 -> 70).  k_vix_sample runs the 32-step test on pseudo-random segments of the
 // launch's rows; k_vix_select picks 5 (32 steps) when at most thr/1024 of them have a failing
-// group, else 4.  Both kernels are then launched and the one not chosen returns at once.
+// group, else 4.  Both kernels are then launched and the one not chosen finds its work counter
+// exhausted (k_vix_arm).
 __global__ void k_vix_sample(const int16_t* __restrict__ z, int ncols, VixArgs a, const int16_t* __restrict__ smap,
                              unsigned long long* __restrict__ counters, int nsamp) {
     __shared__ unsigned long long s_rcp40[256];
@@ -1293,6 +1296,13 @@ __global__ void k_vix_sample(const int16_t* __restrict__ z, int ncols, VixArgs a
     }
 }
 
+// the work counter of the next k_vix_lanes launch: 0 when its group size is the chosen one, else past
+// every tile, so that its warps leave at their first pull (an early return inside the kernel costs
+// the sweep 3 % more instructions: c3 40.6 -> 41.8 ms)
+__global__ void k_vix_arm(unsigned long long* __restrict__ counters, int want) {
+    counters[kVixNext] = (int)counters[kVixSel] == want ? 0ull : 1ull << 62;
+}
+
 __global__ void k_vix_select(unsigned long long* __restrict__ counters, int thr) {
     const unsigned long long fail = counters[kVixSelFail], total = counters[kVixSelTotal];
     counters[kVixSel] = (total >= 1024 && fail * 1024ull <= total * (unsigned long long)thr) ? 5ull : 4ull;
@@ -1317,6 +1327,21 @@ __global__ void k_blockmax(const int16_t* __restrict__ z, int H, int W, int16_t*
             for (int x = G * bc; x < min(G * bc + G, W); ++x) m = max(m, (int)z[(int64_t)y * W + x]);
     }
     bp[idx] = (int16_t)m;
+}
+
+// padded block rows [pr0, pr1) of the 2G-block maxima from the G-block maxima (2 x 2 blocks each)
+__global__ void k_blockmax2(const int16_t* __restrict__ bp, int Hb, int Wb, int16_t* __restrict__ bp2, int Hb2, int Wb2,
+                            int pr0, int pr1) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + (int64_t)pr0 * (Wb2 + 2);
+    if (idx >= (int64_t)pr1 * (Wb2 + 2)) return;
+    const int pr = (int)(idx / (Wb2 + 2)), pc = (int)(idx - (int64_t)pr * (Wb2 + 2));
+    const int br2 = pr - 1, bc2 = pc - 1;
+    int m = -32768;
+    if (br2 >= 0 && br2 < Hb2 && bc2 >= 0 && bc2 < Wb2) {
+        for (int br = 2 * br2; br < min(2 * br2 + 2, Hb); ++br)
+            for (int bc = 2 * bc2; bc < min(2 * bc2 + 2, Wb); ++bc) m = max(m, (int)bp[(int64_t)(br + 1) * (Wb + 2) + bc + 1]);
+    }
+    bp2[idx] = (int16_t)m;
 }
 
 // block-corner rows [q0, q1) of the skip map (from padded block rows q0 .. q1)
@@ -1374,7 +1399,6 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
     a.span = make_fastmod((uint64_t)(2 * p.roi + 1));
     a.smod = make_smallmod((uint32_t)(2 * p.roi + 1));
     a.count_cross = 1;   // (d = 0: not usable; k_vix_lanes needs roi <= 255)
-    a.sel = nullptr; a.sel_want = 0;
     // fp64 tie list (grazing ties: ~1e-4 of segments on the BASELINE terrains);
     // txs_estimate_vix re-runs the stage with a larger list on overflow
     {
@@ -1510,8 +1534,7 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
             if (dual) {
                 int16_t* smap2 = smap + n_fine;
                 int16_t* bp2 = smap2 + nsv2 + nst2;
-                k_blockmax<<<(unsigned)((nbp2 + 255) / 256), 256, 0, c->stream>>>(c->d_z, (int)c->z_rows, (int)c->ncols, bp2, Hb2,
-                                                                                Wb2, G2, 0, Hb2 + 2);
+                k_blockmax2<<<(unsigned)((nbp2 + 255) / 256), 256, 0, c->stream>>>(bp, Hb, Wb, bp2, Hb2, Wb2, 0, Hb2 + 2);
                 TXS_LAUNCHED(c, "vix");
                 const int64_t ns2 = (int64_t)(Hb2 + 1) * (Wb2 + 1);
                 k_skipmap<<<(unsigned)((ns2 + 255) / 256), 256, 0, c->stream>>>(bp2, Hb2, Wb2, smap2, pv2, smap2 + nsv2, pt2, 0,
@@ -1641,18 +1664,15 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
                     fprintf(stderr, "[txs] VIX rows [%d, %d): %llu of %llu sampled segments fail a 32-step group -> %llu-step groups\n",
                             args.row0, args.row_end, h[0], h[1], 1ull << h[2]);
                 }
-                args.sel = c->d_counters + kVixSel; args.sel_want = 4;
-                a32.sel = args.sel; a32.sel_want = 5;
-                TXS_CUDA(c, "vix", cudaMemsetAsync(c->d_counters + kVixNext, 0, sizeof(unsigned long long), c->stream));
+                k_vix_arm<<<1, 1, 0, c->stream>>>(c->d_counters, 4);
                 kq<<<(unsigned)grid, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols, out, args, c->d_gcd,
                                                                    smap, c->d_counters);
                 TXS_LAUNCHED(c, "vix");
-                TXS_CUDA(c, "vix", cudaMemsetAsync(c->d_counters + kVixNext, 0, sizeof(unsigned long long), c->stream));
+                k_vix_arm<<<1, 1, 0, c->stream>>>(c->d_counters, 5);
                 kq32<<<(unsigned)grid, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols, out, a32, c->d_gcd,
                                                                      smap2, c->d_counters);
                 return TXS_OK;
             }
-            args.sel = nullptr; args.sel_want = 0;
             TXS_CUDA(c, "vix", cudaMemsetAsync(c->d_counters + kVixNext, 0, sizeof(unsigned long long), c->stream));
             kq<<<(unsigned)grid, kVixThreads, qsm, c->stream>>>(c->zv(), qp, (int)c->nrows, (int)c->ncols, out, args, c->d_gcd, smap,
                                                                c->d_counters);
@@ -1701,8 +1721,8 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
                     const int pr2_new = loaded >= H ? Hb2 + 2 : (int)(loaded / G2) + 1;
                     if (pr2_new > pr2_done) {
                         const int64_t cnt = (int64_t)(pr2_new - pr2_done) * (Wb2 + 2);
-                        k_blockmax<<<(unsigned)((cnt + 255) / 256), 256, 0, c->stream>>>(c->d_z, (int)H, (int)c->ncols, bp2, Hb2,
-                                                                                       Wb2, G2, pr2_done, pr2_new);
+                        k_blockmax2<<<(unsigned)((cnt + 255) / 256), 256, 0, c->stream>>>(bp, Hb, Wb, bp2, Hb2, Wb2, pr2_done,
+                                                                                        pr2_new);
                         TXS_LAUNCHED(c, "vix");
                         pr2_done = pr2_new;
                     }

@@ -7,7 +7,7 @@ set -u
 O=gpurun_out
 mkdir -p $O
 M=gpu__time_duration.sum,smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_srcunit_tex_op_read.sum,lts__t_sectors_srcunit_tex_op_write.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__throughput.avg.pct_of_peak_sustained_elapsed
-K='regex:k_vix_lanes|k_vix_quads|k_vix<|k_viewshed_evk|k_viewshed_ev<|k_viewshed<|k_gain_full|k_gain_tiled|k_site_loop|k_findmax|k_vix_fp64_ties|k_vs_fp64_ties'
+K='regex:k_batch_|k_vix_lanes|k_vix_quads|k_vix<|k_viewshed_evk|k_viewshed_ev<|k_viewshed<|k_gain_full|k_gain_tiled|k_site_loop|k_findmax|k_vix_fp64_ties|k_vs_fp64_ties'
 for c in "$@"; do
   python profiles/scripts/one_run.py --config $c > $O/one_$c.log 2>&1 && \
   ncu --metrics $M --clock-control none -k "$K" --csv --log-file $O/counts_$c.csv \
