@@ -1143,7 +1143,9 @@ constexpr int kLaneDrawMaxS = 32;
 // first post's S receivers, then its second's, in one loop, so the warp's draw
 // iterations are the max over lanes of the two posts' pair counts together --
 // less divergence than twice the max of one).
-template <int GS, bool MASK, bool LAZY, int P>
+// CC: the crossing statistic compiled in (1), out (0: the cached launches -- the walk geometry is
+// then inlined once, not in both forms), or chosen by a.count_cross (-1).
+template <int GS, bool MASK, bool LAZY, int P, int CC = -1>
 __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_lanes(const int16_t* __restrict__ z,
                                                                    const uint2* __restrict__ qp, int nrows, int ncols,
                                                                    uint8_t* __restrict__ out, VixArgs a,
@@ -1232,6 +1234,9 @@ __global__ void __launch_bounds__(kVixThreads, VIX_MINB) k_vix_lanes(const int16
                     const int pk = s_smp[(q * S + k) * 32 + lane];
                     dr0 = (pk & 0x1ff) - 256;
                     dc0 = ((pk >> 9) & 0x1ff) - 256;
+                    if (CC >= 0)
+                        g = seg_quad_geom<GS, TERR, !LAZY, CC == 1>(z, qp, ncols, a, gcdt, s_rcp40, r, c, E, dr0, dc0, n_cross);
+                    else
                     g = a.count_cross ? seg_quad_geom<GS, TERR, !LAZY, true>(z, qp, ncols, a, gcdt, s_rcp40, r, c, E, dr0, dc0, n_cross)
                                       : seg_quad_geom<GS, TERR, !LAZY, false>(z, qp, ncols, a, gcdt, s_rcp40, r, c, E, dr0, dc0, n_cross);
                 }
@@ -1623,6 +1628,26 @@ txs_status launch_vix(txs_ctx* c, const txs_params& p) {
         const bool lanes = lanes_kernel;
         const bool cached = lanes && c->vix_cross_valid && c->vix_cross_key == key;
         aq.count_cross = cached ? 0 : 1;
+        if (lanes) {   // the default forms with the statistic compiled in or out
+            auto cc_form = [&](decltype(kq) f) -> decltype(kq) {
+                if (f == k_vix_lanes<4, true, true, 2>) return cached ? k_vix_lanes<4, true, true, 2, 0> : k_vix_lanes<4, true, true, 2, 1>;
+                if (f == k_vix_lanes<4, true, true, 1>) return cached ? k_vix_lanes<4, true, true, 1, 0> : k_vix_lanes<4, true, true, 1, 1>;
+                if (f == k_vix_lanes<5, true, true, 2>) return cached ? k_vix_lanes<5, true, true, 2, 0> : k_vix_lanes<5, true, true, 2, 1>;
+                if (f == k_vix_lanes<5, true, true, 1>) return cached ? k_vix_lanes<5, true, true, 1, 0> : k_vix_lanes<5, true, true, 1, 1>;
+                return f;
+            };
+            if (!getenv("TXS_VIX_CCFORM") || atoi(getenv("TXS_VIX_CCFORM")) != 0) {
+                kq = cc_form(kq);
+                if (kq32) kq32 = cc_form(kq32);
+                if (qsm > 40 * 1024) {
+                    TXS_CUDA(c, "vix", cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm));
+                    if (kq32) TXS_CUDA(c, "vix", cudaFuncSetAttribute(kq32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm));
+                }
+                TXS_CUDA(c, "vix", cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kq, kVixThreads, qsm));
+                grid_q = std::min<int64_t>(tiles_q, (int64_t)std::max(1, per_sm) * c->num_sms);
+                if (const char* e = getenv("TXS_VIX_GRID")) grid_q = std::min<int64_t>(tiles_q, std::max(1, atoi(e)));
+            }
+        }
         unsigned long long before = 0;
         if (lanes && !cached)
             TXS_CUDA(c, "vix", cudaMemcpyAsync(&before, c->d_counters + kVixCrossFull, sizeof(before),
