@@ -72,6 +72,28 @@ __global__ void k_vs_pairs(const int16_t* __restrict__ z, uint32_t* __restrict__
     }
 }
 
+// the same planes, four posts per thread (ncols % 4 == 0: 8-byte terrain loads, two 16-byte stores)
+__global__ void k_vs_pairs4(const int16_t* __restrict__ z, uint32_t* __restrict__ out, int H, int ncols, int pw) {
+    const int q = pw >> 2;   // groups of four posts per plane row (pw is a multiple of 16)
+    const int64_t total = (int64_t)H * q;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int y = (int)(t / q), x = (int)(t - (int64_t)y * q) << 2;
+        uint4 lo = make_uint4(0u, 0u, 0u, 0u), hi = lo;
+        if (x < ncols) {
+            const int16_t* zr = z + (int64_t)y * ncols + x;
+            const uint2 a = __ldg(reinterpret_cast<const uint2*>(zr));   // posts x .. x+3 as 16-bit halves
+            const uint2 b = y + 1 < H ? __ldg(reinterpret_cast<const uint2*>(zr + ncols)) : make_uint2(0u, 0u);
+            const uint32_t nx = x + 4 < ncols ? (uint32_t)(uint16_t)__ldg(zr + 4) : 0u;
+            const uint32_t z0 = a.x & 0xffffu, z1 = a.x >> 16, z2 = a.y & 0xffffu, z3 = a.y >> 16;
+            lo = make_uint4(a.x, z0 | (b.x << 16), z1 | (z2 << 16), z1 | (b.x & 0xffff0000u));
+            hi = make_uint4(a.y, z2 | (b.y << 16), z3 | (nx << 16), z3 | (b.y & 0xffff0000u));
+        }
+        uint4* row = reinterpret_cast<uint4*>(out + (int64_t)y * 2 * pw + 2 * x);
+        row[0] = lo;
+        row[1] = hi;
+    }
+}
+
 __device__ __forceinline__ uint32_t vs_pld(const uint32_t* p) {
 #ifdef TXS_BOUNDS_CHECK
     const int16_t* q = (const int16_t*)p;
@@ -977,8 +999,12 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
         const int64_t pwords = c->z_rows * (int64_t)a.p2;
         if (ensure(c, "viewshed", (void**)&c->d_pairs, &c->pairs_cap, sizeof(uint32_t) * pwords) != TXS_OK)
             return TXS_ERR_OUT_OF_MEMORY;
-        k_vs_pairs<<<(unsigned)std::min<int64_t>((c->z_rows * a.pw + 255) / 256, (int64_t)c->num_sms * 32), 256, 0,
-                     c->stream>>>(c->d_z, (uint32_t*)c->d_pairs, (int)c->z_rows, (int)c->ncols, a.pw);
+        if (c->ncols % 4 == 0 && !getenv("TXS_VS_PAIRS1"))   // (measured: c3 1.0 -> see profiles/README.md)
+            k_vs_pairs4<<<(unsigned)std::min<int64_t>((c->z_rows * (a.pw / 4) + 255) / 256, (int64_t)c->num_sms * 32), 256, 0,
+                          c->stream>>>(c->d_z, (uint32_t*)c->d_pairs, (int)c->z_rows, (int)c->ncols, a.pw);
+        else
+            k_vs_pairs<<<(unsigned)std::min<int64_t>((c->z_rows * a.pw + 255) / 256, (int64_t)c->num_sms * 32), 256, 0,
+                         c->stream>>>(c->d_z, (uint32_t*)c->d_pairs, (int)c->z_rows, (int)c->ncols, a.pw);
         TXS_LAUNCHED(c, "viewshed");
         a.pairs = (const uint32_t*)c->d_pairs;
         set_zbounds(c->d_z, c->d_z + c->z_rows * c->ncols, c->stream, (const int16_t*)a.pairs,
