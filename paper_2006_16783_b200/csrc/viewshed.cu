@@ -999,7 +999,7 @@ txs_status launch_viewsheds(txs_ctx* c, const txs_params& p) {
         const int64_t pwords = c->z_rows * (int64_t)a.p2;
         if (ensure(c, "viewshed", (void**)&c->d_pairs, &c->pairs_cap, sizeof(uint32_t) * pwords) != TXS_OK)
             return TXS_ERR_OUT_OF_MEMORY;
-        if (c->ncols % 4 == 0 && !getenv("TXS_VS_PAIRS1"))   // (measured: c3 1.0 -> see profiles/README.md)
+        if (c->ncols % 4 == 0 && !getenv("TXS_VS_PAIRS1"))   // (four posts per thread: c3 VIEWSHED 20.55 -> 20.13 ms; TXS_VS_PAIRS1=1: one post per thread)
             k_vs_pairs4<<<(unsigned)std::min<int64_t>((c->z_rows * (a.pw / 4) + 255) / 256, (int64_t)c->num_sms * 32), 256, 0,
                           c->stream>>>(c->d_z, (uint32_t*)c->d_pairs, (int)c->z_rows, (int)c->ncols, a.pw);
         else
