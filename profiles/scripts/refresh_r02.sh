@@ -7,7 +7,7 @@ O=gpurun_out; mkdir -p $O
 profiles/scripts/kernel_counts.sh c1 c2 c3 c4 c5
 python profiles/scripts/counts_summary.py c1 c2 c3 c4 c5 > $O/counts_summary.log 2>&1   # the bench lines below read it
 python bench.py --config c3 --steps 2 --warmup 1 --no-cpu-baseline > $O/ll_pre.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c3.csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file $O/launches_c3.csv \
     python bench.py --config c3 --steps 2 --warmup 1 --no-cpu-baseline > $O/ll_ncu.log 2>&1
 python profiles/scripts/vix_once.py c3 > $O/vix_once.log 2>&1 && \
 ncu --set full --import-source on --clock-control none -k regex:k_vix_lanes -c 1 -o $O/r02_vix_c3 -f \
